@@ -1,0 +1,106 @@
+// Shared device helpers for libfisedit (sm_100a).
+#pragma once
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <stdint.h>
+#include "../../include/fisedit.h"
+
+#define FIS_DEV __device__ __forceinline__
+
+namespace fis {
+
+FIS_DEV int cur_step(const int* step) { return step ? __ldg(step) : 0; }
+
+FIS_DEV char* ref_base(const fis_ref& r, int t) {
+    return (char*)r.ptr + (long long)t * r.step_stride;
+}
+
+FIS_DEV float load_elem(const char* base, int dtype, long long idx) {
+    if (dtype == FIS_BF16) return __bfloat162float(((const __nv_bfloat16*)base)[idx]);
+    return ((const float*)base)[idx];
+}
+
+FIS_DEV void store_elem(char* base, int dtype, long long idx, float v) {
+    if (dtype == FIS_BF16) ((__nv_bfloat16*)base)[idx] = __float2bfloat16_rn(v);
+    else ((float*)base)[idx] = v;
+}
+
+// Value of a selectable source at source pixel q, channel c (select-on-read).
+FIS_DEV float src_value(const fis_src& s, const char* fresh, const char* cache, int q, int c) {
+    if (s.index) {
+        int i = __ldg(s.index + q);
+        if (i >= 0) return load_elem(fresh, s.fresh.dtype, (long long)i * s.fresh.ld + c);
+        return load_elem(cache, s.cache.dtype, (long long)q * s.cache.ld + c);
+    }
+    return load_elem(fresh, s.fresh.dtype, (long long)q * s.fresh.ld + c);
+}
+
+// Source row pointer (and dtype/ld) for pixel q, used by vectorised gathers.
+struct RowPtr { const char* p; int dtype; };
+FIS_DEV RowPtr src_row(const fis_src& s, const char* fresh, const char* cache, int q) {
+    if (s.index) {
+        int i = __ldg(s.index + q);
+        if (i >= 0) return {fresh + (long long)i * s.fresh.ld * (s.fresh.dtype == FIS_BF16 ? 2 : 4), s.fresh.dtype};
+        return {cache + (long long)q * s.cache.ld * (s.cache.dtype == FIS_BF16 ? 2 : 4), s.cache.dtype};
+    }
+    return {fresh + (long long)q * s.fresh.ld * (s.fresh.dtype == FIS_BF16 ? 2 : 4), s.fresh.dtype};
+}
+
+FIS_DEV float warp_sum(float v) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+FIS_DEV float warp_max(float v) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+// Epilogue shared by the SIMT and tcgen05 GEMMs. Applies bias / time-bias /
+// GN(cached stats)+SiLU / step update / residual and stores. r = GEMM row.
+struct EpiCtx {
+    char* d; char* pre; char* pre2; char* res; char* lat; char* bias2;
+    const float* mean; const float* var;
+    int cpg;  // channels per group
+};
+
+FIS_DEV EpiCtx make_epi(const fis_gemm_args& a, int t) {
+    EpiCtx e;
+    e.d = ref_base(a.d, t);
+    e.pre = a.pre.ptr ? ref_base(a.pre, t) : nullptr;
+    e.pre2 = a.pre2.ptr ? ref_base(a.pre2, t) : nullptr;
+    e.res = a.res.ptr ? ref_base(a.res, t) : nullptr;
+    e.lat = a.lat.ptr ? ref_base(a.lat, t) : nullptr;
+    e.bias2 = a.bias2.ptr ? ref_base(a.bias2, t) : nullptr;
+    e.mean = a.gn_mean.ptr ? (const float*)ref_base(a.gn_mean, t) : nullptr;
+    e.var = a.gn_var.ptr ? (const float*)ref_base(a.gn_var, t) : nullptr;
+    e.cpg = a.groups > 0 ? a.n / a.groups : 1;
+    return e;
+}
+
+FIS_DEV void epilogue_store(const fis_gemm_args& a, const EpiCtx& e, int r, int n, float acc) {
+    float v = acc * a.alpha;
+    if (a.bias) v = __fadd_rn(v, __ldg(a.bias + n));
+    const int orow = a.d_rows ? __ldg(a.d_rows + r) : r;
+    if (e.pre) store_elem(e.pre, a.pre.dtype, (long long)orow * a.pre.ld + n, v);
+    if (e.bias2) v = __fadd_rn(v, load_elem(e.bias2, a.bias2.dtype, n));
+    if (a.epi == FIS_EPI_GN_SILU) {
+        // normalize_with_group_stats (tensors.py:149-180) in f64, then SiLU in f64 (unet.py:291-293)
+        const int g = n / e.cpg;
+        const double y64 = ((double)v - (double)e.mean[g]) / sqrt((double)e.var[g] + (double)a.eps) *
+                               (double)__ldg(a.gamma + n) + (double)__ldg(a.beta + n);
+        const float y = (float)y64;
+        if (e.pre2) store_elem(e.pre2, a.pre2.dtype, (long long)orow * a.pre2.ld + n, y);
+        const double yd = (double)y;
+        v = (float)(yd / (1.0 + exp(-yd)));
+    } else if (a.epi == FIS_EPI_STEP) {
+        const float l = load_elem(e.lat, a.lat.dtype, (long long)orow * a.lat.ld + n);
+        v = __fsub_rn(l, __fmul_rn(a.step_scale, v));
+    }
+    if (e.res) v = __fadd_rn(v, load_elem(e.res, a.res.dtype, (long long)orow * a.res.ld + n));
+    if (a.d_trans) store_elem(e.d, a.d.dtype, (long long)n * a.d.ld + orow, v);
+    else store_elem(e.d, a.d.dtype, (long long)orow * a.d.ld + n, v);
+}
+
+}  // namespace fis

@@ -1,0 +1,213 @@
+// Row-wise / element-wise kernels of the sparse edit step: group-norm statistics
+// and application (+SiLU), scaled row softmax with controlled-mode column pinning,
+// select-on-read 2x2 average pooling and full-map materialisation.
+// All reductions use a fixed order, so outputs are bitwise deterministic.
+#include "fis_common.cuh"
+
+namespace fis {
+
+// ---- group norm statistics (tensors.py:129-146): two-pass f64, rounded to f32
+__global__ void __launch_bounds__(256) gn_stats_kernel(const fis_gn_stats_args a) {
+    const int t = cur_step(a.step);
+    const int g = blockIdx.x;
+    const int cpg = a.c / a.groups;
+    const long long cnt = (long long)a.hw * cpg;
+    const char* x = ref_base(a.x, t);
+    __shared__ double red[256];
+    double s = 0.0;
+    for (long long e = threadIdx.x; e < cnt; e += blockDim.x) {
+        const int q = (int)(e / cpg), c = g * cpg + (int)(e % cpg);
+        s += (double)load_elem(x, a.x.dtype, (long long)q * a.x.ld + c);
+    }
+    red[threadIdx.x] = s;
+    __syncthreads();
+    for (int o = 128; o; o >>= 1) {
+        if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+        __syncthreads();
+    }
+    const double mean = red[0] / (double)cnt;
+    __syncthreads();
+    double v = 0.0;
+    for (long long e = threadIdx.x; e < cnt; e += blockDim.x) {
+        const int q = (int)(e / cpg), c = g * cpg + (int)(e % cpg);
+        const double d = (double)load_elem(x, a.x.dtype, (long long)q * a.x.ld + c) - mean;
+        v += d * d;
+    }
+    red[threadIdx.x] = v;
+    __syncthreads();
+    for (int o = 128; o; o >>= 1) {
+        if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        ((float*)ref_base(a.mean, t))[g] = (float)mean;
+        ((float*)ref_base(a.var, t))[g] = (float)(red[0] / (double)cnt);
+    }
+}
+
+// ---- normalise with given stats (+SiLU) (tensors.py:149-180, unet.py:291-293)
+__global__ void gn_apply_kernel(const fis_gn_apply_args a) {
+    const int t = cur_step(a.step);
+    const char* x = ref_base(a.x, t);
+    const float* mean = (const float*)ref_base(a.mean, t);
+    const float* var = (const float*)ref_base(a.var, t);
+    char* yn = a.y_norm.ptr ? ref_base(a.y_norm, t) : nullptr;
+    char* ys = a.y_silu.ptr ? ref_base(a.y_silu, t) : nullptr;
+    const int cpg = a.c / a.groups;
+    const long long total = (long long)a.rows * a.c;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+         e += (long long)gridDim.x * blockDim.x) {
+        const int r = (int)(e / a.c), c = (int)(e % a.c);
+        const int xr = a.x_rows ? __ldg(a.x_rows + r) : r;
+        const int yr = a.y_rows ? __ldg(a.y_rows + r) : r;
+        const int g = c / cpg;
+        const double xv = (double)load_elem(x, a.x.dtype, (long long)xr * a.x.ld + c);
+        const double y64 = (xv - (double)mean[g]) / sqrt((double)var[g] + (double)a.eps) * (double)a.gamma[c] +
+                           (double)a.beta[c];
+        const float y = (float)y64;
+        if (yn) store_elem(yn, a.y_norm.dtype, (long long)yr * a.y_norm.ld + c, y);
+        if (ys) {
+            const double yd = (double)y;
+            store_elem(ys, a.y_silu.dtype, (long long)yr * a.y_silu.ld + c, (float)(yd / (1.0 + exp(-yd))));
+        }
+    }
+}
+
+// ---- scaled row softmax; one warp per row (tensors.py:183-192, unet.py:555-566)
+__global__ void softmax_kernel(const fis_softmax_args a) {
+    const int t = cur_step(a.step);
+    const int warps = blockDim.x / 32;
+    const int row = blockIdx.x * warps + threadIdx.x / 32;
+    const int lane = threadIdx.x & 31;
+    if (row >= a.rows) return;
+    char* pb = ref_base(a.p, t);
+    char* mb = a.map.ptr ? ref_base(a.map, t) : nullptr;
+    const float* cached = a.cached.ptr ? (const float*)ref_base(a.cached, t) + (long long)row * a.cached.ld : nullptr;
+    const long long prow = (long long)row * a.p.ld;
+    if (a.verbatim) {
+        for (int j = lane; j < a.cols; j += 32) {
+            const float v = cached[j];
+            store_elem(pb, a.p.dtype, prow + j, v);
+            if (mb) ((float*)mb)[(long long)row * a.map.ld + j] = v;
+        }
+    } else {
+        const float* s = (const float*)ref_base(a.s, t) + (long long)row * a.s.ld;
+        float m = -INFINITY;
+        for (int j = lane; j < a.cols; j += 32) m = fmaxf(m, s[j] * a.scale);
+        m = warp_max(m);
+        float sum = 0.f;
+        for (int j = lane; j < a.cols; j += 32) sum += expf(s[j] * a.scale - m);
+        sum = warp_sum(sum);
+        const float inv_sum = 1.0f / sum;
+        if (a.npairs == 0) {
+            for (int j = lane; j < a.cols; j += 32) {
+                const float v = expf(s[j] * a.scale - m) * inv_sum;
+                store_elem(pb, a.p.dtype, prow + j, v);
+                if (mb) ((float*)mb)[(long long)row * a.map.ld + j] = v;
+            }
+        } else {
+            // pin shared-token columns to the cached map, renormalise rows (f32 sum, f64 divide)
+            float rs = 0.f;
+            for (int j = lane; j < a.cols; j += 32) {
+                float v = expf(s[j] * a.scale - m) * inv_sum;
+                for (int i = 0; i < a.npairs; i++)
+                    if (__ldg(a.pair_new + i) == j) v = cached[__ldg(a.pair_old + i)];
+                rs += v;
+            }
+            rs = warp_sum(rs);
+            for (int j = lane; j < a.cols; j += 32) {
+                float v = expf(s[j] * a.scale - m) * inv_sum;
+                for (int i = 0; i < a.npairs; i++)
+                    if (__ldg(a.pair_new + i) == j) v = cached[__ldg(a.pair_old + i)];
+                const float o = (float)((double)v / (double)rs);
+                store_elem(pb, a.p.dtype, prow + j, o);
+                if (mb) ((float*)mb)[(long long)row * a.map.ld + j] = o;
+            }
+        }
+    }
+    for (int j = a.cols + lane; j < a.pad_cols; j += 32) store_elem(pb, a.p.dtype, prow + j, 0.f);
+}
+
+// ---- 2x2 average pool with select-on-read (unet.py:296-298; numpy order (a+b)+(c+d))
+__global__ void pool2_kernel(const fis_pool_args a) {
+    const int t = cur_step(a.step);
+    const char* fr = a.src.fresh.ptr ? ref_base(a.src.fresh, t) : nullptr;
+    const char* ca = a.src.cache.ptr ? ref_base(a.src.cache, t) : nullptr;
+    char* out = ref_base(a.out, t);
+    const int cw = a.src.w / 2;
+    const long long total = (long long)a.n * a.c;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+         e += (long long)gridDim.x * blockDim.x) {
+        const int i = (int)(e / a.c), c = (int)(e % a.c);
+        const int P = a.rows ? __ldg(a.rows + i) : i;
+        const int py = P / cw, px = P - (P / cw) * cw;
+        const int q = (2 * py) * a.src.w + 2 * px;
+        const float v00 = src_value(a.src, fr, ca, q, c), v01 = src_value(a.src, fr, ca, q + 1, c);
+        const float v10 = src_value(a.src, fr, ca, q + a.src.w, c), v11 = src_value(a.src, fr, ca, q + a.src.w + 1, c);
+        const float s = __fadd_rn(__fadd_rn(v00, v01), __fadd_rn(v10, v11));
+        store_elem(out, a.out.dtype, (long long)i * a.out.ld + c, __fmul_rn(s, 0.25f));
+    }
+}
+
+// ---- full-map materialisation: out[q] = select(q)
+__global__ void materialize_kernel(const fis_materialize_args a) {
+    const int t = cur_step(a.step);
+    const char* fr = a.src.fresh.ptr ? ref_base(a.src.fresh, t) : nullptr;
+    const char* ca = a.src.cache.ptr ? ref_base(a.src.cache, t) : nullptr;
+    char* out = ref_base(a.out, t);
+    const long long total = (long long)a.src.h * a.src.w * a.c;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+         e += (long long)gridDim.x * blockDim.x) {
+        const int q = (int)(e / a.c), c = (int)(e % a.c);
+        store_elem(out, a.out.dtype, (long long)q * a.out.ld + c, src_value(a.src, fr, ca, q, c));
+    }
+}
+
+static int grid_for(long long total, int threads) {
+    long long b = (total + threads - 1) / threads;
+    if (b < 1) b = 1;
+    if (b > 148 * 16) b = 148 * 16;
+    return (int)b;
+}
+
+}  // namespace fis
+
+static int fis_check(void) { return cudaGetLastError() == cudaSuccess ? FIS_OK : FIS_ERR_LAUNCH; }
+
+extern "C" int fis_gn_stats(const fis_gn_stats_args* a, void* stream) {
+    if (a->groups <= 0 || a->c % a->groups) return FIS_ERR_SHAPE;
+    fis::gn_stats_kernel<<<a->groups, 256, 0, (cudaStream_t)stream>>>(*a);
+    return fis_check();
+}
+
+extern "C" int fis_gn_apply(const fis_gn_apply_args* a, void* stream) {
+    if (a->groups <= 0 || a->c % a->groups) return FIS_ERR_SHAPE;
+    if (a->rows == 0) return FIS_OK;
+    long long total = (long long)a->rows * a->c;
+    fis::gn_apply_kernel<<<fis::grid_for(total, 256), 256, 0, (cudaStream_t)stream>>>(*a);
+    return fis_check();
+}
+
+extern "C" int fis_softmax(const fis_softmax_args* a, void* stream) {
+    if (a->rows == 0) return FIS_OK;
+    if (a->pad_cols < a->cols) return FIS_ERR_SHAPE;
+    if ((a->verbatim || a->npairs) && !a->cached.ptr) return FIS_ERR_CACHE_MISS;
+    const int warps = 8;
+    fis::softmax_kernel<<<(a->rows + warps - 1) / warps, warps * 32, 0, (cudaStream_t)stream>>>(*a);
+    return fis_check();
+}
+
+extern "C" int fis_pool2(const fis_pool_args* a, void* stream) {
+    if (a->n == 0) return FIS_OK;
+    if (a->src.index && !a->src.cache.ptr) return FIS_ERR_CACHE_MISS;
+    long long total = (long long)a->n * a->c;
+    fis::pool2_kernel<<<fis::grid_for(total, 256), 256, 0, (cudaStream_t)stream>>>(*a);
+    return fis_check();
+}
+
+extern "C" int fis_materialize(const fis_materialize_args* a, void* stream) {
+    if (a->src.index && !a->src.cache.ptr) return FIS_ERR_CACHE_MISS;
+    long long total = (long long)a->src.h * a->src.w * a->c;
+    fis::materialize_kernel<<<fis::grid_for(total, 256), 256, 0, (cudaStream_t)stream>>>(*a);
+    return fis_check();
+}

@@ -1,0 +1,515 @@
+"""Device engine: weights in HBM, the per-generation HBM arena, and the dense and
+sparse (select-on-read) step programs launched through libfisedit.
+
+Layout: every feature map is NHWC-flattened `[pixels, C]`
+(channels contiguous). Per-step cache slabs are `[T+1, pixels, C]` tensors; a
+kernel addresses slab[t] as `base + t*stride` with t read from a device step
+counter, so a captured CUDA graph of one step replays every step.
+
+Sparse step: at a gated level the fresh values of a feature
+live only at the level's active pixels, in a compact `[n_active, C]` buffer in
+row-major active order; a read of pixel q selects `index[q] >= 0 ? fresh :
+cache[t][q]`. Nothing is ever copied from the cache; the cache is never
+mutated by an edit (no compaction, cache.py:538-579 is a numerical no-op).
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib as L
+from .errors import CacheMissError, ContractViolation
+from .model import (NORM_EPS, UNetConfig, build_registry, embed_ids, initial_latent_np, lcs_pairs, step_program,
+                    step_scale)
+
+_ESIZE = {torch.float32: 4, torch.bfloat16: 2}
+
+
+class DRef:
+    """A device buffer as the kernels see it: base (+byte offset) and a per-step stride."""
+
+    __slots__ = ("t", "ss", "off", "ld")
+
+    def __init__(self, t: torch.Tensor, ss: int = 0, off: int = 0, ld: int | None = None):
+        self.t, self.ss, self.off = t, ss, off
+        self.ld = ld if ld is not None else (t.stride(-2) if t.dim() >= 2 else 1)
+
+    def ref(self) -> L.Ref:
+        return L.Ref(self.t.data_ptr() + self.off, self.ss, self.ld, L.dt(self.t))
+
+    def cols(self, c0: int) -> "DRef":
+        """View starting at column c0 (same ld)."""
+        return DRef(self.t, self.ss, self.off + c0 * _ESIZE[self.t.dtype], self.ld)
+
+
+def slab(t: torch.Tensor, prev: bool = False) -> DRef:
+    """Per-step slab [T+1, ...] addressed as slab[t] (or slab[t-1] with prev=True)."""
+    ss = t.stride(0) * t.element_size()
+    return DRef(t[0], ss, -ss if prev else 0, ld=t.stride(1) if t.dim() >= 3 else 1)
+
+
+NULL = L.Ref(None, 0, 0, 0)
+
+
+def _r(x):
+    return x.ref() if x is not None else NULL
+
+
+@dataclass
+class FeatVal:
+    """Runtime value of a feature: full map (index None) or compact fresh rows + select-on-read cache."""
+
+    fresh: DRef
+    level: int
+    c: int
+    index: torch.Tensor | None = None
+    cache: DRef | None = None
+
+
+class Weights:
+    """Device copies of the seeded parameters in GEMM-ready layouts."""
+
+    def __init__(self, layers, topo, config: UNetConfig, act: torch.dtype, dev):
+        self.conv, self.norm, self.sa, self.ca = {}, {}, {}, {}
+        f32 = torch.float32
+        for hl in layers:
+            i, p = hl.info, hl.params
+            if i.kind == "conv":
+                w = p["weight"]  # (co, ci, 3, 3) -> B[co, (ky,kx,ci)]
+                b = torch.from_numpy(np.ascontiguousarray(w.transpose(0, 2, 3, 1).reshape(w.shape[0], -1)))
+                self.conv[i.layer_id] = (b.to(dev, act), torch.from_numpy(p["bias"]).to(dev, f32), hl.c_in)
+            elif i.kind == "norm":
+                self.norm[i.layer_id] = (torch.from_numpy(p["gamma"]).to(dev, f32), torch.from_numpy(p["beta"]).to(dev, f32))
+            elif i.kind == "self_attn":
+                wqk = np.concatenate([p["wq"].T, p["wk"].T], axis=0)
+                self.sa[i.layer_id] = (torch.from_numpy(np.ascontiguousarray(wqk)).to(dev, act),
+                                       torch.from_numpy(np.ascontiguousarray(p["wv"].T)).to(dev, act),
+                                       1.0 / math.sqrt(i.channels))
+            else:
+                self.ca[i.layer_id] = (torch.from_numpy(np.ascontiguousarray(p["wq"].T)).to(dev, act),
+                                       torch.from_numpy(np.ascontiguousarray(p["wk_text"].T)).to(dev, f32),
+                                       torch.from_numpy(np.ascontiguousarray(p["wv_text"].T)).to(dev, f32),
+                                       1.0 / math.sqrt(i.channels))
+        self.time_bias = torch.from_numpy(topo["time_bias"]).to(dev, f32)
+
+
+def _pad(n, m=16):
+    return (n + m - 1) // m * m
+
+
+class Engine:
+    """One model (config + precision) resident on one GPU."""
+
+    def __init__(self, config: UNetConfig, precision: str = "fp32", device=None):
+        L.require_cuda()
+        if precision not in ("fp32", "bf16"):
+            raise ContractViolation(f"precision must be 'fp32' or 'bf16', got {precision!r}")
+        self.config = config
+        self.precision = precision
+        self.dev = torch.device(device or "cuda")
+        self.act = torch.float32 if precision == "fp32" else torch.bfloat16
+        self.gemm_impl = 1 if precision == "fp32" else 0
+        self.layers, self.topo = build_registry(config)
+        self.info = {hl.info.layer_id: hl.info for hl in self.layers}
+        self.prog, self.feats = step_program(config, self.topo)
+        self.W = Weights(self.layers, self.topo, config, self.act, self.dev)
+        self.step_dev = torch.zeros(1, dtype=torch.int32, device=self.dev)
+        self.sms = L.lib().fis_device_sm_count()
+        self._ws = torch.zeros(1, dtype=torch.float32, device=self.dev)
+        self._counters = torch.zeros(1 << 16, dtype=torch.int32, device=self.dev)
+        self.gated = [config.latent_h * config.latent_w >> (2 * l) >= config.gate_fraction * config.latent_h * config.latent_w
+                      for l in range(config.levels)]
+        self.launches = 0
+        self._scratch = {}
+
+    # ------------------------------------------------------------------ helpers
+    def hw(self, level):
+        return (self.config.latent_h >> level) * (self.config.latent_w >> level)
+
+    def grid(self, level):
+        return self.config.latent_h >> level, self.config.latent_w >> level
+
+    def scratch(self, name, shape, dtype=None, zero=False):
+        key = (name, tuple(shape), dtype or self.act)
+        t = self._scratch.get(key)
+        if t is None:
+            t = (torch.zeros if zero else torch.empty)(shape, dtype=dtype or self.act, device=self.dev)
+            self._scratch[key] = t
+        return t
+
+    def _ensure_ws(self, floats):
+        if self._ws.numel() < floats:
+            self._ws = torch.empty(int(floats * 1.25) + 1024, dtype=torch.float32, device=self.dev)
+
+    def _splits(self, m, n, k):
+        tiles = ((m + 63) // 64) * ((n + 63) // 64)
+        ktiles = (k + 15) // 16
+        if tiles >= self.sms or ktiles < 32:
+            return 1
+        s = min(max(1, (2 * self.sms) // tiles), ktiles // 16, 32)
+        return max(1, s)
+
+    def src(self, fv: FeatVal, up=False):
+        h, w = self.grid(fv.level)
+        if fv.index is not None and fv.cache is None:
+            raise CacheMissError("?", "?", "feature cache")
+        return L.Src(fv.fresh.ref(), _r(fv.cache) if fv.index is not None else NULL,
+                     L.ptr(fv.index) if fv.index is not None else None, h, w, fv.c, 1 if up else 0)
+
+    def gemm(self, m, n, k, *, a=None, rows=None, srcs=None, out_hw=None, b: DRef, d: DRef, alpha=1.0, bias=None,
+             bias2=None, pre=None, epi=L.EPI_NONE, gn=None, lat=None, res=None, d_trans=False, splits=None):
+        if m == 0:
+            return
+        g = L.GemmArgs()
+        g.m, g.n, g.k = m, n, k
+        if srcs is not None:
+            g.a_mode = L.A_CONV3X3
+            g.nsrc = len(srcs)
+            for i, s in enumerate(srcs):
+                g.src[i] = s
+            g.out_h, g.out_w = out_hw
+        else:
+            g.a_mode = L.A_ROWS
+            g.a = a.ref()
+        g.rows = L.ptr(rows)
+        g.b = b.ref()
+        g.alpha = alpha
+        g.bias = L.ptr(bias)
+        g.bias2 = _r(bias2)
+        g.pre = _r(pre)
+        g.epi = epi
+        if gn is not None:
+            mean, var, gamma, beta, groups = gn
+            g.gn_mean, g.gn_var = mean.ref(), var.ref()
+            g.gamma, g.beta, g.groups, g.eps = L.ptr(gamma), L.ptr(beta), groups, NORM_EPS
+        g.lat = _r(lat)
+        g.step_scale = float(step_scale(self.config))
+        g.res = _r(res)
+        g.d = d.ref()
+        g.d_trans = 1 if d_trans else 0
+        s = self._splits(m, n, k) if splits is None else splits
+        if s > 1:
+            self._ensure_ws(s * m * n)
+            g.ws = L.ptr(self._ws)
+            g.counters = L.ptr(self._counters)
+        g.splits = s
+        g.step = L.ptr(self.step_dev)
+        g.impl = self.gemm_impl
+        L.call("fis_gemm", g)
+        self.launches += 1
+
+    def softmax(self, rows, cols, pad_cols, s: DRef, scale, p: DRef, map_: DRef | None = None, cached=None,
+                verbatim=False, pairs=None):
+        a = L.SoftmaxArgs()
+        a.rows, a.cols, a.pad_cols = rows, cols, pad_cols
+        a.s, a.scale, a.p, a.map = s.ref(), scale, p.ref(), _r(map_)
+        a.cached = _r(cached)
+        a.verbatim = 1 if verbatim else 0
+        if pairs is not None and not verbatim:
+            po, pn = pairs
+            a.npairs, a.pair_old, a.pair_new = po.numel(), L.ptr(po), L.ptr(pn)
+        a.step = L.ptr(self.step_dev)
+        L.call("fis_softmax", a)
+        self.launches += 1
+
+    # ------------------------------------------------------------ text K/V
+    def text_kv(self, text_emb: np.ndarray):
+        """Per cross layer K [n_text, C] and V^T [C, pad16(n_text)] (unet.py:476-479), once per prompt."""
+        nt = text_emb.shape[0]
+        emb = torch.from_numpy(np.ascontiguousarray(text_emb, dtype=np.float32)).to(self.dev)
+        out = {}
+        for lid, (wq, wk, wv, scale) in self.W.ca.items():
+            c = wq.shape[0]
+            k = torch.empty((nt, c), dtype=self.act, device=self.dev)
+            vt = torch.zeros((c, _pad(nt)), dtype=self.act, device=self.dev)
+            self.gemm(nt, c, emb.shape[1], a=DRef(emb), b=DRef(wk), d=DRef(k), splits=1)
+            self.gemm(nt, c, emb.shape[1], a=DRef(emb), b=DRef(wv), d=DRef(vt), d_trans=True, splits=1)
+            out[lid] = (k, vt)
+        return out
+
+    # ------------------------------------------------------------ building blocks
+    def attn_self(self, lid, m, s: DRef, y1: DRef, level, tag, pre=None):
+        """y1 = s + softmax(s Wq (s Wk)^T * scale) (s Wv) over m tokens (sparse.py:265-300/341-349)."""
+        wqk, wvt, scale = self.W.sa[lid]
+        c = wvt.shape[0]
+        cap = self.hw(level)
+        mp = _pad(cap)
+        qk = self.scratch(f"qk{tag}", (cap, 2 * c))
+        vt = self.scratch(f"vt{tag}", (c, mp), zero=True)
+        S = self.scratch(f"S{tag}", (cap, cap), torch.float32)
+        P = self.scratch(f"P{tag}", (cap, mp), zero=True)
+        self.gemm(m, 2 * c, c, a=s, b=DRef(wqk), d=DRef(qk))
+        self.gemm(m, c, c, a=s, b=DRef(wvt), d=DRef(vt, ld=mp), d_trans=True)
+        qkr = DRef(qk)
+        self.gemm(m, m, c, a=qkr, b=qkr.cols(c), d=DRef(S, ld=m))
+        self.softmax(m, m, _pad(m), DRef(S, ld=m), scale, DRef(P, ld=_pad(m)))
+        self.gemm(m, c, m, a=DRef(P, ld=_pad(m)), b=DRef(vt, ld=mp), d=y1, res=s, pre=pre)
+
+    def attn_cross(self, lid, m, x: DRef, out: DRef, level, tag, kv, pre=None, map_=None, ctrl=None):
+        """out = x + softmax(x Wq K_text^T * scale) V_text (sparse.py:303-338/352-361, unet.py:555-566)."""
+        wq, _, _, scale = self.W.ca[lid]
+        k, vt = kv[lid]
+        c, nt = wq.shape[0], k.shape[0]
+        ntp = vt.shape[1]
+        cap = self.hw(level)
+        q = self.scratch(f"q{tag}", (cap, c))
+        S = self.scratch(f"Sx{tag}", (cap, nt), torch.float32)
+        P = self.scratch(f"Px{tag}", (cap, ntp), zero=True)
+        self.gemm(m, c, c, a=x, b=DRef(wq), d=DRef(q))
+        self.gemm(m, nt, c, a=DRef(q), b=DRef(k), d=DRef(S))
+        if ctrl is not None:
+            cached, verbatim, pairs = ctrl
+            self.softmax(m, nt, ntp, DRef(S), scale, DRef(P), map_, cached=cached, verbatim=verbatim, pairs=pairs)
+        else:
+            self.softmax(m, nt, ntp, DRef(S), scale, DRef(P), map_)
+        self.gemm(m, c, ntp, a=DRef(P), b=DRef(vt), d=out, res=x, pre=pre)
+
+    def gn_stats(self, x: DRef, hw, c, mean: DRef, var: DRef):
+        a = L.GnStatsArgs(hw, c, self.config.groups, x.ref(), mean.ref(), var.ref(), L.ptr(self.step_dev))
+        L.call("fis_gn_stats", a)
+        self.launches += 1
+
+    def gn_apply(self, lid, x: DRef, rows, c, mean: DRef, var: DRef, y_norm: DRef | None, y_silu: DRef | None):
+        gamma, beta = self.W.norm[lid]
+        a = L.GnApplyArgs()
+        a.rows, a.c, a.groups, a.eps = rows, c, self.config.groups, NORM_EPS
+        a.x, a.mean, a.var = x.ref(), mean.ref(), var.ref()
+        a.gamma, a.beta = L.ptr(gamma), L.ptr(beta)
+        a.y_norm, a.y_silu = _r(y_norm), _r(y_silu)
+        a.step = L.ptr(self.step_dev)
+        L.call("fis_gn_apply", a)
+        self.launches += 1
+
+    def pool(self, fv: FeatVal, rows, n, out: DRef):
+        a = L.PoolArgs()
+        a.n, a.c, a.src, a.rows, a.out = n, fv.c, self.src(fv), L.ptr(rows), out.ref()
+        a.step = L.ptr(self.step_dev)
+        L.call("fis_pool2", a)
+        self.launches += 1
+
+    def materialize(self, fv: FeatVal, out: DRef):
+        a = L.MaterializeArgs(fv.c, self.src(fv), out.ref(), L.ptr(self.step_dev))
+        L.call("fis_materialize", a)
+        self.launches += 1
+
+    # ------------------------------------------------------------ one UNet step
+    def run_step(self, plan: "StepPlan"):
+        """Launch one UNet forward + step update (unet.py:430-458,693) for the current device step."""
+        vals = {}
+        cfg = self.config
+        for ins in self.prog:
+            op = ins[0]
+            if op == "stem":
+                lid, f = ins[1], ins[2]
+                self._conv(plan, lid, [(plan.latent_in(), False)], plan.out_buf(f), 0, bias2=slab(self.W.time_bias),
+                           pre=plan.record(lid, 0))
+                vals[f.key] = plan.value(f)
+            elif op == "block":
+                blk, fi, fo = ins[1], ins[2], ins[3]
+                self._block(plan, blk, vals[fi.key], fo)
+                vals[fo.key] = plan.value(fo)
+            elif op == "down":
+                lid, fi, fp, fo = ins[1], ins[2], ins[3], ins[4]
+                lv = fp.level
+                rows, n = plan.rows(lv)
+                self.pool(vals[fi.key], rows, n, plan.out_buf(fp))
+                pv = plan.value(fp)
+                self._conv(plan, lid, [(pv, False)], plan.out_buf(fo), lv, pre=plan.record(lid, 0))
+                vals[fo.key] = plan.value(fo)
+            elif op == "fuse":
+                lid, fu, fs, fo = ins[1], ins[2], ins[3], ins[4]
+                self._conv(plan, lid, [(vals[fu.key], True), (vals[fs.key], False)], plan.out_buf(fo), fo.level,
+                           pre=plan.record(lid, 0))
+                vals[fo.key] = plan.value(fo)
+            else:  # out conv + step update
+                lid, fi = ins[1], ins[2]
+                self._conv(plan, lid, [(vals[fi.key], False)], plan.latent_out(), 0, epi=L.EPI_STEP,
+                           lat=plan.latent_prev_rows(), pre=plan.record(lid, 0))
+        return vals
+
+    def _conv(self, plan, lid, inputs, out: DRef, level, **kw):
+        b, bias, cin = self.W.conv[lid]
+        rows, m = plan.rows(level)
+        srcs = [self.src(fv, up) for fv, up in inputs]
+        self.gemm(m, b.shape[0], b.shape[1], rows=rows, srcs=srcs, out_hw=self.grid(level), b=DRef(b), d=out,
+                  bias=bias, **kw)
+
+    def _block(self, plan, blk, x: FeatVal, fo):
+        """conv -> GN -> SiLU -> +self-attn -> +cross-attn (unet.py:452-458)."""
+        level, c = fo.level, fo.channels
+        cap = self.hw(level)
+        rows, m = plan.rows(level)
+        tag = f"L{level}"
+        s = DRef(self.scratch(f"s{tag}", (cap, c)))
+        nl = blk["norm"]
+        if plan.sparse(level):
+            mean, var = plan.stats(nl)
+            gamma, beta = self.W.norm[nl]
+            self._conv(plan, blk["conv"], [(x, False)], s, level, epi=L.EPI_GN_SILU,
+                       gn=(mean, var, gamma, beta, self.config.groups))
+        else:
+            co = plan.record(blk["conv"], 0) or DRef(self.scratch(f"co{tag}", (cap, c)))
+            self._conv(plan, blk["conv"], [(x, False)], co, level)
+            mean, var = plan.stats(nl)
+            self.gn_stats(co, cap, c, mean, var)
+            self.gn_apply(nl, co, cap, c, mean, var, plan.record(nl, 0), s)
+        y1 = DRef(self.scratch(f"y1{tag}", (cap, c)))
+        self.attn_self(blk["self_attn"], m, s, y1, level, tag, pre=plan.record(blk["self_attn"], 0))
+        lid = blk["cross_attn"]
+        self.attn_cross(lid, m, y1, plan.out_buf(fo), level, tag, plan.kv, pre=plan.record(lid, 0),
+                        map_=plan.record(lid, 3), ctrl=plan.ctrl(lid))
+
+
+# ---------------------------------------------------------------------------
+# HBM arena of one cached generation
+# ---------------------------------------------------------------------------
+
+class Arena:
+    """Per-step HBM slabs of one generation (replaces the CacheStore tiers, cache.py:281-679).
+
+    engine features: FEATURE/POOLED maps of gated levels, gated-norm stats, cross-attention
+    maps, step latents. `full=True` also keeps every reference role (LAYER_OUTPUT of all
+    layers, all norm stats) for API-level `store.get` parity.
+    """
+
+    def __init__(self, eng: Engine, n_text: int, full: bool):
+        cfg = eng.config
+        T = cfg.steps
+        dev, f32 = eng.dev, torch.float32
+        self.eng, self.n_text, self.full, self.T = eng, n_text, full, T
+        self.latent = torch.empty((T + 1, eng.hw(0), cfg.latent_channels), dtype=f32, device=dev)
+        self.feature = {}
+        for key, f in eng.feats.items():
+            if eng.gated[f.level]:
+                self.feature[key] = torch.empty((T + 1, eng.hw(f.level), f.channels), dtype=eng.act, device=dev)
+        self.stats = {}
+        self.maps = {}
+        self.outputs = {}
+        for hl in eng.layers:
+            i = hl.info
+            if i.kind == "norm" and (i.gated or full):
+                self.stats[i.layer_id] = (torch.empty((T + 1, cfg.groups), dtype=f32, device=dev),
+                                          torch.empty((T + 1, cfg.groups), dtype=f32, device=dev))
+            if i.kind == "cross_attn":
+                self.maps[i.layer_id] = torch.empty((T + 1, eng.hw(i.level), n_text), dtype=f32, device=dev)
+            if full:
+                self.outputs[i.layer_id] = torch.empty((T + 1, eng.hw(i.level), i.channels), dtype=f32, device=dev)
+
+    def nbytes(self):
+        ts = [self.latent, *self.feature.values(), *self.maps.values(), *self.outputs.values()]
+        ts += [x for p in self.stats.values() for x in p]
+        return sum(t.numel() * t.element_size() for t in ts)
+
+
+# ---------------------------------------------------------------------------
+# step plans: where each instruction reads and writes
+# ---------------------------------------------------------------------------
+
+class StepPlan:
+    """Dense plan: full maps at every level. Records into an arena when given."""
+
+    def __init__(self, eng: Engine, kv, latents: torch.Tensor, arena: Arena | None = None, ctrl=None):
+        self.eng, self.kv, self.arena, self._ctrl = eng, kv, arena, ctrl
+        self.latents = latents  # [T+1, HW, Cl] f32 slab: [t-1] in, [t] out
+
+    def sparse(self, level):
+        return False
+
+    def rows(self, level):
+        return None, self.eng.hw(level)
+
+    def latent_in(self) -> FeatVal:
+        return FeatVal(slab(self.latents, prev=True), 0, self.eng.config.latent_channels)
+
+    def latent_out(self) -> DRef:
+        return slab(self.latents)
+
+    def latent_prev_rows(self) -> DRef:
+        return slab(self.latents, prev=True)
+
+    def out_buf(self, f) -> DRef:
+        if self.arena is not None and f.key in self.arena.feature:
+            return slab(self.arena.feature[f.key])
+        return DRef(self.eng.scratch(f"feat{f.key}", (self.eng.hw(f.level), f.channels)))
+
+    def value(self, f) -> FeatVal:
+        return FeatVal(self.out_buf(f), f.level, f.channels)
+
+    def record(self, lid, role):
+        a = self.arena
+        if a is None:
+            return None
+        if role == 3:
+            return slab(a.maps[lid]) if lid in a.maps else None
+        if a.full and role == 0:
+            return slab(a.outputs[lid])
+        return None
+
+    def stats(self, nl):
+        a = self.arena
+        if a is not None and nl in a.stats:
+            m, v = a.stats[nl]
+            return slab(m), slab(v)
+        g = self.eng.config.groups
+        return (DRef(self.eng.scratch(f"mean{nl}", (1, g), torch.float32)),
+                DRef(self.eng.scratch(f"var{nl}", (1, g), torch.float32)))
+
+    def ctrl(self, lid):
+        if self._ctrl is None:
+            return None
+        arena, verbatim, pairs = self._ctrl
+        return slab(arena.maps[lid]), verbatim, pairs
+
+
+class SparsePlan(StepPlan):
+    """Select-on-read plan over a cached generation (the edit's sparse steps)."""
+
+    def __init__(self, eng: Engine, kv, arena: Arena, lists, lat_rows: torch.Tensor):
+        super().__init__(eng, kv, arena.latent, None)
+        self.src_arena = arena
+        self.lists = lists  # level -> (rows int32 [n], index int32 [hw], n)
+        self.lat_rows = lat_rows  # [n0, Cl] f32 fresh latent rows (updated in place)
+
+    def sparse(self, level):
+        return self.eng.gated[level]
+
+    def rows(self, level):
+        if self.sparse(level):
+            r, _, n = self.lists[level]
+            return r, n
+        return None, self.eng.hw(level)
+
+    def latent_in(self) -> FeatVal:
+        _, idx, _ = self.lists[0]
+        return FeatVal(DRef(self.lat_rows), 0, self.eng.config.latent_channels, idx,
+                       slab(self.src_arena.latent, prev=True))
+
+    def latent_out(self) -> DRef:
+        return DRef(self.lat_rows)
+
+    def latent_prev_rows(self) -> DRef:
+        return DRef(self.lat_rows)
+
+    def out_buf(self, f) -> DRef:
+        if self.sparse(f.level):
+            return DRef(self.eng.scratch(f"sfeat{f.key}", (self.eng.hw(f.level), f.channels)))
+        return DRef(self.eng.scratch(f"feat{f.key}", (self.eng.hw(f.level), f.channels)))
+
+    def value(self, f) -> FeatVal:
+        if self.sparse(f.level):
+            _, idx, _ = self.lists[f.level]
+            return FeatVal(self.out_buf(f), f.level, f.channels, idx, slab(self.src_arena.feature[f.key]))
+        return FeatVal(self.out_buf(f), f.level, f.channels)
+
+    def record(self, lid, role):
+        return None
+
+    def stats(self, nl):
+        if self.eng.info[nl].gated:
+            m, v = self.src_arena.stats[nl]
+            return slab(m), slab(v)
+        return super().stats(nl)

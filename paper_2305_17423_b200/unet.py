@@ -1,0 +1,410 @@
+"""Model + pipeline API (reference unet.py:1-899) over the B200 engine.
+
+Entry points keep the reference names and signatures:
+  generate_dense(prompt, config, store=None)       unet.py:680
+  detect_mask(session, config, store)              unet.py:709
+  edit(session, config, store) -> EditResult       unet.py:823
+plus UNetConfig, PromptTokens, SharedTokenMap, EditSession, UNet, initial_latent,
+embed_tokens. All compute runs in libfisedit kernels on the GPU; inputs and
+outputs at this boundary are float32 NCHW numpy arrays as in the reference.
+
+Precision: `set_precision("fp32")` (default; fp32 operands, fp32 accumulate —
+the parity mode) or `set_precision("bf16")` (bf16 operands/activations on the
+tcgen05 tensor cores, fp32 accumulate, fp32 softmax/GN/latent — the perf mode).
+"""
+
+from __future__ import annotations
+
+from collections import defaultdict
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib as L
+from .cache import CacheStore, Role
+from .engine import Arena, DRef, Engine, FeatVal, SparsePlan, StepPlan, slab
+from .errors import CacheMissError, ConfigError, ContractViolation
+from .masks import BinaryMask, DevicePlan, run_detect
+from .model import (LayerInfo, UNetConfig, build_registry, embed_ids, initial_latent_np, lcs_pairs,
+                    require_tensor4, step_scale)
+from .sparse import GatherPlan
+from .tensors import LayerMacs, MacsReport, macs_attention, macs_linear
+
+_PRECISION = "fp32"
+_ENGINES: dict = {}
+
+
+def set_precision(p: str) -> None:
+    global _PRECISION
+    if p not in ("fp32", "bf16"):
+        raise ConfigError(f"precision must be 'fp32' or 'bf16', got {p!r}")
+    _PRECISION = p
+
+
+def get_precision() -> str:
+    return _PRECISION
+
+
+def get_engine(config: UNetConfig, precision: str | None = None) -> Engine:
+    p = precision or _PRECISION
+    key = (config.key(), p, torch.cuda.current_device() if torch.cuda.is_available() else -1)
+    eng = _ENGINES.get(key)
+    if eng is None:
+        eng = Engine(config, p)
+        _ENGINES[key] = eng
+    return eng
+
+
+# ---------------------------------------------------------------------------
+# prompts and sessions (unet.py:141-244)
+# ---------------------------------------------------------------------------
+
+@dataclass(frozen=True)
+class PromptTokens:
+    ids: tuple
+
+    def __post_init__(self):
+        object.__setattr__(self, "ids", tuple(int(i) for i in self.ids))
+        if not self.ids:
+            raise ConfigError("prompt must contain at least one token")
+
+
+def embed_tokens(tokens: PromptTokens, config: UNetConfig) -> np.ndarray:
+    return embed_ids(tokens.ids, config)
+
+
+@dataclass(frozen=True)
+class SharedTokenMap:
+    pairs: tuple
+
+    def __post_init__(self):
+        prev = (-1, -1)
+        for p in self.pairs:
+            if not (p[0] > prev[0] and p[1] > prev[1]):
+                raise ContractViolation(f"shared pairs must be strictly increasing, got {self.pairs}")
+            prev = p
+
+    @classmethod
+    def from_ids(cls, old_ids, new_ids) -> "SharedTokenMap":
+        return cls(lcs_pairs(tuple(old_ids), tuple(new_ids)))
+
+
+@dataclass
+class EditSession:
+    old_tokens: PromptTokens
+    new_tokens: PromptTokens
+    shared: SharedTokenMap
+    t1: int
+    t2: int
+    store: CacheStore
+    user_mask: BinaryMask | None = None
+    schedule: tuple = ()
+    mask: BinaryMask | None = None
+
+    @classmethod
+    def create(cls, old_ids, new_ids, config: UNetConfig, store: CacheStore, user_mask=None, t1=None, t2=None):
+        t1 = config.t1 if t1 is None else t1
+        t2 = config.t2 if t2 is None else t2
+        if not (1 <= t1 <= t2 <= config.steps):
+            raise ConfigError(f"need 1 <= t1 <= t2 <= steps, got t1={t1} t2={t2} steps={config.steps}")
+        if user_mask is None and t2 > 10:
+            raise ConfigError(f"detection window ends at step 10 at the latest, got t2={t2}")
+        if user_mask is not None and user_mask.shape != (config.latent_h, config.latent_w):
+            raise ConfigError(f"user mask shape {user_mask.shape} != latent {(config.latent_h, config.latent_w)}")
+        old, new = PromptTokens(tuple(old_ids)), PromptTokens(tuple(new_ids))
+        return cls(old, new, SharedTokenMap.from_ids(old.ids, new.ids), t1, t2, store, user_mask,
+                   tuple(range(1, config.steps + 1)))
+
+
+# ---------------------------------------------------------------------------
+# UNet (layer registry + MAC accounting; unet.py:305-426)
+# ---------------------------------------------------------------------------
+
+class UNet:
+    """Layer registry with stable ids (cache keys) and analytic MACs; weights live on the engine."""
+
+    def __init__(self, config: UNetConfig):
+        self.config = config
+        hl, topo = build_registry(config, with_params=False)
+        self.layers: list[LayerInfo] = [h.info for h in hl]
+        self._cin = {h.info.layer_id: h.c_in for h in hl}
+        self.topo = topo
+        self.cross_layers = [i.layer_id for i in self.layers if i.kind == "cross_attn"]
+        self._by_id = {i.layer_id: i for i in self.layers}
+
+    def info(self, layer_id: int) -> LayerInfo:
+        return self._by_id[layer_id]
+
+    def conv_cin(self, lid):
+        return self._cin[lid]
+
+    def layer_macs(self, info: LayerInfo, px: int, n_text: int) -> int:
+        c = info.channels
+        if info.kind == "conv":
+            return px * c * self._cin[info.layer_id] * 9
+        if info.kind == "norm":
+            return 0
+        if info.kind == "self_attn":
+            return 3 * macs_linear(px, c, c) + macs_attention(px, px, c)
+        return macs_linear(px, c, c) + 2 * macs_linear(n_text, self.config.text_dim, c) + macs_attention(px, n_text, c)
+
+    def dense_step_macs(self, n_text: int) -> dict:
+        return {i.layer_id: self.layer_macs(i, i.h * i.w, n_text) for i in self.layers}
+
+    def sparse_step_macs(self, n_text, active, tile_cost) -> dict:
+        """Per-layer MACs of one SparseMode step (unet.py:604-663): gated convs count plan.cost,
+        gated attention the active-pixel count, ungated layers are dense."""
+        out = {}
+        for i in self.layers:
+            if not i.gated:
+                out[i.layer_id] = self.layer_macs(i, i.h * i.w, n_text)
+            elif i.kind == "conv":
+                out[i.layer_id] = self.layer_macs(i, tile_cost[i.level], n_text)
+            else:
+                out[i.layer_id] = self.layer_macs(i, active[i.level], n_text)
+        return out
+
+
+def initial_latent(config: UNetConfig) -> np.ndarray:
+    return initial_latent_np(config)
+
+
+def _to_nhwc(a: np.ndarray, dev) -> torch.Tensor:
+    n, c, h, w = a.shape
+    return torch.from_numpy(np.ascontiguousarray(a[0].reshape(c, h * w).T)).to(dev)
+
+
+def _to_nchw(t: torch.Tensor, c, h, w) -> np.ndarray:
+    return t.float().reshape(h, w, c).permute(2, 0, 1).reshape(1, c, h, w).contiguous().cpu().numpy()
+
+
+# ---------------------------------------------------------------------------
+# pipeline
+# ---------------------------------------------------------------------------
+
+class _Runner:
+    """Drives Engine steps for t in a range, eagerly or through one captured CUDA graph."""
+
+    def __init__(self, eng: Engine, plan, use_graph: bool):
+        self.eng, self.plan, self.use_graph = eng, plan, use_graph
+        self.graph = None
+
+    def step(self, t: int):
+        eng = self.eng
+        eng.step_dev.fill_(t)
+        if not self.use_graph:
+            eng.run_step(self.plan)
+            return
+        if self.graph is None:
+            # warm (allocates scratch), then capture one step; replays read t from step_dev
+            eng.run_step(self.plan)
+            torch.cuda.synchronize()
+            s = torch.cuda.Stream()
+            s.wait_stream(torch.cuda.current_stream())
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.stream(s):
+                with torch.cuda.graph(g, stream=s):
+                    eng.run_step(self.plan)
+            torch.cuda.current_stream().wait_stream(s)
+            self.graph = g
+            return
+        self.graph.replay()
+
+    def run(self, t0, t1):
+        for t in range(t0, t1 + 1):
+            self.step(t)
+
+
+def _use_graphs():
+    return True
+
+
+def generate_dense(prompt: PromptTokens, config: UNetConfig, store: CacheStore | None = None, *,
+                   record: str = "full", precision: str | None = None) -> np.ndarray:
+    """Dense generation; records the generation into an HBM arena bound to `store` (unet.py:680-696).
+
+    record="full" keeps every reference role (LAYER_OUTPUT, NORM stats, maps, latents);
+    record="engine" keeps only what edits read (features, gated stats, maps, latents).
+    """
+    eng = get_engine(config, precision)
+    text = embed_tokens(prompt, config)
+    kv = eng.text_kv(text)
+    T = config.steps
+    hw = eng.hw(0)
+    if store is not None:
+        arena = Arena(eng, text.shape[0], full=(record == "full"))
+        latents = arena.latent
+    else:
+        arena = None
+        latents = torch.empty((T + 1, hw, config.latent_channels), dtype=torch.float32, device=eng.dev)
+    latents[0].copy_(_to_nhwc(initial_latent_np(config), eng.dev))
+    _Runner(eng, StepPlan(eng, kv, latents, arena), _use_graphs()).run(1, T)
+    if store is not None:
+        arena.prompt = tuple(prompt.ids)
+        store._bind(eng, arena)
+    return _to_nchw(latents[T], config.latent_channels, config.latent_h, config.latent_w)
+
+
+@dataclass
+class _MacsCounter:
+    per_layer: dict = field(default_factory=lambda: defaultdict(int))
+
+    def add(self, layer_id, macs):
+        self.per_layer[layer_id] += macs
+
+    @property
+    def total(self):
+        return sum(self.per_layer.values())
+
+
+@dataclass
+class DetectOutcome:
+    no_edit: bool
+    mask: BinaryMask | None
+    epsilon: float
+    control_latent: np.ndarray | None
+    phase1_macs: _MacsCounter
+    from_user_mask: bool = False
+    _control_dev: object = None
+    diff: object = None
+
+
+def _arena_of(store: CacheStore, config: UNetConfig, t_first: int):
+    a = store.arena if store is not None else None
+    if a is None:
+        unet = UNet(config)
+        lid = next(i.layer_id for i in unet.layers if i.gated)
+        raise CacheMissError(t_first, lid, "layer_output")
+    return a
+
+
+def detect_mask(session: EditSession, config: UNetConfig, store: CacheStore) -> DetectOutcome:
+    """Controlled steps 1..t2 on device, then the fused diff/Otsu/dilate kernel (unet.py:709-752)."""
+    macs = _MacsCounter()
+    if session.user_mask is not None:
+        return DetectOutcome(session.user_mask.is_empty(), session.user_mask, 0.0, None, macs, True)
+    arena = _arena_of(store, config, 1)
+    eng = get_engine(config, arena.eng.precision)
+    text = embed_tokens(session.new_tokens, config)
+    n_new = text.shape[0]
+    kv = eng.text_kv(text)
+    pairs = session.shared.pairs
+    verbatim = len(pairs) == n_new and n_new == arena.n_text
+    po = torch.tensor([p[0] for p in pairs] or [0], dtype=torch.int32, device=eng.dev)
+    pn = torch.tensor([p[1] for p in pairs] or [0], dtype=torch.int32, device=eng.dev)
+    pairs_dev = (po[: len(pairs)], pn[: len(pairs)])
+    t2 = session.t2
+    hw, cl = eng.hw(0), config.latent_channels
+    ys = torch.empty((t2 + 1, hw, cl), dtype=torch.float32, device=eng.dev)
+    ys[0].copy_(_to_nhwc(initial_latent_np(config), eng.dev))
+    plan = StepPlan(eng, kv, ys, None, ctrl=(arena, verbatim, pairs_dev))
+    _Runner(eng, plan, _use_graphs()).run(1, t2)
+    unet = UNet(config)
+    dense = unet.dense_step_macs(n_new)
+    for lid, m in dense.items():
+        macs.add(lid, m * t2)
+    xr = L.Ref(arena.latent[1].data_ptr(), arena.latent.stride(0) * 4, cl, L.F32)
+    yr = L.Ref(ys[1].data_ptr(), ys.stride(0) * 4, cl, L.F32)
+    out = run_detect(config.latent_h, config.latent_w, cl, session.t1, t2, config.dilation_radius, xr, yr)
+    res = out["result"].cpu().tolist()
+    no_edit = bool(out["flags"][0].item())
+    control = ys[t2]
+    ctrl_np = _to_nchw(control, cl, config.latent_h, config.latent_w)
+    if no_edit:
+        return DetectOutcome(True, None, float(res[0]), ctrl_np, macs, False, control)
+    mask = BinaryMask(out["mask"].cpu().numpy().astype(bool).reshape(config.latent_h, config.latent_w))
+    return DetectOutcome(False, mask, float(res[0]), ctrl_np, macs, False, control)
+
+
+@dataclass
+class EditResult:
+    latent: np.ndarray
+    macs: MacsReport
+    cache_stats: object
+    mask: BinaryMask | None
+    no_edit: bool
+    phase1_macs: int
+    phase2_macs: int
+    plans: dict = field(default_factory=dict)
+
+
+def _build_report(unet: UNet, n_text, config, counters):
+    dense = unet.dense_step_macs(n_text)
+    tot = defaultdict(int)
+    for c in counters:
+        for lid, m in c.per_layer.items():
+            tot[lid] += m
+    return MacsReport([LayerMacs(i.layer_id, i.kind, dense[i.layer_id] * config.steps, tot.get(i.layer_id, 0))
+                       for i in unet.layers])
+
+
+class EditPlan:
+    """Device-side plan of one edit: mask pyramid lists + the sparse step plan."""
+
+    def __init__(self, eng: Engine, arena: Arena, mask: BinaryMask, kv, lat0_full: torch.Tensor):
+        cfg = eng.config
+        self.dp = DevicePlan(torch.from_numpy(mask.bits.astype(np.uint8).ravel()).to(eng.dev),
+                             cfg.latent_h, cfg.latent_w, cfg.levels)
+        lists = {l: (self.dp.rows[l], self.dp.index[l], self.dp.n_active[l]) for l in range(cfg.levels)}
+        n0 = self.dp.n_active[0]
+        rows0 = self.dp.rows[0][:n0].long()
+        self.lat_rows = lat0_full.index_select(0, rows0).contiguous()
+        self.plan = SparsePlan(eng, kv, arena, lists, self.lat_rows)
+
+    def final_latent(self, eng: Engine, arena: Arena) -> torch.Tensor:
+        cfg = eng.config
+        out = torch.empty((eng.hw(0), cfg.latent_channels), dtype=torch.float32, device=eng.dev)
+        fv = FeatVal(DRef(self.lat_rows), 0, cfg.latent_channels, self.dp.index[0], DRef(arena.latent[cfg.steps]))
+        eng.step_dev.fill_(0)
+        eng.materialize(fv, DRef(out))
+        return out
+
+
+def edit(session: EditSession, config: UNetConfig, store: CacheStore) -> EditResult:
+    """Incremental regeneration for the edited prompt (unet.py:823-899) on the B200 engine."""
+    unet = UNet(config)
+    n_new = len(session.new_tokens.ids)
+    outcome = detect_mask(session, config, store)
+    session.mask = outcome.mask
+    phase2 = _MacsCounter()
+    cl, H, W, T = config.latent_channels, config.latent_h, config.latent_w, config.steps
+    if outcome.no_edit:
+        arena = _arena_of(store, config, T)
+        latent = _to_nchw(arena.latent[T], cl, H, W)
+        rep = _build_report(unet, n_new, config, [outcome.phase1_macs])
+        return EditResult(latent, rep, store.stats(), outcome.mask, True, outcome.phase1_macs.total, 0)
+    mask = outcome.mask
+    start = 1 if outcome.from_user_mask else session.t2 + 1
+    arena = _arena_of(store, config, start)
+    eng = get_engine(config, arena.eng.precision)
+    kv = eng.text_kv(embed_tokens(session.new_tokens, config))
+    if outcome.from_user_mask:
+        lat0 = _to_nhwc(initial_latent_np(config), eng.dev)
+    else:
+        m = torch.from_numpy(mask.bits.ravel()).to(eng.dev)[:, None]
+        lat0 = torch.where(m, outcome._control_dev, arena.latent[session.t2])
+    plans = {}
+    if mask.all_active():
+        latents = torch.empty((T + 1, eng.hw(0), cl), dtype=torch.float32, device=eng.dev)
+        latents[start - 1].copy_(lat0)
+        _Runner(eng, StepPlan(eng, kv, latents, None), _use_graphs()).run(start, T)
+        final = latents[T]
+        dense = unet.dense_step_macs(n_new)
+        for lid, m_ in dense.items():
+            phase2.add(lid, m_ * (T - start + 1))
+    else:
+        ep = EditPlan(eng, arena, mask, kv, lat0)
+        _Runner(eng, ep.plan, _use_graphs()).run(start, T)
+        final = ep.final_latent(eng, arena)
+        levels = sorted({i.level for i in unet.layers if i.gated})
+        cost = {l: 4 * ep.dp.n_tiles[l] for l in range(config.levels)}
+        per_step = unet.sparse_step_macs(n_new, ep.dp.n_active, cost)
+        for lid, m_ in per_step.items():
+            phase2.add(lid, m_ * (T - start + 1))
+        for l in levels:
+            org = ep.dp.origins(l)
+            plans[l] = GatherPlan((4, 4), (2, 2), (3, 3), org, 4 * len(org), (H >> l, W >> l))
+    latent = _to_nchw(final, cl, H, W)
+    rep = _build_report(unet, n_new, config, [outcome.phase1_macs, phase2])
+    return EditResult(latent, rep, store.stats(), mask, False, outcome.phase1_macs.total, phase2.total, plans)
