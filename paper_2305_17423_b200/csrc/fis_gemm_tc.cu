@@ -1,7 +1,328 @@
-// tcgen05 (5th-gen tensor core) bf16 gather-GEMM — placeholder until the
-// sm_100a kernel lands; reports "unsupported" so dispatch uses the SIMT path.
+// tcgen05 (5th-gen tensor core) bf16 gather-GEMM for sm_100a.
+//
+//   D[r, n] = epi( sum_k A[r,k] * B[n,k] ),  bf16 operands, fp32 accumulation in TMEM.
+//
+// Structure (one CTA = one 128 x BN output tile, one K split):
+//   warps 0-3 : producers — gather the A rows (implicit 3x3 conv with select-on-read,
+//               or plain rows) and the B rows (weights) with 16-byte cp.async straight
+//               into 128B-swizzled K-major shared memory (the canonical UMMA SW128
+//               layout); a stage is published with fence.proxy.async + mbarrier arrive.
+//               After the main loop the same warps run the epilogue: tcgen05.ld of
+//               their 32 TMEM lanes -> fused epilogue (bias, time bias, cached-stat
+//               GN+SiLU, step update, residual) -> global stores.
+//   warp 4    : TMEM allocator + MMA issuer (one elected thread issues
+//               tcgen05.mma.cta_group::1.kind::f16, M=128, N=BN, K=16 per instruction;
+//               tcgen05.commit frees smem stages and finally signals the epilogue).
+// Split-K partials go to a workspace and the last CTA of a tile reduces them in fixed
+// split order (bitwise deterministic). The A gather cannot use TMA tiles: rows are
+// scattered active pixels whose halo reads select between the fresh compact buffer
+// and the step's cache slab per pixel.
 #include "fis_common.cuh"
 
-int fis_gemm_tc_supported(const fis_gemm_args*) { return 0; }
+namespace fis {
+namespace tc {
 
-int fis_gemm_tc_launch(const fis_gemm_args*, cudaStream_t) { return FIS_ERR_UNSUPPORTED; }
+constexpr int BM = 128, BK = 64, STAGES = 4, PRODUCERS = 128, THREADS = 160;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(b)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, bool valid) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(valid ? 16 : 0) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+// K-major, 128B-swizzled UMMA shared-memory descriptor (LBO=16B, SBO=1024B, version 1)
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
+    return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
+           ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+
+// byte offset of 16B chunk j of row r inside a SW128 K-major tile (rows of 128 B)
+__device__ __forceinline__ uint32_t sw128_off(int r, int j) {
+    return (uint32_t)((r >> 3) * 1024 + (r & 7) * 128 + ((j ^ (r & 7)) << 4));
+}
+
+template <int BN>
+struct Smem {
+    static constexpr int A_BYTES = BM * BK * 2;
+    static constexpr int B_BYTES = BN * BK * 2;
+    static constexpr int STAGE = A_BYTES + B_BYTES;
+    static constexpr int TOTAL = STAGES * STAGE + 1024 /*align*/ + 256 /*barriers*/;
+};
+
+// Source pointer of the 64-channel K block starting at k0 for GEMM row r (16B granularity),
+// or nullptr for zero (padding / out of image / beyond K).
+__device__ __forceinline__ const char* a_block_ptr(const fis_gemm_args& a, const char* abase, const char* f0,
+                                                   const char* c0p, const char* f1, const char* c1p, int r, int k0,
+                                                   int cin) {
+    if (r >= a.m) return nullptr;
+    const int p = a.rows ? __ldg(a.rows + r) : r;
+    if (a.a_mode == FIS_A_ROWS) {
+        if (k0 >= a.k) return nullptr;
+        return abase + ((long long)p * a.a.ld + k0) * 2;
+    }
+    const int tap = k0 / cin;
+    int c = k0 - tap * cin;
+    const int oy = p / a.out_w, ox = p - (p / a.out_w) * a.out_w;
+    const int y = oy + tap / 3 - 1, x = ox + tap % 3 - 1;
+    if (y < 0 || x < 0 || y >= a.out_h || x >= a.out_w) return nullptr;
+    const bool second = c >= a.src[0].c;
+    const fis_src& s = second ? a.src[1] : a.src[0];
+    if (second) c -= a.src[0].c;
+    const int sy = s.up ? (y >> 1) : y, sx = s.up ? (x >> 1) : x;
+    const int q = sy * s.w + sx;
+    const char* fr = second ? f1 : f0;
+    const char* ca = second ? c1p : c0p;
+    if (s.index) {
+        const int i = __ldg(s.index + q);
+        if (i >= 0) return fr + ((long long)i * s.fresh.ld + c) * 2;
+        return ca + ((long long)q * s.cache.ld + c) * 2;
+    }
+    return fr + ((long long)q * s.fresh.ld + c) * 2;
+}
+
+template <int BN>
+__global__ void __launch_bounds__(THREADS, 1) gemm_tc_kernel(const fis_gemm_args a) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char* smem = (unsigned char*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    uint64_t* full = (uint64_t*)(smem + STAGES * Smem<BN>::STAGE);
+    uint64_t* empty = full + STAGES;
+    uint64_t* done = empty + STAGES;
+    uint32_t* tmem_slot = (uint32_t*)(done + 1);
+    int* last_flag = (int*)(tmem_slot + 1);
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int t = cur_step(a.step);
+    const int n0 = blockIdx.x * BN, m0 = blockIdx.y * BM;
+    const int kblocks = (a.k + BK - 1) / BK;
+    const int kper = (kblocks + a.splits - 1) / a.splits;
+    const int kb0 = blockIdx.z * kper, kb1 = min(kblocks, kb0 + kper);
+    const int nk = max(0, kb1 - kb0);
+
+    if (tid == 0) {
+        for (int s = 0; s < STAGES; s++) {
+            mbar_init(full + s, PRODUCERS);
+            mbar_init(empty + s, 1);
+        }
+        mbar_init(done, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 4) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "n"(BN < 32 ? 32 : BN));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp < 4) {
+        // ------------------------------------------------------------ producers
+        const char* abase = a.a.ptr ? ref_base(a.a, t) : nullptr;
+        const char* f0 = a.nsrc > 0 && a.src[0].fresh.ptr ? ref_base(a.src[0].fresh, t) : nullptr;
+        const char* c0p = a.nsrc > 0 && a.src[0].cache.ptr ? ref_base(a.src[0].cache, t) : nullptr;
+        const char* f1 = a.nsrc > 1 && a.src[1].fresh.ptr ? ref_base(a.src[1].fresh, t) : nullptr;
+        const char* c1p = a.nsrc > 1 && a.src[1].cache.ptr ? ref_base(a.src[1].cache, t) : nullptr;
+        const char* bbase = ref_base(a.b, t);
+        const int cin = a.a_mode == FIS_A_CONV3X3 ? a.src[0].c + (a.nsrc > 1 ? a.src[1].c : 0) : a.k;
+        const uint32_t sbase = smem_u32(smem);
+        for (int i = 0; i < nk; i++) {
+            const int s = i % STAGES;
+            const int k0 = (kb0 + i) * BK;
+            if (i >= STAGES) mbar_wait(empty + s, ((i / STAGES) & 1) ^ 1);
+            const uint32_t sa = sbase + s * Smem<BN>::STAGE;
+            const uint32_t sb = sa + Smem<BN>::A_BYTES;
+            {   // A: thread tid owns row tid (8 chunks of 16 B)
+                const int r = tid;
+                const char* src = a_block_ptr(a, abase, f0, c0p, f1, c1p, m0 + r, k0, cin);
+#pragma unroll
+                for (int j = 0; j < 8; j++) {
+                    const bool ok = src != nullptr && (a.a_mode == FIS_A_CONV3X3 || k0 + j * 8 < a.k);
+                    cp_async16(sa + sw128_off(r, j), ok ? (const void*)(src + j * 16) : (const void*)bbase, ok);
+                }
+            }
+#pragma unroll
+            for (int rr = 0; rr < BN; rr += PRODUCERS) {  // B: weight rows
+                const int r = rr + tid;
+                if (r < BN) {
+                    const int n = n0 + r;
+                    const char* src = bbase + ((long long)n * a.b.ld + k0) * 2;
+#pragma unroll
+                    for (int j = 0; j < 8; j++) {
+                        const bool ok = n < a.n && k0 + j * 8 < a.k;
+                        cp_async16(sb + sw128_off(r, j), ok ? (const void*)(src + j * 16) : (const void*)bbase, ok);
+                    }
+                }
+            }
+            cp_commit();
+            if (i >= STAGES - 1) {
+                cp_wait<STAGES - 1>();
+                fence_async_smem();
+                mbar_arrive(full + (i - (STAGES - 1)) % STAGES);
+            }
+        }
+        // drain
+        cp_wait<0>();
+        fence_async_smem();
+        for (int i = max(0, nk - (STAGES - 1)); i < nk; i++) mbar_arrive(full + i % STAGES);
+    } else {
+        // ------------------------------------------------------------ MMA issuer
+        const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
+                               ((uint32_t)(BM >> 4) << 24);
+        const uint32_t sbase = smem_u32(smem);
+        for (int i = 0; i < nk; i++) {
+            const int s = i % STAGES;
+            mbar_wait(full + s, (i / STAGES) & 1);
+            tc_fence_after();
+            if (lane == 0) {
+                const uint32_t sa = sbase + s * Smem<BN>::STAGE;
+                const uint32_t sb = sa + Smem<BN>::A_BYTES;
+#pragma unroll
+                for (int kk = 0; kk < BK / 16; kk++) {
+                    const uint64_t ad = sw128_desc(sa + kk * 32), bd = sw128_desc(sb + kk * 32);
+                    const uint32_t acc = (i > 0 || kk > 0) ? 1u : 0u;
+                    asm volatile(
+                        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+                        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem),
+                        "l"(ad), "l"(bd), "r"(idesc), "r"(acc));
+                }
+                asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                                 smem_u32(empty + s))
+                             : "memory");
+            }
+            __syncwarp();
+        }
+        if (lane == 0) {
+            if (nk > 0)
+                asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                                 smem_u32(done))
+                             : "memory");
+            else
+                mbar_arrive(done);
+        }
+        __syncwarp();
+    }
+
+    // ---------------------------------------------------------------- epilogue (warps 0-3)
+    if (warp < 4) {
+        mbar_wait(done, 0);
+        tc_fence_after();
+        const int r = m0 + warp * 32 + lane;
+        const EpiCtx e = make_epi(a, t);
+        float* wsz = a.splits > 1 ? a.ws + (long long)blockIdx.z * a.m * a.n : nullptr;
+#pragma unroll 1
+        for (int cb = 0; cb < BN; cb += 32) {
+            uint32_t v[32];
+            const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + cb;
+            asm volatile(
+                "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+                "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+                : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+                  "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
+                  "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]),
+                  "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]),
+                  "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+                : "r"(taddr));
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            if (r < a.m) {
+#pragma unroll
+                for (int j = 0; j < 32; j++) {
+                    const int n = n0 + cb + j;
+                    if (n < a.n) {
+                        const float acc = nk > 0 ? __uint_as_float(v[j]) : 0.f;
+                        if (wsz) __stcg(wsz + (long long)r * a.n + n, acc);
+                        else epilogue_store(a, e, r, n, acc);
+                    }
+                }
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 4)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(BN < 32 ? 32 : BN));
+
+    if (a.splits > 1) {
+        __threadfence();
+        __syncthreads();
+        const int tile = blockIdx.y * gridDim.x + blockIdx.x;
+        if (tid == 0) *last_flag = (atomicAdd(a.counters + tile, 1) == a.splits - 1);
+        __syncthreads();
+        if (!*last_flag) return;
+        __threadfence();
+        const EpiCtx e = make_epi(a, t);
+        const int rows = min(BM, a.m - m0), cols = min(BN, a.n - n0);
+        for (int idx = tid; idx < rows * cols; idx += THREADS) {
+            const int r = m0 + idx / cols, n = n0 + idx % cols;
+            float s = 0.f;
+            for (int z = 0; z < a.splits; z++) s += __ldcg(a.ws + ((long long)z * a.m + r) * a.n + n);
+            epilogue_store(a, e, r, n, s);
+        }
+        if (tid == 0) a.counters[tile] = 0;
+    }
+}
+
+template <int BN>
+int launch(const fis_gemm_args* a, cudaStream_t stream) {
+    const int smem = Smem<BN>::TOTAL;
+    static bool configured = false;
+    if (!configured) {
+        if (cudaFuncSetAttribute(gemm_tc_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
+            return FIS_ERR_UNSUPPORTED;
+        configured = true;
+    }
+    dim3 grid((a->n + BN - 1) / BN, (a->m + BM - 1) / BM, a->splits > 1 ? a->splits : 1);
+    gemm_tc_kernel<BN><<<grid, THREADS, smem, stream>>>(*a);
+    return cudaGetLastError() == cudaSuccess ? FIS_OK : FIS_ERR_LAUNCH;
+}
+
+}  // namespace tc
+}  // namespace fis
+
+// TC path requirements: bf16 A sources and B; 16-byte aligned rows; CONV segments
+// whose channel counts are multiples of 64 (a 64-wide K block never straddles a tap
+// or a concat boundary); ROWS mode any K (zero-filled tail).
+int fis_gemm_tc_supported(const fis_gemm_args* a) {
+    if (a->b.dtype != FIS_BF16 || (a->b.ld % 8)) return 0;
+    if (a->a_mode == FIS_A_ROWS) {
+        if (a->a.dtype != FIS_BF16 || (a->a.ld % 8)) return 0;
+        return 1;
+    }
+    for (int i = 0; i < a->nsrc; i++) {
+        const fis_src& s = a->src[i];
+        if (s.c % 64) return 0;
+        if (s.fresh.dtype != FIS_BF16 || (s.fresh.ld % 8)) return 0;
+        if (s.index && (s.cache.dtype != FIS_BF16 || (s.cache.ld % 8))) return 0;
+    }
+    return 1;
+}
+
+int fis_gemm_tc_launch(const fis_gemm_args* a, cudaStream_t stream) {
+    if (!fis_gemm_tc_supported(a)) return FIS_ERR_UNSUPPORTED;
+    if (a->n <= 64) return fis::tc::launch<64>(a, stream);
+    if (a->n <= 128 || (a->n % 128) != 0) return fis::tc::launch<128>(a, stream);
+    return fis::tc::launch<128>(a, stream);
+}

@@ -101,37 +101,25 @@ def _pad(n, m=16):
     return (n + m - 1) // m * m
 
 
-class Engine:
-    """One model (config + precision) resident on one GPU."""
+class Launcher:
+    """Kernel launch helpers (GEMM / softmax / GN / pool / materialise) independent of a model."""
 
-    def __init__(self, config: UNetConfig, precision: str = "fp32", device=None):
+    def __init__(self, precision: str = "fp32", device=None):
         L.require_cuda()
         if precision not in ("fp32", "bf16"):
             raise ContractViolation(f"precision must be 'fp32' or 'bf16', got {precision!r}")
-        self.config = config
         self.precision = precision
         self.dev = torch.device(device or "cuda")
         self.act = torch.float32 if precision == "fp32" else torch.bfloat16
         self.gemm_impl = 1 if precision == "fp32" else 0
-        self.layers, self.topo = build_registry(config)
-        self.info = {hl.info.layer_id: hl.info for hl in self.layers}
-        self.prog, self.feats = step_program(config, self.topo)
-        self.W = Weights(self.layers, self.topo, config, self.act, self.dev)
         self.step_dev = torch.zeros(1, dtype=torch.int32, device=self.dev)
         self.sms = L.lib().fis_device_sm_count()
         self._ws = torch.zeros(1, dtype=torch.float32, device=self.dev)
         self._counters = torch.zeros(1 << 16, dtype=torch.int32, device=self.dev)
-        self.gated = [config.latent_h * config.latent_w >> (2 * l) >= config.gate_fraction * config.latent_h * config.latent_w
-                      for l in range(config.levels)]
         self.launches = 0
         self._scratch = {}
-
-    # ------------------------------------------------------------------ helpers
-    def hw(self, level):
-        return (self.config.latent_h >> level) * (self.config.latent_w >> level)
-
-    def grid(self, level):
-        return self.config.latent_h >> level, self.config.latent_w >> level
+        self.groups = 1
+        self.step_scale_value = 1.0
 
     def scratch(self, name, shape, dtype=None, zero=False):
         key = (name, tuple(shape), dtype or self.act)
@@ -140,6 +128,7 @@ class Engine:
             t = (torch.zeros if zero else torch.empty)(shape, dtype=dtype or self.act, device=self.dev)
             self._scratch[key] = t
         return t
+
 
     def _ensure_ws(self, floats):
         if self._ws.numel() < floats:
@@ -152,13 +141,6 @@ class Engine:
             return 1
         s = min(max(1, (2 * self.sms) // tiles), ktiles // 16, 32)
         return max(1, s)
-
-    def src(self, fv: FeatVal, up=False):
-        h, w = self.grid(fv.level)
-        if fv.index is not None and fv.cache is None:
-            raise CacheMissError("?", "?", "feature cache")
-        return L.Src(fv.fresh.ref(), _r(fv.cache) if fv.index is not None else NULL,
-                     L.ptr(fv.index) if fv.index is not None else None, h, w, fv.c, 1 if up else 0)
 
     def gemm(self, m, n, k, *, a=None, rows=None, srcs=None, out_hw=None, b: DRef, d: DRef, alpha=1.0, bias=None,
              bias2=None, pre=None, epi=L.EPI_NONE, gn=None, lat=None, res=None, d_trans=False, splits=None):
@@ -187,7 +169,7 @@ class Engine:
             g.gn_mean, g.gn_var = mean.ref(), var.ref()
             g.gamma, g.beta, g.groups, g.eps = L.ptr(gamma), L.ptr(beta), groups, NORM_EPS
         g.lat = _r(lat)
-        g.step_scale = float(step_scale(self.config))
+        g.step_scale = self.step_scale_value
         g.res = _r(res)
         g.d = d.ref()
         g.d_trans = 1 if d_trans else 0
@@ -215,6 +197,35 @@ class Engine:
         a.step = L.ptr(self.step_dev)
         L.call("fis_softmax", a)
         self.launches += 1
+
+class Engine(Launcher):
+    """One model (config + precision) resident on one GPU."""
+
+    def __init__(self, config: UNetConfig, precision: str = "fp32", device=None):
+        super().__init__(precision, device)
+        self.config = config
+        self.groups = config.groups
+        self.step_scale_value = float(step_scale(config))
+        self.layers, self.topo = build_registry(config)
+        self.info = {hl.info.layer_id: hl.info for hl in self.layers}
+        self.prog, self.feats = step_program(config, self.topo)
+        self.W = Weights(self.layers, self.topo, config, self.act, self.dev)
+        self.gated = [config.latent_h * config.latent_w >> (2 * l) >= config.gate_fraction * config.latent_h * config.latent_w
+                      for l in range(config.levels)]
+
+    # ------------------------------------------------------------------ helpers
+    def hw(self, level):
+        return (self.config.latent_h >> level) * (self.config.latent_w >> level)
+
+    def grid(self, level):
+        return self.config.latent_h >> level, self.config.latent_w >> level
+
+    def src(self, fv: FeatVal, up=False):
+        h, w = self.grid(fv.level)
+        if fv.index is not None and fv.cache is None:
+            raise CacheMissError("?", "?", "feature cache")
+        return L.Src(fv.fresh.ref(), _r(fv.cache) if fv.index is not None else NULL,
+                     L.ptr(fv.index) if fv.index is not None else None, h, w, fv.c, 1 if up else 0)
 
     # ------------------------------------------------------------ text K/V
     def text_kv(self, text_emb: np.ndarray):
@@ -269,14 +280,14 @@ class Engine:
         self.gemm(m, c, ntp, a=DRef(P), b=DRef(vt), d=out, res=x, pre=pre)
 
     def gn_stats(self, x: DRef, hw, c, mean: DRef, var: DRef):
-        a = L.GnStatsArgs(hw, c, self.config.groups, x.ref(), mean.ref(), var.ref(), L.ptr(self.step_dev))
+        a = L.GnStatsArgs(hw, c, self.groups, x.ref(), mean.ref(), var.ref(), L.ptr(self.step_dev))
         L.call("fis_gn_stats", a)
         self.launches += 1
 
     def gn_apply(self, lid, x: DRef, rows, c, mean: DRef, var: DRef, y_norm: DRef | None, y_silu: DRef | None):
         gamma, beta = self.W.norm[lid]
         a = L.GnApplyArgs()
-        a.rows, a.c, a.groups, a.eps = rows, c, self.config.groups, NORM_EPS
+        a.rows, a.c, a.groups, a.eps = rows, c, self.groups, NORM_EPS
         a.x, a.mean, a.var = x.ref(), mean.ref(), var.ref()
         a.gamma, a.beta = L.ptr(gamma), L.ptr(beta)
         a.y_norm, a.y_silu = _r(y_norm), _r(y_silu)

@@ -382,7 +382,7 @@ def edit(session: EditSession, config: UNetConfig, store: CacheStore) -> EditRes
     if outcome.from_user_mask:
         lat0 = _to_nhwc(initial_latent_np(config), eng.dev)
     else:
-        m = torch.from_numpy(mask.bits.ravel()).to(eng.dev)[:, None]
+        m = torch.from_numpy(mask.bits.ravel().copy()).to(eng.dev)[:, None]
         lat0 = torch.where(m, outcome._control_dev, arena.latent[session.t2])
     plans = {}
     if mask.all_active():

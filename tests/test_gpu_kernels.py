@@ -1,0 +1,125 @@
+"""Kernel-level GPU tests: the tcgen05 bf16 gather-GEMM against the SIMT fp32 kernel and a
+plain torch fp32 reference, over the gather modes and fused epilogues the engine uses.
+
+Tolerance: both paths consume the same bf16 operands and accumulate in fp32, so they differ
+only by summation order: max-abs <= 2e-3 * sqrt(K/64) relative to the output scale.
+"""
+
+import math
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import has_gpu
+
+pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not has_gpu(), reason="needs a CUDA GPU")]
+
+
+@pytest.fixture(scope="module")
+def env():
+    from paper_2305_17423_b200 import _lib as L
+    from paper_2305_17423_b200.engine import NULL, DRef, Launcher
+    return L, DRef, NULL, Launcher("bf16")
+
+
+def _run(env, impl, m, n, k, **kw):
+    L, DRef, NULL, lz = env
+    lz.gemm_impl = impl
+    lz.gemm(m, n, k, **kw)
+    torch.cuda.synchronize()
+
+
+def _tol(ref, k):
+    return 3e-3 * max(1.0, ref.abs().max().item()) * math.sqrt(max(k, 64) / 64)
+
+
+@pytest.mark.parametrize("m,n,k,ld", [(200, 320, 320, 320), (400, 77, 320, 320), (37, 640, 401, 416),
+                                      (256, 1280, 2880, 2880), (1024, 256, 640, 640)])
+@pytest.mark.parametrize("splits", [1, 3])
+def test_rows_gemm_tc_vs_simt(env, m, n, k, ld, splits):
+    L, DRef, NULL, lz = env
+    g = torch.Generator(device="cuda").manual_seed(m * 7 + n)
+    A = torch.zeros((m, ld), device="cuda", dtype=torch.bfloat16)
+    A[:, :k] = torch.randn((m, k), device="cuda", generator=g).to(torch.bfloat16)
+    B = torch.randn((n, ld), device="cuda", generator=g).to(torch.bfloat16) / math.sqrt(k)
+    bias = torch.randn(n, device="cuda", generator=g)
+    ref = A[:, :k].float() @ B[:, :k].float().t() + bias
+    outs = []
+    for impl in (1, 2):
+        D = torch.full((m, n), float("nan"), device="cuda")
+        _run(env, impl, m, n, k, a=DRef(A), b=DRef(B), d=DRef(D), bias=bias, splits=splits)
+        outs.append(D)
+    assert (outs[1] - ref).abs().max().item() <= _tol(ref, k)
+    assert (outs[0] - ref).abs().max().item() <= _tol(ref, k)
+
+
+def test_conv_gather_select_upsample_tc_vs_simt(env):
+    """Implicit 3x3 conv over concat(upsample(coarse compact+cache), fine compact+cache) with
+    select-on-read, GN+SiLU epilogue, as the sparse fuse/block convs use it."""
+    L, DRef, NULL, lz = env
+    g = torch.Generator(device="cuda").manual_seed(3)
+    H = W = 32
+    c_up, c_sk, n = 128, 64, 192
+    bf = torch.bfloat16
+    mask = torch.zeros(H * W, dtype=torch.bool, device="cuda")
+    mask.view(H, W)[9:20, 5:17] = True
+    mask.view(H, W)[25, 30] = True
+    rows = torch.nonzero(mask).flatten().int()
+    idx = torch.full((H * W,), -1, dtype=torch.int32, device="cuda")
+    idx[rows.long()] = torch.arange(rows.numel(), dtype=torch.int32, device="cuda")
+    cm = mask.view(H // 2, 2, W // 2, 2).any(3).any(1).flatten()
+    crow = torch.nonzero(cm).flatten().int()
+    cidx = torch.full(((H // 2) * (W // 2),), -1, dtype=torch.int32, device="cuda")
+    cidx[crow.long()] = torch.arange(crow.numel(), dtype=torch.int32, device="cuda")
+    sk_cache = torch.randn((H * W, c_sk), device="cuda", generator=g).to(bf)
+    sk_fresh = torch.randn((rows.numel(), c_sk), device="cuda", generator=g).to(bf)
+    up_cache = torch.randn(((H // 2) * (W // 2), c_up), device="cuda", generator=g).to(bf)
+    up_fresh = torch.randn((crow.numel(), c_up), device="cuda", generator=g).to(bf)
+    Wt = (torch.randn((n, 9 * (c_up + c_sk)), device="cuda", generator=g) / 40).to(bf)
+    bias = torch.randn(n, device="cuda", generator=g) * 0.1
+    groups = 8
+    mean = torch.randn((1, groups), device="cuda", generator=g) * 0.1
+    var = torch.rand((1, groups), device="cuda", generator=g) + 0.5
+    gamma = torch.randn(n, device="cuda", generator=g)
+    beta = torch.randn(n, device="cuda", generator=g)
+    # torch reference: materialise the full input map and run conv
+    skf = sk_cache.float().clone()
+    skf[rows.long()] = sk_fresh.float()
+    upf = up_cache.float().clone()
+    upf[crow.long()] = up_fresh.float()
+    upm = upf.view(H // 2, W // 2, c_up).repeat_interleave(2, 0).repeat_interleave(2, 1)
+    full = torch.cat([upm, skf.view(H, W, c_sk)], dim=2).permute(2, 0, 1)[None]
+    wconv = Wt.float().view(n, 3, 3, c_up + c_sk).permute(0, 3, 1, 2)
+    conv = torch.nn.functional.conv2d(full, wconv, bias, padding=1)[0].permute(1, 2, 0).reshape(H * W, n)[rows.long()]
+    cg = conv.view(-1, groups, n // groups)
+    y = ((cg - mean[0][None, :, None]) / torch.sqrt(var[0][None, :, None] + 1e-5)).reshape(-1, n) * gamma + beta
+    ref = y * torch.sigmoid(y)
+    srcs = [L.Src(DRef(up_fresh).ref(), DRef(up_cache).ref(), L.ptr(cidx), H // 2, W // 2, c_up, 1),
+            L.Src(DRef(sk_fresh).ref(), DRef(sk_cache).ref(), L.ptr(idx), H, W, c_sk, 0)]
+    outs = []
+    for impl in (1, 2):
+        D = torch.full((rows.numel(), n), float("nan"), device="cuda")
+        _run(env, impl, rows.numel(), n, 9 * (c_up + c_sk), rows=rows, srcs=srcs, out_hw=(H, W), b=DRef(Wt),
+             d=DRef(D), bias=bias, epi=L.EPI_GN_SILU, gn=(DRef(mean), DRef(var), gamma, beta, groups), splits=2)
+        outs.append(D)
+    for o in outs:
+        assert (o - ref).abs().max().item() <= 2e-2, (o - ref).abs().max().item()
+    assert (outs[0] - outs[1]).abs().max().item() <= 2e-3
+
+
+def test_transposed_store_and_residual(env):
+    L, DRef, NULL, lz = env
+    g = torch.Generator(device="cuda").manual_seed(9)
+    m, n, k = 300, 320, 320
+    A = torch.randn((m, k), device="cuda", generator=g).to(torch.bfloat16)
+    B = (torch.randn((n, k), device="cuda", generator=g) / 18).to(torch.bfloat16)
+    res = torch.randn((m, n), device="cuda", generator=g).to(torch.bfloat16)
+    ref = A.float() @ B.float().t()
+    for impl in (1, 2):
+        Dt = torch.zeros((n, 304), device="cuda", dtype=torch.bfloat16)
+        _run(env, impl, m, n, k, a=DRef(A), b=DRef(B), d=DRef(Dt), d_trans=True)
+        assert (Dt[:, :m].float().t() - ref).abs().max().item() <= 3e-2
+        D = torch.zeros((m, n), device="cuda")
+        _run(env, impl, m, n, k, a=DRef(A), b=DRef(B), d=DRef(D), res=DRef(res))
+        assert (D - (ref + res.float())).abs().max().item() <= 3e-2
