@@ -201,11 +201,13 @@ def run_ours(args):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with Clocks(local) as clk:
         torch.cuda.synchronize()
+        torch.cuda.profiler.start()  # ncu --profile-from-start off captures only the timed steps
         e0.record(st)
         for i in range(args.steps):
             runner.step(1 + i % T)
         e1.record(st)
         torch.cuda.synchronize()
+        torch.cuda.profiler.stop()
     ms = e0.elapsed_time(e1)
     barrier()
     ms = reduce_max(ms)
