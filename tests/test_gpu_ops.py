@@ -134,7 +134,7 @@ def test_gather_blocks(P):
     b = D.gather_blocks(x, plan)
     (oy, ox), (bh, bw) = plan.origins[0], plan.block
     assert np.array_equal(b[0], x[0, :, oy - 1:oy - 1 + bh, ox - 1:ox - 1 + bw])
-    bits[:] = False
+    bits = np.zeros((16, 16), bool)
     bits[0, 0] = True
     b = D.gather_blocks(x, P.select_gather_plan(P.BinaryMask(bits), (3, 3)))
     assert (b[0, :, 0, :] == 0).all() and (b[0, :, :, 0] == 0).all()
