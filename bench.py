@@ -191,8 +191,8 @@ def run_ours(args):
     runner = U._Runner(eng, ep.plan, True)
     T = cfg.steps
     n0 = eng.launches
-    runner.step(1)  # warm + capture
-    per_step_launches = eng.launches - n0
+    runner.step(1)  # eager warm step + graph capture of one step
+    per_step_launches = (eng.launches - n0) // 2  # kernels in the captured step graph
     for i in range(args.warmup):
         runner.step(1 + (i + 1) % T)
     torch.cuda.synchronize()
