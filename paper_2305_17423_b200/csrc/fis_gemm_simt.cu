@@ -106,7 +106,7 @@ __global__ void __launch_bounds__(STHREADS) gemm_simt_kernel(const fis_gemm_args
 
     const EpiCtx e = make_epi(a, t);
     if (a.splits <= 1) {
-#pragma unroll
+#pragma unroll 1
         for (int i = 0; i < 4; i++) {
             const int r = m0 + ty * 4 + i;
             if (r >= a.m) continue;
@@ -140,11 +140,11 @@ __global__ void __launch_bounds__(STHREADS) gemm_simt_kernel(const fis_gemm_args
     __syncthreads();
     if (!s_last) return;
     __threadfence();
-#pragma unroll
+#pragma unroll 1
     for (int i = 0; i < 4; i++) {
         const int r = m0 + ty * 4 + i;
         if (r >= a.m) continue;
-#pragma unroll
+#pragma unroll 1
         for (int j = 0; j < 4; j++) {
             const int n = n0 + tx * 4 + j;
             if (n >= a.n) continue;

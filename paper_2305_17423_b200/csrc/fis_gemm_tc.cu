@@ -69,8 +69,132 @@ struct Smem {
     static constexpr int A_BYTES = BM * BK * 2;
     static constexpr int B_BYTES = BN * BK * 2;
     static constexpr int STAGE = A_BYTES + B_BYTES;
-    static constexpr int TOTAL = STAGES * STAGE + 1024 /*align*/ + 256 /*barriers*/;
+    static constexpr int EPI = BN * 32;  // per-column epilogue tables
+    static constexpr int TOTAL = STAGES * STAGE + 1024 /*align*/ + 256 /*barriers*/ + EPI;
 };
+
+// Per-column epilogue parameters of this CTA's BN columns, staged once in shared memory.
+struct EpiTab {
+    float* bias; float* b2; float* gamma; float* beta; double* mean; double* rstd;
+};
+
+__device__ __forceinline__ void load_row32(const char* base, int dtype, long long off, int nvalid, float* v) {
+    if (dtype == FIS_BF16) {
+        const __nv_bfloat16* p = (const __nv_bfloat16*)base + off;
+        if (nvalid == 32 && ((uintptr_t)p & 15) == 0) {
+#pragma unroll
+            for (int q = 0; q < 4; q++) {
+                uint4 u = *(const uint4*)(p + 8 * q);
+                const __nv_bfloat162* h = (const __nv_bfloat162*)&u;
+#pragma unroll
+                for (int k = 0; k < 4; k++) {
+                    float2 f = __bfloat1622float2(h[k]);
+                    v[8 * q + 2 * k] = f.x;
+                    v[8 * q + 2 * k + 1] = f.y;
+                }
+            }
+        } else {
+#pragma unroll
+            for (int j = 0; j < 32; j++) if (j < nvalid) v[j] = __bfloat162float(p[j]);
+        }
+    } else {
+        const float* p = (const float*)base + off;
+        if (nvalid == 32 && ((uintptr_t)p & 15) == 0) {
+#pragma unroll
+            for (int q = 0; q < 8; q++) {
+                float4 f = *(const float4*)(p + 4 * q);
+                v[4 * q] = f.x; v[4 * q + 1] = f.y; v[4 * q + 2] = f.z; v[4 * q + 3] = f.w;
+            }
+        } else {
+#pragma unroll
+            for (int j = 0; j < 32; j++) if (j < nvalid) v[j] = p[j];
+        }
+    }
+}
+
+__device__ __forceinline__ void store_row32(char* base, int dtype, long long off, int nvalid, const float* v) {
+    if (dtype == FIS_BF16) {
+        __nv_bfloat16* p = (__nv_bfloat16*)base + off;
+        if (nvalid == 32 && ((uintptr_t)p & 15) == 0) {
+#pragma unroll
+            for (int q = 0; q < 4; q++) {
+                uint4 u;
+                __nv_bfloat162* h = (__nv_bfloat162*)&u;
+#pragma unroll
+                for (int k = 0; k < 4; k++) h[k] = __floats2bfloat162_rn(v[8 * q + 2 * k], v[8 * q + 2 * k + 1]);
+                *(uint4*)(p + 8 * q) = u;
+            }
+        } else {
+#pragma unroll
+            for (int j = 0; j < 32; j++) if (j < nvalid) p[j] = __float2bfloat16_rn(v[j]);
+        }
+    } else {
+        float* p = (float*)base + off;
+        if (nvalid == 32 && ((uintptr_t)p & 15) == 0) {
+#pragma unroll
+            for (int q = 0; q < 8; q++) *(float4*)(p + 4 * q) = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+        } else {
+#pragma unroll
+            for (int j = 0; j < 32; j++) if (j < nvalid) p[j] = v[j];
+        }
+    }
+}
+
+// Fused epilogue of one 32-column chunk of one output row (v holds the fp32 accumulators).
+// Same arithmetic, in the same order, as fis::epilogue_store (fis_common.cuh).
+template <int MODE>
+__device__ __forceinline__ void row_epilogue(const fis_gemm_args& a, const EpiCtx& e, const EpiTab& tb, int r,
+                                             int c0, int n0, float* v) {
+    const int n = n0 + c0;
+    const int nvalid = min(32, a.n - n);
+    if (nvalid <= 0) return;
+    const int orow = a.d_rows ? __ldg(a.d_rows + r) : r;
+#pragma unroll
+    for (int j = 0; j < 32; j++) v[j] = __fadd_rn(v[j] * a.alpha, tb.bias[c0 + j]);
+    if (e.pre) store_row32(e.pre, a.pre.dtype, (long long)orow * a.pre.ld + n, nvalid, v);
+    if (e.bias2) {
+#pragma unroll
+        for (int j = 0; j < 32; j++) v[j] = __fadd_rn(v[j], tb.b2[c0 + j]);
+    }
+    if (MODE == FIS_EPI_GN_SILU) {
+        float y[32];
+#pragma unroll
+        for (int j = 0; j < 32; j++)
+            y[j] = (float)(((double)v[j] - tb.mean[c0 + j]) * tb.rstd[c0 + j] * (double)tb.gamma[c0 + j] +
+                           (double)tb.beta[c0 + j]);
+        if (e.pre2) store_row32(e.pre2, a.pre2.dtype, (long long)orow * a.pre2.ld + n, nvalid, y);
+#pragma unroll
+        for (int j = 0; j < 32; j++) {
+            const double yd = (double)y[j];
+            v[j] = (float)(yd / (1.0 + exp(-yd)));
+        }
+    } else if (MODE == FIS_EPI_STEP) {
+        float l[32];
+        load_row32(e.lat, a.lat.dtype, (long long)orow * a.lat.ld + n, nvalid, l);
+#pragma unroll
+        for (int j = 0; j < 32; j++) v[j] = __fsub_rn(l[j], __fmul_rn(a.step_scale, v[j]));
+    }
+    if (e.res) {
+        float q[32];
+        load_row32(e.res, a.res.dtype, (long long)orow * a.res.ld + n, nvalid, q);
+#pragma unroll
+        for (int j = 0; j < 32; j++) v[j] = __fadd_rn(v[j], q[j]);
+    }
+    if (a.d_trans) {
+#pragma unroll
+        for (int j = 0; j < 32; j++)
+            if (j < nvalid) store_elem(e.d, a.d.dtype, (long long)(n + j) * a.d.ld + orow, v[j]);
+    } else {
+        store_row32(e.d, a.d.dtype, (long long)orow * a.d.ld + n, nvalid, v);
+    }
+}
+
+__device__ __forceinline__ void row_epilogue_any(const fis_gemm_args& a, const EpiCtx& e, const EpiTab& tb, int r,
+                                                 int c0, int n0, float* v) {
+    if (a.epi == FIS_EPI_GN_SILU) row_epilogue<FIS_EPI_GN_SILU>(a, e, tb, r, c0, n0, v);
+    else if (a.epi == FIS_EPI_STEP) row_epilogue<FIS_EPI_STEP>(a, e, tb, r, c0, n0, v);
+    else row_epilogue<FIS_EPI_NONE>(a, e, tb, r, c0, n0, v);
+}
 
 // Source pointer of the 64-channel K block starting at k0 for GEMM row r (16B granularity),
 // or nullptr for zero (padding / out of image / beyond K).
@@ -111,7 +235,7 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_tc_kernel(const fis_gemm_args
     uint64_t* empty = full + STAGES;
     uint64_t* done = empty + STAGES;
     uint32_t* tmem_slot = (uint32_t*)(done + 1);
-    int* last_flag = (int*)(tmem_slot + 1);
+    int* last_flag = (int*)(tmem_slot + 1);  // followed by the epilogue tables
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int t = cur_step(a.step);
@@ -227,35 +351,71 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_tc_kernel(const fis_gemm_args
     }
 
     // ---------------------------------------------------------------- epilogue (warps 0-3)
+    EpiTab tb;
+    {
+        unsigned char* ep = (unsigned char*)(last_flag + 4);
+        ep = (unsigned char*)(((uintptr_t)ep + 15) & ~(uintptr_t)15);
+        tb.mean = (double*)ep;
+        tb.rstd = tb.mean + BN;
+        tb.bias = (float*)(tb.rstd + BN);
+        tb.b2 = tb.bias + BN;
+        tb.gamma = tb.b2 + BN;
+        tb.beta = tb.gamma + BN;
+    }
+    const EpiCtx e = make_epi(a, t);
     if (warp < 4) {
+        // stage per-column parameters while the MMAs drain
+        for (int c = tid; c < BN; c += PRODUCERS) {
+            const int n = n0 + c;
+            const bool ok = n < a.n;
+            tb.bias[c] = ok && a.bias ? __ldg(a.bias + n) : 0.f;
+            tb.b2[c] = ok && e.bias2 ? load_elem(e.bias2, a.bias2.dtype, n) : 0.f;
+            if (a.epi == FIS_EPI_GN_SILU && ok) {
+                const int g = n / e.cpg;
+                tb.mean[c] = (double)e.mean[g];
+                tb.rstd[c] = 1.0 / sqrt((double)e.var[g] + (double)a.eps);
+                tb.gamma[c] = __ldg(a.gamma + n);
+                tb.beta[c] = __ldg(a.beta + n);
+            } else {
+                tb.mean[c] = 0.0; tb.rstd[c] = 0.0; tb.gamma[c] = 0.f; tb.beta[c] = 0.f;
+            }
+        }
+        asm volatile("bar.sync 1, 128;" ::: "memory");
         mbar_wait(done, 0);
         tc_fence_after();
         const int r = m0 + warp * 32 + lane;
-        const EpiCtx e = make_epi(a, t);
         float* wsz = a.splits > 1 ? a.ws + (long long)blockIdx.z * a.m * a.n : nullptr;
 #pragma unroll 1
         for (int cb = 0; cb < BN; cb += 32) {
-            uint32_t v[32];
+            uint32_t u[32];
             const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + cb;
             asm volatile(
                 "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
                 "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-                : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-                  "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
-                  "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]),
-                  "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]),
-                  "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+                : "=r"(u[0]), "=r"(u[1]), "=r"(u[2]), "=r"(u[3]), "=r"(u[4]), "=r"(u[5]), "=r"(u[6]), "=r"(u[7]),
+                  "=r"(u[8]), "=r"(u[9]), "=r"(u[10]), "=r"(u[11]), "=r"(u[12]), "=r"(u[13]), "=r"(u[14]),
+                  "=r"(u[15]), "=r"(u[16]), "=r"(u[17]), "=r"(u[18]), "=r"(u[19]), "=r"(u[20]), "=r"(u[21]),
+                  "=r"(u[22]), "=r"(u[23]), "=r"(u[24]), "=r"(u[25]), "=r"(u[26]), "=r"(u[27]), "=r"(u[28]),
+                  "=r"(u[29]), "=r"(u[30]), "=r"(u[31])
                 : "r"(taddr));
             asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-            if (r < a.m) {
+            if (r < a.m && n0 + cb < a.n) {
+                float v[32];
 #pragma unroll
-                for (int j = 0; j < 32; j++) {
-                    const int n = n0 + cb + j;
-                    if (n < a.n) {
-                        const float acc = nk > 0 ? __uint_as_float(v[j]) : 0.f;
-                        if (wsz) __stcg(wsz + (long long)r * a.n + n, acc);
-                        else epilogue_store(a, e, r, n, acc);
+                for (int j = 0; j < 32; j++) v[j] = nk > 0 ? __uint_as_float(u[j]) : 0.f;
+                if (wsz) {
+                    const int nvalid = min(32, a.n - (n0 + cb));
+                    float* p = wsz + (long long)r * a.n + n0 + cb;
+                    if (nvalid == 32 && ((uintptr_t)p & 15) == 0) {
+#pragma unroll
+                        for (int q = 0; q < 8; q++)
+                            __stcg((float4*)(p + 4 * q), make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]));
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < 32; j++) if (j < nvalid) __stcg(p + j, v[j]);
                     }
+                } else {
+                    row_epilogue_any(a, e, tb, r, cb, n0, v);
                 }
             }
         }
@@ -273,13 +433,33 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_tc_kernel(const fis_gemm_args
         __syncthreads();
         if (!*last_flag) return;
         __threadfence();
-        const EpiCtx e = make_epi(a, t);
-        const int rows = min(BM, a.m - m0), cols = min(BN, a.n - n0);
-        for (int idx = tid; idx < rows * cols; idx += THREADS) {
-            const int r = m0 + idx / cols, n = n0 + idx % cols;
-            float s = 0.f;
-            for (int z = 0; z < a.splits; z++) s += __ldcg(a.ws + ((long long)z * a.m + r) * a.n + n);
-            epilogue_store(a, e, r, n, s);
+        if (warp < 4) {
+            // ordered reduction of the split partials: thread = output row, 32-column chunks
+            const int r = m0 + warp * 32 + lane;
+            if (r < a.m) {
+#pragma unroll 1
+                for (int cb = 0; cb < BN && n0 + cb < a.n; cb += 32) {
+                    const int nvalid = min(32, a.n - (n0 + cb));
+                    float v[32];
+#pragma unroll
+                    for (int j = 0; j < 32; j++) v[j] = 0.f;
+#pragma unroll 1
+                    for (int z = 0; z < a.splits; z++) {
+                        const float* p = a.ws + ((long long)z * a.m + r) * a.n + n0 + cb;
+                        if (nvalid == 32 && ((uintptr_t)p & 15) == 0) {
+#pragma unroll
+                            for (int q = 0; q < 8; q++) {
+                                const float4 f = __ldcg((const float4*)(p + 4 * q));
+                                v[4 * q] += f.x; v[4 * q + 1] += f.y; v[4 * q + 2] += f.z; v[4 * q + 3] += f.w;
+                            }
+                        } else {
+#pragma unroll
+                            for (int j = 0; j < 32; j++) if (j < nvalid) v[j] += __ldcg(p + j);
+                        }
+                    }
+                    row_epilogue_any(a, e, tb, r, cb, n0, v);
+                }
+            }
         }
         if (tid == 0) a.counters[tile] = 0;
     }
