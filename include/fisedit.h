@@ -91,10 +91,14 @@ typedef struct {
     fis_ref res;            /* v += res[r, n] (residual) */
     fis_ref d;              /* output */
     int d_trans;            /* 1: store D[n*ld + r] */
+    int n_split;            /* >0: columns n >= n_split go to d2 at column n - n_split (fused QKV) */
+    fis_ref d2;
+    int d2_trans;
     const int* d_rows;      /* optional row remap for the output (and res/lat/pre): row = d_rows[r] */
     /* scheduling */
-    int splits;             /* split-K factor (>=1); deterministic ordered reduction */
+    int splits;             /* split-K factor; 0 = choose from the tile shape and SM count */
     float* ws;              /* splits*m*n floats when splits > 1 */
+    long long ws_floats;    /* capacity of ws (bounds the automatic split choice) */
     int* counters;          /* per-tile arrival counters (zeroed, self-resetting) */
     const int* step;
     int impl;               /* 0 auto, 1 SIMT fp32-accumulate, 2 tcgen05 bf16 */

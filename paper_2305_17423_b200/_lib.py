@@ -38,8 +38,8 @@ class GemmArgs(C.Structure):
                 ("src", Src * 2), ("b", Ref), ("alpha", C.c_float), ("bias", C.c_void_p), ("bias2", Ref),
                 ("pre", Ref), ("epi", C.c_int), ("gn_mean", Ref), ("gn_var", Ref), ("gamma", C.c_void_p),
                 ("beta", C.c_void_p), ("groups", C.c_int), ("eps", C.c_float), ("pre2", Ref), ("lat", Ref),
-                ("step_scale", C.c_float), ("res", Ref), ("d", Ref), ("d_trans", C.c_int),
-                ("d_rows", C.c_void_p), ("splits", C.c_int), ("ws", C.c_void_p), ("counters", C.c_void_p),
+                ("step_scale", C.c_float), ("res", Ref), ("d", Ref), ("d_trans", C.c_int), ("n_split", C.c_int), ("d2", Ref), ("d2_trans", C.c_int),
+                ("d_rows", C.c_void_p), ("splits", C.c_int), ("ws", C.c_void_p), ("ws_floats", C.c_longlong), ("counters", C.c_void_p),
                 ("step", C.c_void_p), ("impl", C.c_int)]
 
 

@@ -25,6 +25,42 @@ int fis_gemm_counters(int m, int n) {
     return ((m + 63) / 64) * ((n + 15) / 16);
 }
 
+static int sm_count_cached(void) {
+    static int n = 0;
+    if (n <= 0) n = fis_device_sm_count();
+    return n > 0 ? n : 148;
+}
+
+// Split-K so that the grid covers the SMs once (tcgen05: 1 CTA/SM, 128xBN tiles, 64-wide K
+// blocks; SIMT: 64x64 tiles, 16-wide K tiles), keeping >= 4 K blocks per split and
+// bounded by the workspace capacity.
+static int fis_choose_splits(const fis_gemm_args* a, bool tc) {
+    const int sms = sm_count_cached();
+    long long tiles, kb;
+    int minper, target;
+    if (tc) {
+        const int bn = a->n <= 64 ? 64 : 128;
+        tiles = (long long)((a->m + 127) / 128) * ((a->n + bn - 1) / bn);
+        kb = (a->k + 63) / 64;
+        minper = 4;
+        target = sms;
+    } else {
+        tiles = (long long)((a->m + 63) / 64) * ((a->n + 63) / 64);
+        kb = (a->k + 15) / 16;
+        minper = 16;
+        target = 2 * sms;
+    }
+    long long s = target / (tiles > 0 ? tiles : 1);
+    if (s > kb / minper) s = kb / minper;
+    if (s > 32) s = 32;
+    if (s < 2) return 1;
+    while (s > 1 && (long long)s * a->m * a->n > a->ws_floats) s--;
+    // no empty splits: round so every split gets ceil(kb/s) blocks
+    const long long per = (kb + s - 1) / s;
+    s = (kb + per - 1) / per;
+    return (int)(s < 1 ? 1 : s);
+}
+
 int fis_gemm(const fis_gemm_args* a, void* stream) {
     if (a->m < 0 || a->n <= 0 || a->k <= 0) return FIS_ERR_SHAPE;
     if (a->m == 0) return FIS_OK;
@@ -39,10 +75,11 @@ int fis_gemm(const fis_gemm_args* a, void* stream) {
     }
     if (a->epi == FIS_EPI_GN_SILU && (a->groups <= 0 || a->n % a->groups || !a->gn_mean.ptr || !a->gn_var.ptr))
         return a->gn_mean.ptr ? FIS_ERR_SHAPE : FIS_ERR_CACHE_MISS;
-    if (a->splits > 1 && (!a->ws || !a->counters)) return FIS_ERR_SHAPE;
-    if (a->impl == 2 || (a->impl == 0 && fis_gemm_tc_supported(a)))
-        return fis_gemm_tc_launch(a, (cudaStream_t)stream);
-    return fis_gemm_simt_launch(a, (cudaStream_t)stream);
+    const bool tc = a->impl == 2 || (a->impl == 0 && fis_gemm_tc_supported(a));
+    fis_gemm_args g = *a;
+    if (g.splits <= 0) g.splits = fis_choose_splits(&g, tc);
+    if (g.splits > 1 && (!g.ws || !g.counters)) return FIS_ERR_SHAPE;
+    return tc ? fis_gemm_tc_launch(&g, (cudaStream_t)stream) : fis_gemm_simt_launch(&g, (cudaStream_t)stream);
 }
 
 }  // extern "C"

@@ -9,6 +9,14 @@
 
 namespace fis {
 
+// Programmatic dependent launch: every kernel is launched with programmatic stream
+// serialization; it lets its own dependents launch immediately (they are only scheduled
+// once all of this grid's CTAs are resident) and waits for its predecessor's memory
+// before touching global data. Inside a captured CUDA graph this overlaps each kernel's
+// launch + prologue with the previous kernel's tail.
+FIS_DEV void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+FIS_DEV void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 FIS_DEV int cur_step(const int* step) { return step ? __ldg(step) : 0; }
 
 FIS_DEV char* ref_base(const fis_ref& r, int t) {
@@ -60,6 +68,7 @@ FIS_DEV float warp_max(float v) {
 // Epilogue shared by the SIMT and tcgen05 GEMMs. Applies bias / time-bias /
 // GN(cached stats)+SiLU / step update / residual and stores. r = GEMM row.
 struct EpiCtx {
+    char* d2;
     char* d; char* pre; char* pre2; char* res; char* lat; char* bias2;
     const float* mean; const float* var;
     int cpg;  // channels per group
@@ -68,6 +77,7 @@ struct EpiCtx {
 FIS_DEV EpiCtx make_epi(const fis_gemm_args& a, int t) {
     EpiCtx e;
     e.d = ref_base(a.d, t);
+    e.d2 = a.d2.ptr ? ref_base(a.d2, t) : nullptr;
     e.pre = a.pre.ptr ? ref_base(a.pre, t) : nullptr;
     e.pre2 = a.pre2.ptr ? ref_base(a.pre2, t) : nullptr;
     e.res = a.res.ptr ? ref_base(a.res, t) : nullptr;
@@ -99,8 +109,41 @@ FIS_DEV void epilogue_store(const fis_gemm_args& a, const EpiCtx& e, int r, int 
         v = __fsub_rn(l, __fmul_rn(a.step_scale, v));
     }
     if (e.res) v = __fadd_rn(v, load_elem(e.res, a.res.dtype, (long long)orow * a.res.ld + n));
+    if (a.n_split > 0 && n >= a.n_split) {
+        const int n2 = n - a.n_split;
+        if (a.d2_trans) store_elem(e.d2, a.d2.dtype, (long long)n2 * a.d2.ld + orow, v);
+        else store_elem(e.d2, a.d2.dtype, (long long)orow * a.d2.ld + n2, v);
+        return;
+    }
     if (a.d_trans) store_elem(e.d, a.d.dtype, (long long)n * a.d.ld + orow, v);
     else store_elem(e.d, a.d.dtype, (long long)orow * a.d.ld + n, v);
 }
 
 }  // namespace fis
+
+#include <stdlib.h>
+// Launch with the PDL attribute (FIS_PDL=0 in the environment disables it).
+inline bool fis_pdl_enabled() {
+    static int on = -1;
+    if (on < 0) {
+        const char* e = getenv("FIS_PDL");
+        on = (e && e[0] == '0') ? 0 : 1;
+    }
+    return on == 1;
+}
+
+template <typename Arg>
+inline cudaError_t fis_launch(void (*kernel)(Arg), dim3 grid, dim3 block, size_t smem, cudaStream_t stream,
+                              const Arg& arg) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = fis_pdl_enabled() ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kernel, arg);
+}

@@ -41,6 +41,8 @@ __global__ void __launch_bounds__(STHREADS) gemm_simt_kernel(const fis_gemm_args
     __shared__ float Bs[SBK][SBN + 4];
     __shared__ int rowp[SBM], rowy[SBM], rowx[SBM];
     __shared__ int s_last;
+    pdl_trigger();
+    pdl_wait();
     const int t = cur_step(a.step);
     const int tid = threadIdx.x;
     const int n0 = blockIdx.x * SBN, m0 = blockIdx.y * SBM;
@@ -160,6 +162,6 @@ __global__ void __launch_bounds__(STHREADS) gemm_simt_kernel(const fis_gemm_args
 
 int fis_gemm_simt_launch(const fis_gemm_args* a, cudaStream_t stream) {
     dim3 grid((a->n + fis::SBN - 1) / fis::SBN, (a->m + fis::SBM - 1) / fis::SBM, a->splits > 1 ? a->splits : 1);
-    fis::gemm_simt_kernel<<<grid, fis::STHREADS, 0, stream>>>(*a);
-    return cudaGetLastError() == cudaSuccess ? FIS_OK : FIS_ERR_LAUNCH;
+    return fis_launch(fis::gemm_simt_kernel, grid, dim3(fis::STHREADS), 0, stream, *a) == cudaSuccess ? FIS_OK
+                                                                                               : FIS_ERR_LAUNCH;
 }

@@ -22,7 +22,7 @@
 namespace fis {
 namespace tc {
 
-constexpr int BM = 128, BK = 64, STAGES = 4, PRODUCERS = 128, THREADS = 160;
+constexpr int BM = 128, BK = 64, STAGES = 4, PRODUCERS = 256, THREADS = 288, MMA_WARP = 8;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -78,12 +78,12 @@ struct EpiTab {
     float* bias; float* b2; float* gamma; float* beta; double* mean; double* rstd;
 };
 
-__device__ __forceinline__ void load_row32(const char* base, int dtype, long long off, int nvalid, float* v) {
+__device__ __forceinline__ void load_row16(const char* base, int dtype, long long off, int nvalid, float* v) {
     if (dtype == FIS_BF16) {
         const __nv_bfloat16* p = (const __nv_bfloat16*)base + off;
-        if (nvalid == 32 && ((uintptr_t)p & 15) == 0) {
+        if (nvalid == 16 && ((uintptr_t)p & 15) == 0) {
 #pragma unroll
-            for (int q = 0; q < 4; q++) {
+            for (int q = 0; q < 2; q++) {
                 uint4 u = *(const uint4*)(p + 8 * q);
                 const __nv_bfloat162* h = (const __nv_bfloat162*)&u;
 #pragma unroll
@@ -95,29 +95,29 @@ __device__ __forceinline__ void load_row32(const char* base, int dtype, long lon
             }
         } else {
 #pragma unroll
-            for (int j = 0; j < 32; j++) if (j < nvalid) v[j] = __bfloat162float(p[j]);
+            for (int j = 0; j < 16; j++) if (j < nvalid) v[j] = __bfloat162float(p[j]);
         }
     } else {
         const float* p = (const float*)base + off;
-        if (nvalid == 32 && ((uintptr_t)p & 15) == 0) {
+        if (nvalid == 16 && ((uintptr_t)p & 15) == 0) {
 #pragma unroll
-            for (int q = 0; q < 8; q++) {
+            for (int q = 0; q < 4; q++) {
                 float4 f = *(const float4*)(p + 4 * q);
                 v[4 * q] = f.x; v[4 * q + 1] = f.y; v[4 * q + 2] = f.z; v[4 * q + 3] = f.w;
             }
         } else {
 #pragma unroll
-            for (int j = 0; j < 32; j++) if (j < nvalid) v[j] = p[j];
+            for (int j = 0; j < 16; j++) if (j < nvalid) v[j] = p[j];
         }
     }
 }
 
-__device__ __forceinline__ void store_row32(char* base, int dtype, long long off, int nvalid, const float* v) {
+__device__ __forceinline__ void store_row16(char* base, int dtype, long long off, int nvalid, const float* v) {
     if (dtype == FIS_BF16) {
         __nv_bfloat16* p = (__nv_bfloat16*)base + off;
-        if (nvalid == 32 && ((uintptr_t)p & 15) == 0) {
+        if (nvalid == 16 && ((uintptr_t)p & 15) == 0) {
 #pragma unroll
-            for (int q = 0; q < 4; q++) {
+            for (int q = 0; q < 2; q++) {
                 uint4 u;
                 __nv_bfloat162* h = (__nv_bfloat162*)&u;
 #pragma unroll
@@ -126,66 +126,71 @@ __device__ __forceinline__ void store_row32(char* base, int dtype, long long off
             }
         } else {
 #pragma unroll
-            for (int j = 0; j < 32; j++) if (j < nvalid) p[j] = __float2bfloat16_rn(v[j]);
+            for (int j = 0; j < 16; j++) if (j < nvalid) p[j] = __float2bfloat16_rn(v[j]);
         }
     } else {
         float* p = (float*)base + off;
-        if (nvalid == 32 && ((uintptr_t)p & 15) == 0) {
+        if (nvalid == 16 && ((uintptr_t)p & 15) == 0) {
 #pragma unroll
-            for (int q = 0; q < 8; q++) *(float4*)(p + 4 * q) = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+            for (int q = 0; q < 4; q++) *(float4*)(p + 4 * q) = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
         } else {
 #pragma unroll
-            for (int j = 0; j < 32; j++) if (j < nvalid) p[j] = v[j];
+            for (int j = 0; j < 16; j++) if (j < nvalid) p[j] = v[j];
         }
     }
 }
 
-// Fused epilogue of one 32-column chunk of one output row (v holds the fp32 accumulators).
+// Fused epilogue of one 16-column chunk of one output row (v holds the fp32 accumulators).
 // Same arithmetic, in the same order, as fis::epilogue_store (fis_common.cuh).
 template <int MODE>
 __device__ __forceinline__ void row_epilogue(const fis_gemm_args& a, const EpiCtx& e, const EpiTab& tb, int r,
                                              int c0, int n0, float* v) {
     const int n = n0 + c0;
-    const int nvalid = min(32, a.n - n);
+    const int nvalid = min(16, a.n - n);
     if (nvalid <= 0) return;
     const int orow = a.d_rows ? __ldg(a.d_rows + r) : r;
 #pragma unroll
-    for (int j = 0; j < 32; j++) v[j] = __fadd_rn(v[j] * a.alpha, tb.bias[c0 + j]);
-    if (e.pre) store_row32(e.pre, a.pre.dtype, (long long)orow * a.pre.ld + n, nvalid, v);
+    for (int j = 0; j < 16; j++) v[j] = __fadd_rn(v[j] * a.alpha, tb.bias[c0 + j]);
+    if (e.pre) store_row16(e.pre, a.pre.dtype, (long long)orow * a.pre.ld + n, nvalid, v);
     if (e.bias2) {
 #pragma unroll
-        for (int j = 0; j < 32; j++) v[j] = __fadd_rn(v[j], tb.b2[c0 + j]);
+        for (int j = 0; j < 16; j++) v[j] = __fadd_rn(v[j], tb.b2[c0 + j]);
     }
     if (MODE == FIS_EPI_GN_SILU) {
-        float y[32];
+        float y[16];
 #pragma unroll
-        for (int j = 0; j < 32; j++)
+        for (int j = 0; j < 16; j++)
             y[j] = (float)(((double)v[j] - tb.mean[c0 + j]) * tb.rstd[c0 + j] * (double)tb.gamma[c0 + j] +
                            (double)tb.beta[c0 + j]);
-        if (e.pre2) store_row32(e.pre2, a.pre2.dtype, (long long)orow * a.pre2.ld + n, nvalid, y);
+        if (e.pre2) store_row16(e.pre2, a.pre2.dtype, (long long)orow * a.pre2.ld + n, nvalid, y);
 #pragma unroll
-        for (int j = 0; j < 32; j++) {
+        for (int j = 0; j < 16; j++) {
             const double yd = (double)y[j];
             v[j] = (float)(yd / (1.0 + exp(-yd)));
         }
     } else if (MODE == FIS_EPI_STEP) {
-        float l[32];
-        load_row32(e.lat, a.lat.dtype, (long long)orow * a.lat.ld + n, nvalid, l);
+        float l[16];
+        load_row16(e.lat, a.lat.dtype, (long long)orow * a.lat.ld + n, nvalid, l);
 #pragma unroll
-        for (int j = 0; j < 32; j++) v[j] = __fsub_rn(l[j], __fmul_rn(a.step_scale, v[j]));
+        for (int j = 0; j < 16; j++) v[j] = __fsub_rn(l[j], __fmul_rn(a.step_scale, v[j]));
     }
     if (e.res) {
-        float q[32];
-        load_row32(e.res, a.res.dtype, (long long)orow * a.res.ld + n, nvalid, q);
+        float q[16];
+        load_row16(e.res, a.res.dtype, (long long)orow * a.res.ld + n, nvalid, q);
 #pragma unroll
-        for (int j = 0; j < 32; j++) v[j] = __fadd_rn(v[j], q[j]);
+        for (int j = 0; j < 16; j++) v[j] = __fadd_rn(v[j], q[j]);
     }
-    if (a.d_trans) {
+    char* dbase = e.d;
+    int dt = a.d.dtype, dld = a.d.ld, dn = n, trans = a.d_trans;
+    if (a.n_split > 0 && n >= a.n_split) {  // fused QKV: V part goes transposed to d2
+        dbase = e.d2; dt = a.d2.dtype; dld = a.d2.ld; dn = n - a.n_split; trans = a.d2_trans;
+    }
+    if (trans) {
 #pragma unroll
-        for (int j = 0; j < 32; j++)
-            if (j < nvalid) store_elem(e.d, a.d.dtype, (long long)(n + j) * a.d.ld + orow, v[j]);
+        for (int j = 0; j < 16; j++)
+            if (j < nvalid) store_elem(dbase, dt, (long long)(dn + j) * dld + orow, v[j]);
     } else {
-        store_row32(e.d, a.d.dtype, (long long)orow * a.d.ld + n, nvalid, v);
+        store_row16(dbase, dt, (long long)orow * dld + dn, nvalid, v);
     }
 }
 
@@ -196,21 +201,24 @@ __device__ __forceinline__ void row_epilogue_any(const fis_gemm_args& a, const E
     else row_epilogue<FIS_EPI_NONE>(a, e, tb, r, c0, n0, v);
 }
 
-// Source pointer of the 64-channel K block starting at k0 for GEMM row r (16B granularity),
-// or nullptr for zero (padding / out of image / beyond K).
+// Per-row gather geometry, computed once per CTA: the row's pixel p (ROWS: A row) and,
+// for CONV, its (y, x); valid=false rows (beyond M) load zeros.
+struct RowGeo {
+    int p, oy, ox;
+    bool valid;
+};
+
+// Source pointer of the 64-channel K block starting at k0 for one GEMM row (16 B granularity),
+// or nullptr for zero (padding / out of image / beyond K). tap/c/segment are uniform per block.
 __device__ __forceinline__ const char* a_block_ptr(const fis_gemm_args& a, const char* abase, const char* f0,
-                                                   const char* c0p, const char* f1, const char* c1p, int r, int k0,
-                                                   int cin) {
-    if (r >= a.m) return nullptr;
-    const int p = a.rows ? __ldg(a.rows + r) : r;
+                                                   const char* c0p, const char* f1, const char* c1p,
+                                                   const RowGeo& g, int k0, int tap, int c) {
+    if (!g.valid) return nullptr;
     if (a.a_mode == FIS_A_ROWS) {
         if (k0 >= a.k) return nullptr;
-        return abase + ((long long)p * a.a.ld + k0) * 2;
+        return abase + ((long long)g.p * a.a.ld + k0) * 2;
     }
-    const int tap = k0 / cin;
-    int c = k0 - tap * cin;
-    const int oy = p / a.out_w, ox = p - (p / a.out_w) * a.out_w;
-    const int y = oy + tap / 3 - 1, x = ox + tap % 3 - 1;
+    const int y = g.oy + tap / 3 - 1, x = g.ox + tap % 3 - 1;
     if (y < 0 || x < 0 || y >= a.out_h || x >= a.out_w) return nullptr;
     const bool second = c >= a.src[0].c;
     const fis_src& s = second ? a.src[1] : a.src[0];
@@ -238,7 +246,6 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_tc_kernel(const fis_gemm_args
     int* last_flag = (int*)(tmem_slot + 1);  // followed by the epilogue tables
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int t = cur_step(a.step);
     const int n0 = blockIdx.x * BN, m0 = blockIdx.y * BM;
     const int kblocks = (a.k + BK - 1) / BK;
     const int kper = (kblocks + a.splits - 1) / a.splits;
@@ -253,7 +260,7 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_tc_kernel(const fis_gemm_args
         mbar_init(done, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    if (warp == 4) {
+    if (warp == MMA_WARP) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
                      "n"(BN < 32 ? 32 : BN));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
@@ -262,8 +269,11 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_tc_kernel(const fis_gemm_args
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    pdl_trigger();
+    pdl_wait();  // everything above (barrier init, TMEM alloc) overlaps the previous kernel
+    const int t = cur_step(a.step);
 
-    if (warp < 4) {
+    if (warp < MMA_WARP) {
         // ------------------------------------------------------------ producers
         const char* abase = a.a.ptr ? ref_base(a.a, t) : nullptr;
         const char* f0 = a.nsrc > 0 && a.src[0].fresh.ptr ? ref_base(a.src[0].fresh, t) : nullptr;
@@ -273,32 +283,38 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_tc_kernel(const fis_gemm_args
         const char* bbase = ref_base(a.b, t);
         const int cin = a.a_mode == FIS_A_CONV3X3 ? a.src[0].c + (a.nsrc > 1 ? a.src[1].c : 0) : a.k;
         const uint32_t sbase = smem_u32(smem);
+        // thread -> (row, half): two threads share a 128-byte row, 4 chunks of 16 B each
+        const int ar = tid >> 1, j0 = (tid & 1) * 4;
+        RowGeo g;
+        {
+            const int r = m0 + ar;
+            g.valid = r < a.m;
+            g.p = g.valid ? (a.rows ? __ldg(a.rows + r) : r) : 0;
+            g.oy = a.a_mode == FIS_A_CONV3X3 ? g.p / a.out_w : 0;
+            g.ox = g.p - g.oy * a.out_w;
+        }
+        const int bn = n0 + ar;
+        const char* brow = bbase + (long long)bn * a.b.ld * 2;
         for (int i = 0; i < nk; i++) {
             const int s = i % STAGES;
             const int k0 = (kb0 + i) * BK;
             if (i >= STAGES) mbar_wait(empty + s, ((i / STAGES) & 1) ^ 1);
             const uint32_t sa = sbase + s * Smem<BN>::STAGE;
             const uint32_t sb = sa + Smem<BN>::A_BYTES;
-            {   // A: thread tid owns row tid (8 chunks of 16 B)
-                const int r = tid;
-                const char* src = a_block_ptr(a, abase, f0, c0p, f1, c1p, m0 + r, k0, cin);
+            const int tap = a.a_mode == FIS_A_CONV3X3 ? k0 / cin : 0;
+            const int c = k0 - tap * cin;
+            const char* src = a_block_ptr(a, abase, f0, c0p, f1, c1p, g, k0, tap, c);
 #pragma unroll
-                for (int j = 0; j < 8; j++) {
-                    const bool ok = src != nullptr && (a.a_mode == FIS_A_CONV3X3 || k0 + j * 8 < a.k);
-                    cp_async16(sa + sw128_off(r, j), ok ? (const void*)(src + j * 16) : (const void*)bbase, ok);
-                }
+            for (int j = j0; j < j0 + 4; j++) {
+                const bool ok = src != nullptr && (a.a_mode == FIS_A_CONV3X3 || k0 + j * 8 < a.k);
+                cp_async16(sa + sw128_off(ar, j), ok ? (const void*)(src + j * 16) : (const void*)bbase, ok);
             }
+            if (ar < BN) {  // B: weight row ar of this N tile
 #pragma unroll
-            for (int rr = 0; rr < BN; rr += PRODUCERS) {  // B: weight rows
-                const int r = rr + tid;
-                if (r < BN) {
-                    const int n = n0 + r;
-                    const char* src = bbase + ((long long)n * a.b.ld + k0) * 2;
-#pragma unroll
-                    for (int j = 0; j < 8; j++) {
-                        const bool ok = n < a.n && k0 + j * 8 < a.k;
-                        cp_async16(sb + sw128_off(r, j), ok ? (const void*)(src + j * 16) : (const void*)bbase, ok);
-                    }
+                for (int j = j0; j < j0 + 4; j++) {
+                    const bool ok = bn < a.n && k0 + j * 8 < a.k;
+                    cp_async16(sb + sw128_off(ar, j), ok ? (const void*)(brow + (k0 + j * 8) * 2) : (const void*)bbase,
+                               ok);
                 }
             }
             cp_commit();
@@ -363,7 +379,7 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_tc_kernel(const fis_gemm_args
         tb.beta = tb.gamma + BN;
     }
     const EpiCtx e = make_epi(a, t);
-    if (warp < 4) {
+    if (warp < MMA_WARP) {
         // stage per-column parameters while the MMAs drain
         for (int c = tid; c < BN; c += PRODUCERS) {
             const int n = n0 + c;
@@ -380,39 +396,37 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_tc_kernel(const fis_gemm_args
                 tb.mean[c] = 0.0; tb.rstd[c] = 0.0; tb.gamma[c] = 0.f; tb.beta[c] = 0.f;
             }
         }
-        asm volatile("bar.sync 1, 128;" ::: "memory");
+        asm volatile("bar.sync 1, 256;" ::: "memory");
         mbar_wait(done, 0);
         tc_fence_after();
-        const int r = m0 + warp * 32 + lane;
+        const int quarter = warp & 3, half = warp >> 2;
+        const int r = m0 + quarter * 32 + lane;
         float* wsz = a.splits > 1 ? a.ws + (long long)blockIdx.z * a.m * a.n : nullptr;
 #pragma unroll 1
-        for (int cb = 0; cb < BN; cb += 32) {
-            uint32_t u[32];
-            const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + cb;
+        for (int cb = half * (BN / 2); cb < (half + 1) * (BN / 2); cb += 16) {
+            uint32_t u[16];
+            const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) + cb;
             asm volatile(
-                "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-                "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+                "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
                 : "=r"(u[0]), "=r"(u[1]), "=r"(u[2]), "=r"(u[3]), "=r"(u[4]), "=r"(u[5]), "=r"(u[6]), "=r"(u[7]),
                   "=r"(u[8]), "=r"(u[9]), "=r"(u[10]), "=r"(u[11]), "=r"(u[12]), "=r"(u[13]), "=r"(u[14]),
-                  "=r"(u[15]), "=r"(u[16]), "=r"(u[17]), "=r"(u[18]), "=r"(u[19]), "=r"(u[20]), "=r"(u[21]),
-                  "=r"(u[22]), "=r"(u[23]), "=r"(u[24]), "=r"(u[25]), "=r"(u[26]), "=r"(u[27]), "=r"(u[28]),
-                  "=r"(u[29]), "=r"(u[30]), "=r"(u[31])
+                  "=r"(u[15])
                 : "r"(taddr));
             asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
             if (r < a.m && n0 + cb < a.n) {
-                float v[32];
+                float v[16];
 #pragma unroll
-                for (int j = 0; j < 32; j++) v[j] = nk > 0 ? __uint_as_float(u[j]) : 0.f;
+                for (int j = 0; j < 16; j++) v[j] = nk > 0 ? __uint_as_float(u[j]) : 0.f;
                 if (wsz) {
-                    const int nvalid = min(32, a.n - (n0 + cb));
+                    const int nvalid = min(16, a.n - (n0 + cb));
                     float* p = wsz + (long long)r * a.n + n0 + cb;
-                    if (nvalid == 32 && ((uintptr_t)p & 15) == 0) {
+                    if (nvalid == 16 && ((uintptr_t)p & 15) == 0) {
 #pragma unroll
-                        for (int q = 0; q < 8; q++)
+                        for (int q = 0; q < 4; q++)
                             __stcg((float4*)(p + 4 * q), make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]));
                     } else {
 #pragma unroll
-                        for (int j = 0; j < 32; j++) if (j < nvalid) __stcg(p + j, v[j]);
+                        for (int j = 0; j < 16; j++) if (j < nvalid) __stcg(p + j, v[j]);
                     }
                 } else {
                     row_epilogue_any(a, e, tb, r, cb, n0, v);
@@ -422,7 +436,7 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_tc_kernel(const fis_gemm_args
     }
     tc_fence_before();
     __syncthreads();
-    if (warp == 4)
+    if (warp == MMA_WARP)
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(BN < 32 ? 32 : BN));
 
     if (a.splits > 1) {
@@ -433,28 +447,29 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_tc_kernel(const fis_gemm_args
         __syncthreads();
         if (!*last_flag) return;
         __threadfence();
-        if (warp < 4) {
+        if (warp < MMA_WARP) {
             // ordered reduction of the split partials: thread = output row, 32-column chunks
-            const int r = m0 + warp * 32 + lane;
+            const int quarter = warp & 3, half = warp >> 2;
+            const int r = m0 + quarter * 32 + lane;
             if (r < a.m) {
 #pragma unroll 1
-                for (int cb = 0; cb < BN && n0 + cb < a.n; cb += 32) {
-                    const int nvalid = min(32, a.n - (n0 + cb));
-                    float v[32];
+                for (int cb = half * (BN / 2); cb < (half + 1) * (BN / 2) && n0 + cb < a.n; cb += 16) {
+                    const int nvalid = min(16, a.n - (n0 + cb));
+                    float v[16];
 #pragma unroll
-                    for (int j = 0; j < 32; j++) v[j] = 0.f;
+                    for (int j = 0; j < 16; j++) v[j] = 0.f;
 #pragma unroll 1
                     for (int z = 0; z < a.splits; z++) {
                         const float* p = a.ws + ((long long)z * a.m + r) * a.n + n0 + cb;
-                        if (nvalid == 32 && ((uintptr_t)p & 15) == 0) {
+                        if (nvalid == 16 && ((uintptr_t)p & 15) == 0) {
 #pragma unroll
-                            for (int q = 0; q < 8; q++) {
+                            for (int q = 0; q < 4; q++) {
                                 const float4 f = __ldcg((const float4*)(p + 4 * q));
                                 v[4 * q] += f.x; v[4 * q + 1] += f.y; v[4 * q + 2] += f.z; v[4 * q + 3] += f.w;
                             }
                         } else {
 #pragma unroll
-                            for (int j = 0; j < 32; j++) if (j < nvalid) v[j] += __ldcg(p + j);
+                            for (int j = 0; j < 16; j++) if (j < nvalid) v[j] += __ldcg(p + j);
                         }
                     }
                     row_epilogue_any(a, e, tb, r, cb, n0, v);
@@ -475,8 +490,8 @@ int launch(const fis_gemm_args* a, cudaStream_t stream) {
         configured = true;
     }
     dim3 grid((a->n + BN - 1) / BN, (a->m + BM - 1) / BM, a->splits > 1 ? a->splits : 1);
-    gemm_tc_kernel<BN><<<grid, THREADS, smem, stream>>>(*a);
-    return cudaGetLastError() == cudaSuccess ? FIS_OK : FIS_ERR_LAUNCH;
+    return fis_launch(gemm_tc_kernel<BN>, grid, dim3(THREADS), smem, stream, *a) == cudaSuccess ? FIS_OK
+                                                                                            : FIS_ERR_LAUNCH;
 }
 
 }  // namespace tc
@@ -487,6 +502,7 @@ int launch(const fis_gemm_args* a, cudaStream_t stream) {
 // or a concat boundary); ROWS mode any K (zero-filled tail).
 int fis_gemm_tc_supported(const fis_gemm_args* a) {
     if (a->b.dtype != FIS_BF16 || (a->b.ld % 8)) return 0;
+    if (a->n_split > 0 && (a->n_split % 32)) return 0;
     if (a->a_mode == FIS_A_ROWS) {
         if (a->a.dtype != FIS_BF16 || (a->a.ld % 8)) return 0;
         return 1;

@@ -81,6 +81,8 @@ __global__ void __launch_bounds__(MT, 1) mask_detect_kernel(const fis_mask_detec
     __shared__ int valid_s[256];
     __shared__ int best_s;
     const int tid = threadIdx.x;
+    pdl_trigger();
+    pdl_wait();
 
     // Σ_t mean_c |x - y|  (masks.py:136-137): channel order sequential, then /C
     if (a.values_in) {
@@ -266,6 +268,8 @@ __device__ int compact_list(const unsigned char* bits, int n, int* list, int* in
 __global__ void __launch_bounds__(MT, 1) mask_plan_kernel(const fis_mask_plan_args a) {
     extern __shared__ __align__(16) unsigned char sm[];
     __shared__ int sh[72];
+    pdl_trigger();
+    pdl_wait();
     unsigned char* cur = sm;  // level bits
     unsigned char* tb = sm + a.h * a.w;  // tile bits scratch
     int h = a.h, w = a.w;
@@ -324,8 +328,8 @@ extern "C" int fis_mask_detect(const fis_mask_detect_args* a, void* stream) {
     const size_t smem = (size_t)fis_mask_detect_smem(a->h, a->w);
     if (cudaFuncSetAttribute(fis::mask_detect_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
         return FIS_ERR_UNSUPPORTED;
-    fis::mask_detect_kernel<<<1, fis::MT, smem, (cudaStream_t)stream>>>(*a);
-    return cudaGetLastError() == cudaSuccess ? FIS_OK : FIS_ERR_LAUNCH;
+    return fis_launch(fis::mask_detect_kernel, dim3(1), dim3(fis::MT), smem, (cudaStream_t)stream, *a) == cudaSuccess
+               ? FIS_OK : FIS_ERR_LAUNCH;
 }
 
 extern "C" int fis_mask_plan(const fis_mask_plan_args* a, void* stream) {
@@ -333,6 +337,6 @@ extern "C" int fis_mask_plan(const fis_mask_plan_args* a, void* stream) {
     const size_t smem = (size_t)a->h * a->w * 2;
     if (cudaFuncSetAttribute(fis::mask_plan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
         return FIS_ERR_UNSUPPORTED;
-    fis::mask_plan_kernel<<<1, fis::MT, smem, (cudaStream_t)stream>>>(*a);
-    return cudaGetLastError() == cudaSuccess ? FIS_OK : FIS_ERR_LAUNCH;
+    return fis_launch(fis::mask_plan_kernel, dim3(1), dim3(fis::MT), smem, (cudaStream_t)stream, *a) == cudaSuccess
+               ? FIS_OK : FIS_ERR_LAUNCH;
 }

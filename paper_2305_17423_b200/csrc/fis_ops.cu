@@ -8,6 +8,8 @@ namespace fis {
 
 // ---- group norm statistics (tensors.py:129-146): two-pass f64, rounded to f32
 __global__ void __launch_bounds__(256) gn_stats_kernel(const fis_gn_stats_args a) {
+    pdl_trigger();
+    pdl_wait();
     const int t = cur_step(a.step);
     const int g = blockIdx.x;
     const int cpg = a.c / a.groups;
@@ -47,6 +49,8 @@ __global__ void __launch_bounds__(256) gn_stats_kernel(const fis_gn_stats_args a
 
 // ---- normalise with given stats (+SiLU) (tensors.py:149-180, unet.py:291-293)
 __global__ void gn_apply_kernel(const fis_gn_apply_args a) {
+    pdl_trigger();
+    pdl_wait();
     const int t = cur_step(a.step);
     const char* x = ref_base(a.x, t);
     const float* mean = (const float*)ref_base(a.mean, t);
@@ -75,6 +79,8 @@ __global__ void gn_apply_kernel(const fis_gn_apply_args a) {
 
 // ---- scaled row softmax; one warp per row (tensors.py:183-192, unet.py:555-566)
 __global__ void softmax_kernel(const fis_softmax_args a) {
+    pdl_trigger();
+    pdl_wait();
     const int t = cur_step(a.step);
     const int warps = blockDim.x / 32;
     const int row = blockIdx.x * warps + threadIdx.x / 32;
@@ -130,6 +136,8 @@ __global__ void softmax_kernel(const fis_softmax_args a) {
 
 // ---- 2x2 average pool with select-on-read (unet.py:296-298; numpy order (a+b)+(c+d))
 __global__ void pool2_kernel(const fis_pool_args a) {
+    pdl_trigger();
+    pdl_wait();
     const int t = cur_step(a.step);
     const char* fr = a.src.fresh.ptr ? ref_base(a.src.fresh, t) : nullptr;
     const char* ca = a.src.cache.ptr ? ref_base(a.src.cache, t) : nullptr;
@@ -151,6 +159,8 @@ __global__ void pool2_kernel(const fis_pool_args a) {
 
 // ---- full-map materialisation: out[q] = select(q)
 __global__ void materialize_kernel(const fis_materialize_args a) {
+    pdl_trigger();
+    pdl_wait();
     const int t = cur_step(a.step);
     const char* fr = a.src.fresh.ptr ? ref_base(a.src.fresh, t) : nullptr;
     const char* ca = a.src.cache.ptr ? ref_base(a.src.cache, t) : nullptr;
@@ -176,16 +186,15 @@ static int fis_check(void) { return cudaGetLastError() == cudaSuccess ? FIS_OK :
 
 extern "C" int fis_gn_stats(const fis_gn_stats_args* a, void* stream) {
     if (a->groups <= 0 || a->c % a->groups) return FIS_ERR_SHAPE;
-    fis::gn_stats_kernel<<<a->groups, 256, 0, (cudaStream_t)stream>>>(*a);
-    return fis_check();
+    return fis_launch(fis::gn_stats_kernel, dim3(a->groups), dim3(256), 0, (cudaStream_t)stream, *a) == cudaSuccess ? FIS_OK : FIS_ERR_LAUNCH;
 }
 
 extern "C" int fis_gn_apply(const fis_gn_apply_args* a, void* stream) {
     if (a->groups <= 0 || a->c % a->groups) return FIS_ERR_SHAPE;
     if (a->rows == 0) return FIS_OK;
     long long total = (long long)a->rows * a->c;
-    fis::gn_apply_kernel<<<fis::grid_for(total, 256), 256, 0, (cudaStream_t)stream>>>(*a);
-    return fis_check();
+    return fis_launch(fis::gn_apply_kernel, dim3(fis::grid_for(total, 256)), dim3(256), 0, (cudaStream_t)stream, *a) ==
+                   cudaSuccess ? FIS_OK : FIS_ERR_LAUNCH;
 }
 
 extern "C" int fis_softmax(const fis_softmax_args* a, void* stream) {
@@ -193,21 +202,20 @@ extern "C" int fis_softmax(const fis_softmax_args* a, void* stream) {
     if (a->pad_cols < a->cols) return FIS_ERR_SHAPE;
     if ((a->verbatim || a->npairs) && !a->cached.ptr) return FIS_ERR_CACHE_MISS;
     const int warps = 8;
-    fis::softmax_kernel<<<(a->rows + warps - 1) / warps, warps * 32, 0, (cudaStream_t)stream>>>(*a);
-    return fis_check();
+    return fis_launch(fis::softmax_kernel, dim3((a->rows + warps - 1) / warps), dim3(warps * 32), 0, (cudaStream_t)stream, *a) == cudaSuccess ? FIS_OK : FIS_ERR_LAUNCH;
 }
 
 extern "C" int fis_pool2(const fis_pool_args* a, void* stream) {
     if (a->n == 0) return FIS_OK;
     if (a->src.index && !a->src.cache.ptr) return FIS_ERR_CACHE_MISS;
     long long total = (long long)a->n * a->c;
-    fis::pool2_kernel<<<fis::grid_for(total, 256), 256, 0, (cudaStream_t)stream>>>(*a);
-    return fis_check();
+    return fis_launch(fis::pool2_kernel, dim3(fis::grid_for(total, 256)), dim3(256), 0, (cudaStream_t)stream, *a) ==
+                   cudaSuccess ? FIS_OK : FIS_ERR_LAUNCH;
 }
 
 extern "C" int fis_materialize(const fis_materialize_args* a, void* stream) {
     if (a->src.index && !a->src.cache.ptr) return FIS_ERR_CACHE_MISS;
     long long total = (long long)a->src.h * a->src.w * a->c;
-    fis::materialize_kernel<<<fis::grid_for(total, 256), 256, 0, (cudaStream_t)stream>>>(*a);
-    return fis_check();
+    return fis_launch(fis::materialize_kernel, dim3(fis::grid_for(total, 256)), dim3(256), 0, (cudaStream_t)stream, *a) ==
+                   cudaSuccess ? FIS_OK : FIS_ERR_LAUNCH;
 }

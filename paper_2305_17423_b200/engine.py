@@ -85,9 +85,8 @@ class Weights:
             elif i.kind == "norm":
                 self.norm[i.layer_id] = (torch.from_numpy(p["gamma"]).to(dev, f32), torch.from_numpy(p["beta"]).to(dev, f32))
             elif i.kind == "self_attn":
-                wqk = np.concatenate([p["wq"].T, p["wk"].T], axis=0)
-                self.sa[i.layer_id] = (torch.from_numpy(np.ascontiguousarray(wqk)).to(dev, act),
-                                       torch.from_numpy(np.ascontiguousarray(p["wv"].T)).to(dev, act),
+                wqkv = np.concatenate([p["wq"].T, p["wk"].T, p["wv"].T], axis=0)  # [3C, C]
+                self.sa[i.layer_id] = (torch.from_numpy(np.ascontiguousarray(wqkv)).to(dev, act),
                                        1.0 / math.sqrt(i.channels))
             else:
                 self.ca[i.layer_id] = (torch.from_numpy(np.ascontiguousarray(p["wq"].T)).to(dev, act),
@@ -131,6 +130,7 @@ class Launcher:
 
 
     def _ensure_ws(self, floats):
+        floats = min(floats, 1 << 25)  # 128 MB cap; the split choice respects ws_floats
         if self._ws.numel() < floats:
             self._ws = torch.empty(int(floats * 1.25) + 1024, dtype=torch.float32, device=self.dev)
 
@@ -143,7 +143,8 @@ class Launcher:
         return max(1, s)
 
     def gemm(self, m, n, k, *, a=None, rows=None, srcs=None, out_hw=None, b: DRef, d: DRef, alpha=1.0, bias=None,
-             bias2=None, pre=None, epi=L.EPI_NONE, gn=None, lat=None, res=None, d_trans=False, splits=None):
+             bias2=None, pre=None, epi=L.EPI_NONE, gn=None, lat=None, res=None, d_trans=False, splits=None,
+             n_split=0, d2=None, d2_trans=False):
         if m == 0:
             return
         g = L.GemmArgs()
@@ -173,11 +174,12 @@ class Launcher:
         g.res = _r(res)
         g.d = d.ref()
         g.d_trans = 1 if d_trans else 0
-        s = self._splits(m, n, k) if splits is None else splits
-        if s > 1:
-            self._ensure_ws(s * m * n)
-            g.ws = L.ptr(self._ws)
-            g.counters = L.ptr(self._counters)
+        if n_split:
+            g.n_split, g.d2, g.d2_trans = n_split, d2.ref(), 1 if d2_trans else 0
+        s = 0 if splits is None else splits  # 0: the library picks split-K from the tile shape
+        self._ensure_ws((32 if s == 0 else s) * m * n)
+        g.ws, g.ws_floats = L.ptr(self._ws), self._ws.numel()
+        g.counters = L.ptr(self._counters)
         g.splits = s
         g.step = L.ptr(self.step_dev)
         g.impl = self.gemm_impl
@@ -245,16 +247,16 @@ class Engine(Launcher):
     # ------------------------------------------------------------ building blocks
     def attn_self(self, lid, m, s: DRef, y1: DRef, level, tag, pre=None):
         """y1 = s + softmax(s Wq (s Wk)^T * scale) (s Wv) over m tokens (sparse.py:265-300/341-349)."""
-        wqk, wvt, scale = self.W.sa[lid]
-        c = wvt.shape[0]
+        wqkv, scale = self.W.sa[lid]
+        c = wqkv.shape[1]
         cap = self.hw(level)
         mp = _pad(cap)
         qk = self.scratch(f"qk{tag}", (cap, 2 * c))
         vt = self.scratch(f"vt{tag}", (c, mp), zero=True)
         S = self.scratch(f"S{tag}", (cap, cap), torch.float32)
         P = self.scratch(f"P{tag}", (cap, mp), zero=True)
-        self.gemm(m, 2 * c, c, a=s, b=DRef(wqk), d=DRef(qk))
-        self.gemm(m, c, c, a=s, b=DRef(wvt), d=DRef(vt, ld=mp), d_trans=True)
+        # one GEMM for Q|K (row-major) and V (stored transposed as the PV B operand)
+        self.gemm(m, 3 * c, c, a=s, b=DRef(wqkv), d=DRef(qk), n_split=2 * c, d2=DRef(vt, ld=mp), d2_trans=True)
         qkr = DRef(qk)
         self.gemm(m, m, c, a=qkr, b=qkr.cols(c), d=DRef(S, ld=m))
         self.softmax(m, m, _pad(m), DRef(S, ld=m), scale, DRef(P, ld=_pad(m)))
