@@ -60,6 +60,11 @@ class SoftmaxArgs(C.Structure):
                 ("pair_old", C.c_void_p), ("pair_new", C.c_void_p), ("step", C.c_void_p)]
 
 
+class XattnArgs(C.Structure):
+    _fields_ = [("rows", C.c_int), ("c", C.c_int), ("n_text", C.c_int), ("q", Ref), ("k", Ref), ("v", Ref),
+                ("scale", C.c_float), ("res", Ref), ("pre", Ref), ("out", Ref), ("step", C.c_void_p)]
+
+
 class PoolArgs(C.Structure):
     _fields_ = [("n", C.c_int), ("c", C.c_int), ("src", Src), ("rows", C.c_void_p), ("out", Ref),
                 ("step", C.c_void_p)]
@@ -83,7 +88,7 @@ class MaskPlanArgs(C.Structure):
 
 
 _SIGS = {
-    "fis_gemm": GemmArgs, "fis_gn_stats": GnStatsArgs, "fis_gn_apply": GnApplyArgs, "fis_softmax": SoftmaxArgs,
+    "fis_gemm": GemmArgs, "fis_xattn": XattnArgs, "fis_gn_stats": GnStatsArgs, "fis_gn_apply": GnApplyArgs, "fis_softmax": SoftmaxArgs,
     "fis_pool2": PoolArgs, "fis_materialize": MaterializeArgs, "fis_mask_detect": MaskDetectArgs,
     "fis_mask_plan": MaskPlanArgs,
 }

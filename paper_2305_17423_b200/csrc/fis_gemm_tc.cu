@@ -47,6 +47,9 @@ __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, bool v
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(valid ? 16 : 0) : "memory");
 }
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_arrive_noinc(uint64_t* b) {
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(b)) : "memory");
+}
 template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
@@ -317,17 +320,10 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_tc_kernel(const fis_gemm_args
                                ok);
                 }
             }
-            cp_commit();
-            if (i >= STAGES - 1) {
-                cp_wait<STAGES - 1>();
-                fence_async_smem();
-                mbar_arrive(full + (i - (STAGES - 1)) % STAGES);
-            }
+            // the barrier counts this thread's arrival when all its prior cp.async have landed:
+            // no thread-side wait, STAGES stages of loads stay in flight
+            cp_async_arrive_noinc(full + s);
         }
-        // drain
-        cp_wait<0>();
-        fence_async_smem();
-        for (int i = max(0, nk - (STAGES - 1)); i < nk; i++) mbar_arrive(full + i % STAGES);
     } else {
         // ------------------------------------------------------------ MMA issuer
         const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |

@@ -17,9 +17,10 @@ __global__ void __launch_bounds__(256) gn_stats_kernel(const fis_gn_stats_args a
     const char* x = ref_base(a.x, t);
     __shared__ double red[256];
     double s = 0.0;
-    for (long long e = threadIdx.x; e < cnt; e += blockDim.x) {
-        const int q = (int)(e / cpg), c = g * cpg + (int)(e % cpg);
-        s += (double)load_elem(x, a.x.dtype, (long long)q * a.x.ld + c);
+    // thread = pixel (strided), inner loop over the group's contiguous channels (32-bit index math)
+    for (int q = threadIdx.x; q < a.hw; q += blockDim.x) {
+        const long long base = (long long)q * a.x.ld + g * cpg;
+        for (int c = 0; c < cpg; c++) s += (double)load_elem(x, a.x.dtype, base + c);
     }
     red[threadIdx.x] = s;
     __syncthreads();
@@ -30,10 +31,12 @@ __global__ void __launch_bounds__(256) gn_stats_kernel(const fis_gn_stats_args a
     const double mean = red[0] / (double)cnt;
     __syncthreads();
     double v = 0.0;
-    for (long long e = threadIdx.x; e < cnt; e += blockDim.x) {
-        const int q = (int)(e / cpg), c = g * cpg + (int)(e % cpg);
-        const double d = (double)load_elem(x, a.x.dtype, (long long)q * a.x.ld + c) - mean;
-        v += d * d;
+    for (int q = threadIdx.x; q < a.hw; q += blockDim.x) {
+        const long long base = (long long)q * a.x.ld + g * cpg;
+        for (int c = 0; c < cpg; c++) {
+            const double d = (double)load_elem(x, a.x.dtype, base + c) - mean;
+            v += d * d;
+        }
     }
     red[threadIdx.x] = v;
     __syncthreads();
@@ -58,10 +61,9 @@ __global__ void gn_apply_kernel(const fis_gn_apply_args a) {
     char* yn = a.y_norm.ptr ? ref_base(a.y_norm, t) : nullptr;
     char* ys = a.y_silu.ptr ? ref_base(a.y_silu, t) : nullptr;
     const int cpg = a.c / a.groups;
-    const long long total = (long long)a.rows * a.c;
-    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
-         e += (long long)gridDim.x * blockDim.x) {
-        const int r = (int)(e / a.c), c = (int)(e % a.c);
+    const int total = a.rows * a.c;
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
+        const int r = e / a.c, c = e - (e / a.c) * a.c;
         const int xr = a.x_rows ? __ldg(a.x_rows + r) : r;
         const int yr = a.y_rows ? __ldg(a.y_rows + r) : r;
         const int g = c / cpg;
@@ -143,10 +145,9 @@ __global__ void pool2_kernel(const fis_pool_args a) {
     const char* ca = a.src.cache.ptr ? ref_base(a.src.cache, t) : nullptr;
     char* out = ref_base(a.out, t);
     const int cw = a.src.w / 2;
-    const long long total = (long long)a.n * a.c;
-    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
-         e += (long long)gridDim.x * blockDim.x) {
-        const int i = (int)(e / a.c), c = (int)(e % a.c);
+    const int total = a.n * a.c;
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
+        const int i = e / a.c, c = e - (e / a.c) * a.c;
         const int P = a.rows ? __ldg(a.rows + i) : i;
         const int py = P / cw, px = P - (P / cw) * cw;
         const int q = (2 * py) * a.src.w + 2 * px;
@@ -165,10 +166,9 @@ __global__ void materialize_kernel(const fis_materialize_args a) {
     const char* fr = a.src.fresh.ptr ? ref_base(a.src.fresh, t) : nullptr;
     const char* ca = a.src.cache.ptr ? ref_base(a.src.cache, t) : nullptr;
     char* out = ref_base(a.out, t);
-    const long long total = (long long)a.src.h * a.src.w * a.c;
-    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
-         e += (long long)gridDim.x * blockDim.x) {
-        const int q = (int)(e / a.c), c = (int)(e % a.c);
+    const int total = a.src.h * a.src.w * a.c;
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
+        const int q = e / a.c, c = e - (e / a.c) * a.c;
         store_elem(out, a.out.dtype, (long long)q * a.out.ld + c, src_value(a.src, fr, ca, q, c));
     }
 }
@@ -218,4 +218,104 @@ extern "C" int fis_materialize(const fis_materialize_args* a, void* stream) {
     long long total = (long long)a->src.h * a->src.w * a->c;
     return fis_launch(fis::materialize_kernel, dim3(fis::grid_for(total, 256)), dim3(256), 0, (cudaStream_t)stream, *a) ==
                    cudaSuccess ? FIS_OK : FIS_ERR_LAUNCH;
+}
+
+// ---- fused cross-attention over a short text context (<= 128 tokens), warp per query row
+namespace fis {
+
+template <int CPL>  // channels per lane = C / 32 rounded up (<= 40 for C = 1280)
+__global__ void __launch_bounds__(256) xattn_kernel(const fis_xattn_args a) {
+    pdl_trigger();
+    pdl_wait();
+    const int t = cur_step(a.step);
+    const int warps = blockDim.x >> 5;
+    const int row = blockIdx.x * warps + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (row >= a.rows) return;
+    const char* qb = ref_base(a.q, t);
+    const char* kb = ref_base(a.k, t);
+    const char* vb = ref_base(a.v, t);
+    // lane owns channels c = lane + 32*i
+    float q[CPL];
+#pragma unroll
+    for (int i = 0; i < CPL; i++) {
+        const int c = lane + 32 * i;
+        q[i] = c < a.c ? load_elem(qb, a.q.dtype, (long long)row * a.q.ld + c) : 0.f;
+    }
+    float sc[4];
+#pragma unroll
+    for (int jb = 0; jb < 4; jb++) {
+        sc[jb] = -INFINITY;
+        if (jb * 32 >= a.n_text) continue;
+#pragma unroll 4
+        for (int jj = 0; jj < 32; jj++) {
+            const int j = jb * 32 + jj;
+            if (j >= a.n_text) break;
+            float d = 0.f;
+#pragma unroll
+            for (int i = 0; i < CPL; i++) {
+                const int c = lane + 32 * i;
+                if (c < a.c) d = fmaf(q[i], load_elem(kb, a.k.dtype, (long long)j * a.k.ld + c), d);
+            }
+            d = warp_sum(d);
+            if (lane == jj) sc[jb] = d * a.scale;
+        }
+    }
+    float m = fmaxf(fmaxf(sc[0], sc[1]), fmaxf(sc[2], sc[3]));
+    m = warp_max(m);
+    float sum = 0.f;
+#pragma unroll
+    for (int jb = 0; jb < 4; jb++) {
+        sc[jb] = (jb * 32 + lane < a.n_text) ? expf(sc[jb] - m) : 0.f;
+        sum += sc[jb];
+    }
+    sum = warp_sum(sum);
+    const float inv = 1.0f / sum;
+    float o[CPL];
+#pragma unroll
+    for (int i = 0; i < CPL; i++) o[i] = 0.f;
+#pragma unroll
+    for (int jb = 0; jb < 4; jb++) {
+        if (jb * 32 >= a.n_text) continue;
+        const float pj_all = sc[jb] * inv;  // softmax weight of token jb*32+lane (f32, tensors.py:192)
+#pragma unroll 4
+        for (int jj = 0; jj < 32; jj++) {
+            const int j = jb * 32 + jj;
+            if (j >= a.n_text) break;
+            const float pj = __shfl_sync(0xffffffffu, pj_all, jj);
+#pragma unroll
+            for (int i = 0; i < CPL; i++) {
+                const int c = lane + 32 * i;
+                if (c < a.c) o[i] = fmaf(pj, load_elem(vb, a.v.dtype, (long long)j * a.v.ld + c), o[i]);
+            }
+        }
+    }
+    char* ob = ref_base(a.out, t);
+    char* pb = a.pre.ptr ? ref_base(a.pre, t) : nullptr;
+    const char* rb = a.res.ptr ? ref_base(a.res, t) : nullptr;
+#pragma unroll
+    for (int i = 0; i < CPL; i++) {
+        const int c = lane + 32 * i;
+        if (c >= a.c) continue;
+        float v = o[i];
+        if (pb) store_elem(pb, a.pre.dtype, (long long)row * a.pre.ld + c, v);
+        if (rb) v = __fadd_rn(v, load_elem(rb, a.res.dtype, (long long)row * a.res.ld + c));
+        store_elem(ob, a.out.dtype, (long long)row * a.out.ld + c, v);
+    }
+}
+
+}  // namespace fis
+
+extern "C" int fis_xattn(const fis_xattn_args* a, void* stream) {
+    if (a->rows == 0) return FIS_OK;
+    if (a->n_text < 1 || a->n_text > 128 || a->c < 1 || a->c > 32 * 40) return FIS_ERR_UNSUPPORTED;
+    const int warps = 8;
+    const dim3 grid((a->rows + warps - 1) / warps), block(32 * warps);
+    cudaError_t e;
+    const int cpl = (a->c + 31) / 32;
+    if (cpl <= 4) e = fis_launch(fis::xattn_kernel<4>, grid, block, 0, (cudaStream_t)stream, *a);
+    else if (cpl <= 10) e = fis_launch(fis::xattn_kernel<10>, grid, block, 0, (cudaStream_t)stream, *a);
+    else if (cpl <= 20) e = fis_launch(fis::xattn_kernel<20>, grid, block, 0, (cudaStream_t)stream, *a);
+    else e = fis_launch(fis::xattn_kernel<40>, grid, block, 0, (cudaStream_t)stream, *a);
+    return e == cudaSuccess ? FIS_OK : FIS_ERR_LAUNCH;
 }

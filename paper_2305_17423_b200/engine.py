@@ -117,6 +117,7 @@ class Launcher:
         self._counters = torch.zeros(1 << 16, dtype=torch.int32, device=self.dev)
         self.launches = 0
         self._scratch = {}
+        self.fused_xattn = True
         self.groups = 1
         self.step_scale_value = 1.0
 
@@ -241,7 +242,9 @@ class Engine(Launcher):
             vt = torch.zeros((c, _pad(nt)), dtype=self.act, device=self.dev)
             self.gemm(nt, c, emb.shape[1], a=DRef(emb), b=DRef(wk), d=DRef(k), splits=1)
             self.gemm(nt, c, emb.shape[1], a=DRef(emb), b=DRef(wv), d=DRef(vt), d_trans=True, splits=1)
-            out[lid] = (k, vt)
+            v = torch.empty((nt, c), dtype=self.act, device=self.dev)
+            self.gemm(nt, c, emb.shape[1], a=DRef(emb), b=DRef(wv), d=DRef(v), splits=1)
+            out[lid] = (k, vt, v)
         return out
 
     # ------------------------------------------------------------ building blocks
@@ -265,14 +268,21 @@ class Engine(Launcher):
     def attn_cross(self, lid, m, x: DRef, out: DRef, level, tag, kv, pre=None, map_=None, ctrl=None):
         """out = x + softmax(x Wq K_text^T * scale) V_text (sparse.py:303-338/352-361, unet.py:555-566)."""
         wq, _, _, scale = self.W.ca[lid]
-        k, vt = kv[lid]
+        k, vt, v = kv[lid]
         c, nt = wq.shape[0], k.shape[0]
         ntp = vt.shape[1]
         cap = self.hw(level)
         q = self.scratch(f"q{tag}", (cap, c))
+        self.gemm(m, c, c, a=x, b=DRef(wq), d=DRef(q))
+        if ctrl is None and map_ is None and nt <= 128 and self.fused_xattn:
+            # scores + softmax + P.V + residual in one launch (text context <= 128 tokens)
+            a = L.XattnArgs(m, c, nt, DRef(q).ref(), DRef(k).ref(), DRef(v).ref(), scale, x.ref(), _r(pre),
+                            out.ref(), L.ptr(self.step_dev))
+            L.call("fis_xattn", a)
+            self.launches += 1
+            return
         S = self.scratch(f"Sx{tag}", (cap, nt), torch.float32)
         P = self.scratch(f"Px{tag}", (cap, ntp), zero=True)
-        self.gemm(m, c, c, a=x, b=DRef(wq), d=DRef(q))
         self.gemm(m, nt, c, a=DRef(q), b=DRef(k), d=DRef(S))
         if ctrl is not None:
             cached, verbatim, pairs = ctrl
