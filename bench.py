@@ -153,7 +153,9 @@ def run_reference(args):
     if rank != 0:
         return
     threads = os.cpu_count() or 1
-    v, per = cpu_sample(C2, args.mask, args.steps, args.warmup, threads)
+    # bounded sample: at most 10 timed sparse steps (~5 s each on CPU) after <= 1 warm-up
+    n_steps, n_warm = min(args.steps, 10), min(args.warmup, 1)
+    v, per = cpu_sample(C2, args.mask, n_steps, n_warm, threads)
     line = {"metric": METRIC, "value": v, "unit": "edit-steps/s", "impl": "reference", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": per * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64-accumulate/f32", "data": "synthetic",
@@ -161,7 +163,7 @@ def run_reference(args):
                        "model": "sparsedit toy UNet @ SD-1.5 widths (320/640/1280/1280)", "latent": "1x4x64x64",
                        "mask_fraction": args.mask},
             "cpu_baseline": {"value": v, "unit": "edit-steps/s", "cores": threads, "kind": "port",
-                             "sample": f"oracle port (numpy f64 restatement of sparsedit), {args.warmup}+{args.steps} "
+                             "sample": f"oracle port (numpy f64 restatement of sparsedit), {n_warm}+{n_steps} "
                                        "sparse steps at t=1 after one dense caching step"},
             "e2e": {"value": v, "unit": "edit-steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
@@ -214,6 +216,10 @@ def run_ours(args):
     per_ms = ms / max(1, args.steps)
     value = ws * args.steps / (ms / 1e3)
 
+    # --- dense UNet step on the same GPU (what edit() runs for a full mask; SURVEY §8 C3 bar)
+    dense_ms = dense_step_ms(eng, U, P, cfg, kv, args)
+    sweep = mask_sweep(eng, U, P, cfg, arena, kv, lat0, args) if args.sweep else None
+
     # --- per-kernel timing of the gated (sparse) convs: eager instrumented step
     gflop_conv, conv_ms, gemm_ms, dense_gflop = instrumented_conv(eng, ep, U, cfg, mask)
     hbm, tf, src = peaks()
@@ -242,6 +248,8 @@ def run_ours(args):
                      "kernel": "fis_gemm gated-conv gather-GEMMs (13/step)",
                      "note": f"algorithmic {gflop_conv:.2f} GFLOP/step over {conv_ms:.3f} ms of gated-conv GEMM time; "
                              f"all GEMMs {gemm_ms:.3f} ms/step; peak {src}"},
+        "dense_baseline": {"ms_per_step": dense_ms, "steps_per_s": 1e3 / dense_ms,
+                           "sparse_speedup": dense_ms / per_ms},
         "gpu_launches": per_step_launches * args.steps,
         "clocks": clk.summary(),
         "e2e": {"value": T / e2e_s, "unit": "edit-steps/s", "h2d_bytes_per_step": (cfg.latent_h * cfg.latent_w * 17) // T,
@@ -252,11 +260,54 @@ def run_ours(args):
         v, per = cpu_sample(C2, args.mask, 1, 0, os.cpu_count() or 1)
         line["cpu_baseline"] = {"value": v, "unit": "edit-steps/s", "cores": os.cpu_count(), "kind": "port",
                                 "sample": "oracle port, 1 sparse step at t=1 after one dense caching step"}
+    if sweep is not None:
+        line["sweep"] = sweep
     if rank == 0:
         print(json.dumps(line))
     import torch.distributed as dist
     if dist.is_available() and dist.is_initialized():
         dist.destroy_process_group()
+
+
+def _time_runner(runner, T, steps, warmup):
+    import torch
+    runner.step(1)
+    for i in range(warmup):
+        runner.step(1 + (i + 1) % T)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for i in range(steps):
+        runner.step(1 + i % T)
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / max(1, steps)
+
+
+def dense_step_ms(eng, U, P, cfg, kv, args):
+    """Dense forward + step update of the same UNet (no recording), one graph per step."""
+    import torch
+    lat = torch.empty((cfg.steps + 1, eng.hw(0), cfg.latent_channels), dtype=torch.float32, device=eng.dev)
+    lat[0].copy_(U._to_nhwc(P.initial_latent(cfg), eng.dev))
+    runner = U._Runner(eng, U.StepPlan(eng, kv, lat, None), True)
+    return _time_runner(runner, cfg.steps, max(3, args.steps // 2), 3)
+
+
+def mask_sweep(eng, U, P, cfg, arena, kv, lat0, args):
+    """C3: sparse step time vs mask ratio (centered squares), same cache and GPU."""
+    out = []
+    for f in (0.01, 0.05, 0.10, 0.25, 0.50, 1.0):
+        mask = P.centered_square_mask(cfg.latent_h, cfg.latent_w, f)
+        if mask.all_active():
+            continue
+        ep = U.EditPlan(eng, arena, mask, kv, lat0)
+        ms = _time_runner(U._Runner(eng, ep.plan, True), cfg.steps, max(3, args.steps // 2), 3)
+        unet = U.UNet(cfg)
+        cost = {l: 4 * ep.dp.n_tiles[l] for l in range(cfg.levels)}
+        gfl = 2 * sum(unet.sparse_step_macs(77, ep.dp.n_active, cost).values()) / 1e9
+        out.append({"mask_fraction": f, "active_px_L0": ep.dp.n_active[0], "ms_per_step": ms,
+                    "edit_steps_per_s": 1e3 / ms, "algorithmic_gflop_per_step": gfl})
+    return out
 
 
 def instrumented_conv(eng, ep, U, cfg, mask):
@@ -302,6 +353,7 @@ def main():
     ap.add_argument("--mask", type=float, default=0.10)
     ap.add_argument("--precision", default="fp32", choices=["fp32", "bf16"])
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--sweep", action="store_true", help="also time the C3 mask-ratio sweep")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

@@ -229,6 +229,10 @@ typedef struct {
 } fis_mask_plan_args;
 int fis_mask_plan(const fis_mask_plan_args* a, void* stream);
 
+/* profiling: phase timestamps (%globaltimer ns) of CTA (0,0,0) of tcgen05 GEMM launches */
+int fis_trace(int on);
+int fis_trace_read(unsigned long long* out16);
+
 /* misc */
 int fis_abi_version(void);
 const char* fis_last_error(void);

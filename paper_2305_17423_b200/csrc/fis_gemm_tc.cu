@@ -238,6 +238,18 @@ __device__ __forceinline__ const char* a_block_ptr(const fis_gemm_args& a, const
     return fr + ((long long)q * s.fresh.ld + c) * 2;
 }
 
+// Phase timestamps (%globaltimer, ns) of CTA (0,0,0) for profiling the fixed per-launch cost;
+// enabled with fis_trace(1), read with fis_trace_read().
+__device__ int g_trace_on = 0;
+__device__ unsigned long long g_trace[16];
+__device__ __forceinline__ void trace(int slot) {
+    if (g_trace_on && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        g_trace[slot] = t;
+    }
+}
+
 template <int BN>
 __global__ void __launch_bounds__(THREADS, 1) gemm_tc_kernel(const fis_gemm_args a) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -249,6 +261,7 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_tc_kernel(const fis_gemm_args
     int* last_flag = (int*)(tmem_slot + 1);  // followed by the epilogue tables
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    if (tid == 0) trace(0);
     const int n0 = blockIdx.x * BN, m0 = blockIdx.y * BM;
     const int kblocks = (a.k + BK - 1) / BK;
     const int kper = (kblocks + a.splits - 1) / a.splits;
@@ -272,8 +285,10 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_tc_kernel(const fis_gemm_args
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    if (tid == 0) trace(1);
     pdl_trigger();
     pdl_wait();  // everything above (barrier init, TMEM alloc) overlaps the previous kernel
+    if (tid == 0) trace(2);
     const int t = cur_step(a.step);
 
     if (warp < MMA_WARP) {
@@ -323,6 +338,7 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_tc_kernel(const fis_gemm_args
             // the barrier counts this thread's arrival when all its prior cp.async have landed:
             // no thread-side wait, STAGES stages of loads stay in flight
             cp_async_arrive_noinc(full + s);
+            if (tid == 0 && i == 0) trace(3);
         }
     } else {
         // ------------------------------------------------------------ MMA issuer
@@ -332,6 +348,8 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_tc_kernel(const fis_gemm_args
         for (int i = 0; i < nk; i++) {
             const int s = i % STAGES;
             mbar_wait(full + s, (i / STAGES) & 1);
+            if (lane == 0 && i == 0) trace(4);
+            if (lane == 0 && i == nk - 1) trace(5);
             tc_fence_after();
             if (lane == 0) {
                 const uint32_t sa = sbase + s * Smem<BN>::STAGE;
@@ -394,6 +412,7 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_tc_kernel(const fis_gemm_args
         }
         asm volatile("bar.sync 1, 256;" ::: "memory");
         mbar_wait(done, 0);
+        if (tid == 0) trace(6);
         tc_fence_after();
         const int quarter = warp & 3, half = warp >> 2;
         const int r = m0 + quarter * 32 + lane;
@@ -435,6 +454,7 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_tc_kernel(const fis_gemm_args
     if (warp == MMA_WARP)
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(BN < 32 ? 32 : BN));
 
+    if (tid == 0) trace(7);
     if (a.splits > 1) {
         __threadfence();
         __syncthreads();
@@ -517,4 +537,12 @@ int fis_gemm_tc_launch(const fis_gemm_args* a, cudaStream_t stream) {
     if (a->n <= 64) return fis::tc::launch<64>(a, stream);
     if (a->n <= 128 || (a->n % 128) != 0) return fis::tc::launch<128>(a, stream);
     return fis::tc::launch<128>(a, stream);
+}
+
+extern "C" int fis_trace(int on) {
+    return cudaMemcpyToSymbol(fis::tc::g_trace_on, &on, sizeof(int)) == cudaSuccess ? FIS_OK : FIS_ERR_LAUNCH;
+}
+extern "C" int fis_trace_read(unsigned long long* out16) {
+    return cudaMemcpyFromSymbol(out16, fis::tc::g_trace, 16 * sizeof(unsigned long long)) == cudaSuccess
+               ? FIS_OK : FIS_ERR_LAUNCH;
 }

@@ -117,7 +117,7 @@ class Launcher:
         self._counters = torch.zeros(1 << 16, dtype=torch.int32, device=self.dev)
         self.launches = 0
         self._scratch = {}
-        self.fused_xattn = True
+        self.fused_xattn = False  # SIMT xattn is latency-bound; GEMM path until a tcgen05 version lands
         self.groups = 1
         self.step_scale_value = 1.0
 
