@@ -411,6 +411,7 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_tc_kernel(const fis_gemm_args
             }
         }
         asm volatile("bar.sync 1, 256;" ::: "memory");
+        if (tid == 0) trace(10);
         mbar_wait(done, 0);
         if (tid == 0) trace(6);
         tc_fence_after();
@@ -449,8 +450,10 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_tc_kernel(const fis_gemm_args
             }
         }
     }
+    if (tid == 0) trace(8);
     tc_fence_before();
     __syncthreads();
+    if (tid == 0) trace(9);
     if (warp == MMA_WARP)
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(BN < 32 ? 32 : BN));
 

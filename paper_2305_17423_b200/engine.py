@@ -261,8 +261,8 @@ class Engine(Launcher):
         # one GEMM for Q|K (row-major) and V (stored transposed as the PV B operand)
         self.gemm(m, 3 * c, c, a=s, b=DRef(wqkv), d=DRef(qk), n_split=2 * c, d2=DRef(vt, ld=mp), d2_trans=True)
         qkr = DRef(qk)
-        self.gemm(m, m, c, a=qkr, b=qkr.cols(c), d=DRef(S, ld=m))
-        self.softmax(m, m, _pad(m), DRef(S, ld=m), scale, DRef(P, ld=_pad(m)))
+        self.gemm(m, m, c, a=qkr, b=qkr.cols(c), d=DRef(S, ld=_pad(m)))
+        self.softmax(m, m, _pad(m), DRef(S, ld=_pad(m)), scale, DRef(P, ld=_pad(m)))
         self.gemm(m, c, m, a=DRef(P, ld=_pad(m)), b=DRef(vt, ld=mp), d=y1, res=s, pre=pre)
 
     def attn_cross(self, lid, m, x: DRef, out: DRef, level, tag, kv, pre=None, map_=None, ctrl=None):
@@ -281,7 +281,7 @@ class Engine(Launcher):
             L.call("fis_xattn", a)
             self.launches += 1
             return
-        S = self.scratch(f"Sx{tag}", (cap, nt), torch.float32)
+        S = self.scratch(f"Sx{tag}", (cap, ntp), torch.float32)  # ld padded: 16-byte aligned rows
         P = self.scratch(f"Px{tag}", (cap, ntp), zero=True)
         self.gemm(m, nt, c, a=DRef(q), b=DRef(k), d=DRef(S))
         if ctrl is not None:
