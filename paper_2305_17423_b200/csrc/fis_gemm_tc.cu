@@ -380,7 +380,7 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_tc_kernel(const fis_gemm_args
         __syncwarp();
     }
 
-    // ---------------------------------------------------------------- epilogue (warps 0-3)
+    // ---------------------------------------------------------------- epilogue
     EpiTab tb;
     {
         unsigned char* ep = (unsigned char*)(last_flag + 4);
@@ -393,6 +393,10 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_tc_kernel(const fis_gemm_args
         tb.beta = tb.gamma + BN;
     }
     const EpiCtx e = make_epi(a, t);
+    const int S = a.splits > 1 ? a.splits : 1;  // split-K CTAs of this tile = one cluster along z
+    // fp32 partial tile [BM][BN+4] staged in the (now idle) pipeline buffers
+    constexpr int PLD = BN + 4;
+    float* part = (float*)smem;
     if (warp < MMA_WARP) {
         // stage per-column parameters while the MMAs drain
         for (int c = tid; c < BN; c += PRODUCERS) {
@@ -416,8 +420,7 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_tc_kernel(const fis_gemm_args
         if (tid == 0) trace(6);
         tc_fence_after();
         const int quarter = warp & 3, half = warp >> 2;
-        const int r = m0 + quarter * 32 + lane;
-        float* wsz = a.splits > 1 ? a.ws + (long long)blockIdx.z * a.m * a.n : nullptr;
+        const int lr = quarter * 32 + lane, r = m0 + lr;
 #pragma unroll 1
         for (int cb = half * (BN / 2); cb < (half + 1) * (BN / 2); cb += 16) {
             uint32_t u[16];
@@ -429,24 +432,15 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_tc_kernel(const fis_gemm_args
                   "=r"(u[15])
                 : "r"(taddr));
             asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-            if (r < a.m && n0 + cb < a.n) {
-                float v[16];
+            float v[16];
 #pragma unroll
-                for (int j = 0; j < 16; j++) v[j] = nk > 0 ? __uint_as_float(u[j]) : 0.f;
-                if (wsz) {
-                    const int nvalid = min(16, a.n - (n0 + cb));
-                    float* p = wsz + (long long)r * a.n + n0 + cb;
-                    if (nvalid == 16 && ((uintptr_t)p & 15) == 0) {
+            for (int j = 0; j < 16; j++) v[j] = nk > 0 ? __uint_as_float(u[j]) : 0.f;
+            if (S > 1) {
+                float* p = part + lr * PLD + cb;
 #pragma unroll
-                        for (int q = 0; q < 4; q++)
-                            __stcg((float4*)(p + 4 * q), make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]));
-                    } else {
-#pragma unroll
-                        for (int j = 0; j < 16; j++) if (j < nvalid) __stcg(p + j, v[j]);
-                    }
-                } else {
-                    row_epilogue_any(a, e, tb, r, cb, n0, v);
-                }
+                for (int q = 0; q < 4; q++) *(float4*)(p + 4 * q) = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+            } else if (r < a.m && n0 + cb < a.n) {
+                row_epilogue_any(a, e, tb, r, cb, n0, v);
             }
         }
     }
@@ -456,47 +450,42 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_tc_kernel(const fis_gemm_args
     if (tid == 0) trace(9);
     if (warp == MMA_WARP)
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(BN < 32 ? 32 : BN));
-
-    if (tid == 0) trace(7);
-    if (a.splits > 1) {
-        __threadfence();
-        __syncthreads();
-        const int tile = blockIdx.y * gridDim.x + blockIdx.x;
-        if (tid == 0) *last_flag = (atomicAdd(a.counters + tile, 1) == a.splits - 1);
-        __syncthreads();
-        if (!*last_flag) return;
-        __threadfence();
-        if (warp < MMA_WARP) {
-            // ordered reduction of the split partials: thread = output row, 32-column chunks
-            const int quarter = warp & 3, half = warp >> 2;
-            const int r = m0 + quarter * 32 + lane;
-            if (r < a.m) {
+    if (S > 1) {
+        // cluster-wide deterministic split-K reduction over DSMEM: CTA z reduces rows
+        // [z*rows_per, (z+1)*rows_per) of the tile, summing the S partials in split order.
+        asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+        uint32_t rank;
+        asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+        const int rows_per = (BM + S - 1) / S;
+        const int rbeg = (int)rank * rows_per, rend = min(BM, rbeg + rows_per);
+        const int chunks = BN / 16;
+        const uint32_t part_s = smem_u32(part);
+        for (int item = tid; item < (rend - rbeg) * chunks; item += THREADS) {
+            const int lr = rbeg + item / chunks, cb = (item % chunks) * 16;
+            const int r = m0 + lr;
+            if (r >= a.m || n0 + cb >= a.n) continue;
+            const uint32_t off = (uint32_t)((lr * PLD + cb) * 4);
+            float v[16];
+#pragma unroll
+            for (int j = 0; j < 16; j++) v[j] = 0.f;
 #pragma unroll 1
-                for (int cb = half * (BN / 2); cb < (half + 1) * (BN / 2) && n0 + cb < a.n; cb += 16) {
-                    const int nvalid = min(16, a.n - (n0 + cb));
-                    float v[16];
+            for (int z = 0; z < S; z++) {
+                uint32_t ra;
+                asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(part_s + off), "r"(z));
 #pragma unroll
-                    for (int j = 0; j < 16; j++) v[j] = 0.f;
-#pragma unroll 1
-                    for (int z = 0; z < a.splits; z++) {
-                        const float* p = a.ws + ((long long)z * a.m + r) * a.n + n0 + cb;
-                        if (nvalid == 16 && ((uintptr_t)p & 15) == 0) {
-#pragma unroll
-                            for (int q = 0; q < 4; q++) {
-                                const float4 f = __ldcg((const float4*)(p + 4 * q));
-                                v[4 * q] += f.x; v[4 * q + 1] += f.y; v[4 * q + 2] += f.z; v[4 * q + 3] += f.w;
-                            }
-                        } else {
-#pragma unroll
-                            for (int j = 0; j < 16; j++) if (j < nvalid) v[j] += __ldcg(p + j);
-                        }
-                    }
-                    row_epilogue_any(a, e, tb, r, cb, n0, v);
+                for (int q = 0; q < 4; q++) {
+                    float x0, x1, x2, x3;
+                    asm volatile("ld.shared::cluster.v4.f32 {%0,%1,%2,%3}, [%4];"
+                                 : "=f"(x0), "=f"(x1), "=f"(x2), "=f"(x3) : "r"(ra + 16 * q));
+                    v[4 * q] += x0; v[4 * q + 1] += x1; v[4 * q + 2] += x2; v[4 * q + 3] += x3;
                 }
             }
+            row_epilogue_any(a, e, tb, r, cb, n0, v);
         }
-        if (tid == 0) a.counters[tile] = 0;
+        // keep every CTA's shared memory alive until all peers finished reading it
+        asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
     }
+    if (tid == 0) trace(7);
 }
 
 template <int BN>
@@ -506,11 +495,59 @@ int launch(const fis_gemm_args* a, cudaStream_t stream) {
     if (!configured) {
         if (cudaFuncSetAttribute(gemm_tc_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
             return FIS_ERR_UNSUPPORTED;
+        cudaFuncSetAttribute(gemm_tc_kernel<BN>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
         configured = true;
     }
-    dim3 grid((a->n + BN - 1) / BN, (a->m + BM - 1) / BM, a->splits > 1 ? a->splits : 1);
-    return fis_launch(gemm_tc_kernel<BN>, grid, dim3(THREADS), smem, stream, *a) == cudaSuccess ? FIS_OK
-                                                                                            : FIS_ERR_LAUNCH;
+    const int S = a->splits > 1 ? a->splits : 1;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((a->n + BN - 1) / BN, (a->m + BM - 1) / BM, S);
+    cfg.blockDim = dim3(THREADS);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[2];
+    int na = 0;
+    if (S > 1) {
+        attr[na].id = cudaLaunchAttributeClusterDimension;
+        attr[na].val.clusterDim.x = 1;
+        attr[na].val.clusterDim.y = 1;
+        attr[na].val.clusterDim.z = S;
+        na++;
+    }
+    if (fis_pdl_enabled()) {
+        attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[na].val.programmaticStreamSerializationAllowed = 1;
+        na++;
+    }
+    cfg.attrs = attr;
+    cfg.numAttrs = na;
+    return cudaLaunchKernelEx(&cfg, gemm_tc_kernel<BN>, *a) == cudaSuccess ? FIS_OK : FIS_ERR_LAUNCH;
+}
+
+// Largest split-K cluster the device can co-schedule for this kernel (<= 16).
+template <int BN>
+int max_cluster() {
+    static int best = 0;
+    if (best) return best;
+    best = 8;
+    if (cudaFuncSetAttribute(gemm_tc_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, Smem<BN>::TOTAL) !=
+            cudaSuccess ||
+        cudaFuncSetAttribute(gemm_tc_kernel<BN>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess)
+        return best;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(1, 1, 16);
+    cfg.blockDim = dim3(THREADS);
+    cfg.dynamicSmemBytes = Smem<BN>::TOTAL;
+    cudaLaunchAttribute attr;
+    attr.id = cudaLaunchAttributeClusterDimension;
+    attr.val.clusterDim.x = 1;
+    attr.val.clusterDim.y = 1;
+    attr.val.clusterDim.z = 16;
+    cfg.attrs = &attr;
+    cfg.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, gemm_tc_kernel<BN>, &cfg) == cudaSuccess && n >= 1) best = 16;
+    cudaGetLastError();
+    return best;
 }
 
 }  // namespace tc
@@ -534,6 +571,8 @@ int fis_gemm_tc_supported(const fis_gemm_args* a) {
     }
     return 1;
 }
+
+int fis_gemm_tc_max_splits(int n) { return n <= 64 ? fis::tc::max_cluster<64>() : fis::tc::max_cluster<128>(); }
 
 int fis_gemm_tc_launch(const fis_gemm_args* a, cudaStream_t stream) {
     if (!fis_gemm_tc_supported(a)) return FIS_ERR_UNSUPPORTED;
