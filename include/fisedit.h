@@ -102,6 +102,8 @@ typedef struct {
     int* counters;          /* per-tile arrival counters (zeroed, self-resetting) */
     const int* step;
     int impl;               /* 0 auto, 1 SIMT fp32-accumulate, 2 tcgen05 bf16 */
+    int static_meta;        /* 1: rows/index lists are not written by the preceding kernel, so the
+                               gather metadata may be read before the programmatic-launch wait */
 } fis_gemm_args;
 
 int fis_gemm(const fis_gemm_args* args, void* stream);

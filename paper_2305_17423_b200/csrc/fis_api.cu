@@ -4,7 +4,7 @@
 int fis_gemm_simt_launch(const fis_gemm_args* a, cudaStream_t stream);
 int fis_gemm_tc_launch(const fis_gemm_args* a, cudaStream_t stream);
 int fis_gemm_tc_supported(const fis_gemm_args* a);
-int fis_gemm_tc_max_splits(int n);
+int fis_gemm_tc_choose_splits(int m, int n, int k);
 
 extern "C" {
 
@@ -40,17 +40,9 @@ static int fis_choose_splits(const fis_gemm_args* a, bool tc) {
     long long tiles, kb;
     int minper, target;
     if (tc) {
-        // split-K CTAs form one thread-block cluster per tile (DSMEM reduction, no workspace)
-        const int bn = a->n <= 64 ? 64 : 128;
-        tiles = (long long)((a->m + 127) / 128) * ((a->n + bn - 1) / bn);
-        kb = (a->k + 63) / 64;
-        long long s = sms / (tiles > 0 ? tiles : 1);
-        if (s > kb / 3) s = kb / 3;
-        const int cap = fis_gemm_tc_max_splits(a->n);
-        if (s > cap) s = cap;
-        if (s < 2) return 1;
-        const long long per = (kb + s - 1) / s;
-        return (int)((kb + per - 1) / per);
+        // split-K CTAs form one thread-block cluster per tile (DSMEM reduction, no workspace);
+        // S is the largest cluster size whose clusters all fit in one wave
+        return fis_gemm_tc_choose_splits(a->m, a->n, a->k);
     } else {
         tiles = (long long)((a->m + 63) / 64) * ((a->n + 63) / 64);
         kb = (a->k + 15) / 16;

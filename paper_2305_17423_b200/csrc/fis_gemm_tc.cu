@@ -18,6 +18,7 @@
 // scattered active pixels whose halo reads select between the fresh compact buffer
 // and the step's cache slab per pixel.
 #include "fis_common.cuh"
+#include <climits>
 
 namespace fis {
 namespace tc {
@@ -73,7 +74,8 @@ struct Smem {
     static constexpr int B_BYTES = BN * BK * 2;
     static constexpr int STAGE = A_BYTES + B_BYTES;
     static constexpr int EPI = BN * 32;  // per-column epilogue tables
-    static constexpr int TOTAL = STAGES * STAGE + 1024 /*align*/ + 256 /*barriers*/ + EPI;
+    static constexpr int SEL = BM * 2 * 9 * 4;  // per-row, per-segment, per-tap select-on-read table
+    static constexpr int TOTAL = STAGES * STAGE + 1024 /*align*/ + 256 /*barriers*/ + EPI + SEL + 16;
 };
 
 // Per-column epilogue parameters of this CTA's BN columns, staged once in shared memory.
@@ -211,6 +213,30 @@ struct RowGeo {
     bool valid;
 };
 
+constexpr int SEL_ZERO = INT_MIN;
+
+// Select-on-read decisions of one output row for every 3x3 tap of source segment `seg`:
+// >= 0 fresh row (or full-map pixel), <= -2 cache pixel (-2 - q), SEL_ZERO = zero padding.
+__device__ __forceinline__ void build_sel(const fis_gemm_args& a, int p, int seg, int* out9) {
+    const fis_src& s = a.src[seg];
+    const int oy = p / a.out_w, ox = p - (p / a.out_w) * a.out_w;
+#pragma unroll
+    for (int tap = 0; tap < 9; tap++) {
+        const int y = oy + tap / 3 - 1, x = ox + tap % 3 - 1;
+        int v = SEL_ZERO;
+        if (y >= 0 && x >= 0 && y < a.out_h && x < a.out_w) {
+            const int q = (s.up ? (y >> 1) : y) * s.w + (s.up ? (x >> 1) : x);
+            if (s.index) {
+                const int i = __ldg(s.index + q);
+                v = i >= 0 ? i : -2 - q;
+            } else {
+                v = q;
+            }
+        }
+        out9[tap] = v;
+    }
+}
+
 // Source pointer of the 64-channel K block starting at k0 for one GEMM row (16 B granularity),
 // or nullptr for zero (padding / out of image / beyond K). tap/c/segment are uniform per block.
 __device__ __forceinline__ const char* a_block_ptr(const fis_gemm_args& a, const char* abase, const char* f0,
@@ -286,8 +312,24 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_tc_kernel(const fis_gemm_args
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
     if (tid == 0) trace(1);
+    // gather metadata of the producer's row: pixel + (CONV) the select-on-read decision of every
+    // tap of both concat segments, in a shared table; read before the programmatic-launch wait
+    // when the row/index lists are static (they are inside a captured edit step)
+    int* seltab = (int*)(((uintptr_t)(smem + STAGES * Smem<BN>::STAGE + 256 + Smem<BN>::EPI) + 15) & ~(uintptr_t)15);
+    const int ar = tid >> 1, half_id = tid & 1;
+    int row_p = 0;
+    bool row_valid = false;
+    auto build_meta = [&]() {
+        if (warp >= MMA_WARP) return;
+        const int r = m0 + ar;
+        row_valid = r < a.m;
+        row_p = row_valid ? (a.rows ? __ldg(a.rows + r) : r) : 0;
+        if (a.a_mode == FIS_A_CONV3X3 && half_id < a.nsrc) build_sel(a, row_p, half_id, seltab + (ar * 2 + half_id) * 9);
+    };
+    if (a.static_meta) build_meta();
     pdl_trigger();
-    pdl_wait();  // everything above (barrier init, TMEM alloc) overlaps the previous kernel
+    pdl_wait();  // everything above (barrier init, TMEM alloc, static metadata) overlaps the previous kernel
+    if (!a.static_meta) build_meta();
     if (tid == 0) trace(2);
     const int t = cur_step(a.step);
 
@@ -302,15 +344,10 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_tc_kernel(const fis_gemm_args
         const int cin = a.a_mode == FIS_A_CONV3X3 ? a.src[0].c + (a.nsrc > 1 ? a.src[1].c : 0) : a.k;
         const uint32_t sbase = smem_u32(smem);
         // thread -> (row, half): two threads share a 128-byte row, 4 chunks of 16 B each
-        const int ar = tid >> 1, j0 = (tid & 1) * 4;
-        RowGeo g;
-        {
-            const int r = m0 + ar;
-            g.valid = r < a.m;
-            g.p = g.valid ? (a.rows ? __ldg(a.rows + r) : r) : 0;
-            g.oy = a.a_mode == FIS_A_CONV3X3 ? g.p / a.out_w : 0;
-            g.ox = g.p - g.oy * a.out_w;
-        }
+        const int j0 = half_id * 4;
+        __syncwarp();  // the two threads of a row each built one segment's table entries
+        const int* mysel = seltab + ar * 2 * 9;
+        const int src0c = a.nsrc > 0 ? a.src[0].c : 0;
         const int bn = n0 + ar;
         const char* brow = bbase + (long long)bn * a.b.ld * 2;
         for (int i = 0; i < nk; i++) {
@@ -319,9 +356,23 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_tc_kernel(const fis_gemm_args
             if (i >= STAGES) mbar_wait(empty + s, ((i / STAGES) & 1) ^ 1);
             const uint32_t sa = sbase + s * Smem<BN>::STAGE;
             const uint32_t sb = sa + Smem<BN>::A_BYTES;
-            const int tap = a.a_mode == FIS_A_CONV3X3 ? k0 / cin : 0;
-            const int c = k0 - tap * cin;
-            const char* src = a_block_ptr(a, abase, f0, c0p, f1, c1p, g, k0, tap, c);
+            const char* src = nullptr;
+            if (row_valid) {
+                if (a.a_mode == FIS_A_ROWS) {
+                    if (k0 < a.k) src = abase + ((long long)row_p * a.a.ld + k0) * 2;
+                } else {
+                    const int tap = k0 / cin;
+                    int c = k0 - tap * cin;
+                    const int seg = c >= src0c ? 1 : 0;
+                    c -= seg ? src0c : 0;
+                    const int sel = mysel[seg * 9 + tap];
+                    if (sel != SEL_ZERO) {
+                        const fis_src& sr = a.src[seg];
+                        if (sel >= 0) src = (seg ? f1 : f0) + ((long long)sel * sr.fresh.ld + c) * 2;
+                        else src = (seg ? c1p : c0p) + ((long long)(-2 - sel) * sr.cache.ld + c) * 2;
+                    }
+                }
+            }
 #pragma unroll
             for (int j = j0; j < j0 + 4; j++) {
                 const bool ok = src != nullptr && (a.a_mode == FIS_A_CONV3X3 || k0 + j * 8 < a.k);
@@ -523,30 +574,42 @@ int launch(const fis_gemm_args* a, cudaStream_t stream) {
     return cudaLaunchKernelEx(&cfg, gemm_tc_kernel<BN>, *a) == cudaSuccess ? FIS_OK : FIS_ERR_LAUNCH;
 }
 
-// Largest split-K cluster the device can co-schedule for this kernel (<= 16).
+// How many clusters of S CTAs (split-K) the device co-schedules for this kernel, S = 1..16
+// (GPC packing: ~18 SMs per GPC, 1 CTA per SM). Cached per BN.
 template <int BN>
-int max_cluster() {
-    static int best = 0;
-    if (best) return best;
-    best = 8;
-    if (cudaFuncSetAttribute(gemm_tc_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, Smem<BN>::TOTAL) !=
-            cudaSuccess ||
-        cudaFuncSetAttribute(gemm_tc_kernel<BN>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess)
-        return best;
+int active_clusters(int S) {
+    static int table[17] = {0};
+    if (S < 1 || S > 16) return 0;
+    if (table[S]) return table[S];
+    cudaFuncSetAttribute(gemm_tc_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, Smem<BN>::TOTAL);
+    cudaFuncSetAttribute(gemm_tc_kernel<BN>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(1, 1, 16);
+    cfg.gridDim = dim3(1, 1, S);
     cfg.blockDim = dim3(THREADS);
     cfg.dynamicSmemBytes = Smem<BN>::TOTAL;
     cudaLaunchAttribute attr;
     attr.id = cudaLaunchAttributeClusterDimension;
     attr.val.clusterDim.x = 1;
     attr.val.clusterDim.y = 1;
-    attr.val.clusterDim.z = 16;
+    attr.val.clusterDim.z = S;
     cfg.attrs = &attr;
     cfg.numAttrs = 1;
     int n = 0;
-    if (cudaOccupancyMaxActiveClusters(&n, gemm_tc_kernel<BN>, &cfg) == cudaSuccess && n >= 1) best = 16;
+    if (cudaOccupancyMaxActiveClusters(&n, gemm_tc_kernel<BN>, &cfg) != cudaSuccess) n = 0;
     cudaGetLastError();
+    table[S] = n > 0 ? n : -1;
+    return table[S];
+}
+
+// Largest S such that all tiles' clusters run in one wave and each split keeps >= 3 K blocks.
+template <int BN>
+int choose_splits(long long tiles, long long kb) {
+    int best = 1;
+    for (int S = 2; S <= 16; S++) {
+        if (kb / S < 3) break;
+        const int ac = active_clusters<BN>(S);
+        if (ac >= tiles) best = S;
+    }
     return best;
 }
 
@@ -572,7 +635,11 @@ int fis_gemm_tc_supported(const fis_gemm_args* a) {
     return 1;
 }
 
-int fis_gemm_tc_max_splits(int n) { return n <= 64 ? fis::tc::max_cluster<64>() : fis::tc::max_cluster<128>(); }
+int fis_gemm_tc_choose_splits(int m, int n, int k) {
+    const long long kb = (k + fis::tc::BK - 1) / fis::tc::BK;
+    if (n <= 64) return fis::tc::choose_splits<64>((long long)((m + 127) / 128) * ((n + 63) / 64), kb);
+    return fis::tc::choose_splits<128>((long long)((m + 127) / 128) * ((n + 127) / 128), kb);
+}
 
 int fis_gemm_tc_launch(const fis_gemm_args* a, cudaStream_t stream) {
     if (!fis_gemm_tc_supported(a)) return FIS_ERR_UNSUPPORTED;

@@ -118,6 +118,9 @@ class Launcher:
         self.launches = 0
         self._scratch = {}
         self.fused_xattn = False  # SIMT xattn is latency-bound; GEMM path until a tcgen05 version lands
+        # gather lists (rows / pixel->row maps) are written once per edit, before any step runs
+        # (DevicePlan syncs), so GEMMs may read them before the programmatic-launch wait
+        self.static_meta = False
         self.groups = 1
         self.step_scale_value = 1.0
 
@@ -184,6 +187,7 @@ class Launcher:
         g.splits = s
         g.step = L.ptr(self.step_dev)
         g.impl = self.gemm_impl
+        g.static_meta = 1 if self.static_meta else 0
         L.call("fis_gemm", g)
         self.launches += 1
 
@@ -206,6 +210,7 @@ class Engine(Launcher):
 
     def __init__(self, config: UNetConfig, precision: str = "fp32", device=None):
         super().__init__(precision, device)
+        self.static_meta = True
         self.config = config
         self.groups = config.groups
         self.step_scale_value = float(step_scale(config))

@@ -136,6 +136,51 @@ class UNet:
     def info(self, layer_id: int) -> LayerInfo:
         return self._by_id[layer_id]
 
+    # -- per-layer objects with the reference attributes (built lazily: seeded host params) --
+    def layer_objects(self) -> dict:
+        if getattr(self, "_objs", None) is None:
+            from .modes import make_layers
+            hl, topo = build_registry(self.config, with_params=True)
+            self._objs = make_layers(hl)
+            self._time_bias = topo["time_bias"]
+        return self._objs
+
+    @property
+    def time_bias(self):
+        self.layer_objects()
+        return self._time_bias
+
+    @property
+    def stem(self):
+        return self.layer_objects()[self.topo["stem"]]
+
+    @property
+    def out_conv(self):
+        return self.layer_objects()[self.topo["out"]]
+
+    @property
+    def down(self):
+        return [self.layer_objects()[i] for i in self.topo["down"]]
+
+    @property
+    def fuse(self):
+        return {l: self.layer_objects()[i] for l, i in self.topo["fuse"].items()}
+
+    @property
+    def enc_blocks(self):
+        o = self.layer_objects()
+        return [[{k: o[v] for k, v in b.items()} for b in lv] for lv in self.topo["enc"]]
+
+    @property
+    def dec_blocks(self):
+        o = self.layer_objects()
+        return {l: [{k: o[v] for k, v in b.items()} for b in lv] for l, lv in self.topo["dec"].items()}
+
+    def forward(self, latent, t, text_emb, mode):
+        """One denoiser evaluation through the reference mode protocol (unet.py:430-458)."""
+        from .modes import forward
+        return forward(self, latent, t, text_emb, mode)
+
     def conv_cin(self, lid):
         return self._cin[lid]
 
@@ -408,3 +453,13 @@ def edit(session: EditSession, config: UNetConfig, store: CacheStore) -> EditRes
     latent = _to_nchw(final, cl, H, W)
     rep = _build_report(unet, n_new, config, [outcome.phase1_macs, phase2])
     return EditResult(latent, rep, store.stats(), mask, False, outcome.phase1_macs.total, phase2.total, plans)
+
+
+# reference-compatible names of the per-layer mode protocol (unet.py:464-663,676,781)
+from .modes import ControlledMode, DenseMode, SparseMode  # noqa: E402
+from .modes import _MacsCounter as _ModeMacsCounter  # noqa: E402,F401
+from .modes import sparse_contexts as _sparse_contexts  # noqa: E402
+
+
+def _step_scale(config: UNetConfig):
+    return step_scale(config)
