@@ -234,6 +234,7 @@ int fis_mask_plan(const fis_mask_plan_args* a, void* stream);
 /* profiling: phase timestamps (%globaltimer ns) of CTA (0,0,0) of tcgen05 GEMM launches */
 int fis_trace(int on);
 int fis_trace_read(unsigned long long* out16);
+int fis_trace_read_ctas(unsigned long long* out2048); /* per CTA: entry, MMA done, cluster sync, exit */
 
 /* misc */
 int fis_abi_version(void);

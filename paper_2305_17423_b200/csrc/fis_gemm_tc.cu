@@ -268,11 +268,19 @@ __device__ __forceinline__ const char* a_block_ptr(const fis_gemm_args& a, const
 // enabled with fis_trace(1), read with fis_trace_read().
 __device__ int g_trace_on = 0;
 __device__ unsigned long long g_trace[16];
+__device__ unsigned long long g_trace_cta[512][4];  // per CTA: entry, mainloop done, cluster sync 1, exit
+__device__ __forceinline__ unsigned long long gtime() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
 __device__ __forceinline__ void trace(int slot) {
-    if (g_trace_on && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0) {
-        unsigned long long t;
-        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-        g_trace[slot] = t;
+    if (g_trace_on && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0) g_trace[slot] = gtime();
+}
+__device__ __forceinline__ void trace_cta(int slot) {
+    if (g_trace_on) {
+        const int id = (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+        if (id < 512) g_trace_cta[id][slot] = gtime();
     }
 }
 
@@ -287,7 +295,7 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_tc_kernel(const fis_gemm_args
     int* last_flag = (int*)(tmem_slot + 1);  // followed by the epilogue tables
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    if (tid == 0) trace(0);
+    if (tid == 0) { trace(0); trace_cta(0); }
     const int n0 = blockIdx.x * BN, m0 = blockIdx.y * BM;
     const int kblocks = (a.k + BK - 1) / BK;
     const int kper = (kblocks + a.splits - 1) / a.splits;
@@ -468,7 +476,7 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_tc_kernel(const fis_gemm_args
         asm volatile("bar.sync 1, 256;" ::: "memory");
         if (tid == 0) trace(10);
         mbar_wait(done, 0);
-        if (tid == 0) trace(6);
+        if (tid == 0) { trace(6); trace_cta(1); }
         tc_fence_after();
         const int quarter = warp & 3, half = warp >> 2;
         const int lr = quarter * 32 + lane, r = m0 + lr;
@@ -505,6 +513,7 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_tc_kernel(const fis_gemm_args
         // cluster-wide deterministic split-K reduction over DSMEM: CTA z reduces rows
         // [z*rows_per, (z+1)*rows_per) of the tile, summing the S partials in split order.
         asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+        if (tid == 0) trace_cta(2);
         uint32_t rank;
         asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
         const int rows_per = (BM + S - 1) / S;
@@ -536,7 +545,7 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_tc_kernel(const fis_gemm_args
         // keep every CTA's shared memory alive until all peers finished reading it
         asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
     }
-    if (tid == 0) trace(7);
+    if (tid == 0) { trace(7); trace_cta(3); }
 }
 
 template <int BN>
@@ -650,6 +659,10 @@ int fis_gemm_tc_launch(const fis_gemm_args* a, cudaStream_t stream) {
 
 extern "C" int fis_trace(int on) {
     return cudaMemcpyToSymbol(fis::tc::g_trace_on, &on, sizeof(int)) == cudaSuccess ? FIS_OK : FIS_ERR_LAUNCH;
+}
+extern "C" int fis_trace_read_ctas(unsigned long long* out2048) {
+    return cudaMemcpyFromSymbol(out2048, fis::tc::g_trace_cta, 512 * 4 * sizeof(unsigned long long)) == cudaSuccess
+               ? FIS_OK : FIS_ERR_LAUNCH;
 }
 extern "C" int fis_trace_read(unsigned long long* out16) {
     return cudaMemcpyFromSymbol(out16, fis::tc::g_trace, 16 * sizeof(unsigned long long)) == cudaSuccess

@@ -49,3 +49,24 @@ for m, n, k, ldd in shapes:
     ph = ", ".join(f"{nm} +{(buf[i]-t0)/1e3:.2f}" for i, nm in names.items() if buf[i] >= t0)
     print(f"m={m} n={n} k={k}: graph {us:.1f} us/launch ({2*m*n*k/us/1e6:.0f} TFLOP/s, "
           f"B {n*k*2/us/1e3:.0f} GB/s) | {ph}", flush=True)
+
+# per-CTA timelines of a split-K (cluster) launch
+print("--- per-CTA (z, y, x): entry / mma-done / cluster-sync / exit, us from first entry")
+for m, n, k in [(400, 320, 2880), (100, 640, 5760)]:
+    A = torch.randn((m, k), device="cuda", generator=g).to(torch.bfloat16)
+    B = (torch.randn((n, k), device="cuda", generator=g) / math.sqrt(k)).to(torch.bfloat16)
+    D = torch.empty((m, n), device="cuda", dtype=torch.bfloat16)
+    lz.gemm(m, n, k, a=DRef(A), b=DRef(B), d=DRef(D))
+    torch.cuda.synchronize()
+    big = (C.c_ulonglong * 2048)()
+    lib.fis_trace_read_ctas(big)  # clear snapshot
+    lib.fis_trace(1)
+    lz.gemm(m, n, k, a=DRef(A), b=DRef(B), d=DRef(D))
+    torch.cuda.synchronize()
+    lib.fis_trace(0)
+    lib.fis_trace_read_ctas(big)
+    rows = [(i, big[4 * i:4 * i + 4]) for i in range(512) if big[4 * i] > 0]
+    t0 = min(r[1][0] for r in rows)
+    print(f"m={m} n={n} k={k}: {len(rows)} CTAs")
+    for i, r in rows[:48]:
+        print(f"  cta {i:3d}: " + " ".join(f"{(x - t0)/1e3:6.2f}" if x >= t0 else "   -  " for x in r))
