@@ -480,25 +480,36 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_tc_kernel(const fis_gemm_args
         tc_fence_after();
         const int quarter = warp & 3, half = warp >> 2;
         const int lr = quarter * 32 + lane, r = m0 + lr;
-#pragma unroll 1
-        for (int cb = half * (BN / 2); cb < (half + 1) * (BN / 2); cb += 16) {
-            uint32_t u[16];
-            const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) + cb;
+        // all TMEM loads of this thread's row segment first, one wait (latency paid once)
+        constexpr int HC = BN / 2;  // columns per warp half
+        uint32_t u[HC];
+        const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) + half * HC;
+#pragma unroll
+        for (int q = 0; q < HC / 16; q++) {
             asm volatile(
                 "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-                : "=r"(u[0]), "=r"(u[1]), "=r"(u[2]), "=r"(u[3]), "=r"(u[4]), "=r"(u[5]), "=r"(u[6]), "=r"(u[7]),
-                  "=r"(u[8]), "=r"(u[9]), "=r"(u[10]), "=r"(u[11]), "=r"(u[12]), "=r"(u[13]), "=r"(u[14]),
-                  "=r"(u[15])
-                : "r"(taddr));
-            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-            float v[16];
+                : "=r"(u[16 * q + 0]), "=r"(u[16 * q + 1]), "=r"(u[16 * q + 2]), "=r"(u[16 * q + 3]),
+                  "=r"(u[16 * q + 4]), "=r"(u[16 * q + 5]), "=r"(u[16 * q + 6]), "=r"(u[16 * q + 7]),
+                  "=r"(u[16 * q + 8]), "=r"(u[16 * q + 9]), "=r"(u[16 * q + 10]), "=r"(u[16 * q + 11]),
+                  "=r"(u[16 * q + 12]), "=r"(u[16 * q + 13]), "=r"(u[16 * q + 14]), "=r"(u[16 * q + 15])
+                : "r"(taddr + 16 * q));
+        }
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        if (S > 1) {
+            float* p = part + lr * PLD + half * HC;
 #pragma unroll
-            for (int j = 0; j < 16; j++) v[j] = nk > 0 ? __uint_as_float(u[j]) : 0.f;
-            if (S > 1) {
-                float* p = part + lr * PLD + cb;
+            for (int q = 0; q < HC / 4; q++)
+                *(float4*)(p + 4 * q) = nk > 0 ? make_float4(__uint_as_float(u[4 * q]), __uint_as_float(u[4 * q + 1]),
+                                                             __uint_as_float(u[4 * q + 2]), __uint_as_float(u[4 * q + 3]))
+                                               : make_float4(0.f, 0.f, 0.f, 0.f);
+        } else if (r < a.m) {
 #pragma unroll
-                for (int q = 0; q < 4; q++) *(float4*)(p + 4 * q) = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
-            } else if (r < a.m && n0 + cb < a.n) {
+            for (int q = 0; q < HC / 16; q++) {
+                const int cb = half * HC + 16 * q;
+                if (n0 + cb >= a.n) break;
+                float v[16];
+#pragma unroll
+                for (int j = 0; j < 16; j++) v[j] = nk > 0 ? __uint_as_float(u[16 * q + j]) : 0.f;
                 row_epilogue_any(a, e, tb, r, cb, n0, v);
             }
         }
@@ -518,27 +529,44 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_tc_kernel(const fis_gemm_args
         asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
         const int rows_per = (BM + S - 1) / S;
         const int rbeg = (int)rank * rows_per, rend = min(BM, rbeg + rows_per);
-        const int chunks = BN / 16;
         const uint32_t part_s = smem_u32(part);
+        // phase 1: float4 items of the slice; the S remote partials are loaded as one batch and
+        // summed in split order into a local fp32 slice buffer (after this CTA's own partial)
+        float* red = part + BM * PLD;
+        const int q4 = BN / 4;
+        for (int item = tid; item < (rend - rbeg) * q4; item += THREADS) {
+            const int lr = rbeg + item / q4, c4 = (item % q4) * 4;
+            const uint32_t off = (uint32_t)((lr * PLD + c4) * 4);
+            float4 x[16];
+#pragma unroll
+            for (int z = 0; z < 16; z++) {
+                if (z < S) {
+                    uint32_t ra;
+                    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(part_s + off), "r"(z));
+                    asm volatile("ld.shared::cluster.v4.f32 {%0,%1,%2,%3}, [%4];"
+                                 : "=f"(x[z].x), "=f"(x[z].y), "=f"(x[z].z), "=f"(x[z].w) : "r"(ra));
+                }
+            }
+            float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+            for (int z = 0; z < 16; z++) {
+                if (z < S) { acc.x += x[z].x; acc.y += x[z].y; acc.z += x[z].z; acc.w += x[z].w; }
+            }
+            *(float4*)(red + (lr - rbeg) * PLD + c4) = acc;
+        }
+        __syncthreads();
+        // phase 2: fused epilogue of the reduced slice rows, 16-column chunks
+        const int chunks = BN / 16;
         for (int item = tid; item < (rend - rbeg) * chunks; item += THREADS) {
             const int lr = rbeg + item / chunks, cb = (item % chunks) * 16;
             const int r = m0 + lr;
             if (r >= a.m || n0 + cb >= a.n) continue;
-            const uint32_t off = (uint32_t)((lr * PLD + cb) * 4);
             float v[16];
+            const float* p = red + (lr - rbeg) * PLD + cb;
 #pragma unroll
-            for (int j = 0; j < 16; j++) v[j] = 0.f;
-#pragma unroll 1
-            for (int z = 0; z < S; z++) {
-                uint32_t ra;
-                asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(part_s + off), "r"(z));
-#pragma unroll
-                for (int q = 0; q < 4; q++) {
-                    float x0, x1, x2, x3;
-                    asm volatile("ld.shared::cluster.v4.f32 {%0,%1,%2,%3}, [%4];"
-                                 : "=f"(x0), "=f"(x1), "=f"(x2), "=f"(x3) : "r"(ra + 16 * q));
-                    v[4 * q] += x0; v[4 * q + 1] += x1; v[4 * q + 2] += x2; v[4 * q + 3] += x3;
-                }
+            for (int q = 0; q < 4; q++) {
+                const float4 f = *(const float4*)(p + 4 * q);
+                v[4 * q] = f.x; v[4 * q + 1] = f.y; v[4 * q + 2] = f.z; v[4 * q + 3] = f.w;
             }
             row_epilogue_any(a, e, tb, r, cb, n0, v);
         }
