@@ -173,6 +173,24 @@ typedef struct {
 } fis_xattn_args;
 int fis_xattn(const fis_xattn_args* a, void* stream);
 
+/* Fused tensor-core attention (tcgen05): out = res + softmax(Q K^T * scale) V for one query
+ * tile of 128 rows x one output-channel slice per CTA; S and the O slice accumulate in TMEM,
+ * P goes through a swizzled shared-memory tile into the P.V MMA. Replaces attention_scores +
+ * apply_attention + the residual add for self- and cross-attention (sparse.py:265-361,
+ * tensors.py:183-200, unet.py:456-457).  bf16 Q/K/V^T, d % 64 == 0. */
+typedef struct {
+    int m, n_keys, d, dv;   /* queries, keys, head dim (= reduction dim of Q K^T), value dim */
+    fis_ref q;              /* [m, ld] */
+    fis_ref k;              /* [n_keys, ld] */
+    fis_ref vt;             /* [dv, ld]: V transposed (keys contiguous) */
+    float scale;
+    fis_ref res;            /* [m, ld] residual (may be NULL) */
+    fis_ref pre;            /* optional store of the attention output before the residual */
+    fis_ref out;            /* [m, ld] */
+    const int* step;
+} fis_attn_args;
+int fis_attn(const fis_attn_args* a, void* stream);
+
 /* 2x2 average pool with select-on-read of the finer map (unet.py:296-298).
  * Output rows are coarse pixels rows[i] (NULL => all (h/2)*(w/2)). */
 typedef struct {

@@ -65,6 +65,11 @@ class XattnArgs(C.Structure):
                 ("scale", C.c_float), ("res", Ref), ("pre", Ref), ("out", Ref), ("step", C.c_void_p)]
 
 
+class AttnArgs(C.Structure):
+    _fields_ = [("m", C.c_int), ("n_keys", C.c_int), ("d", C.c_int), ("dv", C.c_int), ("q", Ref), ("k", Ref),
+                ("vt", Ref), ("scale", C.c_float), ("res", Ref), ("pre", Ref), ("out", Ref), ("step", C.c_void_p)]
+
+
 class PoolArgs(C.Structure):
     _fields_ = [("n", C.c_int), ("c", C.c_int), ("src", Src), ("rows", C.c_void_p), ("out", Ref),
                 ("step", C.c_void_p)]
@@ -88,7 +93,7 @@ class MaskPlanArgs(C.Structure):
 
 
 _SIGS = {
-    "fis_gemm": GemmArgs, "fis_xattn": XattnArgs, "fis_gn_stats": GnStatsArgs, "fis_gn_apply": GnApplyArgs, "fis_softmax": SoftmaxArgs,
+    "fis_gemm": GemmArgs, "fis_attn": AttnArgs, "fis_xattn": XattnArgs, "fis_gn_stats": GnStatsArgs, "fis_gn_apply": GnApplyArgs, "fis_softmax": SoftmaxArgs,
     "fis_pool2": PoolArgs, "fis_materialize": MaterializeArgs, "fis_mask_detect": MaskDetectArgs,
     "fis_mask_plan": MaskPlanArgs,
 }

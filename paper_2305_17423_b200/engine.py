@@ -117,7 +117,8 @@ class Launcher:
         self._counters = torch.zeros(1 << 16, dtype=torch.int32, device=self.dev)
         self.launches = 0
         self._scratch = {}
-        self.fused_xattn = False  # SIMT xattn is latency-bound; GEMM path until a tcgen05 version lands
+        self.fused_xattn = False  # SIMT xattn is latency-bound; superseded by fis_attn
+        self.fused_attn = True    # tcgen05 fused attention (bf16 mode)
         # gather lists (rows / pixel->row maps) are written once per edit, before any step runs
         # (DevicePlan syncs), so GEMMs may read them before the programmatic-launch wait
         self.static_meta = False
@@ -266,6 +267,10 @@ class Engine(Launcher):
         # one GEMM for Q|K (row-major) and V (stored transposed as the PV B operand)
         self.gemm(m, 3 * c, c, a=s, b=DRef(wqkv), d=DRef(qk), n_split=2 * c, d2=DRef(vt, ld=mp), d2_trans=True)
         qkr = DRef(qk)
+        if self.use_fused_attn(c):
+            # S = QK^T, softmax and P.V (+ residual) in one tcgen05 kernel (fis_attn)
+            self.attn(m, m, c, qkr, qkr.cols(c), DRef(vt, ld=mp), scale, s, y1, pre)
+            return
         self.gemm(m, m, c, a=qkr, b=qkr.cols(c), d=DRef(S, ld=_pad(m)))
         self.softmax(m, m, _pad(m), DRef(S, ld=_pad(m)), scale, DRef(P, ld=_pad(m)))
         self.gemm(m, c, m, a=DRef(P, ld=_pad(m)), b=DRef(vt, ld=mp), d=y1, res=s, pre=pre)
@@ -286,6 +291,9 @@ class Engine(Launcher):
             L.call("fis_xattn", a)
             self.launches += 1
             return
+        if ctrl is None and map_ is None and self.use_fused_attn(c):
+            self.attn(m, nt, c, DRef(q), DRef(k), DRef(vt), scale, x, out, pre)
+            return
         S = self.scratch(f"Sx{tag}", (cap, ntp), torch.float32)  # ld padded: 16-byte aligned rows
         P = self.scratch(f"Px{tag}", (cap, ntp), zero=True)
         self.gemm(m, nt, c, a=DRef(q), b=DRef(k), d=DRef(S))
@@ -295,6 +303,15 @@ class Engine(Launcher):
         else:
             self.softmax(m, nt, ntp, DRef(S), scale, DRef(P), map_)
         self.gemm(m, c, ntp, a=DRef(P), b=DRef(vt), d=out, res=x, pre=pre)
+
+    def use_fused_attn(self, d):
+        return self.fused_attn and self.act == torch.bfloat16 and d % 64 == 0
+
+    def attn(self, m, n_keys, d, q: DRef, k: DRef, vt: DRef, scale, res: DRef, out: DRef, pre=None):
+        a = L.AttnArgs(m, n_keys, d, d, q.ref(), k.ref(), vt.ref(), float(scale), _r(res), _r(pre), out.ref(),
+                       L.ptr(self.step_dev))
+        L.call("fis_attn", a)
+        self.launches += 1
 
     def gn_stats(self, x: DRef, hw, c, mean: DRef, var: DRef):
         a = L.GnStatsArgs(hw, c, self.groups, x.ref(), mean.ref(), var.ref(), L.ptr(self.step_dev))

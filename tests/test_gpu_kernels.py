@@ -123,3 +123,29 @@ def test_transposed_store_and_residual(env):
         D = torch.zeros((m, n), device="cuda")
         _run(env, impl, m, n, k, a=DRef(A), b=DRef(B), d=DRef(D), res=DRef(res))
         assert (D - (ref + res.float())).abs().max().item() <= 3e-2
+
+
+@pytest.mark.parametrize("m,nk,d", [(400, 400, 320), (100, 100, 640), (256, 256, 1280), (64, 64, 1280),
+                                    (400, 77, 320), (1024, 1024, 320), (37, 5, 64), (300, 129, 128)])
+def test_fused_attention_vs_torch(env, m, nk, d):
+    """fis_attn (tcgen05 S=QK^T, softmax, P.V, + residual) against torch fp32 on the same bf16 inputs."""
+    L, DRef, NULL, lz = env
+    g = torch.Generator(device="cuda").manual_seed(m + nk + d)
+    bf = torch.bfloat16
+    Q = torch.randn((m, d), device="cuda", generator=g).to(bf)
+    K = torch.randn((nk, d), device="cuda", generator=g).to(bf)
+    V = torch.randn((nk, d), device="cuda", generator=g).to(bf)
+    ldv = (nk + 15) // 16 * 16
+    Vt = torch.zeros((d, ldv), device="cuda", dtype=bf)
+    Vt[:, :nk] = V.t()
+    res = torch.randn((m, d), device="cuda", generator=g).to(bf)
+    scale = 1.0 / math.sqrt(d)
+    P = torch.softmax(Q.float() @ K.float().t() * scale, dim=1)
+    ref = P @ V.float() + res.float()
+    out = torch.full((m, d), float("nan"), device="cuda", dtype=bf)
+    a = L.AttnArgs(m, nk, d, d, DRef(Q).ref(), DRef(K).ref(), DRef(Vt, ld=ldv).ref(), scale, DRef(res).ref(), NULL,
+                   DRef(out).ref(), None)
+    L.call("fis_attn", a)
+    torch.cuda.synchronize()
+    err = (out.float() - ref).abs().max().item()
+    assert err <= 3e-2 * max(1.0, ref.abs().max().item()), err
