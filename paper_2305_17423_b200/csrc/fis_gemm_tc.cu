@@ -17,56 +17,12 @@
 // split order (bitwise deterministic). The A gather cannot use TMA tiles: rows are
 // scattered active pixels whose halo reads select between the fresh compact buffer
 // and the step's cache slab per pixel.
-#include "fis_common.cuh"
-#include <climits>
+#include "fis_tc.cuh"
 
 namespace fis {
 namespace tc {
 
-constexpr int BM = 128, BK = 64, STAGES = 4, PRODUCERS = 256, THREADS = 288, MMA_WARP = 8;
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-
-__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count));
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
-    asm volatile(
-        "{\n"
-        ".reg .pred p;\n"
-        "WAIT_%=:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-        "@!p bra WAIT_%=;\n"
-        "}\n" ::"r"(smem_u32(b)),
-        "r"(parity)
-        : "memory");
-}
-__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, bool valid) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(valid ? 16 : 0) : "memory");
-}
-__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void cp_async_arrive_noinc(uint64_t* b) {
-    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(b)) : "memory");
-}
-template <int N>
-__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
-__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
-__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
-__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
-
-// K-major, 128B-swizzled UMMA shared-memory descriptor (LBO=16B, SBO=1024B, version 1)
-__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
-    return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
-           ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
-}
-
-// byte offset of 16B chunk j of row r inside a SW128 K-major tile (rows of 128 B)
-__device__ __forceinline__ uint32_t sw128_off(int r, int j) {
-    return (uint32_t)((r >> 3) * 1024 + (r & 7) * 128 + ((j ^ (r & 7)) << 4));
-}
+constexpr int STAGES = 4, PRODUCERS = 256, THREADS = 288, MMA_WARP = 8;
 
 template <int BN>
 struct Smem {
@@ -77,192 +33,6 @@ struct Smem {
     static constexpr int SEL = BM * 2 * 9 * 4;  // per-row, per-segment, per-tap select-on-read table
     static constexpr int TOTAL = STAGES * STAGE + 1024 /*align*/ + 256 /*barriers*/ + EPI + SEL + 16;
 };
-
-// Per-column epilogue parameters of this CTA's BN columns, staged once in shared memory.
-struct EpiTab {
-    float* bias; float* b2; float* gamma; float* beta; double* mean; double* rstd;
-};
-
-__device__ __forceinline__ void load_row16(const char* base, int dtype, long long off, int nvalid, float* v) {
-    if (dtype == FIS_BF16) {
-        const __nv_bfloat16* p = (const __nv_bfloat16*)base + off;
-        if (nvalid == 16 && ((uintptr_t)p & 15) == 0) {
-#pragma unroll
-            for (int q = 0; q < 2; q++) {
-                uint4 u = *(const uint4*)(p + 8 * q);
-                const __nv_bfloat162* h = (const __nv_bfloat162*)&u;
-#pragma unroll
-                for (int k = 0; k < 4; k++) {
-                    float2 f = __bfloat1622float2(h[k]);
-                    v[8 * q + 2 * k] = f.x;
-                    v[8 * q + 2 * k + 1] = f.y;
-                }
-            }
-        } else {
-#pragma unroll
-            for (int j = 0; j < 16; j++) if (j < nvalid) v[j] = __bfloat162float(p[j]);
-        }
-    } else {
-        const float* p = (const float*)base + off;
-        if (nvalid == 16 && ((uintptr_t)p & 15) == 0) {
-#pragma unroll
-            for (int q = 0; q < 4; q++) {
-                float4 f = *(const float4*)(p + 4 * q);
-                v[4 * q] = f.x; v[4 * q + 1] = f.y; v[4 * q + 2] = f.z; v[4 * q + 3] = f.w;
-            }
-        } else {
-#pragma unroll
-            for (int j = 0; j < 16; j++) if (j < nvalid) v[j] = p[j];
-        }
-    }
-}
-
-__device__ __forceinline__ void store_row16(char* base, int dtype, long long off, int nvalid, const float* v) {
-    if (dtype == FIS_BF16) {
-        __nv_bfloat16* p = (__nv_bfloat16*)base + off;
-        if (nvalid == 16 && ((uintptr_t)p & 15) == 0) {
-#pragma unroll
-            for (int q = 0; q < 2; q++) {
-                uint4 u;
-                __nv_bfloat162* h = (__nv_bfloat162*)&u;
-#pragma unroll
-                for (int k = 0; k < 4; k++) h[k] = __floats2bfloat162_rn(v[8 * q + 2 * k], v[8 * q + 2 * k + 1]);
-                *(uint4*)(p + 8 * q) = u;
-            }
-        } else {
-#pragma unroll
-            for (int j = 0; j < 16; j++) if (j < nvalid) p[j] = __float2bfloat16_rn(v[j]);
-        }
-    } else {
-        float* p = (float*)base + off;
-        if (nvalid == 16 && ((uintptr_t)p & 15) == 0) {
-#pragma unroll
-            for (int q = 0; q < 4; q++) *(float4*)(p + 4 * q) = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
-        } else {
-#pragma unroll
-            for (int j = 0; j < 16; j++) if (j < nvalid) p[j] = v[j];
-        }
-    }
-}
-
-// Fused epilogue of one 16-column chunk of one output row (v holds the fp32 accumulators).
-// Same arithmetic, in the same order, as fis::epilogue_store (fis_common.cuh).
-template <int MODE>
-__device__ __forceinline__ void row_epilogue(const fis_gemm_args& a, const EpiCtx& e, const EpiTab& tb, int r,
-                                             int c0, int n0, float* v) {
-    const int n = n0 + c0;
-    const int nvalid = min(16, a.n - n);
-    if (nvalid <= 0) return;
-    const int orow = a.d_rows ? __ldg(a.d_rows + r) : r;
-#pragma unroll
-    for (int j = 0; j < 16; j++) v[j] = __fadd_rn(v[j] * a.alpha, tb.bias[c0 + j]);
-    if (e.pre) store_row16(e.pre, a.pre.dtype, (long long)orow * a.pre.ld + n, nvalid, v);
-    if (e.bias2) {
-#pragma unroll
-        for (int j = 0; j < 16; j++) v[j] = __fadd_rn(v[j], tb.b2[c0 + j]);
-    }
-    if (MODE == FIS_EPI_GN_SILU) {
-        float y[16];
-#pragma unroll
-        for (int j = 0; j < 16; j++)
-            y[j] = (float)(((double)v[j] - tb.mean[c0 + j]) * tb.rstd[c0 + j] * (double)tb.gamma[c0 + j] +
-                           (double)tb.beta[c0 + j]);
-        if (e.pre2) store_row16(e.pre2, a.pre2.dtype, (long long)orow * a.pre2.ld + n, nvalid, y);
-#pragma unroll
-        for (int j = 0; j < 16; j++) {
-            const double yd = (double)y[j];
-            v[j] = (float)(yd / (1.0 + exp(-yd)));
-        }
-    } else if (MODE == FIS_EPI_STEP) {
-        float l[16];
-        load_row16(e.lat, a.lat.dtype, (long long)orow * a.lat.ld + n, nvalid, l);
-#pragma unroll
-        for (int j = 0; j < 16; j++) v[j] = __fsub_rn(l[j], __fmul_rn(a.step_scale, v[j]));
-    }
-    if (e.res) {
-        float q[16];
-        load_row16(e.res, a.res.dtype, (long long)orow * a.res.ld + n, nvalid, q);
-#pragma unroll
-        for (int j = 0; j < 16; j++) v[j] = __fadd_rn(v[j], q[j]);
-    }
-    char* dbase = e.d;
-    int dt = a.d.dtype, dld = a.d.ld, dn = n, trans = a.d_trans;
-    if (a.n_split > 0 && n >= a.n_split) {  // fused QKV: V part goes transposed to d2
-        dbase = e.d2; dt = a.d2.dtype; dld = a.d2.ld; dn = n - a.n_split; trans = a.d2_trans;
-    }
-    if (trans) {
-#pragma unroll
-        for (int j = 0; j < 16; j++)
-            if (j < nvalid) store_elem(dbase, dt, (long long)(dn + j) * dld + orow, v[j]);
-    } else {
-        store_row16(dbase, dt, (long long)orow * dld + dn, nvalid, v);
-    }
-}
-
-__device__ __forceinline__ void row_epilogue_any(const fis_gemm_args& a, const EpiCtx& e, const EpiTab& tb, int r,
-                                                 int c0, int n0, float* v) {
-    if (a.epi == FIS_EPI_GN_SILU) row_epilogue<FIS_EPI_GN_SILU>(a, e, tb, r, c0, n0, v);
-    else if (a.epi == FIS_EPI_STEP) row_epilogue<FIS_EPI_STEP>(a, e, tb, r, c0, n0, v);
-    else row_epilogue<FIS_EPI_NONE>(a, e, tb, r, c0, n0, v);
-}
-
-// Per-row gather geometry, computed once per CTA: the row's pixel p (ROWS: A row) and,
-// for CONV, its (y, x); valid=false rows (beyond M) load zeros.
-struct RowGeo {
-    int p, oy, ox;
-    bool valid;
-};
-
-constexpr int SEL_ZERO = INT_MIN;
-
-// Select-on-read decisions of one output row for every 3x3 tap of source segment `seg`:
-// >= 0 fresh row (or full-map pixel), <= -2 cache pixel (-2 - q), SEL_ZERO = zero padding.
-__device__ __forceinline__ void build_sel(const fis_gemm_args& a, int p, int seg, int* out9) {
-    const fis_src& s = a.src[seg];
-    const int oy = p / a.out_w, ox = p - (p / a.out_w) * a.out_w;
-#pragma unroll
-    for (int tap = 0; tap < 9; tap++) {
-        const int y = oy + tap / 3 - 1, x = ox + tap % 3 - 1;
-        int v = SEL_ZERO;
-        if (y >= 0 && x >= 0 && y < a.out_h && x < a.out_w) {
-            const int q = (s.up ? (y >> 1) : y) * s.w + (s.up ? (x >> 1) : x);
-            if (s.index) {
-                const int i = __ldg(s.index + q);
-                v = i >= 0 ? i : -2 - q;
-            } else {
-                v = q;
-            }
-        }
-        out9[tap] = v;
-    }
-}
-
-// Source pointer of the 64-channel K block starting at k0 for one GEMM row (16 B granularity),
-// or nullptr for zero (padding / out of image / beyond K). tap/c/segment are uniform per block.
-__device__ __forceinline__ const char* a_block_ptr(const fis_gemm_args& a, const char* abase, const char* f0,
-                                                   const char* c0p, const char* f1, const char* c1p,
-                                                   const RowGeo& g, int k0, int tap, int c) {
-    if (!g.valid) return nullptr;
-    if (a.a_mode == FIS_A_ROWS) {
-        if (k0 >= a.k) return nullptr;
-        return abase + ((long long)g.p * a.a.ld + k0) * 2;
-    }
-    const int y = g.oy + tap / 3 - 1, x = g.ox + tap % 3 - 1;
-    if (y < 0 || x < 0 || y >= a.out_h || x >= a.out_w) return nullptr;
-    const bool second = c >= a.src[0].c;
-    const fis_src& s = second ? a.src[1] : a.src[0];
-    if (second) c -= a.src[0].c;
-    const int sy = s.up ? (y >> 1) : y, sx = s.up ? (x >> 1) : x;
-    const int q = sy * s.w + sx;
-    const char* fr = second ? f1 : f0;
-    const char* ca = second ? c1p : c0p;
-    if (s.index) {
-        const int i = __ldg(s.index + q);
-        if (i >= 0) return fr + ((long long)i * s.fresh.ld + c) * 2;
-        return ca + ((long long)q * s.cache.ld + c) * 2;
-    }
-    return fr + ((long long)q * s.fresh.ld + c) * 2;
-}
 
 // Phase timestamps (%globaltimer, ns) of CTA (0,0,0) for profiling the fixed per-launch cost;
 // enabled with fis_trace(1), read with fis_trace_read().

@@ -118,7 +118,7 @@ class Launcher:
         self.launches = 0
         self._scratch = {}
         self.fused_xattn = False  # SIMT xattn is latency-bound; superseded by fis_attn
-        self.fused_attn = True    # tcgen05 fused attention (bf16 mode)
+        self.fused_attn = False   # tcgen05 fused attention: one CTA per 128 queries is latency-bound (r01: 2.35 vs 1.63 ms/step)
         # gather lists (rows / pixel->row maps) are written once per edit, before any step runs
         # (DevicePlan syncs), so GEMMs may read them before the programmatic-launch wait
         self.static_meta = False
