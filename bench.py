@@ -192,9 +192,8 @@ def run_ours(args):
     ep = U.EditPlan(eng, arena, mask, kv, lat0)
     runner = U._Runner(eng, ep.plan, True)
     T = cfg.steps
-    n0 = eng.launches
-    runner.step(1)  # eager warm step + graph capture of one step
-    per_step_launches = (eng.launches - n0) // 2  # kernels in the captured step graph
+    runner.step(1)  # records the step (VM program) or warms + captures a CUDA graph
+    per_step_launches = runner.launches_per_step  # our kernels per step (1 = the step VM)
     for i in range(args.warmup):
         runner.step(1 + (i + 1) % T)
     torch.cuda.synchronize()

@@ -214,7 +214,7 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_tc_kernel(const fis_gemm_args
     {
         unsigned char* ep = (unsigned char*)(last_flag + 4);
         ep = (unsigned char*)(((uintptr_t)ep + 15) & ~(uintptr_t)15);
-        tb.mean = (double*)ep;
+        tb.mean = (float*)ep;
         tb.rstd = tb.mean + BN;
         tb.bias = (float*)(tb.rstd + BN);
         tb.b2 = tb.bias + BN;
@@ -235,12 +235,12 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_tc_kernel(const fis_gemm_args
             tb.b2[c] = ok && e.bias2 ? load_elem(e.bias2, a.bias2.dtype, n) : 0.f;
             if (a.epi == FIS_EPI_GN_SILU && ok) {
                 const int g = n / e.cpg;
-                tb.mean[c] = (double)e.mean[g];
-                tb.rstd[c] = 1.0 / sqrt((double)e.var[g] + (double)a.eps);
+                tb.mean[c] = e.mean[g];
+                tb.rstd[c] = (float)(1.0 / sqrt((double)e.var[g] + (double)a.eps));
                 tb.gamma[c] = __ldg(a.gamma + n);
                 tb.beta[c] = __ldg(a.beta + n);
             } else {
-                tb.mean[c] = 0.0; tb.rstd[c] = 0.0; tb.gamma[c] = 0.f; tb.beta[c] = 0.f;
+                tb.mean[c] = 0.f; tb.rstd[c] = 0.f; tb.gamma[c] = 0.f; tb.beta[c] = 0.f;
             }
         }
         asm volatile("bar.sync 1, 256;" ::: "memory");

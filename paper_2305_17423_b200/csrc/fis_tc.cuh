@@ -55,7 +55,7 @@ __device__ __forceinline__ uint32_t sw128_off(int r, int j) {
 
 // Per-column epilogue parameters of this CTA's BN columns, staged once in shared memory.
 struct EpiTab {
-    float* bias; float* b2; float* gamma; float* beta; double* mean; double* rstd;
+    float* bias; float* b2; float* gamma; float* beta; float* mean; float* rstd;
 };
 
 __device__ __forceinline__ void load_row16(const char* base, int dtype, long long off, int nvalid, float* v) {
@@ -139,15 +139,13 @@ __device__ __forceinline__ void row_epilogue(const fis_gemm_args& a, const EpiCt
     if (MODE == FIS_EPI_GN_SILU) {
         float y[16];
 #pragma unroll
+        // bf16 tensor-core path: cached-stat GN + SiLU in fp32 (the fp32-parity SIMT path,
+        // epilogue_store, keeps the reference's f64 arithmetic)
         for (int j = 0; j < 16; j++)
-            y[j] = (float)(((double)v[j] - tb.mean[c0 + j]) * tb.rstd[c0 + j] * (double)tb.gamma[c0 + j] +
-                           (double)tb.beta[c0 + j]);
+            y[j] = fmaf((v[j] - tb.mean[c0 + j]) * tb.rstd[c0 + j], tb.gamma[c0 + j], tb.beta[c0 + j]);
         if (e.pre2) store_row16(e.pre2, a.pre2.dtype, (long long)orow * a.pre2.ld + n, nvalid, y);
 #pragma unroll
-        for (int j = 0; j < 16; j++) {
-            const double yd = (double)y[j];
-            v[j] = (float)(yd / (1.0 + exp(-yd)));
-        }
+        for (int j = 0; j < 16; j++) v[j] = __fdividef(y[j], 1.0f + __expf(-y[j]));
     } else if (MODE == FIS_EPI_STEP) {
         float l[16];
         load_row16(e.lat, a.lat.dtype, (long long)orow * a.lat.ld + n, nvalid, l);

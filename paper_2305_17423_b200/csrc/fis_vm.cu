@@ -1,0 +1,1203 @@
+// Persistent step VM for sm_100a: one CTA per SM runs a whole recorded UNet step.
+//
+// The host records the launches of one step (Engine.run_step in capture mode) as a list of
+// fis_vm_op records; fis_vm_plan tiles them and fis_vm_run executes them in ONE launch:
+//
+//   op j, item i  ->  CTA (cta0_j + i) mod G          (cta0 rotates from op to op)
+//   an item of op j waits until op dep_j (the previous non-empty op) has completed all of
+//   its items (a device-scope counter per op, release/acquire), so the step's ~100 ops run
+//   back to back with no launch gap, no per-kernel prologue (barrier init, TMEM alloc) and
+//   no tail; a CTA whose next item is a GEMM stages that item's weight (B) tiles into its
+//   shared-memory ring BEFORE the dependency resolves — weights do not depend on the
+//   previous op — so the weight stream of op j+1 overlaps op j.
+//
+// Warp roles (288 threads) as in the per-op tcgen05 GEMM (fis_gemm_tc.cu):
+//   warps 0-7 : producers (A gather with select-on-read, B weight rows; 16-byte cp.async into
+//               SW128 K-major stages) and the epilogue (tcgen05.ld -> fused row epilogue);
+//               they also run the SIMT ops (softmax, GN stats/apply, pool, SIMT GEMM).
+//   warp 8    : MMA issuer; walks the same op list and consumes the smem ring.
+// The ring, its phase and the TMEM accumulator persist across items and ops.
+// Split-K partials go to a workspace; the last-arriving CTA of a tile sums them in split
+// order (bitwise deterministic) and runs the epilogue.
+#include "fis_tc.cuh"
+
+namespace fis {
+namespace vm {
+using namespace fis::tc;
+
+constexpr int STAGES = 5, PRODUCERS = 256, THREADS = 288, MMA_WARP = 8;
+constexpr int MAX_BN = 128;
+constexpr int A_BYTES = BM * BK * 2;
+constexpr int B_BYTES = MAX_BN * BK * 2;
+constexpr int STAGE = A_BYTES + B_BYTES;
+constexpr int OPBUF = 1024;
+constexpr int EPI = MAX_BN * 32;
+constexpr int SEL = BM * 2 * 9 * 4;
+constexpr int RES_LD = 272;                  // bytes per staged residual row (<= 256 B of data)
+constexpr int RES_BYTES = BM * RES_LD;       // epilogue operand tile (residual / latent rows)
+constexpr int SMEM = STAGES * STAGE + RES_BYTES + 1024;  // dynamic: ring + operand tile (+ alignment slack)
+constexpr int ELEMS_PER_ITEM = 2048;  // elementwise ops
+constexpr int SOFTMAX_ROWS = 8;       // one warp per row
+constexpr int SBM = 64, SBN = 64, SBK = 16;  // SIMT GEMM tile
+
+static_assert(sizeof(fis_vm_op) <= OPBUF, "fis_vm_op must fit the shared op buffer");
+
+FIS_DEV void pbar() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
+
+// the step index of this launch (read once per CTA from fis_vm_args.step)
+__shared__ int s_step;
+
+FIS_DEV int ld_acquire(const int* p) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+struct Shared {
+    unsigned char* ring;
+    unsigned char* res;  // staged epilogue operand rows [BM][RES_LD]
+    fis_vm_op* op;
+    EpiTab tb;
+    int* seltab;
+    uint64_t* full;
+    uint64_t* empty;
+    uint64_t* done;
+    uint32_t* tmem_slot;
+    int* flag;
+};
+
+// Shared-memory layout: the ring (dynamic, 1024-aligned) and static shared objects, so every
+// pointer below stays in the shared address space (LDS/STS, no generic loads, no aliasing
+// with global stores).
+extern __shared__ __align__(1024) unsigned char vm_smem[];
+__shared__ __align__(16) fis_vm_op s_op;
+__shared__ float s_tab[6][MAX_BN];
+__shared__ int s_sel[BM * 2 * 9];
+__shared__ __align__(8) uint64_t s_bar[2 * STAGES + 1];
+__shared__ uint32_t s_tmem;
+__shared__ int s_flag;
+
+FIS_DEV Shared carve() {
+    Shared s;
+    const uint32_t a = smem_u32(vm_smem);
+    s.ring = vm_smem + ((1024u - (a & 1023u)) & 1023u);
+    s.res = s.ring + STAGES * STAGE;
+    s.op = &s_op;
+    s.tb.mean = s_tab[0];
+    s.tb.rstd = s_tab[1];
+    s.tb.bias = s_tab[2];
+    s.tb.b2 = s_tab[3];
+    s.tb.gamma = s_tab[4];
+    s.tb.beta = s_tab[5];
+    s.seltab = s_sel;
+    s.full = s_bar;
+    s.empty = s_bar + STAGES;
+    s.done = s_bar + 2 * STAGES;
+    s.tmem_slot = &s_tmem;
+    s.flag = &s_flag;
+    return s;
+}
+
+// ---------------------------------------------------------------------------------- GEMM geometry
+struct GemmItem {
+    int z, tile, n0, m0, kb0, nk, bn;
+};
+
+FIS_DEV GemmItem gemm_item(const fis_vm_op& op, int i) {
+    GemmItem g;
+    const int S = op.splits;
+    g.z = i % S;
+    g.tile = i / S;
+    const int tn = g.tile % op.tiles_n, tm = g.tile / op.tiles_n;
+    g.bn = op.bn;
+    g.n0 = tn * op.bn;
+    g.m0 = tm * BM;
+    const int kblocks = (op.u.gemm.k + BK - 1) / BK;
+    const int per = (kblocks + S - 1) / S;
+    g.kb0 = g.z * per;
+    g.nk = max(0, min(kblocks, g.kb0 + per) - g.kb0);
+    return g;
+}
+
+// ---------------------------------------------------------------------------------- MMA warp
+FIS_DEV void mma_role(const fis_vm_args& va, const Shared& sh, uint32_t tmem, int lane) {
+    const int G = gridDim.x, cta = blockIdx.x;
+    uint32_t it = 0;
+    const uint32_t sbase = smem_u32(sh.ring);
+    for (int j = 0; j < va.n_ops; j++) {
+        const fis_vm_op* op = va.ops + j;
+        if (op->kind != FIS_VM_GEMM || op->impl != 2) continue;
+        const int n_items = op->n_items;
+        for (int i = (cta - op->cta0 + G) % G; i < n_items; i += G) {
+            const GemmItem g = gemm_item(*op, i);
+            const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(g.bn >> 3) << 17) |
+                                   ((uint32_t)(BM >> 4) << 24);
+            for (int q = 0; q < g.nk; q++, it++) {
+                const int s = it % STAGES;
+                mbar_wait(sh.full + s, (it / STAGES) & 1);
+                tc_fence_after();
+                if (lane == 0) {
+                    const uint32_t sa = sbase + s * STAGE, sb = sa + A_BYTES;
+#pragma unroll
+                    for (int kk = 0; kk < BK / 16; kk++) {
+                        const uint64_t ad = sw128_desc(sa + kk * 32), bd = sw128_desc(sb + kk * 32);
+                        const uint32_t acc = (q > 0 || kk > 0) ? 1u : 0u;
+                        asm volatile(
+                            "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+                            "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem),
+                            "l"(ad), "l"(bd), "r"(idesc), "r"(acc));
+                    }
+                    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                                     smem_u32(sh.empty + s))
+                                 : "memory");
+                }
+                __syncwarp();
+            }
+            if (lane == 0)
+                asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                                 smem_u32(sh.done))
+                             : "memory");
+            __syncwarp();
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------------- producers
+FIS_DEV void tmem_ld16(uint32_t taddr, float* v) {
+    uint32_t u[16];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(u[0]), "=r"(u[1]), "=r"(u[2]), "=r"(u[3]), "=r"(u[4]), "=r"(u[5]), "=r"(u[6]), "=r"(u[7]),
+          "=r"(u[8]), "=r"(u[9]), "=r"(u[10]), "=r"(u[11]), "=r"(u[12]), "=r"(u[13]), "=r"(u[14]), "=r"(u[15])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int j = 0; j < 16; j++) v[j] = __uint_as_float(u[j]);
+}
+
+struct ProdState {
+    uint32_t it;      // ring slot sequence number (matches the MMA warp)
+    uint32_t items;   // tcgen05 GEMM items run (parity of the done barrier)
+};
+
+FIS_DEV unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+// phase stamp of item i of the traced op (profiling; fis_vm_args.trace_op / trace_items)
+#define VM_STAMP(slot)                                                                   \
+    do {                                                                                 \
+        if (va.trace_items && j == va.trace_op && tid == 0) va.trace_items[16 * i + (slot)] = gtimer(); \
+    } while (0)
+
+FIS_DEV void trace_start(const fis_vm_args& va, int j, int tid) {
+    if (va.trace && tid == 0) atomicMin(va.trace + 2 * j, gtimer());
+}
+
+// Wait (once per op) until op.dep has completed. Relaxed polling (no per-poll L1
+// invalidation), then one gpu-scope fence: acquire + this SM's L1 invalidated once.
+FIS_DEV int ld_relaxed(const int* p) {
+    int v;
+    asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+FIS_DEV void fence_acq_rel() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+
+FIS_DEV void spin_until(const int* c, int target, int ns) {
+    while (ld_relaxed(c) < target) __nanosleep(ns);
+    fence_acq_rel();
+}
+
+FIS_DEV void wait_dep(const fis_vm_args& va, const fis_vm_op& op, int j, bool& waited, int tid) {
+    if (waited) return;
+    waited = true;
+    if (op.dep < 0) {
+        trace_start(va, j, tid);
+        return;
+    }
+    if (tid == 0) spin_until(va.sync + 1 + op.dep, op.dep_target, va.poll_ns > 0 ? va.poll_ns : 32);
+    trace_start(va, j, tid);
+    pbar();
+}
+
+FIS_DEV void signal_done(const fis_vm_args& va, int j, int tid) {
+    pbar();
+    if (tid == 0) {
+        fence_acq_rel();
+        atomicAdd(va.sync + 1 + j, 1);
+        if (va.trace) atomicMax(va.trace + 2 * j + 1, gtimer());
+    }
+}
+
+FIS_DEV void issue_b(const fis_gemm_args& a, const GemmItem& g, const char* bbase, uint32_t sb, int k0, int ar,
+                     int j0) {
+    if (ar >= g.bn) return;
+    const int bn = g.n0 + ar;
+    const char* brow = bbase + (long long)bn * a.b.ld * 2;
+#pragma unroll
+    for (int j = j0; j < j0 + 4; j++) {
+        const bool ok = bn < a.n && k0 + j * 8 < a.k;
+        cp_async16(sb + sw128_off(ar, j), ok ? (const void*)(brow + (k0 + j * 8) * 2) : (const void*)bbase, ok);
+    }
+}
+
+// Per-column epilogue parameters of the tile (bias, time bias, cached GN stats, gamma/beta).
+FIS_DEV void stage_tables(const fis_gemm_args& a, const EpiCtx& e, const Shared& sh, int n0, int bn, int tid) {
+    for (int c = tid; c < bn; c += PRODUCERS) {
+        const int n = n0 + c;
+        const bool ok = n < a.n;
+        sh.tb.bias[c] = ok && a.bias ? __ldg(a.bias + n) : 0.f;
+        sh.tb.b2[c] = ok && e.bias2 ? load_elem(e.bias2, a.bias2.dtype, n) : 0.f;
+        if (a.epi == FIS_EPI_GN_SILU && ok) {
+            const int gi = n / e.cpg;
+            sh.tb.mean[c] = e.mean[gi];
+            sh.tb.rstd[c] = (float)(1.0 / sqrt((double)e.var[gi] + (double)a.eps));
+            sh.tb.gamma[c] = __ldg(a.gamma + n);
+            sh.tb.beta[c] = __ldg(a.beta + n);
+        } else {
+            sh.tb.mean[c] = 0.f; sh.tb.rstd[c] = 0.f; sh.tb.gamma[c] = 0.f; sh.tb.beta[c] = 0.f;
+        }
+    }
+}
+
+// 8 consecutive elements of one row: vector access when aligned (16 B bf16 / 2x16 B f32)
+FIS_DEV void load8(const char* base, int dtype, long long off, int nvalid, float* v) {
+    if (dtype == FIS_BF16) {
+        const __nv_bfloat16* p = (const __nv_bfloat16*)base + off;
+        if (nvalid == 8 && ((uintptr_t)p & 15) == 0) {
+            const uint4 u = *(const uint4*)p;
+            const __nv_bfloat162* h = (const __nv_bfloat162*)&u;
+#pragma unroll
+            for (int k = 0; k < 4; k++) {
+                const float2 f = __bfloat1622float2(h[k]);
+                v[2 * k] = f.x; v[2 * k + 1] = f.y;
+            }
+            return;
+        }
+#pragma unroll
+        for (int k = 0; k < 8; k++) if (k < nvalid) v[k] = __bfloat162float(p[k]);
+    } else {
+        const float* p = (const float*)base + off;
+        if (nvalid == 8 && ((uintptr_t)p & 15) == 0) {
+            const float4 a0 = *(const float4*)p, a1 = *(const float4*)(p + 4);
+            v[0] = a0.x; v[1] = a0.y; v[2] = a0.z; v[3] = a0.w; v[4] = a1.x; v[5] = a1.y; v[6] = a1.z; v[7] = a1.w;
+            return;
+        }
+#pragma unroll
+        for (int k = 0; k < 8; k++) if (k < nvalid) v[k] = p[k];
+    }
+}
+
+FIS_DEV void store8(char* base, int dtype, long long off, int nvalid, const float* v) {
+    if (dtype == FIS_BF16) {
+        __nv_bfloat16* p = (__nv_bfloat16*)base + off;
+        if (nvalid == 8 && ((uintptr_t)p & 15) == 0) {
+            uint4 u;
+            __nv_bfloat162* h = (__nv_bfloat162*)&u;
+#pragma unroll
+            for (int k = 0; k < 4; k++) h[k] = __floats2bfloat162_rn(v[2 * k], v[2 * k + 1]);
+            *(uint4*)p = u;
+            return;
+        }
+#pragma unroll
+        for (int k = 0; k < 8; k++) if (k < nvalid) p[k] = __float2bfloat16_rn(v[k]);
+    } else {
+        float* p = (float*)base + off;
+        if (nvalid == 8 && ((uintptr_t)p & 15) == 0) {
+            *(float4*)p = make_float4(v[0], v[1], v[2], v[3]);
+            *(float4*)(p + 4) = make_float4(v[4], v[5], v[6], v[7]);
+            return;
+        }
+#pragma unroll
+        for (int k = 0; k < 8; k++) if (k < nvalid) p[k] = v[k];
+    }
+}
+
+// Fused GEMM epilogue of 8 columns of one output row; same operations in the same order as
+// fis::tc::row_epilogue (fis_tc.cuh) so the VM and the per-op kernels agree. Split in two so a
+// thread can issue the global reads (residual, latent rows) of several items before using them.
+struct EpiIn {
+    float x[8];  // latent rows (EPI_STEP) or residual (the plan rejects GEMMs with both)
+};
+
+FIS_DEV void epilogue8_load(const fis_gemm_args& a, const EpiCtx& e, int r, int n, EpiIn& in,
+                            const unsigned char* staged_row) {
+    const int nvalid = min(8, a.n - n);
+    if (staged_row) {  // rows staged in shared memory by stage_operand
+        const int dtype = a.epi == FIS_EPI_STEP ? a.lat.dtype : a.res.dtype;
+        if (dtype == FIS_BF16) {
+            const uint4 u = *(const uint4*)staged_row;
+            const __nv_bfloat162* h = (const __nv_bfloat162*)&u;
+#pragma unroll
+            for (int k = 0; k < 4; k++) {
+                const float2 f = __bfloat1622float2(h[k]);
+                in.x[2 * k] = f.x; in.x[2 * k + 1] = f.y;
+            }
+        } else {
+            const float4 a0 = *(const float4*)staged_row, a1 = *(const float4*)(staged_row + 16);
+            in.x[0] = a0.x; in.x[1] = a0.y; in.x[2] = a0.z; in.x[3] = a0.w;
+            in.x[4] = a1.x; in.x[5] = a1.y; in.x[6] = a1.z; in.x[7] = a1.w;
+        }
+        return;
+    }
+    const int orow = a.d_rows ? __ldg(a.d_rows + r) : r;
+    if (a.epi == FIS_EPI_STEP) load8(e.lat, a.lat.dtype, (long long)orow * a.lat.ld + n, nvalid, in.x);
+    else if (e.res) load8(e.res, a.res.dtype, (long long)orow * a.res.ld + n, nvalid, in.x);
+}
+
+FIS_DEV void epilogue8(const fis_gemm_args& a, const EpiCtx& e, const EpiTab& tb, int r, int c0, int n0, float* v,
+                       const EpiIn& in) {
+    const int n = n0 + c0;
+    const int nvalid = min(8, a.n - n);
+    const int orow = a.d_rows ? __ldg(a.d_rows + r) : r;
+#pragma unroll
+    for (int k = 0; k < 8; k++) v[k] = __fadd_rn(v[k] * a.alpha, tb.bias[c0 + k]);
+    if (e.pre) store8(e.pre, a.pre.dtype, (long long)orow * a.pre.ld + n, nvalid, v);
+    if (e.bias2) {
+#pragma unroll
+        for (int k = 0; k < 8; k++) v[k] = __fadd_rn(v[k], tb.b2[c0 + k]);
+    }
+    if (a.epi == FIS_EPI_GN_SILU) {
+        float y[8];
+#pragma unroll
+        for (int k = 0; k < 8; k++)
+            y[k] = fmaf((v[k] - tb.mean[c0 + k]) * tb.rstd[c0 + k], tb.gamma[c0 + k], tb.beta[c0 + k]);
+        if (e.pre2) store8(e.pre2, a.pre2.dtype, (long long)orow * a.pre2.ld + n, nvalid, y);
+#pragma unroll
+        for (int k = 0; k < 8; k++) v[k] = __fdividef(y[k], 1.0f + __expf(-y[k]));
+    } else if (a.epi == FIS_EPI_STEP) {
+#pragma unroll
+        for (int k = 0; k < 8; k++) v[k] = __fsub_rn(in.x[k], __fmul_rn(a.step_scale, v[k]));
+    }
+    if (e.res && a.epi != FIS_EPI_STEP) {
+#pragma unroll
+        for (int k = 0; k < 8; k++) v[k] = __fadd_rn(v[k], in.x[k]);
+    }
+    char* dbase = e.d;
+    int dt = a.d.dtype, dld = a.d.ld, dn = n, trans = a.d_trans;
+    if (a.n_split > 0 && n >= a.n_split) {  // fused QKV: V part goes transposed to d2
+        dbase = e.d2; dt = a.d2.dtype; dld = a.d2.ld; dn = n - a.n_split; trans = a.d2_trans;
+    }
+    if (trans) {
+#pragma unroll
+        for (int k = 0; k < 8; k++) if (k < nvalid) store_elem(dbase, dt, (long long)(dn + k) * dld + orow, v[k]);
+    } else {
+        store8(dbase, dt, (long long)orow * dld + dn, nvalid, v);
+    }
+}
+
+template <int BN>
+FIS_DEV void gemm_tc_epilogue(const fis_vm_args& va, const Shared& sh, int j, int i,
+                                              const GemmItem& g, ProdState& ps, uint32_t tmem, int tid,
+                                              bool tables_done, bool staged);
+
+// The epilogue's one read operand of this tile (latent rows for EPI_STEP, else the residual):
+// rows [m0, m0+BM) x columns [n0, n0+bn) copied to sh.res with 16-byte cp.async when the row
+// segment fits RES_LD and is 16-byte aligned.  Returns false (direct loads) otherwise.
+FIS_DEV bool stage_operand(const fis_gemm_args& a, const Shared& sh, const GemmItem& g, int t, int tid) {
+    const fis_ref& x = a.epi == FIS_EPI_STEP ? a.lat : a.res;
+    if (!x.ptr || a.d_rows) return false;
+    const int esz = x.dtype == FIS_BF16 ? 2 : 4;
+    const int ncols = min(g.bn, a.n - g.n0);
+    const int seg = ((ncols * esz) + 15) & ~15;
+    if (seg > RES_LD || (ncols * esz) % 16 || ((long long)x.ld * esz) % 16 || ((long long)g.n0 * esz) % 16) return false;
+    const char* base = ref_base(x, t) + (long long)g.n0 * esz;
+    if (((uintptr_t)base) & 15) return false;
+    const int per_row = seg / 16;
+    const int rows = min(BM, a.m - g.m0);
+    const uint32_t dst0 = smem_u32(sh.res);
+    for (int idx = tid; idx < rows * per_row; idx += PRODUCERS) {
+        const int row = idx / per_row, c16 = idx % per_row;
+        const int col_bytes = c16 * 16;
+        const char* src = base + ((long long)(g.m0 + row) * x.ld) * esz + col_bytes;
+        cp_async16(dst0 + row * RES_LD + col_bytes, src, true);
+    }
+    cp_commit();
+    return true;
+}
+
+template <int BN>
+FIS_DEV void gemm_tc_item(const fis_vm_args& va, const Shared& sh, int j, int i, ProdState& ps,
+                                          bool& waited, uint32_t tmem, int tid) {
+    const fis_vm_op& op = *sh.op;
+    const fis_gemm_args& a = op.u.gemm;
+    const GemmItem g = gemm_item(op, i);
+    const int t = s_step;
+    const int ar = tid >> 1, half_id = tid & 1, j0 = half_id * 4;
+    const uint32_t sbase = smem_u32(sh.ring);
+    const char* bbase = ref_base(a.b, t);
+
+    VM_STAMP(0);
+    // ---- weight tiles of the first stages + static epilogue tables: independent of the previous
+    //      op when B is static (weights / per-edit text K/V)
+    if (!op.b_static) wait_dep(va, op, j, waited, tid);
+    const int npre = min(g.nk, STAGES);
+    for (int q = 0; q < npre; q++) {
+        const uint32_t sq = ps.it + q;
+        const int s = sq % STAGES;
+        if (sq >= STAGES) mbar_wait(sh.empty + s, ((sq / STAGES) & 1) ^ 1);
+        issue_b(a, g, bbase, sbase + s * STAGE + A_BYTES, (g.kb0 + q) * BK, ar, j0);
+    }
+    if (op.b_static) stage_tables(a, make_epi(a, t), sh, g.n0, g.bn, tid);
+    // ---- static gather metadata (row/index lists are fixed for the whole edit)
+    const int r = g.m0 + ar;
+    const bool row_valid = r < a.m;
+    const int row_p = row_valid ? (a.rows ? __ldg(a.rows + r) : r) : 0;
+    if (a.a_mode == FIS_A_CONV3X3 && half_id < a.nsrc) build_sel(a, row_p, half_id, sh.seltab + (ar * 2 + half_id) * 9);
+    __syncwarp();  // the two threads of a row each built one segment's select table
+    VM_STAMP(1);
+    wait_dep(va, op, j, waited, tid);
+    VM_STAMP(2);
+
+    const char* abase = a.a.ptr ? ref_base(a.a, t) : nullptr;
+    const char* f0 = a.nsrc > 0 && a.src[0].fresh.ptr ? ref_base(a.src[0].fresh, t) : nullptr;
+    const char* c0p = a.nsrc > 0 && a.src[0].cache.ptr ? ref_base(a.src[0].cache, t) : nullptr;
+    const char* f1 = a.nsrc > 1 && a.src[1].fresh.ptr ? ref_base(a.src[1].fresh, t) : nullptr;
+    const char* c1p = a.nsrc > 1 && a.src[1].cache.ptr ? ref_base(a.src[1].cache, t) : nullptr;
+    const int cin = a.a_mode == FIS_A_CONV3X3 ? a.src[0].c + (a.nsrc > 1 ? a.src[1].c : 0) : a.k;
+    const int src0c = a.nsrc > 0 ? a.src[0].c : 0;
+    const int* mysel = sh.seltab + ar * 2 * 9;
+    for (int q = 0; q < g.nk; q++) {
+        const uint32_t sq = ps.it + q;
+        const int s = sq % STAGES;
+        const uint32_t sa = sbase + s * STAGE;
+        const int k0 = (g.kb0 + q) * BK;
+        if (q >= npre) {
+            mbar_wait(sh.empty + s, ((sq / STAGES) & 1) ^ 1);
+            issue_b(a, g, bbase, sa + A_BYTES, k0, ar, j0);
+        }
+        const char* src = nullptr;
+        if (row_valid) {
+            if (a.a_mode == FIS_A_ROWS) {
+                if (k0 < a.k) src = abase + ((long long)row_p * a.a.ld + k0) * 2;
+            } else {
+                const int tap = k0 / cin;
+                int c = k0 - tap * cin;
+                const int seg = c >= src0c ? 1 : 0;
+                c -= seg ? src0c : 0;
+                const int sel = mysel[seg * 9 + tap];
+                if (sel != SEL_ZERO) {
+                    const fis_src& sr = a.src[seg];
+                    if (sel >= 0) src = (seg ? f1 : f0) + ((long long)sel * sr.fresh.ld + c) * 2;
+                    else src = (seg ? c1p : c0p) + ((long long)(-2 - sel) * sr.cache.ld + c) * 2;
+                }
+            }
+        }
+#pragma unroll
+        for (int jj = j0; jj < j0 + 4; jj++) {
+            const bool ok = src != nullptr && (a.a_mode == FIS_A_CONV3X3 || k0 + jj * 8 < a.k);
+            cp_async16(sa + sw128_off(ar, jj), ok ? (const void*)(src + jj * 16) : (const void*)bbase, ok);
+        }
+        cp_async_arrive_noinc(sh.full + s);
+        if (q == 0) VM_STAMP(8);
+    }
+    ps.it += g.nk;
+    // ---- epilogue operand rows (residual, or latent rows for the step update): produced by
+    //      earlier ops, so fetched now into shared memory, landing while the MMAs run
+    const bool staged = stage_operand(a, sh, g, t, tid);
+    VM_STAMP(3);
+    gemm_tc_epilogue<BN>(va, sh, j, i, g, ps, tmem, tid, op.b_static != 0, staged);
+}
+
+// Epilogue of one tcgen05 GEMM item (separate frame: the gather pointers above are dead here).
+//   1. TMEM -> shared staging tile [BM][BN+4] fp32 (thread = accumulator row)
+//   2. S == 1: fused row epilogue over (row, 16-column chunk) items, consecutive threads on
+//      consecutive chunks of a row (full-sector coalesced loads/stores); transposed outputs use
+//      consecutive threads on consecutive rows instead.
+//      S > 1 : the staged partial is copied (coalesced) to the workspace; the S split CTAs of
+//      the tile meet at a tile counter, then split z reduces rows [z*BM/S, (z+1)*BM/S) over
+//      all S partials in split order (bitwise deterministic) and runs the epilogue on them.
+//      Every split CTA of a tile is resident and co-scheduled (plan: items <= CTAs when S > 1).
+template <int BN>
+FIS_DEV void gemm_tc_epilogue(const fis_vm_args& va, const Shared& sh, int j, int i,
+                                              const GemmItem& g, ProdState& ps, uint32_t tmem, int tid,
+                                              bool tables_done, bool staged) {
+    const fis_vm_op& op = *sh.op;
+    const fis_gemm_args& a = op.u.gemm;
+    const int warp = tid >> 5, lane = tid & 31;
+    const int t = s_step;
+    const EpiCtx e = make_epi(a, t);
+    if (!tables_done) stage_tables(a, e, sh, g.n0, g.bn, tid);
+    VM_STAMP(4);
+    mbar_wait(sh.done, ps.items & 1);
+    ps.items++;
+    tc_fence_after();
+    VM_STAMP(5);
+    // ---- 1. TMEM -> staging (the ring is idle: every MMA of this item has completed)
+    constexpr int PLD = BN + 4;
+    constexpr int hc = BN / 2;  // columns per warp half
+    float* stage = (float*)sh.ring;
+    {
+        const int quarter = warp & 3, half = warp >> 2;
+        const int lr = quarter * 32 + lane;
+        const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) + half * hc;
+        float* dst = stage + lr * PLD + half * hc;
+#pragma unroll 1
+        for (int q = 0; q < hc / 16; q++) {
+            float v[16];
+            tmem_ld16(taddr + 16 * q, v);
+#pragma unroll
+            for (int w = 0; w < 4; w++)
+                *(float4*)(dst + 16 * q + 4 * w) = make_float4(v[4 * w], v[4 * w + 1], v[4 * w + 2], v[4 * w + 3]);
+        }
+        tc_fence_before();
+    }
+    VM_STAMP(9);
+    if (staged) cp_wait<0>();
+    pbar();
+    VM_STAMP(10);
+    const int S = op.splits;
+    constexpr int chunks = BN / 8;  // 8-column epilogue items
+    int r0 = 0, r1 = BM;
+    const float* wsb = nullptr;
+    const long long tile_floats = (long long)BM * BN;
+    if (S > 1) {
+        // ---- 2b. publish the partial (coalesced float4 rows), meet the other splits of the tile
+        float* wsz = va.ws + ((long long)g.tile * S + g.z) * tile_floats;
+        for (int idx = tid; idx < BM * (BN / 4); idx += PRODUCERS) {
+            const int row = idx / (BN / 4), c4 = (idx % (BN / 4)) * 4;
+            __stcg((float4*)(wsz + row * BN + c4), *(const float4*)(stage + row * PLD + c4));
+        }
+        pbar();
+        if (tid == 0) {
+            fence_acq_rel();
+            int* ctr = va.sync + op.sync_base + g.tile;
+            atomicAdd(ctr, 1);
+            spin_until(ctr, S, 32);
+        }
+        pbar();
+        VM_STAMP(11);
+        const int rows_per = (BM + S - 1) / S;
+        r0 = min(BM, g.z * rows_per);
+        r1 = min(BM, r0 + rows_per);
+        wsb = va.ws + (long long)g.tile * S * tile_floats;
+    }
+    // ---- 2. fused epilogue of rows [r0, r1), 8-column items
+    const int nrows = min(r1, a.m - g.m0) - r0;
+    const bool trans = a.d_trans || (a.n_split > 0 && g.n0 >= a.n_split);
+    const int n_items = nrows > 0 ? nrows * chunks : 0;
+    constexpr int IB = 2;  // items per thread in flight (their global reads issued together)
+    long long cy_load = 0, cy_epi = 0, cy0 = clock64();
+    for (int base = tid; base < n_items; base += IB * PRODUCERS) {
+        const long long c0 = clock64();
+        float v[IB][8];
+        EpiIn in[IB];
+        int rowv[IB], cbv[IB];
+#pragma unroll
+        for (int u = 0; u < IB; u++) {
+            const int idx = base + u * PRODUCERS;
+            int row = 0, ch = 0;
+            if (idx < n_items) {
+                if (trans) { row = r0 + idx % nrows; ch = idx / nrows; }
+                else { row = r0 + idx / chunks; ch = idx % chunks; }
+            }
+            rowv[u] = row;
+            cbv[u] = ch * 8;
+            const bool live = idx < n_items && g.n0 + ch * 8 < a.n;
+            if (!live) { cbv[u] = -1; continue; }
+            if (S == 1) {
+                const float4 f0 = *(const float4*)(stage + row * PLD + ch * 8);
+                const float4 f1 = *(const float4*)(stage + row * PLD + ch * 8 + 4);
+                v[u][0] = f0.x; v[u][1] = f0.y; v[u][2] = f0.z; v[u][3] = f0.w;
+                v[u][4] = f1.x; v[u][5] = f1.y; v[u][6] = f1.z; v[u][7] = f1.w;
+            }
+            const int esz = (a.epi == FIS_EPI_STEP ? a.lat.dtype : a.res.dtype) == FIS_BF16 ? 2 : 4;
+            epilogue8_load(a, e, g.m0 + row, g.n0 + ch * 8, in[u],
+                           staged ? sh.res + row * RES_LD + ch * 8 * esz : nullptr);
+        }
+        if (S > 1) {
+#pragma unroll
+            for (int u = 0; u < IB; u++) {
+                if (cbv[u] < 0) continue;
+#pragma unroll
+                for (int jj = 0; jj < 8; jj++) v[u][jj] = 0.f;
+                const float* p = wsb + rowv[u] * BN + cbv[u];
+                int zz = 0;
+                for (; zz + 4 <= S; zz += 4) {  // 8 float4 loads in flight, summed in split order
+                    float4 f[4][2];
+#pragma unroll
+                    for (int q = 0; q < 4; q++)
+#pragma unroll
+                        for (int w = 0; w < 2; w++) f[q][w] = __ldcg((const float4*)(p + (zz + q) * tile_floats) + w);
+#pragma unroll
+                    for (int q = 0; q < 4; q++)
+#pragma unroll
+                        for (int w = 0; w < 2; w++) {
+                            v[u][4 * w] += f[q][w].x; v[u][4 * w + 1] += f[q][w].y;
+                            v[u][4 * w + 2] += f[q][w].z; v[u][4 * w + 3] += f[q][w].w;
+                        }
+                }
+                for (; zz < S; zz++) {
+#pragma unroll
+                    for (int w = 0; w < 2; w++) {
+                        const float4 f = __ldcg((const float4*)(p + zz * tile_floats) + w);
+                        v[u][4 * w] += f.x; v[u][4 * w + 1] += f.y; v[u][4 * w + 2] += f.z; v[u][4 * w + 3] += f.w;
+                    }
+                }
+            }
+        }
+        const long long c1 = clock64();
+#pragma unroll
+        for (int u = 0; u < IB; u++)
+            if (cbv[u] >= 0) epilogue8(a, e, sh.tb, g.m0 + rowv[u], cbv[u], g.n0, v[u], in[u]);
+        cy_load += c1 - c0;
+        cy_epi += clock64() - c1;
+    }
+    if (va.trace_items && j == va.trace_op && tid == 0) {
+        va.trace_items[16 * i + 12] = cy_load;
+        va.trace_items[16 * i + 13] = cy_epi;
+        va.trace_items[16 * i + 14] = clock64() - cy0;
+    }
+    VM_STAMP(6);
+    signal_done(va, j, tid);
+    VM_STAMP(7);
+}
+
+// ---------------------------------------------------------------------------------- SIMT ops
+FIS_DEV float gather_a_simt(const fis_gemm_args& a, const char* f0, const char* c0p, const char* f1, const char* c1p,
+                            const char* abase, int k, int p, int oy, int ox) {
+    if (a.a_mode == FIS_A_ROWS) return load_elem(abase, a.a.dtype, (long long)p * a.a.ld + k);
+    const int cin = a.src[0].c + (a.nsrc > 1 ? a.src[1].c : 0);
+    const int tap = k / cin;
+    int c = k - tap * cin;
+    const int y = oy + tap / 3 - 1, x = ox + tap % 3 - 1;
+    if (y < 0 || x < 0 || y >= a.out_h || x >= a.out_w) return 0.f;
+    const bool second = c >= a.src[0].c;
+    const fis_src& s = second ? a.src[1] : a.src[0];
+    if (second) c -= a.src[0].c;
+    const int sy = s.up ? (y >> 1) : y, sx = s.up ? (x >> 1) : x;
+    return src_value(s, second ? f1 : f0, second ? c1p : c0p, sy * s.w + sx, c);
+}
+
+FIS_DEV void gemm_simt_item(const fis_gemm_args& a, unsigned char* scratch, int item, int tiles_n, int tid) {
+    float (*As)[SBM + 4] = (float (*)[SBM + 4])scratch;
+    float (*Bs)[SBN + 4] = (float (*)[SBN + 4])(scratch + SBK * (SBM + 4) * 4);
+    int* rowp = (int*)(scratch + 2 * SBK * (SBM + 4) * 4);
+    int* rowy = rowp + SBM;
+    int* rowx = rowy + SBM;
+    const int t = s_step;
+    const int n0 = (item % tiles_n) * SBN, m0 = (item / tiles_n) * SBM;
+    const char* abase = a.a.ptr ? ref_base(a.a, t) : nullptr;
+    const char* f0 = a.nsrc > 0 && a.src[0].fresh.ptr ? ref_base(a.src[0].fresh, t) : nullptr;
+    const char* c0p = a.nsrc > 0 && a.src[0].cache.ptr ? ref_base(a.src[0].cache, t) : nullptr;
+    const char* f1 = a.nsrc > 1 && a.src[1].fresh.ptr ? ref_base(a.src[1].fresh, t) : nullptr;
+    const char* c1p = a.nsrc > 1 && a.src[1].cache.ptr ? ref_base(a.src[1].cache, t) : nullptr;
+    const char* bbase = ref_base(a.b, t);
+    if (tid < SBM) {
+        const int r = m0 + tid;
+        const int p = r < a.m ? (a.rows ? __ldg(a.rows + r) : r) : 0;
+        rowp[tid] = p;
+        rowy[tid] = p / max(1, a.out_w);
+        rowx[tid] = p - rowy[tid] * max(1, a.out_w);
+    }
+    pbar();
+    const int tx = tid % 16, ty = tid / 16;
+    float acc[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; i++)
+#pragma unroll
+        for (int jj = 0; jj < 4; jj++) acc[i][jj] = 0.f;
+    const int lk = tid % SBK, lr = tid / SBK;
+    const int ktiles = (a.k + SBK - 1) / SBK;
+    for (int kt = 0; kt < ktiles; kt++) {
+        const int k = kt * SBK + lk;
+#pragma unroll
+        for (int i = 0; i < 4; i++) {
+            const int row = lr + 16 * i;
+            const int r = m0 + row;
+            float v = 0.f;
+            if (r < a.m && k < a.k) v = gather_a_simt(a, f0, c0p, f1, c1p, abase, k, rowp[row], rowy[row], rowx[row]);
+            As[lk][row] = v;
+            const int n = n0 + row;
+            float bv = 0.f;
+            if (n < a.n && k < a.k) bv = load_elem(bbase, a.b.dtype, (long long)n * a.b.ld + k);
+            Bs[lk][row] = bv;
+        }
+        pbar();
+#pragma unroll
+        for (int kk = 0; kk < SBK; kk++) {
+            float av[4], bv[4];
+#pragma unroll
+            for (int i = 0; i < 4; i++) av[i] = As[kk][ty * 4 + i];
+#pragma unroll
+            for (int jj = 0; jj < 4; jj++) bv[jj] = Bs[kk][tx * 4 + jj];
+#pragma unroll
+            for (int i = 0; i < 4; i++)
+#pragma unroll
+                for (int jj = 0; jj < 4; jj++) acc[i][jj] = fmaf(av[i], bv[jj], acc[i][jj]);
+        }
+        pbar();
+    }
+    const EpiCtx e = make_epi(a, t);
+    if (a.epi == FIS_EPI_NONE && !e.res && a.n_split == 0 && !a.d_trans && !a.d_rows) {
+        // bias / time-bias columns read once (all loads in flight), then plain stores
+        float bia[4], b2v[4];
+#pragma unroll
+        for (int jj = 0; jj < 4; jj++) {
+            const int n = n0 + tx * 4 + jj;
+            bia[jj] = n < a.n && a.bias ? __ldg(a.bias + n) : 0.f;
+            b2v[jj] = n < a.n && e.bias2 ? load_elem(e.bias2, a.bias2.dtype, n) : 0.f;
+        }
+#pragma unroll
+        for (int i = 0; i < 4; i++) {
+            const int r = m0 + ty * 4 + i;
+            if (r >= a.m) continue;
+#pragma unroll
+            for (int jj = 0; jj < 4; jj++) {
+                const int n = n0 + tx * 4 + jj;
+                if (n >= a.n) continue;
+                float v = acc[i][jj] * a.alpha;  // same operation order as epilogue_store
+                if (a.bias) v = __fadd_rn(v, bia[jj]);
+                if (e.pre) store_elem(e.pre, a.pre.dtype, (long long)r * a.pre.ld + n, v);
+                if (e.bias2) v = __fadd_rn(v, b2v[jj]);
+                store_elem(e.d, a.d.dtype, (long long)r * a.d.ld + n, v);
+            }
+        }
+        return;
+    }
+#pragma unroll
+    for (int i = 0; i < 4; i++) {
+        const int r = m0 + ty * 4 + i;
+        if (r >= a.m) continue;
+#pragma unroll
+        for (int jj = 0; jj < 4; jj++) {
+            const int n = n0 + tx * 4 + jj;
+            if (n < a.n) epilogue_store(a, e, r, n, acc[i][jj]);
+        }
+    }
+}
+
+// softmax rows [item*8, item*8+8): one warp per row (tensors.py:183-192, unet.py:555-566)
+FIS_DEV void softmax_item(const fis_softmax_args& a, int item, int tid) {
+    const int t = s_step;
+    const int row = item * SOFTMAX_ROWS + (tid >> 5);
+    const int lane = tid & 31;
+    if (row >= a.rows) return;
+    char* pb = ref_base(a.p, t);
+    char* mb = a.map.ptr ? ref_base(a.map, t) : nullptr;
+    const float* cached = a.cached.ptr ? (const float*)ref_base(a.cached, t) + (long long)row * a.cached.ld : nullptr;
+    const long long prow = (long long)row * a.p.ld;
+    if (a.verbatim) {
+        for (int jj = lane; jj < a.cols; jj += 32) {
+            const float v = cached[jj];
+            store_elem(pb, a.p.dtype, prow + jj, v);
+            if (mb) ((float*)mb)[(long long)row * a.map.ld + jj] = v;
+        }
+    } else if (a.npairs == 0 && a.cols <= 32 * 16) {
+        // one pass: the row lives in registers (<= 16 values per lane), all loads in flight at once
+        const float* s = (const float*)ref_base(a.s, t) + (long long)row * a.s.ld;
+        float x[16];
+        float m = -INFINITY;
+#pragma unroll
+        for (int k = 0; k < 16; k++) {
+            const int jj = lane + 32 * k;
+            x[k] = jj < a.cols ? __ldcg(s + jj) * a.scale : -INFINITY;
+        }
+#pragma unroll
+        for (int k = 0; k < 16; k++) m = fmaxf(m, x[k]);
+        m = warp_max(m);
+        float sum = 0.f;
+#pragma unroll
+        for (int k = 0; k < 16; k++) {
+            x[k] = lane + 32 * k < a.cols ? expf(x[k] - m) : 0.f;
+            sum += x[k];
+        }
+        sum = warp_sum(sum);
+        const float inv_sum = 1.0f / sum;
+#pragma unroll
+        for (int k = 0; k < 16; k++) {
+            const int jj = lane + 32 * k;
+            if (jj < a.cols) {
+                const float v = x[k] * inv_sum;
+                store_elem(pb, a.p.dtype, prow + jj, v);
+                if (mb) ((float*)mb)[(long long)row * a.map.ld + jj] = v;
+            }
+        }
+    } else {
+        const float* s = (const float*)ref_base(a.s, t) + (long long)row * a.s.ld;
+        float m = -INFINITY;
+        for (int jj = lane; jj < a.cols; jj += 32) m = fmaxf(m, s[jj] * a.scale);
+        m = warp_max(m);
+        float sum = 0.f;
+        for (int jj = lane; jj < a.cols; jj += 32) sum += expf(s[jj] * a.scale - m);
+        sum = warp_sum(sum);
+        const float inv_sum = 1.0f / sum;
+        if (a.npairs == 0) {
+            for (int jj = lane; jj < a.cols; jj += 32) {
+                const float v = expf(s[jj] * a.scale - m) * inv_sum;
+                store_elem(pb, a.p.dtype, prow + jj, v);
+                if (mb) ((float*)mb)[(long long)row * a.map.ld + jj] = v;
+            }
+        } else {
+            float rs = 0.f;
+            for (int jj = lane; jj < a.cols; jj += 32) {
+                float v = expf(s[jj] * a.scale - m) * inv_sum;
+                for (int i = 0; i < a.npairs; i++)
+                    if (__ldg(a.pair_new + i) == jj) v = cached[__ldg(a.pair_old + i)];
+                rs += v;
+            }
+            rs = warp_sum(rs);
+            for (int jj = lane; jj < a.cols; jj += 32) {
+                float v = expf(s[jj] * a.scale - m) * inv_sum;
+                for (int i = 0; i < a.npairs; i++)
+                    if (__ldg(a.pair_new + i) == jj) v = cached[__ldg(a.pair_old + i)];
+                const float o = (float)((double)v / (double)rs);
+                store_elem(pb, a.p.dtype, prow + jj, o);
+                if (mb) ((float*)mb)[(long long)row * a.map.ld + jj] = o;
+            }
+        }
+    }
+    for (int jj = a.cols + lane; jj < a.pad_cols; jj += 32) store_elem(pb, a.p.dtype, prow + jj, 0.f);
+}
+
+// group-norm statistics of group `g` (tensors.py:129-146): two-pass f64, rounded to f32
+FIS_DEV void gn_stats_item(const fis_gn_stats_args& a, double* red, int g, int tid) {
+    const int t = s_step;
+    const int cpg = a.c / a.groups;
+    const long long cnt = (long long)a.hw * cpg;
+    const char* x = ref_base(a.x, t);
+    double s = 0.0;
+    for (int q = tid; q < a.hw; q += PRODUCERS) {
+        const long long base = (long long)q * a.x.ld + g * cpg;
+        for (int c = 0; c < cpg; c++) s += (double)load_elem(x, a.x.dtype, base + c);
+    }
+    red[tid] = s;
+    pbar();
+    for (int o = 128; o; o >>= 1) {
+        if (tid < o) red[tid] += red[tid + o];
+        pbar();
+    }
+    const double mean = red[0] / (double)cnt;
+    pbar();
+    double v = 0.0;
+    for (int q = tid; q < a.hw; q += PRODUCERS) {
+        const long long base = (long long)q * a.x.ld + g * cpg;
+        for (int c = 0; c < cpg; c++) {
+            const double d = (double)load_elem(x, a.x.dtype, base + c) - mean;
+            v += d * d;
+        }
+    }
+    red[tid] = v;
+    pbar();
+    for (int o = 128; o; o >>= 1) {
+        if (tid < o) red[tid] += red[tid + o];
+        pbar();
+    }
+    if (tid == 0) {
+        ((float*)ref_base(a.mean, t))[g] = (float)mean;
+        ((float*)ref_base(a.var, t))[g] = (float)(red[0] / (double)cnt);
+    }
+}
+
+FIS_DEV void gn_apply_item(const fis_gn_apply_args& a, int item, int tid) {
+    const int t = s_step;
+    const char* x = ref_base(a.x, t);
+    const float* mean = (const float*)ref_base(a.mean, t);
+    const float* var = (const float*)ref_base(a.var, t);
+    char* yn = a.y_norm.ptr ? ref_base(a.y_norm, t) : nullptr;
+    char* ys = a.y_silu.ptr ? ref_base(a.y_silu, t) : nullptr;
+    const int cpg = a.c / a.groups;
+    const int total = a.rows * a.c;
+    const int e1 = min(total, (item + 1) * ELEMS_PER_ITEM);
+    for (int e = item * ELEMS_PER_ITEM + tid; e < e1; e += PRODUCERS) {
+        const int r = e / a.c, c = e - (e / a.c) * a.c;
+        const int xr = a.x_rows ? __ldg(a.x_rows + r) : r;
+        const int yr = a.y_rows ? __ldg(a.y_rows + r) : r;
+        const int g = c / cpg;
+        const double xv = (double)load_elem(x, a.x.dtype, (long long)xr * a.x.ld + c);
+        const double y64 = (xv - (double)mean[g]) / sqrt((double)var[g] + (double)a.eps) * (double)a.gamma[c] +
+                           (double)a.beta[c];
+        const float y = (float)y64;
+        if (yn) store_elem(yn, a.y_norm.dtype, (long long)yr * a.y_norm.ld + c, y);
+        if (ys) {
+            const double yd = (double)y;
+            store_elem(ys, a.y_silu.dtype, (long long)yr * a.y_silu.ld + c, (float)(yd / (1.0 + exp(-yd))));
+        }
+    }
+}
+
+FIS_DEV void pool_item(const fis_pool_args& a, int item, int tid) {
+    const int t = s_step;
+    const char* fr = a.src.fresh.ptr ? ref_base(a.src.fresh, t) : nullptr;
+    const char* ca = a.src.cache.ptr ? ref_base(a.src.cache, t) : nullptr;
+    char* out = ref_base(a.out, t);
+    const int cw = a.src.w / 2;
+    const int total = a.n * a.c;
+    const int e1 = min(total, (item + 1) * ELEMS_PER_ITEM);
+    for (int e = item * ELEMS_PER_ITEM + tid; e < e1; e += PRODUCERS) {
+        const int i = e / a.c, c = e - (e / a.c) * a.c;
+        const int P = a.rows ? __ldg(a.rows + i) : i;
+        const int py = P / cw, px = P - (P / cw) * cw;
+        const int q = (2 * py) * a.src.w + 2 * px;
+        const float v00 = src_value(a.src, fr, ca, q, c), v01 = src_value(a.src, fr, ca, q + 1, c);
+        const float v10 = src_value(a.src, fr, ca, q + a.src.w, c), v11 = src_value(a.src, fr, ca, q + a.src.w + 1, c);
+        const float s = __fadd_rn(__fadd_rn(v00, v01), __fadd_rn(v10, v11));
+        store_elem(out, a.out.dtype, (long long)i * a.out.ld + c, __fmul_rn(s, 0.25f));
+    }
+}
+
+FIS_DEV void materialize_item(const fis_materialize_args& a, int item, int tid) {
+    const int t = s_step;
+    const char* fr = a.src.fresh.ptr ? ref_base(a.src.fresh, t) : nullptr;
+    const char* ca = a.src.cache.ptr ? ref_base(a.src.cache, t) : nullptr;
+    char* out = ref_base(a.out, t);
+    const int total = a.src.h * a.src.w * a.c;
+    const int e1 = min(total, (item + 1) * ELEMS_PER_ITEM);
+    for (int e = item * ELEMS_PER_ITEM + tid; e < e1; e += PRODUCERS) {
+        const int q = e / a.c, c = e - (e / a.c) * a.c;
+        store_elem(out, a.out.dtype, (long long)q * a.out.ld + c, src_value(a.src, fr, ca, q, c));
+    }
+}
+
+FIS_DEV void producer_role(const fis_vm_args& va, const Shared& sh, uint32_t tmem, int tid) {
+    const int G = gridDim.x, cta = blockIdx.x;
+    ProdState ps{0, 0};
+    for (int j = 0; j < va.n_ops; j++) {
+        const fis_vm_op* gop = va.ops + j;
+        const int n_items = gop->n_items;
+        int i = (cta - gop->cta0 + G) % G;
+        if (i >= n_items) continue;
+        // stage the op record in shared memory (previous op's readers are past their last barrier)
+        pbar();
+        {
+            static_assert(sizeof(fis_vm_op) % 8 == 0, "fis_vm_op is copied as 8-byte words");
+            const long long* src = (const long long*)gop;
+            long long* dst = (long long*)sh.op;
+            for (int w = tid; w < (int)sizeof(fis_vm_op) / 8; w += PRODUCERS) dst[w] = __ldg(src + w);
+        }
+        pbar();
+        const fis_vm_op& op = *sh.op;
+        bool waited = false;
+        for (; i < n_items; i += G) {
+            switch (op.kind) {
+                case FIS_VM_GEMM:
+                    if (op.impl == 2) {
+                        if (op.bn == 64) gemm_tc_item<64>(va, sh, j, i, ps, waited, tmem, tid);
+                        else gemm_tc_item<128>(va, sh, j, i, ps, waited, tmem, tid);
+                    } else {
+                        VM_STAMP(0);
+                        wait_dep(va, op, j, waited, tid);
+                        VM_STAMP(2);
+                        gemm_simt_item(op.u.gemm, sh.ring, i, op.tiles_n, tid);
+                        VM_STAMP(6);
+                        signal_done(va, j, tid);
+                        VM_STAMP(7);
+                    }
+                    break;
+                case FIS_VM_SOFTMAX:
+                    VM_STAMP(0);
+                    wait_dep(va, op, j, waited, tid);
+                    VM_STAMP(2);
+                    softmax_item(op.u.softmax, i, tid);
+                    VM_STAMP(6);
+                    signal_done(va, j, tid);
+                    VM_STAMP(7);
+                    break;
+                case FIS_VM_GN_STATS:
+                    wait_dep(va, op, j, waited, tid);
+                    gn_stats_item(op.u.gn_stats, (double*)sh.ring, i, tid);
+                    signal_done(va, j, tid);
+                    break;
+                case FIS_VM_GN_APPLY:
+                    wait_dep(va, op, j, waited, tid);
+                    gn_apply_item(op.u.gn_apply, i, tid);
+                    signal_done(va, j, tid);
+                    break;
+                case FIS_VM_POOL:
+                    wait_dep(va, op, j, waited, tid);
+                    pool_item(op.u.pool, i, tid);
+                    signal_done(va, j, tid);
+                    break;
+                case FIS_VM_MATERIALIZE:
+                    wait_dep(va, op, j, waited, tid);
+                    materialize_item(op.u.materialize, i, tid);
+                    signal_done(va, j, tid);
+                    break;
+                default:
+                    break;
+            }
+        }
+    }
+}
+
+__global__ void __launch_bounds__(THREADS, 1) vm_kernel(const fis_vm_args va) {
+    const Shared sh = carve();
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    if (tid == 0) {
+        for (int s = 0; s < STAGES; s++) {
+            mbar_init(sh.full + s, PRODUCERS);
+            mbar_init(sh.empty + s, 1);
+        }
+        mbar_init(sh.done, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == MMA_WARP) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(sh.tmem_slot)),
+                     "n"(MAX_BN));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *sh.tmem_slot;
+    if (tid == 0) s_step = va.step ? *va.step : 0;
+    __syncthreads();
+
+    if (warp == MMA_WARP) mma_role(va, sh, tmem, lane);
+    else producer_role(va, sh, tmem, tid);
+
+    tc_fence_before();
+    __syncthreads();
+    if (warp == MMA_WARP)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(MAX_BN));
+    // the last CTA to leave resets the per-op completion counters for the next launch
+    if (tid == 0) {
+        __threadfence();
+        const int old = atomicAdd(va.sync, 1);
+        if (old == (int)gridDim.x - 1) {
+            for (int j = 1; j < va.n_sync; j++) va.sync[j] = 0;
+            __threadfence();
+            va.sync[0] = 0;
+        }
+    }
+}
+
+}  // namespace vm
+}  // namespace fis
+
+int fis_gemm_tc_supported(const fis_gemm_args* a);
+
+static int vm_sm_count() {
+    static int n = 0;
+    if (n <= 0) n = fis_device_sm_count();
+    return n > 0 ? n : 148;
+}
+
+extern "C" int fis_vm_op_size(void) { return (int)sizeof(fis_vm_op); }
+
+extern "C" int fis_vm_plan(fis_vm_op* ops, int n, int n_ctas, long long* ws_floats, int* sync_ints) {
+    using namespace fis::vm;
+    const int G = n_ctas > 0 ? n_ctas : vm_sm_count();
+    long long ws = 0;
+    int sync_next = 1 + n;
+    int cta = 0, last = -1;
+    for (int j = 0; j < n; j++) {
+        fis_vm_op& op = ops[j];
+        op.impl = 0; op.bn = 0; op.tiles_n = 0; op.tiles_m = 0; op.splits = 1; op.sync_base = 0;
+        switch (op.kind) {
+            case FIS_VM_GEMM: {
+                const fis_gemm_args& a = op.u.gemm;
+                if (a.m < 0 || a.n <= 0 || a.k <= 0) return FIS_ERR_SHAPE;
+                if (a.a_mode == FIS_A_CONV3X3) {
+                    if (a.nsrc < 1 || a.nsrc > 2) return FIS_ERR_SHAPE;
+                    const int cin = a.src[0].c + (a.nsrc > 1 ? a.src[1].c : 0);
+                    if (a.k != 9 * cin) return FIS_ERR_SHAPE;
+                    for (int i = 0; i < a.nsrc; i++)
+                        if (a.src[i].index && !a.src[i].cache.ptr) return FIS_ERR_CACHE_MISS;
+                }
+                if (a.epi == FIS_EPI_GN_SILU && (a.groups <= 0 || a.n % a.groups || !a.gn_mean.ptr || !a.gn_var.ptr))
+                    return FIS_ERR_SHAPE;
+                if (a.epi == FIS_EPI_STEP && a.res.ptr) return FIS_ERR_UNSUPPORTED;  // one epilogue read per item
+                const bool tc = a.impl != 1 && fis_gemm_tc_supported(&a);
+                if (tc) {
+                    op.impl = 2;
+                    op.bn = a.n <= 64 ? 64 : 128;
+                    op.tiles_n = (a.n + op.bn - 1) / op.bn;
+                    op.tiles_m = (a.m + BM - 1) / BM;
+                    const int tiles = op.tiles_n * op.tiles_m;
+                    const int kb = (a.k + BK - 1) / BK;
+                    // split-K: every split CTA of a tile must be co-resident (they meet at a tile
+                    // counter), so tiles * S <= G
+                    int S = a.splits > 0 ? a.splits : G / (tiles > 0 ? tiles : 1);
+                    if (a.splits <= 0 && S > kb / 2) S = kb / 2;
+                    if (S > G / (tiles > 0 ? tiles : 1)) S = G / (tiles > 0 ? tiles : 1);
+                    if (S > 32) S = 32;
+                    if (S < 1) S = 1;
+                    const int per = (kb + S - 1) / S;
+                    S = (kb + per - 1) / per;
+                    op.splits = S;
+                    op.n_items = tiles * S;
+                    op.n_done = tiles * S;
+                    if (S > 1) {
+                        op.sync_base = sync_next;
+                        sync_next += tiles;
+                        const long long need = (long long)tiles * S * BM * op.bn;
+                        if (need > ws) ws = need;
+                    }
+                } else {
+                    op.impl = 1;
+                    op.tiles_n = (a.n + SBN - 1) / SBN;
+                    op.tiles_m = (a.m + SBM - 1) / SBM;
+                    op.n_items = op.tiles_n * op.tiles_m;
+                    op.n_done = op.n_items;
+                }
+                break;
+            }
+            case FIS_VM_SOFTMAX: {
+                const fis_softmax_args& a = op.u.softmax;
+                if (a.pad_cols < a.cols) return FIS_ERR_SHAPE;
+                if ((a.verbatim || a.npairs) && !a.cached.ptr) return FIS_ERR_CACHE_MISS;
+                op.n_items = (a.rows + SOFTMAX_ROWS - 1) / SOFTMAX_ROWS;
+                break;
+            }
+            case FIS_VM_GN_STATS:
+                if (op.u.gn_stats.groups <= 0 || op.u.gn_stats.c % op.u.gn_stats.groups) return FIS_ERR_SHAPE;
+                op.n_items = op.u.gn_stats.groups;
+                break;
+            case FIS_VM_GN_APPLY: {
+                const fis_gn_apply_args& a = op.u.gn_apply;
+                if (a.groups <= 0 || a.c % a.groups) return FIS_ERR_SHAPE;
+                op.n_items = (int)(((long long)a.rows * a.c + ELEMS_PER_ITEM - 1) / ELEMS_PER_ITEM);
+                break;
+            }
+            case FIS_VM_POOL:
+                if (op.u.pool.src.index && !op.u.pool.src.cache.ptr) return FIS_ERR_CACHE_MISS;
+                op.n_items = (int)(((long long)op.u.pool.n * op.u.pool.c + ELEMS_PER_ITEM - 1) / ELEMS_PER_ITEM);
+                break;
+            case FIS_VM_MATERIALIZE: {
+                const fis_materialize_args& a = op.u.materialize;
+                if (a.src.index && !a.src.cache.ptr) return FIS_ERR_CACHE_MISS;
+                op.n_items = (int)(((long long)a.src.h * a.src.w * a.c + ELEMS_PER_ITEM - 1) / ELEMS_PER_ITEM);
+                break;
+            }
+            default:
+                return FIS_ERR_UNSUPPORTED;
+        }
+        if (op.kind != FIS_VM_GEMM) op.n_done = op.n_items;
+        op.dep = last;
+        op.dep_target = last >= 0 ? ops[last].n_done : 0;
+        op.cta0 = cta;
+        cta = (int)((cta + (long long)op.n_items) % G);
+        if (op.n_items > 0) last = j;
+    }
+    if (ws_floats) *ws_floats = ws;
+    if (sync_ints) *sync_ints = sync_next;
+    return FIS_OK;
+}
+
+extern "C" int fis_vm_run(const fis_vm_args* a, void* stream) {
+    using namespace fis::vm;
+    if (a->n_ops <= 0) return FIS_OK;
+    static bool configured = false;
+    if (!configured) {
+        if (cudaFuncSetAttribute(vm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM) != cudaSuccess)
+            return FIS_ERR_UNSUPPORTED;
+        configured = true;
+    }
+    const int G = a->n_ctas > 0 ? a->n_ctas : vm_sm_count();
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(G);
+    cfg.blockDim = dim3(THREADS);
+    cfg.dynamicSmemBytes = SMEM;
+    cfg.stream = (cudaStream_t)stream;
+    // all CTAs must be co-resident (items wait on other CTAs): cooperative launch guarantees it
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, vm_kernel, *a) == cudaSuccess ? FIS_OK : FIS_ERR_LAUNCH;
+}

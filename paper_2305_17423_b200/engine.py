@@ -16,6 +16,7 @@ mutated by an edit (no compaction, cache.py:538-579 is a numerical no-op).
 from __future__ import annotations
 
 import math
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -124,6 +125,17 @@ class Launcher:
         self.static_meta = False
         self.groups = 1
         self.step_scale_value = 1.0
+        # capture mode: launches are recorded as (entry point, args) for the step VM instead of run
+        self.capture: list | None = None
+        self.use_vm = precision == "bf16" and os.environ.get("FIS_VM", "0") == "1"
+
+    def _call(self, name, args, b_static=False):
+        if self.capture is not None:
+            if name not in L.VM_KINDS:
+                raise ContractViolation(f"{name} cannot run inside the step VM")
+            self.capture.append((name, args, b_static))
+            return
+        L.call(name, args)
 
     def scratch(self, name, shape, dtype=None, zero=False):
         key = (name, tuple(shape), dtype or self.act)
@@ -149,7 +161,9 @@ class Launcher:
 
     def gemm(self, m, n, k, *, a=None, rows=None, srcs=None, out_hw=None, b: DRef, d: DRef, alpha=1.0, bias=None,
              bias2=None, pre=None, epi=L.EPI_NONE, gn=None, lat=None, res=None, d_trans=False, splits=None,
-             n_split=0, d2=None, d2_trans=False):
+             n_split=0, d2=None, d2_trans=False, b_static=False):
+        """b_static: B is not produced inside the step (weights, per-edit text K/V), so the step VM
+        may stage it before the previous op completes."""
         if m == 0:
             return
         g = L.GemmArgs()
@@ -189,7 +203,7 @@ class Launcher:
         g.step = L.ptr(self.step_dev)
         g.impl = self.gemm_impl
         g.static_meta = 1 if self.static_meta else 0
-        L.call("fis_gemm", g)
+        self._call("fis_gemm", g, b_static)
         self.launches += 1
 
     def softmax(self, rows, cols, pad_cols, s: DRef, scale, p: DRef, map_: DRef | None = None, cached=None,
@@ -203,8 +217,73 @@ class Launcher:
             po, pn = pairs
             a.npairs, a.pair_old, a.pair_new = po.numel(), L.ptr(po), L.ptr(pn)
         a.step = L.ptr(self.step_dev)
-        L.call("fis_softmax", a)
+        self._call("fis_softmax", a)
         self.launches += 1
+
+class VmProgram:
+    """A recorded step (list of launches) planned for the persistent step VM (csrc/fis_vm.cu).
+
+    One `run()` = one cooperative launch executing every op of the step back to back."""
+
+    def __init__(self, lz: Launcher, calls):
+        n = len(calls)
+        if n == 0:
+            raise ContractViolation("empty step program")
+        ops = (L.VmOp * n)()
+        for i, (name, args, b_static) in enumerate(calls):
+            kind, field = L.VM_KINDS[name]
+            ops[i].kind = kind
+            ops[i].b_static = 1 if b_static else 0
+            setattr(ops[i].u, field, args)
+        ws, si = L.C.c_longlong(0), L.C.c_int(0)
+        st = L.lib().fis_vm_plan(L.C.byref(ops), n, 0, L.C.byref(ws), L.C.byref(si))
+        if st != 0:
+            raise ContractViolation(f"fis_vm_plan failed (status {st})")
+        self.calls = calls  # keeps the argument structs (and what they point to) alive
+        self.n_ops = n
+        self.ops_host = ops
+        raw = torch.frombuffer(bytearray(bytes(ops)), dtype=torch.uint8)
+        self.ops_dev = raw.to(lz.dev)
+        self.sync = torch.zeros(si.value, dtype=torch.int32, device=lz.dev)
+        self.ws = torch.empty(max(4, ws.value), dtype=torch.float32, device=lz.dev)
+        self.args = L.VmArgs(self.ops_dev.data_ptr(), n, 0, self.sync.data_ptr(), si.value, self.ws.data_ptr(),
+                             lz.step_dev.data_ptr(), None,
+                             int(os.environ.get("FIS_VM_POLL_NS", "0")), -1, None)
+        self.lz = lz
+        self.trace = None
+
+    def enable_trace(self, on: bool = True):
+        """Per-op [first item start, last item end] globaltimer stamps (profiling)."""
+        if on:
+            self.trace = torch.zeros((self.n_ops, 2), dtype=torch.int64, device=self.lz.dev)
+            self.args.trace = self.trace.data_ptr()
+        else:
+            self.trace, self.args.trace = None, None
+
+    def trace_op(self, j):
+        """Record per-item phase stamps of op j ([n_items][8] globaltimer ns)."""
+        n = self.ops_host[j].n_items
+        self.items_trace = torch.zeros((max(1, n), 16), dtype=torch.int64, device=self.lz.dev)
+        self.args.trace_op, self.args.trace_items = j, self.items_trace.data_ptr()
+
+    def reset_trace(self):
+        if self.trace is not None:
+            self.trace[:, 0].fill_(-1)  # ~0ull: atomicMin start
+            self.trace[:, 1].zero_()
+
+    def read_trace(self):
+        """[(kind, n_items, splits, start_ns, end_ns)] relative to the first op's start."""
+        tr = self.trace.cpu().numpy().view(np.uint64).astype(np.float64)
+        t0 = tr[:, 0].min()
+        return [(k, n, s, tr[i, 0] - t0, tr[i, 1] - t0) for i, (k, n, s) in enumerate(self.items())]
+
+    def items(self):
+        return [(self.ops_host[i].kind, self.ops_host[i].n_items, self.ops_host[i].splits) for i in range(self.n_ops)]
+
+    def run(self):
+        L.call("fis_vm_run", self.args)
+        self.lz.launches += 1
+
 
 class Engine(Launcher):
     """One model (config + precision) resident on one GPU."""
@@ -265,7 +344,8 @@ class Engine(Launcher):
         S = self.scratch(f"S{tag}", (cap, cap), torch.float32)
         P = self.scratch(f"P{tag}", (cap, mp), zero=True)
         # one GEMM for Q|K (row-major) and V (stored transposed as the PV B operand)
-        self.gemm(m, 3 * c, c, a=s, b=DRef(wqkv), d=DRef(qk), n_split=2 * c, d2=DRef(vt, ld=mp), d2_trans=True)
+        self.gemm(m, 3 * c, c, a=s, b=DRef(wqkv), d=DRef(qk), n_split=2 * c, d2=DRef(vt, ld=mp), d2_trans=True,
+                  b_static=True)
         qkr = DRef(qk)
         if self.use_fused_attn(c):
             # S = QK^T, softmax and P.V (+ residual) in one tcgen05 kernel (fis_attn)
@@ -283,12 +363,12 @@ class Engine(Launcher):
         ntp = vt.shape[1]
         cap = self.hw(level)
         q = self.scratch(f"q{tag}", (cap, c))
-        self.gemm(m, c, c, a=x, b=DRef(wq), d=DRef(q))
+        self.gemm(m, c, c, a=x, b=DRef(wq), d=DRef(q), b_static=True)
         if ctrl is None and map_ is None and nt <= 128 and self.fused_xattn:
             # scores + softmax + P.V + residual in one launch (text context <= 128 tokens)
             a = L.XattnArgs(m, c, nt, DRef(q).ref(), DRef(k).ref(), DRef(v).ref(), scale, x.ref(), _r(pre),
                             out.ref(), L.ptr(self.step_dev))
-            L.call("fis_xattn", a)
+            self._call("fis_xattn", a)
             self.launches += 1
             return
         if ctrl is None and map_ is None and self.use_fused_attn(c):
@@ -296,13 +376,13 @@ class Engine(Launcher):
             return
         S = self.scratch(f"Sx{tag}", (cap, ntp), torch.float32)  # ld padded: 16-byte aligned rows
         P = self.scratch(f"Px{tag}", (cap, ntp), zero=True)
-        self.gemm(m, nt, c, a=DRef(q), b=DRef(k), d=DRef(S))
+        self.gemm(m, nt, c, a=DRef(q), b=DRef(k), d=DRef(S), b_static=True)  # text K: per edit
         if ctrl is not None:
             cached, verbatim, pairs = ctrl
             self.softmax(m, nt, ntp, DRef(S), scale, DRef(P), map_, cached=cached, verbatim=verbatim, pairs=pairs)
         else:
             self.softmax(m, nt, ntp, DRef(S), scale, DRef(P), map_)
-        self.gemm(m, c, ntp, a=DRef(P), b=DRef(vt), d=out, res=x, pre=pre)
+        self.gemm(m, c, ntp, a=DRef(P), b=DRef(vt), d=out, res=x, pre=pre, b_static=True)  # text V^T
 
     def use_fused_attn(self, d):
         return self.fused_attn and self.act == torch.bfloat16 and d % 64 == 0
@@ -310,12 +390,12 @@ class Engine(Launcher):
     def attn(self, m, n_keys, d, q: DRef, k: DRef, vt: DRef, scale, res: DRef, out: DRef, pre=None):
         a = L.AttnArgs(m, n_keys, d, d, q.ref(), k.ref(), vt.ref(), float(scale), _r(res), _r(pre), out.ref(),
                        L.ptr(self.step_dev))
-        L.call("fis_attn", a)
+        self._call("fis_attn", a)
         self.launches += 1
 
     def gn_stats(self, x: DRef, hw, c, mean: DRef, var: DRef):
         a = L.GnStatsArgs(hw, c, self.groups, x.ref(), mean.ref(), var.ref(), L.ptr(self.step_dev))
-        L.call("fis_gn_stats", a)
+        self._call("fis_gn_stats", a)
         self.launches += 1
 
     def gn_apply(self, lid, x: DRef, rows, c, mean: DRef, var: DRef, y_norm: DRef | None, y_silu: DRef | None):
@@ -326,22 +406,34 @@ class Engine(Launcher):
         a.gamma, a.beta = L.ptr(gamma), L.ptr(beta)
         a.y_norm, a.y_silu = _r(y_norm), _r(y_silu)
         a.step = L.ptr(self.step_dev)
-        L.call("fis_gn_apply", a)
+        self._call("fis_gn_apply", a)
         self.launches += 1
 
     def pool(self, fv: FeatVal, rows, n, out: DRef):
         a = L.PoolArgs()
         a.n, a.c, a.src, a.rows, a.out = n, fv.c, self.src(fv), L.ptr(rows), out.ref()
         a.step = L.ptr(self.step_dev)
-        L.call("fis_pool2", a)
+        self._call("fis_pool2", a)
         self.launches += 1
 
     def materialize(self, fv: FeatVal, out: DRef):
         a = L.MaterializeArgs(fv.c, self.src(fv), out.ref(), L.ptr(self.step_dev))
-        L.call("fis_materialize", a)
+        self._call("fis_materialize", a)
         self.launches += 1
 
     # ------------------------------------------------------------ one UNet step
+    def record_step(self, plan: "StepPlan") -> VmProgram:
+        """Record one step's launches (nothing runs) and plan them for the step VM."""
+        self.capture = []
+        n0 = self.launches
+        try:
+            self.run_step(plan)
+            calls = self.capture
+        finally:
+            self.capture = None
+            self.launches = n0
+        return VmProgram(self, calls)
+
     def run_step(self, plan: "StepPlan"):
         """Launch one UNet forward + step update (unet.py:430-458,693) for the current device step."""
         vals = {}
@@ -381,7 +473,7 @@ class Engine(Launcher):
         rows, m = plan.rows(level)
         srcs = [self.src(fv, up) for fv, up in inputs]
         self.gemm(m, b.shape[0], b.shape[1], rows=rows, srcs=srcs, out_hw=self.grid(level), b=DRef(b), d=out,
-                  bias=bias, **kw)
+                  bias=bias, b_static=True, **kw)
 
     def _block(self, plan, blk, x: FeatVal, fo):
         """conv -> GN -> SiLU -> +self-attn -> +cross-attn (unet.py:452-458)."""

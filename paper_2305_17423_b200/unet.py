@@ -229,11 +229,14 @@ def _to_nchw(t: torch.Tensor, c, h, w) -> np.ndarray:
 # ---------------------------------------------------------------------------
 
 class _Runner:
-    """Drives Engine steps for t in a range, eagerly or through one captured CUDA graph."""
+    """Drives Engine steps for t in a range: eagerly, through one captured CUDA graph, or (bf16)
+    as one persistent step-VM launch per step (csrc/fis_vm.cu)."""
 
     def __init__(self, eng: Engine, plan, use_graph: bool):
         self.eng, self.plan, self.use_graph = eng, plan, use_graph
         self.graph = None
+        self.vm = None
+        self.launches_per_step = None
 
     def step(self, t: int):
         eng = self.eng
@@ -241,9 +244,17 @@ class _Runner:
         if not self.use_graph:
             eng.run_step(self.plan)
             return
+        if eng.use_vm:
+            if self.vm is None:
+                self.vm = eng.record_step(self.plan)
+                self.launches_per_step = 1
+            self.vm.run()
+            return
         if self.graph is None:
             # warm (allocates scratch), then capture one step; replays read t from step_dev
+            n0 = eng.launches
             eng.run_step(self.plan)
+            self.launches_per_step = eng.launches - n0
             torch.cuda.synchronize()
             s = torch.cuda.Stream()
             s.wait_stream(torch.cuda.current_stream())
