@@ -235,10 +235,13 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_tc_kernel(const fis_gemm_args
             tb.b2[c] = ok && e.bias2 ? load_elem(e.bias2, a.bias2.dtype, n) : 0.f;
             if (a.epi == FIS_EPI_GN_SILU && ok) {
                 const int g = n / e.cpg;
-                tb.mean[c] = e.mean[g];
-                tb.rstd[c] = (float)(1.0 / sqrt((double)e.var[g] + (double)a.eps));
-                tb.gamma[c] = __ldg(a.gamma + n);
-                tb.beta[c] = __ldg(a.beta + n);
+                // cached-stat GN folded into one fma per element: y = v * scale + shift
+                const float rstd = (float)(1.0 / sqrt((double)e.var[g] + (double)a.eps));
+                const float scale = rstd * __ldg(a.gamma + n);
+                tb.mean[c] = scale;
+                tb.rstd[c] = fmaf(-e.mean[g], scale, __ldg(a.beta + n));
+                tb.gamma[c] = 0.f;
+                tb.beta[c] = 0.f;
             } else {
                 tb.mean[c] = 0.f; tb.rstd[c] = 0.f; tb.gamma[c] = 0.f; tb.beta[c] = 0.f;
             }

@@ -142,7 +142,7 @@ __device__ __forceinline__ void row_epilogue(const fis_gemm_args& a, const EpiCt
         // bf16 tensor-core path: cached-stat GN + SiLU in fp32 (the fp32-parity SIMT path,
         // epilogue_store, keeps the reference's f64 arithmetic)
         for (int j = 0; j < 16; j++)
-            y[j] = fmaf((v[j] - tb.mean[c0 + j]) * tb.rstd[c0 + j], tb.gamma[c0 + j], tb.beta[c0 + j]);
+            y[j] = fmaf(v[j], tb.mean[c0 + j], tb.rstd[c0 + j]);  // tables hold GN scale / shift
         if (e.pre2) store_row16(e.pre2, a.pre2.dtype, (long long)orow * a.pre2.ld + n, nvalid, y);
 #pragma unroll
         for (int j = 0; j < 16; j++) v[j] = __fdividef(y[j], 1.0f + __expf(-y[j]));

@@ -25,7 +25,7 @@ namespace fis {
 namespace vm {
 using namespace fis::tc;
 
-constexpr int STAGES = 5, PRODUCERS = 256, THREADS = 288, MMA_WARP = 8;
+constexpr int STAGES = 4, PRODUCERS = 256, THREADS = 288, MMA_WARP = 8;
 constexpr int MAX_BN = 128;
 constexpr int A_BYTES = BM * BK * 2;
 constexpr int B_BYTES = MAX_BN * BK * 2;
@@ -35,7 +35,9 @@ constexpr int EPI = MAX_BN * 32;
 constexpr int SEL = BM * 2 * 9 * 4;
 constexpr int RES_LD = 272;                  // bytes per staged residual row (<= 256 B of data)
 constexpr int RES_BYTES = BM * RES_LD;       // epilogue operand tile (residual / latent rows)
-constexpr int SMEM = STAGES * STAGE + RES_BYTES + 1024;  // dynamic: ring + operand tile (+ alignment slack)
+constexpr int P_BYTES = 2 * BM * 64 * 2;     // attention P tile: 128 rows x 128 keys bf16 (two SW128 chunks)
+constexpr int TMEM_COLS = 512;
+constexpr int SMEM = STAGES * STAGE + RES_BYTES + P_BYTES + 1024;  // dynamic: ring + operand tile + P (+ align)
 constexpr int ELEMS_PER_ITEM = 2048;  // elementwise ops
 constexpr int SOFTMAX_ROWS = 8;       // one warp per row
 constexpr int SBM = 64, SBN = 64, SBK = 16;  // SIMT GEMM tile
@@ -56,6 +58,10 @@ FIS_DEV int ld_acquire(const int* p) {
 struct Shared {
     unsigned char* ring;
     unsigned char* res;  // staged epilogue operand rows [BM][RES_LD]
+    unsigned char* pbuf; // attention P tile
+    uint64_t* s_ready;   // attention: every S block of the item is in TMEM
+    uint64_t* p_ready;   // attention: P block written (256 producer arrivals)
+    uint64_t* p_free;    // attention: the P.V MMAs reading the P tile have completed
     fis_vm_op* op;
     EpiTab tb;
     int* seltab;
@@ -73,7 +79,9 @@ extern __shared__ __align__(1024) unsigned char vm_smem[];
 __shared__ __align__(16) fis_vm_op s_op;
 __shared__ float s_tab[6][MAX_BN];
 __shared__ int s_sel[BM * 2 * 9];
-__shared__ __align__(8) uint64_t s_bar[2 * STAGES + 1];
+__shared__ __align__(8) uint64_t s_bar[2 * STAGES + 4];
+__shared__ __align__(16) fis_gemm_args s_ea;   // attention: epilogue view (out = res + O)
+__shared__ float s_rowstat[2][BM];             // attention: per-row partial max / sum of the two halves
 __shared__ uint32_t s_tmem;
 __shared__ int s_flag;
 
@@ -82,6 +90,7 @@ FIS_DEV Shared carve() {
     const uint32_t a = smem_u32(vm_smem);
     s.ring = vm_smem + ((1024u - (a & 1023u)) & 1023u);
     s.res = s.ring + STAGES * STAGE;
+    s.pbuf = s.res + RES_BYTES;
     s.op = &s_op;
     s.tb.mean = s_tab[0];
     s.tb.rstd = s_tab[1];
@@ -93,6 +102,9 @@ FIS_DEV Shared carve() {
     s.full = s_bar;
     s.empty = s_bar + STAGES;
     s.done = s_bar + 2 * STAGES;
+    s.s_ready = s_bar + 2 * STAGES + 1;
+    s.p_ready = s_bar + 2 * STAGES + 2;
+    s.p_free = s_bar + 2 * STAGES + 3;
     s.tmem_slot = &s_tmem;
     s.flag = &s_flag;
     return s;
@@ -119,13 +131,141 @@ FIS_DEV GemmItem gemm_item(const fis_vm_op& op, int i) {
     return g;
 }
 
+// Attention item i: query tile x value slice. S block j (<= 128 keys) lives in TMEM columns
+// [128 j, 128 j + N_j), the O slice in [TMEM_COLS - dvs, TMEM_COLS).
+struct AttnItem {
+    int m0, c0, dvs, nkb, dch, o_col;
+};
+
+FIS_DEV AttnItem attn_item(const fis_vm_op& op, int i) {
+    AttnItem g;
+    g.dvs = op.bn;
+    g.m0 = (i / op.tiles_n) * BM;
+    g.c0 = (i % op.tiles_n) * op.bn;
+    g.nkb = (op.u.attn.n_keys + 127) / 128;
+    g.dch = op.u.attn.d / 64;
+    g.o_col = TMEM_COLS - op.bn;
+    return g;
+}
+FIS_DEV int attn_nb(int n_keys, int j) { return min(128, n_keys - 128 * j); }
+
+FIS_DEV uint32_t idesc_f16(int M, int N) {
+    return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
+FIS_DEV void mma4(uint32_t d, uint32_t sa, uint32_t sb, uint32_t idesc, bool accumulate) {
+#pragma unroll
+    for (int kk = 0; kk < BK / 16; kk++) {
+        const uint64_t ad = sw128_desc(sa + kk * 32), bd = sw128_desc(sb + kk * 32);
+        const uint32_t acc = (accumulate || kk > 0) ? 1u : 0u;
+        asm volatile(
+            "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+            "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
+            "l"(ad), "l"(bd), "r"(idesc), "r"(acc));
+    }
+}
+
+// TMA: 2D tile of a tensor map (box {64 elems, rows}, SW128) into shared memory; completion is
+// counted in bytes on the stage's full barrier
+FIS_DEV void tma2d(uint32_t dst, const void* tmap, int c0, int c1, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+            dst),
+        "l"(tmap), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+        : "memory");
+}
+FIS_DEV void tma3d(uint32_t dst, const void* tmap, int c0, int c1, int c2, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
+            dst),
+        "l"(tmap), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+        : "memory");
+}
+// expect bytes without arriving (a later arrive completes the phase)
+FIS_DEV void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+// arrive when this thread's prior cp.async land; the pending count is incremented now
+FIS_DEV void cp_async_arrive_inc(uint64_t* bar) {
+    asm volatile("cp.async.mbarrier.arrive.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+// mbarrier wait with a sleep back-off (waiting producers leave issue slots to the TMA / MMA threads)
+FIS_DEV void mbar_wait_backoff(uint64_t* b, uint32_t parity) {
+    uint32_t ok;
+    for (;;) {
+        asm volatile(
+            "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(ok)
+            : "r"(smem_u32(b)), "r"(parity)
+            : "memory");
+        if (ok) return;
+        __nanosleep(32);
+    }
+}
+FIS_DEV void expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+FIS_DEV const void* tmap_at(const fis_vm_args& va, int idx) {
+    return idx >= 0 ? (const void*)((const char*)va.tmaps + 128 * (long long)idx) : nullptr;
+}
+
+FIS_DEV void mma_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+                 : "memory");
+}
+
 // ---------------------------------------------------------------------------------- MMA warp
 FIS_DEV void mma_role(const fis_vm_args& va, const Shared& sh, uint32_t tmem, int lane) {
     const int G = gridDim.x, cta = blockIdx.x;
-    uint32_t it = 0;
+    uint32_t it = 0, pb = 0;
     const uint32_t sbase = smem_u32(sh.ring);
     for (int j = 0; j < va.n_ops; j++) {
         const fis_vm_op* op = va.ops + j;
+        if (op->kind == FIS_VM_ATTN) {
+            for (int i = (cta - op->cta0 + G) % G; i < op->n_items; i += G) {
+                const AttnItem g = attn_item(*op, i);
+                const int n_keys = op->u.attn.n_keys;
+                for (int kc = 0; kc < g.dch; kc++) {  // S_j += Q_kc K_j,kc^T, Q chunk shared by every j
+                    int sq_slot = 0;
+                    for (int jb = 0; jb < g.nkb; jb++, it++) {
+                        const int s = it % STAGES;
+                        if (jb == 0) sq_slot = s;
+                        mbar_wait(sh.full + s, (it / STAGES) & 1);
+                        tc_fence_after();
+                        if (lane == 0) {
+                            const uint32_t id = idesc_f16(BM, (attn_nb(n_keys, jb) + 15) & ~15);
+                            mma4(tmem + 128 * jb, sbase + sq_slot * STAGE, sbase + s * STAGE + A_BYTES, id, kc > 0);
+                            if (jb > 0) mma_commit(sh.empty + s);
+                            if (jb == g.nkb - 1) mma_commit(sh.empty + sq_slot);
+                        }
+                        __syncwarp();
+                    }
+                }
+                if (lane == 0) mma_commit(sh.s_ready);
+                __syncwarp();
+                const uint32_t ido = idesc_f16(BM, g.dvs), pbase = smem_u32(sh.pbuf);
+                for (int jb = 0; jb < g.nkb; jb++, pb++) {  // O += P_j V_j
+                    mbar_wait(sh.p_ready, pb & 1);
+                    tc_fence_after();
+                    const int nch = (attn_nb(n_keys, jb) + 63) / 64;
+                    for (int c = 0; c < nch; c++, it++) {
+                        const int s = it % STAGES;
+                        mbar_wait(sh.full + s, (it / STAGES) & 1);
+                        tc_fence_after();
+                        if (lane == 0) {
+                            mma4(tmem + g.o_col, pbase + c * (BM * 128), sbase + s * STAGE + A_BYTES, ido, jb > 0 || c > 0);
+                            mma_commit(sh.empty + s);
+                        }
+                        __syncwarp();
+                    }
+                    if (lane == 0) mma_commit(sh.p_free);
+                    __syncwarp();
+                }
+                if (lane == 0) mma_commit(sh.done);
+                __syncwarp();
+            }
+            continue;
+        }
         if (op->kind != FIS_VM_GEMM || op->impl != 2) continue;
         const int n_items = op->n_items;
         for (int i = (cta - op->cta0 + G) % G; i < n_items; i += G) {
@@ -177,7 +317,9 @@ FIS_DEV void tmem_ld16(uint32_t taddr, float* v) {
 
 struct ProdState {
     uint32_t it;      // ring slot sequence number (matches the MMA warp)
-    uint32_t items;   // tcgen05 GEMM items run (parity of the done barrier)
+    uint32_t items;   // tcgen05 items run (parity of the done barrier)
+    uint32_t attn;    // attention items run (parity of s_ready)
+    uint32_t pb;      // attention P blocks written (parity of p_ready / p_free, matches the MMA warp)
 };
 
 FIS_DEV unsigned long long gtimer() {
@@ -218,7 +360,11 @@ FIS_DEV void wait_dep(const fis_vm_args& va, const fis_vm_op& op, int j, bool& w
         trace_start(va, j, tid);
         return;
     }
-    if (tid == 0) spin_until(va.sync + 1 + op.dep, op.dep_target, va.poll_ns > 0 ? va.poll_ns : 32);
+    if (tid == 0) {
+        spin_until(va.sync + 1 + op.dep, op.dep_target, va.poll_ns > 0 ? va.poll_ns : 32);
+        // the operands were written through the generic proxy; thread 0 reads them with TMA
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+    }
     trace_start(va, j, tid);
     pbar();
 }
@@ -253,10 +399,13 @@ FIS_DEV void stage_tables(const fis_gemm_args& a, const EpiCtx& e, const Shared&
         sh.tb.b2[c] = ok && e.bias2 ? load_elem(e.bias2, a.bias2.dtype, n) : 0.f;
         if (a.epi == FIS_EPI_GN_SILU && ok) {
             const int gi = n / e.cpg;
-            sh.tb.mean[c] = e.mean[gi];
-            sh.tb.rstd[c] = (float)(1.0 / sqrt((double)e.var[gi] + (double)a.eps));
-            sh.tb.gamma[c] = __ldg(a.gamma + n);
-            sh.tb.beta[c] = __ldg(a.beta + n);
+            // cached-stat GN folded into one fma per element: y = v * scale + shift
+            const float rstd = (float)(1.0 / sqrt((double)e.var[gi] + (double)a.eps));
+            const float scale = rstd * __ldg(a.gamma + n);
+            sh.tb.mean[c] = scale;
+            sh.tb.rstd[c] = fmaf(-e.mean[gi], scale, __ldg(a.beta + n));
+            sh.tb.gamma[c] = 0.f;
+            sh.tb.beta[c] = 0.f;
         } else {
             sh.tb.mean[c] = 0.f; sh.tb.rstd[c] = 0.f; sh.tb.gamma[c] = 0.f; sh.tb.beta[c] = 0.f;
         }
@@ -364,7 +513,7 @@ FIS_DEV void epilogue8(const fis_gemm_args& a, const EpiCtx& e, const EpiTab& tb
         float y[8];
 #pragma unroll
         for (int k = 0; k < 8; k++)
-            y[k] = fmaf((v[k] - tb.mean[c0 + k]) * tb.rstd[c0 + k], tb.gamma[c0 + k], tb.beta[c0 + k]);
+            y[k] = fmaf(v[k], tb.mean[c0 + k], tb.rstd[c0 + k]);  // scale / shift (stage_tables)
         if (e.pre2) store8(e.pre2, a.pre2.dtype, (long long)orow * a.pre2.ld + n, nvalid, y);
 #pragma unroll
         for (int k = 0; k < 8; k++) v[k] = __fdividef(y[k], 1.0f + __expf(-y[k]));
@@ -431,22 +580,50 @@ FIS_DEV void gemm_tc_item(const fis_vm_args& va, const Shared& sh, int j, int i,
     const char* bbase = ref_base(a.b, t);
 
     VM_STAMP(0);
+    // Ring protocol: each slot's full barrier expects ONE arrival (thread 0) plus the TMA bytes;
+    // cp.async loads register themselves with incrementing cp.async.mbarrier.arrive before a
+    // producer barrier that precedes thread 0's arrival.  TMA-only k-blocks are issued by
+    // thread 0 alone; the other producers go straight to the epilogue.
     // ---- weight tiles of the first stages + static epilogue tables: independent of the previous
     //      op when B is static (weights / per-edit text K/V)
     if (!op.b_static) wait_dep(va, op, j, waited, tid);
+    const void* tma_b = tmap_at(va, op.tmap_b);
+    const void* tma_a = tmap_at(va, op.tmap_a);
+    const void* tma_a2 = tmap_at(va, op.tmap_a2);
+    const bool conv = a.a_mode == FIS_A_CONV3X3;
+    const int cin = conv ? a.src[0].c + (a.nsrc > 1 ? a.src[1].c : 0) : a.k;
+    const int src0c = a.nsrc > 0 ? a.src[0].c : 0;
+    // k-block q takes A from a TMA map?
+    auto a_map = [&](int k0) -> const void* {
+        if (!conv) return tma_a;
+        const int c = k0 % cin;
+        return c >= src0c ? tma_a2 : tma_a;
+    };
+    const uint32_t b_bytes = (uint32_t)(BK * BN * 2);
     const int npre = min(g.nk, STAGES);
-    for (int q = 0; q < npre; q++) {
-        const uint32_t sq = ps.it + q;
-        const int s = sq % STAGES;
-        if (sq >= STAGES) mbar_wait(sh.empty + s, ((sq / STAGES) & 1) ^ 1);
-        issue_b(a, g, bbase, sbase + s * STAGE + A_BYTES, (g.kb0 + q) * BK, ar, j0);
+    if (tma_b) {
+        if (tid == 0)
+            for (int q = 0; q < npre; q++) {
+                const uint32_t sq = ps.it + q;
+                const int s = sq % STAGES;
+                if (sq >= STAGES) mbar_wait_backoff(sh.empty + s, ((sq / STAGES) & 1) ^ 1);
+                mbar_expect_tx(sh.full + s, b_bytes);
+                tma2d(sbase + s * STAGE + A_BYTES, tma_b, (g.kb0 + q) * BK, g.n0, sh.full + s);
+            }
+    } else {
+        for (int q = 0; q < npre; q++) {
+            const uint32_t sq = ps.it + q;
+            const int s = sq % STAGES;
+            if (sq >= STAGES) mbar_wait_backoff(sh.empty + s, ((sq / STAGES) & 1) ^ 1);
+            issue_b(a, g, bbase, sbase + s * STAGE + A_BYTES, (g.kb0 + q) * BK, ar, j0);
+        }
     }
     if (op.b_static) stage_tables(a, make_epi(a, t), sh, g.n0, g.bn, tid);
     // ---- static gather metadata (row/index lists are fixed for the whole edit)
     const int r = g.m0 + ar;
     const bool row_valid = r < a.m;
     const int row_p = row_valid ? (a.rows ? __ldg(a.rows + r) : r) : 0;
-    if (a.a_mode == FIS_A_CONV3X3 && half_id < a.nsrc) build_sel(a, row_p, half_id, sh.seltab + (ar * 2 + half_id) * 9);
+    if (conv && half_id < a.nsrc) build_sel(a, row_p, half_id, sh.seltab + (ar * 2 + half_id) * 9);
     __syncwarp();  // the two threads of a row each built one segment's select table
     VM_STAMP(1);
     wait_dep(va, op, j, waited, tid);
@@ -457,17 +634,65 @@ FIS_DEV void gemm_tc_item(const fis_vm_args& va, const Shared& sh, int j, int i,
     const char* c0p = a.nsrc > 0 && a.src[0].cache.ptr ? ref_base(a.src[0].cache, t) : nullptr;
     const char* f1 = a.nsrc > 1 && a.src[1].fresh.ptr ? ref_base(a.src[1].fresh, t) : nullptr;
     const char* c1p = a.nsrc > 1 && a.src[1].cache.ptr ? ref_base(a.src[1].cache, t) : nullptr;
-    const int cin = a.a_mode == FIS_A_CONV3X3 ? a.src[0].c + (a.nsrc > 1 ? a.src[1].c : 0) : a.k;
-    const int src0c = a.nsrc > 0 ? a.src[0].c : 0;
     const int* mysel = sh.seltab + ar * 2 * 9;
+    const bool mixed = conv && a.nsrc > 1 && ((tma_a != nullptr) != (tma_a2 != nullptr));
     for (int q = 0; q < g.nk; q++) {
         const uint32_t sq = ps.it + q;
         const int s = sq % STAGES;
         const uint32_t sa = sbase + s * STAGE;
         const int k0 = (g.kb0 + q) * BK;
+        const void* tm = tma_b ? a_map(k0) : nullptr;  // TMA A only together with TMA B
+        if (tm && mixed) {
+            // ---- conv with one TMA segment and one gathered segment: every producer stays in step
+            if (sq >= STAGES) mbar_wait_backoff(sh.empty + s, ((sq / STAGES) & 1) ^ 1);
+            if (tid == 0) {
+                if (q >= npre) {
+                    mbar_expect_tx(sh.full + s, b_bytes);
+                    tma2d(sa + A_BYTES, tma_b, k0, g.n0, sh.full + s);
+                }
+                const int tap = k0 / cin;
+                const int c = k0 - tap * cin;
+                const int cs = c >= src0c ? c - src0c : c;
+                mbar_expect_tx(sh.full + s, (uint32_t)(BM * BK * 2));
+                tma3d(sa, tm, cs, tap % 3 - 1, g.m0 / a.out_w + tap / 3 - 1, sh.full + s);
+            }
+            pbar();
+            if (tid == 0) mbar_arrive(sh.full + s);
+            continue;
+        }
+        if (tm) {
+            // ---- thread 0 alone: (B if not prefetched) + A via TMA, one arrival with the bytes
+            if (tid == 0) {
+                if (q >= npre) {
+                    mbar_wait_backoff(sh.empty + s, ((sq / STAGES) & 1) ^ 1);
+                    mbar_expect_tx(sh.full + s, b_bytes);
+                    tma2d(sa + A_BYTES, tma_b, k0, g.n0, sh.full + s);
+                }
+                expect_tx(sh.full + s, (uint32_t)(BM * BK * 2));
+                if (conv) {
+                    const int tap = k0 / cin;
+                    const int c = k0 - tap * cin;
+                    const int cs = c >= src0c ? c - src0c : c;
+                    tma3d(sa, tm, cs, tap % 3 - 1, g.m0 / a.out_w + tap / 3 - 1, sh.full + s);
+                } else {
+                    tma2d(sa, tm, k0, g.m0, sh.full + s);
+                }
+                if (q == 0) VM_STAMP(8);
+            }
+            continue;
+        }
+        // ---- every producer: gathered A rows (and B rows without TMA) with cp.async; every thread
+        //      waits for the slot itself (only thread 0 waited for the TMA-prefetched B stages)
+        if (sq >= STAGES) mbar_wait_backoff(sh.empty + s, ((sq / STAGES) & 1) ^ 1);
         if (q >= npre) {
-            mbar_wait(sh.empty + s, ((sq / STAGES) & 1) ^ 1);
-            issue_b(a, g, bbase, sa + A_BYTES, k0, ar, j0);
+            if (tma_b) {
+                if (tid == 0) {
+                    mbar_expect_tx(sh.full + s, b_bytes);
+                    tma2d(sa + A_BYTES, tma_b, k0, g.n0, sh.full + s);
+                }
+            } else {
+                issue_b(a, g, bbase, sa + A_BYTES, k0, ar, j0);
+            }
         }
         const char* src = nullptr;
         if (row_valid) {
@@ -488,10 +713,12 @@ FIS_DEV void gemm_tc_item(const fis_vm_args& va, const Shared& sh, int j, int i,
         }
 #pragma unroll
         for (int jj = j0; jj < j0 + 4; jj++) {
-            const bool ok = src != nullptr && (a.a_mode == FIS_A_CONV3X3 || k0 + jj * 8 < a.k);
+            const bool ok = src != nullptr && (conv || k0 + jj * 8 < a.k);
             cp_async16(sa + sw128_off(ar, jj), ok ? (const void*)(src + jj * 16) : (const void*)bbase, ok);
         }
-        cp_async_arrive_noinc(sh.full + s);
+        cp_async_arrive_inc(sh.full + s);
+        pbar();  // every producer's arrival is registered before thread 0's
+        if (tid == 0) mbar_arrive(sh.full + s);
         if (q == 0) VM_STAMP(8);
     }
     ps.it += g.nk;
@@ -500,6 +727,116 @@ FIS_DEV void gemm_tc_item(const fis_vm_args& va, const Shared& sh, int j, int i,
     const bool staged = stage_operand(a, sh, g, t, tid);
     VM_STAMP(3);
     gemm_tc_epilogue<BN>(va, sh, j, i, g, ps, tmem, tid, op.b_static != 0, staged);
+}
+
+// Fast epilogue (bf16 row-major output, no recording stores): thread -> one 8-column chunk,
+// rows strided by PRODUCERS / (BN/8); bias / time-bias / GN parameters of its 8 columns are
+// loaded once into registers; accumulators come from the staging tile (S == 1) or the split
+// partials (S > 1, summed in split order); the residual / latent rows from the staged operand.
+template <int BN, int MODE>
+FIS_DEV void fast_epilogue(const fis_gemm_args& a, const EpiCtx& e, const Shared& sh, const GemmItem& g,
+                           const float* stage, const float* wsb, long long tile_floats, int S, int r0, int nrows,
+                           bool staged, int tid) {
+    constexpr int CH = BN / 8, RSTEP = PRODUCERS / CH, PLD = BN + 4;
+    const int ch = tid % CH, cb = ch * 8, n = g.n0 + cb;
+    if (n >= a.n) return;
+    const int nvalid = min(8, a.n - n);
+    float bias[8], b2[8], gscale[8], gshift[8];
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+        bias[k] = sh.tb.bias[cb + k];
+        b2[k] = sh.tb.b2[cb + k];
+        if (MODE == FIS_EPI_GN_SILU) { gscale[k] = sh.tb.mean[cb + k]; gshift[k] = sh.tb.rstd[cb + k]; }
+    }
+    const float alpha = a.alpha, step_scale = a.step_scale;
+    const bool has_b2 = e.bias2 != nullptr, has_x = staged;
+    const int xdt = MODE == FIS_EPI_STEP ? a.lat.dtype : a.res.dtype;
+    const int xesz = xdt == FIS_BF16 ? 2 : 4;
+    __nv_bfloat16* dst = (__nv_bfloat16*)e.d + n;
+    const int dld = a.d.ld;
+    for (int rr = tid / CH; rr < nrows; rr += RSTEP) {
+        const int row = r0 + rr;
+        float v[8];
+        if (S == 1) {
+            const float4 f0 = *(const float4*)(stage + row * PLD + cb);
+            const float4 f1 = *(const float4*)(stage + row * PLD + cb + 4);
+            v[0] = f0.x; v[1] = f0.y; v[2] = f0.z; v[3] = f0.w; v[4] = f1.x; v[5] = f1.y; v[6] = f1.z; v[7] = f1.w;
+        } else {
+#pragma unroll
+            for (int k = 0; k < 8; k++) v[k] = 0.f;
+            const float* p = wsb + row * BN + cb;
+            int zz = 0;
+            for (; zz + 3 <= S; zz += 3) {  // 6 float4 loads in flight, summed in split order
+                float4 f[3][2];
+#pragma unroll
+                for (int q = 0; q < 3; q++)
+#pragma unroll
+                    for (int w = 0; w < 2; w++) f[q][w] = __ldcg((const float4*)(p + (zz + q) * tile_floats) + w);
+#pragma unroll
+                for (int q = 0; q < 3; q++)
+#pragma unroll
+                    for (int w = 0; w < 2; w++) {
+                        v[4 * w] += f[q][w].x; v[4 * w + 1] += f[q][w].y;
+                        v[4 * w + 2] += f[q][w].z; v[4 * w + 3] += f[q][w].w;
+                    }
+            }
+            for (; zz < S; zz++) {
+#pragma unroll
+                for (int w = 0; w < 2; w++) {
+                    const float4 f = __ldcg((const float4*)(p + zz * tile_floats) + w);
+                    v[4 * w] += f.x; v[4 * w + 1] += f.y; v[4 * w + 2] += f.z; v[4 * w + 3] += f.w;
+                }
+            }
+        }
+        float x[8];
+        if (has_x) {
+            const unsigned char* xr = sh.res + row * RES_LD + cb * xesz;
+            if (xdt == FIS_BF16) {
+                const uint4 u = *(const uint4*)xr;
+                const __nv_bfloat162* h = (const __nv_bfloat162*)&u;
+#pragma unroll
+                for (int k = 0; k < 4; k++) {
+                    const float2 f = __bfloat1622float2(h[k]);
+                    x[2 * k] = f.x; x[2 * k + 1] = f.y;
+                }
+            } else {
+                const float4 a0 = *(const float4*)xr, a1 = *(const float4*)(xr + 16);
+                x[0] = a0.x; x[1] = a0.y; x[2] = a0.z; x[3] = a0.w; x[4] = a1.x; x[5] = a1.y; x[6] = a1.z; x[7] = a1.w;
+            }
+        }
+        // same operations, same order as fis::tc::row_epilogue
+#pragma unroll
+        for (int k = 0; k < 8; k++) v[k] = __fadd_rn(v[k] * alpha, bias[k]);
+        if (has_b2) {
+#pragma unroll
+            for (int k = 0; k < 8; k++) v[k] = __fadd_rn(v[k], b2[k]);
+        }
+        if (MODE == FIS_EPI_GN_SILU) {
+#pragma unroll
+            for (int k = 0; k < 8; k++) {
+                const float y = fmaf(v[k], gscale[k], gshift[k]);
+                v[k] = __fdividef(y, 1.0f + __expf(-y));
+            }
+        } else if (MODE == FIS_EPI_STEP) {
+#pragma unroll
+            for (int k = 0; k < 8; k++) v[k] = __fsub_rn(x[k], __fmul_rn(step_scale, v[k]));
+        }
+        if (MODE != FIS_EPI_STEP && has_x) {
+#pragma unroll
+            for (int k = 0; k < 8; k++) v[k] = __fadd_rn(v[k], x[k]);
+        }
+        __nv_bfloat16* p = dst + (long long)(g.m0 + row) * dld;
+        if (nvalid == 8) {
+            uint4 u;
+            __nv_bfloat162* h = (__nv_bfloat162*)&u;
+#pragma unroll
+            for (int k = 0; k < 4; k++) h[k] = __floats2bfloat162_rn(v[2 * k], v[2 * k + 1]);
+            *(uint4*)p = u;
+        } else {
+#pragma unroll
+            for (int k = 0; k < 8; k++) if (k < nvalid) p[k] = __float2bfloat16_rn(v[k]);
+        }
+    }
 }
 
 // Epilogue of one tcgen05 GEMM item (separate frame: the gather pointers above are dead here).
@@ -522,7 +859,7 @@ FIS_DEV void gemm_tc_epilogue(const fis_vm_args& va, const Shared& sh, int j, in
     const EpiCtx e = make_epi(a, t);
     if (!tables_done) stage_tables(a, e, sh, g.n0, g.bn, tid);
     VM_STAMP(4);
-    mbar_wait(sh.done, ps.items & 1);
+    mbar_wait_backoff(sh.done, ps.items & 1);
     ps.items++;
     tc_fence_after();
     VM_STAMP(5);
@@ -579,6 +916,21 @@ FIS_DEV void gemm_tc_epilogue(const fis_vm_args& va, const Shared& sh, int j, in
     const int nrows = min(r1, a.m - g.m0) - r0;
     const bool trans = a.d_trans || (a.n_split > 0 && g.n0 >= a.n_split);
     const int n_items = nrows > 0 ? nrows * chunks : 0;
+    // fast path: thread = fixed 8-column chunk x rows strided by PRODUCERS/chunks; the column
+    // parameters live in registers, operands come from shared memory
+    if (!trans && !a.d_rows && (staged || (!e.res && a.epi != FIS_EPI_STEP)) && !e.pre && !e.pre2 &&
+        a.d.dtype == FIS_BF16 && (a.d.ld % 8) == 0 && (((uintptr_t)e.d) & 15) == 0 && (g.n0 % 8) == 0) {
+        if (a.epi == FIS_EPI_GN_SILU)
+            fast_epilogue<BN, FIS_EPI_GN_SILU>(a, e, sh, g, stage, wsb, tile_floats, S, r0, nrows, staged, tid);
+        else if (a.epi == FIS_EPI_STEP)
+            fast_epilogue<BN, FIS_EPI_STEP>(a, e, sh, g, stage, wsb, tile_floats, S, r0, nrows, staged, tid);
+        else
+            fast_epilogue<BN, FIS_EPI_NONE>(a, e, sh, g, stage, wsb, tile_floats, S, r0, nrows, staged, tid);
+        VM_STAMP(6);
+        signal_done(va, j, tid);
+        VM_STAMP(7);
+        return;
+    }
     constexpr int IB = 2;  // items per thread in flight (their global reads issued together)
     long long cy_load = 0, cy_epi = 0, cy0 = clock64();
     for (int base = tid; base < n_items; base += IB * PRODUCERS) {
@@ -650,6 +1002,232 @@ FIS_DEV void gemm_tc_epilogue(const fis_vm_args& va, const Shared& sh, int j, in
         va.trace_items[16 * i + 12] = cy_load;
         va.trace_items[16 * i + 13] = cy_epi;
         va.trace_items[16 * i + 14] = clock64() - cy0;
+    }
+    VM_STAMP(6);
+    signal_done(va, j, tid);
+    VM_STAMP(7);
+}
+
+// ---------------------------------------------------------------------------------- attention
+// One item: out[m0:m0+128, c0:c0+dvs] = res + softmax(Q K^T * scale) V for a 128-query tile and
+// a value slice (sparse.py:265-338, tensors.py:183-200, unet.py:456-457), in one CTA:
+//   S_j = Q K_j^T for every 128-key block j into TMEM (keys <= 512 - dvs), exact row max / sum
+//   over all blocks (thread = row half), then per block P_j = exp(S_j*scale - m) / l -> bf16
+//   SW128 tile in shared memory -> O += P_j V_j on the tensor core; epilogue adds the residual.
+template <int DVS>
+FIS_DEV void attn_item_run(const fis_vm_args& va, const Shared& sh, int j, int i, ProdState& ps, bool& waited,
+                           uint32_t tmem, int tid) {
+    const fis_vm_op& op = *sh.op;
+    const fis_attn_args& a = op.u.attn;
+    const AttnItem g = attn_item(op, i);
+    const int t = s_step;
+    const int warp = tid >> 5, lane = tid & 31;
+    const int ar = tid >> 1, j0 = (tid & 1) * 4;
+    const uint32_t sbase = smem_u32(sh.ring);
+    // epilogue view of the output: a GEMM-style epilogue over [m, dv] with the residual
+    if (tid == 0) {
+        fis_gemm_args& e = s_ea;
+        memset(&e, 0, sizeof(e));
+        e.m = a.m; e.n = a.dv; e.k = 1; e.alpha = 1.f; e.epi = FIS_EPI_NONE;
+        e.res = a.res; e.pre = a.pre; e.d = a.out;
+    }
+    for (int c = tid; c < DVS; c += PRODUCERS) {
+        sh.tb.bias[c] = 0.f; sh.tb.b2[c] = 0.f; sh.tb.mean[c] = 0.f; sh.tb.rstd[c] = 0.f;
+    }
+    VM_STAMP(0);
+    wait_dep(va, op, j, waited, tid);  // Q, K, V^T and the residual come from earlier ops
+    pbar();                            // s_ea visible
+    GemmItem ge;
+    ge.z = 0; ge.tile = 0; ge.n0 = g.c0; ge.m0 = g.m0; ge.kb0 = 0; ge.nk = 0; ge.bn = DVS;
+    VM_STAMP(2);
+    const char* qb = ref_base(a.q, t);
+    const char* kb = ref_base(a.k, t);
+    const char* vb = ref_base(a.vt, t);
+    const int n_keys = a.n_keys;
+    const void* tq = tmap_at(va, op.tmap_a);
+    const void* tk = tmap_at(va, op.tmap_b);
+    const void* tv = tmap_at(va, op.tmap_a2);
+    // ---- S phase loads, d-chunk major: slot (kc, jb) carries K chunk (jb, kc); slot (kc, 0) also
+    //      carries Q chunk kc, which the MMAs of every key block of that chunk read
+    const int qr = g.m0 + ar;
+    if (tq && tk) {
+        if (tid == 0) {
+            uint32_t sq = ps.it;
+            for (int kc = 0; kc < g.dch; kc++)
+                for (int jb = 0; jb < g.nkb; jb++, sq++) {
+                    const int s = sq % STAGES;
+                    if (sq >= STAGES) mbar_wait_backoff(sh.empty + s, ((sq / STAGES) & 1) ^ 1);
+                    const uint32_t sa = sbase + s * STAGE;
+                    expect_tx(sh.full + s, (uint32_t)(BM * BK * 2) * (jb == 0 ? 2u : 1u));
+                    if (jb == 0) tma2d(sa, tq, kc * 64, g.m0, sh.full + s);
+                    tma2d(sa + A_BYTES, tk, kc * 64, 128 * jb, sh.full + s);
+                }
+        }
+        ps.it += g.dch * g.nkb;
+    } else {
+        for (int kc = 0; kc < g.dch; kc++)
+            for (int jb = 0; jb < g.nkb; jb++) {
+                const int key = 128 * jb + ar;
+                const uint32_t sq = ps.it++;
+                const int s = sq % STAGES;
+                if (sq >= STAGES) mbar_wait_backoff(sh.empty + s, ((sq / STAGES) & 1) ^ 1);
+                const uint32_t sa = sbase + s * STAGE, sb = sa + A_BYTES;
+                const char* qs = qb + ((long long)qr * a.q.ld + kc * 64) * 2;
+                const char* ks = kb + ((long long)key * a.k.ld + kc * 64) * 2;
+#pragma unroll
+                for (int u = j0; u < j0 + 4; u++) {
+                    if (jb == 0)
+                        cp_async16(sa + sw128_off(ar, u), qr < a.m ? (const void*)(qs + 16 * u) : (const void*)qb,
+                                   qr < a.m);
+                    cp_async16(sb + sw128_off(ar, u), key < n_keys ? (const void*)(ks + 16 * u) : (const void*)qb,
+                               key < n_keys);
+                }
+                cp_async_arrive_inc(sh.full + s);
+                pbar();
+                if (tid == 0) mbar_arrive(sh.full + s);
+            }
+    }
+    const bool staged = stage_operand(s_ea, sh, ge, t, tid);  // residual rows, land during the MMAs
+    VM_STAMP(3);
+    // ---- exact softmax statistics over every key block (thread = row lr, key half hf)
+    mbar_wait_backoff(sh.s_ready, ps.attn & 1);
+    ps.attn++;
+    tc_fence_after();
+    const int quarter = warp & 3, hf = warp >> 2, lr = quarter * 32 + lane;
+    const uint32_t trow = tmem + ((uint32_t)(quarter * 32) << 16);
+    const float scale = a.scale;
+    float mx = -INFINITY;
+    for (int jb = 0; jb < g.nkb; jb++) {
+        const int k0 = 128 * jb + 64 * hf;
+#pragma unroll 1
+        for (int q = 0; q < 4; q++) {
+            if (k0 + 16 * q >= n_keys) break;
+            float v[16];
+            tmem_ld16(trow + 128 * jb + 64 * hf + 16 * q, v);
+#pragma unroll
+            for (int u = 0; u < 16; u++)
+                if (k0 + 16 * q + u < n_keys) mx = fmaxf(mx, v[u] * scale);
+        }
+    }
+    s_rowstat[hf][lr] = mx;
+    pbar();
+    mx = fmaxf(s_rowstat[0][lr], s_rowstat[1][lr]);
+    float sum = 0.f;
+    for (int jb = 0; jb < g.nkb; jb++) {
+        const int k0 = 128 * jb + 64 * hf;
+#pragma unroll 1
+        for (int q = 0; q < 4; q++) {
+            if (k0 + 16 * q >= n_keys) break;
+            float v[16];
+            tmem_ld16(trow + 128 * jb + 64 * hf + 16 * q, v);
+#pragma unroll
+            for (int u = 0; u < 16; u++)
+                if (k0 + 16 * q + u < n_keys) sum += expf(v[u] * scale - mx);
+        }
+    }
+    pbar();  // both halves have read the max
+    s_rowstat[hf][lr] = sum;
+    pbar();
+    const float inv = 1.0f / (s_rowstat[0][lr] + s_rowstat[1][lr]);
+    VM_STAMP(4);
+    // ---- per key block: P_j -> shared memory (SW128 K-major, chunk hf = keys [64 hf, 64 hf + 64)), then V_j
+    const int vr = g.c0 + ar;  // value channel row of V^T loaded by this thread
+    for (int jb = 0; jb < g.nkb; jb++) {
+        if (ps.pb > 0) mbar_wait_backoff(sh.p_free, (ps.pb - 1) & 1);  // the previous P.V MMAs are done with the tile
+        tc_fence_after();
+        const int k0 = 128 * jb + 64 * hf;
+        unsigned char* pt = sh.pbuf + hf * (BM * 128);
+#pragma unroll 1
+        for (int q = 0; q < 4; q++) {
+            float v[16];
+            if (k0 + 16 * q < n_keys) tmem_ld16(trow + 128 * jb + 64 * hf + 16 * q, v);
+            uint4 pk[2];
+            __nv_bfloat162* h = (__nv_bfloat162*)pk;
+#pragma unroll
+            for (int u = 0; u < 8; u++) {
+                const int kk = k0 + 16 * q + 2 * u;
+                const float p0 = kk < n_keys ? expf(v[2 * u] * scale - mx) * inv : 0.f;
+                const float p1 = kk + 1 < n_keys ? expf(v[2 * u + 1] * scale - mx) * inv : 0.f;
+                h[u] = __floats2bfloat162_rn(p0, p1);
+            }
+            *(uint4*)(pt + sw128_off(lr, 2 * q)) = pk[0];
+            *(uint4*)(pt + sw128_off(lr, 2 * q + 1)) = pk[1];
+        }
+        fence_async_smem();  // generic-proxy P writes -> tensor-core reads
+        tc_fence_before();
+        mbar_arrive(sh.p_ready);
+        ps.pb++;
+        // V^T rows (value channels) x 64-key chunks of block j
+        const int nch = (attn_nb(n_keys, jb) + 63) / 64;
+        if (tv) {
+            if (tid == 0)
+                for (int c = 0; c < nch; c++) {
+                    const uint32_t sq = ps.it + c;
+                    const int s = sq % STAGES;
+                    if (sq >= STAGES) mbar_wait_backoff(sh.empty + s, ((sq / STAGES) & 1) ^ 1);
+                    expect_tx(sh.full + s, (uint32_t)(BK * DVS * 2));
+                    tma2d(sbase + s * STAGE + A_BYTES, tv, 128 * jb + 64 * c, g.c0, sh.full + s);
+                }
+            ps.it += nch;
+        } else {
+            for (int c = 0; c < nch; c++) {
+                const uint32_t sq = ps.it++;
+                const int s = sq % STAGES;
+                if (sq >= STAGES) mbar_wait_backoff(sh.empty + s, ((sq / STAGES) & 1) ^ 1);
+                const uint32_t sb = sbase + s * STAGE + A_BYTES;
+                const int kv0 = 128 * jb + 64 * c;
+                if (ar < DVS) {
+                    const char* vs = vb + ((long long)vr * a.vt.ld + kv0) * 2;
+#pragma unroll
+                    for (int u = j0; u < j0 + 4; u++) {
+                        const bool ok = vr < a.dv && kv0 + 8 * u < n_keys;
+                        cp_async16(sb + sw128_off(ar, u), ok ? (const void*)(vs + 16 * u) : (const void*)vb, ok);
+                    }
+                }
+                cp_async_arrive_inc(sh.full + s);
+                pbar();
+                if (tid == 0) mbar_arrive(sh.full + s);
+            }
+        }
+    }
+    // ---- epilogue: O slice (TMEM) -> staging -> + residual -> bf16 rows
+    mbar_wait_backoff(sh.done, ps.items & 1);
+    ps.items++;
+    tc_fence_after();
+    VM_STAMP(5);
+    constexpr int PLD = DVS + 4, hc = DVS / 2;
+    float* stage = (float*)sh.ring;
+    {
+        const uint32_t taddr = trow + g.o_col + hf * hc;
+        float* dst = stage + lr * PLD + hf * hc;
+#pragma unroll 1
+        for (int q = 0; q < hc / 16; q++) {
+            float v[16];
+            tmem_ld16(taddr + 16 * q, v);
+#pragma unroll
+            for (int w = 0; w < 4; w++)
+                *(float4*)(dst + 16 * q + 4 * w) = make_float4(v[4 * w], v[4 * w + 1], v[4 * w + 2], v[4 * w + 3]);
+        }
+        tc_fence_before();
+    }
+    if (staged) cp_wait<0>();
+    pbar();
+    const EpiCtx e = make_epi(s_ea, t);
+    const int nrows = min(BM, a.m - g.m0);
+    if (!e.pre && a.out.dtype == FIS_BF16 && (a.out.ld % 8) == 0 && (((uintptr_t)e.d) & 15) == 0 &&
+        (staged || !e.res)) {
+        fast_epilogue<DVS, FIS_EPI_NONE>(s_ea, e, sh, ge, stage, nullptr, 0, 1, 0, nrows, staged, tid);
+    } else {
+        for (int idx = tid; idx < nrows * (DVS / 8); idx += PRODUCERS) {
+            const int row = idx / (DVS / 8), cb = (idx % (DVS / 8)) * 8;
+            if (g.c0 + cb >= a.dv) continue;
+            float v[8];
+#pragma unroll
+            for (int u = 0; u < 8; u++) v[u] = stage[row * PLD + cb + u];
+            EpiIn in;
+            epilogue8_load(s_ea, e, g.m0 + row, g.c0 + cb, in, nullptr);
+            epilogue8(s_ea, e, sh.tb, g.m0 + row, cb, g.c0, v, in);
+        }
     }
     VM_STAMP(6);
     signal_done(va, j, tid);
@@ -954,7 +1532,7 @@ FIS_DEV void materialize_item(const fis_materialize_args& a, int item, int tid) 
 
 FIS_DEV void producer_role(const fis_vm_args& va, const Shared& sh, uint32_t tmem, int tid) {
     const int G = gridDim.x, cta = blockIdx.x;
-    ProdState ps{0, 0};
+    ProdState ps{0, 0, 0, 0};
     for (int j = 0; j < va.n_ops; j++) {
         const fis_vm_op* gop = va.ops + j;
         const int n_items = gop->n_items;
@@ -986,6 +1564,10 @@ FIS_DEV void producer_role(const fis_vm_args& va, const Shared& sh, uint32_t tme
                         signal_done(va, j, tid);
                         VM_STAMP(7);
                     }
+                    break;
+                case FIS_VM_ATTN:
+                    if (op.bn == 64) attn_item_run<64>(va, sh, j, i, ps, waited, tmem, tid);
+                    else attn_item_run<128>(va, sh, j, i, ps, waited, tmem, tid);
                     break;
                 case FIS_VM_SOFTMAX:
                     VM_STAMP(0);
@@ -1028,15 +1610,18 @@ __global__ void __launch_bounds__(THREADS, 1) vm_kernel(const fis_vm_args va) {
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     if (tid == 0) {
         for (int s = 0; s < STAGES; s++) {
-            mbar_init(sh.full + s, PRODUCERS);
+            mbar_init(sh.full + s, 1);  // thread 0's arrival (+ TMA bytes, + incrementing cp.async arrivals)
             mbar_init(sh.empty + s, 1);
         }
         mbar_init(sh.done, 1);
+        mbar_init(sh.s_ready, 1);
+        mbar_init(sh.p_ready, PRODUCERS);
+        mbar_init(sh.p_free, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == MMA_WARP) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(sh.tmem_slot)),
-                     "n"(MAX_BN));
+                     "n"(TMEM_COLS));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     tc_fence_before();
@@ -1052,7 +1637,7 @@ __global__ void __launch_bounds__(THREADS, 1) vm_kernel(const fis_vm_args va) {
     tc_fence_before();
     __syncthreads();
     if (warp == MMA_WARP)
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(MAX_BN));
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(TMEM_COLS));
     // the last CTA to leave resets the per-op completion counters for the next launch
     if (tid == 0) {
         __threadfence();
@@ -1070,6 +1655,49 @@ __global__ void __launch_bounds__(THREADS, 1) vm_kernel(const fis_vm_args va) {
 
 int fis_gemm_tc_supported(const fis_gemm_args* a);
 
+#include <cuda.h>
+#include <cstring>
+
+// cuTensorMapEncodeTiled resolved through the runtime (no link-time libcuda dependency: the
+// library must load on hosts without a driver; there the plan simply uses no TMA)
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static EncodeTiledFn encode_fn() {
+    static EncodeTiledFn fn = nullptr;
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = (EncodeTiledFn)p;
+        cudaGetLastError();
+    }
+    return fn;
+}
+
+// 2D bf16 tensor map [rows][cols] (row stride ld elements), box {64, box_rows}, 128-byte swizzle,
+// zero fill outside the matrix.  false when TMA cannot address it.
+static bool encode_2d(void* out128, const void* base, long long rows, long long cols, long long ld, int box_rows) {
+    if (!base || rows <= 0 || cols <= 0 || (((uintptr_t)base) & 15) || ((ld * 2) % 16) || ld < cols) return false;
+    CUtensorMap m;
+    cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {(cuuint64_t)(ld * 2)};
+    cuuint32_t box[2] = {64u, (cuuint32_t)box_rows};
+    cuuint32_t es[2] = {1u, 1u};
+    EncodeTiledFn enc = encode_fn();
+    if (!enc) return false;
+    const CUresult r = enc(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims,
+                                              strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                              CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return false;
+    std::memcpy(out128, &m, 128);
+    return true;
+}
+
 static int vm_sm_count() {
     static int n = 0;
     if (n <= 0) n = fis_device_sm_count();
@@ -1078,7 +1706,51 @@ static int vm_sm_count() {
 
 extern "C" int fis_vm_op_size(void) { return (int)sizeof(fis_vm_op); }
 
+// Value-slice width of a VM attention op (64 or 128 columns dividing dv) such that the key
+// blocks (16-column rounded) and the O slice fit the 512 TMEM columns; 0 = not supported.
+extern "C" int fis_vm_attn_slice(int m, int n_keys, int d, int dv) {
+    if (m < 0 || n_keys < 1 || d % 64 || dv <= 0) return 0;
+    const int s_cols = 128 * ((n_keys - 1) / 128) + ((n_keys - 128 * ((n_keys - 1) / 128) + 15) & ~15);
+    for (int w = 128; w >= 64; w -= 64)
+        if (dv % w == 0 && s_cols + w <= fis::vm::TMEM_COLS) return w;
+    return 0;
+}
+
+// 3-D bf16 tensor map of a dense conv source [h][w][c] (pixel stride ld), box {64, w, 128 / w}:
+// one tap of a 128-pixel output tile.
+static bool encode_conv(void* out128, const fis_src& s, int out_h, int out_w) {
+    if (s.index || s.up || s.fresh.step_stride || s.fresh.dtype != FIS_BF16 || !s.fresh.ptr) return false;
+    if (s.h != out_h || s.w != out_w || out_w > 128 || 128 % out_w || (s.c % 64)) return false;
+    const void* base = s.fresh.ptr;
+    const long long ld = s.fresh.ld;
+    if ((((uintptr_t)base) & 15) || ((ld * 2) % 16) || ld < s.c) return false;
+    CUtensorMap m;
+    cuuint64_t dims[3] = {(cuuint64_t)s.c, (cuuint64_t)s.w, (cuuint64_t)s.h};
+    cuuint64_t strides[2] = {(cuuint64_t)(ld * 2), (cuuint64_t)(ld * 2 * s.w)};
+    cuuint32_t box[3] = {64u, (cuuint32_t)out_w, (cuuint32_t)(128 / out_w)};
+    cuuint32_t es[3] = {1u, 1u, 1u};
+    EncodeTiledFn enc = encode_fn();
+    if (!enc) return false;
+    const CUresult r = enc(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims,
+                                              strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                              CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return false;
+    std::memcpy(out128, &m, 128);
+    return true;
+}
+
 extern "C" int fis_vm_plan(fis_vm_op* ops, int n, int n_ctas, long long* ws_floats, int* sync_ints) {
+    int nt = 0;
+    return fis_vm_plan_tma(ops, n, n_ctas, ws_floats, sync_ints, nullptr, 0, &nt);
+}
+
+extern "C" int fis_vm_plan_tma(fis_vm_op* ops, int n, int n_ctas, long long* ws_floats, int* sync_ints, void* tmaps,
+                               int cap, int* n_tmaps) {
+    int nt = 0;
+    // FIS_VM_TMA_MASK (debug): 1 B operands, 2 row-major A, 4 dense-conv A, 8 attention (default all)
+    const char* mask_env = getenv("FIS_VM_TMA_MASK");
+    const int tma_mask = mask_env ? atoi(mask_env) : 15;
     using namespace fis::vm;
     const int G = n_ctas > 0 ? n_ctas : vm_sm_count();
     long long ws = 0;
@@ -1087,6 +1759,7 @@ extern "C" int fis_vm_plan(fis_vm_op* ops, int n, int n_ctas, long long* ws_floa
     for (int j = 0; j < n; j++) {
         fis_vm_op& op = ops[j];
         op.impl = 0; op.bn = 0; op.tiles_n = 0; op.tiles_m = 0; op.splits = 1; op.sync_base = 0;
+        op.tmap_a = -1; op.tmap_b = -1; op.tmap_a2 = -1; op.pad_ = 0;
         switch (op.kind) {
             case FIS_VM_GEMM: {
                 const fis_gemm_args& a = op.u.gemm;
@@ -1121,6 +1794,18 @@ extern "C" int fis_vm_plan(fis_vm_op* ops, int n, int n_ctas, long long* ws_floa
                     op.splits = S;
                     op.n_items = tiles * S;
                     op.n_done = tiles * S;
+                    // TMA for B (weights, K/V operands) and for plain row-major A
+                    if (tmaps && (tma_mask & 1) && nt < cap && a.b.step_stride == 0 &&
+                        encode_2d((char*)tmaps + 128 * nt, a.b.ptr, a.n, a.k, a.b.ld, op.bn))
+                        op.tmap_b = nt++;
+                    if (tmaps && (tma_mask & 2) && nt < cap && a.a_mode == FIS_A_ROWS && !a.rows && a.a.step_stride == 0 &&
+                        a.a.dtype == FIS_BF16 && encode_2d((char*)tmaps + 128 * nt, a.a.ptr, a.m, a.k, a.a.ld, BM))
+                        op.tmap_a = nt++;
+                    if (tmaps && (tma_mask & 4) && a.a_mode == FIS_A_CONV3X3 && !a.rows) {  // dense conv: per-tap boxes
+                        if (nt < cap && encode_conv((char*)tmaps + 128 * nt, a.src[0], a.out_h, a.out_w)) op.tmap_a = nt++;
+                        if (a.nsrc > 1 && nt < cap && encode_conv((char*)tmaps + 128 * nt, a.src[1], a.out_h, a.out_w))
+                            op.tmap_a2 = nt++;
+                    }
                     if (S > 1) {
                         op.sync_base = sync_next;
                         sync_next += tiles;
@@ -1163,6 +1848,24 @@ extern "C" int fis_vm_plan(fis_vm_op* ops, int n, int n_ctas, long long* ws_floa
                 op.n_items = (int)(((long long)a.src.h * a.src.w * a.c + ELEMS_PER_ITEM - 1) / ELEMS_PER_ITEM);
                 break;
             }
+            case FIS_VM_ATTN: {
+                const fis_attn_args& a = op.u.attn;
+                const int dvs = fis_vm_attn_slice(a.m, a.n_keys, a.d, a.dv);
+                if (!dvs || a.q.dtype != FIS_BF16 || a.k.dtype != FIS_BF16 || a.vt.dtype != FIS_BF16 ||
+                    (a.q.ld % 8) || (a.k.ld % 8) || (a.vt.ld % 8))
+                    return FIS_ERR_UNSUPPORTED;
+                op.bn = dvs;
+                op.tiles_n = a.dv / dvs;
+                op.tiles_m = (a.m + BM - 1) / BM;
+                op.n_items = a.m > 0 ? op.tiles_n * op.tiles_m : 0;
+                if (tmaps && (tma_mask & 8) && a.q.step_stride == 0 && a.k.step_stride == 0 && a.vt.step_stride == 0 &&
+                    nt + 3 <= cap) {
+                    if (encode_2d((char*)tmaps + 128 * nt, a.q.ptr, a.m, a.d, a.q.ld, BM)) op.tmap_a = nt++;
+                    if (encode_2d((char*)tmaps + 128 * nt, a.k.ptr, a.n_keys, a.d, a.k.ld, 128)) op.tmap_b = nt++;
+                    if (encode_2d((char*)tmaps + 128 * nt, a.vt.ptr, a.dv, a.n_keys, a.vt.ld, dvs)) op.tmap_a2 = nt++;
+                }
+                break;
+            }
             default:
                 return FIS_ERR_UNSUPPORTED;
         }
@@ -1175,6 +1878,7 @@ extern "C" int fis_vm_plan(fis_vm_op* ops, int n, int n_ctas, long long* ws_floa
     }
     if (ws_floats) *ws_floats = ws;
     if (sync_ints) *sync_ints = sync_next;
+    if (n_tmaps) *n_tmaps = nt;
     return FIS_OK;
 }
 

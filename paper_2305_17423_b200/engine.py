@@ -235,10 +235,16 @@ class VmProgram:
             ops[i].kind = kind
             ops[i].b_static = 1 if b_static else 0
             setattr(ops[i].u, field, args)
-        ws, si = L.C.c_longlong(0), L.C.c_int(0)
-        st = L.lib().fis_vm_plan(L.C.byref(ops), n, 0, L.C.byref(ws), L.C.byref(si))
+        ws, si, nt = L.C.c_longlong(0), L.C.c_int(0), L.C.c_int(0)
+        cap = 3 * n
+        maps = (L.C.c_ubyte * (128 * cap))()
+        use_tma = os.environ.get("FIS_VM_TMA", "1") != "0"
+        st = L.lib().fis_vm_plan_tma(L.C.byref(ops), n, 0, L.C.byref(ws), L.C.byref(si), maps if use_tma else None,
+                                     cap if use_tma else 0, L.C.byref(nt))
         if st != 0:
             raise ContractViolation(f"fis_vm_plan failed (status {st})")
+        self.n_tmaps = nt.value
+        self.tmaps = torch.frombuffer(bytearray(bytes(maps)[:128 * max(1, nt.value)]), dtype=torch.uint8).to(lz.dev)
         self.calls = calls  # keeps the argument structs (and what they point to) alive
         self.n_ops = n
         self.ops_host = ops
@@ -247,7 +253,7 @@ class VmProgram:
         self.sync = torch.zeros(si.value, dtype=torch.int32, device=lz.dev)
         self.ws = torch.empty(max(4, ws.value), dtype=torch.float32, device=lz.dev)
         self.args = L.VmArgs(self.ops_dev.data_ptr(), n, 0, self.sync.data_ptr(), si.value, self.ws.data_ptr(),
-                             lz.step_dev.data_ptr(), None,
+                             lz.step_dev.data_ptr(), self.tmaps.data_ptr(), None,
                              int(os.environ.get("FIS_VM_POLL_NS", "0")), -1, None)
         self.lz = lz
         self.trace = None
@@ -347,7 +353,7 @@ class Engine(Launcher):
         self.gemm(m, 3 * c, c, a=s, b=DRef(wqkv), d=DRef(qk), n_split=2 * c, d2=DRef(vt, ld=mp), d2_trans=True,
                   b_static=True)
         qkr = DRef(qk)
-        if self.use_fused_attn(c):
+        if self.use_fused_attn(c, m, m, pre):
             # S = QK^T, softmax and P.V (+ residual) in one tcgen05 kernel (fis_attn)
             self.attn(m, m, c, qkr, qkr.cols(c), DRef(vt, ld=mp), scale, s, y1, pre)
             return
@@ -371,7 +377,7 @@ class Engine(Launcher):
             self._call("fis_xattn", a)
             self.launches += 1
             return
-        if ctrl is None and map_ is None and self.use_fused_attn(c):
+        if ctrl is None and map_ is None and self.use_fused_attn(c, m, nt, pre):
             self.attn(m, nt, c, DRef(q), DRef(k), DRef(vt), scale, x, out, pre)
             return
         S = self.scratch(f"Sx{tag}", (cap, ntp), torch.float32)  # ld padded: 16-byte aligned rows
@@ -384,8 +390,13 @@ class Engine(Launcher):
             self.softmax(m, nt, ntp, DRef(S), scale, DRef(P), map_)
         self.gemm(m, c, ntp, a=DRef(P), b=DRef(vt), d=out, res=x, pre=pre, b_static=True)  # text V^T
 
-    def use_fused_attn(self, d):
-        return self.fused_attn and self.act == torch.bfloat16 and d % 64 == 0
+    def use_fused_attn(self, d, m=None, n_keys=None, pre=None):
+        if self.act != torch.bfloat16 or d % 64:
+            return False
+        if self.capture is not None and m is not None and pre is None:
+            # the step VM runs attention as one fused op (S in TMEM, P via shared memory)
+            return L.lib().fis_vm_attn_slice(m, n_keys, d, d) > 0
+        return self.fused_attn
 
     def attn(self, m, n_keys, d, q: DRef, k: DRef, vt: DRef, scale, res: DRef, out: DRef, pre=None):
         a = L.AttnArgs(m, n_keys, d, d, q.ref(), k.ref(), vt.ref(), float(scale), _r(res), _r(pre), out.ref(),
