@@ -265,6 +265,8 @@ int fis_mask_plan(const fis_mask_plan_args* a, void* stream);
 #define FIS_VM_POOL 5
 #define FIS_VM_MATERIALIZE 6
 #define FIS_VM_ATTN 7        /* fused attention (fis_attn_args), keys + value slice <= 512 TMEM columns */
+#define FIS_VM_GN 8          /* group norm: statistics of each group over the full map + normalisation (+SiLU),
+                                one item per group (fis_gn_apply_args: mean / var are written) */
 
 typedef struct {
     int kind;               /* FIS_VM_* (set by the caller, with the matching args) */

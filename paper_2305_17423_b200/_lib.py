@@ -14,7 +14,10 @@ import torch
 
 from .errors import CacheMissError, ContractViolation
 
-_LIB_PATH = Path(__file__).resolve().parent / "libfisedit.so"
+import os as _os
+
+# FIS_LIB (profiling experiments): load an alternative in-tree build, e.g. libfisedit_vm6.so
+_LIB_PATH = Path(__file__).resolve().parent / _os.environ.get("FIS_LIB", "libfisedit.so")
 _lib = None
 
 F32, BF16 = 0, 1
@@ -112,7 +115,7 @@ class VmArgs(C.Structure):
 # ops the step VM executes: C entry point -> (FIS_VM_* kind, union member)
 VM_KINDS = {"fis_gemm": (1, "gemm"), "fis_softmax": (2, "softmax"), "fis_gn_stats": (3, "gn_stats"),
             "fis_gn_apply": (4, "gn_apply"), "fis_pool2": (5, "pool"), "fis_materialize": (6, "materialize"),
-            "fis_attn": (7, "attn")}
+            "fis_attn": (7, "attn"), "fis_gn": (8, "gn_apply")}
 
 _SIGS = {
     "fis_gemm": GemmArgs, "fis_attn": AttnArgs, "fis_xattn": XattnArgs, "fis_gn_stats": GnStatsArgs, "fis_gn_apply": GnApplyArgs, "fis_softmax": SoftmaxArgs,

@@ -25,7 +25,19 @@ namespace fis {
 namespace vm {
 using namespace fis::tc;
 
-constexpr int STAGES = 4, PRODUCERS = 256, THREADS = 288, MMA_WARP = 8;
+#ifndef VM_STAGES
+#define VM_STAGES 4
+#endif
+#ifndef VM_FUSED_ATTN
+#define VM_FUSED_ATTN 1
+#endif
+// warps 0-3 producers / epilogue, warp 4 idle, warp 5 MMA (its spin-waits share an SM sub-partition
+// with warp 1, not with warp 0 whose thread 0 issues the TMA loads).  6 warps are allocated
+// registers like 8, so each thread may use 255 registers (no spills in the fused paths).
+constexpr int STAGES = VM_STAGES, PRODUCERS = 128, THREADS = 192, MMA_WARP = 5;
+constexpr int TPR = PRODUCERS / 128;   // producer threads per 128-byte smem row of a stage
+constexpr int CPT = 8 / TPR;           // 16-byte chunks each of them loads per row
+constexpr int WPQ = PRODUCERS / 128;   // epilogue warps per TMEM lane quarter
 constexpr int MAX_BN = 128;
 constexpr int A_BYTES = BM * BK * 2;
 constexpr int B_BYTES = MAX_BN * BK * 2;
@@ -34,17 +46,24 @@ constexpr int OPBUF = 1024;
 constexpr int EPI = MAX_BN * 32;
 constexpr int SEL = BM * 2 * 9 * 4;
 constexpr int RES_LD = 272;                  // bytes per staged residual row (<= 256 B of data)
-constexpr int RES_BYTES = BM * RES_LD;       // epilogue operand tile (residual / latent rows)
-constexpr int P_BYTES = 2 * BM * 64 * 2;     // attention P tile: 128 rows x 128 keys bf16 (two SW128 chunks)
+constexpr int RES_BYTES = VM_FUSED_ATTN ? BM * RES_LD : 0;  // epilogue operand tile (residual / latent rows)
+constexpr int P_BYTES = VM_FUSED_ATTN ? 2 * BM * 64 * 2 : 0;  // attention P tile: 128 x 128 keys bf16 (two SW128 chunks)
 constexpr int TMEM_COLS = 512;
 constexpr int SMEM = STAGES * STAGE + RES_BYTES + P_BYTES + 1024;  // dynamic: ring + operand tile + P (+ align)
 constexpr int ELEMS_PER_ITEM = 2048;  // elementwise ops
-constexpr int SOFTMAX_ROWS = 8;       // one warp per row
-constexpr int SBM = 64, SBN = 64, SBK = 16;  // SIMT GEMM tile
+constexpr int SOFTMAX_ROWS = PRODUCERS / 32;  // one warp per row
+constexpr int SBM = 64, SBN = 64, SBK = 64;  // SIMT GEMM tile (64-deep k passes: all gathers of a pass in flight)
 
 static_assert(sizeof(fis_vm_op) <= OPBUF, "fis_vm_op must fit the shared op buffer");
 
-FIS_DEV void pbar() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
+FIS_DEV void pbar() { asm volatile("bar.sync 1, %0;" ::"n"(PRODUCERS) : "memory"); }
+
+// 2^x on the SFU (bf16-mode softmax: scores are pre-scaled by scale * log2(e))
+FIS_DEV float ex2(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
 
 // the step index of this launch (read once per CTA from fis_vm_args.step)
 __shared__ int s_step;
@@ -62,6 +81,7 @@ struct Shared {
     uint64_t* s_ready;   // attention: every S block of the item is in TMEM
     uint64_t* p_ready;   // attention: P block written (256 producer arrivals)
     uint64_t* p_free;    // attention: the P.V MMAs reading the P tile have completed
+    uint64_t* red;       // split-K: the split partial slices of this CTA's rows have landed
     fis_vm_op* op;
     EpiTab tb;
     int* seltab;
@@ -77,11 +97,11 @@ struct Shared {
 // with global stores).
 extern __shared__ __align__(1024) unsigned char vm_smem[];
 __shared__ __align__(16) fis_vm_op s_op;
-__shared__ float s_tab[6][MAX_BN];
-__shared__ int s_sel[BM * 2 * 9];
-__shared__ __align__(8) uint64_t s_bar[2 * STAGES + 4];
+__shared__ __align__(16) float s_tab[6][MAX_BN];
+__shared__ __align__(16) int s_sel[BM * 2 * 9];
+__shared__ __align__(8) uint64_t s_bar[2 * STAGES + 5];
 __shared__ __align__(16) fis_gemm_args s_ea;   // attention: epilogue view (out = res + O)
-__shared__ float s_rowstat[2][BM];             // attention: per-row partial max / sum of the two halves
+__shared__ __align__(16) float s_rowstat[WPQ][BM];           // attention: per-row partial max / sum of the key halves
 __shared__ uint32_t s_tmem;
 __shared__ int s_flag;
 
@@ -105,9 +125,22 @@ FIS_DEV Shared carve() {
     s.s_ready = s_bar + 2 * STAGES + 1;
     s.p_ready = s_bar + 2 * STAGES + 2;
     s.p_free = s_bar + 2 * STAGES + 3;
+    s.red = s_bar + 2 * STAGES + 4;
     s.tmem_slot = &s_tmem;
     s.flag = &s_flag;
     return s;
+}
+
+// Shared-memory objects by constant address (nothing to keep in registers): the 1024-aligned
+// ring inside the dynamic allocation and an epilogue-table view of s_tab.
+FIS_DEV unsigned char* vm_ring() {
+    const uint32_t a = smem_u32(vm_smem);
+    return vm_smem + ((1024u - (a & 1023u)) & 1023u);
+}
+FIS_DEV EpiTab vm_tab() {
+    EpiTab t;
+    t.mean = s_tab[0]; t.rstd = s_tab[1]; t.bias = s_tab[2]; t.b2 = s_tab[3]; t.gamma = s_tab[4]; t.beta = s_tab[5];
+    return t;
 }
 
 // ---------------------------------------------------------------------------------- GEMM geometry
@@ -190,7 +223,7 @@ FIS_DEV void cp_async_arrive_inc(uint64_t* bar) {
     asm volatile("cp.async.mbarrier.arrive.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 // mbarrier wait with a sleep back-off (waiting producers leave issue slots to the TMA / MMA threads)
-FIS_DEV void mbar_wait_backoff(uint64_t* b, uint32_t parity) {
+FIS_DEV void mbar_wait_backoff(uint64_t* b, uint32_t parity, int ns = 128) {
     uint32_t ok;
     for (;;) {
         asm volatile(
@@ -199,7 +232,7 @@ FIS_DEV void mbar_wait_backoff(uint64_t* b, uint32_t parity) {
             : "r"(smem_u32(b)), "r"(parity)
             : "memory");
         if (ok) return;
-        __nanosleep(32);
+        __nanosleep(ns);
     }
 }
 FIS_DEV void expect_tx(uint64_t* bar, uint32_t bytes) {
@@ -214,67 +247,74 @@ FIS_DEV void mma_commit(uint64_t* bar) {
                  : "memory");
 }
 
+FIS_DEV unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
 // ---------------------------------------------------------------------------------- MMA warp
 FIS_DEV void mma_role(const fis_vm_args& va, const Shared& sh, uint32_t tmem, int lane) {
     const int G = gridDim.x, cta = blockIdx.x;
     uint32_t it = 0, pb = 0;
-    const uint32_t sbase = smem_u32(sh.ring);
+    const uint32_t sbase = smem_u32(vm_ring());
     for (int j = 0; j < va.n_ops; j++) {
         const fis_vm_op* op = va.ops + j;
         if (op->kind == FIS_VM_ATTN) {
             for (int i = (cta - op->cta0 + G) % G; i < op->n_items; i += G) {
                 const AttnItem g = attn_item(*op, i);
                 const int n_keys = op->u.attn.n_keys;
-                for (int kc = 0; kc < g.dch; kc++) {  // S_j += Q_kc K_j,kc^T, Q chunk shared by every j
-                    int sq_slot = 0;
-                    for (int jb = 0; jb < g.nkb; jb++, it++) {
+                for (int jb = 0; jb < g.nkb; jb++) {  // S_j = Q K_j^T
+                    const uint32_t id = idesc_f16(BM, (attn_nb(n_keys, jb) + 15) & ~15);
+                    for (int kc = 0; kc < g.dch; kc++, it++) {
                         const int s = it % STAGES;
-                        if (jb == 0) sq_slot = s;
-                        mbar_wait(sh.full + s, (it / STAGES) & 1);
+                        mbar_wait(s_bar + s, (it / STAGES) & 1);
                         tc_fence_after();
                         if (lane == 0) {
-                            const uint32_t id = idesc_f16(BM, (attn_nb(n_keys, jb) + 15) & ~15);
-                            mma4(tmem + 128 * jb, sbase + sq_slot * STAGE, sbase + s * STAGE + A_BYTES, id, kc > 0);
-                            if (jb > 0) mma_commit(sh.empty + s);
-                            if (jb == g.nkb - 1) mma_commit(sh.empty + sq_slot);
+                            const uint32_t sa = sbase + s * STAGE;
+                            mma4(tmem + 128 * jb, sa, sa + A_BYTES, id, kc > 0);
+                            mma_commit((s_bar + STAGES) + s);
                         }
                         __syncwarp();
                     }
                 }
-                if (lane == 0) mma_commit(sh.s_ready);
+                if (lane == 0) mma_commit((s_bar + 2 * STAGES + 1));
                 __syncwarp();
-                const uint32_t ido = idesc_f16(BM, g.dvs), pbase = smem_u32(sh.pbuf);
+                const uint32_t ido = idesc_f16(BM, g.dvs), pbase = smem_u32((vm_ring() + STAGES * STAGE + RES_BYTES));
                 for (int jb = 0; jb < g.nkb; jb++, pb++) {  // O += P_j V_j
-                    mbar_wait(sh.p_ready, pb & 1);
+                    mbar_wait((s_bar + 2 * STAGES + 2), pb & 1);
                     tc_fence_after();
                     const int nch = (attn_nb(n_keys, jb) + 63) / 64;
                     for (int c = 0; c < nch; c++, it++) {
                         const int s = it % STAGES;
-                        mbar_wait(sh.full + s, (it / STAGES) & 1);
+                        mbar_wait(s_bar + s, (it / STAGES) & 1);
                         tc_fence_after();
                         if (lane == 0) {
                             mma4(tmem + g.o_col, pbase + c * (BM * 128), sbase + s * STAGE + A_BYTES, ido, jb > 0 || c > 0);
-                            mma_commit(sh.empty + s);
+                            mma_commit((s_bar + STAGES) + s);
                         }
                         __syncwarp();
                     }
-                    if (lane == 0) mma_commit(sh.p_free);
+                    if (lane == 0) mma_commit((s_bar + 2 * STAGES + 3));
                     __syncwarp();
                 }
-                if (lane == 0) mma_commit(sh.done);
+                if (lane == 0) mma_commit((s_bar + 2 * STAGES));
                 __syncwarp();
             }
             continue;
         }
         if (op->kind != FIS_VM_GEMM || op->impl != 2) continue;
         const int n_items = op->n_items;
+        const bool traced = va.trace_items && j == va.trace_op && lane == 0;
         for (int i = (cta - op->cta0 + G) % G; i < n_items; i += G) {
             const GemmItem g = gemm_item(*op, i);
             const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(g.bn >> 3) << 17) |
                                    ((uint32_t)(BM >> 4) << 24);
+            if (traced) va.trace_items[16 * i + 14] = gtimer();
             for (int q = 0; q < g.nk; q++, it++) {
                 const int s = it % STAGES;
-                mbar_wait(sh.full + s, (it / STAGES) & 1);
+                mbar_wait(s_bar + s, (it / STAGES) & 1);
+                if (traced && q == 0) va.trace_items[16 * i + 12] = gtimer();
                 tc_fence_after();
                 if (lane == 0) {
                     const uint32_t sa = sbase + s * STAGE, sb = sa + A_BYTES;
@@ -288,15 +328,16 @@ FIS_DEV void mma_role(const fis_vm_args& va, const Shared& sh, uint32_t tmem, in
                             "l"(ad), "l"(bd), "r"(idesc), "r"(acc));
                     }
                     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                                     smem_u32(sh.empty + s))
+                                     smem_u32((s_bar + STAGES) + s))
                                  : "memory");
                 }
                 __syncwarp();
             }
             if (lane == 0)
                 asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                                 smem_u32(sh.done))
+                                 smem_u32((s_bar + 2 * STAGES)))
                              : "memory");
+            if (traced) va.trace_items[16 * i + 13] = gtimer();
             __syncwarp();
         }
     }
@@ -320,13 +361,9 @@ struct ProdState {
     uint32_t items;   // tcgen05 items run (parity of the done barrier)
     uint32_t attn;    // attention items run (parity of s_ready)
     uint32_t pb;      // attention P blocks written (parity of p_ready / p_free, matches the MMA warp)
+    uint32_t red;     // split-K reductions run (parity of the red barrier)
 };
 
-FIS_DEV unsigned long long gtimer() {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    return t;
-}
 
 // phase stamp of item i of the traced op (profiling; fis_vm_args.trace_op / trace_items)
 #define VM_STAMP(slot)                                                                   \
@@ -384,7 +421,7 @@ FIS_DEV void issue_b(const fis_gemm_args& a, const GemmItem& g, const char* bbas
     const int bn = g.n0 + ar;
     const char* brow = bbase + (long long)bn * a.b.ld * 2;
 #pragma unroll
-    for (int j = j0; j < j0 + 4; j++) {
+    for (int j = j0; j < j0 + CPT; j++) {
         const bool ok = bn < a.n && k0 + j * 8 < a.k;
         cp_async16(sb + sw128_off(ar, j), ok ? (const void*)(brow + (k0 + j * 8) * 2) : (const void*)bbase, ok);
     }
@@ -395,19 +432,19 @@ FIS_DEV void stage_tables(const fis_gemm_args& a, const EpiCtx& e, const Shared&
     for (int c = tid; c < bn; c += PRODUCERS) {
         const int n = n0 + c;
         const bool ok = n < a.n;
-        sh.tb.bias[c] = ok && a.bias ? __ldg(a.bias + n) : 0.f;
-        sh.tb.b2[c] = ok && e.bias2 ? load_elem(e.bias2, a.bias2.dtype, n) : 0.f;
+        vm_tab().bias[c] = ok && a.bias ? __ldg(a.bias + n) : 0.f;
+        vm_tab().b2[c] = ok && e.bias2 ? load_elem(e.bias2, a.bias2.dtype, n) : 0.f;
         if (a.epi == FIS_EPI_GN_SILU && ok) {
             const int gi = n / e.cpg;
             // cached-stat GN folded into one fma per element: y = v * scale + shift
             const float rstd = (float)(1.0 / sqrt((double)e.var[gi] + (double)a.eps));
             const float scale = rstd * __ldg(a.gamma + n);
-            sh.tb.mean[c] = scale;
-            sh.tb.rstd[c] = fmaf(-e.mean[gi], scale, __ldg(a.beta + n));
-            sh.tb.gamma[c] = 0.f;
-            sh.tb.beta[c] = 0.f;
+            vm_tab().mean[c] = scale;
+            vm_tab().rstd[c] = fmaf(-e.mean[gi], scale, __ldg(a.beta + n));
+            vm_tab().gamma[c] = 0.f;
+            vm_tab().beta[c] = 0.f;
         } else {
-            sh.tb.mean[c] = 0.f; sh.tb.rstd[c] = 0.f; sh.tb.gamma[c] = 0.f; sh.tb.beta[c] = 0.f;
+            vm_tab().mean[c] = 0.f; vm_tab().rstd[c] = 0.f; vm_tab().gamma[c] = 0.f; vm_tab().beta[c] = 0.f;
         }
     }
 }
@@ -544,9 +581,10 @@ FIS_DEV void gemm_tc_epilogue(const fis_vm_args& va, const Shared& sh, int j, in
                                               bool tables_done, bool staged);
 
 // The epilogue's one read operand of this tile (latent rows for EPI_STEP, else the residual):
-// rows [m0, m0+BM) x columns [n0, n0+bn) copied to sh.res with 16-byte cp.async when the row
+// rows [m0, m0+BM) x columns [n0, n0+bn) copied to (vm_ring() + STAGES * STAGE) with 16-byte cp.async when the row
 // segment fits RES_LD and is 16-byte aligned.  Returns false (direct loads) otherwise.
 FIS_DEV bool stage_operand(const fis_gemm_args& a, const Shared& sh, const GemmItem& g, int t, int tid) {
+    if (RES_BYTES == 0) return false;
     const fis_ref& x = a.epi == FIS_EPI_STEP ? a.lat : a.res;
     if (!x.ptr || a.d_rows) return false;
     const int esz = x.dtype == FIS_BF16 ? 2 : 4;
@@ -557,7 +595,7 @@ FIS_DEV bool stage_operand(const fis_gemm_args& a, const Shared& sh, const GemmI
     if (((uintptr_t)base) & 15) return false;
     const int per_row = seg / 16;
     const int rows = min(BM, a.m - g.m0);
-    const uint32_t dst0 = smem_u32(sh.res);
+    const uint32_t dst0 = smem_u32((vm_ring() + STAGES * STAGE));
     for (int idx = tid; idx < rows * per_row; idx += PRODUCERS) {
         const int row = idx / per_row, c16 = idx % per_row;
         const int col_bytes = c16 * 16;
@@ -571,12 +609,12 @@ FIS_DEV bool stage_operand(const fis_gemm_args& a, const Shared& sh, const GemmI
 template <int BN>
 FIS_DEV void gemm_tc_item(const fis_vm_args& va, const Shared& sh, int j, int i, ProdState& ps,
                                           bool& waited, uint32_t tmem, int tid) {
-    const fis_vm_op& op = *sh.op;
+    const fis_vm_op& op = s_op;
     const fis_gemm_args& a = op.u.gemm;
     const GemmItem g = gemm_item(op, i);
     const int t = s_step;
-    const int ar = tid >> 1, half_id = tid & 1, j0 = half_id * 4;
-    const uint32_t sbase = smem_u32(sh.ring);
+    const int ar = tid / TPR, half_id = tid % TPR, j0 = half_id * CPT;
+    const uint32_t sbase = smem_u32(vm_ring());
     const char* bbase = ref_base(a.b, t);
 
     VM_STAMP(0);
@@ -606,15 +644,15 @@ FIS_DEV void gemm_tc_item(const fis_vm_args& va, const Shared& sh, int j, int i,
             for (int q = 0; q < npre; q++) {
                 const uint32_t sq = ps.it + q;
                 const int s = sq % STAGES;
-                if (sq >= STAGES) mbar_wait_backoff(sh.empty + s, ((sq / STAGES) & 1) ^ 1);
-                mbar_expect_tx(sh.full + s, b_bytes);
-                tma2d(sbase + s * STAGE + A_BYTES, tma_b, (g.kb0 + q) * BK, g.n0, sh.full + s);
+                if (sq >= STAGES) mbar_wait((s_bar + STAGES) + s, ((sq / STAGES) & 1) ^ 1);
+                mbar_expect_tx(s_bar + s, b_bytes);
+                tma2d(sbase + s * STAGE + A_BYTES, tma_b, (g.kb0 + q) * BK, g.n0, s_bar + s);
             }
     } else {
         for (int q = 0; q < npre; q++) {
             const uint32_t sq = ps.it + q;
             const int s = sq % STAGES;
-            if (sq >= STAGES) mbar_wait_backoff(sh.empty + s, ((sq / STAGES) & 1) ^ 1);
+            if (sq >= STAGES) mbar_wait((s_bar + STAGES) + s, ((sq / STAGES) & 1) ^ 1);
             issue_b(a, g, bbase, sbase + s * STAGE + A_BYTES, (g.kb0 + q) * BK, ar, j0);
         }
     }
@@ -623,7 +661,8 @@ FIS_DEV void gemm_tc_item(const fis_vm_args& va, const Shared& sh, int j, int i,
     const int r = g.m0 + ar;
     const bool row_valid = r < a.m;
     const int row_p = row_valid ? (a.rows ? __ldg(a.rows + r) : r) : 0;
-    if (conv && half_id < a.nsrc) build_sel(a, row_p, half_id, sh.seltab + (ar * 2 + half_id) * 9);
+    if (conv)
+        for (int seg = half_id; seg < a.nsrc; seg += TPR) build_sel(a, row_p, seg, s_sel + (ar * 2 + seg) * 9);
     __syncwarp();  // the two threads of a row each built one segment's select table
     VM_STAMP(1);
     wait_dep(va, op, j, waited, tid);
@@ -634,7 +673,7 @@ FIS_DEV void gemm_tc_item(const fis_vm_args& va, const Shared& sh, int j, int i,
     const char* c0p = a.nsrc > 0 && a.src[0].cache.ptr ? ref_base(a.src[0].cache, t) : nullptr;
     const char* f1 = a.nsrc > 1 && a.src[1].fresh.ptr ? ref_base(a.src[1].fresh, t) : nullptr;
     const char* c1p = a.nsrc > 1 && a.src[1].cache.ptr ? ref_base(a.src[1].cache, t) : nullptr;
-    const int* mysel = sh.seltab + ar * 2 * 9;
+    const int* mysel = s_sel + ar * 2 * 9;
     const bool mixed = conv && a.nsrc > 1 && ((tma_a != nullptr) != (tma_a2 != nullptr));
     for (int q = 0; q < g.nk; q++) {
         const uint32_t sq = ps.it + q;
@@ -644,38 +683,38 @@ FIS_DEV void gemm_tc_item(const fis_vm_args& va, const Shared& sh, int j, int i,
         const void* tm = tma_b ? a_map(k0) : nullptr;  // TMA A only together with TMA B
         if (tm && mixed) {
             // ---- conv with one TMA segment and one gathered segment: every producer stays in step
-            if (sq >= STAGES) mbar_wait_backoff(sh.empty + s, ((sq / STAGES) & 1) ^ 1);
+            if (sq >= STAGES) mbar_wait((s_bar + STAGES) + s, ((sq / STAGES) & 1) ^ 1);
             if (tid == 0) {
                 if (q >= npre) {
-                    mbar_expect_tx(sh.full + s, b_bytes);
-                    tma2d(sa + A_BYTES, tma_b, k0, g.n0, sh.full + s);
+                    mbar_expect_tx(s_bar + s, b_bytes);
+                    tma2d(sa + A_BYTES, tma_b, k0, g.n0, s_bar + s);
                 }
                 const int tap = k0 / cin;
                 const int c = k0 - tap * cin;
                 const int cs = c >= src0c ? c - src0c : c;
-                mbar_expect_tx(sh.full + s, (uint32_t)(BM * BK * 2));
-                tma3d(sa, tm, cs, tap % 3 - 1, g.m0 / a.out_w + tap / 3 - 1, sh.full + s);
+                mbar_expect_tx(s_bar + s, (uint32_t)(BM * BK * 2));
+                tma3d(sa, tm, cs, tap % 3 - 1, g.m0 / a.out_w + tap / 3 - 1, s_bar + s);
             }
             pbar();
-            if (tid == 0) mbar_arrive(sh.full + s);
+            if (tid == 0) mbar_arrive(s_bar + s);
             continue;
         }
         if (tm) {
             // ---- thread 0 alone: (B if not prefetched) + A via TMA, one arrival with the bytes
             if (tid == 0) {
                 if (q >= npre) {
-                    mbar_wait_backoff(sh.empty + s, ((sq / STAGES) & 1) ^ 1);
-                    mbar_expect_tx(sh.full + s, b_bytes);
-                    tma2d(sa + A_BYTES, tma_b, k0, g.n0, sh.full + s);
+                    mbar_wait((s_bar + STAGES) + s, ((sq / STAGES) & 1) ^ 1);
+                    mbar_expect_tx(s_bar + s, b_bytes);
+                    tma2d(sa + A_BYTES, tma_b, k0, g.n0, s_bar + s);
                 }
-                expect_tx(sh.full + s, (uint32_t)(BM * BK * 2));
+                expect_tx(s_bar + s, (uint32_t)(BM * BK * 2));
                 if (conv) {
                     const int tap = k0 / cin;
                     const int c = k0 - tap * cin;
                     const int cs = c >= src0c ? c - src0c : c;
-                    tma3d(sa, tm, cs, tap % 3 - 1, g.m0 / a.out_w + tap / 3 - 1, sh.full + s);
+                    tma3d(sa, tm, cs, tap % 3 - 1, g.m0 / a.out_w + tap / 3 - 1, s_bar + s);
                 } else {
-                    tma2d(sa, tm, k0, g.m0, sh.full + s);
+                    tma2d(sa, tm, k0, g.m0, s_bar + s);
                 }
                 if (q == 0) VM_STAMP(8);
             }
@@ -683,12 +722,12 @@ FIS_DEV void gemm_tc_item(const fis_vm_args& va, const Shared& sh, int j, int i,
         }
         // ---- every producer: gathered A rows (and B rows without TMA) with cp.async; every thread
         //      waits for the slot itself (only thread 0 waited for the TMA-prefetched B stages)
-        if (sq >= STAGES) mbar_wait_backoff(sh.empty + s, ((sq / STAGES) & 1) ^ 1);
+        if (sq >= STAGES) mbar_wait((s_bar + STAGES) + s, ((sq / STAGES) & 1) ^ 1);
         if (q >= npre) {
             if (tma_b) {
                 if (tid == 0) {
-                    mbar_expect_tx(sh.full + s, b_bytes);
-                    tma2d(sa + A_BYTES, tma_b, k0, g.n0, sh.full + s);
+                    mbar_expect_tx(s_bar + s, b_bytes);
+                    tma2d(sa + A_BYTES, tma_b, k0, g.n0, s_bar + s);
                 }
             } else {
                 issue_b(a, g, bbase, sa + A_BYTES, k0, ar, j0);
@@ -712,13 +751,13 @@ FIS_DEV void gemm_tc_item(const fis_vm_args& va, const Shared& sh, int j, int i,
             }
         }
 #pragma unroll
-        for (int jj = j0; jj < j0 + 4; jj++) {
+        for (int jj = j0; jj < j0 + CPT; jj++) {
             const bool ok = src != nullptr && (conv || k0 + jj * 8 < a.k);
             cp_async16(sa + sw128_off(ar, jj), ok ? (const void*)(src + jj * 16) : (const void*)bbase, ok);
         }
-        cp_async_arrive_inc(sh.full + s);
+        cp_async_arrive_inc(s_bar + s);
         pbar();  // every producer's arrival is registered before thread 0's
-        if (tid == 0) mbar_arrive(sh.full + s);
+        if (tid == 0) mbar_arrive(s_bar + s);
         if (q == 0) VM_STAMP(8);
     }
     ps.it += g.nk;
@@ -741,13 +780,12 @@ FIS_DEV void fast_epilogue(const fis_gemm_args& a, const EpiCtx& e, const Shared
     const int ch = tid % CH, cb = ch * 8, n = g.n0 + cb;
     if (n >= a.n) return;
     const int nvalid = min(8, a.n - n);
-    float bias[8], b2[8], gscale[8], gshift[8];
-#pragma unroll
-    for (int k = 0; k < 8; k++) {
-        bias[k] = sh.tb.bias[cb + k];
-        b2[k] = sh.tb.b2[cb + k];
-        if (MODE == FIS_EPI_GN_SILU) { gscale[k] = sh.tb.mean[cb + k]; gshift[k] = sh.tb.rstd[cb + k]; }
-    }
+    // column parameters stay in shared memory (re-read per row: two 16-byte LDS each) so the
+    // row loop needs no extra registers
+    auto ld8 = [&](const float* t, float* o) {
+        const float4 x0 = *(const float4*)(t + cb), x1 = *(const float4*)(t + cb + 4);
+        o[0] = x0.x; o[1] = x0.y; o[2] = x0.z; o[3] = x0.w; o[4] = x1.x; o[5] = x1.y; o[6] = x1.z; o[7] = x1.w;
+    };
     const float alpha = a.alpha, step_scale = a.step_scale;
     const bool has_b2 = e.bias2 != nullptr, has_x = staged;
     const int xdt = MODE == FIS_EPI_STEP ? a.lat.dtype : a.res.dtype;
@@ -771,7 +809,7 @@ FIS_DEV void fast_epilogue(const fis_gemm_args& a, const EpiCtx& e, const Shared
 #pragma unroll
                 for (int q = 0; q < 3; q++)
 #pragma unroll
-                    for (int w = 0; w < 2; w++) f[q][w] = __ldcg((const float4*)(p + (zz + q) * tile_floats) + w);
+                    for (int w = 0; w < 2; w++) f[q][w] = *((const float4*)(p + (zz + q) * tile_floats) + w);
 #pragma unroll
                 for (int q = 0; q < 3; q++)
 #pragma unroll
@@ -783,14 +821,14 @@ FIS_DEV void fast_epilogue(const fis_gemm_args& a, const EpiCtx& e, const Shared
             for (; zz < S; zz++) {
 #pragma unroll
                 for (int w = 0; w < 2; w++) {
-                    const float4 f = __ldcg((const float4*)(p + zz * tile_floats) + w);
+                    const float4 f = *((const float4*)(p + zz * tile_floats) + w);
                     v[4 * w] += f.x; v[4 * w + 1] += f.y; v[4 * w + 2] += f.z; v[4 * w + 3] += f.w;
                 }
             }
         }
         float x[8];
         if (has_x) {
-            const unsigned char* xr = sh.res + row * RES_LD + cb * xesz;
+            const unsigned char* xr = (vm_ring() + STAGES * STAGE) + row * RES_LD + cb * xesz;
             if (xdt == FIS_BF16) {
                 const uint4 u = *(const uint4*)xr;
                 const __nv_bfloat162* h = (const __nv_bfloat162*)&u;
@@ -805,16 +843,24 @@ FIS_DEV void fast_epilogue(const fis_gemm_args& a, const EpiCtx& e, const Shared
             }
         }
         // same operations, same order as fis::tc::row_epilogue
+        {
+            float t8[8];
+            ld8(vm_tab().bias, t8);
 #pragma unroll
-        for (int k = 0; k < 8; k++) v[k] = __fadd_rn(v[k] * alpha, bias[k]);
-        if (has_b2) {
+            for (int k = 0; k < 8; k++) v[k] = __fadd_rn(v[k] * alpha, t8[k]);
+            if (has_b2) {
+                ld8(vm_tab().b2, t8);
 #pragma unroll
-            for (int k = 0; k < 8; k++) v[k] = __fadd_rn(v[k], b2[k]);
+                for (int k = 0; k < 8; k++) v[k] = __fadd_rn(v[k], t8[k]);
+            }
         }
         if (MODE == FIS_EPI_GN_SILU) {
+            float gs[8], gh[8];
+            ld8(vm_tab().mean, gs);
+            ld8(vm_tab().rstd, gh);
 #pragma unroll
             for (int k = 0; k < 8; k++) {
-                const float y = fmaf(v[k], gscale[k], gshift[k]);
+                const float y = fmaf(v[k], gs[k], gh[k]);
                 v[k] = __fdividef(y, 1.0f + __expf(-y));
             }
         } else if (MODE == FIS_EPI_STEP) {
@@ -852,23 +898,23 @@ template <int BN>
 FIS_DEV void gemm_tc_epilogue(const fis_vm_args& va, const Shared& sh, int j, int i,
                                               const GemmItem& g, ProdState& ps, uint32_t tmem, int tid,
                                               bool tables_done, bool staged) {
-    const fis_vm_op& op = *sh.op;
+    const fis_vm_op& op = s_op;
     const fis_gemm_args& a = op.u.gemm;
     const int warp = tid >> 5, lane = tid & 31;
     const int t = s_step;
     const EpiCtx e = make_epi(a, t);
     if (!tables_done) stage_tables(a, e, sh, g.n0, g.bn, tid);
     VM_STAMP(4);
-    mbar_wait_backoff(sh.done, ps.items & 1);
+    mbar_wait_backoff((s_bar + 2 * STAGES), ps.items & 1);
     ps.items++;
     tc_fence_after();
     VM_STAMP(5);
     // ---- 1. TMEM -> staging (the ring is idle: every MMA of this item has completed)
     constexpr int PLD = BN + 4;
-    constexpr int hc = BN / 2;  // columns per warp half
-    float* stage = (float*)sh.ring;
+    constexpr int hc = BN / WPQ;  // columns per warp of a lane quarter
+    float* stage = (float*)vm_ring();
     {
-        const int quarter = warp & 3, half = warp >> 2;
+        const int quarter = warp & 3, half = warp >> 2;  // WPQ warps share a lane quarter
         const int lr = quarter * 32 + lane;
         const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) + half * hc;
         float* dst = stage + lr * PLD + half * hc;
@@ -891,26 +937,51 @@ FIS_DEV void gemm_tc_epilogue(const fis_vm_args& va, const Shared& sh, int j, in
     int r0 = 0, r1 = BM;
     const float* wsb = nullptr;
     const long long tile_floats = (long long)BM * BN;
+    long long tile_floats_red = tile_floats;  // stride between split partials as the reduce reads them
     if (S > 1) {
-        // ---- 2b. publish the partial (coalesced float4 rows), meet the other splits of the tile
+        // ---- 2b. publish the partial with bulk copies (one 512 B row per thread), meet the other
+        //      splits of the tile, then bulk-load this split's rows of all S partials into smem
         float* wsz = va.ws + ((long long)g.tile * S + g.z) * tile_floats;
-        for (int idx = tid; idx < BM * (BN / 4); idx += PRODUCERS) {
-            const int row = idx / (BN / 4), c4 = (idx % (BN / 4)) * 4;
-            __stcg((float4*)(wsz + row * BN + c4), *(const float4*)(stage + row * PLD + c4));
+        if (tid < BM) {
+            asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(wsz + tid * BN),
+                         "r"(smem_u32(stage + tid * PLD)), "r"(BN * 4)
+                         : "memory");
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+            asm volatile("fence.proxy.async.global;" ::: "memory");
         }
         pbar();
+        const int rows_per = (BM + S - 1) / S;
+        r0 = min(BM, g.z * rows_per);
+        r1 = min(BM, r0 + rows_per);
+        const int slice_floats = rows_per * BN;
+        float* red = (float*)vm_ring();  // staging is free once the partial is published
         if (tid == 0) {
             fence_acq_rel();
             int* ctr = va.sync + op.sync_base + g.tile;
             atomicAdd(ctr, 1);
             spin_until(ctr, S, 32);
+            asm volatile("fence.proxy.async.global;" ::: "memory");
+            const uint32_t bytes = (uint32_t)((r1 - r0) * BN * 4);
+            if (bytes) {
+                expect_tx((s_bar + 2 * STAGES + 4), bytes * S);
+                const float* src0 = va.ws + (long long)g.tile * S * tile_floats + (long long)r0 * BN;
+                for (int z = 0; z < S; z++)
+                    asm volatile(
+                        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                            smem_u32(red + z * slice_floats)),
+                        "l"(src0 + z * tile_floats), "r"(bytes), "r"(smem_u32((s_bar + 2 * STAGES + 4)))
+                        : "memory");
+            } else {
+                mbar_arrive((s_bar + 2 * STAGES + 4));
+            }
         }
-        pbar();
+        mbar_wait_backoff((s_bar + 2 * STAGES + 4), ps.red & 1, 32);
+        ps.red++;
         VM_STAMP(11);
-        const int rows_per = (BM + S - 1) / S;
-        r0 = min(BM, g.z * rows_per);
-        r1 = min(BM, r0 + rows_per);
-        wsb = va.ws + (long long)g.tile * S * tile_floats;
+        // the reduce reads index wsb + row * BN + z * tile_floats with row in [r0, r1)
+        wsb = red - r0 * BN;
+        tile_floats_red = slice_floats;
     }
     // ---- 2. fused epilogue of rows [r0, r1), 8-column items
     const int nrows = min(r1, a.m - g.m0) - r0;
@@ -921,11 +992,11 @@ FIS_DEV void gemm_tc_epilogue(const fis_vm_args& va, const Shared& sh, int j, in
     if (!trans && !a.d_rows && (staged || (!e.res && a.epi != FIS_EPI_STEP)) && !e.pre && !e.pre2 &&
         a.d.dtype == FIS_BF16 && (a.d.ld % 8) == 0 && (((uintptr_t)e.d) & 15) == 0 && (g.n0 % 8) == 0) {
         if (a.epi == FIS_EPI_GN_SILU)
-            fast_epilogue<BN, FIS_EPI_GN_SILU>(a, e, sh, g, stage, wsb, tile_floats, S, r0, nrows, staged, tid);
+            fast_epilogue<BN, FIS_EPI_GN_SILU>(a, e, sh, g, stage, wsb, tile_floats_red, S, r0, nrows, staged, tid);
         else if (a.epi == FIS_EPI_STEP)
-            fast_epilogue<BN, FIS_EPI_STEP>(a, e, sh, g, stage, wsb, tile_floats, S, r0, nrows, staged, tid);
+            fast_epilogue<BN, FIS_EPI_STEP>(a, e, sh, g, stage, wsb, tile_floats_red, S, r0, nrows, staged, tid);
         else
-            fast_epilogue<BN, FIS_EPI_NONE>(a, e, sh, g, stage, wsb, tile_floats, S, r0, nrows, staged, tid);
+            fast_epilogue<BN, FIS_EPI_NONE>(a, e, sh, g, stage, wsb, tile_floats_red, S, r0, nrows, staged, tid);
         VM_STAMP(6);
         signal_done(va, j, tid);
         VM_STAMP(7);
@@ -958,7 +1029,7 @@ FIS_DEV void gemm_tc_epilogue(const fis_vm_args& va, const Shared& sh, int j, in
             }
             const int esz = (a.epi == FIS_EPI_STEP ? a.lat.dtype : a.res.dtype) == FIS_BF16 ? 2 : 4;
             epilogue8_load(a, e, g.m0 + row, g.n0 + ch * 8, in[u],
-                           staged ? sh.res + row * RES_LD + ch * 8 * esz : nullptr);
+                           staged ? (vm_ring() + STAGES * STAGE) + row * RES_LD + ch * 8 * esz : nullptr);
         }
         if (S > 1) {
 #pragma unroll
@@ -973,7 +1044,7 @@ FIS_DEV void gemm_tc_epilogue(const fis_vm_args& va, const Shared& sh, int j, in
 #pragma unroll
                     for (int q = 0; q < 4; q++)
 #pragma unroll
-                        for (int w = 0; w < 2; w++) f[q][w] = __ldcg((const float4*)(p + (zz + q) * tile_floats) + w);
+                        for (int w = 0; w < 2; w++) f[q][w] = *((const float4*)(p + (zz + q) * tile_floats_red) + w);
 #pragma unroll
                     for (int q = 0; q < 4; q++)
 #pragma unroll
@@ -985,7 +1056,7 @@ FIS_DEV void gemm_tc_epilogue(const fis_vm_args& va, const Shared& sh, int j, in
                 for (; zz < S; zz++) {
 #pragma unroll
                     for (int w = 0; w < 2; w++) {
-                        const float4 f = __ldcg((const float4*)(p + zz * tile_floats) + w);
+                        const float4 f = *((const float4*)(p + zz * tile_floats_red) + w);
                         v[u][4 * w] += f.x; v[u][4 * w + 1] += f.y; v[u][4 * w + 2] += f.z; v[u][4 * w + 3] += f.w;
                     }
                 }
@@ -994,7 +1065,7 @@ FIS_DEV void gemm_tc_epilogue(const fis_vm_args& va, const Shared& sh, int j, in
         const long long c1 = clock64();
 #pragma unroll
         for (int u = 0; u < IB; u++)
-            if (cbv[u] >= 0) epilogue8(a, e, sh.tb, g.m0 + rowv[u], cbv[u], g.n0, v[u], in[u]);
+            if (cbv[u] >= 0) epilogue8(a, e, vm_tab(), g.m0 + rowv[u], cbv[u], g.n0, v[u], in[u]);
         cy_load += c1 - c0;
         cy_epi += clock64() - c1;
     }
@@ -1017,13 +1088,13 @@ FIS_DEV void gemm_tc_epilogue(const fis_vm_args& va, const Shared& sh, int j, in
 template <int DVS>
 FIS_DEV void attn_item_run(const fis_vm_args& va, const Shared& sh, int j, int i, ProdState& ps, bool& waited,
                            uint32_t tmem, int tid) {
-    const fis_vm_op& op = *sh.op;
+    const fis_vm_op& op = s_op;
     const fis_attn_args& a = op.u.attn;
     const AttnItem g = attn_item(op, i);
     const int t = s_step;
     const int warp = tid >> 5, lane = tid & 31;
-    const int ar = tid >> 1, j0 = (tid & 1) * 4;
-    const uint32_t sbase = smem_u32(sh.ring);
+    const int ar = tid / TPR, j0 = (tid % TPR) * CPT;
+    const uint32_t sbase = smem_u32(vm_ring());
     // epilogue view of the output: a GEMM-style epilogue over [m, dv] with the residual
     if (tid == 0) {
         fis_gemm_args& e = s_ea;
@@ -1032,11 +1103,12 @@ FIS_DEV void attn_item_run(const fis_vm_args& va, const Shared& sh, int j, int i
         e.res = a.res; e.pre = a.pre; e.d = a.out;
     }
     for (int c = tid; c < DVS; c += PRODUCERS) {
-        sh.tb.bias[c] = 0.f; sh.tb.b2[c] = 0.f; sh.tb.mean[c] = 0.f; sh.tb.rstd[c] = 0.f;
+        vm_tab().bias[c] = 0.f; vm_tab().b2[c] = 0.f; vm_tab().mean[c] = 0.f; vm_tab().rstd[c] = 0.f;
     }
     VM_STAMP(0);
     wait_dep(va, op, j, waited, tid);  // Q, K, V^T and the residual come from earlier ops
     pbar();                            // s_ea visible
+    if (va.trace_items && j == va.trace_op && tid == 0) va.trace_items[16 * i + 14] = clock64();
     GemmItem ge;
     ge.z = 0; ge.tile = 0; ge.n0 = g.c0; ge.m0 = g.m0; ge.kb0 = 0; ge.nk = 0; ge.bn = DVS;
     VM_STAMP(2);
@@ -1047,156 +1119,170 @@ FIS_DEV void attn_item_run(const fis_vm_args& va, const Shared& sh, int j, int i
     const void* tq = tmap_at(va, op.tmap_a);
     const void* tk = tmap_at(va, op.tmap_b);
     const void* tv = tmap_at(va, op.tmap_a2);
-    // ---- S phase loads, d-chunk major: slot (kc, jb) carries K chunk (jb, kc); slot (kc, 0) also
-    //      carries Q chunk kc, which the MMAs of every key block of that chunk read
+    // ---- S phase loads, key-block major: slot (jb, kc) carries Q chunk kc and K chunk (jb, kc)
     const int qr = g.m0 + ar;
     if (tq && tk) {
         if (tid == 0) {
             uint32_t sq = ps.it;
-            for (int kc = 0; kc < g.dch; kc++)
-                for (int jb = 0; jb < g.nkb; jb++, sq++) {
+            for (int jb = 0; jb < g.nkb; jb++)
+                for (int kc = 0; kc < g.dch; kc++, sq++) {
                     const int s = sq % STAGES;
-                    if (sq >= STAGES) mbar_wait_backoff(sh.empty + s, ((sq / STAGES) & 1) ^ 1);
+                    if (sq >= STAGES) mbar_wait((s_bar + STAGES) + s, ((sq / STAGES) & 1) ^ 1);
                     const uint32_t sa = sbase + s * STAGE;
-                    expect_tx(sh.full + s, (uint32_t)(BM * BK * 2) * (jb == 0 ? 2u : 1u));
-                    if (jb == 0) tma2d(sa, tq, kc * 64, g.m0, sh.full + s);
-                    tma2d(sa + A_BYTES, tk, kc * 64, 128 * jb, sh.full + s);
+                    expect_tx(s_bar + s, (uint32_t)(2 * BM * BK * 2));
+                    tma2d(sa, tq, kc * 64, g.m0, s_bar + s);
+                    tma2d(sa + A_BYTES, tk, kc * 64, 128 * jb, s_bar + s);
                 }
         }
         ps.it += g.dch * g.nkb;
     } else {
-        for (int kc = 0; kc < g.dch; kc++)
-            for (int jb = 0; jb < g.nkb; jb++) {
+        for (int jb = 0; jb < g.nkb; jb++)
+            for (int kc = 0; kc < g.dch; kc++) {
                 const int key = 128 * jb + ar;
                 const uint32_t sq = ps.it++;
                 const int s = sq % STAGES;
-                if (sq >= STAGES) mbar_wait_backoff(sh.empty + s, ((sq / STAGES) & 1) ^ 1);
+                if (sq >= STAGES) mbar_wait((s_bar + STAGES) + s, ((sq / STAGES) & 1) ^ 1);
                 const uint32_t sa = sbase + s * STAGE, sb = sa + A_BYTES;
                 const char* qs = qb + ((long long)qr * a.q.ld + kc * 64) * 2;
                 const char* ks = kb + ((long long)key * a.k.ld + kc * 64) * 2;
 #pragma unroll
-                for (int u = j0; u < j0 + 4; u++) {
-                    if (jb == 0)
-                        cp_async16(sa + sw128_off(ar, u), qr < a.m ? (const void*)(qs + 16 * u) : (const void*)qb,
-                                   qr < a.m);
+                for (int u = j0; u < j0 + CPT; u++) {
+                    cp_async16(sa + sw128_off(ar, u), qr < a.m ? (const void*)(qs + 16 * u) : (const void*)qb, qr < a.m);
                     cp_async16(sb + sw128_off(ar, u), key < n_keys ? (const void*)(ks + 16 * u) : (const void*)qb,
                                key < n_keys);
                 }
-                cp_async_arrive_inc(sh.full + s);
+                cp_async_arrive_inc(s_bar + s);
                 pbar();
-                if (tid == 0) mbar_arrive(sh.full + s);
+                if (tid == 0) mbar_arrive(s_bar + s);
             }
     }
     const bool staged = stage_operand(s_ea, sh, ge, t, tid);  // residual rows, land during the MMAs
     VM_STAMP(3);
     // ---- exact softmax statistics over every key block (thread = row lr, key half hf)
-    mbar_wait_backoff(sh.s_ready, ps.attn & 1);
+    mbar_wait_backoff((s_bar + 2 * STAGES + 1), ps.attn & 1);
     ps.attn++;
     tc_fence_after();
+    VM_STAMP(8);
+    constexpr int KPT = 128 / WPQ;  // keys of a block handled by each thread of a row
     const int quarter = warp & 3, hf = warp >> 2, lr = quarter * 32 + lane;
     const uint32_t trow = tmem + ((uint32_t)(quarter * 32) << 16);
-    const float scale = a.scale;
+    const float scale = a.scale * 1.4426950408889634f;  // exp(s*scale - m) = 2^(s*scale*log2e - m')
     float mx = -INFINITY;
     for (int jb = 0; jb < g.nkb; jb++) {
-        const int k0 = 128 * jb + 64 * hf;
+        const int k0 = 128 * jb + KPT * hf;
 #pragma unroll 1
-        for (int q = 0; q < 4; q++) {
+        for (int q = 0; q < KPT / 16; q++) {
             if (k0 + 16 * q >= n_keys) break;
             float v[16];
-            tmem_ld16(trow + 128 * jb + 64 * hf + 16 * q, v);
+            tmem_ld16(trow + 128 * jb + KPT * hf + 16 * q, v);
 #pragma unroll
             for (int u = 0; u < 16; u++)
                 if (k0 + 16 * q + u < n_keys) mx = fmaxf(mx, v[u] * scale);
         }
     }
-    s_rowstat[hf][lr] = mx;
-    pbar();
-    mx = fmaxf(s_rowstat[0][lr], s_rowstat[1][lr]);
+    VM_STAMP(9);
+    if (WPQ > 1) {
+        s_rowstat[hf][lr] = mx;
+        pbar();
+        mx = fmaxf(s_rowstat[0][lr], s_rowstat[1][lr]);
+    }
     float sum = 0.f;
     for (int jb = 0; jb < g.nkb; jb++) {
-        const int k0 = 128 * jb + 64 * hf;
+        const int k0 = 128 * jb + KPT * hf;
 #pragma unroll 1
-        for (int q = 0; q < 4; q++) {
+        for (int q = 0; q < KPT / 16; q++) {
             if (k0 + 16 * q >= n_keys) break;
             float v[16];
-            tmem_ld16(trow + 128 * jb + 64 * hf + 16 * q, v);
+            tmem_ld16(trow + 128 * jb + KPT * hf + 16 * q, v);
 #pragma unroll
             for (int u = 0; u < 16; u++)
-                if (k0 + 16 * q + u < n_keys) sum += expf(v[u] * scale - mx);
+                if (k0 + 16 * q + u < n_keys) sum += ex2(fmaf(v[u], scale, -mx));
         }
     }
-    pbar();  // both halves have read the max
-    s_rowstat[hf][lr] = sum;
-    pbar();
-    const float inv = 1.0f / (s_rowstat[0][lr] + s_rowstat[1][lr]);
+    if (WPQ > 1) {
+        pbar();  // both halves have read the max
+        s_rowstat[hf][lr] = sum;
+        pbar();
+        sum = s_rowstat[0][lr] + s_rowstat[1][lr];
+    }
+    const float inv = 1.0f / sum;
     VM_STAMP(4);
-    // ---- per key block: P_j -> shared memory (SW128 K-major, chunk hf = keys [64 hf, 64 hf + 64)), then V_j
+    VM_STAMP(10);
+    // ---- per key block: P_j -> shared memory (SW128 K-major, chunk hf = keys [64 hf, 64 hf + 64)).
+    //      V_j's chunks are loaded one block ahead (they only need ring slots), so each P.V MMA
+    //      finds its operands resident as soon as P_j is written.
     const int vr = g.c0 + ar;  // value channel row of V^T loaded by this thread
-    for (int jb = 0; jb < g.nkb; jb++) {
-        if (ps.pb > 0) mbar_wait_backoff(sh.p_free, (ps.pb - 1) & 1);  // the previous P.V MMAs are done with the tile
-        tc_fence_after();
-        const int k0 = 128 * jb + 64 * hf;
-        unsigned char* pt = sh.pbuf + hf * (BM * 128);
-#pragma unroll 1
-        for (int q = 0; q < 4; q++) {
-            float v[16];
-            if (k0 + 16 * q < n_keys) tmem_ld16(trow + 128 * jb + 64 * hf + 16 * q, v);
-            uint4 pk[2];
-            __nv_bfloat162* h = (__nv_bfloat162*)pk;
-#pragma unroll
-            for (int u = 0; u < 8; u++) {
-                const int kk = k0 + 16 * q + 2 * u;
-                const float p0 = kk < n_keys ? expf(v[2 * u] * scale - mx) * inv : 0.f;
-                const float p1 = kk + 1 < n_keys ? expf(v[2 * u + 1] * scale - mx) * inv : 0.f;
-                h[u] = __floats2bfloat162_rn(p0, p1);
-            }
-            *(uint4*)(pt + sw128_off(lr, 2 * q)) = pk[0];
-            *(uint4*)(pt + sw128_off(lr, 2 * q + 1)) = pk[1];
-        }
-        fence_async_smem();  // generic-proxy P writes -> tensor-core reads
-        tc_fence_before();
-        mbar_arrive(sh.p_ready);
-        ps.pb++;
-        // V^T rows (value channels) x 64-key chunks of block j
+    auto issue_v = [&](int jb) {
         const int nch = (attn_nb(n_keys, jb) + 63) / 64;
         if (tv) {
             if (tid == 0)
                 for (int c = 0; c < nch; c++) {
                     const uint32_t sq = ps.it + c;
                     const int s = sq % STAGES;
-                    if (sq >= STAGES) mbar_wait_backoff(sh.empty + s, ((sq / STAGES) & 1) ^ 1);
-                    expect_tx(sh.full + s, (uint32_t)(BK * DVS * 2));
-                    tma2d(sbase + s * STAGE + A_BYTES, tv, 128 * jb + 64 * c, g.c0, sh.full + s);
+                    if (sq >= STAGES) mbar_wait((s_bar + STAGES) + s, ((sq / STAGES) & 1) ^ 1);
+                    expect_tx(s_bar + s, (uint32_t)(BK * DVS * 2));
+                    tma2d(sbase + s * STAGE + A_BYTES, tv, 128 * jb + 64 * c, g.c0, s_bar + s);
                 }
             ps.it += nch;
         } else {
             for (int c = 0; c < nch; c++) {
                 const uint32_t sq = ps.it++;
                 const int s = sq % STAGES;
-                if (sq >= STAGES) mbar_wait_backoff(sh.empty + s, ((sq / STAGES) & 1) ^ 1);
+                if (sq >= STAGES) mbar_wait((s_bar + STAGES) + s, ((sq / STAGES) & 1) ^ 1);
                 const uint32_t sb = sbase + s * STAGE + A_BYTES;
                 const int kv0 = 128 * jb + 64 * c;
                 if (ar < DVS) {
                     const char* vs = vb + ((long long)vr * a.vt.ld + kv0) * 2;
 #pragma unroll
-                    for (int u = j0; u < j0 + 4; u++) {
+                    for (int u = j0; u < j0 + CPT; u++) {
                         const bool ok = vr < a.dv && kv0 + 8 * u < n_keys;
                         cp_async16(sb + sw128_off(ar, u), ok ? (const void*)(vs + 16 * u) : (const void*)vb, ok);
                     }
                 }
-                cp_async_arrive_inc(sh.full + s);
+                cp_async_arrive_inc(s_bar + s);
                 pbar();
-                if (tid == 0) mbar_arrive(sh.full + s);
+                if (tid == 0) mbar_arrive(s_bar + s);
             }
         }
+    };
+    issue_v(0);
+    for (int jb = 0; jb < g.nkb; jb++) {
+        if (ps.pb > 0) mbar_wait_backoff((s_bar + 2 * STAGES + 3), (ps.pb - 1) & 1, 32);  // previous P.V MMAs done with the tile
+        tc_fence_after();
+        const int k0 = 128 * jb + KPT * hf;
+#pragma unroll 1
+        for (int q = 0; q < KPT / 16; q++) {
+            unsigned char* pt = (vm_ring() + STAGES * STAGE + RES_BYTES) + ((KPT * hf + 16 * q) / 64) * (BM * 128);
+            const int unit = ((16 * q) % 64) / 8;  // 16-byte unit of the 64-key SW128 chunk
+            float v[16];
+            if (k0 + 16 * q < n_keys) tmem_ld16(trow + 128 * jb + KPT * hf + 16 * q, v);
+            uint4 pk[2];
+            __nv_bfloat162* h = (__nv_bfloat162*)pk;
+#pragma unroll
+            for (int u = 0; u < 8; u++) {
+                const int kk = k0 + 16 * q + 2 * u;
+                const float p0 = kk < n_keys ? ex2(fmaf(v[2 * u], scale, -mx)) * inv : 0.f;
+                const float p1 = kk + 1 < n_keys ? ex2(fmaf(v[2 * u + 1], scale, -mx)) * inv : 0.f;
+                h[u] = __floats2bfloat162_rn(p0, p1);
+            }
+            *(uint4*)(pt + sw128_off(lr, unit)) = pk[0];
+            *(uint4*)(pt + sw128_off(lr, unit + 1)) = pk[1];
+        }
+        fence_async_smem();  // generic-proxy P writes -> tensor-core reads
+        tc_fence_before();
+        mbar_arrive((s_bar + 2 * STAGES + 2));
+        ps.pb++;
+        if (jb == 0) VM_STAMP(11);
+        if (jb == g.nkb - 1) VM_STAMP(12);
+        if (jb + 1 < g.nkb) issue_v(jb + 1);
     }
     // ---- epilogue: O slice (TMEM) -> staging -> + residual -> bf16 rows
-    mbar_wait_backoff(sh.done, ps.items & 1);
+    mbar_wait_backoff((s_bar + 2 * STAGES), ps.items & 1);
     ps.items++;
     tc_fence_after();
     VM_STAMP(5);
-    constexpr int PLD = DVS + 4, hc = DVS / 2;
-    float* stage = (float*)sh.ring;
+    constexpr int PLD = DVS + 4, hc = DVS / WPQ;
+    float* stage = (float*)vm_ring();
     {
         const uint32_t taddr = trow + g.o_col + hf * hc;
         float* dst = stage + lr * PLD + hf * hc;
@@ -1226,12 +1312,13 @@ FIS_DEV void attn_item_run(const fis_vm_args& va, const Shared& sh, int j, int i
             for (int u = 0; u < 8; u++) v[u] = stage[row * PLD + cb + u];
             EpiIn in;
             epilogue8_load(s_ea, e, g.m0 + row, g.c0 + cb, in, nullptr);
-            epilogue8(s_ea, e, sh.tb, g.m0 + row, cb, g.c0, v, in);
+            epilogue8(s_ea, e, vm_tab(), g.m0 + row, cb, g.c0, v, in);
         }
     }
     VM_STAMP(6);
     signal_done(va, j, tid);
     VM_STAMP(7);
+    if (va.trace_items && j == va.trace_op && tid == 0) va.trace_items[16 * i + 15] = clock64();
 }
 
 // ---------------------------------------------------------------------------------- SIMT ops
@@ -1250,7 +1337,57 @@ FIS_DEV float gather_a_simt(const fis_gemm_args& a, const char* f0, const char* 
     return src_value(s, second ? f1 : f0, second ? c1p : c0p, sy * s.w + sx, c);
 }
 
-FIS_DEV void gemm_simt_item(const fis_gemm_args& a, unsigned char* scratch, int item, int tiles_n, int tid) {
+// Implicit 3x3 conv with 16-byte input pixels (the stem: 4 fp32 latent channels, unet.py:434):
+// thread = (output pixel, 32-column half); its 9 taps are read once as float4 rows with
+// select-on-read, the 64 x 36 weight tile sits in shared memory.  Same summation order as the
+// SIMT tile (k ascending, fmaf), then the fis::epilogue_store operations.
+__device__ __noinline__ bool stem_item(const fis_gemm_args& a, unsigned char* scratch, int item, int tiles_n, int tid) {
+    const fis_src& sr = a.src[0];
+    if (a.a_mode != FIS_A_CONV3X3 || a.nsrc != 1 || sr.c != 4 || sr.fresh.dtype != FIS_F32 || sr.up ||
+        (sr.index && sr.cache.dtype != FIS_F32) || a.k != 36 || PRODUCERS != 128)
+        return false;
+    const int t = s_step;
+    const int n0 = (item % tiles_n) * SBN, m0 = (item / tiles_n) * SBM;
+    float* Ws = (float*)scratch;  // [SBN][37]
+    const char* bbase = ref_base(a.b, t);
+    for (int e = tid; e < SBN * 36; e += PRODUCERS) {
+        const int n = e / 36, k = e % 36;
+        Ws[n * 37 + k] = n0 + n < a.n ? load_elem(bbase, a.b.dtype, (long long)(n0 + n) * a.b.ld + k) : 0.f;
+    }
+    const char* fr = ref_base(sr.fresh, t);
+    const char* ca = sr.index ? ref_base(sr.cache, t) : nullptr;
+    const int lr = tid % SBM, half = tid / SBM;
+    const int r = m0 + lr;
+    float x[36];
+    if (r < a.m) {
+        const int p = a.rows ? __ldg(a.rows + r) : r;
+        const int oy = p / a.out_w, ox = p - oy * a.out_w;
+#pragma unroll
+        for (int tap = 0; tap < 9; tap++) {
+            const int y = oy + tap / 3 - 1, xx = ox + tap % 3 - 1;
+            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (y >= 0 && xx >= 0 && y < a.out_h && xx < a.out_w) {
+                const RowPtr rp = src_row(sr, fr, ca, y * sr.w + xx);
+                v = *(const float4*)rp.p;
+            }
+            x[4 * tap] = v.x; x[4 * tap + 1] = v.y; x[4 * tap + 2] = v.z; x[4 * tap + 3] = v.w;
+        }
+    }
+    pbar();
+    if (r >= a.m) return true;
+    const EpiCtx e = make_epi(a, t);
+    for (int cc = 0; cc < SBN / 2; cc++) {
+        const int nl = half * (SBN / 2) + cc, n = n0 + nl;
+        if (n >= a.n) break;
+        float acc = 0.f;
+#pragma unroll
+        for (int k = 0; k < 36; k++) acc = fmaf(x[k], Ws[nl * 37 + k], acc);
+        epilogue_store(a, e, r, n, acc);
+    }
+    return true;
+}
+
+__device__ __noinline__ void gemm_simt_item(const fis_gemm_args& a, unsigned char* scratch, int item, int tiles_n, int tid) {
     float (*As)[SBM + 4] = (float (*)[SBM + 4])scratch;
     float (*Bs)[SBN + 4] = (float (*)[SBN + 4])(scratch + SBK * (SBM + 4) * 4);
     int* rowp = (int*)(scratch + 2 * SBK * (SBM + 4) * 4);
@@ -1272,19 +1409,20 @@ FIS_DEV void gemm_simt_item(const fis_gemm_args& a, unsigned char* scratch, int 
         rowx[tid] = p - rowy[tid] * max(1, a.out_w);
     }
     pbar();
+    constexpr int TY = PRODUCERS / 16, RPT = SBM / TY;  // thread grid 16 x TY, RPT rows x 4 columns each
     const int tx = tid % 16, ty = tid / 16;
-    float acc[4][4];
+    float acc[RPT][4];
 #pragma unroll
-    for (int i = 0; i < 4; i++)
+    for (int i = 0; i < RPT; i++)
 #pragma unroll
         for (int jj = 0; jj < 4; jj++) acc[i][jj] = 0.f;
-    const int lk = tid % SBK, lr = tid / SBK;
     const int ktiles = (a.k + SBK - 1) / SBK;
     for (int kt = 0; kt < ktiles; kt++) {
-        const int k = kt * SBK + lk;
-#pragma unroll
-        for (int i = 0; i < 4; i++) {
-            const int row = lr + 16 * i;
+        // the (row, k) elements of this pass: 32 A + 32 B gathers per thread, all independent
+#pragma unroll 4
+        for (int e = tid; e < SBM * SBK; e += PRODUCERS) {
+            const int row = e / SBK, lk = e % SBK;
+            const int k = kt * SBK + lk;
             const int r = m0 + row;
             float v = 0.f;
             if (r < a.m && k < a.k) v = gather_a_simt(a, f0, c0p, f1, c1p, abase, k, rowp[row], rowy[row], rowx[row]);
@@ -1297,13 +1435,13 @@ FIS_DEV void gemm_simt_item(const fis_gemm_args& a, unsigned char* scratch, int 
         pbar();
 #pragma unroll
         for (int kk = 0; kk < SBK; kk++) {
-            float av[4], bv[4];
+            float av[RPT], bv[4];
 #pragma unroll
-            for (int i = 0; i < 4; i++) av[i] = As[kk][ty * 4 + i];
+            for (int i = 0; i < RPT; i++) av[i] = As[kk][ty * RPT + i];
 #pragma unroll
             for (int jj = 0; jj < 4; jj++) bv[jj] = Bs[kk][tx * 4 + jj];
 #pragma unroll
-            for (int i = 0; i < 4; i++)
+            for (int i = 0; i < RPT; i++)
 #pragma unroll
                 for (int jj = 0; jj < 4; jj++) acc[i][jj] = fmaf(av[i], bv[jj], acc[i][jj]);
         }
@@ -1320,8 +1458,8 @@ FIS_DEV void gemm_simt_item(const fis_gemm_args& a, unsigned char* scratch, int 
             b2v[jj] = n < a.n && e.bias2 ? load_elem(e.bias2, a.bias2.dtype, n) : 0.f;
         }
 #pragma unroll
-        for (int i = 0; i < 4; i++) {
-            const int r = m0 + ty * 4 + i;
+        for (int i = 0; i < RPT; i++) {
+            const int r = m0 + ty * RPT + i;
             if (r >= a.m) continue;
 #pragma unroll
             for (int jj = 0; jj < 4; jj++) {
@@ -1337,8 +1475,8 @@ FIS_DEV void gemm_simt_item(const fis_gemm_args& a, unsigned char* scratch, int 
         return;
     }
 #pragma unroll
-    for (int i = 0; i < 4; i++) {
-        const int r = m0 + ty * 4 + i;
+    for (int i = 0; i < RPT; i++) {
+        const int r = m0 + ty * RPT + i;
         if (r >= a.m) continue;
 #pragma unroll
         for (int jj = 0; jj < 4; jj++) {
@@ -1349,7 +1487,7 @@ FIS_DEV void gemm_simt_item(const fis_gemm_args& a, unsigned char* scratch, int 
 }
 
 // softmax rows [item*8, item*8+8): one warp per row (tensors.py:183-192, unet.py:555-566)
-FIS_DEV void softmax_item(const fis_softmax_args& a, int item, int tid) {
+__device__ __noinline__ void softmax_item(const fis_softmax_args& a, int item, int tid) {
     const int t = s_step;
     const int row = item * SOFTMAX_ROWS + (tid >> 5);
     const int lane = tid & 31;
@@ -1432,7 +1570,7 @@ FIS_DEV void softmax_item(const fis_softmax_args& a, int item, int tid) {
 }
 
 // group-norm statistics of group `g` (tensors.py:129-146): two-pass f64, rounded to f32
-FIS_DEV void gn_stats_item(const fis_gn_stats_args& a, double* red, int g, int tid) {
+__device__ __noinline__ void gn_stats_item(const fis_gn_stats_args& a, double* red, int g, int tid) {
     const int t = s_step;
     const int cpg = a.c / a.groups;
     const long long cnt = (long long)a.hw * cpg;
@@ -1444,7 +1582,7 @@ FIS_DEV void gn_stats_item(const fis_gn_stats_args& a, double* red, int g, int t
     }
     red[tid] = s;
     pbar();
-    for (int o = 128; o; o >>= 1) {
+    for (int o = PRODUCERS / 2; o; o >>= 1) {
         if (tid < o) red[tid] += red[tid + o];
         pbar();
     }
@@ -1460,7 +1598,7 @@ FIS_DEV void gn_stats_item(const fis_gn_stats_args& a, double* red, int g, int t
     }
     red[tid] = v;
     pbar();
-    for (int o = 128; o; o >>= 1) {
+    for (int o = PRODUCERS / 2; o; o >>= 1) {
         if (tid < o) red[tid] += red[tid + o];
         pbar();
     }
@@ -1470,7 +1608,7 @@ FIS_DEV void gn_stats_item(const fis_gn_stats_args& a, double* red, int g, int t
     }
 }
 
-FIS_DEV void gn_apply_item(const fis_gn_apply_args& a, int item, int tid) {
+__device__ __noinline__ void gn_apply_item(const fis_gn_apply_args& a, int item, int tid) {
     const int t = s_step;
     const char* x = ref_base(a.x, t);
     const float* mean = (const float*)ref_base(a.mean, t);
@@ -1497,7 +1635,7 @@ FIS_DEV void gn_apply_item(const fis_gn_apply_args& a, int item, int tid) {
     }
 }
 
-FIS_DEV void pool_item(const fis_pool_args& a, int item, int tid) {
+__device__ __noinline__ void pool_item(const fis_pool_args& a, int item, int tid) {
     const int t = s_step;
     const char* fr = a.src.fresh.ptr ? ref_base(a.src.fresh, t) : nullptr;
     const char* ca = a.src.cache.ptr ? ref_base(a.src.cache, t) : nullptr;
@@ -1505,6 +1643,39 @@ FIS_DEV void pool_item(const fis_pool_args& a, int item, int tid) {
     const int cw = a.src.w / 2;
     const int total = a.n * a.c;
     const int e1 = min(total, (item + 1) * ELEMS_PER_ITEM);
+    const bool vec = a.src.fresh.dtype == FIS_BF16 && (!a.src.index || a.src.cache.dtype == FIS_BF16) &&
+                     a.out.dtype == FIS_BF16 && (a.c % 8) == 0 && (a.src.fresh.ld % 8) == 0 &&
+                     (!a.src.index || (a.src.cache.ld % 8) == 0) && (a.out.ld % 8) == 0 &&
+                     ((((uintptr_t)fr) | ((uintptr_t)ca) | ((uintptr_t)out)) & 15) == 0;
+    if (vec) {
+        // 8 channels (16 bytes) per unit: the 4 source rows are selected once, read as one vector each
+        for (int e = item * ELEMS_PER_ITEM + tid * 8; e < e1; e += PRODUCERS * 8) {
+            const int i = e / a.c, c = e - (e / a.c) * a.c;
+            const int P = a.rows ? __ldg(a.rows + i) : i;
+            const int py = P / cw, px = P - (P / cw) * cw;
+            const int q = (2 * py) * a.src.w + 2 * px;
+            const int qs[4] = {q, q + 1, q + a.src.w, q + a.src.w + 1};
+            uint4 u[4];
+#pragma unroll
+            for (int k = 0; k < 4; k++) {
+                const RowPtr rp = src_row(a.src, fr, ca, qs[k]);
+                u[k] = *(const uint4*)((const __nv_bfloat16*)rp.p + c);
+            }
+            uint4 o;
+            __nv_bfloat162* oh = (__nv_bfloat162*)&o;
+#pragma unroll
+            for (int h = 0; h < 4; h++) {
+                const float2 a0 = __bfloat1622float2(((const __nv_bfloat162*)&u[0])[h]);
+                const float2 a1 = __bfloat1622float2(((const __nv_bfloat162*)&u[1])[h]);
+                const float2 a2 = __bfloat1622float2(((const __nv_bfloat162*)&u[2])[h]);
+                const float2 a3 = __bfloat1622float2(((const __nv_bfloat162*)&u[3])[h]);
+                oh[h] = __floats2bfloat162_rn(__fmul_rn(__fadd_rn(__fadd_rn(a0.x, a1.x), __fadd_rn(a2.x, a3.x)), 0.25f),
+                                              __fmul_rn(__fadd_rn(__fadd_rn(a0.y, a1.y), __fadd_rn(a2.y, a3.y)), 0.25f));
+            }
+            *(uint4*)((__nv_bfloat16*)out + (long long)i * a.out.ld + c) = o;
+        }
+        return;
+    }
     for (int e = item * ELEMS_PER_ITEM + tid; e < e1; e += PRODUCERS) {
         const int i = e / a.c, c = e - (e / a.c) * a.c;
         const int P = a.rows ? __ldg(a.rows + i) : i;
@@ -1517,7 +1688,127 @@ FIS_DEV void pool_item(const fis_pool_args& a, int item, int tid) {
     }
 }
 
-FIS_DEV void materialize_item(const fis_materialize_args& a, int item, int tid) {
+// Group norm of one group (item = group): two-pass f64 statistics over the full map (rounded to
+// f32, tensors.py:129-146), written to mean/var, then the group's channels normalised with them
+// (+ SiLU) in fp32 (bf16 step VM).  Fuses group_norm's reduction and normalize_with_group_stats.
+__device__ __noinline__ void gn_item(const fis_gn_apply_args& a, double* red, int g, int tid) {
+    const int t = s_step;
+    const char* x = ref_base(a.x, t);
+    const int cpg = a.c / a.groups;
+    const int hw = a.rows;
+    const long long cnt = (long long)hw * cpg;
+    const int c0 = g * cpg;
+    auto reduce = [&](double v) -> double {
+#pragma unroll
+        for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if ((tid & 31) == 0) red[tid >> 5] = v;
+        pbar();
+        double r = 0.0;
+        for (int w = 0; w < PRODUCERS / 32; w++) r += red[w];
+        pbar();
+        return r;
+    };
+    char* yn = a.y_norm.ptr ? ref_base(a.y_norm, t) : nullptr;
+    char* ys = a.y_silu.ptr ? ref_base(a.y_silu, t) : nullptr;
+    const int vpr = cpg / 8;  // 16-byte vectors of the group per pixel
+    constexpr int MAXV = 12;  // group data held in registers: <= MAXV * PRODUCERS vectors
+    const bool vec = a.x.dtype == FIS_BF16 && (cpg % 8) == 0 && (a.x.ld % 8) == 0 && (c0 % 8) == 0 &&
+                     hw * vpr <= MAXV * PRODUCERS && (!yn || a.y_norm.dtype == FIS_BF16) &&
+                     (!ys || a.y_silu.dtype == FIS_BF16) && (((uintptr_t)x) & 15) == 0;
+    if (vec) {
+        // one vectorised read of the group into registers, f64 two-pass statistics from them
+        uint4 u[MAXV];
+        double s = 0.0;
+#pragma unroll
+        for (int k = 0; k < MAXV; k++) {
+            const int e = tid + k * PRODUCERS;
+            if (e < hw * vpr) {
+                const int q = e / vpr, c = c0 + 8 * (e % vpr);
+                u[k] = *(const uint4*)((const __nv_bfloat16*)x + (long long)q * a.x.ld + c);
+                const __nv_bfloat162* h = (const __nv_bfloat162*)&u[k];
+#pragma unroll
+                for (int w = 0; w < 4; w++) {
+                    const float2 f = __bfloat1622float2(h[w]);
+                    s += (double)f.x;
+                    s += (double)f.y;
+                }
+            }
+        }
+        const double mean = reduce(s) / (double)cnt;
+        double v = 0.0;
+#pragma unroll
+        for (int k = 0; k < MAXV; k++) {
+            const int e = tid + k * PRODUCERS;
+            if (e < hw * vpr) {
+                const __nv_bfloat162* h = (const __nv_bfloat162*)&u[k];
+#pragma unroll
+                for (int w = 0; w < 4; w++) {
+                    const float2 f = __bfloat1622float2(h[w]);
+                    const double d0 = (double)f.x - mean, d1 = (double)f.y - mean;
+                    v += d0 * d0;
+                    v += d1 * d1;
+                }
+            }
+        }
+        const double var = reduce(v) / (double)cnt;
+        const float mean_f = (float)mean, var_f = (float)var;
+        if (tid == 0) {
+            ((float*)ref_base(a.mean, t))[g] = mean_f;
+            ((float*)ref_base(a.var, t))[g] = var_f;
+        }
+        const float rstd = (float)(1.0 / sqrt((double)var_f + (double)a.eps));
+#pragma unroll
+        for (int k = 0; k < MAXV; k++) {
+            const int e = tid + k * PRODUCERS;
+            if (e < hw * vpr) {
+                const int q = e / vpr, c = c0 + 8 * (e % vpr);
+                const __nv_bfloat162* h = (const __nv_bfloat162*)&u[k];
+                uint4 on, os;
+                __nv_bfloat162* hn = (__nv_bfloat162*)&on;
+                __nv_bfloat162* hs = (__nv_bfloat162*)&os;
+#pragma unroll
+                for (int w = 0; w < 4; w++) {
+                    const float2 f = __bfloat1622float2(h[w]);
+                    const float y0 = fmaf((f.x - mean_f) * rstd, __ldg(a.gamma + c + 2 * w), __ldg(a.beta + c + 2 * w));
+                    const float y1 = fmaf((f.y - mean_f) * rstd, __ldg(a.gamma + c + 2 * w + 1), __ldg(a.beta + c + 2 * w + 1));
+                    hn[w] = __floats2bfloat162_rn(y0, y1);
+                    hs[w] = __floats2bfloat162_rn(__fdividef(y0, 1.0f + __expf(-y0)), __fdividef(y1, 1.0f + __expf(-y1)));
+                }
+                if (yn) *(uint4*)((__nv_bfloat16*)yn + (long long)q * a.y_norm.ld + c) = on;
+                if (ys) *(uint4*)((__nv_bfloat16*)ys + (long long)q * a.y_silu.ld + c) = os;
+            }
+        }
+        return;
+    }
+    double s = 0.0;
+    for (int e = tid; e < hw * cpg; e += PRODUCERS) {
+        const int q = e / cpg, c = c0 + (e - (e / cpg) * cpg);
+        s += (double)load_elem(x, a.x.dtype, (long long)q * a.x.ld + c);
+    }
+    const double mean = reduce(s) / (double)cnt;
+    double v = 0.0;
+    for (int e = tid; e < hw * cpg; e += PRODUCERS) {
+        const int q = e / cpg, c = c0 + (e - (e / cpg) * cpg);
+        const double d = (double)load_elem(x, a.x.dtype, (long long)q * a.x.ld + c) - mean;
+        v += d * d;
+    }
+    const double var = reduce(v) / (double)cnt;
+    const float mean_f = (float)mean, var_f = (float)var;
+    if (tid == 0) {
+        ((float*)ref_base(a.mean, t))[g] = mean_f;
+        ((float*)ref_base(a.var, t))[g] = var_f;
+    }
+    const float rstd = (float)(1.0 / sqrt((double)var_f + (double)a.eps));
+    for (int e = tid; e < hw * cpg; e += PRODUCERS) {
+        const int q = e / cpg, c = c0 + (e - (e / cpg) * cpg);
+        const float xv = load_elem(x, a.x.dtype, (long long)q * a.x.ld + c);
+        const float y = fmaf((xv - mean_f) * rstd, __ldg(a.gamma + c), __ldg(a.beta + c));
+        if (yn) store_elem(yn, a.y_norm.dtype, (long long)q * a.y_norm.ld + c, y);
+        if (ys) store_elem(ys, a.y_silu.dtype, (long long)q * a.y_silu.ld + c, __fdividef(y, 1.0f + __expf(-y)));
+    }
+}
+
+__device__ __noinline__ void materialize_item(const fis_materialize_args& a, int item, int tid) {
     const int t = s_step;
     const char* fr = a.src.fresh.ptr ? ref_base(a.src.fresh, t) : nullptr;
     const char* ca = a.src.cache.ptr ? ref_base(a.src.cache, t) : nullptr;
@@ -1532,7 +1823,7 @@ FIS_DEV void materialize_item(const fis_materialize_args& a, int item, int tid) 
 
 FIS_DEV void producer_role(const fis_vm_args& va, const Shared& sh, uint32_t tmem, int tid) {
     const int G = gridDim.x, cta = blockIdx.x;
-    ProdState ps{0, 0, 0, 0};
+    ProdState ps{0, 0, 0, 0, 0};
     for (int j = 0; j < va.n_ops; j++) {
         const fis_vm_op* gop = va.ops + j;
         const int n_items = gop->n_items;
@@ -1543,11 +1834,11 @@ FIS_DEV void producer_role(const fis_vm_args& va, const Shared& sh, uint32_t tme
         {
             static_assert(sizeof(fis_vm_op) % 8 == 0, "fis_vm_op is copied as 8-byte words");
             const long long* src = (const long long*)gop;
-            long long* dst = (long long*)sh.op;
+            long long* dst = (long long*)(&s_op);
             for (int w = tid; w < (int)sizeof(fis_vm_op) / 8; w += PRODUCERS) dst[w] = __ldg(src + w);
         }
         pbar();
-        const fis_vm_op& op = *sh.op;
+        const fis_vm_op& op = s_op;
         bool waited = false;
         for (; i < n_items; i += G) {
             switch (op.kind) {
@@ -1559,7 +1850,8 @@ FIS_DEV void producer_role(const fis_vm_args& va, const Shared& sh, uint32_t tme
                         VM_STAMP(0);
                         wait_dep(va, op, j, waited, tid);
                         VM_STAMP(2);
-                        gemm_simt_item(op.u.gemm, sh.ring, i, op.tiles_n, tid);
+                        if (!stem_item(op.u.gemm, vm_ring(), i, op.tiles_n, tid))
+                            gemm_simt_item(op.u.gemm, vm_ring(), i, op.tiles_n, tid);
                         VM_STAMP(6);
                         signal_done(va, j, tid);
                         VM_STAMP(7);
@@ -1580,7 +1872,15 @@ FIS_DEV void producer_role(const fis_vm_args& va, const Shared& sh, uint32_t tme
                     break;
                 case FIS_VM_GN_STATS:
                     wait_dep(va, op, j, waited, tid);
-                    gn_stats_item(op.u.gn_stats, (double*)sh.ring, i, tid);
+                    gn_stats_item(op.u.gn_stats, (double*)vm_ring(), i, tid);
+                    signal_done(va, j, tid);
+                    break;
+                case FIS_VM_GN:
+                    VM_STAMP(0);
+                    wait_dep(va, op, j, waited, tid);
+                    VM_STAMP(2);
+                    gn_item(op.u.gn_apply, (double*)vm_ring(), i, tid);
+                    VM_STAMP(6);
                     signal_done(va, j, tid);
                     break;
                 case FIS_VM_GN_APPLY:
@@ -1610,29 +1910,30 @@ __global__ void __launch_bounds__(THREADS, 1) vm_kernel(const fis_vm_args va) {
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     if (tid == 0) {
         for (int s = 0; s < STAGES; s++) {
-            mbar_init(sh.full + s, 1);  // thread 0's arrival (+ TMA bytes, + incrementing cp.async arrivals)
-            mbar_init(sh.empty + s, 1);
+            mbar_init(s_bar + s, 1);  // thread 0's arrival (+ TMA bytes, + incrementing cp.async arrivals)
+            mbar_init((s_bar + STAGES) + s, 1);
         }
-        mbar_init(sh.done, 1);
-        mbar_init(sh.s_ready, 1);
-        mbar_init(sh.p_ready, PRODUCERS);
-        mbar_init(sh.p_free, 1);
+        mbar_init((s_bar + 2 * STAGES), 1);
+        mbar_init((s_bar + 2 * STAGES + 1), 1);
+        mbar_init((s_bar + 2 * STAGES + 2), PRODUCERS);
+        mbar_init((s_bar + 2 * STAGES + 3), 1);
+        mbar_init((s_bar + 2 * STAGES + 4), 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == MMA_WARP) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(sh.tmem_slot)),
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32((&s_tmem))),
                      "n"(TMEM_COLS));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
-    const uint32_t tmem = *sh.tmem_slot;
+    const uint32_t tmem = *(&s_tmem);
     if (tid == 0) s_step = va.step ? *va.step : 0;
     __syncthreads();
 
     if (warp == MMA_WARP) mma_role(va, sh, tmem, lane);
-    else producer_role(va, sh, tmem, tid);
+    else if (tid < PRODUCERS) producer_role(va, sh, tmem, tid);
 
     tc_fence_before();
     __syncthreads();
@@ -1709,6 +2010,7 @@ extern "C" int fis_vm_op_size(void) { return (int)sizeof(fis_vm_op); }
 // Value-slice width of a VM attention op (64 or 128 columns dividing dv) such that the key
 // blocks (16-column rounded) and the O slice fit the 512 TMEM columns; 0 = not supported.
 extern "C" int fis_vm_attn_slice(int m, int n_keys, int d, int dv) {
+    if (!VM_FUSED_ATTN) return 0;
     if (m < 0 || n_keys < 1 || d % 64 || dv <= 0) return 0;
     const int s_cols = 128 * ((n_keys - 1) / 128) + ((n_keys - 128 * ((n_keys - 1) / 128) + 15) & ~15);
     for (int w = 128; w >= 64; w -= 64)
@@ -1832,6 +2134,12 @@ extern "C" int fis_vm_plan_tma(fis_vm_op* ops, int n, int n_ctas, long long* ws_
                 if (op.u.gn_stats.groups <= 0 || op.u.gn_stats.c % op.u.gn_stats.groups) return FIS_ERR_SHAPE;
                 op.n_items = op.u.gn_stats.groups;
                 break;
+            case FIS_VM_GN: {
+                const fis_gn_apply_args& a = op.u.gn_apply;
+                if (a.groups <= 0 || a.c % a.groups || a.x_rows || a.y_rows) return FIS_ERR_SHAPE;
+                op.n_items = a.rows > 0 ? a.groups : 0;
+                break;
+            }
             case FIS_VM_GN_APPLY: {
                 const fis_gn_apply_args& a = op.u.gn_apply;
                 if (a.groups <= 0 || a.c % a.groups) return FIS_ERR_SHAPE;

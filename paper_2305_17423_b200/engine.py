@@ -409,7 +409,8 @@ class Engine(Launcher):
         self._call("fis_gn_stats", a)
         self.launches += 1
 
-    def gn_apply(self, lid, x: DRef, rows, c, mean: DRef, var: DRef, y_norm: DRef | None, y_silu: DRef | None):
+    def gn_apply(self, lid, x: DRef, rows, c, mean: DRef, var: DRef, y_norm: DRef | None, y_silu: DRef | None,
+                 fused_stats: bool = False):
         gamma, beta = self.W.norm[lid]
         a = L.GnApplyArgs()
         a.rows, a.c, a.groups, a.eps = rows, c, self.groups, NORM_EPS
@@ -417,7 +418,7 @@ class Engine(Launcher):
         a.gamma, a.beta = L.ptr(gamma), L.ptr(beta)
         a.y_norm, a.y_silu = _r(y_norm), _r(y_silu)
         a.step = L.ptr(self.step_dev)
-        self._call("fis_gn_apply", a)
+        self._call("fis_gn" if fused_stats else "fis_gn_apply", a)
         self.launches += 1
 
     def pool(self, fv: FeatVal, rows, n, out: DRef):
@@ -503,8 +504,12 @@ class Engine(Launcher):
             co = plan.record(blk["conv"], 0) or DRef(self.scratch(f"co{tag}", (cap, c)))
             self._conv(plan, blk["conv"], [(x, False)], co, level)
             mean, var = plan.stats(nl)
-            self.gn_stats(co, cap, c, mean, var)
-            self.gn_apply(nl, co, cap, c, mean, var, plan.record(nl, 0), s)
+            if self.capture is not None:
+                # step VM: statistics + normalisation of each group in one op
+                self.gn_apply(nl, co, cap, c, mean, var, plan.record(nl, 0), s, fused_stats=True)
+            else:
+                self.gn_stats(co, cap, c, mean, var)
+                self.gn_apply(nl, co, cap, c, mean, var, plan.record(nl, 0), s)
         y1 = DRef(self.scratch(f"y1{tag}", (cap, c)))
         self.attn_self(blk["self_attn"], m, s, y1, level, tag, pre=plan.record(blk["self_attn"], 0))
         lid = blk["cross_attn"]

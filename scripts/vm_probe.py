@@ -15,7 +15,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2305_17423_b200 import _lib as L  # noqa: E402
 from paper_2305_17423_b200.engine import DRef, Launcher, VmProgram  # noqa: E402
 
-KIND = {1: "gemm", 2: "softmax", 3: "gn_stats", 4: "gn_apply", 5: "pool", 6: "materialize", 7: "attn"}
+KIND = {1: "gemm", 2: "softmax", 3: "gn_stats", 4: "gn_apply", 5: "pool", 6: "materialize", 7: "attn", 8: "gn"}
 
 
 def gemm_equivalence():
@@ -107,8 +107,9 @@ def step_trace(dense=False):
               "0 start,1 B issued,2 dep ok,3 A issued,4 tables,5 mma done,6 epi done,7 signaled,8 A0 issued,"
               "9 tmem staged,10 staged+bar,11 split met):")
         for i in range(min(st.shape[0], 4)):
-            vals = ["   -  " if v == 0 else f"{(v - t_dep) / 1e3:6.2f}" for v in st[i][:12]]
-            vals += [f"{v:7.0f}cy" for v in st[i][12:15]]
+            vals = ["   -  " if v == 0 else f"{(v - t_dep) / 1e3:6.2f}" for v in st[i][:14]]
+            if st[i][15] and st[i][14] and st[i][7] and st[i][2]:
+                vals.append(f"clk {(st[i][15] - st[i][14]) / (st[i][7] - st[i][2]) * 1e3:5.0f} MHz")
             print(f"   item {i:3d}: " + " ".join(vals))
         vm.args.trace_op, vm.args.trace_items = -1, None
 
@@ -154,7 +155,7 @@ def single_op():
         print(f"single op {m}x{n}x{k} res={res}: items {vm.items()[0][1]} splits {vm.items()[0][2]} "
               f"tma a/b {vm.ops_host[0].tmap_a}/{vm.ops_host[0].tmap_b}: {e0.elapsed_time(e1) * 100:.1f} us/launch")
         for i in range(min(st.shape[0], 6)):
-            print("   " + " ".join("   -  " if v == 0 else f"{(v - t0) / 1e3:6.2f}" for v in st[i][:12]))
+            print("   " + " ".join("   -  " if v == 0 else f"{(v - t0) / 1e3:6.2f}" for v in st[i][:15]))
 
 
 if __name__ == "__main__" and "single" in sys.argv:
