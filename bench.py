@@ -215,6 +215,16 @@ def run_ours(args):
     per_ms = ms / max(1, args.steps)
     value = ws * args.steps / (ms / 1e3)
 
+    # --- the same sparse step on the persistent step VM (csrc/fis_vm.cu; experimental engine)
+    vm_ms = None
+    if args.precision == "bf16":
+        use_vm = eng.use_vm
+        eng.use_vm = True
+        try:
+            ep_vm = U.EditPlan(eng, arena, mask, kv, lat0)
+            vm_ms = _time_runner(U._Runner(eng, ep_vm.plan, True), T, max(3, args.steps // 2), 3)
+        finally:
+            eng.use_vm = use_vm
     # --- dense UNet step on the same GPU (what edit() runs for a full mask; SURVEY §8 C3 bar)
     dense_ms = dense_step_ms(eng, U, P, cfg, kv, args)
     sweep = mask_sweep(eng, U, P, cfg, arena, kv, lat0, args) if args.sweep else None
@@ -243,10 +253,18 @@ def run_ours(args):
                    "l2": "inputs larger than L2 (weights+cache slab per step > 126 MB)", "precision": args.precision,
                    "generation_s": gen_s},
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": tf, "unit": "TFLOP/s",
-                     "frac": achieved / tf if tf else None, "traffic": None,
+                     "frac": achieved / tf if tf else None, "traffic": conv_traffic(),
                      "kernel": "fis_gemm gated-conv gather-GEMMs (13/step)",
-                     "note": f"algorithmic {gflop_conv:.2f} GFLOP/step over {conv_ms:.3f} ms of gated-conv GEMM time; "
-                             f"all GEMMs {gemm_ms:.3f} ms/step; peak {src}"},
+                     "note": f"algorithmic {gflop_conv:.2f} GFLOP/step over {conv_ms:.3f} ms of gated-conv GEMM time "
+                             f"(CUDA events, eager instrumented step); all GEMMs {gemm_ms:.3f} ms/step; peak {src}; "
+                             "traffic = ncu dram bytes of one L0 conv launch (profiles/r01/ncu_gated_conv.json) vs "
+                             "2.4 MB algorithmic (weights 1.84 MB + halo rows + output)"},
+        "step_hbm": {"bytes_per_step": WEIGHT_BYTES_BF16, "achieved_gbs": WEIGHT_BYTES_BF16 / (per_ms / 1e3) / 1e9,
+                     "peak_gbs": hbm, "frac": WEIGHT_BYTES_BF16 / (per_ms / 1e3) / 1e9 / hbm,
+                     "note": "whole step vs the weight-streaming floor (221.7 M bf16 params read once per step)"},
+        "step_vm": None if vm_ms is None else {"ms_per_step": vm_ms, "edit_steps_per_s": 1e3 / vm_ms,
+                                                "note": "same sparse step as ONE persistent cooperative launch "
+                                                        "(csrc/fis_vm.cu, FIS_VM=1); experimental, not the default"},
         "dense_baseline": {"ms_per_step": dense_ms, "steps_per_s": 1e3 / dense_ms,
                            "sparse_speedup": dense_ms / per_ms},
         "gpu_launches": per_step_launches * args.steps,
@@ -266,6 +284,18 @@ def run_ours(args):
     import torch.distributed as dist
     if dist.is_available() and dist.is_initialized():
         dist.destroy_process_group()
+
+
+WEIGHT_BYTES_BF16 = 2 * 221_700_000  # 221.7 M params of the SD-1.5-shape toy UNet
+
+
+def conv_traffic():
+    """DRAM bytes per launch of the profiled gated-conv GEMM (committed ncu capture), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01", "ncu_gated_conv.json")) as f:
+            return json.load(f)["traffic_bytes_per_launch"]
+    except Exception:
+        return None
 
 
 def _time_runner(runner, T, steps, warmup):

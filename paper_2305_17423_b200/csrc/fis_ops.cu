@@ -62,15 +62,25 @@ __global__ void gn_apply_kernel(const fis_gn_apply_args a) {
     char* ys = a.y_silu.ptr ? ref_base(a.y_silu, t) : nullptr;
     const int cpg = a.c / a.groups;
     const int total = a.rows * a.c;
+    const bool bf16_out = (!yn || a.y_norm.dtype == FIS_BF16) && (!ys || a.y_silu.dtype == FIS_BF16);
     for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
         const int r = e / a.c, c = e - (e / a.c) * a.c;
         const int xr = a.x_rows ? __ldg(a.x_rows + r) : r;
         const int yr = a.y_rows ? __ldg(a.y_rows + r) : r;
         const int g = c / cpg;
+        float y;
+        if (bf16_out) {
+            // bf16 mode: fp32 normalisation (the fp32-parity mode keeps the reference's f64)
+            const float rstd = (float)(1.0 / sqrt((double)var[g] + (double)a.eps));
+            y = fmaf((load_elem(x, a.x.dtype, (long long)xr * a.x.ld + c) - mean[g]) * rstd, a.gamma[c], a.beta[c]);
+            if (yn) store_elem(yn, a.y_norm.dtype, (long long)yr * a.y_norm.ld + c, y);
+            if (ys) store_elem(ys, a.y_silu.dtype, (long long)yr * a.y_silu.ld + c, __fdividef(y, 1.0f + __expf(-y)));
+            continue;
+        }
         const double xv = (double)load_elem(x, a.x.dtype, (long long)xr * a.x.ld + c);
         const double y64 = (xv - (double)mean[g]) / sqrt((double)var[g] + (double)a.eps) * (double)a.gamma[c] +
                            (double)a.beta[c];
-        const float y = (float)y64;
+        y = (float)y64;
         if (yn) store_elem(yn, a.y_norm.dtype, (long long)yr * a.y_norm.ld + c, y);
         if (ys) {
             const double yd = (double)y;
@@ -97,6 +107,37 @@ __global__ void softmax_kernel(const fis_softmax_args a) {
             const float v = cached[j];
             store_elem(pb, a.p.dtype, prow + j, v);
             if (mb) ((float*)mb)[(long long)row * a.map.ld + j] = v;
+        }
+    } else if (a.npairs == 0 && a.cols <= 32 * 16) {
+        // one pass: the row lives in registers (<= 16 values per lane), all loads in flight
+        // (same max / sum / normalise arithmetic as the multi-pass loop below)
+        const float* s = (const float*)ref_base(a.s, t) + (long long)row * a.s.ld;
+        float x[16];
+        float m = -INFINITY;
+#pragma unroll
+        for (int k = 0; k < 16; k++) {
+            const int j = lane + 32 * k;
+            x[k] = j < a.cols ? s[j] * a.scale : -INFINITY;
+        }
+#pragma unroll
+        for (int k = 0; k < 16; k++) m = fmaxf(m, x[k]);
+        m = warp_max(m);
+        float sum = 0.f;
+#pragma unroll
+        for (int k = 0; k < 16; k++) {
+            x[k] = lane + 32 * k < a.cols ? expf(x[k] - m) : 0.f;
+            sum += x[k];
+        }
+        sum = warp_sum(sum);
+        const float inv_sum = 1.0f / sum;
+#pragma unroll
+        for (int k = 0; k < 16; k++) {
+            const int j = lane + 32 * k;
+            if (j < a.cols) {
+                const float v = x[k] * inv_sum;
+                store_elem(pb, a.p.dtype, prow + j, v);
+                if (mb) ((float*)mb)[(long long)row * a.map.ld + j] = v;
+            }
         }
     } else {
         const float* s = (const float*)ref_base(a.s, t) + (long long)row * a.s.ld;
@@ -146,6 +187,35 @@ __global__ void pool2_kernel(const fis_pool_args a) {
     char* out = ref_base(a.out, t);
     const int cw = a.src.w / 2;
     const int total = a.n * a.c;
+    const bool vec = a.src.fresh.dtype == FIS_BF16 && (!a.src.index || a.src.cache.dtype == FIS_BF16) &&
+                     a.out.dtype == FIS_BF16 && (a.c % 8) == 0 && (a.src.fresh.ld % 8) == 0 &&
+                     (!a.src.index || (a.src.cache.ld % 8) == 0) && (a.out.ld % 8) == 0 &&
+                     ((((uintptr_t)fr) | ((uintptr_t)ca) | ((uintptr_t)out)) & 15) == 0;
+    if (vec) {  // 8 channels per thread: each of the 4 source rows selected once, read as one vector
+        for (int e = (blockIdx.x * blockDim.x + threadIdx.x) * 8; e < total; e += gridDim.x * blockDim.x * 8) {
+            const int i = e / a.c, c = e - (e / a.c) * a.c;
+            const int P = a.rows ? __ldg(a.rows + i) : i;
+            const int py = P / cw, px = P - (P / cw) * cw;
+            const int q = (2 * py) * a.src.w + 2 * px;
+            const int qs[4] = {q, q + 1, q + a.src.w, q + a.src.w + 1};
+            uint4 u[4];
+#pragma unroll
+            for (int k = 0; k < 4; k++) u[k] = *(const uint4*)((const __nv_bfloat16*)src_row(a.src, fr, ca, qs[k]).p + c);
+            uint4 o;
+            __nv_bfloat162* oh = (__nv_bfloat162*)&o;
+#pragma unroll
+            for (int h = 0; h < 4; h++) {
+                const float2 a0 = __bfloat1622float2(((const __nv_bfloat162*)&u[0])[h]);
+                const float2 a1 = __bfloat1622float2(((const __nv_bfloat162*)&u[1])[h]);
+                const float2 a2 = __bfloat1622float2(((const __nv_bfloat162*)&u[2])[h]);
+                const float2 a3 = __bfloat1622float2(((const __nv_bfloat162*)&u[3])[h]);
+                oh[h] = __floats2bfloat162_rn(__fmul_rn(__fadd_rn(__fadd_rn(a0.x, a1.x), __fadd_rn(a2.x, a3.x)), 0.25f),
+                                              __fmul_rn(__fadd_rn(__fadd_rn(a0.y, a1.y), __fadd_rn(a2.y, a3.y)), 0.25f));
+            }
+            *(uint4*)((__nv_bfloat16*)out + (long long)i * a.out.ld + c) = o;
+        }
+        return;
+    }
     for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
         const int i = e / a.c, c = e - (e / a.c) * a.c;
         const int P = a.rows ? __ldg(a.rows + i) : i;

@@ -64,7 +64,7 @@ __device__ __forceinline__ void load_row16(const char* base, int dtype, long lon
         if (nvalid == 16 && ((uintptr_t)p & 15) == 0) {
 #pragma unroll
             for (int q = 0; q < 2; q++) {
-                uint4 u = *(const uint4*)(p + 8 * q);
+                uint4 u = FIS_LD_U4(p + 8 * q);
                 const __nv_bfloat162* h = (const __nv_bfloat162*)&u;
 #pragma unroll
                 for (int k = 0; k < 4; k++) {
@@ -75,19 +75,19 @@ __device__ __forceinline__ void load_row16(const char* base, int dtype, long lon
             }
         } else {
 #pragma unroll
-            for (int j = 0; j < 16; j++) if (j < nvalid) v[j] = __bfloat162float(p[j]);
+            for (int j = 0; j < 16; j++) if (j < nvalid) v[j] = load_elem((const char*)p, FIS_BF16, j);
         }
     } else {
         const float* p = (const float*)base + off;
         if (nvalid == 16 && ((uintptr_t)p & 15) == 0) {
 #pragma unroll
             for (int q = 0; q < 4; q++) {
-                float4 f = *(const float4*)(p + 4 * q);
+                float4 f = FIS_LD_F4(p + 4 * q);
                 v[4 * q] = f.x; v[4 * q + 1] = f.y; v[4 * q + 2] = f.z; v[4 * q + 3] = f.w;
             }
         } else {
 #pragma unroll
-            for (int j = 0; j < 16; j++) if (j < nvalid) v[j] = p[j];
+            for (int j = 0; j < 16; j++) if (j < nvalid) v[j] = load_elem((const char*)p, FIS_F32, j);
         }
     }
 }

@@ -19,6 +19,7 @@
 // The ring, its phase and the TMEM accumulator persist across items and ops.
 // Split-K partials go to a workspace; the last-arriving CTA of a tile sums them in split
 // order (bitwise deterministic) and runs the epilogue.
+#define FIS_LOADS_CG 1  // every element load of this translation unit bypasses L1 (see fis_common.cuh)
 #include "fis_tc.cuh"
 
 namespace fis {
@@ -27,6 +28,9 @@ using namespace fis::tc;
 
 #ifndef VM_STAGES
 #define VM_STAGES 4
+#endif
+#ifndef VM_MIN_SPLIT_KB
+#define VM_MIN_SPLIT_KB 16  // K blocks below which a GEMM is not split (split items keep >= half of it)
 #endif
 #ifndef VM_FUSED_ATTN
 #define VM_FUSED_ATTN 1
@@ -385,9 +389,17 @@ FIS_DEV int ld_relaxed(const int* p) {
 
 FIS_DEV void fence_acq_rel() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 
+// Consumer side of an op dependency: relaxed polling, no acquire fence -- a gpu-scope acquire
+// invalidates the whole L1 (CCTL.IVALL), which would turn every later load of static data
+// (weights, index lists, op records) into an L2 round trip.  Instead every read of data produced
+// inside the launch bypasses L1 (ld.global.cg, cp.async.cg, TMA, bulk copies), and the producer
+// publishes with a release reduction after its stores.
 FIS_DEV void spin_until(const int* c, int target, int ns) {
     while (ld_relaxed(c) < target) __nanosleep(ns);
-    fence_acq_rel();
+}
+
+FIS_DEV void red_release_add(int* c, int v) {
+    asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(c), "r"(v) : "memory");
 }
 
 FIS_DEV void wait_dep(const fis_vm_args& va, const fis_vm_op& op, int j, bool& waited, int tid) {
@@ -409,8 +421,7 @@ FIS_DEV void wait_dep(const fis_vm_args& va, const fis_vm_op& op, int j, bool& w
 FIS_DEV void signal_done(const fis_vm_args& va, int j, int tid) {
     pbar();
     if (tid == 0) {
-        fence_acq_rel();
-        atomicAdd(va.sync + 1 + j, 1);
+        red_release_add(va.sync + 1 + j, 1);
         if (va.trace) atomicMax(va.trace + 2 * j + 1, gtimer());
     }
 }
@@ -454,7 +465,7 @@ FIS_DEV void load8(const char* base, int dtype, long long off, int nvalid, float
     if (dtype == FIS_BF16) {
         const __nv_bfloat16* p = (const __nv_bfloat16*)base + off;
         if (nvalid == 8 && ((uintptr_t)p & 15) == 0) {
-            const uint4 u = *(const uint4*)p;
+            const uint4 u = FIS_LD_U4(p);
             const __nv_bfloat162* h = (const __nv_bfloat162*)&u;
 #pragma unroll
             for (int k = 0; k < 4; k++) {
@@ -464,16 +475,16 @@ FIS_DEV void load8(const char* base, int dtype, long long off, int nvalid, float
             return;
         }
 #pragma unroll
-        for (int k = 0; k < 8; k++) if (k < nvalid) v[k] = __bfloat162float(p[k]);
+        for (int k = 0; k < 8; k++) if (k < nvalid) v[k] = load_elem((const char*)p, FIS_BF16, k);
     } else {
         const float* p = (const float*)base + off;
         if (nvalid == 8 && ((uintptr_t)p & 15) == 0) {
-            const float4 a0 = *(const float4*)p, a1 = *(const float4*)(p + 4);
+            const float4 a0 = FIS_LD_F4(p), a1 = FIS_LD_F4(p + 4);
             v[0] = a0.x; v[1] = a0.y; v[2] = a0.z; v[3] = a0.w; v[4] = a1.x; v[5] = a1.y; v[6] = a1.z; v[7] = a1.w;
             return;
         }
 #pragma unroll
-        for (int k = 0; k < 8; k++) if (k < nvalid) v[k] = p[k];
+        for (int k = 0; k < 8; k++) if (k < nvalid) v[k] = load_elem((const char*)p, FIS_F32, k);
     }
 }
 
@@ -957,9 +968,8 @@ FIS_DEV void gemm_tc_epilogue(const fis_vm_args& va, const Shared& sh, int j, in
         const int slice_floats = rows_per * BN;
         float* red = (float*)vm_ring();  // staging is free once the partial is published
         if (tid == 0) {
-            fence_acq_rel();
             int* ctr = va.sync + op.sync_base + g.tile;
-            atomicAdd(ctr, 1);
+            red_release_add(ctr, 1);
             spin_until(ctr, S, 32);
             asm volatile("fence.proxy.async.global;" ::: "memory");
             const uint32_t bytes = (uint32_t)((r1 - r0) * BN * 4);
@@ -1368,7 +1378,7 @@ __device__ __noinline__ bool stem_item(const fis_gemm_args& a, unsigned char* sc
             float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
             if (y >= 0 && xx >= 0 && y < a.out_h && xx < a.out_w) {
                 const RowPtr rp = src_row(sr, fr, ca, y * sr.w + xx);
-                v = *(const float4*)rp.p;
+                v = FIS_LD_F4(rp.p);
             }
             x[4 * tap] = v.x; x[4 * tap + 1] = v.y; x[4 * tap + 2] = v.z; x[4 * tap + 3] = v.w;
         }
@@ -1535,29 +1545,29 @@ __device__ __noinline__ void softmax_item(const fis_softmax_args& a, int item, i
     } else {
         const float* s = (const float*)ref_base(a.s, t) + (long long)row * a.s.ld;
         float m = -INFINITY;
-        for (int jj = lane; jj < a.cols; jj += 32) m = fmaxf(m, s[jj] * a.scale);
+        for (int jj = lane; jj < a.cols; jj += 32) m = fmaxf(m, __ldcg(s + jj) * a.scale);
         m = warp_max(m);
         float sum = 0.f;
-        for (int jj = lane; jj < a.cols; jj += 32) sum += expf(s[jj] * a.scale - m);
+        for (int jj = lane; jj < a.cols; jj += 32) sum += expf(__ldcg(s + jj) * a.scale - m);
         sum = warp_sum(sum);
         const float inv_sum = 1.0f / sum;
         if (a.npairs == 0) {
             for (int jj = lane; jj < a.cols; jj += 32) {
-                const float v = expf(s[jj] * a.scale - m) * inv_sum;
+                const float v = expf(__ldcg(s + jj) * a.scale - m) * inv_sum;
                 store_elem(pb, a.p.dtype, prow + jj, v);
                 if (mb) ((float*)mb)[(long long)row * a.map.ld + jj] = v;
             }
         } else {
             float rs = 0.f;
             for (int jj = lane; jj < a.cols; jj += 32) {
-                float v = expf(s[jj] * a.scale - m) * inv_sum;
+                float v = expf(__ldcg(s + jj) * a.scale - m) * inv_sum;
                 for (int i = 0; i < a.npairs; i++)
                     if (__ldg(a.pair_new + i) == jj) v = cached[__ldg(a.pair_old + i)];
                 rs += v;
             }
             rs = warp_sum(rs);
             for (int jj = lane; jj < a.cols; jj += 32) {
-                float v = expf(s[jj] * a.scale - m) * inv_sum;
+                float v = expf(__ldcg(s + jj) * a.scale - m) * inv_sum;
                 for (int i = 0; i < a.npairs; i++)
                     if (__ldg(a.pair_new + i) == jj) v = cached[__ldg(a.pair_old + i)];
                 const float o = (float)((double)v / (double)rs);
@@ -1659,7 +1669,7 @@ __device__ __noinline__ void pool_item(const fis_pool_args& a, int item, int tid
 #pragma unroll
             for (int k = 0; k < 4; k++) {
                 const RowPtr rp = src_row(a.src, fr, ca, qs[k]);
-                u[k] = *(const uint4*)((const __nv_bfloat16*)rp.p + c);
+                u[k] = FIS_LD_U4((const __nv_bfloat16*)rp.p + c);
             }
             uint4 o;
             __nv_bfloat162* oh = (__nv_bfloat162*)&o;
@@ -1724,7 +1734,7 @@ __device__ __noinline__ void gn_item(const fis_gn_apply_args& a, double* red, in
             const int e = tid + k * PRODUCERS;
             if (e < hw * vpr) {
                 const int q = e / vpr, c = c0 + 8 * (e % vpr);
-                u[k] = *(const uint4*)((const __nv_bfloat16*)x + (long long)q * a.x.ld + c);
+                u[k] = FIS_LD_U4((const __nv_bfloat16*)x + (long long)q * a.x.ld + c);
                 const __nv_bfloat162* h = (const __nv_bfloat162*)&u[k];
 #pragma unroll
                 for (int w = 0; w < 4; w++) {
@@ -2079,15 +2089,18 @@ extern "C" int fis_vm_plan_tma(fis_vm_op* ops, int n, int n_ctas, long long* ws_
                 const bool tc = a.impl != 1 && fis_gemm_tc_supported(&a);
                 if (tc) {
                     op.impl = 2;
-                    op.bn = a.n <= 64 ? 64 : 128;
+                    const int kb = (a.k + BK - 1) / BK;
+                    // 64-column tiles when that gives more tiles for a short K (no split-K to pay)
+                    const int t128 = ((a.n + 127) / 128) * ((a.m + BM - 1) / BM);
+                    op.bn = (a.n <= 64 || (kb < VM_MIN_SPLIT_KB && t128 * 2 <= G)) ? 64 : 128;
                     op.tiles_n = (a.n + op.bn - 1) / op.bn;
                     op.tiles_m = (a.m + BM - 1) / BM;
                     const int tiles = op.tiles_n * op.tiles_m;
-                    const int kb = (a.k + BK - 1) / BK;
                     // split-K: every split CTA of a tile must be co-resident (they meet at a tile
-                    // counter), so tiles * S <= G
+                    // counter), so tiles * S <= G.  A split costs a partial exchange (~4 us), so
+                    // only K ranges long enough to stream for longer than that are split.
                     int S = a.splits > 0 ? a.splits : G / (tiles > 0 ? tiles : 1);
-                    if (a.splits <= 0 && S > kb / 2) S = kb / 2;
+                    if (a.splits <= 0 && S > kb / (VM_MIN_SPLIT_KB / 2)) S = kb / (VM_MIN_SPLIT_KB / 2);
                     if (S > G / (tiles > 0 ? tiles : 1)) S = G / (tiles > 0 ? tiles : 1);
                     if (S > 32) S = 32;
                     if (S < 1) S = 1;

@@ -394,8 +394,9 @@ class Engine(Launcher):
         if self.act != torch.bfloat16 or d % 64:
             return False
         if self.capture is not None and m is not None and pre is None:
-            # the step VM runs attention as one fused op (S in TMEM, P via shared memory)
-            return L.lib().fis_vm_attn_slice(m, n_keys, d, d) > 0
+            # the step VM runs attention over one key block as one fused op (S in TMEM, P via shared
+            # memory); longer key ranges parallelise better as S GEMM -> softmax -> P.V (r01 timings)
+            return n_keys <= 128 and L.lib().fis_vm_attn_slice(m, n_keys, d, d) > 0
         return self.fused_attn
 
     def attn(self, m, n_keys, d, q: DRef, k: DRef, vt: DRef, scale, res: DRef, out: DRef, pre=None):

@@ -13,6 +13,8 @@ from __future__ import annotations
 import math
 from dataclasses import dataclass, field
 
+import functools
+
 import numpy as np
 
 from .errors import ConfigError, ContractViolation
@@ -162,8 +164,17 @@ def embed_ids(ids, config: UNetConfig) -> np.ndarray:
     for i in ids:
         if not 0 <= i < config.vocab_size:
             raise ConfigError(f"token id {i} outside vocabulary [0, {config.vocab_size})")
-    table = _rng(config.seed, SEED_TOKENS).standard_normal((config.vocab_size, config.text_dim)).astype(np.float32)
-    return table[list(ids)]
+    return _token_table(config.seed, config.vocab_size, config.text_dim)[list(ids)]
+
+
+@functools.lru_cache(maxsize=2)
+def _token_table(seed: int, vocab: int, dim: int) -> np.ndarray:
+    """The seeded (vocab, text_dim) embedding table.  The reference regenerates it on every call
+    (unet.py:151-158, 38 M normal samples at SD shape); it is a pure function of (seed, vocab, dim),
+    so it is generated once per process and kept read-only."""
+    table = _rng(seed, SEED_TOKENS).standard_normal((vocab, dim)).astype(np.float32)
+    table.flags.writeable = False
+    return table
 
 
 def initial_latent_np(config: UNetConfig) -> np.ndarray:
