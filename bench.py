@@ -227,6 +227,13 @@ def run_ours(args):
             eng.use_vm = use_vm
     # --- dense UNet step on the same GPU (what edit() runs for a full mask; SURVEY §8 C3 bar)
     dense_ms = dense_step_ms(eng, U, P, cfg, kv, args)
+    # --- C5-style: R concurrent independent requests on this GPU (one stream each)
+    batched = None
+    if args.requests > 1:
+        bv, bms = batched_requests(eng, U, P, cfg, args.requests, args)
+        batched = {"requests_per_gpu": args.requests, "edit_steps_per_s": bv, "ms_per_round": bms,
+                   "masks": "5/10/25% squares at distinct offsets, distinct prompts, own cached generations",
+                   "note": "each request's step graph replayed on its own CUDA stream (SURVEY §8 C5 per-GPU shard)"}
     sweep = mask_sweep(eng, U, P, cfg, arena, kv, lat0, args) if args.sweep else None
 
     # --- per-kernel timing of the gated (sparse) convs: eager instrumented step
@@ -279,6 +286,8 @@ def run_ours(args):
                                 "sample": "oracle port, 1 sparse step at t=1 after one dense caching step"}
     if sweep is not None:
         line["sweep"] = sweep
+    if batched is not None:
+        line["batched"] = batched
     if rank == 0:
         print(json.dumps(line))
     import torch.distributed as dist
@@ -311,6 +320,59 @@ def _time_runner(runner, T, steps, warmup):
     e1.record()
     torch.cuda.synchronize()
     return e0.elapsed_time(e1) / max(1, steps)
+
+
+def batched_requests(eng, U, P, cfg, R, args):
+    """C5-style throughput on one GPU: R independent edit requests (own cached generation, prompt,
+    mask, activations and step counter), each a captured step graph replayed on its own CUDA stream.
+    Returns (edit-steps/s over all requests, ms per round of R steps)."""
+    import torch
+    runners, streams = [], []
+    fracs = (0.05, 0.10, 0.25)
+    for r in range(R):
+        old = tuple((i * 7 + r) % 49000 + 1 for i in range(77))
+        new = tuple(99 + r if i == 3 else v for i, v in enumerate(old))
+        store = P.CacheStore()
+        eng.ns = 0
+        P.generate_dense(P.PromptTokens(old), cfg, store, record="engine")
+        side = int(round((fracs[r % 3] * 64 * 64) ** 0.5))
+        y0, x0 = (7 * r) % (64 - side), (13 * r) % (64 - side)
+        bits = np.zeros((64, 64), dtype=bool)
+        bits[y0:y0 + side, x0:x0 + side] = True
+        kv = eng.text_kv(P.embed_tokens(P.PromptTokens(new), cfg))
+        lat0 = U._to_nhwc(P.initial_latent(cfg), eng.dev)
+        ep = U.EditPlan(eng, store.arena, P.BinaryMask(bits), kv, lat0)
+        run = U._Runner(eng, ep.plan, True, ns=r + 1)
+        run._keep = (store, ep, kv)
+        run.step(1)  # warm + capture
+        runners.append(run)
+        streams.append(torch.cuda.Stream())
+    torch.cuda.synchronize()
+    T = cfg.steps
+    n = max(3, args.steps // 2)
+
+    def round_(t):
+        for run, st in zip(runners, streams):
+            with torch.cuda.stream(st):
+                run.step(t)
+
+    for i in range(3):
+        round_(1 + (i + 1) % T)
+    torch.cuda.synchronize()
+    main = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(main)
+    for st in streams:
+        st.wait_stream(main)
+    for i in range(n):
+        round_(1 + i % T)
+    for st in streams:
+        main.wait_stream(st)
+    e1.record(main)
+    torch.cuda.synchronize()
+    eng.ns = 0
+    ms = e0.elapsed_time(e1)
+    return R * n / (ms / 1e3), ms / n
 
 
 def dense_step_ms(eng, U, P, cfg, kv, args):
@@ -383,6 +445,8 @@ def main():
     ap.add_argument("--precision", default="bf16", choices=["fp32", "bf16"])
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--sweep", action="store_true", help="also time the C3 mask-ratio sweep")
+    ap.add_argument("--requests", type=int, default=8,
+                    help="also time R concurrent edit requests on each GPU (C5 shard; 1 disables)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

@@ -112,10 +112,11 @@ class Launcher:
         self.dev = torch.device(device or "cuda")
         self.act = torch.float32 if precision == "fp32" else torch.bfloat16
         self.gemm_impl = 1 if precision == "fp32" else 0
-        self.step_dev = torch.zeros(1, dtype=torch.int32, device=self.dev)
         self.sms = L.lib().fis_device_sm_count()
-        self._ws = torch.zeros(1, dtype=torch.float32, device=self.dev)
-        self._counters = torch.zeros(1 << 16, dtype=torch.int32, device=self.dev)
+        # namespace of the request being driven: requests that run concurrently (one CUDA stream
+        # each) own separate scratch activations, split-K workspaces and step counters
+        self.ns = 0
+        self._ns_state = {}
         self.launches = 0
         self._scratch = {}
         self.fused_xattn = False  # SIMT xattn is latency-bound; superseded by fis_attn
@@ -137,8 +138,30 @@ class Launcher:
             return
         L.call(name, args)
 
+    def _state(self):
+        st = self._ns_state.get(self.ns)
+        if st is None:
+            st = {"step": torch.zeros(1, dtype=torch.int32, device=self.dev),
+                  "ws": torch.zeros(1, dtype=torch.float32, device=self.dev),
+                  "counters": torch.zeros(1 << 16, dtype=torch.int32, device=self.dev)}
+            self._ns_state[self.ns] = st
+        return st
+
+    @property
+    def step_dev(self) -> torch.Tensor:
+        """Device step counter t of the current namespace (kernels read the step from it)."""
+        return self._state()["step"]
+
+    @property
+    def _ws(self) -> torch.Tensor:
+        return self._state()["ws"]
+
+    @property
+    def _counters(self) -> torch.Tensor:
+        return self._state()["counters"]
+
     def scratch(self, name, shape, dtype=None, zero=False):
-        key = (name, tuple(shape), dtype or self.act)
+        key = (self.ns, name, tuple(shape), dtype or self.act)
         t = self._scratch.get(key)
         if t is None:
             t = (torch.zeros if zero else torch.empty)(shape, dtype=dtype or self.act, device=self.dev)
@@ -149,7 +172,7 @@ class Launcher:
     def _ensure_ws(self, floats):
         floats = min(floats, 1 << 25)  # 128 MB cap; the split choice respects ws_floats
         if self._ws.numel() < floats:
-            self._ws = torch.empty(int(floats * 1.25) + 1024, dtype=torch.float32, device=self.dev)
+            self._state()["ws"] = torch.empty(int(floats * 1.25) + 1024, dtype=torch.float32, device=self.dev)
 
     def _splits(self, m, n, k):
         tiles = ((m + 63) // 64) * ((n + 63) // 64)

@@ -232,14 +232,17 @@ class _Runner:
     """Drives Engine steps for t in a range: eagerly, through one captured CUDA graph, or (bf16)
     as one persistent step-VM launch per step (csrc/fis_vm.cu)."""
 
-    def __init__(self, eng: Engine, plan, use_graph: bool):
-        self.eng, self.plan, self.use_graph = eng, plan, use_graph
+    def __init__(self, eng: Engine, plan, use_graph: bool, ns: int = 0):
+        self.eng, self.plan, self.use_graph, self.ns = eng, plan, use_graph, ns
         self.graph = None
         self.vm = None
         self.launches_per_step = None
 
     def step(self, t: int):
+        """One step on the current CUDA stream (each concurrently driven request owns a namespace
+        `ns` of scratch buffers and step counter, and its own stream)."""
         eng = self.eng
+        eng.ns = self.ns
         eng.step_dev.fill_(t)
         if not self.use_graph:
             eng.run_step(self.plan)
