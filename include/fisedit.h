@@ -115,9 +115,10 @@ int fis_gemm_counters(int m, int n);
  * Replaces group_norm's reduction (tensors.py:129-146). */
 typedef struct {
     int hw, c, groups;
-    fis_ref x;              /* [hw, ld] */
-    fis_ref mean, var;      /* [groups] f32 */
+    fis_ref x;              /* [n_img * hw, ld] */
+    fis_ref mean, var;      /* [n_img][groups] f32 */
     const int* step;
+    int n_img;              /* stacked images (batched requests), statistics per image; 0/1 = one */
 } fis_gn_stats_args;
 int fis_gn_stats(const fis_gn_stats_args* a, void* stream);
 
@@ -135,6 +136,8 @@ typedef struct {
     fis_ref y_silu;         /* optional */
     const int* y_rows;
     const int* step;
+    int img_rows;           /* > 0: row r uses the statistics of image r / img_rows (mean/var [img][groups]) */
+    const int* row_img;     /* optional per-row image index (overrides img_rows) */
 } fis_gn_apply_args;
 int fis_gn_apply(const fis_gn_apply_args* a, void* stream);
 
@@ -188,6 +191,12 @@ typedef struct {
     fis_ref pre;            /* optional store of the attention output before the residual */
     fis_ref out;            /* [m, ld] */
     const int* step;
+    /* ragged segments (batched requests): queries [q_seg[2s], q_seg[2s+1]) attend to keys
+     * [k_seg[2s], k_seg[2s+1]) only; nseg = 0: one segment of m queries x n_keys keys */
+    int nseg;
+    int max_seg_q;          /* largest q_seg[s+1] - q_seg[s] (sizes the grid) */
+    const int* q_seg;       /* [2 * nseg] device (begin, end) pairs */
+    const int* k_seg;       /* [2 * nseg] device (begin, end) pairs */
 } fis_attn_args;
 int fis_attn(const fis_attn_args* a, void* stream);
 

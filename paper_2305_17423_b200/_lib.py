@@ -48,13 +48,14 @@ class GemmArgs(C.Structure):
 
 class GnStatsArgs(C.Structure):
     _fields_ = [("hw", C.c_int), ("c", C.c_int), ("groups", C.c_int), ("x", Ref), ("mean", Ref), ("var", Ref),
-                ("step", C.c_void_p)]
+                ("step", C.c_void_p), ("n_img", C.c_int)]
 
 
 class GnApplyArgs(C.Structure):
     _fields_ = [("rows", C.c_int), ("c", C.c_int), ("groups", C.c_int), ("eps", C.c_float), ("x", Ref),
                 ("x_rows", C.c_void_p), ("mean", Ref), ("var", Ref), ("gamma", C.c_void_p), ("beta", C.c_void_p),
-                ("y_norm", Ref), ("y_silu", Ref), ("y_rows", C.c_void_p), ("step", C.c_void_p)]
+                ("y_norm", Ref), ("y_silu", Ref), ("y_rows", C.c_void_p), ("step", C.c_void_p),
+                ("img_rows", C.c_int), ("row_img", C.c_void_p)]
 
 
 class SoftmaxArgs(C.Structure):
@@ -70,7 +71,8 @@ class XattnArgs(C.Structure):
 
 class AttnArgs(C.Structure):
     _fields_ = [("m", C.c_int), ("n_keys", C.c_int), ("d", C.c_int), ("dv", C.c_int), ("q", Ref), ("k", Ref),
-                ("vt", Ref), ("scale", C.c_float), ("res", Ref), ("pre", Ref), ("out", Ref), ("step", C.c_void_p)]
+                ("vt", Ref), ("scale", C.c_float), ("res", Ref), ("pre", Ref), ("out", Ref), ("step", C.c_void_p),
+                ("nseg", C.c_int), ("max_seg_q", C.c_int), ("q_seg", C.c_void_p), ("k_seg", C.c_void_p)]
 
 
 class PoolArgs(C.Structure):

@@ -33,7 +33,8 @@ __device__ __forceinline__ float gather_a(const fis_gemm_args& a, int t, const c
     const fis_src& s = second ? a.src[1] : a.src[0];
     if (second) c -= a.src[0].c;
     const int sy = s.up ? (y >> 1) : y, sx = s.up ? (x >> 1) : x;
-    return src_value(s, second ? f1 : f0, second ? c1p : c0p, sy * s.w + sx, c);
+    const int img = p / (a.out_h * a.out_w);  // stacked images (batched requests)
+    return src_value(s, second ? f1 : f0, second ? c1p : c0p, img * s.h * s.w + sy * s.w + sx, c);
 }
 
 __global__ void __launch_bounds__(STHREADS) gemm_simt_kernel(const fis_gemm_args a) {
@@ -62,8 +63,9 @@ __global__ void __launch_bounds__(STHREADS) gemm_simt_kernel(const fis_gemm_args
         int p = r < a.m ? (a.rows ? __ldg(a.rows + r) : r) : 0;
         rowp[tid] = p;
         if (a.a_mode == FIS_A_CONV3X3) {
-            rowy[tid] = p / a.out_w;
-            rowx[tid] = p - (p / a.out_w) * a.out_w;
+            const int lp = p % (a.out_h * a.out_w);  // pixel within its stacked image
+            rowy[tid] = lp / a.out_w;
+            rowx[tid] = lp - (lp / a.out_w) * a.out_w;
         }
     }
     __syncthreads();

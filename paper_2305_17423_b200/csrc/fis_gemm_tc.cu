@@ -476,8 +476,18 @@ __global__ void __launch_bounds__(THREADS, 1) attn_tc_kernel(const fis_attn_args
     uint32_t* tmem_slot = (uint32_t*)(o_done + 1);
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int m0 = blockIdx.y * 128, c0 = blockIdx.x * dvs;
-    const int nkb = (a.n_keys + 127) / 128, dch = a.d / 64;
+    // ragged segments (batched requests): rows [q_beg, q_end) attend to keys [k_beg, k_beg + n_keys)
+    int q_beg = 0, q_end = a.m, k_beg = 0, n_keys = a.n_keys;
+    if (a.nseg > 0) {
+        const int sg = blockIdx.z;
+        q_beg = __ldg(a.q_seg + 2 * sg);
+        q_end = __ldg(a.q_seg + 2 * sg + 1);
+        k_beg = __ldg(a.k_seg + 2 * sg);
+        n_keys = __ldg(a.k_seg + 2 * sg + 1) - k_beg;
+    }
+    const int m0 = q_beg + blockIdx.y * 128, c0 = blockIdx.x * dvs;
+    if (m0 >= q_end || n_keys <= 0) return;  // uniform for the CTA, before any barrier
+    const int nkb = (n_keys + 127) / 128, dch = a.d / 64;
     const bool single = nkb == 1;
     if (tid == 0) {
         for (int i = 0; i < AT_STAGES; i++) {
@@ -520,23 +530,23 @@ __global__ void __launch_bounds__(THREADS, 1) attn_tc_kernel(const fis_attn_args
                     if (it >= AT_STAGES) mbar_wait(empty + st, ((it / AT_STAGES) & 1) ^ 1);
                     const uint32_t sa = sbase + st * AT_STAGE, sb = sa + AT_A;
                     if (kc < dch) {  // S item: Q chunk + K chunk
-                        const int qr = m0 + pr, key = j * 128 + pr;
+                        const int qr = m0 + pr, key = j * 128 + pr;  // key index within the segment
                         const char* qs = qb + ((long long)qr * a.q.ld + kc * 64) * 2;
-                        const char* ks = kb + ((long long)key * a.k.ld + kc * 64) * 2;
+                        const char* ks = kb + ((long long)(k_beg + key) * a.k.ld + kc * 64) * 2;
 #pragma unroll
                         for (int u = 0; u < 8; u++) {
-                            cp_async16(sa + sw128_off(pr, u), qr < a.m ? (const void*)(qs + 16 * u) : (const void*)dummy, qr < a.m);
-                            cp_async16(sb + sw128_off(pr, u), key < a.n_keys ? (const void*)(ks + 16 * u) : (const void*)dummy,
-                                       key < a.n_keys);
+                            cp_async16(sa + sw128_off(pr, u), qr < q_end ? (const void*)(qs + 16 * u) : (const void*)dummy, qr < q_end);
+                            cp_async16(sb + sw128_off(pr, u), key < n_keys ? (const void*)(ks + 16 * u) : (const void*)dummy,
+                                       key < n_keys);
                         }
                     } else {  // PV item: V^T chunk (rows = value channels, K = keys)
                         const int k0 = j * 128 + (kc - dch) * 64;
                         for (int row = pr; row < dvs; row += 128) {
                             const int ch = c0 + row;
-                            const char* vs = vb + ((long long)ch * a.vt.ld + k0) * 2;
+                            const char* vs = vb + ((long long)ch * a.vt.ld + k_beg + k0) * 2;
 #pragma unroll
                             for (int u = 0; u < 8; u++) {
-                                const bool ok = ch < a.dv && k0 + 8 * u < a.n_keys;
+                                const bool ok = ch < a.dv && k0 + 8 * u < n_keys;
                                 cp_async16(sb + sw128_off(row, u), ok ? (const void*)(vs + 16 * u) : (const void*)dummy, ok);
                             }
                         }
@@ -615,12 +625,12 @@ __global__ void __launch_bounds__(THREADS, 1) attn_tc_kernel(const fis_attn_args
                         float cm = -INFINITY;
 #pragma unroll
                         for (int q = 0; q < 32; q++)
-                            if (kbase + cb + q < a.n_keys) cm = fmaxf(cm, v[q] * a.scale);
+                            if (kbase + cb + q < n_keys) cm = fmaxf(cm, v[q] * a.scale);
                         const float mn = fmaxf(mrow, cm);
                         float add = 0.f;
 #pragma unroll
                         for (int q = 0; q < 32; q++)
-                            if (kbase + cb + q < a.n_keys) add += expf(v[q] * a.scale - mn);
+                            if (kbase + cb + q < n_keys) add += expf(v[q] * a.scale - mn);
                         lrow = (mrow == -INFINITY ? 0.f : lrow * expf(mrow - mn)) + add;
                         mrow = mn;
                     }
@@ -639,8 +649,8 @@ __global__ void __launch_bounds__(THREADS, 1) attn_tc_kernel(const fis_attn_args
 #pragma unroll
                             for (int e2 = 0; e2 < 4; e2++) {
                                 const int q0 = 8 * u + 2 * e2;
-                                const float p0 = kbase + cb + q0 < a.n_keys ? expf(v[q0] * a.scale - mrow) * inv : 0.f;
-                                const float p1 = kbase + cb + q0 + 1 < a.n_keys ? expf(v[q0 + 1] * a.scale - mrow) * inv : 0.f;
+                                const float p0 = kbase + cb + q0 < n_keys ? expf(v[q0] * a.scale - mrow) * inv : 0.f;
+                                const float p1 = kbase + cb + q0 + 1 < n_keys ? expf(v[q0 + 1] * a.scale - mrow) * inv : 0.f;
                                 h[e2] = __floats2bfloat162_rn(p0, p1);
                             }
                             const int unit = ((cb & 63) >> 3) + u;
@@ -660,7 +670,7 @@ __global__ void __launch_bounds__(THREADS, 1) attn_tc_kernel(const fis_attn_args
         mbar_wait(o_done, 0);
         tc_fence_after();
         {  // tcgen05.ld is warp-collective: every lane loads, only rows < m store
-            const bool live = r < a.m;
+            const bool live = r < q_end;
             char* ob = ref_base(a.out, t);
             char* pbp = a.pre.ptr ? ref_base(a.pre, t) : nullptr;
             const char* rb = a.res.ptr ? ref_base(a.res, t) : nullptr;
@@ -764,7 +774,8 @@ extern "C" int fis_attn(const fis_attn_args* a, void* stream) {
         configured = true;
     }
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(a->dv / dvs, (a->m + 127) / 128, 1);
+    cfg.gridDim = a->nseg > 0 ? dim3(a->dv / dvs, (a->max_seg_q + 127) / 128, a->nseg)
+                              : dim3(a->dv / dvs, (a->m + 127) / 128, 1);
     cfg.blockDim = dim3(fis::tc::THREADS);
     cfg.dynamicSmemBytes = fis::tc::AT_SMEM;
     cfg.stream = (cudaStream_t)stream;

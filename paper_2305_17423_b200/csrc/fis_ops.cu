@@ -11,10 +11,10 @@ __global__ void __launch_bounds__(256) gn_stats_kernel(const fis_gn_stats_args a
     pdl_trigger();
     pdl_wait();
     const int t = cur_step(a.step);
-    const int g = blockIdx.x;
+    const int g = blockIdx.x, img = blockIdx.y;  // one CTA per (group, stacked image)
     const int cpg = a.c / a.groups;
     const long long cnt = (long long)a.hw * cpg;
-    const char* x = ref_base(a.x, t);
+    const char* x = ref_base(a.x, t) + (long long)img * a.hw * a.x.ld * (a.x.dtype == FIS_BF16 ? 2 : 4);
     __shared__ double red[256];
     double s = 0.0;
     // thread = pixel (strided), inner loop over the group's contiguous channels (32-bit index math)
@@ -45,8 +45,8 @@ __global__ void __launch_bounds__(256) gn_stats_kernel(const fis_gn_stats_args a
         __syncthreads();
     }
     if (threadIdx.x == 0) {
-        ((float*)ref_base(a.mean, t))[g] = (float)mean;
-        ((float*)ref_base(a.var, t))[g] = (float)(red[0] / (double)cnt);
+        ((float*)ref_base(a.mean, t))[img * a.groups + g] = (float)mean;
+        ((float*)ref_base(a.var, t))[img * a.groups + g] = (float)(red[0] / (double)cnt);
     }
 }
 
@@ -67,7 +67,7 @@ __global__ void gn_apply_kernel(const fis_gn_apply_args a) {
         const int r = e / a.c, c = e - (e / a.c) * a.c;
         const int xr = a.x_rows ? __ldg(a.x_rows + r) : r;
         const int yr = a.y_rows ? __ldg(a.y_rows + r) : r;
-        const int g = c / cpg;
+        const int g = (a.row_img ? __ldg(a.row_img + r) : (a.img_rows > 0 ? r / a.img_rows : 0)) * a.groups + c / cpg;
         float y;
         if (bf16_out) {
             // bf16 mode: fp32 normalisation (the fp32-parity mode keeps the reference's f64)
@@ -185,7 +185,7 @@ __global__ void pool2_kernel(const fis_pool_args a) {
     const char* fr = a.src.fresh.ptr ? ref_base(a.src.fresh, t) : nullptr;
     const char* ca = a.src.cache.ptr ? ref_base(a.src.cache, t) : nullptr;
     char* out = ref_base(a.out, t);
-    const int cw = a.src.w / 2;
+    const int cw = a.src.w / 2, chw = (a.src.h / 2) * cw;
     const int total = a.n * a.c;
     const bool vec = a.src.fresh.dtype == FIS_BF16 && (!a.src.index || a.src.cache.dtype == FIS_BF16) &&
                      a.out.dtype == FIS_BF16 && (a.c % 8) == 0 && (a.src.fresh.ld % 8) == 0 &&
@@ -195,8 +195,9 @@ __global__ void pool2_kernel(const fis_pool_args a) {
         for (int e = (blockIdx.x * blockDim.x + threadIdx.x) * 8; e < total; e += gridDim.x * blockDim.x * 8) {
             const int i = e / a.c, c = e - (e / a.c) * a.c;
             const int P = a.rows ? __ldg(a.rows + i) : i;
-            const int py = P / cw, px = P - (P / cw) * cw;
-            const int q = (2 * py) * a.src.w + 2 * px;
+            const int img = P / chw, lP = P - img * chw;  // stacked images (batched requests)
+            const int py = lP / cw, px = lP - (lP / cw) * cw;
+            const int q = img * a.src.h * a.src.w + (2 * py) * a.src.w + 2 * px;
             const int qs[4] = {q, q + 1, q + a.src.w, q + a.src.w + 1};
             uint4 u[4];
 #pragma unroll
@@ -219,8 +220,9 @@ __global__ void pool2_kernel(const fis_pool_args a) {
     for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
         const int i = e / a.c, c = e - (e / a.c) * a.c;
         const int P = a.rows ? __ldg(a.rows + i) : i;
-        const int py = P / cw, px = P - (P / cw) * cw;
-        const int q = (2 * py) * a.src.w + 2 * px;
+        const int img = P / chw, lP = P - img * chw;
+        const int py = lP / cw, px = lP - (lP / cw) * cw;
+        const int q = img * a.src.h * a.src.w + (2 * py) * a.src.w + 2 * px;
         const float v00 = src_value(a.src, fr, ca, q, c), v01 = src_value(a.src, fr, ca, q + 1, c);
         const float v10 = src_value(a.src, fr, ca, q + a.src.w, c), v11 = src_value(a.src, fr, ca, q + a.src.w + 1, c);
         const float s = __fadd_rn(__fadd_rn(v00, v01), __fadd_rn(v10, v11));
@@ -256,7 +258,7 @@ static int fis_check(void) { return cudaGetLastError() == cudaSuccess ? FIS_OK :
 
 extern "C" int fis_gn_stats(const fis_gn_stats_args* a, void* stream) {
     if (a->groups <= 0 || a->c % a->groups) return FIS_ERR_SHAPE;
-    return fis_launch(fis::gn_stats_kernel, dim3(a->groups), dim3(256), 0, (cudaStream_t)stream, *a) == cudaSuccess ? FIS_OK : FIS_ERR_LAUNCH;
+    return fis_launch(fis::gn_stats_kernel, dim3(a->groups, a->n_img > 1 ? a->n_img : 1), dim3(256), 0, (cudaStream_t)stream, *a) == cudaSuccess ? FIS_OK : FIS_ERR_LAUNCH;
 }
 
 extern "C" int fis_gn_apply(const fis_gn_apply_args* a, void* stream) {

@@ -192,13 +192,18 @@ constexpr int SEL_ZERO = INT_MIN;
 // >= 0 fresh row (or full-map pixel), <= -2 cache pixel (-2 - q), SEL_ZERO = zero padding.
 __device__ __forceinline__ void build_sel(const fis_gemm_args& a, int p, int seg, int* out9) {
     const fis_src& s = a.src[seg];
-    const int oy = p / a.out_w, ox = p - (p / a.out_w) * a.out_w;
+    // pixels of several stacked images (batched requests): image = p / (out_h * out_w); taps never
+    // cross an image border; the source pixel is offset by the image's h * w source pixels
+    const int ipx = a.out_h * a.out_w;
+    const int img = p / ipx, lp = p - img * ipx;
+    const int oy = lp / a.out_w, ox = lp - (lp / a.out_w) * a.out_w;
+    const int qimg = img * s.h * s.w;
 #pragma unroll
     for (int tap = 0; tap < 9; tap++) {
         const int y = oy + tap / 3 - 1, x = ox + tap % 3 - 1;
         int v = SEL_ZERO;
         if (y >= 0 && x >= 0 && y < a.out_h && x < a.out_w) {
-            const int q = (s.up ? (y >> 1) : y) * s.w + (s.up ? (x >> 1) : x);
+            const int q = qimg + (s.up ? (y >> 1) : y) * s.w + (s.up ? (x >> 1) : x);
             if (s.index) {
                 const int i = __ldg(s.index + q);
                 v = i >= 0 ? i : -2 - q;
@@ -208,33 +213,6 @@ __device__ __forceinline__ void build_sel(const fis_gemm_args& a, int p, int seg
         }
         out9[tap] = v;
     }
-}
-
-// Source pointer of the 64-channel K block starting at k0 for one GEMM row (16 B granularity),
-// or nullptr for zero (padding / out of image / beyond K). tap/c/segment are uniform per block.
-__device__ __forceinline__ const char* a_block_ptr(const fis_gemm_args& a, const char* abase, const char* f0,
-                                                   const char* c0p, const char* f1, const char* c1p,
-                                                   const RowGeo& g, int k0, int tap, int c) {
-    if (!g.valid) return nullptr;
-    if (a.a_mode == FIS_A_ROWS) {
-        if (k0 >= a.k) return nullptr;
-        return abase + ((long long)g.p * a.a.ld + k0) * 2;
-    }
-    const int y = g.oy + tap / 3 - 1, x = g.ox + tap % 3 - 1;
-    if (y < 0 || x < 0 || y >= a.out_h || x >= a.out_w) return nullptr;
-    const bool second = c >= a.src[0].c;
-    const fis_src& s = second ? a.src[1] : a.src[0];
-    if (second) c -= a.src[0].c;
-    const int sy = s.up ? (y >> 1) : y, sx = s.up ? (x >> 1) : x;
-    const int q = sy * s.w + sx;
-    const char* fr = second ? f1 : f0;
-    const char* ca = second ? c1p : c0p;
-    if (s.index) {
-        const int i = __ldg(s.index + q);
-        if (i >= 0) return fr + ((long long)i * s.fresh.ld + c) * 2;
-        return ca + ((long long)q * s.cache.ld + c) * 2;
-    }
-    return fr + ((long long)q * s.fresh.ld + c) * 2;
 }
 
 }  // namespace tc
