@@ -12,8 +12,8 @@ from .masks import (BinaryMask, DiffMap, MaskPyramid, OtsuResult, accumulate_dif
 from .model import UNetConfig
 from .sparse import GatherPlan, SparseLayerContext, select_gather_plan
 from .tensors import ConvWeights, LayerMacs, MacsReport, load_tensor, macs_attention, macs_conv, save_tensor
-from .unet import (EditResult, EditSession, PromptTokens, SharedTokenMap, UNet, detect_mask, edit, embed_tokens,
-                   generate_dense, get_precision, initial_latent, set_precision)
+from .unet import (EditResult, EditSession, PromptTokens, SharedTokenMap, UNet, detect_mask, edit, edit_batch,
+                   embed_tokens, generate_dense, generate_dense_batch, get_precision, initial_latent, set_precision)
 
 __version__ = "0.1.0"
 

@@ -5,6 +5,8 @@ int fis_gemm_simt_launch(const fis_gemm_args* a, cudaStream_t stream);
 int fis_gemm_tc_launch(const fis_gemm_args* a, cudaStream_t stream);
 int fis_gemm_tc_supported(const fis_gemm_args* a);
 int fis_gemm_tc_choose_splits(int m, int n, int k);
+int fis_gemm_big_eligible(const fis_gemm_args* a);
+int fis_gemm_big_launch(const fis_gemm_args* a, cudaStream_t stream);
 
 extern "C" {
 
@@ -75,6 +77,11 @@ int fis_gemm(const fis_gemm_args* a, void* stream) {
     if (a->epi == FIS_EPI_GN_SILU && (a->groups <= 0 || a->n % a->groups || !a->gn_mean.ptr || !a->gn_var.ptr))
         return a->gn_mean.ptr ? FIS_ERR_SHAPE : FIS_ERR_CACHE_MISS;
     const bool tc = a->impl == 2 || (a->impl == 0 && fis_gemm_tc_supported(a));
+    // large M (stacked requests): persistent tcgen05 kernel with TMA weights (fis_gemm_big.cu)
+    if (tc && a->impl == 0 && fis_gemm_big_eligible(a)) {
+        const int rc = fis_gemm_big_launch(a, (cudaStream_t)stream);
+        if (rc != FIS_ERR_UNSUPPORTED) return rc;
+    }
     fis_gemm_args g = *a;
     if (g.splits <= 0) g.splits = fis_choose_splits(&g, tc);
     if (!tc && g.splits > 1 && (!g.ws || !g.counters)) return FIS_ERR_SHAPE;

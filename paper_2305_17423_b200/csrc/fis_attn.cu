@@ -1,0 +1,377 @@
+// Fused attention on tcgen05 with TMA operand staging (sm_100a).
+//
+//   out[r, c0:c0+dvs] = res + softmax(Q K^T * scale) (V^T)^T      (unet.py:279-293, sparse.py:265-361)
+//
+// One CTA = one 128-query tile x one value slice (dvs <= 256 columns) of one segment. Ragged
+// segments (batched requests) restrict each query run to its own key run.
+//
+//   warp 4 (lane 0) : TMA producer. Per 64-wide chunk: Q {64 x 128} + K {64 x 128} for a score
+//                     block, or V^T {64 keys x dvs} for a P.V block; one expect_tx per stage.
+//                     Rows past the end of a matrix are zero-filled by TMA; rows of a neighbouring
+//                     segment are masked in the softmax (P = 0).
+//   warp 5          : TMEM allocator + MMA issuer: S_j = Q K_j^T into one of two 128-column TMEM
+//                     buffers, O += P_j V_j into 256 columns; pass 2 issues S_{j+1} before P_j.V_j so
+//                     the tensor core works while the softmax warps read S_j.
+//   warps 0-3       : softmax (thread = query row): pass 1 keeps the running max / sum over all
+//                     key blocks, pass 2 writes P_j = exp(s - m) / l as bf16 into one of two SW128
+//                     P tiles; then the epilogue (O + residual -> out).
+// A segment of <= 128 keys takes one pass (statistics and P from the same S).
+#include "fis_tc.cuh"
+#include "fis_tma.cuh"
+
+namespace fis {
+namespace attn {
+
+using namespace fis::tc;
+
+constexpr int THREADS = 192, TMA_WARP = 4, MMA_WARP = 5;
+constexpr int STAGES = 3;
+constexpr int A_BYTES = 128 * 64 * 2;            // Q chunk
+constexpr int B_BYTES = 256 * 64 * 2;            // K chunk (128 keys) or V^T chunk (<= 256 rows)
+constexpr int STAGE = A_BYTES + B_BYTES;
+constexpr int P_BYTES = 2 * 128 * 64 * 2;        // P tile: 128 rows x 128 keys, two 64-key SW128 chunks
+constexpr int SMEM = STAGES * STAGE + 2 * P_BYTES + 1024 + 256;
+constexpr uint32_t O_COL = 256;                  // TMEM: S buffers at 0 / 128, O at 256
+
+FIS_DEV void tma2d(uint32_t dst, const void* tmap, int c0, int c1, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+            dst),
+        "l"(tmap), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+        : "memory");
+}
+FIS_DEV void arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+FIS_DEV void mma_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+                 : "memory");
+}
+FIS_DEV uint32_t idesc_bf16(int M, int N) {
+    return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+FIS_DEV void mma_bf16(uint32_t tmem_d, uint64_t ad, uint64_t bd, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+        "l"(ad), "l"(bd), "r"(idesc), "r"(acc));
+}
+FIS_DEV void tmem_ld32(uint32_t taddr, float* v) {
+    uint32_t u[32];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(u[0]), "=r"(u[1]), "=r"(u[2]), "=r"(u[3]), "=r"(u[4]), "=r"(u[5]), "=r"(u[6]), "=r"(u[7]),
+          "=r"(u[8]), "=r"(u[9]), "=r"(u[10]), "=r"(u[11]), "=r"(u[12]), "=r"(u[13]), "=r"(u[14]), "=r"(u[15]),
+          "=r"(u[16]), "=r"(u[17]), "=r"(u[18]), "=r"(u[19]), "=r"(u[20]), "=r"(u[21]), "=r"(u[22]), "=r"(u[23]),
+          "=r"(u[24]), "=r"(u[25]), "=r"(u[26]), "=r"(u[27]), "=r"(u[28]), "=r"(u[29]), "=r"(u[30]), "=r"(u[31])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int j = 0; j < 32; j++) v[j] = __uint_as_float(u[j]);
+}
+
+// The MMA order (and so the producer's load order) of one pass: S blocks 0..nkb-1; in pass 2
+// step u issues S_u (u < nkb) and then P_{u-1}.V_{u-1} (u >= 1).
+__global__ void __launch_bounds__(THREADS, 1)
+    attn_kernel(const fis_attn_args a, const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
+                const __grid_constant__ CUtensorMap tv, int dvs) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+    unsigned char* ptile = smem + STAGES * STAGE;
+    uint64_t* full = (uint64_t*)(ptile + 2 * P_BYTES);
+    uint64_t* empty = full + STAGES;
+    uint64_t* s_ready = empty + STAGES;  // [2]
+    uint64_t* s_free = s_ready + 2;      // [2]
+    uint64_t* p_ready = s_free + 2;      // [2]
+    uint64_t* p_free = p_ready + 2;      // [2]
+    uint64_t* o_done = p_free + 2;
+    uint32_t* tmem_slot = (uint32_t*)(o_done + 1);
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    int q_beg = 0, q_end = a.m, k_beg = 0, n_keys = a.n_keys;
+    if (a.nseg > 0) {
+        const int sg = blockIdx.z;
+        q_beg = __ldg(a.q_seg + 2 * sg);
+        q_end = __ldg(a.q_seg + 2 * sg + 1);
+        k_beg = __ldg(a.k_seg + 2 * sg);
+        n_keys = __ldg(a.k_seg + 2 * sg + 1) - k_beg;
+    }
+    const int m0 = q_beg + blockIdx.y * 128, c0 = blockIdx.x * dvs;
+    if (m0 >= q_end || n_keys <= 0) return;  // uniform for the CTA, before any barrier
+    const int nkb = (n_keys + 127) / 128, dch = a.d / 64;
+    const bool single = nkb == 1;
+    const int first_pass = single ? 2 : 1;
+    if (tid == 0) {
+        for (int i = 0; i < STAGES; i++) {
+            mbar_init(full + i, 1);
+            mbar_init(empty + i, 1);
+        }
+        for (int b = 0; b < 2; b++) {
+            mbar_init(s_ready + b, 1);
+            mbar_init(s_free + b, 128);
+            mbar_init(p_ready + b, 128);
+            mbar_init(p_free + b, 1);
+        }
+        mbar_init(o_done, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == TMA_WARP && lane == 0) {
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&tq) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&tk) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&tv) : "memory");
+    }
+    if (warp == MMA_WARP) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    pdl_trigger();
+    pdl_wait();
+    const int t = cur_step(a.step);
+
+    if (warp == TMA_WARP) {
+        // ------------------------------------------------------------ TMA producer
+        if (lane == 0) {
+            const uint32_t sbase = smem_u32(smem);
+            int it = 0;
+            auto stage = [&](uint32_t bytes) {
+                const int st = it % STAGES;
+                if (it >= STAGES) mbar_wait(empty + st, ((it / STAGES) & 1) ^ 1);
+                arrive_expect_tx(full + st, bytes);
+                it++;
+                return st;
+            };
+            auto load_s = [&](int j) {
+                for (int kc = 0; kc < dch; kc++) {
+                    const int st = stage(2 * A_BYTES);
+                    const uint32_t sa = sbase + st * STAGE;
+                    tma2d(sa, &tq, kc * 64, m0, full + st);
+                    tma2d(sa + A_BYTES, &tk, kc * 64, k_beg + j * 128, full + st);
+                }
+            };
+            auto load_v = [&](int j) {
+                for (int h = 0; h < 2; h++) {
+                    const int st = stage((uint32_t)(dvs * 64 * 2));
+                    tma2d(sbase + st * STAGE + A_BYTES, &tv, k_beg + j * 128 + h * 64, c0, full + st);
+                }
+            };
+            if (!single)
+                for (int j = 0; j < nkb; j++) load_s(j);
+            for (int u = 0; u <= nkb; u++) {
+                if (u < nkb) load_s(u);
+                if (u >= 1) load_v(u - 1);
+            }
+        }
+    } else if (warp == MMA_WARP) {
+        // ------------------------------------------------------------ MMA issuer
+        const uint32_t sbase = smem_u32(smem), pbase = smem_u32(ptile);
+        const uint32_t id_s = idesc_bf16(128, 128), id_o = idesc_bf16(128, dvs);
+        int it = 0, sb = 0;
+        auto mma_s = [&]() {
+            const int b = sb & 1;
+            if (sb >= 2) mbar_wait(s_free + b, ((sb >> 1) & 1) ^ 1);  // softmax has read S_{sb-2}
+            for (int kc = 0; kc < dch; kc++) {
+                const int st = it % STAGES;
+                mbar_wait(full + st, (it / STAGES) & 1);
+                tc_fence_after();
+                if (lane == 0) {
+                    const uint32_t sa = sbase + st * STAGE, sbb = sa + A_BYTES;
+#pragma unroll
+                    for (int kk = 0; kk < 4; kk++)
+                        mma_bf16(tmem + b * 128, sw128_desc(sa + kk * 32), sw128_desc(sbb + kk * 32), id_s,
+                                 (kc | kk) ? 1u : 0u);
+                    mma_commit(empty + st);
+                    if (kc == dch - 1) mma_commit(s_ready + b);
+                }
+                __syncwarp();
+                it++;
+            }
+            sb++;
+        };
+        auto mma_pv = [&](int j) {
+            const int pb = j & 1;
+            mbar_wait(p_ready + pb, (j >> 1) & 1);  // P_j written
+            for (int h = 0; h < 2; h++) {
+                const int st = it % STAGES;
+                mbar_wait(full + st, (it / STAGES) & 1);
+                tc_fence_after();
+                if (lane == 0) {
+                    const uint32_t sbb = sbase + st * STAGE + A_BYTES;
+                    const uint32_t pa = pbase + pb * P_BYTES + h * (128 * 128);
+#pragma unroll
+                    for (int kk = 0; kk < 4; kk++)
+                        mma_bf16(tmem + O_COL, sw128_desc(pa + kk * 32), sw128_desc(sbb + kk * 32), id_o,
+                                 (j | h | kk) ? 1u : 0u);
+                    mma_commit(empty + st);
+                    if (h == 1) {
+                        mma_commit(p_free + pb);
+                        if (j == nkb - 1) mma_commit(o_done);
+                    }
+                }
+                __syncwarp();
+                it++;
+            }
+        };
+        if (!single)
+            for (int j = 0; j < nkb; j++) mma_s();
+        for (int u = 0; u <= nkb; u++) {
+            if (u < nkb) mma_s();
+            if (u >= 1) mma_pv(u - 1);
+        }
+    } else {
+        // ------------------------------------------------------------ softmax + epilogue (warps 0-3)
+        const int lr = tid, r = m0 + lr;
+        const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
+        float mrow = -INFINITY, lrow = 0.f;
+        int sb = 0;
+        float v[32];
+        for (int pass = first_pass; pass <= 2; pass++) {
+            for (int j = 0; j < nkb; j++) {
+                const int b = sb & 1;
+                mbar_wait(s_ready + b, (sb >> 1) & 1);
+                tc_fence_after();
+                const uint32_t trow = tmem + lane_off + b * 128;
+                const int kbase = j * 128;
+                if (pass == 1 || single) {  // row statistics (online over this block)
+#pragma unroll 1
+                    for (int cb = 0; cb < 128; cb += 32) {
+                        tmem_ld32(trow + cb, v);
+                        float cm = -INFINITY;
+#pragma unroll
+                        for (int q = 0; q < 32; q++)
+                            if (kbase + cb + q < n_keys) cm = fmaxf(cm, v[q] * a.scale);
+                        const float mn = fmaxf(mrow, cm);
+                        float add = 0.f;
+#pragma unroll
+                        for (int q = 0; q < 32; q++)
+                            if (kbase + cb + q < n_keys) add += expf(v[q] * a.scale - mn);
+                        lrow = (mrow == -INFINITY ? 0.f : lrow * expf(mrow - mn)) + add;
+                        mrow = mn;
+                    }
+                }
+                if (pass == 2) {  // P_j = exp(s*scale - m) / l -> bf16 P tile j & 1 (SW128, K-major)
+                    const int pb = j & 1;
+                    if (j >= 2) mbar_wait(p_free + pb, ((j >> 1) & 1) ^ 1);  // P.V_{j-2} done
+                    const float inv = 1.0f / lrow;
+                    unsigned char* pt0 = ptile + pb * P_BYTES;
+#pragma unroll 1
+                    for (int cb = 0; cb < 128; cb += 32) {
+                        tmem_ld32(trow + cb, v);
+                        unsigned char* pt = pt0 + (cb >> 6) * (128 * 128);
+#pragma unroll
+                        for (int u = 0; u < 4; u++) {
+                            uint4 pk;
+                            __nv_bfloat162* h = (__nv_bfloat162*)&pk;
+#pragma unroll
+                            for (int e2 = 0; e2 < 4; e2++) {
+                                const int q0 = 8 * u + 2 * e2;
+                                const float p0 = kbase + cb + q0 < n_keys ? expf(v[q0] * a.scale - mrow) * inv : 0.f;
+                                const float p1 =
+                                    kbase + cb + q0 + 1 < n_keys ? expf(v[q0 + 1] * a.scale - mrow) * inv : 0.f;
+                                h[e2] = __floats2bfloat162_rn(p0, p1);
+                            }
+                            const int unit = ((cb & 63) >> 3) + u;
+                            *(uint4*)(pt + sw128_off(lr, unit)) = pk;
+                        }
+                    }
+                    tc_fence_before();
+                    mbar_arrive(s_free + b);  // S_j fully read
+                    fence_async_smem();       // generic-proxy P writes -> tensor-core reads
+                    mbar_arrive(p_ready + pb);
+                } else {
+                    tc_fence_before();
+                    mbar_arrive(s_free + b);
+                }
+                sb++;
+            }
+        }
+        // epilogue: O row slice + residual -> out
+        mbar_wait(o_done, 0);
+        tc_fence_after();
+        {  // tcgen05.ld is warp-collective: every lane loads, rows of this segment store
+            const bool live = r < q_end;
+            char* ob = ref_base(a.out, t);
+            char* pbp = a.pre.ptr ? ref_base(a.pre, t) : nullptr;
+            const char* rb = a.res.ptr ? ref_base(a.res, t) : nullptr;
+#pragma unroll 1
+            for (int cb = 0; cb < dvs; cb += 32) {
+                tmem_ld32(tmem + lane_off + O_COL + cb, v);
+                const int n = c0 + cb;
+                const int nvalid = min(32, a.dv - n);
+                if (nvalid <= 0) break;
+                if (!live) continue;
+                if (pbp) {
+                    store_row16(pbp, a.pre.dtype, (long long)r * a.pre.ld + n, min(16, nvalid), v);
+                    if (nvalid > 16) store_row16(pbp, a.pre.dtype, (long long)r * a.pre.ld + n + 16, nvalid - 16, v + 16);
+                }
+                if (rb) {
+                    float q[16];
+                    load_row16(rb, a.res.dtype, (long long)r * a.res.ld + n, min(16, nvalid), q);
+#pragma unroll
+                    for (int e2 = 0; e2 < 16; e2++) v[e2] = __fadd_rn(v[e2], q[e2]);
+                    if (nvalid > 16) {
+                        load_row16(rb, a.res.dtype, (long long)r * a.res.ld + n + 16, nvalid - 16, q);
+#pragma unroll
+                        for (int e2 = 0; e2 < 16; e2++) v[16 + e2] = __fadd_rn(v[16 + e2], q[e2]);
+                    }
+                }
+                store_row16(ob, a.out.dtype, (long long)r * a.out.ld + n, min(16, nvalid), v);
+                if (nvalid > 16) store_row16(ob, a.out.dtype, (long long)r * a.out.ld + n + 16, nvalid - 16, v + 16);
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == MMA_WARP) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+}
+
+}  // namespace attn
+}  // namespace fis
+
+// value-slice width: largest multiple of 32 dividing dv with <= 256 columns
+static int attn_slice(int dv) {
+    for (int w = 256; w >= 32; w -= 32)
+        if (dv % w == 0) return w;
+    return 0;
+}
+
+// Q [m][d], K [n_keys][d] (with segments: n_keys = rows of K), V^T [dv][>= n_keys]; bf16, rows
+// 16-byte aligned, no per-step stride (scratch activations / per-edit text K/V).
+extern "C" int fis_attn(const fis_attn_args* a, void* stream) {
+    if (a->m == 0) return FIS_OK;
+    if (a->d % 64 || a->n_keys < 1 || a->q.dtype != FIS_BF16 || a->k.dtype != FIS_BF16 || a->vt.dtype != FIS_BF16 ||
+        (a->q.ld % 8) || (a->k.ld % 8) || (a->vt.ld % 8) || a->q.step_stride || a->k.step_stride ||
+        a->vt.step_stride)
+        return FIS_ERR_UNSUPPORTED;
+    const int dvs = attn_slice(a->dv);
+    if (!dvs) return FIS_ERR_UNSUPPORTED;
+    CUtensorMap tq, tk, tv;
+    if (!encode_2d(&tq, a->q.ptr, a->m, a->d, a->q.ld, 128) ||
+        !encode_2d(&tk, a->k.ptr, a->n_keys, a->d, a->k.ld, 128) ||
+        !encode_2d(&tv, a->vt.ptr, a->dv, a->n_keys, a->vt.ld, dvs))
+        return FIS_ERR_UNSUPPORTED;
+    static bool configured = false;
+    if (!configured) {
+        if (cudaFuncSetAttribute(fis::attn::attn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 fis::attn::SMEM) != cudaSuccess)
+            return FIS_ERR_UNSUPPORTED;
+        configured = true;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = a->nseg > 0 ? dim3(a->dv / dvs, (a->max_seg_q + 127) / 128, a->nseg)
+                              : dim3(a->dv / dvs, (a->m + 127) / 128, 1);
+    cfg.blockDim = dim3(fis::attn::THREADS);
+    cfg.dynamicSmemBytes = fis::attn::SMEM;
+    cfg.stream = (cudaStream_t)stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = fis_pdl_enabled() ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, fis::attn::attn_kernel, *a, tq, tk, tv, dvs) == cudaSuccess ? FIS_OK
+                                                                                                : FIS_ERR_LAUNCH;
+}

@@ -1,0 +1,446 @@
+// Persistent warp-specialised tcgen05 gather-GEMM for large M (stacked / batched requests).
+//
+//   D[r, n] = epi( sum_k A[r,k] * B[n,k] ),  bf16 operands, fp32 accumulation in TMEM.
+//
+// The per-op kernel (fis_gemm_tc.cu) runs one 128 x 128 tile per CTA with split-K clusters:
+// right for the batch-1 step (M = 100-400 rows, weight-streaming bound), but at M in the
+// thousands (R requests stepped as one batch) it pays a fresh prologue per tile, 1 CTA per SM
+// in waves, and 64 flop per L2 byte. This kernel keeps one CTA per SM for the whole GEMM:
+//
+//   warps 0-3 : A producers. Thread = tile row: per tile it builds the row's select-on-read
+//               decisions (3x3 conv taps over the fresh compact rows / the cached slab, image
+//               aware), then per 64-wide K block gathers its 128-byte row with cp.async into
+//               the SW128 K-major stage (arrival counted on the stage's full barrier).
+//   warp 4    : B producer: one thread issues a TMA tile load {64 x BN} of the weights per
+//               stage (128-byte swizzle, zero fill past N / K), expect_tx on the full barrier.
+//   warp 5    : TMEM allocator + MMA issuer (tcgen05.mma.cta_group::1.kind::f16, M=128, N=BN,
+//               K=16; commit frees the stage; a tile's last commit signals the epilogue).
+//   warps 6-9 : epilogue: tcgen05.ld of the tile's accumulator (TMEM lanes = rows), fused
+//               row epilogue (bias, time bias, cached-stat GN + SiLU, step update, residual,
+//               QKV split / transposed V) and stores.
+// Two TMEM accumulators (2 x BN <= 512 columns) let the epilogue of tile i overlap the main
+// loop of tile i+1. Tiles run N-fastest so consecutive CTAs share the gathered A rows in L2.
+// BN is a multiple of 16 in [128, 256] dividing N where possible (UMMA N; 320 -> 160,
+// 960 -> 240, 1280 -> 256), so no tile column is wasted.
+#include "fis_tc.cuh"
+#include "fis_tma.cuh"
+
+namespace fis {
+namespace big {
+
+using namespace fis::tc;
+
+constexpr int THREADS = 320;
+constexpr int A_WARPS = 4, B_WARP = 4, MMA_WARP = 5, EPI_WARP0 = 6;
+constexpr int A_BYTES = BM * BK * 2;     // 16 KB
+constexpr int SMEM_BUDGET = 200 * 1024;  // pipeline stages
+constexpr int MAX_STAGES = 8;
+constexpr int ACC_STRIDE = 256;          // TMEM column offset of accumulator 1
+constexpr int LAG = 2;  // cp.async stages in flight per A-producer thread
+constexpr int SEL_BYTES = BM * 19 * 4;  // select-on-read table [128][18] + row pixels [128]
+
+struct Layout {
+    int bn, stage, stages, total;
+};
+
+__host__ __device__ inline Layout layout(int bn) {
+    Layout l;
+    l.bn = bn;
+    l.stage = A_BYTES + bn * BK * 2;
+    l.stages = SMEM_BUDGET / l.stage;
+    if (l.stages > MAX_STAGES) l.stages = MAX_STAGES;
+    // stages + barriers (2 per stage + 4) + TMEM slot + epilogue tables (6 x BN floats) +
+    // per-row select-on-read table (128 rows x 2 segments x 9 taps) + align
+    l.total = l.stages * l.stage + 1024 + 256 + 6 * bn * 4 + SEL_BYTES + 64;
+    return l;
+}
+
+FIS_DEV void tma2d(uint32_t dst, const void* tmap, int c0, int c1, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+            dst),
+        "l"(tmap), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+        : "memory");
+}
+FIS_DEV void arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+FIS_DEV void mma_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+                 : "memory");
+}
+FIS_DEV void tmem_ld16(uint32_t taddr, uint32_t* u) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(u[0]), "=r"(u[1]), "=r"(u[2]), "=r"(u[3]), "=r"(u[4]), "=r"(u[5]), "=r"(u[6]), "=r"(u[7]),
+          "=r"(u[8]), "=r"(u[9]), "=r"(u[10]), "=r"(u[11]), "=r"(u[12]), "=r"(u[13]), "=r"(u[14]), "=r"(u[15])
+        : "r"(taddr));
+}
+FIS_DEV void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+// debug timeline (FIS_BIG_DBG & 4): CTA 0's per-stage times [role][iteration] (%globaltimer ns)
+__device__ unsigned long long g_big_trace[3][256];
+FIS_DEV unsigned long long gtime() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+__global__ void __launch_bounds__(THREADS, 1)
+    gemm_big_kernel(const fis_gemm_args a, const __grid_constant__ CUtensorMap tmap_b, int bn, int dbg) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    // align by pointer arithmetic on the shared array (keeps the shared address space: LDS/STS)
+    unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+    const Layout L = layout(bn);
+    uint64_t* full = (uint64_t*)(smem + L.stages * L.stage);
+    uint64_t* empty = full + L.stages;
+    uint64_t* acc_full = empty + L.stages;  // [2]
+    uint64_t* acc_empty = acc_full + 2;     // [2]
+    uint32_t* tmem_slot = (uint32_t*)(acc_empty + 2);
+    float* tabs = (float*)(smem + L.stages * L.stage + 256);
+    int* seltab = (int*)(tabs + 6 * bn);
+    int* rowtab = seltab + BM * 18;
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int tiles_n = (a.n + bn - 1) / bn, tiles_m = (a.m + BM - 1) / BM;
+    const int ntiles = tiles_m * tiles_n;
+    const int kblocks = (a.k + BK - 1) / BK;
+
+    if (tid == 0) {
+        for (int s = 0; s < L.stages; s++) {
+            mbar_init(full + s, A_WARPS * 32 + 1);
+            mbar_init(empty + s, 1);
+        }
+        for (int b = 0; b < 2; b++) {
+            mbar_init(acc_full + b, 1);
+            mbar_init(acc_empty + b, 128);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == B_WARP && lane == 0)
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&tmap_b) : "memory");
+    if (warp == MMA_WARP) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    pdl_trigger();
+    pdl_wait();
+    const int t = cur_step(a.step);
+
+    if (warp < A_WARPS) {
+        // ------------------------------------------------------------ A producers
+        // Row metadata: thread tid resolves tile row tid (pixel, and for CONV the select-on-read
+        // decision of every tap) into shared tables. Loads: lane l copies 16-byte chunk l & 7 of
+        // rows w*32 + 4*i + (l >> 3), i = 0..7, so each warp instruction reads four whole 128-byte
+        // rows (coalesced) and writes them conflict-free into the swizzled stage.
+        const char* abase = a.a.ptr ? ref_base(a.a, t) : nullptr;
+        const char* f0 = a.nsrc > 0 && a.src[0].fresh.ptr ? ref_base(a.src[0].fresh, t) : nullptr;
+        const char* c0p = a.nsrc > 0 && a.src[0].cache.ptr ? ref_base(a.src[0].cache, t) : nullptr;
+        const char* f1 = a.nsrc > 1 && a.src[1].fresh.ptr ? ref_base(a.src[1].fresh, t) : nullptr;
+        const char* c1p = a.nsrc > 1 && a.src[1].cache.ptr ? ref_base(a.src[1].cache, t) : nullptr;
+        const bool conv = a.a_mode == FIS_A_CONV3X3;
+        const long long ldf0 = a.src[0].fresh.ld, ldc0 = a.src[0].cache.ld;
+        const long long ldf1 = a.src[1].fresh.ld, ldc1 = a.src[1].cache.ld;
+        const long long lda = a.a.ld;
+        const int src0c = a.nsrc > 0 ? a.src[0].c : 0;
+        const int cin = conv ? src0c + (a.nsrc > 1 ? a.src[1].c : 0) : a.k;
+        const uint32_t sbase = smem_u32(smem);
+        const char* dummy = (const char*)a.b.ptr;
+        const int j = lane & 7, rbase = warp * 32 + (lane >> 3);
+        int it = 0;
+        int last_m = -1;
+        for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+            const int mt = tile / tiles_n;
+            if (mt != last_m) {  // row metadata once per M tile
+                last_m = mt;
+                const int r = mt * BM + tid;
+                const bool valid = r < a.m;
+                const int p = valid ? (a.rows ? __ldg(a.rows + r) : r) : -1;
+                rowtab[tid] = p;
+                if (conv) {
+                    int* sel = seltab + tid * 18;
+                    if (valid) {
+                        build_sel(a, p, 0, sel);
+                        if (a.nsrc > 1) build_sel(a, p, 1, sel + 9);
+                    } else {
+#pragma unroll
+                        for (int q = 0; q < 18; q++) sel[q] = SEL_ZERO;
+                    }
+                }
+                __syncwarp();
+            }
+            // rows mode: this thread's 8 row pointers for the whole tile
+            const char* rp[8];
+            if (!conv) {
+#pragma unroll
+                for (int i = 0; i < 8; i++) {
+                    const int p = rowtab[rbase + 4 * i];
+                    rp[i] = p >= 0 ? abase + (long long)p * lda * 2 + j * 16 : nullptr;
+                }
+            }
+            for (int kb = 0; kb < kblocks; kb++, it++) {
+                const int s = it % L.stages;
+                if (it >= L.stages) mbar_wait(empty + s, ((it / L.stages) & 1) ^ 1);
+                if ((dbg & 4) && blockIdx.x == 0 && tid == 0 && it < 256) g_big_trace[0][it] = gtime();
+                const int k0 = kb * BK;
+                const uint32_t sa = sbase + s * L.stage;
+                const char* src[8];
+                if (conv) {
+                    const int tap = k0 / cin;
+                    int c = k0 - tap * cin;
+                    const int seg = c >= src0c ? 1 : 0;
+                    c -= seg ? src0c : 0;
+                    const char* fb = (seg ? f1 : f0) + (c + j * 8) * 2;
+                    const char* cb = (seg ? c1p : c0p) + (c + j * 8) * 2;
+                    const long long ldf = (seg ? ldf1 : ldf0) * 2, ldc = (seg ? ldc1 : ldc0) * 2;
+                    const int* selc = seltab + rbase * 18 + seg * 9 + tap;
+                    int v[8];
+#pragma unroll
+                    for (int i = 0; i < 8; i++) v[i] = selc[i * 4 * 18];  // 8 independent shared loads
+#pragma unroll
+                    for (int i = 0; i < 8; i++)
+                        src[i] = v[i] == SEL_ZERO ? nullptr
+                                 : v[i] >= 0      ? fb + (long long)v[i] * ldf
+                                                  : cb + (long long)(-2 - v[i]) * ldc;
+                } else {
+                    const bool kok = k0 + j * 8 < a.k && !(dbg & 2);
+#pragma unroll
+                    for (int i = 0; i < 8; i++) src[i] = rp[i] && kok ? rp[i] + k0 * 2 : nullptr;
+                }
+#pragma unroll
+                for (int i = 0; i < 8; i++) {
+                    const bool ok = src[i] != nullptr && !(dbg & 2);
+                    cp_async16(sa + sw128_off(rbase + 4 * i, j), ok ? (const void*)src[i] : (const void*)dummy, ok);
+                }
+                if (dbg & 8) {
+                    cp_async_arrive_noinc(full + s);
+                } else {
+                    // keep LAG stages of this thread's copies in flight; publish the oldest one
+                    cp_commit();
+                    if (it >= LAG) {
+                        cp_wait<LAG>();
+                        fence_async_smem();
+                        mbar_arrive(full + (it - LAG) % L.stages);
+                    }
+                }
+            }
+        }
+        if (!(dbg & 8)) {  // drain: publish the last LAG stages
+            cp_wait<0>();
+            fence_async_smem();
+            for (int q = it - LAG < 0 ? 0 : it - LAG; q < it; q++) mbar_arrive(full + q % L.stages);
+        }
+    } else if (warp == B_WARP) {
+        // ------------------------------------------------------------ B producer (TMA)
+        if (lane == 0) {
+            const uint32_t sbase = smem_u32(smem);
+            const uint32_t bbytes = (uint32_t)(bn * BK * 2);
+            int it = 0;
+            for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+                const int n0 = (tile % tiles_n) * bn;
+                for (int kb = 0; kb < kblocks; kb++, it++) {
+                    const int s = it % L.stages;
+                    if (it >= L.stages) mbar_wait(empty + s, ((it / L.stages) & 1) ^ 1);
+                    if ((dbg & 4) && blockIdx.x == 0 && it < 256) g_big_trace[1][it] = gtime();
+                    arrive_expect_tx(full + s, bbytes);
+                    tma2d(sbase + s * L.stage + A_BYTES, &tmap_b, kb * BK, n0, full + s);
+                }
+            }
+        }
+    } else if (warp == MMA_WARP) {
+        // ------------------------------------------------------------ MMA issuer
+        const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(bn >> 3) << 17) |
+                               ((uint32_t)(BM >> 4) << 24);
+        const uint32_t sbase = smem_u32(smem);
+        int it = 0, lt = 0;
+        for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, lt++) {
+            const int buf = lt & 1;
+            if (lt >= 2) mbar_wait(acc_empty + buf, ((lt >> 1) & 1) ^ 1);  // epilogue drained this buffer
+            tc_fence_after();
+            const uint32_t dt = tmem + buf * ACC_STRIDE;
+            for (int kb = 0; kb < kblocks; kb++, it++) {
+                const int s = it % L.stages;
+                mbar_wait(full + s, (it / L.stages) & 1);
+                tc_fence_after();
+                if ((dbg & 4) && blockIdx.x == 0 && lane == 0 && it < 256) g_big_trace[2][it] = gtime();
+                if (lane == 0) {
+                    const uint32_t sa = sbase + s * L.stage, sb = sa + A_BYTES;
+#pragma unroll
+                    for (int kk = 0; kk < BK / 16; kk++) {
+                        const uint64_t ad = sw128_desc(sa + kk * 32), bd = sw128_desc(sb + kk * 32);
+                        const uint32_t acc = (kb > 0 || kk > 0) ? 1u : 0u;
+                        asm volatile(
+                            "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+                            "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(dt),
+                            "l"(ad), "l"(bd), "r"(idesc), "r"(acc));
+                    }
+                    mma_commit(empty + s);
+                    if (kb == kblocks - 1) mma_commit(acc_full + buf);
+                }
+                __syncwarp();
+            }
+        }
+    } else {
+        // ------------------------------------------------------------ epilogue (warps 6-9)
+        const int et = tid - EPI_WARP0 * 32;  // 0..127
+        const int quarter = warp & 3;         // TMEM lane quarter this warp may access
+        const int lr = quarter * 32 + lane;   // tile row of this thread
+        const EpiCtx e = make_epi(a, t);
+        EpiTab tb;
+        tb.mean = tabs;
+        tb.rstd = tb.mean + bn;
+        tb.bias = tb.rstd + bn;
+        tb.b2 = tb.bias + bn;
+        tb.gamma = tb.b2 + bn;
+        tb.beta = tb.gamma + bn;
+        int lt = 0;
+        for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, lt++) {
+            const int m0 = (tile / tiles_n) * BM, n0 = (tile % tiles_n) * bn;
+            asm volatile("bar.sync 1, 128;" ::: "memory");  // previous tile's table reads done
+            for (int c = et; c < bn; c += 128) {
+                const int n = n0 + c;
+                const bool ok = n < a.n;
+                tb.bias[c] = ok && a.bias ? __ldg(a.bias + n) : 0.f;
+                tb.b2[c] = ok && e.bias2 ? load_elem(e.bias2, a.bias2.dtype, n) : 0.f;
+                if (a.epi == FIS_EPI_GN_SILU && ok) {
+                    const int g = n / e.cpg;
+                    const float rstd = (float)(1.0 / sqrt((double)e.var[g] + (double)a.eps));
+                    const float scale = rstd * __ldg(a.gamma + n);
+                    tb.mean[c] = scale;
+                    tb.rstd[c] = fmaf(-e.mean[g], scale, __ldg(a.beta + n));
+                } else {
+                    tb.mean[c] = 0.f;
+                    tb.rstd[c] = 0.f;
+                }
+            }
+            asm volatile("bar.sync 1, 128;" ::: "memory");
+            const int buf = lt & 1;
+            mbar_wait(acc_full + buf, (lt >> 1) & 1);
+            tc_fence_after();
+            const uint32_t taddr = tmem + buf * ACC_STRIDE + ((uint32_t)(quarter * 32) << 16);
+            const int r = m0 + lr;
+            for (int cb = 0; cb < bn; cb += 32) {
+                uint32_t u[32];
+                const bool two = cb + 16 < bn;
+                tmem_ld16(taddr + cb, u);
+                if (two) tmem_ld16(taddr + cb + 16, u + 16);
+                tmem_wait_ld();
+                if (r < a.m && !(dbg & 1)) {
+                    float v[16];
+#pragma unroll
+                    for (int j = 0; j < 16; j++) v[j] = __uint_as_float(u[j]);
+                    row_epilogue_any(a, e, tb, r, cb, n0, v);
+                    if (two) {
+#pragma unroll
+                        for (int j = 0; j < 16; j++) v[j] = __uint_as_float(u[16 + j]);
+                        row_epilogue_any(a, e, tb, r, cb + 16, n0, v);
+                    }
+                }
+            }
+            tc_fence_before();
+            mbar_arrive(acc_empty + buf);
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == MMA_WARP) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+}
+
+}  // namespace big
+}  // namespace fis
+
+// ---------------------------------------------------------------------------- host side
+
+namespace {
+
+// Weight tensor maps, cached by (base, n, k, ld, box): a captured step re-encodes nothing.
+struct MapEntry {
+    const void* base;
+    long long n, k, ld;
+    int box;
+    CUtensorMap map;
+};
+constexpr int MAP_CACHE = 512;
+MapEntry g_maps[MAP_CACHE];
+int g_nmaps = 0, g_next = 0;
+
+const CUtensorMap* weight_map(const void* base, long long n, long long k, long long ld, int box) {
+    for (int i = 0; i < g_nmaps; i++) {
+        const MapEntry& m = g_maps[i];
+        if (m.base == base && m.n == n && m.k == k && m.ld == ld && m.box == box) return &m.map;
+    }
+    MapEntry e{base, n, k, ld, box, {}};
+    if (!encode_2d(&e.map, base, n, k, ld, box)) return nullptr;
+    int slot;
+    if (g_nmaps < MAP_CACHE) slot = g_nmaps++;
+    else { slot = g_next; g_next = (g_next + 1) % MAP_CACHE; }
+    g_maps[slot] = e;
+    return &g_maps[slot].map;
+}
+
+int sms() {
+    static int n = 0;
+    if (n <= 0) n = fis_device_sm_count();
+    return n > 0 ? n : 148;
+}
+
+}  // namespace
+
+// Tile width: the largest multiple of 16 in [128, 256] dividing N; else 256 (or N rounded up
+// to 16 when N < 256).
+int fis_gemm_big_bn(int n) {
+    static int force = getenv("FIS_BIG_BN") ? atoi(getenv("FIS_BIG_BN")) : 0;
+    if (force) return force;
+    for (int bn = 256; bn >= 128; bn -= 16)
+        if (n % bn == 0) return bn;
+    if (n < 256) return (n + 15) & ~15;
+    return 256;
+}
+
+// The persistent kernel takes GEMMs whose tile count fills the SMs (stacked requests): bf16 A
+// (gathered rows or 3x3 conv), static bf16 weights addressable by TMA, no split-K.
+int fis_gemm_big_eligible(const fis_gemm_args* a) {
+    if (getenv("FIS_BIG") && getenv("FIS_BIG")[0] == '0') return 0;
+    if (a->splits > 1 || a->n < 128 || a->b.step_stride != 0) return 0;
+    const int bn = fis_gemm_big_bn(a->n);
+    const long long tiles = (long long)((a->m + 127) / 128) * ((a->n + bn - 1) / bn);
+    return tiles >= sms() ? 1 : 0;
+}
+
+int fis_gemm_big_launch(const fis_gemm_args* a, cudaStream_t stream) {
+    const int bn = fis_gemm_big_bn(a->n);
+    const CUtensorMap* tm = weight_map(a->b.ptr, a->n, a->k, a->b.ld, bn);
+    if (!tm) return FIS_ERR_UNSUPPORTED;
+    const fis::big::Layout L = fis::big::layout(bn);
+    static int configured_smem = 0;
+    if (configured_smem < L.total) {
+        if (cudaFuncSetAttribute(fis::big::gemm_big_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 227 * 1024) != cudaSuccess)
+            return FIS_ERR_UNSUPPORTED;
+        configured_smem = 227 * 1024;
+    }
+    const long long tiles = (long long)((a->m + 127) / 128) * ((a->n + bn - 1) / bn);
+    const int grid = (int)(tiles < sms() ? tiles : sms());
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(fis::big::THREADS);
+    cfg.dynamicSmemBytes = L.total;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = fis_pdl_enabled() ? 1 : 0;
+    static int dbg = getenv("FIS_BIG_DBG") ? atoi(getenv("FIS_BIG_DBG")) : 0;  // 1: no stores, 2: no A loads
+    return cudaLaunchKernelEx(&cfg, fis::big::gemm_big_kernel, *a, *tm, bn, dbg) == cudaSuccess ? FIS_OK
+                                                                                              : FIS_ERR_LAUNCH;
+}
+
+extern "C" int fis_big_trace_read(unsigned long long* out768) {
+    return cudaMemcpyFromSymbol(out768, fis::big::g_big_trace, sizeof(fis::big::g_big_trace)) == cudaSuccess
+               ? FIS_OK : FIS_ERR_LAUNCH;
+}

@@ -424,287 +424,6 @@ int choose_splits(long long tiles, long long kb) {
 }
 
 
-// ============================================================================ fused attention
-// out[r, c0:c0+dvs] = res + softmax(Q K^T * scale) V^T^T for one 128-query tile x one value slice.
-constexpr int AT_STAGES = 3;
-constexpr int AT_A = 128 * 64 * 2;       // Q chunk: 128 rows x 64 (SW128 K-major)
-constexpr int AT_B = 256 * 64 * 2;       // K chunk (128 keys) or V^T chunk (<= 256 rows) x 64
-constexpr int AT_STAGE = AT_A + AT_B;
-constexpr int AT_P = 2 * 128 * 64 * 2;   // P tile: 128 rows x 128 keys as two 64-key SW128 chunks
-constexpr int AT_SMEM = AT_STAGES * AT_STAGE + AT_P + 1024 + 256;
-
-__device__ __forceinline__ uint32_t idesc_bf16(int M, int N) {
-    return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
-}
-
-__device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t ad, uint64_t bd, uint32_t idesc, uint32_t acc) {
-    asm volatile(
-        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
-        "l"(ad), "l"(bd), "r"(idesc), "r"(acc));
-}
-__device__ __forceinline__ void mma_commit(uint64_t* bar) {
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
-                 : "memory");
-}
-__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
-    uint32_t u[32];
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-        : "=r"(u[0]), "=r"(u[1]), "=r"(u[2]), "=r"(u[3]), "=r"(u[4]), "=r"(u[5]), "=r"(u[6]), "=r"(u[7]),
-          "=r"(u[8]), "=r"(u[9]), "=r"(u[10]), "=r"(u[11]), "=r"(u[12]), "=r"(u[13]), "=r"(u[14]), "=r"(u[15]),
-          "=r"(u[16]), "=r"(u[17]), "=r"(u[18]), "=r"(u[19]), "=r"(u[20]), "=r"(u[21]), "=r"(u[22]), "=r"(u[23]),
-          "=r"(u[24]), "=r"(u[25]), "=r"(u[26]), "=r"(u[27]), "=r"(u[28]), "=r"(u[29]), "=r"(u[30]), "=r"(u[31])
-        : "r"(taddr));
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-    for (int j = 0; j < 32; j++) v[j] = __uint_as_float(u[j]);
-}
-
-__global__ void __launch_bounds__(THREADS, 1) attn_tc_kernel(const fis_attn_args a, int dvs) {
-    extern __shared__ __align__(1024) unsigned char smem_raw[];
-    unsigned char* smem = (unsigned char*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-    unsigned char* ptile = smem + AT_STAGES * AT_STAGE;
-    uint64_t* full = (uint64_t*)(ptile + AT_P);
-    uint64_t* empty = full + AT_STAGES;
-    uint64_t* s_ready = empty + AT_STAGES;
-    uint64_t* s_free = s_ready + 1;
-    uint64_t* p_ready = s_free + 1;
-    uint64_t* p_free = p_ready + 1;
-    uint64_t* o_done = p_free + 1;
-    uint32_t* tmem_slot = (uint32_t*)(o_done + 1);
-
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    // ragged segments (batched requests): rows [q_beg, q_end) attend to keys [k_beg, k_beg + n_keys)
-    int q_beg = 0, q_end = a.m, k_beg = 0, n_keys = a.n_keys;
-    if (a.nseg > 0) {
-        const int sg = blockIdx.z;
-        q_beg = __ldg(a.q_seg + 2 * sg);
-        q_end = __ldg(a.q_seg + 2 * sg + 1);
-        k_beg = __ldg(a.k_seg + 2 * sg);
-        n_keys = __ldg(a.k_seg + 2 * sg + 1) - k_beg;
-    }
-    const int m0 = q_beg + blockIdx.y * 128, c0 = blockIdx.x * dvs;
-    if (m0 >= q_end || n_keys <= 0) return;  // uniform for the CTA, before any barrier
-    const int nkb = (n_keys + 127) / 128, dch = a.d / 64;
-    const bool single = nkb == 1;
-    if (tid == 0) {
-        for (int i = 0; i < AT_STAGES; i++) {
-            mbar_init(full + i, 128);
-            mbar_init(empty + i, 1);
-        }
-        mbar_init(s_ready, 1);
-        mbar_init(s_free, 128);
-        mbar_init(p_ready, 128);
-        mbar_init(p_free, 1);
-        mbar_init(o_done, 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    if (warp == MMA_WARP) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-    }
-    tc_fence_before();
-    __syncthreads();
-    tc_fence_after();
-    const uint32_t tmem = *tmem_slot;
-    pdl_trigger();
-    pdl_wait();
-    const int t = cur_step(a.step);
-    const int first_pass = single ? 2 : 1;
-
-    if (warp >= 4 && warp < 8) {
-        // ------------------------------------------------------------ producers (128 threads)
-        const int pr = tid - 128;
-        const char* qb = ref_base(a.q, t);
-        const char* kb = ref_base(a.k, t);
-        const char* vb = ref_base(a.vt, t);
-        const char* dummy = qb;
-        const uint32_t sbase = smem_u32(smem);
-        int it = 0;
-        for (int pass = first_pass; pass <= 2; pass++) {
-            for (int j = 0; j < nkb; j++) {
-                for (int kc = 0; kc < dch + (pass == 2 ? 2 : 0); kc++) {
-                    const int st = it % AT_STAGES;
-                    if (it >= AT_STAGES) mbar_wait(empty + st, ((it / AT_STAGES) & 1) ^ 1);
-                    const uint32_t sa = sbase + st * AT_STAGE, sb = sa + AT_A;
-                    if (kc < dch) {  // S item: Q chunk + K chunk
-                        const int qr = m0 + pr, key = j * 128 + pr;  // key index within the segment
-                        const char* qs = qb + ((long long)qr * a.q.ld + kc * 64) * 2;
-                        const char* ks = kb + ((long long)(k_beg + key) * a.k.ld + kc * 64) * 2;
-#pragma unroll
-                        for (int u = 0; u < 8; u++) {
-                            cp_async16(sa + sw128_off(pr, u), qr < q_end ? (const void*)(qs + 16 * u) : (const void*)dummy, qr < q_end);
-                            cp_async16(sb + sw128_off(pr, u), key < n_keys ? (const void*)(ks + 16 * u) : (const void*)dummy,
-                                       key < n_keys);
-                        }
-                    } else {  // PV item: V^T chunk (rows = value channels, K = keys)
-                        const int k0 = j * 128 + (kc - dch) * 64;
-                        for (int row = pr; row < dvs; row += 128) {
-                            const int ch = c0 + row;
-                            const char* vs = vb + ((long long)ch * a.vt.ld + k_beg + k0) * 2;
-#pragma unroll
-                            for (int u = 0; u < 8; u++) {
-                                const bool ok = ch < a.dv && k0 + 8 * u < n_keys;
-                                cp_async16(sb + sw128_off(row, u), ok ? (const void*)(vs + 16 * u) : (const void*)dummy, ok);
-                            }
-                        }
-                    }
-                    cp_async_arrive_noinc(full + st);
-                    it++;
-                }
-            }
-        }
-    } else if (warp == MMA_WARP) {
-        // ------------------------------------------------------------ MMA issuer
-        const uint32_t sbase = smem_u32(smem), pbase = smem_u32(ptile);
-        const uint32_t id_s = idesc_bf16(128, 128), id_o = idesc_bf16(128, dvs);
-        int it = 0, sb = 0, pb = 0;
-        for (int pass = first_pass; pass <= 2; pass++) {
-            for (int j = 0; j < nkb; j++) {
-                for (int kc = 0; kc < dch; kc++) {  // S = Q K_j^T
-                    const int st = it % AT_STAGES;
-                    mbar_wait(full + st, (it / AT_STAGES) & 1);
-                    if (kc == 0 && sb > 0) mbar_wait(s_free, (sb - 1) & 1);  // softmax has read the previous S
-                    tc_fence_after();
-                    if (lane == 0) {
-                        const uint32_t sa = sbase + st * AT_STAGE, sbb = sa + AT_A;
-#pragma unroll
-                        for (int kk = 0; kk < 4; kk++)
-                            mma_bf16(tmem, sw128_desc(sa + kk * 32), sw128_desc(sbb + kk * 32), id_s, (kc | kk) ? 1u : 0u);
-                        mma_commit(empty + st);
-                        if (kc == dch - 1) mma_commit(s_ready);
-                    }
-                    __syncwarp();
-                    it++;
-                }
-                sb++;
-                if (pass == 2) {
-                    mbar_wait(p_ready, pb & 1);  // P of block j written to the P tile
-                    for (int kc = 0; kc < 2; kc++) {  // O += P_j V_j
-                        const int st = it % AT_STAGES;
-                        mbar_wait(full + st, (it / AT_STAGES) & 1);
-                        tc_fence_after();
-                        if (lane == 0) {
-                            const uint32_t sbb = sbase + st * AT_STAGE + AT_A;
-                            const uint32_t pa = pbase + kc * (128 * 128);
-#pragma unroll
-                            for (int kk = 0; kk < 4; kk++)
-                                mma_bf16(tmem + 128, sw128_desc(pa + kk * 32), sw128_desc(sbb + kk * 32), id_o,
-                                         (pb | kc | kk) ? 1u : 0u);
-                            mma_commit(empty + st);
-                            if (kc == 1) {
-                                mma_commit(p_free);
-                                if (j == nkb - 1) mma_commit(o_done);
-                            }
-                        }
-                        __syncwarp();
-                        it++;
-                    }
-                    pb++;
-                }
-            }
-        }
-    } else {
-        // ------------------------------------------------------------ softmax + epilogue (warps 0-3)
-        const int lr = tid, r = m0 + lr;
-        const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
-        float mrow = -INFINITY, lrow = 0.f;
-        int sb = 0, pb = 0;
-        float v[32];
-        for (int pass = first_pass; pass <= 2; pass++) {
-            for (int j = 0; j < nkb; j++) {
-                mbar_wait(s_ready, sb & 1);
-                tc_fence_after();
-                const int kbase = j * 128;
-                if (pass == 1 || single) {  // row statistics (online over this block)
-#pragma unroll 1
-                    for (int cb = 0; cb < 128; cb += 32) {
-                        tmem_ld32(trow + cb, v);
-                        float cm = -INFINITY;
-#pragma unroll
-                        for (int q = 0; q < 32; q++)
-                            if (kbase + cb + q < n_keys) cm = fmaxf(cm, v[q] * a.scale);
-                        const float mn = fmaxf(mrow, cm);
-                        float add = 0.f;
-#pragma unroll
-                        for (int q = 0; q < 32; q++)
-                            if (kbase + cb + q < n_keys) add += expf(v[q] * a.scale - mn);
-                        lrow = (mrow == -INFINITY ? 0.f : lrow * expf(mrow - mn)) + add;
-                        mrow = mn;
-                    }
-                }
-                if (pass == 2) {  // P = exp(s*scale - m) / l  -> bf16 P tile (SW128, K-major)
-                    if (pb > 0) mbar_wait(p_free, (pb - 1) & 1);
-                    const float inv = 1.0f / lrow;
-#pragma unroll 1
-                    for (int cb = 0; cb < 128; cb += 32) {
-                        tmem_ld32(trow + cb, v);
-                        unsigned char* pt = ptile + (cb >> 6) * (128 * 128);
-#pragma unroll
-                        for (int u = 0; u < 4; u++) {
-                            uint4 pk;
-                            __nv_bfloat162* h = (__nv_bfloat162*)&pk;
-#pragma unroll
-                            for (int e2 = 0; e2 < 4; e2++) {
-                                const int q0 = 8 * u + 2 * e2;
-                                const float p0 = kbase + cb + q0 < n_keys ? expf(v[q0] * a.scale - mrow) * inv : 0.f;
-                                const float p1 = kbase + cb + q0 + 1 < n_keys ? expf(v[q0 + 1] * a.scale - mrow) * inv : 0.f;
-                                h[e2] = __floats2bfloat162_rn(p0, p1);
-                            }
-                            const int unit = ((cb & 63) >> 3) + u;
-                            *(uint4*)(pt + sw128_off(lr, unit)) = pk;
-                        }
-                    }
-                    fence_async_smem();  // generic-proxy P writes -> tensor-core (async proxy) reads
-                    mbar_arrive(p_ready);
-                    pb++;
-                }
-                tc_fence_before();
-                mbar_arrive(s_free);
-                sb++;
-            }
-        }
-        // epilogue: O row slice -> + residual -> store
-        mbar_wait(o_done, 0);
-        tc_fence_after();
-        {  // tcgen05.ld is warp-collective: every lane loads, only rows < m store
-            const bool live = r < q_end;
-            char* ob = ref_base(a.out, t);
-            char* pbp = a.pre.ptr ? ref_base(a.pre, t) : nullptr;
-            const char* rb = a.res.ptr ? ref_base(a.res, t) : nullptr;
-#pragma unroll 1
-            for (int cb = 0; cb < dvs; cb += 32) {
-                tmem_ld32(trow + 128 + cb, v);
-                const int n = c0 + cb;
-                const int nvalid = min(32, a.dv - n);
-                if (nvalid <= 0) break;
-                if (!live) continue;
-                if (pbp) {
-                    store_row16(pbp, a.pre.dtype, (long long)r * a.pre.ld + n, min(16, nvalid), v);
-                    if (nvalid > 16) store_row16(pbp, a.pre.dtype, (long long)r * a.pre.ld + n + 16, nvalid - 16, v + 16);
-                }
-                if (rb) {
-                    float q[16];
-                    load_row16(rb, a.res.dtype, (long long)r * a.res.ld + n, min(16, nvalid), q);
-#pragma unroll
-                    for (int e2 = 0; e2 < 16; e2++) v[e2] = __fadd_rn(v[e2], q[e2]);
-                    if (nvalid > 16) {
-                        load_row16(rb, a.res.dtype, (long long)r * a.res.ld + n + 16, nvalid - 16, q);
-#pragma unroll
-                        for (int e2 = 0; e2 < 16; e2++) v[16 + e2] = __fadd_rn(v[16 + e2], q[e2]);
-                    }
-                }
-                store_row16(ob, a.out.dtype, (long long)r * a.out.ld + n, min(16, nvalid), v);
-                if (nvalid > 16) store_row16(ob, a.out.dtype, (long long)r * a.out.ld + n + 16, nvalid - 16, v + 16);
-            }
-        }
-    }
-    tc_fence_before();
-    __syncthreads();
-    if (warp == MMA_WARP) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
-}
 }  // namespace tc
 }  // namespace fis
 
@@ -750,39 +469,4 @@ extern "C" int fis_trace_read_ctas(unsigned long long* out2048) {
 extern "C" int fis_trace_read(unsigned long long* out16) {
     return cudaMemcpyFromSymbol(out16, fis::tc::g_trace, 16 * sizeof(unsigned long long)) == cudaSuccess
                ? FIS_OK : FIS_ERR_LAUNCH;
-}
-
-// value-slice width: largest multiple of 32 dividing dv with <= 256 columns (TMEM: 128 S + slice)
-static int attn_slice(int dv) {
-    for (int w = 256; w >= 32; w -= 32)
-        if (dv % w == 0) return w;
-    return 0;
-}
-
-extern "C" int fis_attn(const fis_attn_args* a, void* stream) {
-    if (a->m == 0) return FIS_OK;
-    if (a->d % 64 || a->n_keys < 1 || a->q.dtype != FIS_BF16 || a->k.dtype != FIS_BF16 || a->vt.dtype != FIS_BF16 ||
-        (a->q.ld % 8) || (a->k.ld % 8) || (a->vt.ld % 8))
-        return FIS_ERR_UNSUPPORTED;
-    const int dvs = attn_slice(a->dv);
-    if (!dvs) return FIS_ERR_UNSUPPORTED;
-    static bool configured = false;
-    if (!configured) {
-        if (cudaFuncSetAttribute(fis::tc::attn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 fis::tc::AT_SMEM) != cudaSuccess)
-            return FIS_ERR_UNSUPPORTED;
-        configured = true;
-    }
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = a->nseg > 0 ? dim3(a->dv / dvs, (a->max_seg_q + 127) / 128, a->nseg)
-                              : dim3(a->dv / dvs, (a->m + 127) / 128, 1);
-    cfg.blockDim = dim3(fis::tc::THREADS);
-    cfg.dynamicSmemBytes = fis::tc::AT_SMEM;
-    cfg.stream = (cudaStream_t)stream;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = fis_pdl_enabled() ? 1 : 0;
-    return cudaLaunchKernelEx(&cfg, fis::tc::attn_tc_kernel, *a, dvs) == cudaSuccess ? FIS_OK : FIS_ERR_LAUNCH;
 }

@@ -117,10 +117,14 @@ class Launcher:
         # each) own separate scratch activations, split-K workspaces and step counters
         self.ns = 0
         self._ns_state = {}
+        # stacked images of the step being launched (BatchedSparsePlan: R requests as one batch)
+        self.batch = 1
         self.launches = 0
         self._scratch = {}
         self.fused_xattn = False  # SIMT xattn is latency-bound; superseded by fis_attn
-        self.fused_attn = False   # tcgen05 fused attention: one CTA per 128 queries is latency-bound (r01: 2.35 vs 1.63 ms/step)
+        # tcgen05 fused attention (csrc/fis_attn.cu: TMA-fed, double-buffered S/P) instead of
+        # S GEMM -> softmax -> P.V GEMM (FIS_FUSED_ATTN=0 restores the three-launch path)
+        self.fused_attn = os.environ.get("FIS_FUSED_ATTN", "1") == "1"
         # gather lists (rows / pixel->row maps) are written once per edit, before any step runs
         # (DevicePlan syncs), so GEMMs may read them before the programmatic-launch wait
         self.static_meta = False
@@ -334,6 +338,10 @@ class Engine(Launcher):
     def hw(self, level):
         return (self.config.latent_h >> level) * (self.config.latent_w >> level)
 
+    def cap(self, level):
+        """Row capacity of a level's activations: its pixels times the stacked images."""
+        return self.hw(level) * self.batch
+
     def grid(self, level):
         return self.config.latent_h >> level, self.config.latent_w >> level
 
@@ -362,11 +370,13 @@ class Engine(Launcher):
         return out
 
     # ------------------------------------------------------------ building blocks
-    def attn_self(self, lid, m, s: DRef, y1: DRef, level, tag, pre=None):
-        """y1 = s + softmax(s Wq (s Wk)^T * scale) (s Wv) over m tokens (sparse.py:265-300/341-349)."""
+    def attn_self(self, lid, m, s: DRef, y1: DRef, level, tag, pre=None, segs=None):
+        """y1 = s + softmax(s Wq (s Wk)^T * scale) (s Wv) over m tokens (sparse.py:265-300/341-349).
+
+        segs (batched requests): (q_seg, nseg, max_q) -- each request's rows attend to its own rows."""
         wqkv, scale = self.W.sa[lid]
         c = wqkv.shape[1]
-        cap = self.hw(level)
+        cap = self.cap(level)
         mp = _pad(cap)
         qk = self.scratch(f"qk{tag}", (cap, 2 * c))
         vt = self.scratch(f"vt{tag}", (c, mp), zero=True)
@@ -376,6 +386,10 @@ class Engine(Launcher):
         self.gemm(m, 3 * c, c, a=s, b=DRef(wqkv), d=DRef(qk), n_split=2 * c, d2=DRef(vt, ld=mp), d2_trans=True,
                   b_static=True)
         qkr = DRef(qk)
+        if segs is not None:
+            qseg, nseg, maxq = segs
+            self.attn(m, m, c, qkr, qkr.cols(c), DRef(vt, ld=mp), scale, s, y1, pre, segs=(qseg, qseg, nseg, maxq))
+            return
         if self.use_fused_attn(c, m, m, pre):
             # S = QK^T, softmax and P.V (+ residual) in one tcgen05 kernel (fis_attn)
             self.attn(m, m, c, qkr, qkr.cols(c), DRef(vt, ld=mp), scale, s, y1, pre)
@@ -384,15 +398,21 @@ class Engine(Launcher):
         self.softmax(m, m, _pad(m), DRef(S, ld=_pad(m)), scale, DRef(P, ld=_pad(m)))
         self.gemm(m, c, m, a=DRef(P, ld=_pad(m)), b=DRef(vt, ld=mp), d=y1, res=s, pre=pre)
 
-    def attn_cross(self, lid, m, x: DRef, out: DRef, level, tag, kv, pre=None, map_=None, ctrl=None):
-        """out = x + softmax(x Wq K_text^T * scale) V_text (sparse.py:303-338/352-361, unet.py:555-566)."""
+    def attn_cross(self, lid, m, x: DRef, out: DRef, level, tag, kv, pre=None, map_=None, ctrl=None, segs=None):
+        """out = x + softmax(x Wq K_text^T * scale) V_text (sparse.py:303-338/352-361, unet.py:555-566).
+
+        segs (batched requests): (q_seg, k_seg, nseg, max_q) -- each request's rows attend to its
+        own prompt's keys (stacked K / V^T of all requests)."""
         wq, _, _, scale = self.W.ca[lid]
         k, vt, v = kv[lid]
         c, nt = wq.shape[0], k.shape[0]
         ntp = vt.shape[1]
-        cap = self.hw(level)
+        cap = self.cap(level)
         q = self.scratch(f"q{tag}", (cap, c))
         self.gemm(m, c, c, a=x, b=DRef(wq), d=DRef(q), b_static=True)
+        if segs is not None:
+            self.attn(m, nt, c, DRef(q), DRef(k), DRef(vt), scale, x, out, pre, segs=segs)
+            return
         if ctrl is None and map_ is None and nt <= 128 and self.fused_xattn:
             # scores + softmax + P.V + residual in one launch (text context <= 128 tokens)
             a = L.XattnArgs(m, c, nt, DRef(q).ref(), DRef(k).ref(), DRef(v).ref(), scale, x.ref(), _r(pre),
@@ -422,21 +442,27 @@ class Engine(Launcher):
             return n_keys <= 128 and L.lib().fis_vm_attn_slice(m, n_keys, d, d) > 0
         return self.fused_attn
 
-    def attn(self, m, n_keys, d, q: DRef, k: DRef, vt: DRef, scale, res: DRef, out: DRef, pre=None):
+    def attn(self, m, n_keys, d, q: DRef, k: DRef, vt: DRef, scale, res: DRef, out: DRef, pre=None, segs=None):
+        if self.act != torch.bfloat16:
+            raise ContractViolation("fused attention (fis_attn) runs on bf16 operands only")
         a = L.AttnArgs(m, n_keys, d, d, q.ref(), k.ref(), vt.ref(), float(scale), _r(res), _r(pre), out.ref(),
                        L.ptr(self.step_dev))
+        if segs is not None:
+            qseg, kseg, nseg, maxq = segs
+            a.nseg, a.max_seg_q, a.q_seg, a.k_seg = nseg, maxq, L.ptr(qseg), L.ptr(kseg)
         self._call("fis_attn", a)
         self.launches += 1
 
-    def gn_stats(self, x: DRef, hw, c, mean: DRef, var: DRef):
-        a = L.GnStatsArgs(hw, c, self.groups, x.ref(), mean.ref(), var.ref(), L.ptr(self.step_dev))
+    def gn_stats(self, x: DRef, hw, c, mean: DRef, var: DRef, n_img=1):
+        a = L.GnStatsArgs(hw, c, self.groups, x.ref(), mean.ref(), var.ref(), L.ptr(self.step_dev), n_img)
         self._call("fis_gn_stats", a)
         self.launches += 1
 
     def gn_apply(self, lid, x: DRef, rows, c, mean: DRef, var: DRef, y_norm: DRef | None, y_silu: DRef | None,
-                 fused_stats: bool = False):
+                 fused_stats: bool = False, img_rows=0, row_img=None):
         gamma, beta = self.W.norm[lid]
         a = L.GnApplyArgs()
+        a.img_rows, a.row_img = img_rows, L.ptr(row_img)
         a.rows, a.c, a.groups, a.eps = rows, c, self.groups, NORM_EPS
         a.x, a.mean, a.var = x.ref(), mean.ref(), var.ref()
         a.gamma, a.beta = L.ptr(gamma), L.ptr(beta)
@@ -452,8 +478,10 @@ class Engine(Launcher):
         self._call("fis_pool2", a)
         self.launches += 1
 
-    def materialize(self, fv: FeatVal, out: DRef):
-        a = L.MaterializeArgs(fv.c, self.src(fv), out.ref(), L.ptr(self.step_dev))
+    def materialize(self, fv: FeatVal, out: DRef, n_img: int = 1):
+        src = self.src(fv)
+        src.h *= n_img  # stacked images: a per-pixel op over n_img * h * w pixels
+        a = L.MaterializeArgs(fv.c, src, out.ref(), L.ptr(self.step_dev))
         self._call("fis_materialize", a)
         self.launches += 1
 
@@ -474,6 +502,9 @@ class Engine(Launcher):
         """Launch one UNet forward + step update (unet.py:430-458,693) for the current device step."""
         vals = {}
         cfg = self.config
+        self.batch = plan.batch
+        if plan.batch > 1 and self.capture is not None:
+            raise ContractViolation("batched steps run as per-op graphs, not in the step VM")
         for ins in self.prog:
             op = ins[0]
             if op == "stem":
@@ -514,12 +545,23 @@ class Engine(Launcher):
     def _block(self, plan, blk, x: FeatVal, fo):
         """conv -> GN -> SiLU -> +self-attn -> +cross-attn (unet.py:452-458)."""
         level, c = fo.level, fo.channels
-        cap = self.hw(level)
+        cap = self.cap(level)
         rows, m = plan.rows(level)
         tag = f"L{level}"
         s = DRef(self.scratch(f"s{tag}", (cap, c)))
         nl = blk["norm"]
-        if plan.sparse(level):
+        if plan.batch > 1:
+            # stacked requests: GN statistics per image, so the norm runs after the conv
+            co = DRef(self.scratch(f"co{tag}", (cap, c)))
+            self._conv(plan, blk["conv"], [(x, False)], co, level)
+            mean, var = plan.stats(nl)
+            if plan.sparse(level):  # cached statistics of each row's request
+                self.gn_apply(nl, co, m, c, mean, var, None, s, row_img=plan.row_img(level))
+            else:
+                hw = self.hw(level)
+                self.gn_stats(co, hw, c, mean, var, n_img=plan.batch)
+                self.gn_apply(nl, co, m, c, mean, var, None, s, img_rows=hw)
+        elif plan.sparse(level):
             mean, var = plan.stats(nl)
             gamma, beta = self.W.norm[nl]
             self._conv(plan, blk["conv"], [(x, False)], s, level, epi=L.EPI_GN_SILU,
@@ -535,10 +577,12 @@ class Engine(Launcher):
                 self.gn_stats(co, cap, c, mean, var)
                 self.gn_apply(nl, co, cap, c, mean, var, plan.record(nl, 0), s)
         y1 = DRef(self.scratch(f"y1{tag}", (cap, c)))
-        self.attn_self(blk["self_attn"], m, s, y1, level, tag, pre=plan.record(blk["self_attn"], 0))
+        qs = plan.segments(level)
+        self.attn_self(blk["self_attn"], m, s, y1, level, tag, pre=plan.record(blk["self_attn"], 0), segs=qs)
         lid = blk["cross_attn"]
+        xs = None if qs is None else (qs[0], plan.key_segments(), qs[1], qs[2])
         self.attn_cross(lid, m, y1, plan.out_buf(fo), level, tag, plan.kv, pre=plan.record(lid, 0),
-                        map_=plan.record(lid, 3), ctrl=plan.ctrl(lid))
+                        map_=plan.record(lid, 3), ctrl=plan.ctrl(lid), segs=xs)
 
 
 # ---------------------------------------------------------------------------
@@ -553,28 +597,51 @@ class Arena:
     layers, all norm stats) for API-level `store.get` parity.
     """
 
-    def __init__(self, eng: Engine, n_text: int, full: bool):
+    def __init__(self, eng: Engine, n_text: int, full: bool, batch: int = 1):
+        """batch > 1: a stacked arena of `batch` generations (image r = rows [r*hw, (r+1)*hw) of
+        every level, statistics [T+1, batch, groups]); `view(r)` is generation r's arena."""
         cfg = eng.config
         T = cfg.steps
         dev, f32 = eng.dev, torch.float32
-        self.eng, self.n_text, self.full, self.T = eng, n_text, full, T
-        self.latent = torch.empty((T + 1, eng.hw(0), cfg.latent_channels), dtype=f32, device=dev)
+        if batch > 1 and full:
+            raise ContractViolation("a stacked arena records the engine roles only")
+        self.eng, self.n_text, self.full, self.T, self.batch = eng, n_text, full, T, batch
+        self.latent = torch.empty((T + 1, batch * eng.hw(0), cfg.latent_channels), dtype=f32, device=dev)
         self.feature = {}
         for key, f in eng.feats.items():
             if eng.gated[f.level]:
-                self.feature[key] = torch.empty((T + 1, eng.hw(f.level), f.channels), dtype=eng.act, device=dev)
+                self.feature[key] = torch.empty((T + 1, batch * eng.hw(f.level), f.channels), dtype=eng.act,
+                                                device=dev)
         self.stats = {}
         self.maps = {}
         self.outputs = {}
+        sshape = (T + 1, cfg.groups) if batch == 1 else (T + 1, batch, cfg.groups)
         for hl in eng.layers:
             i = hl.info
             if i.kind == "norm" and (i.gated or full):
-                self.stats[i.layer_id] = (torch.empty((T + 1, cfg.groups), dtype=f32, device=dev),
-                                          torch.empty((T + 1, cfg.groups), dtype=f32, device=dev))
-            if i.kind == "cross_attn":
+                self.stats[i.layer_id] = (torch.empty(sshape, dtype=f32, device=dev),
+                                          torch.empty(sshape, dtype=f32, device=dev))
+            if i.kind == "cross_attn" and batch == 1:  # stacked: each view owns its maps
                 self.maps[i.layer_id] = torch.empty((T + 1, eng.hw(i.level), n_text), dtype=f32, device=dev)
             if full:
                 self.outputs[i.layer_id] = torch.empty((T + 1, eng.hw(i.level), i.channels), dtype=f32, device=dev)
+
+    def view(self, r: int, n_text: int) -> "Arena":
+        """Arena of stacked generation r (prompt of n_text tokens): strided views of the stacked
+        slabs, own cross-attention maps."""
+        v = Arena.__new__(Arena)
+        v.eng, v.n_text, v.full, v.T, v.batch = self.eng, n_text, False, self.T, 1
+        v.stacked, v.index = self, r
+        hw = self.eng.hw
+        v.latent = self.latent[:, r * hw(0):(r + 1) * hw(0)]
+        v.feature = {k: t[:, r * hw(self.eng.feats[k].level):(r + 1) * hw(self.eng.feats[k].level)]
+                     for k, t in self.feature.items()}
+        v.stats = {k: (m[:, r], s[:, r]) for k, (m, s) in self.stats.items()}
+        v.maps = {i.layer_id: torch.empty((self.T + 1, hw(i.level), n_text), dtype=torch.float32,
+                                          device=self.eng.dev)
+                  for i in self.eng.info.values() if i.kind == "cross_attn"}
+        v.outputs = {}
+        return v
 
     def nbytes(self):
         ts = [self.latent, *self.feature.values(), *self.maps.values(), *self.outputs.values()]
@@ -589,6 +656,12 @@ class Arena:
 class StepPlan:
     """Dense plan: full maps at every level. Records into an arena when given."""
 
+    batch = 1  # stacked images per step
+
+    def segments(self, level):
+        """Attention query segments (q_seg, nseg, max_q) of stacked requests; None: one sequence."""
+        return None
+
     def __init__(self, eng: Engine, kv, latents: torch.Tensor, arena: Arena | None = None, ctrl=None):
         self.eng, self.kv, self.arena, self._ctrl = eng, kv, arena, ctrl
         self.latents = latents  # [T+1, HW, Cl] f32 slab: [t-1] in, [t] out
@@ -597,7 +670,7 @@ class StepPlan:
         return False
 
     def rows(self, level):
-        return None, self.eng.hw(level)
+        return None, self.eng.cap(level)
 
     def latent_in(self) -> FeatVal:
         return FeatVal(slab(self.latents, prev=True), 0, self.eng.config.latent_channels)
@@ -611,7 +684,7 @@ class StepPlan:
     def out_buf(self, f) -> DRef:
         if self.arena is not None and f.key in self.arena.feature:
             return slab(self.arena.feature[f.key])
-        return DRef(self.eng.scratch(f"feat{f.key}", (self.eng.hw(f.level), f.channels)))
+        return DRef(self.eng.scratch(f"feat{f.key}", (self.eng.cap(f.level), f.channels)))
 
     def value(self, f) -> FeatVal:
         return FeatVal(self.out_buf(f), f.level, f.channels)
@@ -632,8 +705,8 @@ class StepPlan:
             m, v = a.stats[nl]
             return slab(m), slab(v)
         g = self.eng.config.groups
-        return (DRef(self.eng.scratch(f"mean{nl}", (1, g), torch.float32)),
-                DRef(self.eng.scratch(f"var{nl}", (1, g), torch.float32)))
+        return (DRef(self.eng.scratch(f"mean{nl}", (self.batch, g), torch.float32)),
+                DRef(self.eng.scratch(f"var{nl}", (self.batch, g), torch.float32)))
 
     def ctrl(self, lid):
         if self._ctrl is None:
@@ -658,7 +731,7 @@ class SparsePlan(StepPlan):
         if self.sparse(level):
             r, _, n = self.lists[level]
             return r, n
-        return None, self.eng.hw(level)
+        return None, self.eng.cap(level)
 
     def latent_in(self) -> FeatVal:
         _, idx, _ = self.lists[0]
@@ -673,8 +746,8 @@ class SparsePlan(StepPlan):
 
     def out_buf(self, f) -> DRef:
         if self.sparse(f.level):
-            return DRef(self.eng.scratch(f"sfeat{f.key}", (self.eng.hw(f.level), f.channels)))
-        return DRef(self.eng.scratch(f"feat{f.key}", (self.eng.hw(f.level), f.channels)))
+            return DRef(self.eng.scratch(f"sfeat{f.key}", (self.eng.cap(f.level), f.channels)))
+        return DRef(self.eng.scratch(f"feat{f.key}", (self.eng.cap(f.level), f.channels)))
 
     def value(self, f) -> FeatVal:
         if self.sparse(f.level):
@@ -690,3 +763,30 @@ class SparsePlan(StepPlan):
             m, v = self.src_arena.stats[nl]
             return slab(m), slab(v)
         return super().stats(nl)
+
+
+class BatchedSparsePlan(SparsePlan):
+    """R edit requests stepped as one stacked batch (the per-GPU shard of requests).
+
+    Rows of all requests are concatenated per gated level (each request's run padded to a
+    multiple of 16 rows, so attention segments start 16-byte aligned); dense levels stack the
+    R full maps. Every GEMM of the step then runs once over all requests' rows, reading each
+    weight once per step for R requests. Attention is block-diagonal (each request's queries
+    see only its own rows / its own prompt's keys) and GroupNorm uses each image's statistics.
+    """
+
+    def __init__(self, eng: Engine, kv, arena: Arena, lists, lat_rows: torch.Tensor, qsegs, kseg, row_img):
+        super().__init__(eng, kv, arena, lists, lat_rows)
+        self.batch = arena.batch
+        self._qsegs = qsegs      # level -> (int32 [2R] device, R, max rows per request)
+        self._kseg = kseg        # int32 [2R] device: each request's text keys in the stacked K / V^T
+        self._row_img = row_img  # gated level -> int32 [rows] device: request of each compact row
+
+    def segments(self, level):
+        return self._qsegs[level]
+
+    def key_segments(self):
+        return self._kseg
+
+    def row_img(self, level):
+        return self._row_img[level]

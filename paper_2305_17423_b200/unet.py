@@ -23,7 +23,7 @@ import torch
 
 from . import _lib as L
 from .cache import CacheStore, Role
-from .engine import Arena, DRef, Engine, FeatVal, SparsePlan, StepPlan, slab
+from .engine import Arena, BatchedSparsePlan, DRef, Engine, FeatVal, SparsePlan, StepPlan, _pad, slab
 from .errors import CacheMissError, ConfigError, ContractViolation
 from .masks import BinaryMask, DevicePlan, run_detect
 from .model import (LayerInfo, UNetConfig, build_registry, embed_ids, initial_latent_np, lcs_pairs,
@@ -247,7 +247,7 @@ class _Runner:
         if not self.use_graph:
             eng.run_step(self.plan)
             return
-        if eng.use_vm:
+        if eng.use_vm and self.plan.batch == 1:
             if self.vm is None:
                 self.vm = eng.record_step(self.plan)
                 self.launches_per_step = 1
@@ -280,7 +280,7 @@ def _use_graphs():
 
 
 def generate_dense(prompt: PromptTokens, config: UNetConfig, store: CacheStore | None = None, *,
-                   record: str = "full", precision: str | None = None) -> np.ndarray:
+                   record: str = "full", precision: str | None = None, _arena: Arena | None = None) -> np.ndarray:
     """Dense generation; records the generation into an HBM arena bound to `store` (unet.py:680-696).
 
     record="full" keeps every reference role (LAYER_OUTPUT, NORM stats, maps, latents);
@@ -291,7 +291,10 @@ def generate_dense(prompt: PromptTokens, config: UNetConfig, store: CacheStore |
     kv = eng.text_kv(text)
     T = config.steps
     hw = eng.hw(0)
-    if store is not None:
+    if _arena is not None:  # a view of a stacked arena (generate_dense_batch)
+        arena = _arena
+        latents = arena.latent
+    elif store is not None:
         arena = Arena(eng, text.shape[0], full=(record == "full"))
         latents = arena.latent
     else:
@@ -477,3 +480,147 @@ from .modes import sparse_contexts as _sparse_contexts  # noqa: E402
 
 def _step_scale(config: UNetConfig):
     return step_scale(config)
+
+
+# ---------------------------------------------------------------------------
+# batched requests: R edits of one model stepped as one stacked batch
+# ---------------------------------------------------------------------------
+
+def generate_dense_batch(prompts, config: UNetConfig, stores, *, precision: str | None = None) -> list:
+    """Dense generations of R prompts recorded into ONE stacked arena (generation r = image r of
+    every slab), each bound to its CacheStore; `edit_batch` then steps their edits together.
+    Returns the R final latents (NCHW numpy), as R generate_dense calls would."""
+    if len(prompts) != len(stores) or not prompts:
+        raise ContractViolation("generate_dense_batch needs one store per prompt")
+    eng = get_engine(config, precision)
+    stacked = Arena(eng, 0, full=False, batch=len(prompts))
+    finals = []
+    for r, (p, st) in enumerate(zip(prompts, stores)):
+        view = stacked.view(r, len(p.ids))
+        finals.append(generate_dense(p, config, st, record="engine", precision=precision, _arena=view))
+    return finals
+
+
+def stack_text_kv(eng: Engine, kvs):
+    """Stack R prompts' text K [n, C] / V^T [C, n] per cross layer, each padded to a multiple of
+    16 keys (zeros), plus the key segments [2R] of each request."""
+    R = len(kvs)
+    lid0 = next(iter(kvs[0]))
+    nts = [kv[lid0][0].shape[0] for kv in kvs]
+    ks = _pad(max(nts))
+    out = {}
+    for lid in kvs[0]:
+        c = kvs[0][lid][0].shape[1]
+        K = torch.zeros((R * ks, c), dtype=eng.act, device=eng.dev)
+        VT = torch.zeros((c, R * ks), dtype=eng.act, device=eng.dev)
+        for r, kv in enumerate(kvs):
+            k, vt, _ = kv[lid]
+            K[r * ks: r * ks + nts[r]] = k
+            VT[:, r * ks: r * ks + nts[r]] = vt[:, :nts[r]]
+        out[lid] = (K, VT, None)
+    kseg = torch.tensor([v for r in range(R) for v in (r * ks, r * ks + nts[r])], dtype=torch.int32, device=eng.dev)
+    return out, kseg
+
+
+class BatchedEditPlan:
+    """Device plan of R edits over one stacked arena: per-request mask pyramids, concatenated
+    row lists (each request's run padded to 16 rows), stacked pixel->row maps, attention
+    segments and the BatchedSparsePlan that steps them as one batch."""
+
+    def __init__(self, eng: Engine, stacked: Arena, masks, kvs, lat0s):
+        cfg = eng.config
+        R = stacked.batch
+        if not (len(masks) == len(kvs) == len(lat0s) == R):
+            raise ContractViolation(f"need {R} masks / prompts / start latents for a {R}-request arena")
+        if eng.act != torch.bfloat16:
+            raise ContractViolation("batched edits run in bf16 (fused segment attention)")
+        dev, i32 = eng.dev, torch.int32
+        self.R = R
+        self.dps = [DevicePlan(torch.from_numpy(m.bits.astype(np.uint8).ravel()).to(dev), cfg.latent_h,
+                               cfg.latent_w, cfg.levels) for m in masks]
+        lists, qsegs, row_img = {}, {}, {}
+        for l in range(cfg.levels):
+            hw = eng.hw(l)
+            if not eng.gated[l]:
+                seg = [v for r in range(R) for v in (r * hw, (r + 1) * hw)]
+                qsegs[l] = (torch.tensor(seg, dtype=i32, device=dev), R, hw)
+                continue
+            rows, idx, seg, img = [], [], [], []
+            start = 0
+            for r, dp in enumerate(self.dps):
+                n = dp.n_active[l]
+                npad = _pad(n)
+                rr = dp.rows[l][:n] + r * hw
+                if npad > n:  # padding rows repeat a live row of the request (never read back)
+                    rr = torch.cat([rr, rr[:1].expand(npad - n)])
+                ii = dp.index[l]
+                idx.append(torch.where(ii >= 0, ii + start, ii))
+                rows.append(rr)
+                seg += [start, start + n]
+                img.append(torch.full((npad,), r, dtype=i32, device=dev))
+                start += npad
+            rows_t = torch.cat(rows).to(i32).contiguous() if start else torch.zeros(1, dtype=i32, device=dev)
+            lists[l] = (rows_t, torch.cat(idx).to(i32).contiguous(), start)
+            qsegs[l] = (torch.tensor(seg, dtype=i32, device=dev), R, max(1, max(dp.n_active[l] for dp in self.dps)))
+            row_img[l] = torch.cat(img).contiguous() if start else torch.zeros(1, dtype=i32, device=dev)
+        self.lists = lists
+        lat0 = torch.cat(list(lat0s), 0)
+        r0, _, n0 = lists[0]
+        self.lat_rows = lat0.index_select(0, r0[:n0].long()).contiguous()
+        kv, kseg = stack_text_kv(eng, kvs)
+        self.kv = kv
+        self.plan = BatchedSparsePlan(eng, kv, stacked, lists, self.lat_rows, qsegs, kseg, row_img)
+
+    def final_latents(self, eng: Engine, stacked: Arena) -> torch.Tensor:
+        """[R * hw, Cl] f32: fresh rows where masked, the cached generation elsewhere."""
+        cfg = eng.config
+        out = torch.empty((self.R * eng.hw(0), cfg.latent_channels), dtype=torch.float32, device=eng.dev)
+        fv = FeatVal(DRef(self.lat_rows), 0, cfg.latent_channels, self.lists[0][1], DRef(stacked.latent[cfg.steps]))
+        eng.step_dev.fill_(0)
+        eng.materialize(fv, DRef(out), n_img=self.R)
+        return out
+
+
+def edit_batch(sessions, config: UNetConfig) -> list:
+    """R edits whose stores come from one `generate_dense_batch`, stepped as ONE stacked batch.
+
+    Per request this matches `edit(session, config, session.store)` (unet.py:823-899) up to the
+    bf16 bound: masks (user or detected) and prompts are per request; all requests must share
+    the sparse phase's first step (same t2 with detection, or all user masks). Returns one
+    EditResult per session (MAC reports omitted: `macs` is None)."""
+    if not sessions:
+        return []
+    views = [s.store.arena for s in sessions]
+    stacked = getattr(views[0], "stacked", None)
+    if stacked is None or any(getattr(v, "stacked", None) is not stacked for v in views) or \
+            sorted(v.index for v in views) != list(range(stacked.batch)):
+        raise ContractViolation("edit_batch needs the stores of one generate_dense_batch, one session each")
+    order = sorted(range(len(sessions)), key=lambda i: views[i].index)
+    sessions = [sessions[i] for i in order]
+    outcomes = [detect_mask(s, config, s.store) for s in sessions]
+    starts = {1 if o.from_user_mask else s.t2 + 1 for s, o in zip(sessions, outcomes)}
+    if len(starts) != 1:
+        raise ContractViolation(f"batched edits must share the sparse phase's first step, got {sorted(starts)}")
+    start = starts.pop()
+    eng = get_engine(config, stacked.eng.precision)
+    cl, H, W, T = config.latent_channels, config.latent_h, config.latent_w, config.steps
+    masks, kvs, lat0s = [], [], []
+    for s, o, v in zip(sessions, outcomes, views):
+        s.mask = o.mask
+        # a no-edit request rides along with an empty mask: its latent stays the cached one
+        masks.append(o.mask if o.mask is not None else BinaryMask(np.zeros((H, W), dtype=bool)))
+        kvs.append(eng.text_kv(embed_tokens(s.new_tokens, config)))
+        if o.from_user_mask or o.mask is None:
+            lat0s.append(_to_nhwc(initial_latent_np(config), eng.dev))
+        else:
+            m = torch.from_numpy(o.mask.bits.ravel().copy()).to(eng.dev)[:, None]
+            lat0s.append(torch.where(m, o._control_dev, v.latent[s.t2]))
+    bp = BatchedEditPlan(eng, stacked, masks, kvs, lat0s)
+    _Runner(eng, bp.plan, _use_graphs()).run(start, T)
+    final = bp.final_latents(eng, stacked)
+    hw = eng.hw(0)
+    results = [None] * len(sessions)
+    for r, (s, o) in enumerate(zip(sessions, outcomes)):
+        lat = _to_nchw(final[r * hw:(r + 1) * hw], cl, H, W)
+        results[order[r]] = EditResult(lat, None, s.store.stats(), o.mask, o.no_edit, o.phase1_macs.total, 0)
+    return results

@@ -149,3 +149,53 @@ def test_fused_attention_vs_torch(env, m, nk, d):
     torch.cuda.synchronize()
     err = (out.float() - ref).abs().max().item()
     assert err <= 3e-2 * max(1.0, ref.abs().max().item()), err
+
+
+@pytest.mark.parametrize("d,qlens,klens,kpad", [
+    (320, [205, 410, 1024, 0, 37], None, 0),          # self-attention: keys = own rows
+    (640, [64, 300, 129], [77, 77, 77], 80),           # cross-attention: stacked prompts padded to 80
+    (1280, [256, 256, 256], None, 0)])
+def test_segment_attention_vs_torch(env, d, qlens, klens, kpad):
+    """fis_attn with ragged segments (batched requests): each query run attends to its own key run only."""
+    L, DRef, NULL, lz = env
+    g = torch.Generator(device="cuda").manual_seed(d + len(qlens))
+    bf = torch.bfloat16
+    starts = [0]
+    for n in qlens:  # runs padded to 16 rows like BatchedEditPlan
+        starts.append(starts[-1] + (n + 15) // 16 * 16)
+    m = starts[-1]
+    Q = torch.randn((m, d), device="cuda", generator=g).to(bf)
+    res = torch.randn((m, d), device="cuda", generator=g).to(bf)
+    if klens is None:  # self
+        K = torch.randn((m, d), device="cuda", generator=g).to(bf)
+        V = torch.randn((m, d), device="cuda", generator=g).to(bf)
+        kseg = [(starts[i], starts[i] + qlens[i]) for i in range(len(qlens))]
+    else:
+        nk = kpad * len(klens)
+        K = torch.randn((nk, d), device="cuda", generator=g).to(bf)
+        V = torch.randn((nk, d), device="cuda", generator=g).to(bf)
+        kseg = [(kpad * i, kpad * i + klens[i]) for i in range(len(klens))]
+    nk = K.shape[0]
+    ldv = (nk + 15) // 16 * 16
+    Vt = torch.zeros((d, ldv), device="cuda", dtype=bf)
+    Vt[:, :nk] = V.t()
+    qseg = [(starts[i], starts[i] + qlens[i]) for i in range(len(qlens))]
+    qs = torch.tensor([v for p in qseg for v in p], dtype=torch.int32, device="cuda")
+    ks = torch.tensor([v for p in kseg for v in p], dtype=torch.int32, device="cuda")
+    scale = 1.0 / math.sqrt(d)
+    out = torch.zeros((m, d), device="cuda", dtype=bf)
+    a = L.AttnArgs(m, nk, d, d, DRef(Q).ref(), DRef(K).ref(), DRef(Vt, ld=ldv).ref(), scale, DRef(res).ref(), NULL,
+                   DRef(out).ref(), None)
+    a.nseg, a.max_seg_q, a.q_seg, a.k_seg = len(qseg), max(1, max(qlens)), L.ptr(qs), L.ptr(ks)
+    L.call("fis_attn", a)
+    torch.cuda.synchronize()
+    for (q0, q1), (k0, k1) in zip(qseg, kseg):
+        if q1 == q0:
+            continue
+        P = torch.softmax(Q[q0:q1].float() @ K[k0:k1].float().t() * scale, dim=1)
+        ref = P @ V[k0:k1].float() + res[q0:q1].float()
+        err = (out[q0:q1].float() - ref).abs().max().item()
+        assert err <= 3e-2 * max(1.0, ref.abs().max().item()), (q0, q1, err)
+    # padding rows between runs are not written
+    for i in range(len(qlens)):
+        assert (out[qseg[i][1]:starts[i + 1]] == 0).all()
