@@ -122,9 +122,11 @@ class Launcher:
         self.launches = 0
         self._scratch = {}
         self.fused_xattn = False  # SIMT xattn is latency-bound; superseded by fis_attn
-        # tcgen05 fused attention (csrc/fis_attn.cu: TMA-fed, double-buffered S/P) instead of
-        # S GEMM -> softmax -> P.V GEMM (FIS_FUSED_ATTN=0 restores the three-launch path)
-        self.fused_attn = os.environ.get("FIS_FUSED_ATTN", "1") == "1"
+        # tcgen05 fused attention (csrc/fis_attn.cu) for single sequences: one CTA per 128 queries x
+        # value slice leaves most SMs idle at batch 1 (r01: 1.75 vs 1.58 ms sparse step, 4.39 vs
+        # 3.06 ms dense), so S GEMM -> softmax -> P.V GEMM stays the default there; stacked
+        # requests always use it (segments). FIS_FUSED_ATTN=1 forces it.
+        self.fused_attn = os.environ.get("FIS_FUSED_ATTN", "0") == "1"
         # gather lists (rows / pixel->row maps) are written once per edit, before any step runs
         # (DevicePlan syncs), so GEMMs may read them before the programmatic-launch wait
         self.static_meta = False
