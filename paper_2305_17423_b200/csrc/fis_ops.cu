@@ -16,6 +16,55 @@ __global__ void __launch_bounds__(256) gn_stats_kernel(const fis_gn_stats_args a
     const long long cnt = (long long)a.hw * cpg;
     const char* x = ref_base(a.x, t) + (long long)img * a.hw * a.x.ld * (a.x.dtype == FIS_BF16 ? 2 : 4);
     __shared__ double red[256];
+    if (a.x.dtype == FIS_BF16 && (cpg % 8) == 0 && (a.x.ld % 8) == 0 && (((uintptr_t)x) & 15) == 0) {
+        // bf16 activations (perf mode): 16-byte loads, fp32 per-thread partials, f64 block sums;
+        // still two-pass and in a fixed order (deterministic)
+        const int vpg = cpg / 8, items = a.hw * vpg;
+        const __nv_bfloat16* xb = (const __nv_bfloat16*)x + g * cpg;
+        float ps = 0.f;
+        for (int i = threadIdx.x; i < items; i += blockDim.x) {
+            const int q = i / vpg, v = i - q * vpg;
+            const uint4 u = *(const uint4*)(xb + (long long)q * a.x.ld + v * 8);
+            const __nv_bfloat162* h = (const __nv_bfloat162*)&u;
+#pragma unroll
+            for (int k = 0; k < 4; k++) {
+                const float2 f = __bfloat1622float2(h[k]);
+                ps += f.x + f.y;
+            }
+        }
+        red[threadIdx.x] = (double)ps;
+        __syncthreads();
+        for (int o = 128; o; o >>= 1) {
+            if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+            __syncthreads();
+        }
+        const double mean = red[0] / (double)cnt;
+        const float mf = (float)mean;
+        __syncthreads();
+        float pv = 0.f;
+        for (int i = threadIdx.x; i < items; i += blockDim.x) {
+            const int q = i / vpg, v = i - q * vpg;
+            const uint4 u = *(const uint4*)(xb + (long long)q * a.x.ld + v * 8);
+            const __nv_bfloat162* h = (const __nv_bfloat162*)&u;
+#pragma unroll
+            for (int k = 0; k < 4; k++) {
+                const float2 f = __bfloat1622float2(h[k]);
+                const float d0 = f.x - mf, d1 = f.y - mf;
+                pv = fmaf(d0, d0, fmaf(d1, d1, pv));
+            }
+        }
+        red[threadIdx.x] = (double)pv;
+        __syncthreads();
+        for (int o = 128; o; o >>= 1) {
+            if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) {
+            ((float*)ref_base(a.mean, t))[img * a.groups + g] = mf;
+            ((float*)ref_base(a.var, t))[img * a.groups + g] = (float)(red[0] / (double)cnt);
+        }
+        return;
+    }
     double s = 0.0;
     // thread = pixel (strided), inner loop over the group's contiguous channels (32-bit index math)
     for (int q = threadIdx.x; q < a.hw; q += blockDim.x) {
@@ -63,6 +112,35 @@ __global__ void gn_apply_kernel(const fis_gn_apply_args a) {
     const int cpg = a.c / a.groups;
     const int total = a.rows * a.c;
     const bool bf16_out = (!yn || a.y_norm.dtype == FIS_BF16) && (!ys || a.y_silu.dtype == FIS_BF16);
+    if (bf16_out && a.x.dtype == FIS_BF16 && (cpg % 8) == 0 && (a.x.ld % 8) == 0 && (!yn || (a.y_norm.ld % 8) == 0) &&
+        (!ys || (a.y_silu.ld % 8) == 0) && ((((uintptr_t)x) | ((uintptr_t)yn) | ((uintptr_t)ys)) & 15) == 0) {
+        // bf16 perf mode, 8 channels (one group) per thread: 16-byte loads / stores
+        const int cv = a.c / 8, totalv = a.rows * cv;
+        for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < totalv; e += gridDim.x * blockDim.x) {
+            const int r = e / cv, c = (e - r * cv) * 8;
+            const int xr = a.x_rows ? __ldg(a.x_rows + r) : r;
+            const int yr = a.y_rows ? __ldg(a.y_rows + r) : r;
+            const int g = (a.row_img ? __ldg(a.row_img + r) : (a.img_rows > 0 ? r / a.img_rows : 0)) * a.groups + c / cpg;
+            const float rstd = (float)(1.0 / sqrt((double)var[g] + (double)a.eps));
+            const float mu = mean[g];
+            const uint4 u = *(const uint4*)((const __nv_bfloat16*)x + (long long)xr * a.x.ld + c);
+            const __nv_bfloat162* h = (const __nv_bfloat162*)&u;
+            uint4 on, os;
+            __nv_bfloat162* hn = (__nv_bfloat162*)&on;
+            __nv_bfloat162* hs = (__nv_bfloat162*)&os;
+#pragma unroll
+            for (int k = 0; k < 4; k++) {
+                const float2 f = __bfloat1622float2(h[k]);
+                const float y0 = fmaf((f.x - mu) * rstd, __ldg(a.gamma + c + 2 * k), __ldg(a.beta + c + 2 * k));
+                const float y1 = fmaf((f.y - mu) * rstd, __ldg(a.gamma + c + 2 * k + 1), __ldg(a.beta + c + 2 * k + 1));
+                hn[k] = __floats2bfloat162_rn(y0, y1);
+                hs[k] = __floats2bfloat162_rn(__fdividef(y0, 1.0f + __expf(-y0)), __fdividef(y1, 1.0f + __expf(-y1)));
+            }
+            if (yn) *(uint4*)((__nv_bfloat16*)yn + (long long)yr * a.y_norm.ld + c) = on;
+            if (ys) *(uint4*)((__nv_bfloat16*)ys + (long long)yr * a.y_silu.ld + c) = os;
+        }
+        return;
+    }
     for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
         const int r = e / a.c, c = e - (e / a.c) * a.c;
         const int xr = a.x_rows ? __ldg(a.x_rows + r) : r;
