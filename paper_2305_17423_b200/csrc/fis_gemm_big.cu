@@ -24,6 +24,7 @@
 // 960 -> 240, 1280 -> 256), so no tile column is wasted.
 #include "fis_tc.cuh"
 #include "fis_tma.cuh"
+#include <cstdio>
 
 namespace fis {
 namespace big {
@@ -36,6 +37,7 @@ constexpr int A_BYTES = BM * BK * 2;     // 16 KB
 constexpr int SMEM_BUDGET = 200 * 1024;  // pipeline stages
 constexpr int MAX_STAGES = 8;
 constexpr int ACC_STRIDE = 256;          // TMEM column offset of accumulator 1
+constexpr int A_CPASYNC = 0, A_TMA_ROWS = 1, A_TMA_CONV = 2;  // how A tiles are staged
 constexpr int LAG = 2;  // cp.async stages in flight per A-producer thread
 constexpr int SEL_BYTES = BM * 19 * 4;  // select-on-read table [128][18] + row pixels [128]
 
@@ -62,6 +64,13 @@ FIS_DEV void tma2d(uint32_t dst, const void* tmap, int c0, int c1, uint64_t* bar
         "l"(tmap), "r"(c0), "r"(c1), "r"(smem_u32(bar))
         : "memory");
 }
+FIS_DEV void tma4d(uint32_t dst, const void* tmap, int c0, int c1, int c2, int c3, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], "
+        "[%6];" ::"r"(dst),
+        "l"(tmap), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar))
+        : "memory");
+}
 FIS_DEV void arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
 }
@@ -86,8 +95,39 @@ FIS_DEV unsigned long long gtime() {
     return t;
 }
 
+__device__ int* g_dbg_host = nullptr;
+// mbarrier wait with a watchdog (FIS_BIG_DBG & 16): report the stuck role and trap
+FIS_DEV void wait_dbg(uint64_t* b, uint32_t parity, int dbg, int role, int it) {
+    if (!(dbg & 16)) { mbar_wait(b, parity); return; }
+    if (g_dbg_host && threadIdx.x % 32 == 0) {  // heartbeat: last wait entered per (cta < 4, role)
+        if (blockIdx.x < 4) ((volatile int*)g_dbg_host)[8 * 4000 + blockIdx.x * 8 + role] = it + 1;
+    }
+    const unsigned long long t0 = gtime();
+    for (long long n = 0;; n++) {
+        uint32_t ok;
+        asm volatile(
+            "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(ok)
+            : "r"(smem_u32(b)), "r"(parity)
+            : "memory");
+        if (ok) return;
+        if ((n & 255) == 0 && gtime() - t0 > 2000000000ull && g_dbg_host) {
+            // report once per (cta, role) into host-mapped memory and keep waiting
+            volatile int* h = g_dbg_host + 8 * ((blockIdx.x * 8 + role) % 4096);
+            if (h[0] == 0) {
+                h[1] = blockIdx.x; h[2] = threadIdx.x; h[3] = role; h[4] = it; h[5] = (int)parity;
+                __threadfence_system();
+                h[0] = 1;
+                __threadfence_system();
+            }
+        }
+    }
+}
+
 __global__ void __launch_bounds__(THREADS, 1)
-    gemm_big_kernel(const fis_gemm_args a, const __grid_constant__ CUtensorMap tmap_b, int bn, int dbg) {
+    gemm_big_kernel(const fis_gemm_args a, const __grid_constant__ CUtensorMap tmap_b,
+                    const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_a2, int bn,
+                    int amode, int dbg) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     // align by pointer arithmetic on the shared array (keeps the shared address space: LDS/STS)
     unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -108,7 +148,7 @@ __global__ void __launch_bounds__(THREADS, 1)
 
     if (tid == 0) {
         for (int s = 0; s < L.stages; s++) {
-            mbar_init(full + s, A_WARPS * 32 + 1);
+            mbar_init(full + s, amode == A_CPASYNC ? A_WARPS * 32 + 1 : 1);
             mbar_init(empty + s, 1);
         }
         for (int b = 0; b < 2; b++) {
@@ -132,6 +172,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int t = cur_step(a.step);
 
     if (warp < A_WARPS) {
+        if (amode != A_CPASYNC) goto teardown;  // TMA stages A: these warps have no role
         // ------------------------------------------------------------ A producers
         // Row metadata: thread tid resolves tile row tid (pixel, and for CONV the select-on-read
         // decision of every tap) into shared tables. Loads: lane l copies 16-byte chunk l & 7 of
@@ -184,7 +225,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             }
             for (int kb = 0; kb < kblocks; kb++, it++) {
                 const int s = it % L.stages;
-                if (it >= L.stages) mbar_wait(empty + s, ((it / L.stages) & 1) ^ 1);
+                if (it >= L.stages) wait_dbg(empty + s, ((it / L.stages) & 1) ^ 1, dbg, 0, it);
                 if ((dbg & 4) && blockIdx.x == 0 && tid == 0 && it < 256) g_big_trace[0][it] = gtime();
                 const int k0 = kb * BK;
                 const uint32_t sa = sbase + s * L.stage;
@@ -238,16 +279,32 @@ __global__ void __launch_bounds__(THREADS, 1)
         // ------------------------------------------------------------ B producer (TMA)
         if (lane == 0) {
             const uint32_t sbase = smem_u32(smem);
-            const uint32_t bbytes = (uint32_t)(bn * BK * 2);
+            const uint32_t bbytes = (uint32_t)(bn * BK * 2) + (amode != A_CPASYNC ? A_BYTES : 0);
+            // TMA A geometry: 128 consecutive output pixels = a box of whole image rows (hw >= 128)
+            // or of whole images (hw < 128); 3x3 taps are shifted boxes, padding = TMA zero fill
+            const int ow = a.out_w, ohw = a.out_h * a.out_w;
+            const int cin0 = a.nsrc > 0 ? a.src[0].c : 0, cin = cin0 + (a.nsrc > 1 ? a.src[1].c : 0);
             int it = 0;
             for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-                const int n0 = (tile % tiles_n) * bn;
+                const int n0 = (tile % tiles_n) * bn, m0 = (tile / tiles_n) * BM;
+                const int img = amode == A_TMA_CONV ? m0 / ohw : 0;
+                const int y0 = amode == A_TMA_CONV && ohw >= BM ? (m0 - img * ohw) / ow : 0;
                 for (int kb = 0; kb < kblocks; kb++, it++) {
                     const int s = it % L.stages;
-                    if (it >= L.stages) mbar_wait(empty + s, ((it / L.stages) & 1) ^ 1);
+                    if (it >= L.stages) wait_dbg(empty + s, ((it / L.stages) & 1) ^ 1, dbg, 1, it);
                     if ((dbg & 4) && blockIdx.x == 0 && it < 256) g_big_trace[1][it] = gtime();
                     arrive_expect_tx(full + s, bbytes);
-                    tma2d(sbase + s * L.stage + A_BYTES, &tmap_b, kb * BK, n0, full + s);
+                    const uint32_t sa = sbase + s * L.stage;
+                    tma2d(sa + A_BYTES, &tmap_b, kb * BK, n0, full + s);
+                    if (amode == A_TMA_ROWS) {
+                        tma2d(sa, &tmap_a, kb * BK, m0, full + s);
+                    } else if (amode == A_TMA_CONV) {
+                        const int k0 = kb * BK, tap = k0 / cin;
+                        int c = k0 - tap * cin;
+                        const bool seg1 = c >= cin0;
+                        c -= seg1 ? cin0 : 0;
+                        tma4d(sa, seg1 ? &tmap_a2 : &tmap_a, c, tap % 3 - 1, y0 + tap / 3 - 1, img, full + s);
+                    }
                 }
             }
         }
@@ -259,12 +316,12 @@ __global__ void __launch_bounds__(THREADS, 1)
         int it = 0, lt = 0;
         for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, lt++) {
             const int buf = lt & 1;
-            if (lt >= 2) mbar_wait(acc_empty + buf, ((lt >> 1) & 1) ^ 1);  // epilogue drained this buffer
+            if (lt >= 2) wait_dbg(acc_empty + buf, ((lt >> 1) & 1) ^ 1, dbg, 2, lt);  // epilogue drained this buffer
             tc_fence_after();
             const uint32_t dt = tmem + buf * ACC_STRIDE;
             for (int kb = 0; kb < kblocks; kb++, it++) {
                 const int s = it % L.stages;
-                mbar_wait(full + s, (it / L.stages) & 1);
+                wait_dbg(full + s, (it / L.stages) & 1, dbg, 3, it);
                 tc_fence_after();
                 if ((dbg & 4) && blockIdx.x == 0 && lane == 0 && it < 256) g_big_trace[2][it] = gtime();
                 if (lane == 0) {
@@ -319,7 +376,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             }
             asm volatile("bar.sync 1, 128;" ::: "memory");
             const int buf = lt & 1;
-            mbar_wait(acc_full + buf, (lt >> 1) & 1);
+            wait_dbg(acc_full + buf, (lt >> 1) & 1, dbg, 4, lt);
             tc_fence_after();
             const uint32_t taddr = tmem + buf * ACC_STRIDE + ((uint32_t)(quarter * 32) << 16);
             const int r = m0 + lr;
@@ -345,6 +402,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             mbar_arrive(acc_empty + buf);
         }
     }
+teardown:
     tc_fence_before();
     __syncthreads();
     if (warp == MMA_WARP) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
@@ -408,13 +466,67 @@ int fis_gemm_big_eligible(const fis_gemm_args* a) {
     if (a->splits > 1 || a->n < 128 || a->b.step_stride != 0) return 0;
     const int bn = fis_gemm_big_bn(a->n);
     const long long tiles = (long long)((a->m + 127) / 128) * ((a->n + bn - 1) / bn);
-    return tiles >= sms() ? 1 : 0;
+    static long long min_tiles = getenv("FIS_BIG_MIN_TILES") ? atoll(getenv("FIS_BIG_MIN_TILES")) : -1;
+    return tiles >= (min_tiles >= 0 ? min_tiles : sms()) ? 1 : 0;
+}
+
+// 4-D bf16 map of a dense stacked source [img][h][w][c] (pixel stride ld), box {64, w, bh, bi}
+// covering 128 consecutive pixels.
+static bool encode_conv4(CUtensorMap* out, const fis_src& s, long long images) {
+    const int hw = s.h * s.w;
+    int bh, bi;
+    if (hw >= 128) {
+        if (128 % s.w || hw % 128) return false;
+        bh = 128 / s.w;
+        bi = 1;
+    } else {
+        if (128 % hw) return false;
+        bh = s.h;
+        bi = 128 / hw;
+    }
+    if (s.w > 256 || bh > 256 || (((uintptr_t)s.fresh.ptr) & 15) || (s.fresh.ld % 8) || s.fresh.ld < s.c) return false;
+    EncodeTiledFn enc = encode_fn();
+    if (!enc) return false;
+    const long long rb = s.fresh.ld * 2;
+    cuuint64_t dims[4] = {(cuuint64_t)s.c, (cuuint64_t)s.w, (cuuint64_t)s.h, (cuuint64_t)images};
+    cuuint64_t strides[3] = {(cuuint64_t)rb, (cuuint64_t)(rb * s.w), (cuuint64_t)(rb * hw)};
+    cuuint32_t box[4] = {64u, (cuuint32_t)s.w, (cuuint32_t)bh, (cuuint32_t)bi};
+    cuuint32_t es[4] = {1u, 1u, 1u, 1u};
+    return enc(out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(s.fresh.ptr), dims, strides, box, es,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// TMA staging of A when every source is a plain bf16 matrix without per-step stride: contiguous
+// rows (ROWS, no row list) or dense 3x3 conv sources at the output resolution (no select-on-read,
+// no upsampling, no row list).
+static int choose_amode(const fis_gemm_args* a, CUtensorMap* ta, CUtensorMap* ta2) {
+    static int off = getenv("FIS_BIG_TMA_A") && getenv("FIS_BIG_TMA_A")[0] == '0';
+    if (off || a->rows) return fis::big::A_CPASYNC;
+    if (a->a_mode == FIS_A_ROWS) {
+        if (a->a.step_stride || a->a.dtype != FIS_BF16) return fis::big::A_CPASYNC;
+        return encode_2d(ta, a->a.ptr, a->m, a->k, a->a.ld, 128) ? fis::big::A_TMA_ROWS : fis::big::A_CPASYNC;
+    }
+    const int hw = a->out_h * a->out_w;
+    if (hw <= 0 || a->m % hw) return fis::big::A_CPASYNC;
+    for (int i = 0; i < a->nsrc; i++) {
+        const fis_src& s = a->src[i];
+        if (s.index || s.up || s.fresh.step_stride || s.fresh.dtype != FIS_BF16 || s.h != a->out_h || s.w != a->out_w)
+            return fis::big::A_CPASYNC;
+        if (!encode_conv4(i ? ta2 : ta, s, a->m / hw)) return fis::big::A_CPASYNC;
+    }
+    if (a->nsrc < 2) *ta2 = *ta;
+    return fis::big::A_TMA_CONV;
 }
 
 int fis_gemm_big_launch(const fis_gemm_args* a, cudaStream_t stream) {
     const int bn = fis_gemm_big_bn(a->n);
     const CUtensorMap* tm = weight_map(a->b.ptr, a->n, a->k, a->b.ld, bn);
     if (!tm) return FIS_ERR_UNSUPPORTED;
+    CUtensorMap ta, ta2;
+    std::memset(&ta, 0, sizeof(ta));
+    std::memset(&ta2, 0, sizeof(ta2));
+    const int amode = choose_amode(a, &ta, &ta2);
     const fis::big::Layout L = fis::big::layout(bn);
     static int configured_smem = 0;
     if (configured_smem < L.total) {
@@ -436,11 +548,15 @@ int fis_gemm_big_launch(const fis_gemm_args* a, cudaStream_t stream) {
     cfg.attrs = attr;
     cfg.numAttrs = fis_pdl_enabled() ? 1 : 0;
     static int dbg = getenv("FIS_BIG_DBG") ? atoi(getenv("FIS_BIG_DBG")) : 0;  // 1: no stores, 2: no A loads
-    return cudaLaunchKernelEx(&cfg, fis::big::gemm_big_kernel, *a, *tm, bn, dbg) == cudaSuccess ? FIS_OK
-                                                                                              : FIS_ERR_LAUNCH;
+    return cudaLaunchKernelEx(&cfg, fis::big::gemm_big_kernel, *a, *tm, ta, ta2, bn, amode, dbg) == cudaSuccess
+               ? FIS_OK : FIS_ERR_LAUNCH;
 }
 
 extern "C" int fis_big_trace_read(unsigned long long* out768) {
     return cudaMemcpyFromSymbol(out768, fis::big::g_big_trace, sizeof(fis::big::g_big_trace)) == cudaSuccess
                ? FIS_OK : FIS_ERR_LAUNCH;
+}
+
+extern "C" int fis_big_debug_buf(int* host_mapped) {
+    return cudaMemcpyToSymbol(fis::big::g_dbg_host, &host_mapped, sizeof(int*)) == cudaSuccess ? FIS_OK : FIS_ERR_LAUNCH;
 }

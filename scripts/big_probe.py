@@ -87,6 +87,14 @@ def rows_gemm(m, n, k):
     return d
 
 
+if len(sys.argv) > 1 and sys.argv[1] == "medium":
+    for (m, n, k) in [(256, 256, 512), (256, 256, 1024), (1024, 1024, 1024), (4096, 3840, 1280)]:
+        rows_gemm(m, n, k)
+    sys.exit(0)
+if len(sys.argv) > 1 and sys.argv[1] == "small":
+    rows_gemm(256, 256, 128)
+    conv_dense(2, 16, 16, 64, 128)
+    sys.exit(0)
 if len(sys.argv) > 1 and sys.argv[1] == "quick":
     rows_gemm(4096, 3840, 1280)
     conv_dense(32, 16, 16, 1280, 1280)

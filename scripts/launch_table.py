@@ -1,0 +1,36 @@
+"""Join an ncu launch list (gpu__time_duration CSV) with prof_batch.py's launch sequence.
+
+    python scripts/launch_table.py gpurun_out/batch_launches.csv gpurun_out/batch_seq.txt
+"""
+import csv
+import json
+import re
+import sys
+from collections import defaultdict
+
+
+def main(csv_path, seq_path, top=30):
+    rows = list(csv.reader(open(csv_path)))
+    hdr, ks = None, []
+    for r in rows:
+        if r and r[0] == "ID":
+            hdr = r
+            continue
+        if hdr and len(r) == len(hdr):
+            d = dict(zip(hdr, r))
+            if d["Metric Name"] == "gpu__time_duration.sum":
+                ks.append((d["Kernel Name"], float(d["Metric Value"].replace(",", ""))))
+    seq = [json.loads(l.split(" ", 1)[1]) for l in open(seq_path) if re.match(r"^\d+ \{", l)]
+    agg, cnt = defaultdict(float), defaultdict(int)
+    for (kn, t), s in zip(ks, seq):
+        key = s["op"] + (f" n={s['n']} k={s['k']}" if s["op"] == "fis_gemm" else "") + f" m={s.get('m', s.get('rows'))}"
+        agg[key] += t
+        cnt[key] += 1
+    tot = sum(t for _, t in ks)
+    print(f"{len(ks)} launches, {len(seq)} ops, total {tot / 1e3:.1f} us")
+    for k, v in sorted(agg.items(), key=lambda x: -x[1])[:top]:
+        print(f"{v / 1e3:8.1f} us  {100 * v / tot:5.1f}%  x{cnt[k]:<3d} {k}")
+
+
+if __name__ == "__main__":
+    main(*sys.argv[1:3])
