@@ -37,7 +37,14 @@ constexpr int A_BYTES = BM * BK * 2;     // 16 KB
 constexpr int SMEM_BUDGET = 200 * 1024;  // pipeline stages
 constexpr int MAX_STAGES = 8;
 constexpr int ACC_STRIDE = 256;          // TMEM column offset of accumulator 1
-constexpr int A_CPASYNC = 0, A_TMA_ROWS = 1, A_TMA_CONV = 2;  // how A tiles are staged
+constexpr int A_CPASYNC = 0, A_TMA_ROWS = 1, A_TMA_CONV = 2, A_TMA_GATHER = 3;  // how A tiles are staged
+
+// TMA gather4 sources of a sparse conv: per segment a fresh-row map and a cache-pixel map (2-D, box
+// {64, 1}); row coordinate = t * rows_per_step + row.
+struct GatherMaps {
+    CUtensorMap fresh[2], cache[2];
+    int fresh_rps[2], cache_rps[2];
+};
 constexpr int LAG = 2;  // cp.async stages in flight per A-producer thread
 constexpr int SEL_BYTES = BM * 19 * 4;  // select-on-read table [128][18] + row pixels [128]
 
@@ -69,6 +76,13 @@ FIS_DEV void tma4d(uint32_t dst, const void* tmap, int c0, int c1, int c2, int c
         "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], "
         "[%6];" ::"r"(dst),
         "l"(tmap), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar))
+        : "memory");
+}
+FIS_DEV void tma_gather4(uint32_t dst, const void* tmap, int c, int r0, int r1, int r2, int r3, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, "
+        "%4, %5, %6}], [%7];" ::"r"(dst),
+        "l"(tmap), "r"(c), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(smem_u32(bar))
         : "memory");
 }
 FIS_DEV void arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
@@ -126,8 +140,8 @@ FIS_DEV void wait_dbg(uint64_t* b, uint32_t parity, int dbg, int role, int it) {
 
 __global__ void __launch_bounds__(THREADS, 1)
     gemm_big_kernel(const fis_gemm_args a, const __grid_constant__ CUtensorMap tmap_b,
-                    const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_a2, int bn,
-                    int amode, int dbg) {
+                    const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_a2,
+                    const __grid_constant__ GatherMaps gm, int bn, int amode, int dbg) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     // align by pointer arithmetic on the shared array (keeps the shared address space: LDS/STS)
     unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -145,10 +159,12 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int tiles_n = (a.n + bn - 1) / bn, tiles_m = (a.m + BM - 1) / BM;
     const int ntiles = tiles_m * tiles_n;
     const int kblocks = (a.k + BK - 1) / BK;
+    // tile width bn <= 512: nsub MMAs of bns columns per K block; two TMEM accumulators when they fit
+    const int nsub = bn > 256 ? 2 : 1, bns = bn / nsub, nbuf = 2 * bn <= 512 ? 2 : 1;
 
     if (tid == 0) {
         for (int s = 0; s < L.stages; s++) {
-            mbar_init(full + s, amode == A_CPASYNC ? A_WARPS * 32 + 1 : 1);
+            mbar_init(full + s, amode == A_CPASYNC ? A_WARPS * 32 + 1 : amode == A_TMA_GATHER ? A_WARPS * 8 + 1 : 1);
             mbar_init(empty + s, 1);
         }
         for (int b = 0; b < 2; b++) {
@@ -172,7 +188,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int t = cur_step(a.step);
 
     if (warp < A_WARPS) {
-        if (amode != A_CPASYNC) goto teardown;  // TMA stages A: these warps have no role
+        if (amode != A_CPASYNC && amode != A_TMA_GATHER) goto teardown;  // TMA stages A: no role here
         // ------------------------------------------------------------ A producers
         // Row metadata: thread tid resolves tile row tid (pixel, and for CONV the select-on-read
         // decision of every tap) into shared tables. Loads: lane l copies 16-byte chunk l & 7 of
@@ -213,6 +229,58 @@ __global__ void __launch_bounds__(THREADS, 1)
                     }
                 }
                 __syncwarp();
+            }
+            if (amode == A_TMA_GATHER) {
+                // lanes 0-7 of each warp own 4-row groups: one TMA gather4 per group and K block when
+                // the 4 rows come from one source (fresh rows / cached pixels, zero padding = OOB
+                // row); a group mixing both sources is copied with cp.async (mask borders only)
+                const int g0 = 4 * (warp * 8 + lane);
+                for (int kb = 0; kb < kblocks; kb++, it++) {
+                    const int s = it % L.stages;
+                    if (it >= L.stages) wait_dbg(empty + s, ((it / L.stages) & 1) ^ 1, dbg, 0, it);
+                    if ((dbg & 4) && blockIdx.x == 0 && tid == 0 && it < 256) g_big_trace[0][it] = gtime();
+                    if (lane < 8) {
+                        const int k0 = kb * BK, tap = k0 / cin;
+                        int c = k0 - tap * cin;
+                        const int seg = c >= src0c ? 1 : 0;
+                        c -= seg ? src0c : 0;
+                        int v[4], nf = 0, nc = 0;
+#pragma unroll
+                        for (int i = 0; i < 4; i++) {
+                            v[i] = seltab[(g0 + i) * 18 + seg * 9 + tap];
+                            nf += v[i] >= 0;
+                            nc += v[i] <= -2 && v[i] != SEL_ZERO;
+                        }
+                        const uint32_t dst = sbase + s * L.stage + g0 * 128;
+                        if (nc == 0 || nf == 0) {
+                            const bool fr = nc == 0;
+                            const int base = t * (fr ? gm.fresh_rps[seg] : gm.cache_rps[seg]);
+                            int rr[4];
+#pragma unroll
+                            for (int i = 0; i < 4; i++)
+                                rr[i] = v[i] == SEL_ZERO ? -1 : base + (fr ? v[i] : -2 - v[i]);
+                            arrive_expect_tx(full + s, 4 * 128);
+                            tma_gather4(dst, fr ? (seg ? &gm.fresh[1] : &gm.fresh[0]) : (seg ? &gm.cache[1] : &gm.cache[0]),
+                                        c, rr[0], rr[1], rr[2], rr[3], full + s);
+                        } else {
+                            const char* fb = (seg ? f1 : f0) + c * 2;
+                            const char* cb = (seg ? c1p : c0p) + c * 2;
+                            const long long ldf = (seg ? ldf1 : ldf0) * 2, ldc = (seg ? ldc1 : ldc0) * 2;
+#pragma unroll
+                            for (int i = 0; i < 4; i++) {
+                                const char* src = v[i] == SEL_ZERO ? nullptr
+                                                  : v[i] >= 0      ? fb + (long long)v[i] * ldf
+                                                                   : cb + (long long)(-2 - v[i]) * ldc;
+#pragma unroll
+                                for (int q = 0; q < 8; q++)
+                                    cp_async16(sbase + s * L.stage + sw128_off(g0 + i, q),
+                                               src ? (const void*)(src + q * 16) : (const void*)dummy, src != nullptr);
+                            }
+                            cp_async_arrive_noinc(full + s);
+                        }
+                    }
+                }
+                continue;
             }
             // rows mode: this thread's 8 row pointers for the whole tile
             const char* rp[8];
@@ -270,7 +338,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                 }
             }
         }
-        if (!(dbg & 8)) {  // drain: publish the last LAG stages
+        if (!(dbg & 8) && amode == A_CPASYNC) {  // drain: publish the last LAG stages
             cp_wait<0>();
             fence_async_smem();
             for (int q = it - LAG < 0 ? 0 : it - LAG; q < it; q++) mbar_arrive(full + q % L.stages);
@@ -279,7 +347,9 @@ __global__ void __launch_bounds__(THREADS, 1)
         // ------------------------------------------------------------ B producer (TMA)
         if (lane == 0) {
             const uint32_t sbase = smem_u32(smem);
-            const uint32_t bbytes = (uint32_t)(bn * BK * 2) + (amode != A_CPASYNC ? A_BYTES : 0);
+            // A bytes are expected here only when this thread also issues the A tile (rows / dense conv);
+            // gather lanes expect their own 4-row bytes
+            const uint32_t bbytes = (uint32_t)(bn * BK * 2) + (amode == A_TMA_ROWS || amode == A_TMA_CONV ? A_BYTES : 0);
             // TMA A geometry: 128 consecutive output pixels = a box of whole image rows (hw >= 128)
             // or of whole images (hw < 128); 3x3 taps are shifted boxes, padding = TMA zero fill
             const int ow = a.out_w, ohw = a.out_h * a.out_w;
@@ -295,7 +365,8 @@ __global__ void __launch_bounds__(THREADS, 1)
                     if ((dbg & 4) && blockIdx.x == 0 && it < 256) g_big_trace[1][it] = gtime();
                     arrive_expect_tx(full + s, bbytes);
                     const uint32_t sa = sbase + s * L.stage;
-                    tma2d(sa + A_BYTES, &tmap_b, kb * BK, n0, full + s);
+                    for (int j = 0; j < nsub; j++)
+                        tma2d(sa + A_BYTES + j * bns * 128, &tmap_b, kb * BK, n0 + j * bns, full + s);
                     if (amode == A_TMA_ROWS) {
                         tma2d(sa, &tmap_a, kb * BK, m0, full + s);
                     } else if (amode == A_TMA_CONV) {
@@ -310,13 +381,13 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
     } else if (warp == MMA_WARP) {
         // ------------------------------------------------------------ MMA issuer
-        const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(bn >> 3) << 17) |
+        const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(bns >> 3) << 17) |
                                ((uint32_t)(BM >> 4) << 24);
         const uint32_t sbase = smem_u32(smem);
         int it = 0, lt = 0;
         for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, lt++) {
-            const int buf = lt & 1;
-            if (lt >= 2) wait_dbg(acc_empty + buf, ((lt >> 1) & 1) ^ 1, dbg, 2, lt);  // epilogue drained this buffer
+            const int buf = lt % nbuf, use = lt / nbuf;
+            if (use >= 1) wait_dbg(acc_empty + buf, (use & 1) ^ 1, dbg, 2, lt);  // epilogue drained this buffer
             tc_fence_after();
             const uint32_t dt = tmem + buf * ACC_STRIDE;
             for (int kb = 0; kb < kblocks; kb++, it++) {
@@ -326,14 +397,16 @@ __global__ void __launch_bounds__(THREADS, 1)
                 if ((dbg & 4) && blockIdx.x == 0 && lane == 0 && it < 256) g_big_trace[2][it] = gtime();
                 if (lane == 0) {
                     const uint32_t sa = sbase + s * L.stage, sb = sa + A_BYTES;
+                    for (int j = 0; j < nsub; j++) {  // tiles wider than 256: one MMA per 128 x bns half
 #pragma unroll
-                    for (int kk = 0; kk < BK / 16; kk++) {
-                        const uint64_t ad = sw128_desc(sa + kk * 32), bd = sw128_desc(sb + kk * 32);
-                        const uint32_t acc = (kb > 0 || kk > 0) ? 1u : 0u;
-                        asm volatile(
-                            "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-                            "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(dt),
-                            "l"(ad), "l"(bd), "r"(idesc), "r"(acc));
+                        for (int kk = 0; kk < BK / 16; kk++) {
+                            const uint64_t ad = sw128_desc(sa + kk * 32), bd = sw128_desc(sb + j * bns * 128 + kk * 32);
+                            const uint32_t acc = (kb > 0 || kk > 0) ? 1u : 0u;
+                            asm volatile(
+                                "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+                                "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(dt + j * bns),
+                                "l"(ad), "l"(bd), "r"(idesc), "r"(acc));
+                        }
                     }
                     mma_commit(empty + s);
                     if (kb == kblocks - 1) mma_commit(acc_full + buf);
@@ -375,8 +448,8 @@ __global__ void __launch_bounds__(THREADS, 1)
                 }
             }
             asm volatile("bar.sync 1, 128;" ::: "memory");
-            const int buf = lt & 1;
-            wait_dbg(acc_full + buf, (lt >> 1) & 1, dbg, 4, lt);
+            const int buf = lt % nbuf;
+            wait_dbg(acc_full + buf, (lt / nbuf) & 1, dbg, 4, lt);
             tc_fence_after();
             const uint32_t taddr = tmem + buf * ACC_STRIDE + ((uint32_t)(quarter * 32) << 16);
             const int r = m0 + lr;
@@ -459,15 +532,22 @@ int fis_gemm_big_bn(int n) {
     return 256;
 }
 
+static bool tma_a_ok(const fis_gemm_args* a);
+static bool gather_ok(const fis_gemm_args* a);
+
 // The persistent kernel takes GEMMs whose tile count fills the SMs (stacked requests): bf16 A
-// (gathered rows or 3x3 conv), static bf16 weights addressable by TMA, no split-K.
+// (gathered rows or 3x3 conv), static bf16 weights addressable by TMA, no split-K. With TMA-staged
+// A (dense maps / contiguous rows) it beats the per-op kernel from ~40 tiles on.
 int fis_gemm_big_eligible(const fis_gemm_args* a) {
     if (getenv("FIS_BIG") && getenv("FIS_BIG")[0] == '0') return 0;
     if (a->splits > 1 || a->n < 128 || a->b.step_stride != 0) return 0;
     const int bn = fis_gemm_big_bn(a->n);
     const long long tiles = (long long)((a->m + 127) / 128) * ((a->n + bn - 1) / bn);
     static long long min_tiles = getenv("FIS_BIG_MIN_TILES") ? atoll(getenv("FIS_BIG_MIN_TILES")) : -1;
-    return tiles >= (min_tiles >= 0 ? min_tiles : sms()) ? 1 : 0;
+    if (min_tiles >= 0) return tiles >= min_tiles ? 1 : 0;
+    // gathered (cp.async) A: the per-op kernel's 2-threads-per-row gather is as fast (r01 probe)
+    if (tiles >= 40 && tma_a_ok(a)) return 1;
+    return tiles >= 100 && gather_ok(a) ? 1 : 0;  // TMA gather4 pays off from ~100 tiles (r01 probe)
 }
 
 // 4-D bf16 map of a dense stacked source [img][h][w][c] (pixel stride ld), box {64, w, bh, bi}
@@ -497,12 +577,32 @@ static bool encode_conv4(CUtensorMap* out, const fis_src& s, long long images) {
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+static bool conv_box_ok(const fis_src& s) {
+    const int hw = s.h * s.w;
+    if (hw >= 128) return 128 % s.w == 0 && hw % 128 == 0 && s.w <= 256;
+    return 128 % hw == 0;
+}
+
+static bool tma_a_ok(const fis_gemm_args* a) {
+    static int off = getenv("FIS_BIG_TMA_A") && getenv("FIS_BIG_TMA_A")[0] == '0';
+    if (off || a->rows) return false;
+    if (a->a_mode == FIS_A_ROWS) return !a->a.step_stride && a->a.dtype == FIS_BF16 && (a->a.ld % 8) == 0;
+    const int hw = a->out_h * a->out_w;
+    if (hw <= 0 || a->m % hw) return false;
+    for (int i = 0; i < a->nsrc; i++) {
+        const fis_src& s = a->src[i];
+        if (s.index || s.up || s.fresh.step_stride || s.fresh.dtype != FIS_BF16 || s.h != a->out_h ||
+            s.w != a->out_w || !conv_box_ok(s) || (s.fresh.ld % 8))
+            return false;
+    }
+    return true;
+}
+
 // TMA staging of A when every source is a plain bf16 matrix without per-step stride: contiguous
 // rows (ROWS, no row list) or dense 3x3 conv sources at the output resolution (no select-on-read,
 // no upsampling, no row list).
 static int choose_amode(const fis_gemm_args* a, CUtensorMap* ta, CUtensorMap* ta2) {
-    static int off = getenv("FIS_BIG_TMA_A") && getenv("FIS_BIG_TMA_A")[0] == '0';
-    if (off || a->rows) return fis::big::A_CPASYNC;
+    if (!tma_a_ok(a)) return fis::big::A_CPASYNC;
     if (a->a_mode == FIS_A_ROWS) {
         if (a->a.step_stride || a->a.dtype != FIS_BF16) return fis::big::A_CPASYNC;
         return encode_2d(ta, a->a.ptr, a->m, a->k, a->a.ld, 128) ? fis::big::A_TMA_ROWS : fis::big::A_CPASYNC;
@@ -519,14 +619,72 @@ static int choose_amode(const fis_gemm_args* a, CUtensorMap* ta, CUtensorMap* ta
     return fis::big::A_TMA_CONV;
 }
 
+// Sparse convs (select-on-read over compact fresh rows + the cached slab): TMA gather4 per source.
+static bool gather_ok(const fis_gemm_args* a) {
+    static int off = getenv("FIS_BIG_GATHER") && getenv("FIS_BIG_GATHER")[0] == '0';
+    if (off || a->a_mode != FIS_A_CONV3X3) return false;
+    for (int i = 0; i < a->nsrc; i++) {
+        const fis_src& s = a->src[i];
+        if (s.fresh.dtype != FIS_BF16 || (s.fresh.ld % 8) || (((uintptr_t)s.fresh.ptr) & 15) ||
+            (s.fresh.step_stride % (s.fresh.ld * 2)))
+            return false;
+        if (s.index && (s.cache.dtype != FIS_BF16 || (s.cache.ld % 8) || (((uintptr_t)s.cache.ptr) & 15) ||
+                        (s.cache.step_stride % (s.cache.ld * 2))))
+            return false;
+    }
+    return true;
+}
+
+static bool encode_gather(const fis_gemm_args* a, fis::big::GatherMaps* gm) {
+    const long long huge = 1ll << 30;
+    for (int i = 0; i < a->nsrc; i++) {
+        const fis_src& s = a->src[i];
+        if (!encode_2d(&gm->fresh[i], s.fresh.ptr, huge, s.c, s.fresh.ld, 1)) return false;
+        gm->fresh_rps[i] = (int)(s.fresh.step_stride / (s.fresh.ld * 2));
+        if (s.index) {
+            if (!encode_2d(&gm->cache[i], s.cache.ptr, huge, s.c, s.cache.ld, 1)) return false;
+            gm->cache_rps[i] = (int)(s.cache.step_stride / (s.cache.ld * 2));
+        } else {
+            gm->cache[i] = gm->fresh[i];
+            gm->cache_rps[i] = gm->fresh_rps[i];
+        }
+    }
+    if (a->nsrc < 2) {
+        gm->fresh[1] = gm->fresh[0];
+        gm->cache[1] = gm->cache[0];
+        gm->fresh_rps[1] = gm->fresh_rps[0];
+        gm->cache_rps[1] = gm->cache_rps[0];
+    }
+    return true;
+}
+
+// Gathered A is the expensive operand: one tile covers up to 512 output columns (two MMAs per K
+// block, single accumulator) so each gathered row is loaded once per 320-512 columns.
+static int wide_bn(int n) {
+    static int off = getenv("FIS_BIG_WIDE") && getenv("FIS_BIG_WIDE")[0] == '0';
+    if (off) return 0;
+    for (int bn = 512; bn > 256; bn -= 32)
+        if (n % bn == 0 && (bn / 2) % 16 == 0) return bn;
+    return 0;
+}
+
 int fis_gemm_big_launch(const fis_gemm_args* a, cudaStream_t stream) {
-    const int bn = fis_gemm_big_bn(a->n);
-    const CUtensorMap* tm = weight_map(a->b.ptr, a->n, a->k, a->b.ld, bn);
-    if (!tm) return FIS_ERR_UNSUPPORTED;
     CUtensorMap ta, ta2;
     std::memset(&ta, 0, sizeof(ta));
     std::memset(&ta2, 0, sizeof(ta2));
-    const int amode = choose_amode(a, &ta, &ta2);
+    int amode = choose_amode(a, &ta, &ta2);
+    static fis::big::GatherMaps gm;  // kernel parameter copy; static keeps it off the stack
+    std::memset(&gm, 0, sizeof(gm));
+    static int gmode = getenv("FIS_BIG_GATHER") ? atoi(getenv("FIS_BIG_GATHER")) : 1;  // 2: cp.async gather
+    if (amode == fis::big::A_CPASYNC && gmode == 1 && gather_ok(a) && encode_gather(a, &gm))
+        amode = fis::big::A_TMA_GATHER;
+    int bn = fis_gemm_big_bn(a->n);
+    if (amode == fis::big::A_CPASYNC || amode == fis::big::A_TMA_GATHER) {
+        const int w = wide_bn(a->n);
+        if (w) bn = w;
+    }
+    const CUtensorMap* tm = weight_map(a->b.ptr, a->n, a->k, a->b.ld, bn > 256 ? bn / 2 : bn);
+    if (!tm) return FIS_ERR_UNSUPPORTED;
     const fis::big::Layout L = fis::big::layout(bn);
     static int configured_smem = 0;
     if (configured_smem < L.total) {
@@ -548,7 +706,7 @@ int fis_gemm_big_launch(const fis_gemm_args* a, cudaStream_t stream) {
     cfg.attrs = attr;
     cfg.numAttrs = fis_pdl_enabled() ? 1 : 0;
     static int dbg = getenv("FIS_BIG_DBG") ? atoi(getenv("FIS_BIG_DBG")) : 0;  // 1: no stores, 2: no A loads
-    return cudaLaunchKernelEx(&cfg, fis::big::gemm_big_kernel, *a, *tm, ta, ta2, bn, amode, dbg) == cudaSuccess
+    return cudaLaunchKernelEx(&cfg, fis::big::gemm_big_kernel, *a, *tm, ta, ta2, gm, bn, amode, dbg) == cudaSuccess
                ? FIS_OK : FIS_ERR_LAUNCH;
 }
 

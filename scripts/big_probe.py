@@ -61,7 +61,13 @@ def conv_dense(R, h, w, cin, cout):
 def conv_gather(R, h, w, cin, cout, frac):
     hw = h * w
     cache = rnd(R * hw, cin)
-    act = torch.rand(R * hw, device=dev, generator=g) < frac
+    # one square per image (the bench's user masks), at an image-dependent offset
+    act = torch.zeros((R, h, w), dtype=torch.bool, device=dev)
+    side = max(1, int(round((frac * hw) ** 0.5)))
+    for r in range(R):
+        y0, x0 = (7 * r) % (h - side + 1), (13 * r) % (w - side + 1)
+        act[r, y0:y0 + side, x0:x0 + side] = True
+    act = act.flatten()
     rows = act.nonzero().flatten().to(torch.int32)
     n = rows.numel()
     index = torch.full((R * hw,), -1, dtype=torch.int32, device=dev)
@@ -98,6 +104,16 @@ if len(sys.argv) > 1 and sys.argv[1] == "small":
 if len(sys.argv) > 1 and sys.argv[1] == "quick":
     rows_gemm(4096, 3840, 1280)
     conv_dense(32, 16, 16, 1280, 1280)
+    sys.exit(0)
+if len(sys.argv) > 1 and sys.argv[1] == "gtrace":
+    import ctypes
+    conv_gather(32, 64, 64, 320, 320, 0.12)
+    buf = (ctypes.c_ulonglong * 768)()
+    L.lib().fis_big_trace_read(buf)
+    t = list(buf)
+    t0 = min(x for x in t if x)
+    for i in range(0, 60):
+        print(i, [(t[r * 256 + i] - t0) if t[r * 256 + i] else None for r in range(3)])
     sys.exit(0)
 if len(sys.argv) > 1 and sys.argv[1] == "trace":
     import ctypes
