@@ -215,6 +215,13 @@ def run_ours(args):
     per_ms = ms / max(1, args.steps)
     value = ws * args.steps / (ms / 1e3)
 
+    # --- end-to-end through the public API (host mask in, host latent out, all T steps); measured
+    # before the batched section so its ~100 GB stacked arena does not sit in the allocator
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    P.edit(P.EditSession.create(OLD_IDS, NEW_IDS, cfg, store, user_mask=mask), cfg, store)
+    torch.cuda.synchronize()
+    e2e_s = reduce_max(time.perf_counter() - t0)
     # --- the same sparse step on the persistent step VM (csrc/fis_vm.cu; experimental engine)
     vm_ms = None
     if args.precision == "bf16":
@@ -229,31 +236,22 @@ def run_ours(args):
     dense_ms = dense_step_ms(eng, U, P, cfg, kv, args)
     # --- C5-style: R concurrent independent requests on this GPU (one stream each)
     batched = None
-    if args.requests > 1 and args.precision == "bf16":
-        sv, sms, srows = stacked_requests(eng, U, P, cfg, args.requests, args)
-        bv, bms = batched_requests(eng, U, P, cfg, args.requests, args)
-        batched = {"requests_per_gpu": args.requests, "edit_steps_per_s": sv, "ms_per_batched_step": sms,
-                   "rows_L0": srows,
-                   "masks": "5/10/25% squares at distinct offsets, distinct prompts, own cached generations",
-                   "note": "R requests stepped as ONE stacked batch (BatchedEditPlan: concatenated rows, weights "
-                           "read once per step for all R, segment attention; SURVEY §8 C5 per-GPU shard)",
-                   "concurrent_streams": {"edit_steps_per_s": bv, "ms_per_round": bms,
-                                          "note": "same R requests, one step graph per request on its own stream"}}
+    R = args.requests if args.requests > 0 else max(1, 64 // ws)  # C5: 64 requests over the box
+    if R > 1 and args.precision == "bf16":
+        _, tf_peak, _ = peaks()
+        batched = stacked_requests(eng, U, P, cfg, R, args, tf_peak)
+        # whole job: all ranks' requests over the slowest rank's batched step (no collective in the step)
+        batched["edit_steps_per_s_all_ranks"] = ws * R * 1e3 / reduce_max(batched["ms_per_batched_step"])
+        batched.update({"masks": "5/10/25% squares at distinct offsets, distinct prompts, own cached generations",
+                        "note": "C5: 64 requests sharded by request over the GPUs, each GPU's R = 64 / N stepped "
+                                "as ONE stacked batch (BatchedEditPlan: concatenated rows, weights read once per "
+                                "step for all R, block-diagonal segment attention); no collective"})
     sweep = mask_sweep(eng, U, P, cfg, arena, kv, lat0, args) if args.sweep else None
 
     # --- per-kernel timing of the gated (sparse) convs: eager instrumented step
     gflop_conv, conv_ms, gemm_ms, dense_gflop = instrumented_conv(eng, ep, U, cfg, mask)
     hbm, tf, src = peaks()
     achieved = gflop_conv / (conv_ms / 1e3) / 1e3 if conv_ms > 0 else 0.0  # TFLOP/s
-    # --- end-to-end through the public API (host mask in, host latent out, all T steps)
-    e2e_s = None
-    if rank == 0 or True:
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        res = P.edit(P.EditSession.create(OLD_IDS, NEW_IDS, cfg, store, user_mask=mask), cfg, store)
-        torch.cuda.synchronize()
-        e2e_s = time.perf_counter() - t0
-    e2e_s = reduce_max(e2e_s)
     line = {
         "metric": METRIC, "value": value, "unit": "edit-steps/s", "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": per_ms, "higher_is_better": True, "scaling": "weak",
@@ -386,23 +384,71 @@ def _request(r, cfg):
     return old, new, bits
 
 
-def stacked_requests(eng, U, P, cfg, R, args):
+def stacked_requests(eng, U, P, cfg, R, args, peak_tf):
     """C5 throughput on one GPU: R edit requests stepped as ONE stacked batch (BatchedEditPlan:
     concatenated rows, every weight read once per step for all R requests; segment attention).
-    Returns (edit-steps/s over all requests, ms per batched step, active L0 rows)."""
+    Returns a dict: device-timed edit-steps/s over all R requests, the gated-conv gather-GEMMs'
+    tensor-core rate in that step, and one end-to-end edit_batch() call (host masks / prompts in,
+    host latents out)."""
     import torch
+    t0 = time.perf_counter()
     reqs = [_request(r, cfg) for r in range(R)]
     stores = [P.CacheStore() for _ in reqs]
     eng.ns = 0
     U.generate_dense_batch([P.PromptTokens(o) for o, _, _ in reqs], cfg, stores)
     stacked = stores[0].arena.stacked
+    setup_s = time.perf_counter() - t0
     kvs = [eng.text_kv(P.embed_tokens(P.PromptTokens(n), cfg)) for _, n, _ in reqs]
     lat0 = U._to_nhwc(P.initial_latent(cfg), eng.dev)
     bp = U.BatchedEditPlan(eng, stacked, [P.BinaryMask(b) for _, _, b in reqs], kvs, [lat0] * R)
     run = U._Runner(eng, bp.plan, True, ns=100)
     ms = _time_runner(run, cfg.steps, max(3, args.steps // 2), 3)
+    # gated-conv gather-GEMMs of the batched step: CUDA events around each launch (eager step);
+    # algorithmic FLOPs count active rows only (each request's run is padded to 16 rows)
+    st = torch.cuda.current_stream()
+    recs, orig = [], eng.gemm
+
+    def timed(m, n, k, **kw):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(st)
+        orig(m, n, k, **kw)
+        b.record(st)
+        recs.append((m, n, k, kw.get("srcs") is not None and kw.get("rows") is not None, a, b))
+
+    eng.gemm = timed
+    try:
+        eng.ns = 100
+        eng.step_dev.fill_(5)
+        eng.run_step(bp.plan)
+        torch.cuda.synchronize()
+    finally:
+        eng.gemm = orig
+        eng.ns = 0
+    active = {l: sum(dp.n_active[l] for dp in bp.dps) for l in range(cfg.levels)}
+    padded = {l: bp.lists[l][2] for l in bp.lists}
+    conv_ms, conv_fl = 0.0, 0.0
+    for m, n, k, g, a, b in recs:
+        if g:
+            lvl = next(l for l in padded if padded[l] == m)
+            conv_ms += a.elapsed_time(b)
+            conv_fl += 2.0 * active[lvl] * n * k
+    tf = conv_fl / (conv_ms / 1e3) / 1e12 if conv_ms > 0 else 0.0
+    # end to end through the public API: R sessions in, R host latents out
+    sessions = [P.EditSession.create(o, n, cfg, st_, user_mask=P.BinaryMask(b))
+                for (o, n, b), st_ in zip(reqs, stores)]
+    torch.cuda.synchronize()
+    t1 = time.perf_counter()
+    P.edit_batch(sessions, cfg)
+    torch.cuda.synchronize()
+    e2e_s = time.perf_counter() - t1
     eng.ns = 0
-    return R * 1e3 / ms, ms, bp.lists[0][2]
+    return {"requests_per_gpu": R, "edit_steps_per_s": R * 1e3 / ms, "ms_per_batched_step": ms,
+            "rows_L0_L1": [padded[0], padded.get(1)], "active_L0_L1": [active[0], active[1]],
+            "gated_conv": {"achieved_tflops": tf, "peak_tflops": peak_tf, "frac": tf / peak_tf if peak_tf else None,
+                           "gflop_per_step": conv_fl / 1e9, "ms_per_step": conv_ms},
+            "e2e": {"edit_steps_per_s": R * cfg.steps / e2e_s, "seconds": e2e_s,
+                    "note": "one edit_batch() call: R sessions (host masks, prompts) -> R host latents, all T steps"},
+            "setup_generation_s": setup_s}
 
 
 def dense_step_ms(eng, U, P, cfg, kv, args):
@@ -475,8 +521,8 @@ def main():
     ap.add_argument("--precision", default="bf16", choices=["fp32", "bf16"])
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--sweep", action="store_true", help="also time the C3 mask-ratio sweep")
-    ap.add_argument("--requests", type=int, default=8,
-                    help="also time R concurrent edit requests on each GPU (C5 shard; 1 disables)")
+    ap.add_argument("--requests", type=int, default=0,
+                    help="requests per GPU of the C5 batched measurement (0: 64 / n_gpus; 1 disables)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

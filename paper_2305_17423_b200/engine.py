@@ -382,8 +382,6 @@ class Engine(Launcher):
         mp = _pad(cap)
         qk = self.scratch(f"qk{tag}", (cap, 2 * c))
         vt = self.scratch(f"vt{tag}", (c, mp), zero=True)
-        S = self.scratch(f"S{tag}", (cap, cap), torch.float32)
-        P = self.scratch(f"P{tag}", (cap, mp), zero=True)
         # one GEMM for Q|K (row-major) and V (stored transposed as the PV B operand)
         self.gemm(m, 3 * c, c, a=s, b=DRef(wqkv), d=DRef(qk), n_split=2 * c, d2=DRef(vt, ld=mp), d2_trans=True,
                   b_static=True)
@@ -396,6 +394,8 @@ class Engine(Launcher):
             # S = QK^T, softmax and P.V (+ residual) in one tcgen05 kernel (fis_attn)
             self.attn(m, m, c, qkr, qkr.cols(c), DRef(vt, ld=mp), scale, s, y1, pre)
             return
+        S = self.scratch(f"S{tag}", (cap, cap), torch.float32)  # unfused path only (cap^2)
+        P = self.scratch(f"P{tag}", (cap, mp), zero=True)
         self.gemm(m, m, c, a=qkr, b=qkr.cols(c), d=DRef(S, ld=_pad(m)))
         self.softmax(m, m, _pad(m), DRef(S, ld=_pad(m)), scale, DRef(P, ld=_pad(m)))
         self.gemm(m, c, m, a=DRef(P, ld=_pad(m)), b=DRef(vt, ld=mp), d=y1, res=s, pre=pre)
