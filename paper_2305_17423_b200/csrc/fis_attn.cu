@@ -47,6 +47,11 @@ FIS_DEV void mma_commit(uint64_t* bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
                  : "memory");
 }
+FIS_DEV float ex2(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
 FIS_DEV uint32_t idesc_bf16(int M, int N) {
     return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
@@ -226,6 +231,8 @@ __global__ void __launch_bounds__(THREADS, 1)
         // ------------------------------------------------------------ softmax + epilogue (warps 0-3)
         const int lr = tid, r = m0 + lr;
         const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
+        // softmax in the log2 domain: x = s * scale * log2(e); P = 2^(x - m - log2 l) (one FFMA + EX2)
+        const float sl = a.scale * 1.4426950408889634f;
         float mrow = -INFINITY, lrow = 0.f;
         int sb = 0;
         float v[32];
@@ -240,27 +247,39 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll 1
                     for (int cb = 0; cb < 128; cb += 32) {
                         tmem_ld32(trow + cb, v);
+                        const int lim = n_keys - kbase - cb;  // valid keys in this chunk
                         float cm = -INFINITY;
+                        if (lim >= 32) {
 #pragma unroll
-                        for (int q = 0; q < 32; q++)
-                            if (kbase + cb + q < n_keys) cm = fmaxf(cm, v[q] * a.scale);
-                        const float mn = fmaxf(mrow, cm);
+                            for (int q = 0; q < 32; q++) cm = fmaxf(cm, v[q]);
+                        } else {
+#pragma unroll
+                            for (int q = 0; q < 32; q++)
+                                if (q < lim) cm = fmaxf(cm, v[q]);
+                        }
+                        const float mn = fmaxf(mrow, cm * sl);
                         float add = 0.f;
+                        if (lim >= 32) {
 #pragma unroll
-                        for (int q = 0; q < 32; q++)
-                            if (kbase + cb + q < n_keys) add += expf(v[q] * a.scale - mn);
-                        lrow = (mrow == -INFINITY ? 0.f : lrow * expf(mrow - mn)) + add;
+                            for (int q = 0; q < 32; q++) add += ex2(fmaf(v[q], sl, -mn));
+                        } else {
+#pragma unroll
+                            for (int q = 0; q < 32; q++)
+                                if (q < lim) add += ex2(fmaf(v[q], sl, -mn));
+                        }
+                        lrow = (mrow == -INFINITY ? 0.f : lrow * ex2(mrow - mn)) + add;
                         mrow = mn;
                     }
                 }
-                if (pass == 2) {  // P_j = exp(s*scale - m) / l -> bf16 P tile j & 1 (SW128, K-major)
+                if (pass == 2) {  // P_j -> bf16 P tile j & 1 (SW128, K-major)
                     const int pb = j & 1;
                     if (j >= 2) mbar_wait(p_free + pb, ((j >> 1) & 1) ^ 1);  // P.V_{j-2} done
-                    const float inv = 1.0f / lrow;
+                    const float off = mrow + __log2f(lrow);
                     unsigned char* pt0 = ptile + pb * P_BYTES;
 #pragma unroll 1
                     for (int cb = 0; cb < 128; cb += 32) {
                         tmem_ld32(trow + cb, v);
+                        const int lim = n_keys - kbase - cb;
                         unsigned char* pt = pt0 + (cb >> 6) * (128 * 128);
 #pragma unroll
                         for (int u = 0; u < 4; u++) {
@@ -269,9 +288,8 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
                             for (int e2 = 0; e2 < 4; e2++) {
                                 const int q0 = 8 * u + 2 * e2;
-                                const float p0 = kbase + cb + q0 < n_keys ? expf(v[q0] * a.scale - mrow) * inv : 0.f;
-                                const float p1 =
-                                    kbase + cb + q0 + 1 < n_keys ? expf(v[q0 + 1] * a.scale - mrow) * inv : 0.f;
+                                const float p0 = q0 < lim ? ex2(fmaf(v[q0], sl, -off)) : 0.f;
+                                const float p1 = q0 + 1 < lim ? ex2(fmaf(v[q0 + 1], sl, -off)) : 0.f;
                                 h[e2] = __floats2bfloat162_rn(p0, p1);
                             }
                             const int unit = ((cb & 63) >> 3) + u;

@@ -20,8 +20,9 @@ def main():
     cfg = P.UNetConfig(**bench.C2)
     eng = U.get_engine(cfg)
     for R in [int(x) for x in args.R.split(",")]:
-        v, ms, rows = bench.stacked_requests(eng, U, P, cfg, R, args)
-        out = {"R": R, "stacked_steps_per_s": v, "ms_per_batched_step": ms, "rows_L0": rows}
+        d = bench.stacked_requests(eng, U, P, cfg, R, args, 1633.8)
+        out = {"R": R, "stacked_steps_per_s": d["edit_steps_per_s"], "ms_per_batched_step": d["ms_per_batched_step"],
+               "gated_conv_tflops": d["gated_conv"]["achieved_tflops"], "e2e": d["e2e"]["edit_steps_per_s"]}
         if args.streams and R > 1:
             bv, bms = bench.batched_requests(eng, U, P, cfg, R, args)
             out.update(streams_steps_per_s=bv, streams_ms_per_round=bms)
