@@ -99,6 +99,7 @@ FIS_DEV void tmem_ld16(uint32_t taddr, uint32_t* u) {
           "=r"(u[8]), "=r"(u[9]), "=r"(u[10]), "=r"(u[11]), "=r"(u[12]), "=r"(u[13]), "=r"(u[14]), "=r"(u[15])
         : "r"(taddr));
 }
+FIS_DEV void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 FIS_DEV void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
 // debug timeline (FIS_BIG_DBG & 4): CTA 0's per-stage times [role][iteration] (%globaltimer ns)
@@ -169,7 +170,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
         for (int b = 0; b < 2; b++) {
             mbar_init(acc_full + b, 1);
-            mbar_init(acc_empty + b, 128);
+            mbar_init(acc_empty + b, amode == A_TMA_ROWS || amode == A_TMA_CONV ? 256 : 128);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -188,7 +189,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int t = cur_step(a.step);
 
     if (warp < A_WARPS) {
-        if (amode != A_CPASYNC && amode != A_TMA_GATHER) goto teardown;  // TMA stages A: no role here
+        if (amode != A_CPASYNC && amode != A_TMA_GATHER) goto epilogue_role;  // TMA stages A: help the epilogue
         // ------------------------------------------------------------ A producers
         // Row metadata: thread tid resolves tile row tid (pixel, and for CONV the select-on-read
         // decision of every tap) into shared tables. Loads: lane l copies 16-byte chunk l & 7 of
@@ -415,10 +416,19 @@ __global__ void __launch_bounds__(THREADS, 1)
             }
         }
     } else {
-        // ------------------------------------------------------------ epilogue (warps 6-9)
-        const int et = tid - EPI_WARP0 * 32;  // 0..127
+        goto epilogue_role;
+    }
+    goto teardown;
+epilogue_role : {
+        // ------------------------------------------------------------ epilogue
+        // warps 6-9 (group 0); with TMA-staged A the idle warps 0-3 join as group 1 and the two
+        // groups take alternate 16-column chunks of every tile
+        const int nepi = amode == A_TMA_ROWS || amode == A_TMA_CONV ? 256 : 128;
+        const int grp = warp < A_WARPS ? 1 : 0;
+        const int et = grp ? tid + 128 : tid - EPI_WARP0 * 32;  // 0..nepi-1
         const int quarter = warp & 3;         // TMEM lane quarter this warp may access
         const int lr = quarter * 32 + lane;   // tile row of this thread
+        const int cstep = nepi == 256 ? 2 : 1;
         const EpiCtx e = make_epi(a, t);
         EpiTab tb;
         tb.mean = tabs;
@@ -430,8 +440,8 @@ __global__ void __launch_bounds__(THREADS, 1)
         int lt = 0;
         for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, lt++) {
             const int m0 = (tile / tiles_n) * BM, n0 = (tile % tiles_n) * bn;
-            asm volatile("bar.sync 1, 128;" ::: "memory");  // previous tile's table reads done
-            for (int c = et; c < bn; c += 128) {
+            named_sync(1, nepi);  // previous tile's table reads done
+            for (int c = et; c < bn; c += nepi) {
                 const int n = n0 + c;
                 const bool ok = n < a.n;
                 tb.bias[c] = ok && a.bias ? __ldg(a.bias + n) : 0.f;
@@ -447,28 +457,21 @@ __global__ void __launch_bounds__(THREADS, 1)
                     tb.rstd[c] = 0.f;
                 }
             }
-            asm volatile("bar.sync 1, 128;" ::: "memory");
+            named_sync(1, nepi);
             const int buf = lt % nbuf;
             wait_dbg(acc_full + buf, (lt / nbuf) & 1, dbg, 4, lt);
             tc_fence_after();
             const uint32_t taddr = tmem + buf * ACC_STRIDE + ((uint32_t)(quarter * 32) << 16);
             const int r = m0 + lr;
-            for (int cb = 0; cb < bn; cb += 32) {
-                uint32_t u[32];
-                const bool two = cb + 16 < bn;
+            for (int cb = 16 * grp; cb < bn; cb += 16 * cstep) {
+                uint32_t u[16];
                 tmem_ld16(taddr + cb, u);
-                if (two) tmem_ld16(taddr + cb + 16, u + 16);
                 tmem_wait_ld();
                 if (r < a.m && !(dbg & 1)) {
                     float v[16];
 #pragma unroll
                     for (int j = 0; j < 16; j++) v[j] = __uint_as_float(u[j]);
                     row_epilogue_any(a, e, tb, r, cb, n0, v);
-                    if (two) {
-#pragma unroll
-                        for (int j = 0; j < 16; j++) v[j] = __uint_as_float(u[16 + j]);
-                        row_epilogue_any(a, e, tb, r, cb + 16, n0, v);
-                    }
                 }
             }
             tc_fence_before();

@@ -112,7 +112,8 @@ __global__ void gn_apply_kernel(const fis_gn_apply_args a) {
     const int cpg = a.c / a.groups;
     const int total = a.rows * a.c;
     const bool bf16_out = (!yn || a.y_norm.dtype == FIS_BF16) && (!ys || a.y_silu.dtype == FIS_BF16);
-    if (bf16_out && a.x.dtype == FIS_BF16 && (cpg % 8) == 0 && (a.x.ld % 8) == 0 && (!yn || (a.y_norm.ld % 8) == 0) &&
+    if (bf16_out && a.x.dtype == FIS_BF16 && cpg >= 8 && (a.c % 8) == 0 && (a.x.ld % 8) == 0 &&
+        (!yn || (a.y_norm.ld % 8) == 0) &&
         (!ys || (a.y_silu.ld % 8) == 0) && ((((uintptr_t)x) | ((uintptr_t)yn) | ((uintptr_t)ys)) & 15) == 0) {
         // bf16 perf mode, 8 channels (one group) per thread: 16-byte loads / stores
         const int cv = a.c / 8, totalv = a.rows * cv;
@@ -120,9 +121,16 @@ __global__ void gn_apply_kernel(const fis_gn_apply_args a) {
             const int r = e / cv, c = (e - r * cv) * 8;
             const int xr = a.x_rows ? __ldg(a.x_rows + r) : r;
             const int yr = a.y_rows ? __ldg(a.y_rows + r) : r;
-            const int g = (a.row_img ? __ldg(a.row_img + r) : (a.img_rows > 0 ? r / a.img_rows : 0)) * a.groups + c / cpg;
-            const float rstd = (float)(1.0 / sqrt((double)var[g] + (double)a.eps));
-            const float mu = mean[g];
+            // 8 channels span at most two groups (cpg >= 8): g0 below `split`, g0 + 1 from it
+            const int gi = (a.row_img ? __ldg(a.row_img + r) : (a.img_rows > 0 ? r / a.img_rows : 0)) * a.groups;
+            const int g0 = c / cpg, split = (g0 + 1) * cpg - c;
+            const float rstd0 = (float)(1.0 / sqrt((double)var[gi + g0] + (double)a.eps));
+            const float mu0 = mean[gi + g0];
+            float rstd1 = rstd0, mu1 = mu0;
+            if (split < 8) {
+                rstd1 = (float)(1.0 / sqrt((double)var[gi + g0 + 1] + (double)a.eps));
+                mu1 = mean[gi + g0 + 1];
+            }
             const uint4 u = *(const uint4*)((const __nv_bfloat16*)x + (long long)xr * a.x.ld + c);
             const __nv_bfloat162* h = (const __nv_bfloat162*)&u;
             uint4 on, os;
@@ -131,8 +139,11 @@ __global__ void gn_apply_kernel(const fis_gn_apply_args a) {
 #pragma unroll
             for (int k = 0; k < 4; k++) {
                 const float2 f = __bfloat1622float2(h[k]);
-                const float y0 = fmaf((f.x - mu) * rstd, __ldg(a.gamma + c + 2 * k), __ldg(a.beta + c + 2 * k));
-                const float y1 = fmaf((f.y - mu) * rstd, __ldg(a.gamma + c + 2 * k + 1), __ldg(a.beta + c + 2 * k + 1));
+                const bool s0 = 2 * k >= split, s1 = 2 * k + 1 >= split;
+                const float y0 = fmaf((f.x - (s0 ? mu1 : mu0)) * (s0 ? rstd1 : rstd0), __ldg(a.gamma + c + 2 * k),
+                                      __ldg(a.beta + c + 2 * k));
+                const float y1 = fmaf((f.y - (s1 ? mu1 : mu0)) * (s1 ? rstd1 : rstd0), __ldg(a.gamma + c + 2 * k + 1),
+                                      __ldg(a.beta + c + 2 * k + 1));
                 hn[k] = __floats2bfloat162_rn(y0, y1);
                 hs[k] = __floats2bfloat162_rn(__fdividef(y0, 1.0f + __expf(-y0)), __fdividef(y1, 1.0f + __expf(-y1)));
             }
