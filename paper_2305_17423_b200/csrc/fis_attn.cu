@@ -106,6 +106,9 @@ __global__ void __launch_bounds__(THREADS, 1)
     if (m0 >= q_end || n_keys <= 0) return;  // uniform for the CTA, before any barrier
     const int nkb = (n_keys + 127) / 128, dch = a.d / 64;
     const bool single = nkb == 1;
+    // two key blocks: both S blocks stay resident in the two TMEM buffers, so the statistics pass
+    // and the P pass read the same S (no recompute, half the Q/K traffic)
+    const bool resident = nkb == 2;
     const int first_pass = single ? 2 : 1;
     if (tid == 0) {
         for (int i = 0; i < STAGES; i++) {
@@ -164,11 +167,18 @@ __global__ void __launch_bounds__(THREADS, 1)
                     tma2d(sbase + st * STAGE + A_BYTES, &tv, k_beg + j * 128 + h * 64, c0, full + st);
                 }
             };
-            if (!single)
-                for (int j = 0; j < nkb; j++) load_s(j);
-            for (int u = 0; u <= nkb; u++) {
-                if (u < nkb) load_s(u);
-                if (u >= 1) load_v(u - 1);
+            if (resident) {
+                load_s(0);
+                load_s(1);
+                load_v(0);
+                load_v(1);
+            } else {
+                if (!single)
+                    for (int j = 0; j < nkb; j++) load_s(j);
+                for (int u = 0; u <= nkb; u++) {
+                    if (u < nkb) load_s(u);
+                    if (u >= 1) load_v(u - 1);
+                }
             }
         }
     } else if (warp == MMA_WARP) {
@@ -221,11 +231,18 @@ __global__ void __launch_bounds__(THREADS, 1)
                 it++;
             }
         };
-        if (!single)
-            for (int j = 0; j < nkb; j++) mma_s();
-        for (int u = 0; u <= nkb; u++) {
-            if (u < nkb) mma_s();
-            if (u >= 1) mma_pv(u - 1);
+        if (resident) {
+            mma_s();
+            mma_s();
+            mma_pv(0);
+            mma_pv(1);
+        } else {
+            if (!single)
+                for (int j = 0; j < nkb; j++) mma_s();
+            for (int u = 0; u <= nkb; u++) {
+                if (u < nkb) mma_s();
+                if (u >= 1) mma_pv(u - 1);
+            }
         }
     } else {
         // ------------------------------------------------------------ softmax + epilogue (warps 0-3)
@@ -237,6 +254,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         int sb = 0;
         float v[32];
         for (int pass = first_pass; pass <= 2; pass++) {
+            if (resident) sb = 0;  // pass 2 re-reads the resident S blocks (their phases already completed)
             for (int j = 0; j < nkb; j++) {
                 const int b = sb & 1;
                 mbar_wait(s_ready + b, (sb >> 1) & 1);
