@@ -72,7 +72,8 @@ class XattnArgs(C.Structure):
 class AttnArgs(C.Structure):
     _fields_ = [("m", C.c_int), ("n_keys", C.c_int), ("d", C.c_int), ("dv", C.c_int), ("q", Ref), ("k", Ref),
                 ("vt", Ref), ("scale", C.c_float), ("res", Ref), ("pre", Ref), ("out", Ref), ("step", C.c_void_p),
-                ("nseg", C.c_int), ("max_seg_q", C.c_int), ("q_seg", C.c_void_p), ("k_seg", C.c_void_p)]
+                ("nseg", C.c_int), ("max_seg_q", C.c_int), ("q_seg", C.c_void_p), ("k_seg", C.c_void_p),
+                ("max_seg_k", C.c_int), ("ws", C.c_void_p), ("ws_bytes", C.c_longlong)]
 
 
 class PoolArgs(C.Structure):

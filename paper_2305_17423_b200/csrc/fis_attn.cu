@@ -18,6 +18,7 @@
 // A segment of <= 128 keys takes one pass (statistics and P from the same S).
 #include "fis_tc.cuh"
 #include "fis_tma.cuh"
+#include <cstring>
 
 namespace fis {
 namespace attn {
@@ -32,6 +33,10 @@ constexpr int STAGE = A_BYTES + B_BYTES;
 constexpr int P_BYTES = 2 * 128 * 64 * 2;        // P tile: 128 rows x 128 keys, two 64-key SW128 chunks
 constexpr int SMEM = STAGES * STAGE + 2 * P_BYTES + 1024 + 256;
 constexpr uint32_t O_COL = 256;                  // TMEM: S buffers at 0 / 128, O at 256
+// P sharing across the value slices of a query tile (segments of <= 256 keys): a P_OUT launch
+// (slice 0 only) computes S, the softmax and writes P (bf16, [row][256]) to scratch; the P_IN
+// launch (every slice) TMA-loads those P tiles and runs only P.V + the epilogue
+constexpr int P_NONE = 0, P_OUT = 1, P_IN = 2;
 
 FIS_DEV void tma2d(uint32_t dst, const void* tmap, int c0, int c1, uint64_t* bar) {
     asm volatile(
@@ -80,7 +85,7 @@ FIS_DEV void tmem_ld32(uint32_t taddr, float* v) {
 // step u issues S_u (u < nkb) and then P_{u-1}.V_{u-1} (u >= 1).
 __global__ void __launch_bounds__(THREADS, 1)
     attn_kernel(const fis_attn_args a, const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
-                const __grid_constant__ CUtensorMap tv, int dvs) {
+                const __grid_constant__ CUtensorMap tv, const __grid_constant__ CUtensorMap tp, int dvs, int pmode) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     unsigned char* ptile = smem + STAGES * STAGE;
@@ -118,7 +123,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         for (int b = 0; b < 2; b++) {
             mbar_init(s_ready + b, 1);
             mbar_init(s_free + b, 128);
-            mbar_init(p_ready + b, 128);
+            mbar_init(p_ready + b, pmode == P_IN ? 1 : 128);
             mbar_init(p_free + b, 1);
         }
         mbar_init(o_done, 1);
@@ -167,7 +172,16 @@ __global__ void __launch_bounds__(THREADS, 1)
                     tma2d(sbase + st * STAGE + A_BYTES, &tv, k_beg + j * 128 + h * 64, c0, full + st);
                 }
             };
-            if (resident) {
+            if (pmode == P_IN) {  // P tiles of this query tile from the scratch (written by the P_OUT launch)
+                for (int j = 0; j < nkb; j++) {
+                    arrive_expect_tx(p_ready + j, (uint32_t)P_BYTES);
+                    for (int h = 0; h < 2; h++)
+                        tma2d(smem_u32(ptile) + j * P_BYTES + h * (128 * 128), &tp, j * 128 + h * 64, m0, p_ready + j);
+                    load_v(j);
+                }
+            } else if (pmode == P_OUT) {
+                for (int j = 0; j < nkb; j++) load_s(j);
+            } else if (resident) {
                 load_s(0);
                 load_s(1);
                 load_v(0);
@@ -231,7 +245,11 @@ __global__ void __launch_bounds__(THREADS, 1)
                 it++;
             }
         };
-        if (resident) {
+        if (pmode == P_IN) {
+            for (int j = 0; j < nkb; j++) mma_pv(j);
+        } else if (pmode == P_OUT) {
+            for (int j = 0; j < nkb; j++) mma_s();
+        } else if (resident) {
             mma_s();
             mma_s();
             mma_pv(0);
@@ -253,7 +271,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         float mrow = -INFINITY, lrow = 0.f;
         int sb = 0;
         float v[32];
-        for (int pass = first_pass; pass <= 2; pass++) {
+        for (int pass = first_pass; pass <= 2 && pmode != P_IN; pass++) {
             if (resident) sb = 0;  // pass 2 re-reads the resident S blocks (their phases already completed)
             for (int j = 0; j < nkb; j++) {
                 const int b = sb & 1;
@@ -289,7 +307,30 @@ __global__ void __launch_bounds__(THREADS, 1)
                         mrow = mn;
                     }
                 }
-                if (pass == 2) {  // P_j -> bf16 P tile j & 1 (SW128, K-major)
+                if (pass == 2 && pmode == P_OUT) {  // P_j -> the P scratch row (keys of this segment)
+                    const float off = mrow + __log2f(lrow);
+                    __nv_bfloat16* prow = (__nv_bfloat16*)a.ws + (long long)r * 256 + kbase;
+#pragma unroll 1
+                    for (int cb = 0; cb < 128; cb += 32) {
+                        tmem_ld32(trow + cb, v);
+                        const int lim = n_keys - kbase - cb;
+#pragma unroll
+                        for (int u = 0; u < 4; u++) {
+                            uint4 pk;
+                            __nv_bfloat162* h = (__nv_bfloat162*)&pk;
+#pragma unroll
+                            for (int e2 = 0; e2 < 4; e2++) {
+                                const int q0 = 8 * u + 2 * e2;
+                                const float p0 = q0 < lim ? ex2(fmaf(v[q0], sl, -off)) : 0.f;
+                                const float p1 = q0 + 1 < lim ? ex2(fmaf(v[q0 + 1], sl, -off)) : 0.f;
+                                h[e2] = __floats2bfloat162_rn(p0, p1);
+                            }
+                            if (r < q_end) *(uint4*)(prow + cb + 8 * u) = pk;
+                        }
+                    }
+                    tc_fence_before();
+                    mbar_arrive(s_free + b);
+                } else if (pass == 2) {  // P_j -> bf16 P tile j & 1 (SW128, K-major)
                     const int pb = j & 1;
                     if (j >= 2) mbar_wait(p_free + pb, ((j >> 1) & 1) ^ 1);  // P.V_{j-2} done
                     const float off = mrow + __log2f(lrow);
@@ -326,6 +367,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             }
         }
         // epilogue: O row slice + residual -> out
+        if (pmode == P_OUT) goto done;
         mbar_wait(o_done, 0);
         tc_fence_after();
         {  // tcgen05.ld is warp-collective: every lane loads, rows of this segment store
@@ -360,6 +402,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             }
         }
     }
+done:
     tc_fence_before();
     __syncthreads();
     if (warp == MMA_WARP) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
@@ -385,11 +428,15 @@ extern "C" int fis_attn(const fis_attn_args* a, void* stream) {
         return FIS_ERR_UNSUPPORTED;
     const int dvs = attn_slice(a->dv);
     if (!dvs) return FIS_ERR_UNSUPPORTED;
-    CUtensorMap tq, tk, tv;
+    CUtensorMap tq, tk, tv, tp;
     if (!encode_2d(&tq, a->q.ptr, a->m, a->d, a->q.ld, 128) ||
         !encode_2d(&tk, a->k.ptr, a->n_keys, a->d, a->k.ld, 128) ||
         !encode_2d(&tv, a->vt.ptr, a->dv, a->n_keys, a->vt.ld, dvs))
         return FIS_ERR_UNSUPPORTED;
+    static int share_off = getenv("FIS_ATTN_SHARE") && getenv("FIS_ATTN_SHARE")[0] == '0';
+    const bool share = !share_off && a->max_seg_k > 0 && a->max_seg_k <= 256 && a->dv / dvs > 1 && a->ws &&
+                       a->ws_bytes >= (long long)a->m * 256 * 2 && encode_2d(&tp, a->ws, a->m, 256, 256, 128);
+    if (!share) std::memset(&tp, 0, sizeof(tp));
     static bool configured = false;
     if (!configured) {
         if (cudaFuncSetAttribute(fis::attn::attn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -398,8 +445,8 @@ extern "C" int fis_attn(const fis_attn_args* a, void* stream) {
         configured = true;
     }
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = a->nseg > 0 ? dim3(a->dv / dvs, (a->max_seg_q + 127) / 128, a->nseg)
-                              : dim3(a->dv / dvs, (a->m + 127) / 128, 1);
+    const dim3 grid = a->nseg > 0 ? dim3(a->dv / dvs, (a->max_seg_q + 127) / 128, a->nseg)
+                                  : dim3(a->dv / dvs, (a->m + 127) / 128, 1);
     cfg.blockDim = dim3(fis::attn::THREADS);
     cfg.dynamicSmemBytes = fis::attn::SMEM;
     cfg.stream = (cudaStream_t)stream;
@@ -408,6 +455,14 @@ extern "C" int fis_attn(const fis_attn_args* a, void* stream) {
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = fis_pdl_enabled() ? 1 : 0;
-    return cudaLaunchKernelEx(&cfg, fis::attn::attn_kernel, *a, tq, tk, tv, dvs) == cudaSuccess ? FIS_OK
-                                                                                                : FIS_ERR_LAUNCH;
+    if (share) {  // P once per query tile (slice 0), then every slice's P.V from the scratch
+        cfg.gridDim = dim3(1, grid.y, grid.z);
+        if (cudaLaunchKernelEx(&cfg, fis::attn::attn_kernel, *a, tq, tk, tv, tp, dvs, (int)fis::attn::P_OUT) !=
+            cudaSuccess)
+            return FIS_ERR_LAUNCH;
+    }
+    cfg.gridDim = grid;
+    return cudaLaunchKernelEx(&cfg, fis::attn::attn_kernel, *a, tq, tk, tv, tp, dvs,
+                              share ? (int)fis::attn::P_IN : (int)fis::attn::P_NONE) == cudaSuccess
+               ? FIS_OK : FIS_ERR_LAUNCH;
 }

@@ -388,7 +388,8 @@ class Engine(Launcher):
         qkr = DRef(qk)
         if segs is not None:
             qseg, nseg, maxq = segs
-            self.attn(m, m, c, qkr, qkr.cols(c), DRef(vt, ld=mp), scale, s, y1, pre, segs=(qseg, qseg, nseg, maxq))
+            self.attn(m, m, c, qkr, qkr.cols(c), DRef(vt, ld=mp), scale, s, y1, pre,
+                      segs=(qseg, qseg, nseg, maxq, maxq))
             return
         if self.use_fused_attn(c, m, m, pre):
             # S = QK^T, softmax and P.V (+ residual) in one tcgen05 kernel (fis_attn)
@@ -450,8 +451,11 @@ class Engine(Launcher):
         a = L.AttnArgs(m, n_keys, d, d, q.ref(), k.ref(), vt.ref(), float(scale), _r(res), _r(pre), out.ref(),
                        L.ptr(self.step_dev))
         if segs is not None:
-            qseg, kseg, nseg, maxq = segs
+            qseg, kseg, nseg, maxq, maxk = segs
             a.nseg, a.max_seg_q, a.q_seg, a.k_seg = nseg, maxq, L.ptr(qseg), L.ptr(kseg)
+            if maxk <= 256:  # value slices share one P per query tile (P scratch [m, 256] bf16)
+                ws = self.scratch("attn_p", (m * 256,), torch.bfloat16)
+                a.max_seg_k, a.ws, a.ws_bytes = maxk, L.ptr(ws), ws.numel() * 2
         self._call("fis_attn", a)
         self.launches += 1
 
@@ -582,7 +586,7 @@ class Engine(Launcher):
         qs = plan.segments(level)
         self.attn_self(blk["self_attn"], m, s, y1, level, tag, pre=plan.record(blk["self_attn"], 0), segs=qs)
         lid = blk["cross_attn"]
-        xs = None if qs is None else (qs[0], plan.key_segments(), qs[1], qs[2])
+        xs = None if qs is None else (qs[0], plan.key_segments(), qs[1], qs[2], plan.max_keys())
         self.attn_cross(lid, m, y1, plan.out_buf(fo), level, tag, plan.kv, pre=plan.record(lid, 0),
                         map_=plan.record(lid, 3), ctrl=plan.ctrl(lid), segs=xs)
 
@@ -777,8 +781,10 @@ class BatchedSparsePlan(SparsePlan):
     see only its own rows / its own prompt's keys) and GroupNorm uses each image's statistics.
     """
 
-    def __init__(self, eng: Engine, kv, arena: Arena, lists, lat_rows: torch.Tensor, qsegs, kseg, row_img):
+    def __init__(self, eng: Engine, kv, arena: Arena, lists, lat_rows: torch.Tensor, qsegs, kseg, row_img,
+                 max_keys: int = 256):
         super().__init__(eng, kv, arena, lists, lat_rows)
+        self._max_keys = max_keys  # longest prompt (text keys of one request)
         self.batch = arena.batch
         self._qsegs = qsegs      # level -> (int32 [2R] device, R, max rows per request)
         self._kseg = kseg        # int32 [2R] device: each request's text keys in the stacked K / V^T
@@ -789,6 +795,9 @@ class BatchedSparsePlan(SparsePlan):
 
     def key_segments(self):
         return self._kseg
+
+    def max_keys(self):
+        return self._max_keys
 
     def row_img(self, level):
         return self._row_img[level]

@@ -569,7 +569,9 @@ class BatchedEditPlan:
         self.lat_rows = lat0.index_select(0, r0[:n0].long()).contiguous()
         kv, kseg = stack_text_kv(eng, kvs)
         self.kv = kv
-        self.plan = BatchedSparsePlan(eng, kv, stacked, lists, self.lat_rows, qsegs, kseg, row_img)
+        lid0 = next(iter(kvs[0]))
+        max_keys = max(kv[lid0][0].shape[0] for kv in kvs)
+        self.plan = BatchedSparsePlan(eng, kv, stacked, lists, self.lat_rows, qsegs, kseg, row_img, max_keys)
 
     def final_latents(self, eng: Engine, stacked: Arena) -> torch.Tensor:
         """[R * hw, Cl] f32: fresh rows where masked, the cached generation elsewhere."""

@@ -154,8 +154,10 @@ def test_fused_attention_vs_torch(env, m, nk, d):
 @pytest.mark.parametrize("d,qlens,klens,kpad", [
     (320, [205, 410, 1024, 0, 37], None, 0),          # self-attention: keys = own rows
     (640, [64, 300, 129], [77, 77, 77], 80),           # cross-attention: stacked prompts padded to 80
-    (1280, [256, 256, 256], None, 0)])
-def test_segment_attention_vs_torch(env, d, qlens, klens, kpad):
+    (1280, [256, 256, 256], None, 0),
+    (640, [100, 256, 17], None, 0)])
+@pytest.mark.parametrize("share", [False, True])
+def test_segment_attention_vs_torch(env, d, qlens, klens, kpad, share):
     """fis_attn with ragged segments (batched requests): each query run attends to its own key run only."""
     L, DRef, NULL, lz = env
     g = torch.Generator(device="cuda").manual_seed(d + len(qlens))
@@ -187,6 +189,10 @@ def test_segment_attention_vs_torch(env, d, qlens, klens, kpad):
     a = L.AttnArgs(m, nk, d, d, DRef(Q).ref(), DRef(K).ref(), DRef(Vt, ld=ldv).ref(), scale, DRef(res).ref(), NULL,
                    DRef(out).ref(), None)
     a.nseg, a.max_seg_q, a.q_seg, a.k_seg = len(qseg), max(1, max(qlens)), L.ptr(qs), L.ptr(ks)
+    max_k = max(k1 - k0 for k0, k1 in kseg)
+    if share and max_k <= 256:  # value slices share one P per query tile through the scratch
+        ws = torch.empty(m * 256, device="cuda", dtype=bf)
+        a.max_seg_k, a.ws, a.ws_bytes = max_k, L.ptr(ws), ws.numel() * 2
     L.call("fis_attn", a)
     torch.cuda.synchronize()
     for (q0, q1), (k0, k1) in zip(qseg, kseg):
