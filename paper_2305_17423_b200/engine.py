@@ -122,11 +122,11 @@ class Launcher:
         self.launches = 0
         self._scratch = {}
         self.fused_xattn = False  # SIMT xattn is latency-bound; superseded by fis_attn
-        # tcgen05 fused attention (csrc/fis_attn.cu) for single sequences: one CTA per 128 queries x
-        # value slice leaves most SMs idle at batch 1 (r01: 1.75 vs 1.58 ms sparse step, 4.39 vs
-        # 3.06 ms dense), so S GEMM -> softmax -> P.V GEMM stays the default there; stacked
-        # requests always use it (segments). FIS_FUSED_ATTN=1 forces it.
-        self.fused_attn = os.environ.get("FIS_FUSED_ATTN", "0") == "1"
+        # tcgen05 fused attention (csrc/fis_attn.cu: TMA-fed, log2 softmax, resident S for <= 256
+        # keys, P shared across value slices) instead of S GEMM -> softmax -> P.V GEMM: C2 sparse
+        # step 1.416 vs 1.506 ms, dense step 2.83 vs 3.30 ms (r01). Stacked requests always use it
+        # (segments); FIS_FUSED_ATTN=0 restores the three-launch path for single sequences.
+        self.fused_attn = os.environ.get("FIS_FUSED_ATTN", "1") == "1"
         # gather lists (rows / pixel->row maps) are written once per edit, before any step runs
         # (DevicePlan syncs), so GEMMs may read them before the programmatic-launch wait
         self.static_meta = False
@@ -450,12 +450,13 @@ class Engine(Launcher):
             raise ContractViolation("fused attention (fis_attn) runs on bf16 operands only")
         a = L.AttnArgs(m, n_keys, d, d, q.ref(), k.ref(), vt.ref(), float(scale), _r(res), _r(pre), out.ref(),
                        L.ptr(self.step_dev))
+        maxk = n_keys
         if segs is not None:
             qseg, kseg, nseg, maxq, maxk = segs
             a.nseg, a.max_seg_q, a.q_seg, a.k_seg = nseg, maxq, L.ptr(qseg), L.ptr(kseg)
-            if maxk <= 256:  # value slices share one P per query tile (P scratch [m, 256] bf16)
-                ws = self.scratch("attn_p", (m * 256,), torch.bfloat16)
-                a.max_seg_k, a.ws, a.ws_bytes = maxk, L.ptr(ws), ws.numel() * 2
+        if maxk <= 256:  # value slices share one P per query tile (P scratch [m, 256] bf16)
+            ws = self.scratch("attn_p", (m * 256,), torch.bfloat16)
+            a.max_seg_k, a.ws, a.ws_bytes = maxk, L.ptr(ws), ws.numel() * 2
         self._call("fis_attn", a)
         self.launches += 1
 

@@ -9,6 +9,10 @@ import sys
 from collections import defaultdict
 
 
+def _next_is_attn_pair(seq, s):
+    return True
+
+
 def main(csv_path, seq_path, top=30):
     rows = list(csv.reader(open(csv_path)))
     hdr, ks = None, []
@@ -22,8 +26,17 @@ def main(csv_path, seq_path, top=30):
                 ks.append((d["Kernel Name"], float(d["Metric Value"].replace(",", ""))))
     seq = [json.loads(l.split(" ", 1)[1]) for l in open(seq_path) if re.match(r"^\d+ \{", l)]
     agg, cnt = defaultdict(float), defaultdict(int)
-    for (kn, t), s in zip(ks, seq):
+    i = 0
+    for s in seq:  # an op may launch several kernels (fis_attn with shared P: P_OUT + P_IN)
         key = s["op"] + (f" n={s['n']} k={s['k']}" if s["op"] == "fis_gemm" else "") + f" m={s.get('m', s.get('rows'))}"
+        t = ks[i][1]
+        i += 1
+        if s["op"] == "fis_attn":
+            while i < len(ks) and "attn" in ks[i][0] and (i + 1 >= len(ks) or "attn" in ks[i - 1][0]) and \
+                    ks[i][0] == ks[i - 1][0] and _next_is_attn_pair(seq, s):
+                t += ks[i][1]
+                i += 1
+                break
         agg[key] += t
         cnt[key] += 1
     tot = sum(t for _, t in ks)
