@@ -197,9 +197,9 @@ typedef struct {
     int max_seg_q;          /* largest q_seg[s+1] - q_seg[s] (sizes the grid) */
     const int* q_seg;       /* [2 * nseg] device (begin, end) pairs */
     const int* k_seg;       /* [2 * nseg] device (begin, end) pairs */
-    int max_seg_k;          /* > 0: longest key run; <= 256 lets the value slices of a query tile
-                               share one P (computed once into ws) instead of recomputing S */
-    void* ws;               /* P scratch: [m][256] bf16 (may be NULL) */
+    int max_seg_k;          /* > 0: longest key run; lets the value slices of a query tile share
+                               one P (computed once into ws) instead of recomputing S */
+    void* ws;               /* P scratch: [m][128 * ceil(max_seg_k / 128)] bf16 (may be NULL) */
     long long ws_bytes;
 } fis_attn_args;
 int fis_attn(const fis_attn_args* a, void* stream);

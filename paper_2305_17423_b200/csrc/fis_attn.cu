@@ -115,6 +115,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     // and the P pass read the same S (no recompute, half the Q/K traffic)
     const bool resident = nkb == 2;
     const int first_pass = single ? 2 : 1;
+    const int pw = ((a.max_seg_k + 127) / 128) * 128;  // P scratch row width (P sharing)
     if (tid == 0) {
         for (int i = 0; i < STAGES; i++) {
             mbar_init(full + i, 1);
@@ -174,12 +175,17 @@ __global__ void __launch_bounds__(THREADS, 1)
             };
             if (pmode == P_IN) {  // P tiles of this query tile from the scratch (written by the P_OUT launch)
                 for (int j = 0; j < nkb; j++) {
-                    arrive_expect_tx(p_ready + j, (uint32_t)P_BYTES);
+                    const int pb = j & 1;
+                    if (j >= 2) mbar_wait(p_free + pb, ((j >> 1) & 1) ^ 1);  // P.V_{j-2} done with the buffer
+                    arrive_expect_tx(p_ready + pb, (uint32_t)P_BYTES);
                     for (int h = 0; h < 2; h++)
-                        tma2d(smem_u32(ptile) + j * P_BYTES + h * (128 * 128), &tp, j * 128 + h * 64, m0, p_ready + j);
+                        tma2d(smem_u32(ptile) + pb * P_BYTES + h * (128 * 128), &tp, j * 128 + h * 64, m0,
+                              p_ready + pb);
                     load_v(j);
                 }
-            } else if (pmode == P_OUT) {
+            } else if (pmode == P_OUT) {  // statistics pass (unless S is resident) + P pass
+                if (!(resident || single))
+                    for (int j = 0; j < nkb; j++) load_s(j);
                 for (int j = 0; j < nkb; j++) load_s(j);
             } else if (resident) {
                 load_s(0);
@@ -248,6 +254,8 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (pmode == P_IN) {
             for (int j = 0; j < nkb; j++) mma_pv(j);
         } else if (pmode == P_OUT) {
+            if (!(resident || single))
+                for (int j = 0; j < nkb; j++) mma_s();
             for (int j = 0; j < nkb; j++) mma_s();
         } else if (resident) {
             mma_s();
@@ -309,7 +317,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                 }
                 if (pass == 2 && pmode == P_OUT) {  // P_j -> the P scratch row (keys of this segment)
                     const float off = mrow + __log2f(lrow);
-                    __nv_bfloat16* prow = (__nv_bfloat16*)a.ws + (long long)r * 256 + kbase;
+                    __nv_bfloat16* prow = (__nv_bfloat16*)a.ws + (long long)r * pw + kbase;
 #pragma unroll 1
                     for (int cb = 0; cb < 128; cb += 32) {
                         tmem_ld32(trow + cb, v);
@@ -434,8 +442,9 @@ extern "C" int fis_attn(const fis_attn_args* a, void* stream) {
         !encode_2d(&tv, a->vt.ptr, a->dv, a->n_keys, a->vt.ld, dvs))
         return FIS_ERR_UNSUPPORTED;
     static int share_off = getenv("FIS_ATTN_SHARE") && getenv("FIS_ATTN_SHARE")[0] == '0';
-    const bool share = !share_off && a->max_seg_k > 0 && a->max_seg_k <= 256 && a->dv / dvs > 1 && a->ws &&
-                       a->ws_bytes >= (long long)a->m * 256 * 2 && encode_2d(&tp, a->ws, a->m, 256, 256, 128);
+    const long long pw = ((long long)a->max_seg_k + 127) / 128 * 128;
+    const bool share = !share_off && a->max_seg_k > 0 && a->max_seg_k <= 4096 && a->dv / dvs > 1 && a->ws &&
+                       a->ws_bytes >= (long long)a->m * pw * 2 && encode_2d(&tp, a->ws, a->m, pw, pw, 128);
     if (!share) std::memset(&tp, 0, sizeof(tp));
     static bool configured = false;
     if (!configured) {

@@ -454,8 +454,8 @@ class Engine(Launcher):
         if segs is not None:
             qseg, kseg, nseg, maxq, maxk = segs
             a.nseg, a.max_seg_q, a.q_seg, a.k_seg = nseg, maxq, L.ptr(qseg), L.ptr(kseg)
-        if maxk <= 256:  # value slices share one P per query tile (P scratch [m, 256] bf16)
-            ws = self.scratch("attn_p", (m * 256,), torch.bfloat16)
+        if maxk <= 4096:  # value slices share one P per query tile (P scratch [m, 128 * ceil(maxk / 128)])
+            ws = self.scratch("attn_p", (m * _pad(maxk, 128),), torch.bfloat16)
             a.max_seg_k, a.ws, a.ws_bytes = maxk, L.ptr(ws), ws.numel() * 2
         self._call("fis_attn", a)
         self.launches += 1

@@ -190,8 +190,8 @@ def test_segment_attention_vs_torch(env, d, qlens, klens, kpad, share):
                    DRef(out).ref(), None)
     a.nseg, a.max_seg_q, a.q_seg, a.k_seg = len(qseg), max(1, max(qlens)), L.ptr(qs), L.ptr(ks)
     max_k = max(k1 - k0 for k0, k1 in kseg)
-    if share and max_k <= 256:  # value slices share one P per query tile through the scratch
-        ws = torch.empty(m * 256, device="cuda", dtype=bf)
+    if share:  # value slices share one P per query tile through the scratch [m, 128 * ceil(max_k / 128)]
+        ws = torch.empty(m * ((max_k + 127) // 128 * 128), device="cuda", dtype=bf)
         a.max_seg_k, a.ws, a.ws_bytes = max_k, L.ptr(ws), ws.numel() * 2
     L.call("fis_attn", a)
     torch.cuda.synchronize()
