@@ -443,7 +443,12 @@ extern "C" int fis_attn(const fis_attn_args* a, void* stream) {
         return FIS_ERR_UNSUPPORTED;
     static int share_off = getenv("FIS_ATTN_SHARE") && getenv("FIS_ATTN_SHARE")[0] == '0';
     const long long pw = ((long long)a->max_seg_k + 127) / 128 * 128;
+    // long key runs: sharing P trades one extra (serial) launch for 1/slices of the S work, which
+    // pays only when the grid has CTAs to spare (stacked requests), not at batch 1
+    const long long ctas = (long long)(a->dv / dvs) * ((a->nseg > 0 ? a->max_seg_q : a->m) + 127) / 128 *
+                           (a->nseg > 0 ? a->nseg : 1);
     const bool share = !share_off && a->max_seg_k > 0 && a->max_seg_k <= 4096 && a->dv / dvs > 1 && a->ws &&
+                       (a->max_seg_k <= 256 || ctas >= 2 * 148) &&
                        a->ws_bytes >= (long long)a->m * pw * 2 && encode_2d(&tp, a->ws, a->m, pw, pw, 128);
     if (!share) std::memset(&tp, 0, sizeof(tp));
     static bool configured = false;
