@@ -45,7 +45,8 @@ struct GatherMaps {
     CUtensorMap fresh[2], cache[2];
     int fresh_rps[2], cache_rps[2];
 };
-constexpr int LAG = 2;  // cp.async stages in flight per A-producer thread
+constexpr int LAG = 2;
+constexpr int GATHER_WARPS = 2;  // A warps issuing TMA gather4 in the gather mode; the rest use cp.async  // cp.async stages in flight per A-producer thread
 constexpr int SEL_BYTES = BM * 19 * 4;  // select-on-read table [128][18] + row pixels [128]
 
 struct Layout {
@@ -165,7 +166,9 @@ __global__ void __launch_bounds__(THREADS, 1)
 
     if (tid == 0) {
         for (int s = 0; s < L.stages; s++) {
-            mbar_init(full + s, amode == A_CPASYNC ? A_WARPS * 32 + 1 : amode == A_TMA_GATHER ? A_WARPS * 8 + 1 : 1);
+            mbar_init(full + s, amode == A_CPASYNC      ? A_WARPS * 32 + 1
+                                : amode == A_TMA_GATHER ? GATHER_WARPS * 8 + (A_WARPS - GATHER_WARPS) * 32 + 1
+                                                        : 1);
             mbar_init(empty + s, 1);
         }
         for (int b = 0; b < 2; b++) {
@@ -235,12 +238,35 @@ __global__ void __launch_bounds__(THREADS, 1)
                 // lanes 0-7 of each warp own 4-row groups: one TMA gather4 per group and K block when
                 // the 4 rows come from one source (fresh rows / cached pixels, zero padding = OOB
                 // row); a group mixing both sources is copied with cp.async (mask borders only)
+                // (hybrid: warps < GATHER_WARPS issue gather4 for their rows, the other A warps
+                // copy theirs with cp.async, so the TMA unit and the LSU work in parallel)
                 const int g0 = 4 * (warp * 8 + lane);
                 for (int kb = 0; kb < kblocks; kb++, it++) {
                     const int s = it % L.stages;
                     if (it >= L.stages) wait_dbg(empty + s, ((it / L.stages) & 1) ^ 1, dbg, 0, it);
                     if ((dbg & 4) && blockIdx.x == 0 && tid == 0 && it < 256) g_big_trace[0][it] = gtime();
-                    if (lane < 8) {
+                    if (warp >= GATHER_WARPS) {
+                        const int k0 = kb * BK, tap = k0 / cin;
+                        int c = k0 - tap * cin;
+                        const int seg = c >= src0c ? 1 : 0;
+                        c -= seg ? src0c : 0;
+                        const char* fb = (seg ? f1 : f0) + (c + j * 8) * 2;
+                        const char* cb = (seg ? c1p : c0p) + (c + j * 8) * 2;
+                        const long long ldf = (seg ? ldf1 : ldf0) * 2, ldc = (seg ? ldc1 : ldc0) * 2;
+                        const int* selc = seltab + rbase * 18 + seg * 9 + tap;
+                        int v[8];
+#pragma unroll
+                        for (int i = 0; i < 8; i++) v[i] = selc[i * 4 * 18];
+#pragma unroll
+                        for (int i = 0; i < 8; i++) {
+                            const char* src = v[i] == SEL_ZERO ? nullptr
+                                              : v[i] >= 0      ? fb + (long long)v[i] * ldf
+                                                               : cb + (long long)(-2 - v[i]) * ldc;
+                            cp_async16(sbase + s * L.stage + sw128_off(rbase + 4 * i, j),
+                                       src ? (const void*)src : (const void*)dummy, src != nullptr);
+                        }
+                        cp_async_arrive_noinc(full + s);
+                    } else if (lane < 8) {
                         const int k0 = kb * BK, tap = k0 / cin;
                         int c = k0 - tap * cin;
                         const int seg = c >= src0c ? 1 : 0;
