@@ -86,3 +86,22 @@ def test_batched_detected_masks(P):
         if r.mask is not None:
             assert np.array_equal(r.mask.bits, one.mask.bits)
         assert np.abs(r.latent - one.latent).max() <= BF16_FINAL_TOL
+
+
+def test_batched_odd_latent_and_repeat_rounds(P):
+    """96x96 latent (SD-2 shape, C4; levels 96/48/24: dense-level boxes that TMA cannot tile since
+    128 % 48 != 0) and two edit rounds on the same stores (the HBM cache is never compacted)."""
+    cfg = _cfg(P, latent_h=96, latent_w=96, channels=(64, 128, 128))
+    reqs = [((3, 5, 7, 11), (3, 5, 9, 11), (5, 6, 20)), ((2, 4, 6), (2, 8, 6), (40, 55, 24))]
+    stores = [P.CacheStore() for _ in reqs]
+    finals = P.generate_dense_batch([P.PromptTokens(o) for o, _, _ in reqs], cfg, stores)
+    masks = [P.BinaryMask(_square(96, 96, *sq)) for _, _, sq in reqs]
+    for _ in range(2):
+        res = P.edit_batch([P.EditSession.create(o, n, cfg, st, user_mask=m)
+                            for (o, n, _), st, m in zip(reqs, stores, masks)], cfg)
+        for (old, new, _), m, final, r in zip(reqs, masks, finals, res):
+            store = P.CacheStore()
+            P.generate_dense(P.PromptTokens(old), cfg, store, record="engine")
+            one = P.edit(P.EditSession.create(old, new, cfg, store, user_mask=m), cfg, store)
+            assert np.abs(r.latent - one.latent).max() <= BF16_FINAL_TOL
+            assert np.array_equal(r.latent[:, :, ~m.bits], final[:, :, ~m.bits])
