@@ -203,6 +203,8 @@ typedef struct {
     long long ws_bytes;
 } fis_attn_args;
 int fis_attn(const fis_attn_args* a, void* stream);
+/* kernel launches one fis_attn call makes: 1, or 2 when the value slices share P (0: unsupported) */
+int fis_attn_launches(const fis_attn_args* a);
 
 /* 2x2 average pool with select-on-read of the finer map (unet.py:296-298).
  * Output rows are coarse pixels rows[i] (NULL => all (h/2)*(w/2)). */

@@ -426,6 +426,24 @@ static int attn_slice(int dv) {
     return 0;
 }
 
+// P sharing (P_OUT + P_IN launches) for this call? Long key runs trade one extra serial launch for
+// 1/slices of the S work, which pays only when the grid has CTAs to spare (stacked requests).
+static bool attn_share(const fis_attn_args* a, int dvs) {
+    static int share_off = getenv("FIS_ATTN_SHARE") && getenv("FIS_ATTN_SHARE")[0] == '0';
+    const long long pw = ((long long)a->max_seg_k + 127) / 128 * 128;
+    const long long ctas = (long long)(a->dv / dvs) * (((a->nseg > 0 ? a->max_seg_q : a->m) + 127) / 128) *
+                           (a->nseg > 0 ? a->nseg : 1);
+    return !share_off && a->max_seg_k > 0 && a->max_seg_k <= 4096 && a->dv / dvs > 1 && a->ws &&
+           (a->max_seg_k <= 256 || ctas >= 2 * 148) && a->ws_bytes >= (long long)a->m * pw * 2;
+}
+
+// Kernel launches one fis_attn call makes (1, or 2 when the value slices share P); 0 = unsupported.
+extern "C" int fis_attn_launches(const fis_attn_args* a) {
+    const int dvs = attn_slice(a->dv);
+    if (!dvs) return 0;
+    return attn_share(a, dvs) ? 2 : 1;
+}
+
 // Q [m][d], K [n_keys][d] (with segments: n_keys = rows of K), V^T [dv][>= n_keys]; bf16, rows
 // 16-byte aligned, no per-step stride (scratch activations / per-edit text K/V).
 extern "C" int fis_attn(const fis_attn_args* a, void* stream) {
@@ -441,15 +459,8 @@ extern "C" int fis_attn(const fis_attn_args* a, void* stream) {
         !encode_2d(&tk, a->k.ptr, a->n_keys, a->d, a->k.ld, 128) ||
         !encode_2d(&tv, a->vt.ptr, a->dv, a->n_keys, a->vt.ld, dvs))
         return FIS_ERR_UNSUPPORTED;
-    static int share_off = getenv("FIS_ATTN_SHARE") && getenv("FIS_ATTN_SHARE")[0] == '0';
     const long long pw = ((long long)a->max_seg_k + 127) / 128 * 128;
-    // long key runs: sharing P trades one extra (serial) launch for 1/slices of the S work, which
-    // pays only when the grid has CTAs to spare (stacked requests), not at batch 1
-    const long long ctas = (long long)(a->dv / dvs) * ((a->nseg > 0 ? a->max_seg_q : a->m) + 127) / 128 *
-                           (a->nseg > 0 ? a->nseg : 1);
-    const bool share = !share_off && a->max_seg_k > 0 && a->max_seg_k <= 4096 && a->dv / dvs > 1 && a->ws &&
-                       (a->max_seg_k <= 256 || ctas >= 2 * 148) &&
-                       a->ws_bytes >= (long long)a->m * pw * 2 && encode_2d(&tp, a->ws, a->m, pw, pw, 128);
+    const bool share = attn_share(a, dvs) && encode_2d(&tp, a->ws, a->m, pw, pw, 128);
     if (!share) std::memset(&tp, 0, sizeof(tp));
     static bool configured = false;
     if (!configured) {

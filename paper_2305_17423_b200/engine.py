@@ -15,6 +15,7 @@ mutated by an edit (no compaction, cache.py:538-579 is a numerical no-op).
 
 from __future__ import annotations
 
+import ctypes as C
 import math
 import os
 from dataclasses import dataclass
@@ -458,7 +459,7 @@ class Engine(Launcher):
             ws = self.scratch("attn_p", (m * _pad(maxk, 128),), torch.bfloat16)
             a.max_seg_k, a.ws, a.ws_bytes = maxk, L.ptr(ws), ws.numel() * 2
         self._call("fis_attn", a)
-        self.launches += 1
+        self.launches += max(1, L.lib().fis_attn_launches(C.byref(a)))  # kernels (2 when P is shared)
 
     def gn_stats(self, x: DRef, hw, c, mean: DRef, var: DRef, n_img=1):
         a = L.GnStatsArgs(hw, c, self.groups, x.ref(), mean.ref(), var.ref(), L.ptr(self.step_dev), n_img)
