@@ -456,6 +456,11 @@ epilogue_role : {
         const int lr = quarter * 32 + lane;   // tile row of this thread
         const int cstep = nepi == 256 ? 2 : 1;
         const EpiCtx e = make_epi(a, t);
+        // fast row stores: bf16 row-major d (16-byte aligned rows), epilogue = bias (+ residual) only;
+        // same arithmetic as row_epilogue (alpha == 1: v * 1 is exact)
+        const bool fast = a.epi == FIS_EPI_NONE && a.alpha == 1.0f && !e.pre && !e.pre2 && !e.bias2 && !e.lat &&
+                          !a.d_rows && !a.d_trans && a.d.dtype == FIS_BF16 && (a.d.ld % 8) == 0 &&
+                          (((uintptr_t)e.d) & 15) == 0 && (!e.res || (a.res.ld % 8) == 0);
         EpiTab tb;
         tb.mean = tabs;
         tb.rstd = tb.mean + bn;
@@ -497,7 +502,27 @@ epilogue_role : {
                     float v[16];
 #pragma unroll
                     for (int j = 0; j < 16; j++) v[j] = __uint_as_float(u[j]);
-                    row_epilogue_any(a, e, tb, r, cb, n0, v);
+                    const int n = n0 + cb;
+                    if (fast && n + 16 <= (a.n_split > 0 ? a.n_split : a.n)) {
+                        // plain bf16 row store (+ bias, + residual): no per-chunk mode dispatch
+#pragma unroll
+                        for (int j = 0; j < 16; j++) v[j] = __fadd_rn(v[j], tb.bias[cb + j]);
+                        if (e.res) {
+                            float q[16];
+                            load_row16(e.res, a.res.dtype, (long long)r * a.res.ld + n, 16, q);
+#pragma unroll
+                            for (int j = 0; j < 16; j++) v[j] = __fadd_rn(v[j], q[j]);
+                        }
+                        uint4 o[2];
+                        __nv_bfloat162* h = (__nv_bfloat162*)o;
+#pragma unroll
+                        for (int j = 0; j < 8; j++) h[j] = __floats2bfloat162_rn(v[2 * j], v[2 * j + 1]);
+                        uint4* dp = (uint4*)((__nv_bfloat16*)e.d + (long long)r * a.d.ld + n);
+                        dp[0] = o[0];
+                        dp[1] = o[1];
+                    } else {
+                        row_epilogue_any(a, e, tb, r, cb, n0, v);
+                    }
                 }
             }
             tc_fence_before();
