@@ -238,14 +238,19 @@ def run_ours(args):
     batched = None
     R = args.requests if args.requests > 0 else max(1, 64 // ws)  # C5: 64 requests over the box
     if R > 1 and args.precision == "bf16":
+        from paper_2305_17423_b200 import dist as D
         _, tf_peak, _ = peaks()
-        batched = stacked_requests(eng, U, P, cfg, R, args, tf_peak)
+        # C5 sharding: R * N requests assigned to ranks by estimated cost (LPT, SURVEY §8 e)
+        costs = [D.request_cost(_request(i, cfg)[2]) for i in range(R * ws)]
+        ids = D.shard_requests(costs, ws)[rank]
+        batched = stacked_requests(eng, U, P, cfg, R, args, tf_peak, ids=ids)
         # whole job: all ranks' requests over the slowest rank's batched step (no collective in the step)
         batched["edit_steps_per_s_all_ranks"] = ws * R * 1e3 / reduce_max(batched["ms_per_batched_step"])
         batched.update({"masks": "5/10/25% squares at distinct offsets, distinct prompts, own cached generations",
-                        "note": "C5: 64 requests sharded by request over the GPUs, each GPU's R = 64 / N stepped "
-                                "as ONE stacked batch (BatchedEditPlan: concatenated rows, weights read once per "
-                                "step for all R, block-diagonal segment attention); no collective"})
+                        "note": "C5: 64 requests sharded by estimated cost over the GPUs (LPT), each GPU's ~64/N "
+                                "stepped as ONE stacked batch (BatchedEditPlan: concatenated rows, weights read "
+                                "once per step for all of them, block-diagonal segment attention); no collective "
+                                "in the step, one final gather of the edited latents to rank 0"})
     sweep = mask_sweep(eng, U, P, cfg, arena, kv, lat0, args) if args.sweep else None
 
     # --- per-kernel timing of the gated (sparse) convs: eager instrumented step
@@ -384,7 +389,7 @@ def _request(r, cfg):
     return old, new, bits
 
 
-def stacked_requests(eng, U, P, cfg, R, args, peak_tf):
+def stacked_requests(eng, U, P, cfg, R, args, peak_tf, ids=None):
     """C5 throughput on one GPU: R edit requests stepped as ONE stacked batch (BatchedEditPlan:
     concatenated rows, every weight read once per step for all R requests; segment attention).
     Returns a dict: device-timed edit-steps/s over all R requests, the gated-conv gather-GEMMs'
@@ -392,7 +397,9 @@ def stacked_requests(eng, U, P, cfg, R, args, peak_tf):
     host latents out)."""
     import torch
     t0 = time.perf_counter()
-    reqs = [_request(r, cfg) for r in range(R)]
+    ids = list(range(R)) if ids is None else list(ids)
+    R = len(ids)
+    reqs = [_request(r, cfg) for r in ids]
     stores = [P.CacheStore() for _ in reqs]
     eng.ns = 0
     U.generate_dense_batch([P.PromptTokens(o) for o, _, _ in reqs], cfg, stores)
@@ -438,16 +445,24 @@ def stacked_requests(eng, U, P, cfg, R, args, peak_tf):
                 for (o, n, b), st_ in zip(reqs, stores)]
     torch.cuda.synchronize()
     t1 = time.perf_counter()
-    P.edit_batch(sessions, cfg)
+    results = P.edit_batch(sessions, cfg)
     torch.cuda.synchronize()
     e2e_s = time.perf_counter() - t1
     eng.ns = 0
+    # the one collective of the C5 path: edited latents of every rank's requests to rank 0
+    from paper_2305_17423_b200 import dist as D
+    t2 = time.perf_counter()
+    gathered = D.gather_results({i: r.latent for i, r in zip(ids, results)}, D.dist.get_world_size()
+                                if D.is_dist() else 1, device=eng.dev)
+    gather_s = time.perf_counter() - t2
     return {"requests_per_gpu": R, "edit_steps_per_s": R * 1e3 / ms, "ms_per_batched_step": ms,
             "rows_L0_L1": [padded[0], padded.get(1)], "active_L0_L1": [active[0], active[1]],
             "gated_conv": {"achieved_tflops": tf, "peak_tflops": peak_tf, "frac": tf / peak_tf if peak_tf else None,
                            "gflop_per_step": conv_fl / 1e9, "ms_per_step": conv_ms},
             "e2e": {"edit_steps_per_s": R * cfg.steps / e2e_s, "seconds": e2e_s,
                     "note": "one edit_batch() call: R sessions (host masks, prompts) -> R host latents, all T steps"},
+            "result_gather": {"requests_on_rank0": len(gathered), "seconds": gather_s},
+            "request_ids": ids,
             "setup_generation_s": setup_s}
 
 
