@@ -433,8 +433,14 @@ static bool attn_share(const fis_attn_args* a, int dvs) {
     const long long pw = ((long long)a->max_seg_k + 127) / 128 * 128;
     const long long ctas = (long long)(a->dv / dvs) * (((a->nseg > 0 ? a->max_seg_q : a->m) + 127) / 128) *
                            (a->nseg > 0 ? a->nseg : 1);
-    return !share_off && a->max_seg_k > 0 && a->max_seg_k <= 4096 && a->dv / dvs > 1 && a->ws &&
-           (a->max_seg_k <= 256 || ctas >= 2 * 148) && a->ws_bytes >= (long long)a->m * pw * 2;
+    const int slices = a->dv / dvs;
+    if (share_off || a->max_seg_k <= 0 || a->max_seg_k > 4096 || slices < 2 || !a->ws ||
+        a->ws_bytes < (long long)a->m * pw * 2)
+        return false;
+    // one key block: recomputing S per slice is cheap unless the head dim is large (r01: L0 cross
+    // attention 23 + 48 us shared vs one launch unshared)
+    if (a->max_seg_k <= 128) return (long long)a->d * (slices - 1) >= 1280;
+    return a->max_seg_k <= 256 || ctas >= 2 * 148;
 }
 
 // Kernel launches one fis_attn call makes (1, or 2 when the value slices share P); 0 = unsupported.
