@@ -9,10 +9,6 @@ import sys
 from collections import defaultdict
 
 
-def _next_is_attn_pair(seq, s):
-    return True
-
-
 def main(csv_path, seq_path, top=30):
     rows = list(csv.reader(open(csv_path)))
     hdr, ks = None, []
@@ -27,16 +23,14 @@ def main(csv_path, seq_path, top=30):
     seq = [json.loads(l.split(" ", 1)[1]) for l in open(seq_path) if re.match(r"^\d+ \{", l)]
     agg, cnt = defaultdict(float), defaultdict(int)
     i = 0
-    for s in seq:  # an op may launch several kernels (fis_attn with shared P: P_OUT + P_IN)
+    for s in seq:  # a fis_attn op launches one kernel, or two (P_OUT + P_IN) when P is shared
         key = s["op"] + (f" n={s['n']} k={s['k']}" if s["op"] == "fis_gemm" else "") + f" m={s.get('m', s.get('rows'))}"
         t = ks[i][1]
         i += 1
-        if s["op"] == "fis_attn":
-            while i < len(ks) and "attn" in ks[i][0] and (i + 1 >= len(ks) or "attn" in ks[i - 1][0]) and \
-                    ks[i][0] == ks[i - 1][0] and _next_is_attn_pair(seq, s):
-                t += ks[i][1]
-                i += 1
-                break
+        nxt = seq[seq.index(s) + 1]["op"] if s is not seq[-1] else None
+        if s["op"] == "fis_attn" and i < len(ks) and "attn" in ks[i][0] and nxt != "fis_attn":
+            t += ks[i][1]
+            i += 1
         agg[key] += t
         cnt[key] += 1
     tot = sum(t for _, t in ks)
