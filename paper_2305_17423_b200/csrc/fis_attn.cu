@@ -31,12 +31,18 @@ constexpr int A_BYTES = 128 * 64 * 2;            // Q chunk
 constexpr int B_BYTES = 256 * 64 * 2;            // K chunk (128 keys) or V^T chunk (<= 256 rows)
 constexpr int STAGE = A_BYTES + B_BYTES;
 constexpr int P_BYTES = 2 * 128 * 64 * 2;        // P tile: 128 rows x 128 keys, two 64-key SW128 chunks
-constexpr int SMEM = STAGES * STAGE + 2 * P_BYTES + 1024 + 256;
+constexpr int SMEM = STAGES * STAGE + 2 * P_BYTES + 1024 + 256 + 1024;  // + key-split statistics exchange
 constexpr uint32_t O_COL = 256;                  // TMEM: S buffers at 0 / 128, O at 256
 // P sharing across the value slices of a query tile (segments of <= 256 keys): a P_OUT launch
 // (slice 0 only) computes S, the softmax and writes P (bf16, [row][256]) to scratch; the P_IN
 // launch (every slice) TMA-loads those P tiles and runs only P.V + the epilogue
-constexpr int P_NONE = 0, P_OUT = 1, P_IN = 2;
+// P_OUT_KS: P_OUT for two-block key runs split over a 2-CTA cluster (CTA = one key block); the
+// row max / sum of the two blocks are exchanged through distributed shared memory
+constexpr int P_NONE = 0, P_OUT = 1, P_IN = 2, P_OUT_KS = 3;
+
+FIS_DEV void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
 
 FIS_DEV void tma2d(uint32_t dst, const void* tmap, int c0, int c1, uint64_t* bar) {
     asm volatile(
@@ -85,7 +91,9 @@ FIS_DEV void tmem_ld32(uint32_t taddr, float* v) {
 // step u issues S_u (u < nkb) and then P_{u-1}.V_{u-1} (u >= 1).
 __global__ void __launch_bounds__(THREADS, 1)
     attn_kernel(const fis_attn_args a, const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
-                const __grid_constant__ CUtensorMap tv, const __grid_constant__ CUtensorMap tp, int dvs, int pmode) {
+                const __grid_constant__ CUtensorMap tv, const __grid_constant__ CUtensorMap tp, int dvs, int pmode_in) {
+    const bool ks = pmode_in == P_OUT_KS;
+    const int pmode = ks ? P_OUT : pmode_in;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     unsigned char* ptile = smem + STAGES * STAGE;
@@ -97,6 +105,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     uint64_t* p_free = p_ready + 2;      // [2]
     uint64_t* o_done = p_free + 2;
     uint32_t* tmem_slot = (uint32_t*)(o_done + 1);
+    float2* xst = (float2*)(ptile + 2 * P_BYTES + 256);  // [128] key-split (max, sum) exchange
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     int q_beg = 0, q_end = a.m, k_beg = 0, n_keys = a.n_keys;
@@ -107,8 +116,20 @@ __global__ void __launch_bounds__(THREADS, 1)
         k_beg = __ldg(a.k_seg + 2 * sg);
         n_keys = __ldg(a.k_seg + 2 * sg + 1) - k_beg;
     }
-    const int m0 = q_beg + blockIdx.y * 128, c0 = blockIdx.x * dvs;
-    if (m0 >= q_end || n_keys <= 0) return;  // uniform for the CTA, before any barrier
+    const int m0 = q_beg + blockIdx.y * 128, c0 = ks ? 0 : blockIdx.x * dvs;
+    if (m0 >= q_end || n_keys <= 0) return;  // uniform for the CTA (and its cluster peer), before any barrier
+    // key split: this CTA owns key block blockIdx.x of the run; a run of <= 128 keys leaves CTA 1 idle
+    const int kb_off = ks ? (int)blockIdx.x * 128 : 0;
+    bool idle = false;
+    if (ks) {
+        k_beg += kb_off;
+        n_keys -= kb_off;
+        if (n_keys <= 0) {
+            idle = true;
+            n_keys = 1;
+        }
+        if (n_keys > 128) n_keys = 128;
+    }
     const int nkb = (n_keys + 127) / 128, dch = a.d / 64;
     const bool single = nkb == 1;
     // two key blocks: both S blocks stay resident in the two TMEM buffers, so the statistics pass
@@ -147,6 +168,9 @@ __global__ void __launch_bounds__(THREADS, 1)
     pdl_wait();
     const int t = cur_step(a.step);
 
+    if (idle && warp != TMA_WARP && warp != MMA_WARP) goto ks_softmax;
+    if (idle) goto done;
+    if (ks && warp < 4) goto ks_softmax;
     if (warp == TMA_WARP) {
         // ------------------------------------------------------------ TMA producer
         if (lane == 0) {
@@ -410,7 +434,74 @@ __global__ void __launch_bounds__(THREADS, 1)
             }
         }
     }
+    goto done;
+ks_softmax : {
+        // key split (P_OUT_KS): statistics of this CTA's key block, exchange with the peer block's
+        // through DSMEM, then P of this block from the same (resident) S
+        const int lr = tid, r = m0 + lr;
+        const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
+        const float sl = a.scale * 1.4426950408889634f;
+        float mrow = -INFINITY, lrow = 0.f;
+        float v[32];
+        if (!idle) {
+            mbar_wait(s_ready, 0);
+            tc_fence_after();
+#pragma unroll 1
+            for (int cb = 0; cb < 128; cb += 32) {
+                tmem_ld32(trow + cb, v);
+                const int lim = n_keys - cb;
+                float cm = -INFINITY;
+#pragma unroll
+                for (int q = 0; q < 32; q++)
+                    if (q < lim) cm = fmaxf(cm, v[q]);
+                const float mn = fmaxf(mrow, cm * sl);
+                float add = 0.f;
+#pragma unroll
+                for (int q = 0; q < 32; q++)
+                    if (q < lim) add += ex2(fmaf(v[q], sl, -mn));
+                lrow = (mrow == -INFINITY ? 0.f : lrow * ex2(mrow - mn)) + add;
+                mrow = mn;
+            }
+        }
+        xst[lr] = make_float2(mrow, lrow);
+        cluster_sync_all();  // phase 1: both blocks' statistics written
+        uint32_t ra;
+        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(smem_u32(xst + lr)), "r"((int)blockIdx.x ^ 1));
+        float pm, pl;
+        asm volatile("ld.shared::cluster.v2.f32 {%0, %1}, [%2];" : "=f"(pm), "=f"(pl) : "r"(ra) : "memory");
+        const float M = fmaxf(mrow, pm);
+        const float Ls = (mrow == -INFINITY ? 0.f : lrow * ex2(mrow - M)) + (pm == -INFINITY ? 0.f : pl * ex2(pm - M));
+        if (!idle) {
+            const float off = M + __log2f(Ls);
+            __nv_bfloat16* prow = (__nv_bfloat16*)a.ws + (long long)r * pw + kb_off;
+#pragma unroll 1
+            for (int cb = 0; cb < 128; cb += 32) {
+                tmem_ld32(trow + cb, v);
+                const int lim = n_keys - cb;
+#pragma unroll
+                for (int u = 0; u < 4; u++) {
+                    uint4 pk;
+                    __nv_bfloat162* h = (__nv_bfloat162*)&pk;
+#pragma unroll
+                    for (int e2 = 0; e2 < 4; e2++) {
+                        const int q0 = 8 * u + 2 * e2;
+                        const float p0 = q0 < lim ? ex2(fmaf(v[q0], sl, -off)) : 0.f;
+                        const float p1 = q0 + 1 < lim ? ex2(fmaf(v[q0 + 1], sl, -off)) : 0.f;
+                        h[e2] = __floats2bfloat162_rn(p0, p1);
+                    }
+                    if (r < q_end) *(uint4*)(prow + cb + 8 * u) = pk;
+                }
+            }
+        }
+        cluster_sync_all();  // phase 2: the peer has read our statistics
+        goto teardown;
+    }
 done:
+    if (ks) {  // producer / MMA warps (and an idle CTA's) take part in both cluster phases
+        cluster_sync_all();
+        cluster_sync_all();
+    }
+teardown:
     tc_fence_before();
     __syncthreads();
     if (warp == MMA_WARP) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
@@ -487,10 +578,28 @@ extern "C" int fis_attn(const fis_attn_args* a, void* stream) {
     cfg.attrs = attr;
     cfg.numAttrs = fis_pdl_enabled() ? 1 : 0;
     if (share) {  // P once per query tile (slice 0), then every slice's P.V from the scratch
-        cfg.gridDim = dim3(1, grid.y, grid.z);
-        if (cudaLaunchKernelEx(&cfg, fis::attn::attn_kernel, *a, tq, tk, tv, tp, dvs, (int)fis::attn::P_OUT) !=
-            cudaSuccess)
+        static int ks_off = getenv("FIS_ATTN_KSPLIT") && getenv("FIS_ATTN_KSPLIT")[0] == '0';
+        const bool ksplit = !ks_off && a->max_seg_k > 128 && a->max_seg_k <= 256;
+        cudaLaunchAttribute at2[2];
+        at2[0] = attr[0];
+        at2[1].id = cudaLaunchAttributeClusterDimension;
+        at2[1].val.clusterDim.x = 2;
+        at2[1].val.clusterDim.y = 1;
+        at2[1].val.clusterDim.z = 1;
+        cfg.gridDim = dim3(ksplit ? 2 : 1, grid.y, grid.z);
+        if (ksplit) {  // two key blocks over a 2-CTA cluster
+            cfg.attrs = at2;
+            cfg.numAttrs = 2;
+            if (!fis_pdl_enabled()) {
+                cfg.attrs = at2 + 1;
+                cfg.numAttrs = 1;
+            }
+        }
+        if (cudaLaunchKernelEx(&cfg, fis::attn::attn_kernel, *a, tq, tk, tv, tp, dvs,
+                               (int)(ksplit ? fis::attn::P_OUT_KS : fis::attn::P_OUT)) != cudaSuccess)
             return FIS_ERR_LAUNCH;
+        cfg.attrs = attr;
+        cfg.numAttrs = fis_pdl_enabled() ? 1 : 0;
     }
     cfg.gridDim = grid;
     return cudaLaunchKernelEx(&cfg, fis::attn::attn_kernel, *a, tq, tk, tv, tp, dvs,
