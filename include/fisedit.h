@@ -216,6 +216,10 @@ typedef struct {
     const int* step;
 } fis_pool_args;
 int fis_pool2(const fis_pool_args* a, void* stream);
+/* Nearest 2x upsample (unet.py:301-302) of the (dense) source map src [img][h][w][c] into
+ * out [img][2h][2w][c]; n = output pixels. Materialises the coarse half of a fuse concat so the
+ * fuse conv of a dense level can stage its A operand with TMA (stacked requests). */
+int fis_up2(const fis_pool_args* a, void* stream);
 
 /* Materialise a full map from a selectable source: out[q] = value(q) for all q.
  * Replaces the cached-copy + pixel scatter of sparse ops (sparse.py:209-220,248-250,298-299). */

@@ -122,7 +122,7 @@ VM_KINDS = {"fis_gemm": (1, "gemm"), "fis_softmax": (2, "softmax"), "fis_gn_stat
 
 _SIGS = {
     "fis_gemm": GemmArgs, "fis_attn": AttnArgs, "fis_xattn": XattnArgs, "fis_gn_stats": GnStatsArgs, "fis_gn_apply": GnApplyArgs, "fis_softmax": SoftmaxArgs,
-    "fis_pool2": PoolArgs, "fis_materialize": MaterializeArgs, "fis_mask_detect": MaskDetectArgs,
+    "fis_pool2": PoolArgs, "fis_up2": PoolArgs, "fis_materialize": MaterializeArgs, "fis_mask_detect": MaskDetectArgs,
     "fis_mask_plan": MaskPlanArgs, "fis_vm_run": VmArgs,
 }
 

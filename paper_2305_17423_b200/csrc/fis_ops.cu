@@ -334,6 +334,25 @@ __global__ void materialize_kernel(const fis_materialize_args a) {
     }
 }
 
+// ---- nearest 2x upsample of a dense map (unet.py:301-302), 8 channels per thread
+__global__ void up2_kernel(const fis_pool_args a) {
+    pdl_trigger();
+    pdl_wait();
+    const int t = cur_step(a.step);
+    const char* fr = ref_base(a.src.fresh, t);
+    char* out = ref_base(a.out, t);
+    const int ow = 2 * a.src.w, ohw = 4 * a.src.h * a.src.w, cv = a.c / 8;
+    const long long total = (long long)a.n * cv;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total; e += (long long)gridDim.x * blockDim.x) {
+        const int p = (int)(e / cv), c = (int)(e - (long long)p * cv) * 8;
+        const int img = p / ohw, lp = p - img * ohw;
+        const int y = lp / ow, x = lp - y * ow;
+        const long long q = (long long)img * a.src.h * a.src.w + (y >> 1) * a.src.w + (x >> 1);
+        *(uint4*)((__nv_bfloat16*)out + (long long)p * a.out.ld + c) =
+            *(const uint4*)((const __nv_bfloat16*)fr + q * a.src.fresh.ld + c);
+    }
+}
+
 static int grid_for(long long total, int threads) {
     long long b = (total + threads - 1) / threads;
     if (b < 1) b = 1;
@@ -355,6 +374,16 @@ extern "C" int fis_gn_apply(const fis_gn_apply_args* a, void* stream) {
     if (a->rows == 0) return FIS_OK;
     long long total = (long long)a->rows * a->c;
     return fis_launch(fis::gn_apply_kernel, dim3(fis::grid_for(total, 256)), dim3(256), 0, (cudaStream_t)stream, *a) ==
+                   cudaSuccess ? FIS_OK : FIS_ERR_LAUNCH;
+}
+
+extern "C" int fis_up2(const fis_pool_args* a, void* stream) {
+    if (a->n == 0) return FIS_OK;
+    if (a->src.index || a->src.fresh.dtype != FIS_BF16 || a->out.dtype != FIS_BF16 || a->c % 8 ||
+        (a->src.fresh.ld % 8) || (a->out.ld % 8))
+        return FIS_ERR_UNSUPPORTED;
+    const long long total = (long long)a->n * (a->c / 8);
+    return fis_launch(fis::up2_kernel, dim3(fis::grid_for(total, 256)), dim3(256), 0, (cudaStream_t)stream, *a) ==
                    cudaSuccess ? FIS_OK : FIS_ERR_LAUNCH;
 }
 

@@ -486,6 +486,13 @@ class Engine(Launcher):
         self._call("fis_pool2", a)
         self.launches += 1
 
+    def up2(self, fv: FeatVal, n, out: DRef):
+        a = L.PoolArgs()
+        a.n, a.c, a.src, a.rows, a.out = n, fv.c, self.src(fv), None, out.ref()
+        a.step = L.ptr(self.step_dev)
+        self._call("fis_up2", a)
+        self.launches += 1
+
     def materialize(self, fv: FeatVal, out: DRef, n_img: int = 1):
         src = self.src(fv)
         src.h *= n_img  # stacked images: a per-pixel op over n_img * h * w pixels
@@ -534,8 +541,16 @@ class Engine(Launcher):
                 vals[fo.key] = plan.value(fo)
             elif op == "fuse":
                 lid, fu, fs, fo = ins[1], ins[2], ins[3], ins[4]
-                self._conv(plan, lid, [(vals[fu.key], True), (vals[fs.key], False)], plan.out_buf(fo), fo.level,
-                           pre=plan.record(lid, 0))
+                up = vals[fu.key]
+                if plan.batch > 1 and not plan.sparse(fo.level) and up.index is None and self.act == torch.bfloat16:
+                    # stacked dense level: materialise the 2x upsample once so the fuse conv's A
+                    # operand is a dense map the persistent GEMM stages with TMA
+                    buf = DRef(self.scratch(f"up{fo.level}", (self.cap(fo.level), fu.channels)))
+                    self.up2(up, self.cap(fo.level), buf)
+                    srcs = [(FeatVal(buf, fo.level, fu.channels), False), (vals[fs.key], False)]
+                else:
+                    srcs = [(up, True), (vals[fs.key], False)]
+                self._conv(plan, lid, srcs, plan.out_buf(fo), fo.level, pre=plan.record(lid, 0))
                 vals[fo.key] = plan.value(fo)
             else:  # out conv + step update
                 lid, fi = ins[1], ins[2]
