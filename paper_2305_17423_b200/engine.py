@@ -372,6 +372,29 @@ class Engine(Launcher):
             out[lid] = (k, vt, v)
         return out
 
+    def text_kv_stacked(self, text_embs):
+        """Text K / V^T of R prompts computed as ONE GEMM pair per cross layer over the stacked
+        embeddings (each prompt padded to pad16(max tokens) zero rows, so the pad keys are zero):
+        returns ({lid: (K [R*ks, C], V^T [C, R*ks], None)}, key segments int32 [2R], max tokens)."""
+        R = len(text_embs)
+        nts = [e.shape[0] for e in text_embs]
+        ks = _pad(max(nts))
+        emb = np.zeros((R * ks, text_embs[0].shape[1]), dtype=np.float32)
+        for r, e in enumerate(text_embs):
+            emb[r * ks: r * ks + nts[r]] = e
+        emb_d = torch.from_numpy(emb).to(self.dev)
+        out = {}
+        for lid, (wq, wk, wv, scale) in self.W.ca.items():
+            c = wq.shape[0]
+            k = torch.empty((R * ks, c), dtype=self.act, device=self.dev)
+            vt = torch.empty((c, R * ks), dtype=self.act, device=self.dev)
+            self.gemm(R * ks, c, emb.shape[1], a=DRef(emb_d), b=DRef(wk), d=DRef(k))
+            self.gemm(R * ks, c, emb.shape[1], a=DRef(emb_d), b=DRef(wv), d=DRef(vt), d_trans=True)
+            out[lid] = (k, vt, None)
+        kseg = torch.tensor([v for r in range(R) for v in (r * ks, r * ks + nts[r])], dtype=torch.int32,
+                            device=self.dev)
+        return out, kseg, max(nts)
+
     # ------------------------------------------------------------ building blocks
     def attn_self(self, lid, m, s: DRef, y1: DRef, level, tag, pre=None, segs=None):
         """y1 = s + softmax(s Wq (s Wk)^T * scale) (s Wv) over m tokens (sparse.py:265-300/341-349).

@@ -527,10 +527,12 @@ class BatchedEditPlan:
     row lists (each request's run padded to 16 rows), stacked pixel->row maps, attention
     segments and the BatchedSparsePlan that steps them as one batch."""
 
-    def __init__(self, eng: Engine, stacked: Arena, masks, kvs, lat0s):
+    def __init__(self, eng: Engine, stacked: Arena, masks, kvs, lat0s, stacked_kv=None):
+        """kvs: per-request text K/V dicts (Engine.text_kv), or None with stacked_kv =
+        Engine.text_kv_stacked(...) (one GEMM pair per cross layer for all requests)."""
         cfg = eng.config
         R = stacked.batch
-        if not (len(masks) == len(kvs) == len(lat0s) == R):
+        if not (len(masks) == len(lat0s) == R and (kvs is None or len(kvs) == R)):
             raise ContractViolation(f"need {R} masks / prompts / start latents for a {R}-request arena")
         if eng.act != torch.bfloat16:
             raise ContractViolation("batched edits run in bf16 (fused segment attention)")
@@ -567,10 +569,13 @@ class BatchedEditPlan:
         lat0 = torch.cat(list(lat0s), 0)
         r0, _, n0 = lists[0]
         self.lat_rows = lat0.index_select(0, r0[:n0].long()).contiguous()
-        kv, kseg = stack_text_kv(eng, kvs)
+        if stacked_kv is not None:
+            kv, kseg, max_keys = stacked_kv
+        else:
+            kv, kseg = stack_text_kv(eng, kvs)
+            lid0 = next(iter(kvs[0]))
+            max_keys = max(kv_[lid0][0].shape[0] for kv_ in kvs)
         self.kv = kv
-        lid0 = next(iter(kvs[0]))
-        max_keys = max(kv[lid0][0].shape[0] for kv in kvs)
         self.plan = BatchedSparsePlan(eng, kv, stacked, lists, self.lat_rows, qsegs, kseg, row_img, max_keys)
 
     def final_latents(self, eng: Engine, stacked: Arena) -> torch.Tensor:
@@ -606,23 +611,27 @@ def edit_batch(sessions, config: UNetConfig) -> list:
     start = starts.pop()
     eng = get_engine(config, stacked.eng.precision)
     cl, H, W, T = config.latent_channels, config.latent_h, config.latent_w, config.steps
-    masks, kvs, lat0s = [], [], []
+    masks, lat0s = [], []
+    lat_init = None
     for s, o, v in zip(sessions, outcomes, views):
         s.mask = o.mask
         # a no-edit request rides along with an empty mask: its latent stays the cached one
         masks.append(o.mask if o.mask is not None else BinaryMask(np.zeros((H, W), dtype=bool)))
-        kvs.append(eng.text_kv(embed_tokens(s.new_tokens, config)))
         if o.from_user_mask or o.mask is None:
-            lat0s.append(_to_nhwc(initial_latent_np(config), eng.dev))
+            if lat_init is None:  # the seeded initial latent is the same for every request
+                lat_init = _to_nhwc(initial_latent_np(config), eng.dev)
+            lat0s.append(lat_init)
         else:
             m = torch.from_numpy(o.mask.bits.ravel().copy()).to(eng.dev)[:, None]
             lat0s.append(torch.where(m, o._control_dev, v.latent[s.t2]))
-    bp = BatchedEditPlan(eng, stacked, masks, kvs, lat0s)
+    skv = eng.text_kv_stacked([embed_tokens(s.new_tokens, config) for s in sessions])
+    bp = BatchedEditPlan(eng, stacked, masks, None, lat0s, stacked_kv=skv)
     _Runner(eng, bp.plan, _use_graphs()).run(start, T)
     final = bp.final_latents(eng, stacked)
     hw = eng.hw(0)
+    fin = final.view(len(sessions), H, W, cl).permute(0, 3, 1, 2).contiguous().cpu().numpy()  # one D2H
     results = [None] * len(sessions)
     for r, (s, o) in enumerate(zip(sessions, outcomes)):
-        lat = _to_nchw(final[r * hw:(r + 1) * hw], cl, H, W)
-        results[order[r]] = EditResult(lat, None, s.store.stats(), o.mask, o.no_edit, o.phase1_macs.total, 0)
+        results[order[r]] = EditResult(fin[r:r + 1], None, s.store.stats(), o.mask, o.no_edit,
+                                       o.phase1_macs.total, 0)
     return results
