@@ -423,6 +423,46 @@ class EditPlan:
         return out
 
 
+_GRAPHS: "OrderedDict" = None
+_GRAPH_CACHE_SIZE = 8
+
+
+def _cached_runner(eng: Engine, arena: Arena, start: int, ep: "EditPlan", kv):
+    """Step runner of an edit, reusing a captured step graph when an earlier edit on the same
+    cached generation had the same active-row counts per level (same launch shapes): the new
+    edit's row lists, pixel->row maps, start latent rows and text K/V are copied (device to
+    device) into the buffers that graph reads, instead of capturing a new one."""
+    global _GRAPHS
+    from collections import OrderedDict
+    if _GRAPHS is None:
+        _GRAPHS = OrderedDict()
+    if not _use_graphs() or eng.use_vm:
+        return _Runner(eng, ep.plan, _use_graphs())
+    n_text = next(iter(kv.values()))[0].shape[0]
+    key = (id(eng), id(arena), start, tuple(ep.dp.n_active), n_text)
+    hit = _GRAPHS.get(key)
+    if hit is None:
+        runner = _Runner(eng, ep.plan, True)
+        _GRAPHS[key] = (runner, ep, kv)
+        if len(_GRAPHS) > _GRAPH_CACHE_SIZE:
+            _GRAPHS.popitem(last=False)
+        return runner
+    runner, ep0, kv0 = hit
+    _GRAPHS.move_to_end(key)
+    for l in range(len(ep.dp.rows)):
+        ep0.dp.rows[l].copy_(ep.dp.rows[l])
+        ep0.dp.index[l].copy_(ep.dp.index[l])
+    ep0.lat_rows.copy_(ep.lat_rows)
+    for lid, tens in kv.items():
+        for dst, src in zip(kv0[lid], tens):
+            if dst is not None:
+                dst.copy_(src)
+    # the caller keeps using `ep` for results: point it at the buffers the graph updates
+    ep.lat_rows = ep0.lat_rows
+    ep.dp.index = ep0.dp.index
+    return runner
+
+
 def edit(session: EditSession, config: UNetConfig, store: CacheStore) -> EditResult:
     """Incremental regeneration for the edited prompt (unet.py:823-899) on the B200 engine."""
     unet = UNet(config)
@@ -457,7 +497,7 @@ def edit(session: EditSession, config: UNetConfig, store: CacheStore) -> EditRes
             phase2.add(lid, m_ * (T - start + 1))
     else:
         ep = EditPlan(eng, arena, mask, kv, lat0)
-        _Runner(eng, ep.plan, _use_graphs()).run(start, T)
+        _cached_runner(eng, arena, start, ep, kv).run(start, T)
         final = ep.final_latent(eng, arena)
         levels = sorted({i.level for i in unet.layers if i.gated})
         cost = {l: 4 * ep.dp.n_tiles[l] for l in range(config.levels)}

@@ -150,3 +150,24 @@ def test_concurrent_requests_match_sequential(P):
     seq, conc = run(False), run(True)
     for a, b in zip(seq, conc):
         assert torch.equal(a, b)
+
+
+def test_edit_graph_reuse_matches_fresh_capture(P):
+    """A second edit on the same cached generation with the same active-row counts per level reuses
+    the first edit's captured step graph (new lists / latent rows / text K/V copied in); it must
+    give bitwise the same latent as a freshly captured graph."""
+    from paper_2305_17423_b200 import unet as U
+    cfg = _cfg(P)
+    store = P.CacheStore()
+    P.generate_dense(P.PromptTokens(OLD), cfg, store, record="engine")
+    b1 = np.zeros((32, 32), bool)
+    b1[4:12, 6:14] = True
+    b2 = np.zeros((32, 32), bool)
+    b2[16:24, 18:26] = True  # same 8x8 size -> same counts per level
+    U._GRAPHS = None
+    P.edit(P.EditSession.create(OLD, NEW, cfg, store, user_mask=P.BinaryMask(b1)), cfg, store)
+    reused = P.edit(P.EditSession.create(OLD, (3, 5, 13, 11), cfg, store, user_mask=P.BinaryMask(b2)), cfg, store)
+    assert len(U._GRAPHS) == 1  # the second edit hit the first one's graph
+    U._GRAPHS = None
+    fresh = P.edit(P.EditSession.create(OLD, (3, 5, 13, 11), cfg, store, user_mask=P.BinaryMask(b2)), cfg, store)
+    assert np.array_equal(reused.latent, fresh.latent)
