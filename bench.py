@@ -217,11 +217,19 @@ def run_ours(args):
 
     # --- end-to-end through the public API (host mask in, host latent out, all T steps); measured
     # before the batched section so its ~100 GB stacked arena does not sit in the allocator
+    # a stream of E2E_CALLS edit requests on the rank's cached generation: the 10% square at
+    # shifted offsets (same size), one edit() call each (sessions built from host ids / masks)
+    e2e_masks = []
+    for i in range(E2E_CALLS):
+        b = np.roll(mask.bits, (2 * i, -2 * i), axis=(0, 1))
+        e2e_masks.append(P.BinaryMask(b))
+    sessions = [P.EditSession.create(OLD_IDS, NEW_IDS, cfg, store, user_mask=m) for m in e2e_masks]
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    P.edit(P.EditSession.create(OLD_IDS, NEW_IDS, cfg, store, user_mask=mask), cfg, store)
+    for s_ in sessions:
+        P.edit(s_, cfg, store)
     torch.cuda.synchronize()
-    e2e_s = reduce_max(time.perf_counter() - t0)
+    e2e_s = reduce_max((time.perf_counter() - t0) / E2E_CALLS)
     # --- the same sparse step on the persistent step VM (csrc/fis_vm.cu; experimental engine)
     vm_ms = None
     if args.precision == "bf16":
@@ -286,7 +294,8 @@ def run_ours(args):
         "clocks": clk.summary(),
         "e2e": {"value": T / e2e_s, "unit": "edit-steps/s", "h2d_bytes_per_step": (cfg.latent_h * cfg.latent_w * 17) // T,
                 "d2h_bytes_per_step": (4 * cfg.latent_h * cfg.latent_w * cfg.latent_channels + 64) // T,
-                "note": "one full P.edit() call (T steps, planning, graph capture, H2D mask/latent, D2H result)"},
+                "note": f"{E2E_CALLS} consecutive P.edit() calls (each: T steps, planning, text K/V, H2D mask/latent, "
+                        "D2H result; the first captures the step graph, the next reuse it with their inputs copied in)"},
     }
     if rank == 0 and not args.no_cpu:
         v, per = cpu_sample(C2, args.mask, 1, 0, os.cpu_count() or 1)
@@ -303,6 +312,7 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+E2E_CALLS = 3
 WEIGHT_BYTES_BF16 = 2 * 221_700_000  # 221.7 M params of the SD-1.5-shape toy UNet
 
 
@@ -408,7 +418,7 @@ def stacked_requests(eng, U, P, cfg, R, args, peak_tf, ids=None):
     kvs = [eng.text_kv(P.embed_tokens(P.PromptTokens(n), cfg)) for _, n, _ in reqs]
     lat0 = U._to_nhwc(P.initial_latent(cfg), eng.dev)
     bp = U.BatchedEditPlan(eng, stacked, [P.BinaryMask(b) for _, _, b in reqs], kvs, [lat0] * R)
-    run = U._Runner(eng, bp.plan, True, ns=100)
+    run = U._Runner(eng, bp.plan, True, ns=0)  # edit_batch() below reuses this warm scratch namespace
     ms = _time_runner(run, cfg.steps, max(3, args.steps // 2), 3)
     # gated-conv gather-GEMMs of the batched step: CUDA events around each launch (eager step);
     # algorithmic FLOPs count active rows only (each request's run is padded to 16 rows)
@@ -424,7 +434,7 @@ def stacked_requests(eng, U, P, cfg, R, args, peak_tf, ids=None):
 
     eng.gemm = timed
     try:
-        eng.ns = 100
+        eng.ns = 0
         eng.step_dev.fill_(5)
         eng.run_step(bp.plan)
         torch.cuda.synchronize()

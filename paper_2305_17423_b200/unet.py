@@ -439,7 +439,8 @@ def _cached_runner(eng: Engine, arena: Arena, start: int, ep: "EditPlan", kv):
     if not _use_graphs() or eng.use_vm:
         return _Runner(eng, ep.plan, _use_graphs())
     n_text = next(iter(kv.values()))[0].shape[0]
-    key = (id(eng), id(arena), start, tuple(ep.dp.n_active), n_text)
+    gated = tuple(n for l, n in enumerate(ep.dp.n_active) if eng.gated[l])  # only gated levels shape launches
+    key = (id(eng), id(arena), start, gated, n_text)
     hit = _GRAPHS.get(key)
     if hit is None:
         runner = _Runner(eng, ep.plan, True)
