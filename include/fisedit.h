@@ -139,6 +139,10 @@ typedef struct {
     int img_rows;           /* > 0: row r uses the statistics of image r / img_rows (mean/var [img][groups]) */
     const int* row_img;     /* optional per-row image index (overrides img_rows) */
 } fis_gn_apply_args;
+/* Dense group norm computing its own statistics (group_norm, tensors.py:129-146, + SiLU):
+ * rows = n_img * img_rows (img_rows = 0: one image), statistics written to mean / var
+ * [img][groups]; no row lists. One launch for bf16 maps with 8 | channels per group. */
+int fis_gn(const fis_gn_apply_args* a, void* stream);
 int fis_gn_apply(const fis_gn_apply_args* a, void* stream);
 
 /* Row softmax of scaled scores, optional controlled-mode column substitution.

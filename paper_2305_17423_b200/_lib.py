@@ -121,7 +121,7 @@ VM_KINDS = {"fis_gemm": (1, "gemm"), "fis_softmax": (2, "softmax"), "fis_gn_stat
             "fis_attn": (7, "attn"), "fis_gn": (8, "gn_apply")}
 
 _SIGS = {
-    "fis_gemm": GemmArgs, "fis_attn": AttnArgs, "fis_xattn": XattnArgs, "fis_gn_stats": GnStatsArgs, "fis_gn_apply": GnApplyArgs, "fis_softmax": SoftmaxArgs,
+    "fis_gemm": GemmArgs, "fis_attn": AttnArgs, "fis_xattn": XattnArgs, "fis_gn_stats": GnStatsArgs, "fis_gn_apply": GnApplyArgs, "fis_gn": GnApplyArgs, "fis_softmax": SoftmaxArgs,
     "fis_pool2": PoolArgs, "fis_up2": PoolArgs, "fis_materialize": MaterializeArgs, "fis_mask_detect": MaskDetectArgs,
     "fis_mask_plan": MaskPlanArgs, "fis_vm_run": VmArgs,
 }

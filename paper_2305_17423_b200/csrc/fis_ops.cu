@@ -353,6 +353,86 @@ __global__ void up2_kernel(const fis_pool_args a) {
     }
 }
 
+// ---- dense group norm in one launch (statistics + normalise + SiLU), bf16 maps, one CTA per
+// (group, stacked image): the group's hw x cpg block is read three times from L2 instead of
+// a statistics launch followed by a separate apply launch (same arithmetic as the pair)
+__global__ void __launch_bounds__(256) gn_fused_kernel(const fis_gn_apply_args a) {
+    pdl_trigger();
+    pdl_wait();
+    const int hw = a.img_rows;  // pixels per image (set by fis_gn)
+    const int t = cur_step(a.step);
+    const int g = blockIdx.x, img = blockIdx.y, tid = threadIdx.x;
+    const int cpg = a.c / a.groups, vpg = cpg / 8, items = hw * vpg;
+    const long long cnt = (long long)hw * cpg;
+    const __nv_bfloat16* x = (const __nv_bfloat16*)ref_base(a.x, t) + (long long)img * hw * a.x.ld + g * cpg;
+    __shared__ double red[256];
+    float ps = 0.f;
+    for (int i = tid; i < items; i += blockDim.x) {
+        const int q = i / vpg, v = i - q * vpg;
+        const uint4 u = *(const uint4*)(x + (long long)q * a.x.ld + v * 8);
+        const __nv_bfloat162* h = (const __nv_bfloat162*)&u;
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+            const float2 f = __bfloat1622float2(h[k]);
+            ps += f.x + f.y;
+        }
+    }
+    red[tid] = (double)ps;
+    __syncthreads();
+    for (int o = 128; o; o >>= 1) {
+        if (tid < o) red[tid] += red[tid + o];
+        __syncthreads();
+    }
+    const float mf = (float)(red[0] / (double)cnt);
+    __syncthreads();
+    float pv = 0.f;
+    for (int i = tid; i < items; i += blockDim.x) {
+        const int q = i / vpg, v = i - q * vpg;
+        const uint4 u = *(const uint4*)(x + (long long)q * a.x.ld + v * 8);
+        const __nv_bfloat162* h = (const __nv_bfloat162*)&u;
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+            const float2 f = __bfloat1622float2(h[k]);
+            const float d0 = f.x - mf, d1 = f.y - mf;
+            pv = fmaf(d0, d0, fmaf(d1, d1, pv));
+        }
+    }
+    red[tid] = (double)pv;
+    __syncthreads();
+    for (int o = 128; o; o >>= 1) {
+        if (tid < o) red[tid] += red[tid + o];
+        __syncthreads();
+    }
+    const float vf = (float)(red[0] / (double)cnt);
+    if (tid == 0) {
+        ((float*)ref_base(a.mean, t))[img * a.groups + g] = mf;
+        ((float*)ref_base(a.var, t))[img * a.groups + g] = vf;
+    }
+    const float rstd = (float)(1.0 / sqrt((double)vf + (double)a.eps));
+    char* yn = a.y_norm.ptr ? ref_base(a.y_norm, t) : nullptr;
+    char* ys = a.y_silu.ptr ? ref_base(a.y_silu, t) : nullptr;
+    for (int i = tid; i < items; i += blockDim.x) {
+        const int q = i / vpg, v = i - q * vpg;
+        const int c = g * cpg + v * 8;
+        const long long row = (long long)img * hw + q;
+        const uint4 u = *(const uint4*)(x + (long long)q * a.x.ld + v * 8);
+        const __nv_bfloat162* h = (const __nv_bfloat162*)&u;
+        uint4 on, os;
+        __nv_bfloat162* hn = (__nv_bfloat162*)&on;
+        __nv_bfloat162* hs = (__nv_bfloat162*)&os;
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+            const float2 f = __bfloat1622float2(h[k]);
+            const float y0 = fmaf((f.x - mf) * rstd, __ldg(a.gamma + c + 2 * k), __ldg(a.beta + c + 2 * k));
+            const float y1 = fmaf((f.y - mf) * rstd, __ldg(a.gamma + c + 2 * k + 1), __ldg(a.beta + c + 2 * k + 1));
+            hn[k] = __floats2bfloat162_rn(y0, y1);
+            hs[k] = __floats2bfloat162_rn(__fdividef(y0, 1.0f + __expf(-y0)), __fdividef(y1, 1.0f + __expf(-y1)));
+        }
+        if (yn) *(uint4*)((__nv_bfloat16*)yn + row * a.y_norm.ld + c) = on;
+        if (ys) *(uint4*)((__nv_bfloat16*)ys + row * a.y_silu.ld + c) = os;
+    }
+}
+
 static int grid_for(long long total, int threads) {
     long long b = (total + threads - 1) / threads;
     if (b < 1) b = 1;
@@ -367,6 +447,37 @@ static int fis_check(void) { return cudaGetLastError() == cudaSuccess ? FIS_OK :
 extern "C" int fis_gn_stats(const fis_gn_stats_args* a, void* stream) {
     if (a->groups <= 0 || a->c % a->groups) return FIS_ERR_SHAPE;
     return fis_launch(fis::gn_stats_kernel, dim3(a->groups, a->n_img > 1 ? a->n_img : 1), dim3(256), 0, (cudaStream_t)stream, *a) == cudaSuccess ? FIS_OK : FIS_ERR_LAUNCH;
+}
+
+extern "C" int fis_gn_apply(const fis_gn_apply_args* a, void* stream);
+
+// Dense group norm with its own statistics (written to mean/var per image): rows = n_img * img_rows
+// (img_rows = 0: one image). bf16 maps with 8 | channels-per-group take the one-launch kernel;
+// otherwise statistics + apply are two launches.
+extern "C" int fis_gn(const fis_gn_apply_args* a, void* stream) {
+    if (a->groups <= 0 || a->c % a->groups) return FIS_ERR_SHAPE;
+    if (a->rows == 0) return FIS_OK;
+    const int hw = a->img_rows > 0 ? a->img_rows : a->rows;
+    if (a->rows % hw || a->x_rows || a->y_rows || a->row_img) return FIS_ERR_SHAPE;
+    const int n_img = a->rows / hw, cpg = a->c / a->groups;
+    const bool vec = a->x.dtype == FIS_BF16 && cpg % 8 == 0 && (a->x.ld % 8) == 0 &&
+                     (!a->y_norm.ptr || (a->y_norm.dtype == FIS_BF16 && (a->y_norm.ld % 8) == 0)) &&
+                     (!a->y_silu.ptr || (a->y_silu.dtype == FIS_BF16 && (a->y_silu.ld % 8) == 0)) &&
+                     ((((uintptr_t)a->x.ptr) | ((uintptr_t)a->y_norm.ptr) | ((uintptr_t)a->y_silu.ptr)) & 15) == 0;
+    if (vec) {
+        fis_gn_apply_args ap = *a;
+        ap.img_rows = hw;
+        return fis_launch(fis::gn_fused_kernel, dim3(a->groups, n_img), dim3(256), 0, (cudaStream_t)stream, ap) ==
+                       cudaSuccess ? FIS_OK : FIS_ERR_LAUNCH;
+    }
+    fis_gn_stats_args st = {};
+    st.hw = hw; st.c = a->c; st.groups = a->groups; st.x = a->x; st.mean = a->mean; st.var = a->var;
+    st.step = a->step; st.n_img = n_img;
+    const int rc = fis_gn_stats(&st, stream);
+    if (rc != FIS_OK) return rc;
+    fis_gn_apply_args ap = *a;
+    ap.img_rows = n_img > 1 ? hw : 0;
+    return fis_gn_apply(&ap, stream);
 }
 
 extern "C" int fis_gn_apply(const fis_gn_apply_args* a, void* stream) {

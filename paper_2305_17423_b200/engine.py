@@ -604,9 +604,8 @@ class Engine(Launcher):
             if plan.sparse(level):  # cached statistics of each row's request
                 self.gn_apply(nl, co, m, c, mean, var, None, s, row_img=plan.row_img(level))
             else:
-                hw = self.hw(level)
-                self.gn_stats(co, hw, c, mean, var, n_img=plan.batch)
-                self.gn_apply(nl, co, m, c, mean, var, None, s, img_rows=hw)
+                # statistics per image + normalise + SiLU in one launch (fis_gn)
+                self.gn_apply(nl, co, m, c, mean, var, None, s, fused_stats=True, img_rows=self.hw(level))
         elif plan.sparse(level):
             mean, var = plan.stats(nl)
             gamma, beta = self.W.norm[nl]
@@ -616,12 +615,9 @@ class Engine(Launcher):
             co = plan.record(blk["conv"], 0) or DRef(self.scratch(f"co{tag}", (cap, c)))
             self._conv(plan, blk["conv"], [(x, False)], co, level)
             mean, var = plan.stats(nl)
-            if self.capture is not None:
-                # step VM: statistics + normalisation of each group in one op
-                self.gn_apply(nl, co, cap, c, mean, var, plan.record(nl, 0), s, fused_stats=True)
-            else:
-                self.gn_stats(co, cap, c, mean, var)
-                self.gn_apply(nl, co, cap, c, mean, var, plan.record(nl, 0), s)
+            # statistics + normalisation (+ SiLU) of each group in one op (fis_gn; the step VM
+            # runs the same op kind)
+            self.gn_apply(nl, co, cap, c, mean, var, plan.record(nl, 0), s, fused_stats=True)
         y1 = DRef(self.scratch(f"y1{tag}", (cap, c)))
         qs = plan.segments(level)
         self.attn_self(blk["self_attn"], m, s, y1, level, tag, pre=plan.record(blk["self_attn"], 0), segs=qs)
