@@ -528,6 +528,9 @@ static bool attn_share(const fis_attn_args* a, int dvs) {
     if (share_off || a->max_seg_k <= 0 || a->max_seg_k > 4096 || slices < 2 || !a->ws ||
         a->ws_bytes < (long long)a->m * pw * 2)
         return false;
+    // batch 1 (a grid smaller than the GPU): the slices' redundant S work runs in parallel anyway,
+    // a second (serial) launch only adds latency (r01 C2 step: 1.358 ms unshared vs 1.390 shared)
+    if (ctas < 148) return false;
     // one key block: recomputing S per slice is cheap unless the head dim is large (r01: L0 cross
     // attention 23 + 48 us shared vs one launch unshared)
     if (a->max_seg_k <= 128) return (long long)a->d * (slices - 1) >= 1280;
