@@ -136,14 +136,18 @@ __global__ void gn_apply_kernel(const fis_gn_apply_args a) {
             uint4 on, os;
             __nv_bfloat162* hn = (__nv_bfloat162*)&on;
             __nv_bfloat162* hs = (__nv_bfloat162*)&os;
+            // gamma / beta as two 16-byte loads each (scalar loads made this kernel L1-bound)
+            float ga[8], be[8];
+            *(float4*)ga = __ldg((const float4*)(a.gamma + c));
+            *(float4*)(ga + 4) = __ldg((const float4*)(a.gamma + c + 4));
+            *(float4*)be = __ldg((const float4*)(a.beta + c));
+            *(float4*)(be + 4) = __ldg((const float4*)(a.beta + c + 4));
 #pragma unroll
             for (int k = 0; k < 4; k++) {
                 const float2 f = __bfloat1622float2(h[k]);
                 const bool s0 = 2 * k >= split, s1 = 2 * k + 1 >= split;
-                const float y0 = fmaf((f.x - (s0 ? mu1 : mu0)) * (s0 ? rstd1 : rstd0), __ldg(a.gamma + c + 2 * k),
-                                      __ldg(a.beta + c + 2 * k));
-                const float y1 = fmaf((f.y - (s1 ? mu1 : mu0)) * (s1 ? rstd1 : rstd0), __ldg(a.gamma + c + 2 * k + 1),
-                                      __ldg(a.beta + c + 2 * k + 1));
+                const float y0 = fmaf((f.x - (s0 ? mu1 : mu0)) * (s0 ? rstd1 : rstd0), ga[2 * k], be[2 * k]);
+                const float y1 = fmaf((f.y - (s1 ? mu1 : mu0)) * (s1 ? rstd1 : rstd0), ga[2 * k + 1], be[2 * k + 1]);
                 hn[k] = __floats2bfloat162_rn(y0, y1);
                 hs[k] = __floats2bfloat162_rn(__fdividef(y0, 1.0f + __expf(-y0)), __fdividef(y1, 1.0f + __expf(-y1)));
             }
@@ -420,11 +424,16 @@ __global__ void __launch_bounds__(256) gn_fused_kernel(const fis_gn_apply_args a
         uint4 on, os;
         __nv_bfloat162* hn = (__nv_bfloat162*)&on;
         __nv_bfloat162* hs = (__nv_bfloat162*)&os;
+        float ga[8], be[8];
+        *(float4*)ga = __ldg((const float4*)(a.gamma + c));
+        *(float4*)(ga + 4) = __ldg((const float4*)(a.gamma + c + 4));
+        *(float4*)be = __ldg((const float4*)(a.beta + c));
+        *(float4*)(be + 4) = __ldg((const float4*)(a.beta + c + 4));
 #pragma unroll
         for (int k = 0; k < 4; k++) {
             const float2 f = __bfloat1622float2(h[k]);
-            const float y0 = fmaf((f.x - mf) * rstd, __ldg(a.gamma + c + 2 * k), __ldg(a.beta + c + 2 * k));
-            const float y1 = fmaf((f.y - mf) * rstd, __ldg(a.gamma + c + 2 * k + 1), __ldg(a.beta + c + 2 * k + 1));
+            const float y0 = fmaf((f.x - mf) * rstd, ga[2 * k], be[2 * k]);
+            const float y1 = fmaf((f.y - mf) * rstd, ga[2 * k + 1], be[2 * k + 1]);
             hn[k] = __floats2bfloat162_rn(y0, y1);
             hs[k] = __floats2bfloat162_rn(__fdividef(y0, 1.0f + __expf(-y0)), __fdividef(y1, 1.0f + __expf(-y1)));
         }
