@@ -62,6 +62,14 @@ static int fis_choose_splits(const fis_gemm_args* a, bool tc) {
     return (int)(s < 1 ? 1 : s);
 }
 
+// Which kernel fis_gemm would run for these arguments: 0 SIMT, 1 per-op tcgen05, 2 persistent
+// large-M tcgen05 (csrc/fis_gemm_big.cu). Host-only query (no launch).
+int fis_gemm_kernel_kind(const fis_gemm_args* a) {
+    const bool tc = a->impl == 2 || (a->impl == 0 && fis_gemm_tc_supported(a));
+    if (!tc) return 0;
+    return a->impl == 0 && fis_gemm_big_eligible(a) ? 2 : 1;
+}
+
 int fis_gemm(const fis_gemm_args* a, void* stream) {
     if (a->m < 0 || a->n <= 0 || a->k <= 0) return FIS_ERR_SHAPE;
     if (a->m == 0) return FIS_OK;

@@ -233,6 +233,7 @@ class Launcher:
         g.step = L.ptr(self.step_dev)
         g.impl = self.gemm_impl
         g.static_meta = 1 if self.static_meta else 0
+        self.last_gemm = g  # inspected by tests (fis_gemm_kernel_kind)
         self._call("fis_gemm", g, b_static)
         self.launches += 1
 
