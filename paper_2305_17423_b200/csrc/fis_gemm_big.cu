@@ -45,6 +45,7 @@ struct GatherMaps {
     CUtensorMap fresh[2], cache[2];
     int fresh_rps[2], cache_rps[2];
 };
+constexpr int STG_BYTES = 8 * 16 * 32 * 2;  // per epilogue warp: a 16-column x 32-row bf16 transpose tile
 constexpr int LAG = 2;
 constexpr int GATHER_WARPS = 2;  // A warps issuing TMA gather4 in the gather mode; the rest use cp.async  // cp.async stages in flight per A-producer thread
 constexpr int SEL_BYTES = BM * 19 * 4;  // select-on-read table [128][18] + row pixels [128]
@@ -61,7 +62,7 @@ __host__ __device__ inline Layout layout(int bn) {
     if (l.stages > MAX_STAGES) l.stages = MAX_STAGES;
     // stages + barriers (2 per stage + 4) + TMEM slot + epilogue tables (6 x BN floats) +
     // per-row select-on-read table (128 rows x 2 segments x 9 taps) + align
-    l.total = l.stages * l.stage + 1024 + 256 + 6 * bn * 4 + SEL_BYTES + 64;
+    l.total = l.stages * l.stage + 1024 + 256 + 6 * bn * 4 + SEL_BYTES + STG_BYTES + 64;
     return l;
 }
 
@@ -156,6 +157,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     float* tabs = (float*)(smem + L.stages * L.stage + 256);
     int* seltab = (int*)(tabs + 6 * bn);
     int* rowtab = seltab + BM * 18;
+    __nv_bfloat16* stg_all = (__nv_bfloat16*)(rowtab + BM);  // [8 warps][16][32] transposed-store staging
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int tiles_n = (a.n + bn - 1) / bn, tiles_m = (a.m + BM - 1) / BM;
@@ -461,6 +463,9 @@ epilogue_role : {
         const bool fast = a.epi == FIS_EPI_NONE && a.alpha == 1.0f && !e.pre && !e.pre2 && !e.bias2 && !e.lat &&
                           !a.d_rows && !a.d_trans && a.d.dtype == FIS_BF16 && (a.d.ld % 8) == 0 &&
                           (((uintptr_t)e.d) & 15) == 0 && (!e.res || (a.res.ld % 8) == 0);
+        // transposed V^T of a fused QKV (n >= n_split) through the staging tile
+        const bool tfast = fast && !e.res && a.n_split > 0 && a.d2_trans && a.d2.dtype == FIS_BF16 &&
+                           (a.d2.ld % 8) == 0 && (((uintptr_t)e.d2) & 15) == 0 && !(dbg & 1);
         EpiTab tb;
         tb.mean = tabs;
         tb.rstd = tb.mean + bn;
@@ -498,6 +503,31 @@ epilogue_role : {
                 uint32_t u[16];
                 tmem_ld16(taddr + cb, u);
                 tmem_wait_ld();
+                const int nn = n0 + cb;
+                if (tfast && nn >= a.n_split && nn + 16 <= a.n) {
+                    // transposed V^T chunk (fused QKV): stage the warp's 32 rows x 16 columns in shared
+                    // memory, then store 16-byte runs of 8 rows per column (warp-uniform path)
+                    __nv_bfloat16* stg = stg_all + (warp - (grp ? 0 : EPI_WARP0) + (grp ? 4 : 0)) * (16 * 32);
+#pragma unroll
+                    for (int j = 0; j < 16; j++)
+                        stg[j * 32 + lane] = __float2bfloat16_rn(__fadd_rn(__uint_as_float(u[j]), tb.bias[cb + j]));
+                    __syncwarp();
+                    const int r0 = m0 + quarter * 32, dn = nn - a.n_split;
+#pragma unroll
+                    for (int q = 0; q < 2; q++) {
+                        const int idx = lane + 32 * q, j = idx >> 2, p8 = (idx & 3) * 8;
+                        const uint4 val = *(const uint4*)(stg + j * 32 + p8);
+                        __nv_bfloat16* dst = (__nv_bfloat16*)e.d2 + (long long)(dn + j) * a.d2.ld + r0 + p8;
+                        if (r0 + p8 + 8 <= a.m) {
+                            *(uint4*)dst = val;
+                        } else {
+                            const __nv_bfloat16* sv = (const __nv_bfloat16*)&val;
+                            for (int i = 0; i < 8 && r0 + p8 + i < a.m; i++) dst[i] = sv[i];
+                        }
+                    }
+                    __syncwarp();
+                    continue;
+                }
                 if (r < a.m && !(dbg & 1)) {
                     float v[16];
 #pragma unroll
