@@ -330,8 +330,13 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_tc_kernel(const fis_gemm_args
         __syncthreads();
         // phase 2: fused epilogue of the reduced slice rows, 16-column chunks
         const int chunks = BN / 16;
-        for (int item = tid; item < (rend - rbeg) * chunks; item += THREADS) {
-            const int lr = rbeg + item / chunks, cb = (item % chunks) * 16;
+        // transposed outputs (V^T of a fused QKV, or d_trans): rows fastest across threads so a warp
+        // stores 32 consecutive rows of each column (coalesced); row-major outputs: columns fastest
+        const bool tile_trans = a.d_trans || (a.d2_trans && a.n_split > 0 && n0 >= a.n_split);
+        const int nrows = rend - rbeg;
+        for (int item = tid; item < nrows * chunks; item += THREADS) {
+            const int lr = rbeg + (tile_trans ? item % nrows : item / chunks);
+            const int cb = (tile_trans ? item / nrows : item % chunks) * 16;
             const int r = m0 + lr;
             if (r >= a.m || n0 + cb >= a.n) continue;
             float v[16];
