@@ -110,6 +110,8 @@ int fis_gemm(const fis_gemm_args* args, void* stream);
 /* which kernel fis_gemm picks for these arguments: 0 SIMT, 1 per-op tcgen05 (split-K clusters),
  * 2 persistent large-M tcgen05 (TMA / gather4 staging); host-only, no launch */
 int fis_gemm_kernel_kind(const fis_gemm_args* a);
+/* number of persistent-kernel launches so far (diagnostics / tests) */
+long long fis_gemm_big_launch_count(void);
 /* workspace floats / counters needed for a given problem */
 long long fis_gemm_ws_floats(int m, int n, int splits);
 int fis_gemm_counters(int m, int n);

@@ -752,6 +752,10 @@ static int wide_bn(int n) {
     return 0;
 }
 
+static long long g_big_launched = 0;
+// persistent-kernel launches so far (tests check that fis_gemm did not fall back to the per-op kernel)
+extern "C" long long fis_gemm_big_launch_count(void) { return g_big_launched; }
+
 int fis_gemm_big_launch(const fis_gemm_args* a, cudaStream_t stream) {
     CUtensorMap ta, ta2;
     std::memset(&ta, 0, sizeof(ta));
@@ -772,10 +776,15 @@ int fis_gemm_big_launch(const fis_gemm_args* a, cudaStream_t stream) {
     const fis::big::Layout L = fis::big::layout(bn);
     static int configured_smem = 0;
     if (configured_smem < L.total) {
-        if (cudaFuncSetAttribute(fis::big::gemm_big_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 227 * 1024) != cudaSuccess)
+        // dynamic + static shared memory must fit the 227 KB per-block limit
+        cudaFuncAttributes fa;
+        const int stat = cudaFuncGetAttributes(&fa, fis::big::gemm_big_kernel) == cudaSuccess ? (int)fa.sharedSizeBytes : 1024;
+        const int maxdyn = 227 * 1024 - stat;
+        if (L.total > maxdyn ||
+            cudaFuncSetAttribute(fis::big::gemm_big_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, maxdyn) !=
+                cudaSuccess)
             return FIS_ERR_UNSUPPORTED;
-        configured_smem = 227 * 1024;
+        configured_smem = maxdyn;
     }
     const long long tiles = (long long)((a->m + 127) / 128) * ((a->n + bn - 1) / bn);
     const int grid = (int)(tiles < sms() ? tiles : sms());
@@ -790,8 +799,10 @@ int fis_gemm_big_launch(const fis_gemm_args* a, cudaStream_t stream) {
     cfg.attrs = attr;
     cfg.numAttrs = fis_pdl_enabled() ? 1 : 0;
     static int dbg = getenv("FIS_BIG_DBG") ? atoi(getenv("FIS_BIG_DBG")) : 0;  // 1: no stores, 2: no A loads
-    return cudaLaunchKernelEx(&cfg, fis::big::gemm_big_kernel, *a, *tm, ta, ta2, gm, bn, amode, dbg) == cudaSuccess
-               ? FIS_OK : FIS_ERR_LAUNCH;
+    if (cudaLaunchKernelEx(&cfg, fis::big::gemm_big_kernel, *a, *tm, ta, ta2, gm, bn, amode, dbg) != cudaSuccess)
+        return FIS_ERR_LAUNCH;
+    g_big_launched++;
+    return FIS_OK;
 }
 
 extern "C" int fis_big_trace_read(unsigned long long* out768) {

@@ -33,12 +33,18 @@ def _kind(lz):
 
 
 def _both(run, out):
+    """Run with the persistent kernel, then with the per-op kernel (FIS_BIG=0); also checks that
+    the first run really launched the persistent kernel (no silent fallback)."""
+    from paper_2305_17423_b200 import _lib as L
     res = []
     for big in ("1", "0"):
         os.environ["FIS_BIG"] = big
         out.zero_()
+        n0 = L.lib().fis_gemm_big_launch_count()
         run()
         torch.cuda.synchronize()
+        if big == "1":
+            assert L.lib().fis_gemm_big_launch_count() > n0, "persistent GEMM fell back to the per-op kernel"
         res.append(out.clone())
     os.environ.pop("FIS_BIG", None)
     return res
