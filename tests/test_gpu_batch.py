@@ -105,3 +105,29 @@ def test_batched_odd_latent_and_repeat_rounds(P):
             one = P.edit(P.EditSession.create(old, new, cfg, store, user_mask=m), cfg, store)
             assert np.abs(r.latent - one.latent).max() <= BF16_FINAL_TOL
             assert np.array_equal(r.latent[:, :, ~m.bits], final[:, :, ~m.bits])
+
+
+def test_batched_no_edit_request_rides_along(P):
+    """A request whose detection finds nothing to edit (same prompt) rides along in the batch with
+    an empty mask: its latent is the cached generation's, bit-exactly; the other request equals
+    its own edit()."""
+    cfg = _cfg(P)
+    pairs = [((3, 5, 7, 11), (3, 5, 7, 11)), ((2, 4, 6), (2, 8, 6))]
+    stores = [P.CacheStore() for _ in pairs]
+    finals = P.generate_dense_batch([P.PromptTokens(o) for o, _ in pairs], cfg, stores)
+    res = P.edit_batch([P.EditSession.create(o, n, cfg, st) for (o, n), st in zip(pairs, stores)], cfg)
+    assert res[0].no_edit and res[0].mask is None
+    assert np.array_equal(res[0].latent, finals[0])
+    store = P.CacheStore()
+    P.generate_dense(P.PromptTokens(pairs[1][0]), cfg, store, record="engine")
+    one = P.edit(P.EditSession.create(pairs[1][0], pairs[1][1], cfg, store), cfg, store)
+    assert np.abs(res[1].latent - one.latent).max() <= BF16_FINAL_TOL
+
+
+def test_edit_batch_rejects_foreign_stores(P):
+    cfg = _cfg(P)
+    store = P.CacheStore()
+    P.generate_dense(P.PromptTokens((3, 5, 7, 11)), cfg, store, record="engine")
+    with pytest.raises(P.ContractViolation):
+        P.edit_batch([P.EditSession.create((3, 5, 7, 11), (3, 5, 9, 11), cfg, store,
+                                           user_mask=P.centered_square_mask(32, 32, 0.1))], cfg)
