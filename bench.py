@@ -224,6 +224,11 @@ def run_ours(args):
         b = np.roll(mask.bits, (2 * i, -2 * i), axis=(0, 1))
         e2e_masks.append(P.BinaryMask(b))
     sessions = [P.EditSession.create(OLD_IDS, NEW_IDS, cfg, store, user_mask=m) for m in e2e_masks]
+    # one untimed edit() first (process-level one-time costs: lazy imports, tensor-map encodes),
+    # and a garbage-collection pass so the timed calls start from a clean heap
+    P.edit(P.EditSession.create(OLD_IDS, NEW_IDS, cfg, store, user_mask=mask), cfg, store)
+    import gc
+    gc.collect()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     for s_ in sessions:
@@ -294,8 +299,9 @@ def run_ours(args):
         "clocks": clk.summary(),
         "e2e": {"value": T / e2e_s, "unit": "edit-steps/s", "h2d_bytes_per_step": (cfg.latent_h * cfg.latent_w * 17) // T,
                 "d2h_bytes_per_step": (4 * cfg.latent_h * cfg.latent_w * cfg.latent_channels + 64) // T,
-                "note": f"{E2E_CALLS} consecutive P.edit() calls (each: T steps, planning, text K/V, H2D mask/latent, "
-                        "D2H result; the first captures the step graph, the next reuse it with their inputs copied in)"},
+                "note": f"{E2E_CALLS} consecutive P.edit() calls after one untimed warm-up call (each: T steps, "
+                        "planning, text K/V, H2D mask/latent, D2H result; step graphs reused when the launch shapes "
+                        "match, inputs copied in)"},
     }
     if rank == 0 and not args.no_cpu:
         v, per = cpu_sample(C2, args.mask, 1, 0, os.cpu_count() or 1)

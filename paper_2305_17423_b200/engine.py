@@ -368,8 +368,10 @@ class Engine(Launcher):
             vt = torch.zeros((c, _pad(nt)), dtype=self.act, device=self.dev)
             self.gemm(nt, c, emb.shape[1], a=DRef(emb), b=DRef(wk), d=DRef(k), splits=1)
             self.gemm(nt, c, emb.shape[1], a=DRef(emb), b=DRef(wv), d=DRef(vt), d_trans=True, splits=1)
-            v = torch.empty((nt, c), dtype=self.act, device=self.dev)
-            self.gemm(nt, c, emb.shape[1], a=DRef(emb), b=DRef(wv), d=DRef(v), splits=1)
+            v = None
+            if self.fused_xattn:  # row-major V only for the SIMT cross-attention kernel
+                v = torch.empty((nt, c), dtype=self.act, device=self.dev)
+                self.gemm(nt, c, emb.shape[1], a=DRef(emb), b=DRef(wv), d=DRef(v), splits=1)
             out[lid] = (k, vt, v)
         return out
 
