@@ -459,6 +459,8 @@ def stacked_requests(eng, U, P, cfg, R, args, peak_tf, ids=None):
     # end to end through the public API: R sessions in, R host latents out
     sessions = [P.EditSession.create(o, n, cfg, st_, user_mask=P.BinaryMask(b))
                 for (o, n, b), st_ in zip(reqs, stores)]
+    import gc
+    gc.collect()
     torch.cuda.synchronize()
     t1 = time.perf_counter()
     results = P.edit_batch(sessions, cfg)
