@@ -597,6 +597,14 @@ const CUtensorMap* weight_map(const void* base, long long n, long long k, long l
     return &g_maps[slot].map;
 }
 
+}  // namespace
+
+const CUtensorMap* fis_weight_map(const void* base, long long n, long long k, long long ld, int box) {
+    return weight_map(base, n, k, ld, box);
+}
+
+namespace {
+
 int sms() {
     static int n = 0;
     if (n <= 0) n = fis_device_sm_count();
