@@ -11,8 +11,24 @@ each rank edits its own request (weak scaling, no collective in the step).
 
 Timing: W warm-up steps, then K steps bracketed by barrier + synchronize, CUDA
 events on the launching stream, max over ranks. Inputs larger than L2: each
-step streams 444 MB (bf16) / 887 MB (fp32) of weights plus that step's cache
-slab, so no L2 flush is needed.
+step streams 444 MB (bf16) of weights plus that step's cache slab, so no L2
+flush is needed. Clocks: NVML polled every ~1 ms on a thread during the timed
+region.
+
+Per-kernel numbers (roofline, kernel shares) come from CUPTI kernel records
+(torch.profiler) of graph replays of the SAME captured step: each kernel's
+critical-path time is end_i - end_{i-1} (kernels overlap their prologue with the
+previous kernel through programmatic dependent launch), so the per-kernel times
+of one replay sum to the step.
+
+Sections of the JSON line beyond the base contract:
+  roofline       gated-conv gather-GEMMs of the timed step (algorithmic FLOPs / CUPTI time)
+  kernels        per-op-class share of the step (CUPTI, graph replay)
+  sweep          C3: sparse step vs mask ratio 1..100% + random-dilated 10%, vs the dense step
+  fp32_parity    the same step in the fp32 parity precision
+  c4             SD-2 shape (96x96, 1024-wide text): sparse step + multi-round edit() e2e
+  batched        C5: 64 requests over the N GPUs, each GPU's share stepped as one stacked batch
+  cpu_baseline   the reference package's own CPU path (baseline/_ref) on a bounded sample
 """
 
 from __future__ import annotations
@@ -20,7 +36,6 @@ from __future__ import annotations
 import argparse
 import json
 import os
-import subprocess
 import sys
 import threading
 import time
@@ -33,64 +48,78 @@ sys.path.insert(0, ROOT)
 C2 = dict(latent_h=64, latent_w=64, latent_channels=4, channels=(320, 640, 1280, 1280), blocks_per_level=2,
           groups=32, steps=50, t1=5, t2=10, gate_fraction=0.25, dilation_radius=1, text_dim=768,
           vocab_size=49408, seed=0)
+C4 = dict(C2, latent_h=96, latent_w=96, text_dim=1024)
 OLD_IDS = tuple(range(1, 78))
 NEW_IDS = tuple(99 if i == 3 else v for i, v in enumerate(OLD_IDS))
 METRIC = "edit-steps/sec at SD-1.5 512^2 vs mask ratio; sparse-conv % of TC peak"
+WEIGHT_BYTES_BF16 = 2 * 221_700_000  # SURVEY §0 item 6: 221.7 M params of the SD-1.5-shape toy UNet
+E2E_CALLS = 5
 
 
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
             d = json.load(f)
-        return d["hbm_gbs"], d["bf16_tflops"], "measured"
+        return d["hbm_gbs"], d["bf16_tflops"], "measured (MEASURED_PEAKS.json, burst)"
     except Exception:
-        return 6650.0, 1590.0, "fallback"
+        return 6650.0, 1590.0, "fallback (B200_PROFILING.md)"
 
 
 class Clocks:
-    """nvidia-smi sampler during the timed region."""
+    """NVML sampler of SM clock and throttle reasons on a thread (~1 ms period) during the timed
+    region (nvidia-smi's 100 ms minimum period cannot resolve a ~30 ms region)."""
+
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+               "sw_power_cap": 0x4}
 
     def __init__(self, idx):
-        self.idx, self.p, self.lines = idx, None, []
+        self.idx, self.samples, self.max_mhz, self.reasons = idx, [], None, set()
+        self._stop = threading.Event()
+        self._h = None
 
     def __enter__(self):
-        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
         try:
-            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.idx), f"--query-gpu={q}", "--format=csv,noheader,nounits",
-                                       "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
-            self.t.start()
+            import pynvml as N
+            N.nvmlInit()
+            self._N = N
+            self._h = N.nvmlDeviceGetHandleByIndex(self.idx)
+            self.max_mhz = float(N.nvmlDeviceGetMaxClockInfo(self._h, N.NVML_CLOCK_SM))
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
         except Exception:
-            self.p = None
+            self._h = None
         return self
 
-    def _read(self):
-        for line in self.p.stdout:
-            self.lines.append(line.strip())
+    def _sample(self):
+        N = self._N
+        self.samples.append(float(N.nvmlDeviceGetClockInfo(self._h, N.NVML_CLOCK_SM)))
+        r = N.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+        for name, bit in self.REASONS.items():
+            if r & bit:
+                self.reasons.add(name)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self._sample()
+            except Exception:
+                return
+            time.sleep(0.001)
 
     def __exit__(self, *a):
-        if self.p is not None:
-            self.p.terminate()
-            self.p.wait()
+        if self._h is not None:
+            self._stop.set()
+            self._t.join()
+            if not self.samples:
+                try:
+                    self._sample()
+                except Exception:
+                    pass
 
     def summary(self):
-        sm, mx, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            parts = [x.strip() for x in ln.split(",")]
-            if len(parts) < 6:
-                continue
-            try:
-                sm.append(float(parts[0]))
-                mx = float(parts[1])
-            except ValueError:
-                continue
-            for n, v in zip(names, parts[2:]):
-                if v.lower().startswith("active"):
-                    reasons.add(n)
-        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm)}
+        s = self.samples
+        return {"sm_mhz": float(np.median(s)) if s else None, "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(s), "source": "NVML, ~1 ms period"}
 
 
 def dist_init():
@@ -122,14 +151,54 @@ def barrier():
 
 
 # ----------------------------------------------------------------------------- CPU arms
-def cpu_sample(cfg_d, frac, steps, warmup, threads):
-    """Oracle port (CPU restatement of the reference, numpy f64) timed on host cores.
+def _ref_package():
+    """The unmodified reference package installed in baseline/_ref (pip --target), or None."""
+    path = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(path, "sparsedit")):
+        return None
+    if path not in sys.path:
+        sys.path.insert(0, path)
+    try:
+        import sparsedit
+        return sparsedit
+    except Exception:
+        return None
 
-    Bounded sample: weights + one dense step (to create the step-1 cache), then
-    `warmup + steps` sparse steps at t=1. Returns (edit-steps/s, seconds per step)."""
-    os.environ.setdefault("OPENBLAS_NUM_THREADS", str(threads))
+
+def ref_sample(cfg_d, frac, steps, warmup):
+    """The reference package's own CPU path (sparsedit 0.1.0 from baseline/_ref): UNet(config),
+    one dense caching step t=1 recorded into its CacheStore (DenseMode recorder, unet.py:680-696),
+    then `warmup + steps` sparse steps at t=1 through SparseMode over that cache with the 10%
+    centered-square plan (unet.py:868-883). Returns (edit-steps/s, s/step, setup s)."""
+    sd = _ref_package()
+    from sparsedit import unet as RU
+    t0 = time.perf_counter()
+    cfg = RU.UNetConfig(**dict(cfg_d, channels=tuple(cfg_d["channels"])))
+    net = RU.UNet(cfg)
+    store = sd.CacheStore()
+    text_old = RU.embed_tokens(RU.PromptTokens(OLD_IDS), cfg)
+    text_new = RU.embed_tokens(RU.PromptTokens(NEW_IDS), cfg)
+    lat = RU.initial_latent(cfg)
+    rec = lambda lid, role, payload: store.put((1, lid, role), payload)
+    net.forward(lat, 1, text_old, RU.DenseMode(cfg.groups, recorder=rec))
+    mask = sd.centered_square_mask(cfg.latent_h, cfg.latent_w, frac)
+    pyr = sd.build_pyramid(mask, cfg.levels)
+    plans = {lv: sd.select_gather_plan(pyr.levels[lv], (3, 3)) for lv in RU._gated_levels(net)}
+    setup = time.perf_counter() - t0
+    times = []
+    for i in range(warmup + steps):
+        t1 = time.perf_counter()
+        ctx = RU._sparse_contexts(net, store, 1)
+        net.forward(lat, 1, text_new, RU.SparseMode(cfg, pyr, plans, ctx, pool=store.buffer_pool))
+        times.append(time.perf_counter() - t1)
+    per = float(np.mean(times[warmup:]))
+    return 1.0 / per, per, setup
+
+
+def port_sample(cfg_d, frac, steps, warmup):
+    """Oracle port (numpy f64 restatement of the reference) on the same bounded sample."""
     from oracle import sparsedit_oracle as O
-    cfg = O.cfg_of(dict(cfg_d, steps=cfg_d["steps"]))
+    cfg = O.cfg_of(dict(cfg_d))
     net = O.build_net(cfg)
     text_old, text_new = O.embed(OLD_IDS, cfg), O.embed(NEW_IDS, cfg)
     lat = O.init_latent(cfg)
@@ -144,32 +213,139 @@ def cpu_sample(cfg_d, frac, steps, warmup, threads):
         t0 = time.perf_counter()
         O.forward(net, lat, 1, text_new, O.SparseOps(net, pyr, plans, cache, 1))
         times.append(time.perf_counter() - t0)
-    per = float(np.mean(times[warmup:])) if steps else float("nan")
+    per = float(np.mean(times[warmup:]))
     return 1.0 / per, per
 
 
+def cpu_baseline(frac, steps, warmup):
+    threads = os.cpu_count() or 1
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", str(threads))
+    if _ref_package() is not None:
+        v, per, setup = ref_sample(C2, frac, steps, warmup)
+        return {"value": v, "unit": "edit-steps/s", "cores": threads, "kind": "reference",
+                "ms_per_step": per * 1e3,
+                "sample": f"reference package sparsedit 0.1.0 (baseline/_ref, unmodified): UNet + one dense caching "
+                          f"step t=1 into its CacheStore ({setup:.1f} s setup, not timed), then {warmup}+{steps} "
+                          f"SparseMode steps at t=1 (10% centered square), numpy/OpenBLAS on {threads} threads"}
+    v, per = port_sample(C2, frac, steps, warmup)
+    return {"value": v, "unit": "edit-steps/s", "cores": threads, "kind": "port", "ms_per_step": per * 1e3,
+            "sample": f"oracle port (numpy f64 restatement), {warmup}+{steps} sparse steps at t=1 after one dense "
+                      "caching step"}
+
+
 def run_reference(args):
-    ws, rank, _ = int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")), 0
+    rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    threads = os.cpu_count() or 1
-    # bounded sample: at most 10 timed sparse steps (~5 s each on CPU) after <= 1 warm-up
-    n_steps, n_warm = min(args.steps, 10), min(args.warmup, 1)
-    v, per = cpu_sample(C2, args.mask, n_steps, n_warm, threads)
+    # bounded sample: the reference's sparse C2 step takes ~9 s on 8 cores, so at most 6 timed
+    # steps after at most 1 warm-up (the line reports the counts actually timed)
+    n_steps, n_warm = max(1, min(args.steps, 6)), min(args.warmup, 1)
+    cb = cpu_baseline(args.mask, n_steps, n_warm)
+    v = cb["value"]
     line = {"metric": METRIC, "value": v, "unit": "edit-steps/s", "impl": "reference", "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": per * 1e3, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64-accumulate/f32", "data": "synthetic",
-            "config": {"workload": f"C2 SD-1.5-shape sparse edit step, {int(args.mask*100)}% centered-square user mask",
-                       "model": "sparsedit toy UNet @ SD-1.5 widths (320/640/1280/1280)", "latent": "1x4x64x64",
-                       "mask_fraction": args.mask},
-            "cpu_baseline": {"value": v, "unit": "edit-steps/s", "cores": threads, "kind": "port",
-                             "sample": f"oracle port (numpy f64 restatement of sparsedit), {n_warm}+{n_steps} "
-                                       "sparse steps at t=1 after one dense caching step"},
+            "steps": n_steps, "warmup": n_warm, "steps_requested": args.steps, "warmup_requested": args.warmup,
+            "ms_per_step": cb["ms_per_step"], "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64-accumulate/f32", "data": "synthetic",
+            "config": {"workload": f"C2 SD-1.5-shape sparse edit step, {int(args.mask * 100)}% centered-square user mask",
+                       "model": "sparsedit toy UNet @ SD-1.5 widths (320/640/1280/1280), 2 blocks/level",
+                       "latent": "1x4x64x64", "text": "77x768", "mask_fraction": args.mask},
+            "cpu_baseline": cb,
             "e2e": {"value": v, "unit": "edit-steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
 
 
+# ----------------------------------------------------------------------------- kernel timing
+def _op_log(eng, plan):
+    """Ops (and kernel counts) of one step, in launch order (one eager step with the op log on)."""
+    import torch
+    eng.op_log = []
+    try:
+        eng.step_dev.fill_(1)
+        eng.run_step(plan)
+        torch.cuda.synchronize()
+        return eng.op_log
+    finally:
+        eng.op_log = None
+
+
+def replay_kernels(runner, ops, T, reps=3):
+    """CUPTI kernel records of `reps` graph replays of the runner's captured step, mapped to ops.
+
+    Returns [(op dict, critical-path us, kernel name)] of the LAST replay (L2/TLB warm) or None
+    when the profiler sees a different kernel count than the op log."""
+    import torch
+    from torch.profiler import ProfilerActivity, profile
+    n_k = sum(o["kernels"] for o in ops)
+    runner.step(2)
+    torch.cuda.synchronize()
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        for i in range(reps):
+            runner.step(2 + i % (T - 1))
+        torch.cuda.synchronize()
+    ks = []
+    for e in prof.events():
+        if e.device_type != torch.autograd.DeviceType.CUDA:
+            continue
+        nm = e.name
+        if "fis::" not in nm:  # torch's step-counter fill, memcpy/memset records
+            continue
+        ks.append((e.time_range.start, e.time_range.end, nm))
+    ks.sort()
+    if len(ks) != reps * n_k:
+        return None
+    last = ks[(reps - 1) * n_k:]
+    out, i, prev_end = [], 0, None
+    for o in ops:
+        seg = last[i:i + o["kernels"]]
+        i += o["kernels"]
+        end = max(s[1] for s in seg)
+        start = min(s[0] for s in seg)
+        crit = end - (max(prev_end, start) if prev_end is not None else start)
+        out.append((o, max(0.0, crit), seg[0][2]))
+        prev_end = end if prev_end is None else max(prev_end, end)
+    return out
+
+
+def kernel_summary(table, step_us):
+    agg = {}
+    for o, us, name in table:
+        if o["op"] == "fis_gemm":
+            cls = "gathered conv" if o.get("gathered") else ("dense conv" if o.get("conv") else "projection GEMM")
+        elif o["op"] == "fis_attn":
+            cls = "attention"
+        else:
+            cls = o["op"]
+        a = agg.setdefault(cls, [0, 0.0])
+        a[0] += o["kernels"]
+        a[1] += us
+    tot = sum(v[1] for v in agg.values())
+    return {k: {"kernels": v[0], "us": round(v[1], 2), "share": round(v[1] / tot, 4) if tot else None}
+            for k, v in sorted(agg.items(), key=lambda x: -x[1][1])} | {"sum_us": round(tot, 2),
+                                                                     "step_us_events": round(step_us, 2)}
+
+
+def gated_conv_flops(o, active):
+    """Algorithmic FLOPs of a gathered conv launch: 2 * active rows * N * K (plan.cost pixels at
+    batch 1; padding rows of stacked requests excluded)."""
+    return 2.0 * active * o["n"] * o["k"]
+
+
 # ----------------------------------------------------------------------------- GPU arm
+def _time_runner(runner, T, steps, warmup):
+    import torch
+    runner.step(1)
+    for i in range(warmup):
+        runner.step(1 + (i + 1) % T)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for i in range(steps):
+        runner.step(1 + i % T)
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / max(1, steps)
+
+
 def run_ours(args):
     import torch
     ws, rank, local = dist_init()
@@ -179,6 +355,7 @@ def run_ours(args):
     P.set_precision(args.precision)
     cfg = P.UNetConfig(**C2)
     eng = U.get_engine(cfg)
+    hbm, tf_peak, peak_src = peaks()
     # --- cached generation of this rank's request (not timed: per-request setup)
     store = P.CacheStore()
     t0 = time.perf_counter()
@@ -190,10 +367,11 @@ def run_ours(args):
     kv = eng.text_kv(P.embed_tokens(P.PromptTokens(NEW_IDS), cfg))
     lat0 = U._to_nhwc(P.initial_latent(cfg), eng.dev)
     ep = U.EditPlan(eng, arena, mask, kv, lat0)
+    ops = _op_log(eng, ep.plan)
     runner = U._Runner(eng, ep.plan, True)
     T = cfg.steps
-    runner.step(1)  # records the step (VM program) or warms + captures a CUDA graph
-    per_step_launches = runner.launches_per_step  # our kernels per step (1 = the step VM)
+    runner.step(1)  # warms + captures the step graph
+    per_step_launches = runner.launches_per_step
     for i in range(args.warmup):
         runner.step(1 + (i + 1) % T)
     torch.cuda.synchronize()
@@ -215,18 +393,30 @@ def run_ours(args):
     per_ms = ms / max(1, args.steps)
     value = ws * args.steps / (ms / 1e3)
 
-    # --- end-to-end through the public API (host mask in, host latent out, all T steps); measured
-    # before the batched section so its ~100 GB stacked arena does not sit in the allocator
-    # a stream of E2E_CALLS edit requests on the rank's cached generation: the 10% square at
-    # shifted offsets (same size), one edit() call each (sessions built from host ids / masks)
-    e2e_masks = []
-    for i in range(E2E_CALLS):
-        b = np.roll(mask.bits, (2 * i, -2 * i), axis=(0, 1))
-        e2e_masks.append(P.BinaryMask(b))
+    # --- per-kernel times of the same captured step (CUPTI, graph replay)
+    table = replay_kernels(runner, ops, T)
+    unet = U.UNet(cfg)
+    cost = {l: 4 * ep.dp.n_tiles[l] for l in range(cfg.levels)}
+    conv_fl = sum(2 * unet.layer_macs(i, cost[i.level], 77) for i in unet.layers if i.kind == "conv" and i.gated)
+    roof = {"bound": "tensor", "achieved": None, "peak": tf_peak, "unit": "TFLOP/s", "frac": None, "traffic": None}
+    kern = None
+    if table is not None:
+        conv_us = sum(us for o, us, _ in table if o["op"] == "fis_gemm" and o.get("gathered"))
+        n_conv = sum(1 for o, _, _ in table if o["op"] == "fis_gemm" and o.get("gathered"))
+        ach = conv_fl / (conv_us * 1e-6) / 1e12 if conv_us else None
+        roof.update(achieved=ach, frac=ach / tf_peak if ach else None,
+                    traffic=conv_traffic(), kernel=f"fis_gemm gated-conv gather-GEMMs ({n_conv}/step)",
+                    note=f"algorithmic {conv_fl / 1e9:.2f} GFLOP/step (2 x plan.cost x c_out x 9 c_in, reference "
+                         f"SparseMode accounting) over {conv_us:.1f} us/step of gated-conv critical-path time "
+                         f"(CUPTI kernel records of graph replays of the timed step, end_i - end_(i-1)); peak "
+                         f"{peak_src}; traffic = ncu dram bytes per launch of the L0 gated conv "
+                         f"(profiles/r02/ncu_gated_conv.json); batch 1 is latency / weight-stream bound "
+                         f"(SURVEY §7 H1), the batched section carries the tensor-bound roofline")
+        kern = kernel_summary(table, per_ms * 1e3)
+    # --- end-to-end through the public API (host mask in, host latent out, all T steps)
+    e2e_masks = [P.BinaryMask(np.roll(mask.bits, (2 * i, -2 * i), axis=(0, 1))) for i in range(E2E_CALLS)]
     sessions = [P.EditSession.create(OLD_IDS, NEW_IDS, cfg, store, user_mask=m) for m in e2e_masks]
-    # one untimed edit() first (process-level one-time costs: lazy imports, tensor-map encodes),
-    # and a garbage-collection pass so the timed calls start from a clean heap
-    P.edit(P.EditSession.create(OLD_IDS, NEW_IDS, cfg, store, user_mask=mask), cfg, store)
+    P.edit(P.EditSession.create(OLD_IDS, NEW_IDS, cfg, store, user_mask=mask), cfg, store)  # untimed warm-up
     import gc
     gc.collect()
     call_s = []
@@ -237,66 +427,28 @@ def run_ours(args):
         torch.cuda.synchronize()
         call_s.append(time.perf_counter() - t0)
     e2e_s = reduce_max(float(np.median(call_s)))
-    # --- the same sparse step on the persistent step VM (csrc/fis_vm.cu; experimental engine)
-    vm_ms = None
-    if args.precision == "bf16":
-        use_vm = eng.use_vm
-        eng.use_vm = True
-        try:
-            ep_vm = U.EditPlan(eng, arena, mask, kv, lat0)
-            vm_ms = _time_runner(U._Runner(eng, ep_vm.plan, True), T, max(3, args.steps // 2), 3)
-        finally:
-            eng.use_vm = use_vm
-    # --- dense UNet step on the same GPU (what edit() runs for a full mask; SURVEY §8 C3 bar)
-    dense_ms = dense_step_ms(eng, U, P, cfg, kv, args)
-    # --- C5-style: R concurrent independent requests on this GPU (one stream each)
-    batched = None
-    R = args.requests if args.requests > 0 else max(1, 64 // ws)  # C5: 64 requests over the box
-    if R > 1 and args.precision == "bf16":
-        from paper_2305_17423_b200 import dist as D
-        _, tf_peak, _ = peaks()
-        # C5 sharding: R * N requests assigned to ranks by estimated cost (LPT, SURVEY §8 e)
-        costs = [D.request_cost(_request(i, cfg)[2]) for i in range(R * ws)]
-        ids = D.shard_requests(costs, ws)[rank]
-        batched = stacked_requests(eng, U, P, cfg, R, args, tf_peak, ids=ids)
-        # whole job: all ranks' requests over the slowest rank's batched step (no collective in the step)
-        batched["edit_steps_per_s_all_ranks"] = ws * R * 1e3 / reduce_max(batched["ms_per_batched_step"])
-        batched.update({"masks": "5/10/25% squares at distinct offsets, distinct prompts, own cached generations",
-                        "note": "C5: 64 requests sharded by estimated cost over the GPUs (LPT), each GPU's ~64/N "
-                                "stepped as ONE stacked batch (BatchedEditPlan: concatenated rows, weights read "
-                                "once per step for all of them, block-diagonal segment attention); no collective "
-                                "in the step, one final gather of the edited latents to rank 0"})
-    sweep = mask_sweep(eng, U, P, cfg, arena, kv, lat0, args) if args.sweep else None
-
-    # --- per-kernel timing of the gated (sparse) convs: eager instrumented step
-    gflop_conv, conv_ms, gemm_ms, dense_gflop = instrumented_conv(eng, ep, U, cfg, mask)
-    hbm, tf, src = peaks()
-    achieved = gflop_conv / (conv_ms / 1e3) / 1e3 if conv_ms > 0 else 0.0  # TFLOP/s
+    # --- dense UNet step on the same GPU (what edit() runs for a full mask)
+    dense_ms, dense_kern = dense_step(eng, U, P, cfg, kv, args)
+    sweep = mask_sweep(eng, U, P, cfg, arena, kv, lat0, args, dense_ms) if not args.no_sweep else None
     line = {
         "metric": METRIC, "value": value, "unit": "edit-steps/s", "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": per_ms, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "bf16" if args.precision == "bf16" else "f32", "data": "synthetic",
-        "config": {"workload": f"C2 SD-1.5-shape sparse edit step, {int(args.mask*100)}% centered-square user mask",
+        "config": {"workload": f"C2 SD-1.5-shape sparse edit step, {int(args.mask * 100)}% centered-square user mask",
                    "model": "sparsedit toy UNet @ SD-1.5 widths (320/640/1280/1280), 2 blocks/level",
                    "latent": "1x4x64x64", "text": "77x768", "schedule_steps": T, "mask_fraction": args.mask,
                    "active_px_L0_L1": ep.dp.n_active[:2], "requests_per_gpu": 1, "parallelism": f"replicas x{ws}",
-                   "l2": "inputs larger than L2 (weights+cache slab per step > 126 MB)", "precision": args.precision,
-                   "generation_s": gen_s},
-        "roofline": {"bound": "tensor", "achieved": achieved, "peak": tf, "unit": "TFLOP/s",
-                     "frac": achieved / tf if tf else None, "traffic": conv_traffic(),
-                     "kernel": "fis_gemm gated-conv gather-GEMMs (13/step)",
-                     "note": f"algorithmic {gflop_conv:.2f} GFLOP/step over {conv_ms:.3f} ms of gated-conv GEMM time "
-                             f"(CUDA events, eager instrumented step); all GEMMs {gemm_ms:.3f} ms/step; peak {src}; "
-                             "traffic = ncu dram bytes of one L0 conv launch (profiles/r01/ncu_gated_conv.json) vs "
-                             "2.4 MB algorithmic (weights 1.84 MB + halo rows + output)"},
+                   "l2": "inputs larger than L2 (weights + cache slab streamed per step > 126 MB); no flush",
+                   "precision": args.precision, "generation_s": gen_s},
+        "roofline": roof,
+        "kernels": kern,
         "step_hbm": {"bytes_per_step": WEIGHT_BYTES_BF16, "achieved_gbs": WEIGHT_BYTES_BF16 / (per_ms / 1e3) / 1e9,
                      "peak_gbs": hbm, "frac": WEIGHT_BYTES_BF16 / (per_ms / 1e3) / 1e9 / hbm,
                      "note": "whole step vs the weight-streaming floor (221.7 M bf16 params read once per step)"},
-        "step_vm": None if vm_ms is None else {"ms_per_step": vm_ms, "edit_steps_per_s": 1e3 / vm_ms,
-                                                "note": "same sparse step as ONE persistent cooperative launch "
-                                                        "(csrc/fis_vm.cu, FIS_VM=1); experimental, not the default"},
-        "dense_baseline": {"ms_per_step": dense_ms, "steps_per_s": 1e3 / dense_ms,
-                           "sparse_speedup": dense_ms / per_ms},
+        "dense_baseline": {"ms_per_step": dense_ms, "steps_per_s": 1e3 / dense_ms, "sparse_speedup": dense_ms / per_ms,
+                           "tflops": 310.0 / dense_ms, "frac_of_peak": 310.0 / dense_ms / tf_peak,
+                           "kernels": dense_kern,
+                           "note": "dense C2 step (310.0 GFLOP algorithmic) on the same GPU, one graph replay each"},
         "gpu_launches": per_step_launches * args.steps,
         "clocks": clk.summary(),
         "e2e": {"value": T / e2e_s, "unit": "edit-steps/s", "h2d_bytes_per_step": (cfg.latent_h * cfg.latent_w * 17) // T,
@@ -306,14 +458,29 @@ def run_ours(args):
                         "shapes match, inputs copied in)",
                 "call_seconds": [round(x, 5) for x in call_s]},
     }
-    if rank == 0 and not args.no_cpu:
-        v, per = cpu_sample(C2, args.mask, 1, 0, os.cpu_count() or 1)
-        line["cpu_baseline"] = {"value": v, "unit": "edit-steps/s", "cores": os.cpu_count(), "kind": "port",
-                                "sample": "oracle port, 1 sparse step at t=1 after one dense caching step"}
     if sweep is not None:
         line["sweep"] = sweep
-    if batched is not None:
+    del runner, ep
+    # --- the same step in the fp32 parity precision (SIMT fp32; the numerics of tensors.py:76-94)
+    if args.precision == "bf16" and not args.no_fp32:
+        line["fp32_parity"] = fp32_parity_step(U, P, cfg, args, mask)
+    # --- C4: SD-2 shape, multi-round edits against one HBM generation
+    if not args.no_c4:
+        line["c4"] = c4_section(U, P, args)
+    # --- C5: 64 requests over the box, each GPU's share as one stacked batch
+    R = args.requests if args.requests > 0 else max(1, 64 // ws)
+    if R > 1 and args.precision == "bf16":
+        from paper_2305_17423_b200 import dist as D
+        store.close()
+        del store, arena
+        torch.cuda.empty_cache()
+        costs = [D.request_cost(_request(i, cfg)[2]) for i in range(R * ws)]
+        ids = D.shard_requests(costs, ws)[rank]
+        batched = stacked_requests(eng, U, P, cfg, args, tf_peak, ids=ids)
+        batched["edit_steps_per_s_all_ranks"] = ws * len(ids) * 1e3 / reduce_max(batched["ms_per_batched_step"])
         line["batched"] = batched
+    if rank == 0 and not args.no_cpu:
+        line["cpu_baseline"] = cpu_baseline(args.mask, 1, 0)
     if rank == 0:
         print(json.dumps(line))
     import torch.distributed as dist
@@ -321,79 +488,110 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
-E2E_CALLS = 5
-WEIGHT_BYTES_BF16 = 2 * 221_700_000  # SURVEY §0 item 6: 221.7 M params of the SD-1.5-shape toy UNet
-
-
 def conv_traffic():
-    """DRAM bytes per launch of the profiled gated-conv GEMM (committed ncu capture), or None."""
-    try:
-        with open(os.path.join(ROOT, "profiles", "r01", "ncu_gated_conv.json")) as f:
-            return json.load(f)["traffic_bytes_per_launch"]
-    except Exception:
-        return None
+    """DRAM bytes per launch of the profiled gated-conv GEMM (committed ncu --set full capture)."""
+    for r in ("r02", "r01"):
+        try:
+            with open(os.path.join(ROOT, "profiles", r, "ncu_gated_conv.json")) as f:
+                return json.load(f)["traffic_bytes_per_launch"]
+        except Exception:
+            continue
+    return None
 
 
-def _time_runner(runner, T, steps, warmup):
+def dense_step(eng, U, P, cfg, kv, args):
+    """Dense forward + step update of the same UNet (no recording), one graph replay per step."""
     import torch
-    runner.step(1)
-    for i in range(warmup):
-        runner.step(1 + (i + 1) % T)
-    torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    for i in range(steps):
-        runner.step(1 + i % T)
-    e1.record()
-    torch.cuda.synchronize()
-    return e0.elapsed_time(e1) / max(1, steps)
+    lat = torch.empty((cfg.steps + 1, eng.hw(0), cfg.latent_channels), dtype=torch.float32, device=eng.dev)
+    lat[0].copy_(U._to_nhwc(P.initial_latent(cfg), eng.dev))
+    plan = U.StepPlan(eng, kv, lat, None)
+    ops = _op_log(eng, plan)
+    runner = U._Runner(eng, plan, True)
+    ms = _time_runner(runner, cfg.steps, max(5, args.steps // 2), 3)
+    table = replay_kernels(runner, ops, cfg.steps)
+    return ms, (kernel_summary(table, ms * 1e3) if table is not None else None)
 
 
-def batched_requests(eng, U, P, cfg, R, args):
-    """C5-style throughput on one GPU: R independent edit requests (own cached generation, prompt,
-    mask, activations and step counter), each a captured step graph replayed on its own CUDA stream.
-    Returns (edit-steps/s over all requests, ms per round of R steps)."""
+def random_dilated(P, cfg, seed, frac=0.10):
+    """SURVEY §8 C1/C3 random-dilated mask: dilate(PCG64(s).random((H, W)) < f / 9, 1)."""
+    g = np.random.Generator(np.random.PCG64(seed))
+    return P.dilate(P.BinaryMask(g.random((cfg.latent_h, cfg.latent_w)) < frac / 9), 1)
+
+
+def mask_sweep(eng, U, P, cfg, arena, kv, lat0, args, dense_ms):
+    """C3 (cli.py:304-365): sparse step vs mask ratio on the same cache and GPU; 100% is the dense
+    step edit() runs for a full mask (unet.py:877-878)."""
+    unet = U.UNet(cfg)
+    out = []
+    cases = [(f, f"centered square {f:.0%}", P.centered_square_mask(cfg.latent_h, cfg.latent_w, f))
+             for f in (0.01, 0.05, 0.10, 0.25, 0.50, 1.0)]
+    cases.append((0.10, "random dilated 10% (seed 0)", random_dilated(P, cfg, 0)))
+    dense_gfl = 2 * sum(unet.dense_step_macs(77).values()) / 1e9
+    for f, name, mask in cases:
+        if mask.all_active():
+            ms, act, gfl = dense_ms, cfg.latent_h * cfg.latent_w, dense_gfl
+        else:
+            ep = U.EditPlan(eng, arena, mask, kv, lat0)
+            ms = _time_runner(U._Runner(eng, ep.plan, True), cfg.steps, max(5, args.steps // 2), 3)
+            cost = {l: 4 * ep.dp.n_tiles[l] for l in range(cfg.levels)}
+            gfl = 2 * sum(unet.sparse_step_macs(77, ep.dp.n_active, cost).values()) / 1e9
+            act = ep.dp.n_active[0]
+        out.append({"mask": name, "mask_fraction": round(act / (cfg.latent_h * cfg.latent_w), 4),
+                    "active_px_L0": act, "ms_per_step": ms, "edit_steps_per_s": 1e3 / ms,
+                    "algorithmic_gflop_per_step": gfl, "speedup_vs_dense": dense_ms / ms,
+                    "mac_ratio_vs_dense": dense_gfl / gfl})
+    return out
+
+
+def fp32_parity_step(U, P, cfg, args, mask):
+    """The C2 sparse step in fp32 parity precision (fp32 operands, fp32 accumulate)."""
     import torch
-    runners, streams = [], []
-    for r in range(R):
-        old, new, bits = _request(r, cfg)
-        store = P.CacheStore()
-        eng.ns = 0
-        P.generate_dense(P.PromptTokens(old), cfg, store, record="engine")
-        kv = eng.text_kv(P.embed_tokens(P.PromptTokens(new), cfg))
-        lat0 = U._to_nhwc(P.initial_latent(cfg), eng.dev)
-        ep = U.EditPlan(eng, store.arena, P.BinaryMask(bits), kv, lat0)
-        run = U._Runner(eng, ep.plan, True, ns=r + 1)
-        run._keep = (store, ep, kv)
-        run.step(1)  # warm + capture
-        runners.append(run)
-        streams.append(torch.cuda.Stream())
-    torch.cuda.synchronize()
-    T = cfg.steps
-    n = max(3, args.steps // 2)
+    eng = U.get_engine(cfg, "fp32")
+    store = P.CacheStore()
+    P.generate_dense(P.PromptTokens(OLD_IDS), cfg, store, record="engine", precision="fp32")
+    kv = eng.text_kv(P.embed_tokens(P.PromptTokens(NEW_IDS), cfg))
+    lat0 = U._to_nhwc(P.initial_latent(cfg), eng.dev)
+    ep = U.EditPlan(eng, store.arena, mask, kv, lat0)
+    ms = _time_runner(U._Runner(eng, ep.plan, True), cfg.steps, max(5, args.steps // 2), 3)
+    store.close()
+    del ep, store
+    torch.cuda.empty_cache()
+    return {"ms_per_step": ms, "edit_steps_per_s": 1e3 / ms, "dtype": "f32",
+            "note": "same C2 10% step, set_precision('fp32'): fp32 operands / accumulation (SIMT FFMA GEMMs), "
+                    "the parity mode pinned to the oracle at <= 1e-4 per step (tests/test_gpu_c2_parity.py)"}
 
-    def round_(t):
-        for run, st in zip(runners, streams):
-            with torch.cuda.stream(st):
-                run.step(t)
 
-    for i in range(3):
-        round_(1 + (i + 1) % T)
-    torch.cuda.synchronize()
-    main = torch.cuda.current_stream()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(main)
-    for st in streams:
-        st.wait_stream(main)
-    for i in range(n):
-        round_(1 + i % T)
-    for st in streams:
-        main.wait_stream(st)
-    e1.record(main)
-    torch.cuda.synchronize()
-    eng.ns = 0
-    ms = e0.elapsed_time(e1)
-    return R * n / (ms / 1e3), ms / n
+def c4_section(U, P, args):
+    """BASELINE configs[3]: SD-2 shape (96x96 latent, 1024-wide text), bf16. Device-timed sparse
+    step at 10% and end-to-end edit() rounds (new prompt + mask each) on ONE HBM generation."""
+    import torch
+    cfg = P.UNetConfig(**C4)
+    eng = U.get_engine(cfg, "bf16")
+    store = P.CacheStore()
+    P.generate_dense(P.PromptTokens(OLD_IDS), cfg, store, record="engine", precision="bf16")
+    kv = eng.text_kv(P.embed_tokens(P.PromptTokens(NEW_IDS), cfg))
+    lat0 = U._to_nhwc(P.initial_latent(cfg), eng.dev)
+    mask = P.centered_square_mask(96, 96, 0.10)
+    ep = U.EditPlan(eng, store.arena, mask, kv, lat0)
+    ms = _time_runner(U._Runner(eng, ep.plan, True), cfg.steps, max(5, args.steps // 2), 3)
+    dense_ms, _ = dense_step(eng, U, P, cfg, kv, args)
+    rounds = []
+    for k, f in enumerate((0.10, 0.05, 0.25)):
+        new = tuple(200 + k if i == 3 + k else v for i, v in enumerate(OLD_IDS))
+        m = P.BinaryMask(np.roll(P.centered_square_mask(96, 96, f).bits, (6 * k, -4 * k), axis=(0, 1)))
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        P.edit(P.EditSession.create(OLD_IDS, new, cfg, store, user_mask=m), cfg, store)
+        torch.cuda.synchronize()
+        rounds.append({"mask_fraction": f, "seconds": time.perf_counter() - t0})
+    store.close()
+    del ep, store
+    torch.cuda.empty_cache()
+    return {"ms_per_step": ms, "edit_steps_per_s": 1e3 / ms, "dense_ms_per_step": dense_ms,
+            "sparse_speedup": dense_ms / ms, "rounds_e2e": rounds,
+            "e2e_edit_steps_per_s": [cfg.steps / r["seconds"] for r in rounds],
+            "note": "96x96x4 latent, 77x1024 text, 10% centered square; rounds = successive edit() calls (new "
+                    "prompt and mask each, incl. planning and graph capture) against one recorded generation"}
 
 
 def _request(r, cfg):
@@ -408,15 +606,15 @@ def _request(r, cfg):
     return old, new, bits
 
 
-def stacked_requests(eng, U, P, cfg, R, args, peak_tf, ids=None):
-    """C5 throughput on one GPU: R edit requests stepped as ONE stacked batch (BatchedEditPlan:
-    concatenated rows, every weight read once per step for all R requests; segment attention).
-    Returns a dict: device-timed edit-steps/s over all R requests, the gated-conv gather-GEMMs'
-    tensor-core rate in that step, and one end-to-end edit_batch() call (host masks / prompts in,
-    host latents out)."""
+def stacked_requests(eng, U, P, cfg, args, peak_tf, ids):
+    """C5 throughput on one GPU: this rank's requests stepped as ONE stacked batch
+    (BatchedEditPlan: concatenated rows, every weight read once per step for all of them;
+    block-diagonal segment attention). Device-timed edit-steps/s, the gated-conv gather-GEMMs'
+    tensor-core rate inside graph replays of that step (CUPTI), and one end-to-end edit_batch()
+    call (host masks / prompts in, host latents out)."""
     import torch
     t0 = time.perf_counter()
-    ids = list(range(R)) if ids is None else list(ids)
+    ids = list(ids)
     R = len(ids)
     reqs = [_request(r, cfg) for r in ids]
     stores = [P.CacheStore() for _ in reqs]
@@ -427,39 +625,32 @@ def stacked_requests(eng, U, P, cfg, R, args, peak_tf, ids=None):
     kvs = [eng.text_kv(P.embed_tokens(P.PromptTokens(n), cfg)) for _, n, _ in reqs]
     lat0 = U._to_nhwc(P.initial_latent(cfg), eng.dev)
     bp = U.BatchedEditPlan(eng, stacked, [P.BinaryMask(b) for _, _, b in reqs], kvs, [lat0] * R)
-    run = U._Runner(eng, bp.plan, True, ns=0)  # edit_batch() below reuses this warm scratch namespace
-    ms = _time_runner(run, cfg.steps, max(3, args.steps // 2), 3)
-    # gated-conv gather-GEMMs of the batched step: CUDA events around each launch (eager step);
-    # algorithmic FLOPs count active rows only (each request's run is padded to 16 rows)
-    st = torch.cuda.current_stream()
-    recs, orig = [], eng.gemm
-
-    def timed(m, n, k, **kw):
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(st)
-        orig(m, n, k, **kw)
-        b.record(st)
-        recs.append((m, n, k, kw.get("srcs") is not None and kw.get("rows") is not None, a, b))
-
-    eng.gemm = timed
-    try:
-        eng.ns = 0
-        eng.step_dev.fill_(5)
-        eng.run_step(bp.plan)
-        torch.cuda.synchronize()
-    finally:
-        eng.gemm = orig
-        eng.ns = 0
+    ops = _op_log(eng, bp.plan)
+    run = U._Runner(eng, bp.plan, True, ns=0)
+    ms = _time_runner(run, cfg.steps, max(5, args.steps // 2), 3)
+    table = replay_kernels(run, ops, cfg.steps)
     active = {l: sum(dp.n_active[l] for dp in bp.dps) for l in range(cfg.levels)}
     padded = {l: bp.lists[l][2] for l in bp.lists}
-    conv_ms, conv_fl = 0.0, 0.0
-    for m, n, k, g, a, b in recs:
-        if g:
-            lvl = next(l for l in padded if padded[l] == m)
-            conv_ms += a.elapsed_time(b)
-            conv_fl += 2.0 * active[lvl] * n * k
-    tf = conv_fl / (conv_ms / 1e3) / 1e12 if conv_ms > 0 else 0.0
-    # end to end through the public API: R sessions in, R host latents out
+    gc_ = None
+    kern = None
+    if table is not None:
+        conv_us, conv_fl = 0.0, 0.0
+        per = []
+        for o, us, name in table:
+            if o["op"] == "fis_gemm" and o.get("gathered"):
+                lvl = next(l for l in padded if padded[l] == o["m"])
+                conv_us += us
+                fl = gated_conv_flops(o, active[lvl])
+                conv_fl += fl
+                per.append({"m_rows": o["m"], "n": o["n"], "k": o["k"], "us": round(us, 2),
+                            "tflops": round(fl / (us * 1e-6) / 1e12, 1) if us else None})
+        tf = conv_fl / (conv_us * 1e-6) / 1e12 if conv_us else 0.0
+        gc_ = {"bound": "tensor", "achieved": tf, "peak": peak_tf, "unit": "TFLOP/s",
+               "frac": tf / peak_tf if peak_tf else None, "gflop_per_step": conv_fl / 1e9,
+               "us_per_step": conv_us, "per_launch": per,
+               "note": "gathered (select-on-read) 3x3 conv GEMMs of the stacked step; algorithmic FLOPs = 2 x active "
+                       "rows x N x K (16-row request padding excluded); CUPTI critical-path time in graph replay"}
+        kern = kernel_summary(table, ms * 1e3)
     sessions = [P.EditSession.create(o, n, cfg, st_, user_mask=P.BinaryMask(b))
                 for (o, n, b), st_ in zip(reqs, stores)]
     import gc
@@ -470,7 +661,6 @@ def stacked_requests(eng, U, P, cfg, R, args, peak_tf, ids=None):
     torch.cuda.synchronize()
     e2e_s = time.perf_counter() - t1
     eng.ns = 0
-    # the one collective of the C5 path: edited latents of every rank's requests to rank 0
     from paper_2305_17423_b200 import dist as D
     t2 = time.perf_counter()
     gathered = D.gather_results({i: r.latent for i, r in zip(ids, results)}, D.dist.get_world_size()
@@ -478,73 +668,14 @@ def stacked_requests(eng, U, P, cfg, R, args, peak_tf, ids=None):
     gather_s = time.perf_counter() - t2
     return {"requests_per_gpu": R, "edit_steps_per_s": R * 1e3 / ms, "ms_per_batched_step": ms,
             "rows_L0_L1": [padded[0], padded.get(1)], "active_L0_L1": [active[0], active[1]],
-            "gated_conv": {"achieved_tflops": tf, "peak_tflops": peak_tf, "frac": tf / peak_tf if peak_tf else None,
-                           "gflop_per_step": conv_fl / 1e9, "ms_per_step": conv_ms},
+            "gated_conv": gc_, "kernels": kern,
             "e2e": {"edit_steps_per_s": R * cfg.steps / e2e_s, "seconds": e2e_s,
                     "note": "one edit_batch() call: R sessions (host masks, prompts) -> R host latents, all T steps"},
             "result_gather": {"requests_on_rank0": len(gathered), "seconds": gather_s},
-            "request_ids": ids,
-            "setup_generation_s": setup_s}
-
-
-def dense_step_ms(eng, U, P, cfg, kv, args):
-    """Dense forward + step update of the same UNet (no recording), one graph per step."""
-    import torch
-    lat = torch.empty((cfg.steps + 1, eng.hw(0), cfg.latent_channels), dtype=torch.float32, device=eng.dev)
-    lat[0].copy_(U._to_nhwc(P.initial_latent(cfg), eng.dev))
-    runner = U._Runner(eng, U.StepPlan(eng, kv, lat, None), True)
-    return _time_runner(runner, cfg.steps, max(3, args.steps // 2), 3)
-
-
-def mask_sweep(eng, U, P, cfg, arena, kv, lat0, args):
-    """C3: sparse step time vs mask ratio (centered squares), same cache and GPU."""
-    out = []
-    for f in (0.01, 0.05, 0.10, 0.25, 0.50, 1.0):
-        mask = P.centered_square_mask(cfg.latent_h, cfg.latent_w, f)
-        if mask.all_active():
-            continue
-        ep = U.EditPlan(eng, arena, mask, kv, lat0)
-        ms = _time_runner(U._Runner(eng, ep.plan, True), cfg.steps, max(3, args.steps // 2), 3)
-        unet = U.UNet(cfg)
-        cost = {l: 4 * ep.dp.n_tiles[l] for l in range(cfg.levels)}
-        gfl = 2 * sum(unet.sparse_step_macs(77, ep.dp.n_active, cost).values()) / 1e9
-        out.append({"mask_fraction": f, "active_px_L0": ep.dp.n_active[0], "ms_per_step": ms,
-                    "edit_steps_per_s": 1e3 / ms, "algorithmic_gflop_per_step": gfl})
-    return out
-
-
-def instrumented_conv(eng, ep, U, cfg, mask):
-    """Eager step with CUDA events around every GEMM; returns gated-conv GFLOP, ms, all-GEMM ms."""
-    import torch
-    st = torch.cuda.current_stream()
-    records = []
-    orig = eng.gemm
-
-    def timed(m, n, k, **kw):
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(st)
-        orig(m, n, k, **kw)
-        b.record(st)
-        records.append((m, n, k, kw.get("srcs") is not None and kw.get("rows") is not None, a, b))
-
-    eng.gemm = timed
-    try:
-        eng.step_dev.fill_(5)
-        eng.run_step(ep.plan)
-        torch.cuda.synchronize()
-    finally:
-        eng.gemm = orig
-    conv_ms = sum(a.elapsed_time(b) for (_, _, _, g, a, b) in records if g)
-    all_ms = sum(a.elapsed_time(b) for (*_, a, b) in records)
-    # algorithmic FLOPs of gated convs = 2 * plan.cost * c_out * c_in * 9 (reference accounting)
-    unet = U.UNet(cfg)
-    cost = {l: 4 * ep.dp.n_tiles[l] for l in range(cfg.levels)}
-    fl = 0
-    for i in unet.layers:
-        if i.kind == "conv" and i.gated:
-            fl += 2 * unet.layer_macs(i, cost[i.level], 77)
-    dense = 2 * sum(unet.dense_step_macs(77).values())
-    return fl / 1e9, conv_ms, all_ms, dense / 1e9
+            "setup_generation_s": setup_s,
+            "masks": "5/10/25% squares at distinct offsets, distinct prompts, own cached generations",
+            "note": "C5: 64 requests sharded by estimated cost over the GPUs (LPT), each GPU's ~64/N stepped as ONE "
+                    "stacked batch; no collective in the step, one final gather of the edited latents to rank 0"}
 
 
 def main():
@@ -556,7 +687,9 @@ def main():
     ap.add_argument("--mask", type=float, default=0.10)
     ap.add_argument("--precision", default="bf16", choices=["fp32", "bf16"])
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--sweep", action="store_true", help="also time the C3 mask-ratio sweep")
+    ap.add_argument("--no-sweep", action="store_true")
+    ap.add_argument("--no-fp32", action="store_true")
+    ap.add_argument("--no-c4", action="store_true")
     ap.add_argument("--requests", type=int, default=0,
                     help="requests per GPU of the C5 batched measurement (0: 64 / n_gpus; 1 disables)")
     args = ap.parse_args()

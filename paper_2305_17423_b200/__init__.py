@@ -5,7 +5,7 @@ all compute runs in hand-written sm_100a kernels (libfisedit.so, C ABI in
 include/fisedit.h). See DESIGN.md.
 """
 
-from .cache import BufferPool, CacheKey, CacheStats, CacheStore, Role
+from .cache import BufferPool, CacheKey, CacheStats, CacheStore, CompactTensor, Role, compact_tensor, materialize_payload
 from .errors import CacheMissError, ConfigError, ContractViolation
 from .masks import (BinaryMask, DiffMap, MaskPyramid, OtsuResult, accumulate_diff, build_pyramid,
                     centered_square_mask, dilate, mask_from_tensor, mask_to_tensor, otsu_threshold, save_mask_pgm)

@@ -133,6 +133,8 @@ class CacheStore:
     # -- public operations ------------------------------------------------------
     def put(self, key, payload, overwrite: bool = False) -> None:
         k = _as_key(key)
+        if isinstance(payload, CompactTensor):
+            payload = payload.materialize()
         if not isinstance(payload, np.ndarray):
             raise ContractViolation(f"unsupported payload type {type(payload)}")
         if payload.dtype != np.float32:
@@ -215,7 +217,20 @@ class CacheStore:
     def hot_keys(self):
         return set(self.keys())
 
+    def graph_cache(self) -> dict:
+        """Captured edit-step graphs over this store's generation (unet._cached_runner). Owned by
+        the store, not the arena: a graph's plan references the arena, so keeping them here
+        avoids a reference cycle (whose collection could run inside a later graph capture) and
+        frees them deterministically with the store or on close()."""
+        g = getattr(self, "_graphs", None)
+        if g is None:
+            from collections import OrderedDict
+            g = self._graphs = OrderedDict()
+        return g
+
     def close(self) -> None:
+        if getattr(self, "_graphs", None):
+            self._graphs.clear()
         self._arena = None
         self._extra.clear()
         self._closed = True
@@ -227,5 +242,52 @@ class CacheStore:
         self.close()
 
 
+@dataclass(frozen=True)
+class CompactTensor:
+    """A layer output kept only at the pixels outside an edit mask (reference cache.py:64-92).
+
+    `values` [n, c, n_stored] holds the stored (mask-complement) pixels in row-major pixel
+    order; `index` lists either the active or the stored pixel ids, whichever list is shorter
+    (`index_is_active` says which). The HBM arena never compacts (edits read the pristine
+    generation); this type exists for callers of the reference payload API.
+    """
+
+    shape: tuple
+    values: np.ndarray
+    index: np.ndarray
+    index_is_active: bool
+
+    @property
+    def nbytes(self) -> int:
+        return int(self.values.nbytes + self.index.nbytes)
+
+    def stored_positions(self) -> np.ndarray:
+        hw = int(self.shape[2]) * int(self.shape[3])
+        if not self.index_is_active:
+            return self.index.astype(np.int64)
+        keep = np.ones(hw, dtype=bool)
+        keep[self.index.astype(np.int64)] = False
+        return np.flatnonzero(keep)
+
+    def materialize(self) -> np.ndarray:
+        """Full float32 tensor: stored pixels restored, zeros at the active ones."""
+        n, c, h, w = (int(v) for v in self.shape)
+        out = np.zeros((n, c, h * w), dtype=np.float32)
+        out[:, :, self.stored_positions()] = self.values
+        return out.reshape(n, c, h, w)
+
+
+def compact_tensor(arr: np.ndarray, mask_bits: np.ndarray) -> CompactTensor:
+    """Drop the mask-active pixels of a (n, c, h, w) payload (reference cache.py:95-105)."""
+    n, c, h, w = arr.shape
+    bits = np.asarray(mask_bits, dtype=bool).ravel()
+    stored, active = np.flatnonzero(~bits), np.flatnonzero(bits)
+    vals = arr.reshape(n, c, h * w)[:, :, stored].copy()
+    use_active = active.size <= stored.size
+    idx = (active if use_active else stored).astype(np.int32)
+    return CompactTensor((n, c, h, w), vals, idx, use_active)
+
+
 def materialize_payload(payload):
-    return payload
+    """Full ndarray of a payload (CompactTensor materialised, arrays returned as is)."""
+    return payload.materialize() if isinstance(payload, CompactTensor) else payload

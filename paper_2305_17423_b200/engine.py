@@ -121,6 +121,9 @@ class Launcher:
         # stacked images of the step being launched (BatchedSparsePlan: R requests as one batch)
         self.batch = 1
         self.launches = 0
+        # when a list: every launch appends {"op", "kernels", ...shape} (bench.py maps profiled
+        # kernels of a step back to ops with it)
+        self.op_log: list | None = None
         self._scratch = {}
         self.fused_xattn = False  # SIMT xattn is latency-bound; superseded by fis_attn
         # tcgen05 fused attention (csrc/fis_attn.cu: TMA-fed, log2 softmax, resident S for <= 256
@@ -144,6 +147,11 @@ class Launcher:
             self.capture.append((name, args, b_static))
             return
         L.call(name, args)
+
+    def _count(self, name, kernels=1, **info):
+        self.launches += kernels
+        if self.op_log is not None and self.capture is None:
+            self.op_log.append(dict(op=name, kernels=kernels, **info))
 
     def _state(self):
         st = self._ns_state.get(self.ns)
@@ -176,10 +184,12 @@ class Launcher:
         return t
 
 
+    WS_FLOATS = (1 << 25) + 1024  # 128 MB split-K workspace per namespace; the split choice respects ws_floats
+
     def _ensure_ws(self, floats):
-        floats = min(floats, 1 << 25)  # 128 MB cap; the split choice respects ws_floats
-        if self._ws.numel() < floats:
-            self._state()["ws"] = torch.empty(int(floats * 1.25) + 1024, dtype=torch.float32, device=self.dev)
+        # allocated once at its cap and never replaced: captured CUDA graphs hold its raw pointer
+        if self._ws.numel() < self.WS_FLOATS:
+            self._state()["ws"] = torch.empty(self.WS_FLOATS, dtype=torch.float32, device=self.dev)
 
     def _splits(self, m, n, k):
         tiles = ((m + 63) // 64) * ((n + 63) // 64)
@@ -235,7 +245,7 @@ class Launcher:
         g.static_meta = 1 if self.static_meta else 0
         self.last_gemm = g  # inspected by tests (fis_gemm_kernel_kind)
         self._call("fis_gemm", g, b_static)
-        self.launches += 1
+        self._count("fis_gemm", m=m, n=n, k=k, gathered=rows is not None and srcs is not None, conv=srcs is not None)
 
     def softmax(self, rows, cols, pad_cols, s: DRef, scale, p: DRef, map_: DRef | None = None, cached=None,
                 verbatim=False, pairs=None):
@@ -249,7 +259,7 @@ class Launcher:
             a.npairs, a.pair_old, a.pair_new = po.numel(), L.ptr(po), L.ptr(pn)
         a.step = L.ptr(self.step_dev)
         self._call("fis_softmax", a)
-        self.launches += 1
+        self._count("fis_softmax", rows=rows, cols=cols)
 
 class VmProgram:
     """A recorded step (list of launches) planned for the persistent step VM (csrc/fis_vm.cu).
@@ -448,7 +458,7 @@ class Engine(Launcher):
             a = L.XattnArgs(m, c, nt, DRef(q).ref(), DRef(k).ref(), DRef(v).ref(), scale, x.ref(), _r(pre),
                             out.ref(), L.ptr(self.step_dev))
             self._call("fis_xattn", a)
-            self.launches += 1
+            self._count("fis_xattn", m=m, n_keys=nt)
             return
         if ctrl is None and map_ is None and self.use_fused_attn(c, m, nt, pre):
             self.attn(m, nt, c, DRef(q), DRef(k), DRef(vt), scale, x, out, pre)
@@ -485,12 +495,14 @@ class Engine(Launcher):
             ws = self.scratch("attn_p", (m * _pad(maxk, 128),), torch.bfloat16)
             a.max_seg_k, a.ws, a.ws_bytes = maxk, L.ptr(ws), ws.numel() * 2
         self._call("fis_attn", a)
-        self.launches += max(1, L.lib().fis_attn_launches(C.byref(a)))  # kernels (2 when P is shared)
+        # kernels (2 when P is shared)
+        self._count("fis_attn", max(1, L.lib().fis_attn_launches(C.byref(a))), m=m, n_keys=n_keys, d=d,
+                    segs=segs is not None)
 
     def gn_stats(self, x: DRef, hw, c, mean: DRef, var: DRef, n_img=1):
         a = L.GnStatsArgs(hw, c, self.groups, x.ref(), mean.ref(), var.ref(), L.ptr(self.step_dev), n_img)
         self._call("fis_gn_stats", a)
-        self.launches += 1
+        self._count("fis_gn_stats", rows=hw, c=c)
 
     def gn_apply(self, lid, x: DRef, rows, c, mean: DRef, var: DRef, y_norm: DRef | None, y_silu: DRef | None,
                  fused_stats: bool = False, img_rows=0, row_img=None):
@@ -503,28 +515,28 @@ class Engine(Launcher):
         a.y_norm, a.y_silu = _r(y_norm), _r(y_silu)
         a.step = L.ptr(self.step_dev)
         self._call("fis_gn" if fused_stats else "fis_gn_apply", a)
-        self.launches += 1
+        self._count("fis_gn" if fused_stats else "fis_gn_apply", rows=rows, c=c)
 
     def pool(self, fv: FeatVal, rows, n, out: DRef):
         a = L.PoolArgs()
         a.n, a.c, a.src, a.rows, a.out = n, fv.c, self.src(fv), L.ptr(rows), out.ref()
         a.step = L.ptr(self.step_dev)
         self._call("fis_pool2", a)
-        self.launches += 1
+        self._count("fis_pool2", rows=n, c=fv.c)
 
     def up2(self, fv: FeatVal, n, out: DRef):
         a = L.PoolArgs()
         a.n, a.c, a.src, a.rows, a.out = n, fv.c, self.src(fv), None, out.ref()
         a.step = L.ptr(self.step_dev)
         self._call("fis_up2", a)
-        self.launches += 1
+        self._count("fis_up2", rows=n, c=fv.c)
 
     def materialize(self, fv: FeatVal, out: DRef, n_img: int = 1):
         src = self.src(fv)
         src.h *= n_img  # stacked images: a per-pixel op over n_img * h * w pixels
         a = L.MaterializeArgs(fv.c, src, out.ref(), L.ptr(self.step_dev))
         self._call("fis_materialize", a)
-        self.launches += 1
+        self._count("fis_materialize", c=fv.c)
 
     # ------------------------------------------------------------ one UNet step
     def record_step(self, plan: "StepPlan") -> VmProgram:

@@ -262,9 +262,16 @@ class _Runner:
             s = torch.cuda.Stream()
             s.wait_stream(torch.cuda.current_stream())
             g = torch.cuda.CUDAGraph()
-            with torch.cuda.stream(s):
-                with torch.cuda.graph(g, stream=s):
-                    eng.run_step(self.plan)
+            import gc
+            gc_on = gc.isenabled()
+            gc.disable()  # a collection inside the capture could destroy other graphs (invalidating it)
+            try:
+                with torch.cuda.stream(s):
+                    with torch.cuda.graph(g, stream=s):
+                        eng.run_step(self.plan)
+            finally:
+                if gc_on:
+                    gc.enable()
             torch.cuda.current_stream().wait_stream(s)
             self.graph = g
             return
@@ -338,6 +345,11 @@ def _arena_of(store: CacheStore, config: UNetConfig, t_first: int):
         unet = UNet(config)
         lid = next(i.layer_id for i in unet.layers if i.gated)
         raise CacheMissError(t_first, lid, "layer_output")
+    if a.eng.config.key() != config.key():
+        # the kernels would read the recorded slabs with another model's shapes (reference:
+        # ContractViolation / CacheMissError on a cached-shape mismatch, sparse.py:174-181)
+        raise ContractViolation(f"store holds a generation of a different UNetConfig "
+                                f"({a.eng.config.key()} != {config.key()})")
     return a
 
 
@@ -423,33 +435,30 @@ class EditPlan:
         return out
 
 
-_GRAPHS: "OrderedDict" = None
-_GRAPH_CACHE_SIZE = 8
+_GRAPH_CACHE_SIZE = 4  # captured edit-step graphs kept per cached generation (CacheStore.graph_cache)
 
 
-def _cached_runner(eng: Engine, arena: Arena, start: int, ep: "EditPlan", kv):
+def _cached_runner(eng: Engine, store: CacheStore, start: int, ep: "EditPlan", kv):
     """Step runner of an edit, reusing a captured step graph when an earlier edit on the same
     cached generation had the same active-row counts per level (same launch shapes): the new
     edit's row lists, pixel->row maps, start latent rows and text K/V are copied (device to
-    device) into the buffers that graph reads, instead of capturing a new one."""
-    global _GRAPHS
-    from collections import OrderedDict
-    if _GRAPHS is None:
-        _GRAPHS = OrderedDict()
+    device) into the buffers that graph reads, instead of capturing a new one. The graphs are
+    owned by the store (CacheStore.graph_cache: freed with it, or by close())."""
     if not _use_graphs() or eng.use_vm:
         return _Runner(eng, ep.plan, _use_graphs())
+    graphs = store.graph_cache()
     n_text = next(iter(kv.values()))[0].shape[0]
     gated = tuple(n for l, n in enumerate(ep.dp.n_active) if eng.gated[l])  # only gated levels shape launches
-    key = (id(eng), id(arena), start, gated, n_text)
-    hit = _GRAPHS.get(key)
+    key = (id(eng), start, gated, n_text)
+    hit = graphs.get(key)
     if hit is None:
         runner = _Runner(eng, ep.plan, True)
-        _GRAPHS[key] = (runner, ep, kv)
-        if len(_GRAPHS) > _GRAPH_CACHE_SIZE:
-            _GRAPHS.popitem(last=False)
+        graphs[key] = (runner, ep, kv)
+        if len(graphs) > _GRAPH_CACHE_SIZE:
+            graphs.popitem(last=False)
         return runner
     runner, ep0, kv0 = hit
-    _GRAPHS.move_to_end(key)
+    graphs.move_to_end(key)
     for l in range(len(ep.dp.rows)):
         ep0.dp.rows[l].copy_(ep.dp.rows[l])
         ep0.dp.index[l].copy_(ep.dp.index[l])
@@ -489,28 +498,47 @@ def edit(session: EditSession, config: UNetConfig, store: CacheStore) -> EditRes
         lat0 = torch.where(m, outcome._control_dev, arena.latent[session.t2])
     plans = {}
     if mask.all_active():
-        latents = torch.empty((T + 1, eng.hw(0), cl), dtype=torch.float32, device=eng.dev)
-        latents[start - 1].copy_(lat0)
-        _Runner(eng, StepPlan(eng, kv, latents, None), _use_graphs()).run(start, T)
-        final = latents[T]
-        dense = unet.dense_step_macs(n_new)
-        for lid, m_ in dense.items():
-            phase2.add(lid, m_ * (T - start + 1))
+        final = _dense_edit(eng, kv, lat0, start)
+        _add_dense_macs(phase2, unet, n_new, T - start + 1)
     else:
         ep = EditPlan(eng, arena, mask, kv, lat0)
-        _cached_runner(eng, arena, start, ep, kv).run(start, T)
+        _cached_runner(eng, store, start, ep, kv).run(start, T)
         final = ep.final_latent(eng, arena)
-        levels = sorted({i.level for i in unet.layers if i.gated})
-        cost = {l: 4 * ep.dp.n_tiles[l] for l in range(config.levels)}
-        per_step = unet.sparse_step_macs(n_new, ep.dp.n_active, cost)
-        for lid, m_ in per_step.items():
-            phase2.add(lid, m_ * (T - start + 1))
-        for l in levels:
-            org = ep.dp.origins(l)
-            plans[l] = GatherPlan((4, 4), (2, 2), (3, 3), org, 4 * len(org), (H >> l, W >> l))
+        _add_sparse_macs(phase2, unet, n_new, ep.dp, T - start + 1)
+        plans = _gather_plans(unet, ep.dp)
     latent = _to_nchw(final, cl, H, W)
     rep = _build_report(unet, n_new, config, [outcome.phase1_macs, phase2])
     return EditResult(latent, rep, store.stats(), mask, False, outcome.phase1_macs.total, phase2.total, plans)
+
+
+def _dense_edit(eng: Engine, kv, lat0: torch.Tensor, start: int) -> torch.Tensor:
+    """Full-mask edit: plain dense steps start..T with fresh statistics (unet.py:860,877-878)."""
+    cfg = eng.config
+    latents = torch.empty((cfg.steps + 1, eng.hw(0), cfg.latent_channels), dtype=torch.float32, device=eng.dev)
+    latents[start - 1].copy_(lat0)
+    _Runner(eng, StepPlan(eng, kv, latents, None), _use_graphs()).run(start, cfg.steps)
+    return latents[cfg.steps]
+
+
+def _add_dense_macs(counter: _MacsCounter, unet: UNet, n_text: int, n_steps: int):
+    for lid, m_ in unet.dense_step_macs(n_text).items():
+        counter.add(lid, m_ * n_steps)
+
+
+def _add_sparse_macs(counter: _MacsCounter, unet: UNet, n_text: int, dp: DevicePlan, n_steps: int):
+    """SparseMode MACs (unet.py:604-663): gated convs count plan.cost, attention active pixels."""
+    cost = {l: 4 * dp.n_tiles[l] for l in range(unet.config.levels)}
+    for lid, m_ in unet.sparse_step_macs(n_text, dp.n_active, cost).items():
+        counter.add(lid, m_ * n_steps)
+
+
+def _gather_plans(unet: UNet, dp: DevicePlan) -> dict:
+    cfg = unet.config
+    plans = {}
+    for l in sorted({i.level for i in unet.layers if i.gated}):
+        org = dp.origins(l)
+        plans[l] = GatherPlan((4, 4), (2, 2), (3, 3), org, 4 * len(org), (cfg.latent_h >> l, cfg.latent_w >> l))
+    return plans
 
 
 # reference-compatible names of the per-layer mode protocol (unet.py:464-663,676,781)
@@ -665,14 +693,34 @@ def edit_batch(sessions, config: UNetConfig) -> list:
         else:
             m = torch.from_numpy(o.mask.bits.ravel().copy()).to(eng.dev)[:, None]
             lat0s.append(torch.where(m, o._control_dev, v.latent[s.t2]))
-    skv = eng.text_kv_stacked([embed_tokens(s.new_tokens, config) for s in sessions])
-    bp = BatchedEditPlan(eng, stacked, masks, None, lat0s, stacked_kv=skv)
+    # an all-active mask is a plain dense edit with fresh GroupNorm statistics (unet.py:860,877-878),
+    # not a sparse step over the old generation's cached statistics: such requests ride in the
+    # stacked batch with an empty mask (their rows are never read back) and are stepped densely
+    full = [o.mask is not None and o.mask.all_active() for o in outcomes]
+    batch_masks = [BinaryMask(np.zeros((H, W), dtype=bool)) if f else m for f, m in zip(full, masks)]
+    texts = [embed_tokens(s.new_tokens, config) for s in sessions]
+    skv = eng.text_kv_stacked(texts)
+    bp = BatchedEditPlan(eng, stacked, batch_masks, None, lat0s, stacked_kv=skv)
     _Runner(eng, bp.plan, _use_graphs()).run(start, T)
     final = bp.final_latents(eng, stacked)
     hw = eng.hw(0)
+    for r, f in enumerate(full):
+        if f:
+            final[r * hw:(r + 1) * hw] = _dense_edit(eng, eng.text_kv(texts[r]), lat0s[r], start)
     fin = final.view(len(sessions), H, W, cl).permute(0, 3, 1, 2).contiguous().cpu().numpy()  # one D2H
+    unet = UNet(config)
     results = [None] * len(sessions)
     for r, (s, o) in enumerate(zip(sessions, outcomes)):
-        results[order[r]] = EditResult(fin[r:r + 1], None, s.store.stats(), o.mask, o.no_edit,
-                                       o.phase1_macs.total, 0)
+        n_new = len(s.new_tokens.ids)
+        phase2 = _MacsCounter()
+        plans = {}
+        if not o.no_edit:
+            if full[r]:
+                _add_dense_macs(phase2, unet, n_new, T - start + 1)
+            else:
+                _add_sparse_macs(phase2, unet, n_new, bp.dps[r], T - start + 1)
+                plans = _gather_plans(unet, bp.dps[r])
+        rep = _build_report(unet, n_new, config, [o.phase1_macs, phase2])
+        results[order[r]] = EditResult(fin[r:r + 1], rep, s.store.stats(), o.mask, o.no_edit,
+                                       o.phase1_macs.total, phase2.total, plans)
     return results

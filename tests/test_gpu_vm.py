@@ -168,11 +168,12 @@ def test_edit_graph_reuse_matches_fresh_capture(P):
     b1[4:12, 6:14] = True
     b2 = np.zeros((32, 32), bool)
     b2[16:24, 18:26] = True  # same 8x8 size -> same counts per level
-    U._GRAPHS = None
+    graphs = store.graph_cache()  # captured edit graphs are owned by the store of the generation
+    graphs.clear()
     P.edit(P.EditSession.create(OLD, NEW, cfg, store, user_mask=P.BinaryMask(b1)), cfg, store)
     reused = P.edit(P.EditSession.create(OLD, (3, 5, 13, 11), cfg, store, user_mask=P.BinaryMask(b2)), cfg, store)
-    assert len(U._GRAPHS) == 1  # the second edit hit the first one's graph
-    U._GRAPHS = None
+    assert len(graphs) == 1  # the second edit hit the first one's graph
+    graphs.clear()
     fresh = P.edit(P.EditSession.create(OLD, (3, 5, 13, 11), cfg, store, user_mask=P.BinaryMask(b2)), cfg, store)
     eng.use_vm = vm
     assert np.array_equal(reused.latent, fresh.latent)
