@@ -356,6 +356,9 @@ int fis_vm_attn_slice(int m, int n_keys, int d, int dv);
 int fis_trace(int on);
 int fis_trace_read(unsigned long long* out16);
 int fis_trace_read_ctas(unsigned long long* out2048); /* per CTA: entry, MMA done, cluster sync, exit */
+/* launch trace: buf (device, >= 16 + 16 * 4096 u64, zeroed) receives, per kernel launch in start
+   order, CTA (0,0,0)'s %globaltimer phase stamps (buf[0] = launch counter); NULL switches it off */
+int fis_trace_launches(unsigned long long* buf);
 
 /* misc */
 int fis_abi_version(void);

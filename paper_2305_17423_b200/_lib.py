@@ -159,6 +159,8 @@ def lib():
         L.fis_gemm_kernel_kind.argtypes = [C.POINTER(GemmArgs)]
         L.fis_gemm_kernel_kind.restype = C.c_int
         L.fis_gemm_big_launch_count.restype = C.c_longlong
+        L.fis_trace_launches.argtypes = [C.c_void_p]
+        L.fis_trace_launches.restype = C.c_int
         L.fis_attn_launches.argtypes = [C.POINTER(AttnArgs)]
         L.fis_attn_launches.restype = C.c_int
         if L.fis_vm_op_size() != C.sizeof(VmOp):

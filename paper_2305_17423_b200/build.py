@@ -35,16 +35,19 @@ def _stale() -> bool:
     return any(p.stat().st_mtime > t for p in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, trace: bool = False) -> Path:
+    """trace=True: a profiling build with the launch / phase probes (-DFIS_TRACE) into
+    libfisedit_trace.so (load it with FIS_LIB=libfisedit_trace.so); the product build has none."""
+    lib = PKG / "libfisedit_trace.so" if trace else LIB
+    if not force and not trace and not _stale():
         return LIB
-    objdir = PKG / "build"
+    objdir = PKG / ("build_trace" if trace else "build")
     objdir.mkdir(exist_ok=True)
     objs = []
     procs = []
     for src in sources():
         obj = objdir / (src.stem + ".o")
-        cmd = [NVCC, *ARCH, *FLAGS, "-c", str(src), "-o", str(obj)]
+        cmd = [NVCC, *ARCH, *FLAGS, *(["-DFIS_TRACE"] if trace else []), "-c", str(src), "-o", str(obj)]
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
         procs.append((src, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT)))
@@ -58,13 +61,12 @@ def build(force: bool = False, verbose: bool = False) -> Path:
             failed.append(src.name)
     if failed:
         raise RuntimeError(f"nvcc failed for {failed}")
-    tmp = LIB.with_suffix(".so.tmp")
+    tmp = lib.with_suffix(".so.tmp")
     cmd = [NVCC, *ARCH, "-shared", "-o", str(tmp), *map(str, objs), "-lcuda"]
     subprocess.run(cmd, check=True)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose="-v" in sys.argv)
-    print(LIB)
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, trace="--trace" in sys.argv))

@@ -9,6 +9,16 @@ int fis_gemm_big_eligible(const fis_gemm_args* a);
 int fis_gemm_big_launch(const fis_gemm_args* a, cudaStream_t stream);
 
 extern "C" {
+int fis_ltr_set_tc(unsigned long long* p);
+int fis_ltr_set_attn(unsigned long long* p);
+int fis_ltr_set_simt(unsigned long long* p);
+int fis_ltr_set_ops(unsigned long long* p);
+int fis_ltr_set_big(unsigned long long* p);
+
+int fis_trace_launches(unsigned long long* buf) {
+    return fis_ltr_set_tc(buf) | fis_ltr_set_attn(buf) | fis_ltr_set_simt(buf) | fis_ltr_set_ops(buf) |
+           fis_ltr_set_big(buf);
+}
 
 int fis_abi_version(void) { return FIS_ABI_VERSION; }
 

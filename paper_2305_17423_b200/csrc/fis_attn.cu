@@ -26,10 +26,11 @@ namespace attn {
 using namespace fis::tc;
 
 constexpr int THREADS = 192, TMA_WARP = 4, MMA_WARP = 5;
-constexpr int STAGES = 3;
-constexpr int A_BYTES = 128 * 64 * 2;            // Q chunk
-constexpr int B_BYTES = 256 * 64 * 2;            // K chunk (128 keys) or V^T chunk (<= 256 rows)
-constexpr int STAGE = A_BYTES + B_BYTES;
+// a stage holds a Q chunk + a K chunk (S block) or one V^T chunk (<= 256 rows x 64 keys): 32 KB,
+// four of them (128 KB of operands in flight per CTA; the S passes are bound by bytes in flight)
+constexpr int STAGES = 4;
+constexpr int A_BYTES = 128 * 64 * 2;            // Q chunk (K chunk at +A_BYTES)
+constexpr int STAGE = 2 * A_BYTES;               // = V^T chunk bytes at dvs = 256
 constexpr int P_BYTES = 2 * 128 * 64 * 2;        // P tile: 128 rows x 128 keys, two 64-key SW128 chunks
 constexpr int SMEM = STAGES * STAGE + 2 * P_BYTES + 1024 + 256 + 1024;  // + key-split statistics exchange
 constexpr uint32_t O_COL = 256;                  // TMEM: S buffers at 0 / 128, O at 256
@@ -108,6 +109,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     float2* xst = (float2*)(ptile + 2 * P_BYTES + 256);  // [128] key-split (max, sum) exchange
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int ls = ltr_begin(2 + pmode_in * 16);  // thread 0 of CTA (0,0,0) only
     int q_beg = 0, q_end = a.m, k_beg = 0, n_keys = a.n_keys;
     if (a.nseg > 0) {
         const int sg = blockIdx.z;
@@ -164,9 +166,26 @@ __global__ void __launch_bounds__(THREADS, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    const int t = cur_step(a.step);  // host-written before the step: safe to read before the wait
+    ltr(ls, 1);
+    if (warp == TMA_WARP && lane == 0 && a.nseg == 0 && !idle) {
+        // cross attention: K and V^T are the per-edit text keys / values (no kernel of the step writes
+        // them) -> pull this CTA's chunks into L2 while the previous kernel runs. Self attention reads
+        // K / V from the QKV GEMM just before it (already in L2): K lives in the Q buffer's rows.
+        const char* qb = (const char*)a.q.ptr;
+        const char* kb = (const char*)a.k.ptr;
+        const bool self_kv = kb >= qb && kb < qb + (long long)a.m * a.q.ld * 2;
+        if (!self_kv) {
+            const int nkb2 = (n_keys + 127) / 128, dch2 = a.d / 64;
+            for (int j = 0; j < nkb2; j++)
+                for (int kc = 0; kc < dch2; kc++) tma_prefetch2d(&tk, kc * 64, k_beg + j * 128);
+            for (int j = 0; j < nkb2; j++)
+                for (int h = 0; h < 2; h++) tma_prefetch2d(&tv, k_beg + j * 128 + h * 64, c0);
+        }
+    }
     pdl_trigger();
     pdl_wait();
-    const int t = cur_step(a.step);
+    ltr(ls, 2);
 
     if (idle && warp != TMA_WARP && warp != MMA_WARP) goto ks_softmax;
     if (idle) goto done;
@@ -194,7 +213,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             auto load_v = [&](int j) {
                 for (int h = 0; h < 2; h++) {
                     const int st = stage((uint32_t)(dvs * 64 * 2));
-                    tma2d(sbase + st * STAGE + A_BYTES, &tv, k_beg + j * 128 + h * 64, c0, full + st);
+                    tma2d(sbase + st * STAGE, &tv, k_beg + j * 128 + h * 64, c0, full + st);
                 }
             };
             if (pmode == P_IN) {  // P tiles of this query tile from the scratch (written by the P_OUT launch)
@@ -259,7 +278,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                 mbar_wait(full + st, (it / STAGES) & 1);
                 tc_fence_after();
                 if (lane == 0) {
-                    const uint32_t sbb = sbase + st * STAGE + A_BYTES;
+                    const uint32_t sbb = sbase + st * STAGE;  // V^T chunk
                     const uint32_t pa = pbase + pb * P_BYTES + h * (128 * 128);
 #pragma unroll
                     for (int kk = 0; kk < 4; kk++)
@@ -308,6 +327,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             for (int j = 0; j < nkb; j++) {
                 const int b = sb & 1;
                 mbar_wait(s_ready + b, (sb >> 1) & 1);
+                if (sb == 0) ltr(ls, 3);
                 tc_fence_after();
                 const uint32_t trow = tmem + lane_off + b * 128;
                 const int kbase = j * 128;
@@ -401,36 +421,48 @@ __global__ void __launch_bounds__(THREADS, 1)
         // epilogue: O row slice + residual -> out
         if (pmode == P_OUT) goto done;
         mbar_wait(o_done, 0);
+        ltr(ls, 4);
         tc_fence_after();
-        {  // tcgen05.ld is warp-collective: every lane loads, rows of this segment store
-            const bool live = r < q_end;
-            char* ob = ref_base(a.out, t);
-            char* pbp = a.pre.ptr ? ref_base(a.pre, t) : nullptr;
-            const char* rb = a.res.ptr ? ref_base(a.res, t) : nullptr;
+        {
+            // stage the O row slice (fp32) in the idle pipeline stages, then the 128 softmax threads
+            // add the residual and store 16-column chunks columns-fastest (coalesced 16-byte runs)
+            // instead of one row per thread (whose residual loads serialised one L2 round trip per
+            // 32 columns)
+            constexpr int OLD = 256 + 4;  // staging row pitch (floats)
+            float* ost = (float*)smem;
 #pragma unroll 1
             for (int cb = 0; cb < dvs; cb += 32) {
                 tmem_ld32(tmem + lane_off + O_COL + cb, v);
-                const int n = c0 + cb;
-                const int nvalid = min(32, a.dv - n);
-                if (nvalid <= 0) break;
-                if (!live) continue;
-                if (pbp) {
-                    store_row16(pbp, a.pre.dtype, (long long)r * a.pre.ld + n, min(16, nvalid), v);
-                    if (nvalid > 16) store_row16(pbp, a.pre.dtype, (long long)r * a.pre.ld + n + 16, nvalid - 16, v + 16);
+#pragma unroll
+                for (int q = 0; q < 8; q++)
+                    *(float4*)(ost + lr * OLD + cb + 4 * q) = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+            }
+            asm volatile("bar.sync 2, 128;" ::: "memory");
+            char* ob = ref_base(a.out, t);
+            char* pbp = a.pre.ptr ? ref_base(a.pre, t) : nullptr;
+            const char* rb = a.res.ptr ? ref_base(a.res, t) : nullptr;
+            const int chunks = dvs / 16;
+            const int nrows = min(128, q_end - m0);
+#pragma unroll 1
+            for (int item = tid; item < nrows * chunks; item += 128) {
+                const int rr = item / chunks, cc = (item % chunks) * 16;
+                const int n = c0 + cc, row = m0 + rr;
+                const int nvalid = min(16, a.dv - n);
+                if (nvalid <= 0) continue;
+                float w[16];
+#pragma unroll
+                for (int q = 0; q < 4; q++) {
+                    const float4 f = *(const float4*)(ost + rr * OLD + cc + 4 * q);
+                    w[4 * q] = f.x; w[4 * q + 1] = f.y; w[4 * q + 2] = f.z; w[4 * q + 3] = f.w;
                 }
+                if (pbp) store_row16(pbp, a.pre.dtype, (long long)row * a.pre.ld + n, nvalid, w);
                 if (rb) {
                     float q[16];
-                    load_row16(rb, a.res.dtype, (long long)r * a.res.ld + n, min(16, nvalid), q);
+                    load_row16(rb, a.res.dtype, (long long)row * a.res.ld + n, nvalid, q);
 #pragma unroll
-                    for (int e2 = 0; e2 < 16; e2++) v[e2] = __fadd_rn(v[e2], q[e2]);
-                    if (nvalid > 16) {
-                        load_row16(rb, a.res.dtype, (long long)r * a.res.ld + n + 16, nvalid - 16, q);
-#pragma unroll
-                        for (int e2 = 0; e2 < 16; e2++) v[16 + e2] = __fadd_rn(v[16 + e2], q[e2]);
-                    }
+                    for (int e2 = 0; e2 < 16; e2++) w[e2] = __fadd_rn(w[e2], q[e2]);
                 }
-                store_row16(ob, a.out.dtype, (long long)r * a.out.ld + n, min(16, nvalid), v);
-                if (nvalid > 16) store_row16(ob, a.out.dtype, (long long)r * a.out.ld + n + 16, nvalid - 16, v + 16);
+                store_row16(ob, a.out.dtype, (long long)row * a.out.ld + n, nvalid, w);
             }
         }
     }
@@ -505,10 +537,13 @@ teardown:
     tc_fence_before();
     __syncthreads();
     if (warp == MMA_WARP) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+    ltr(ls, 7);
 }
 
 }  // namespace attn
 }  // namespace fis
+
+FIS_LTR_SETTER(fis_ltr_set_attn)
 
 // value-slice width: largest multiple of 32 dividing dv with <= 256 columns
 static int attn_slice(int dv) {

@@ -19,6 +19,43 @@ FIS_DEV void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::
 
 FIS_DEV int cur_step(const int* step) { return step ? __ldg(step) : 0; }
 
+// Launch trace (profiling builds only: `python -m paper_2305_17423_b200.build --trace` compiles with
+// FIS_TRACE into libfisedit_trace.so, loaded with FIS_LIB=libfisedit_trace.so). CTA (0,0,0) of every
+// kernel takes the next slot of the installed buffer (atomic counter at buf[0]) and records
+// %globaltimer phase stamps at buf[16 + 16 * slot + phase]; phase 15 = kernel kind. Production builds
+// compile every probe to nothing: each probe is a dependent global load on the issuing thread's path.
+static __device__ unsigned long long* g_ltr = nullptr;
+FIS_DEV unsigned long long ltr_now() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#ifdef FIS_TRACE
+FIS_DEV int ltr_begin(int kind) {
+    unsigned long long* b = g_ltr;
+    if (!b || (blockIdx.x | blockIdx.y | blockIdx.z) || threadIdx.x) return -1;
+    const unsigned long long t = ltr_now();
+    const int s = (int)atomicAdd(b, 1ull);
+    if (s >= 4096) return -1;
+    b[16 + 16 * s] = t;
+    b[16 + 16 * s + 15] = (unsigned long long)kind;
+    return s;
+}
+FIS_DEV void ltr(int slot, int phase) {
+    if (slot >= 0) g_ltr[16 + 16 * slot + phase] = ltr_now();
+}
+#else
+FIS_DEV int ltr_begin(int) { return -1; }
+FIS_DEV void ltr(int, int) {}
+#endif
+#ifdef FIS_TRACE
+#define FIS_LTR_SETTER(fn) \
+    extern "C" int fn(unsigned long long* p) { return cudaMemcpyToSymbol(fis::g_ltr, &p, sizeof(p)) == cudaSuccess ? 0 : 1; }
+#else
+#define FIS_LTR_SETTER(fn) \
+    extern "C" int fn(unsigned long long*) { return FIS_ERR_UNSUPPORTED; }
+#endif
+
 FIS_DEV char* ref_base(const fis_ref& r, int t) {
     return (char*)r.ptr + (long long)t * r.step_stride;
 }

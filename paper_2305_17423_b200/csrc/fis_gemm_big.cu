@@ -145,6 +145,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     gemm_big_kernel(const fis_gemm_args a, const __grid_constant__ CUtensorMap tmap_b,
                     const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_a2,
                     const __grid_constant__ GatherMaps gm, int bn, int amode, int dbg) {
+    const int ls = ltr_begin(4);
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     // align by pointer arithmetic on the shared array (keeps the shared address space: LDS/STS)
     unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -189,9 +190,10 @@ __global__ void __launch_bounds__(THREADS, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    const int t = cur_step(a.step);  // host-written before the step: safe to read before the wait
     pdl_trigger();
     pdl_wait();
-    const int t = cur_step(a.step);
+    ltr(ls, 2);
 
     if (warp < A_WARPS) {
         if (amode != A_CPASYNC && amode != A_TMA_GATHER) goto epilogue_role;  // TMA stages A: help the epilogue
@@ -821,3 +823,5 @@ extern "C" int fis_big_trace_read(unsigned long long* out768) {
 extern "C" int fis_big_debug_buf(int* host_mapped) {
     return cudaMemcpyToSymbol(fis::big::g_dbg_host, &host_mapped, sizeof(int*)) == cudaSuccess ? FIS_OK : FIS_ERR_LAUNCH;
 }
+
+FIS_LTR_SETTER(fis_ltr_set_big)

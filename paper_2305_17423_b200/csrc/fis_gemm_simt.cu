@@ -38,12 +38,14 @@ __device__ __forceinline__ float gather_a(const fis_gemm_args& a, int t, const c
 }
 
 __global__ void __launch_bounds__(STHREADS) gemm_simt_kernel(const fis_gemm_args a) {
+    const int ls = ltr_begin(3);
     __shared__ float As[SBK][SBM + 4];
     __shared__ float Bs[SBK][SBN + 4];
     __shared__ int rowp[SBM], rowy[SBM], rowx[SBM];
     __shared__ int s_last;
     pdl_trigger();
     pdl_wait();
+    ltr(ls, 2);
     const int t = cur_step(a.step);
     const int tid = threadIdx.x;
     const int n0 = blockIdx.x * SBN, m0 = blockIdx.y * SBM;
@@ -167,3 +169,5 @@ int fis_gemm_simt_launch(const fis_gemm_args* a, cudaStream_t stream) {
     return fis_launch(fis::gemm_simt_kernel, grid, dim3(fis::STHREADS), 0, stream, *a) == cudaSuccess ? FIS_OK
                                                                                                : FIS_ERR_LAUNCH;
 }
+
+FIS_LTR_SETTER(fis_ltr_set_simt)

@@ -26,16 +26,22 @@ const CUtensorMap* fis_weight_map(const void* base, long long n, long long k, lo
 namespace fis {
 namespace tc {
 
-constexpr int STAGES = 4, PRODUCERS = 256, THREADS = 288, MMA_WARP = 8;
+constexpr int PRODUCERS = 256, THREADS = 288, MMA_WARP = 8;
 
 template <int BN>
 struct Smem {
     static constexpr int A_BYTES = BM * BK * 2;
     static constexpr int B_BYTES = BN * BK * 2;
     static constexpr int STAGE = A_BYTES + B_BYTES;
+    static constexpr int STAGES = 4;
     static constexpr int EPI = BN * 32;  // per-column epilogue tables
     static constexpr int SEL = BM * 2 * 9 * 4;  // per-row, per-segment, per-tap select-on-read table
-    static constexpr int TOTAL = STAGES * STAGE + 1024 /*align*/ + 256 /*barriers*/ + EPI + SEL + 16;
+    // split-K receive buffer (dedicated: peers push into it while this CTA's main loop may still
+    // run): S - 1 row slices of ceil(BM / S) rows x (BN + 4) fp32, maximised over S = 2..16
+    static constexpr int rx_bytes(int S) { return (S - 1) * ((BM + S - 1) / S) * (BN + 4) * 4; }
+    static constexpr int rx_max(int S) { return S > 16 ? 0 : (rx_bytes(S) > rx_max(S + 1) ? rx_bytes(S) : rx_max(S + 1)); }
+    static constexpr int RX = rx_max(2);
+    static constexpr int TOTAL = STAGES * STAGE + 1024 /*align*/ + 256 /*barriers*/ + EPI + SEL + 16 + RX;
 };
 
 // Phase timestamps (%globaltimer, ns) of CTA (0,0,0) for profiling the fixed per-launch cost;
@@ -48,6 +54,7 @@ __device__ __forceinline__ unsigned long long gtime() {
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     return t;
 }
+#ifdef FIS_TRACE
 __device__ __forceinline__ void trace(int slot) {
     if (g_trace_on && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0) g_trace[slot] = gtime();
 }
@@ -57,6 +64,10 @@ __device__ __forceinline__ void trace_cta(int slot) {
         if (id < 512) g_trace_cta[id][slot] = gtime();
     }
 }
+#else  // production build: no probes (each is a global load of g_trace_on on thread 0's path)
+__device__ __forceinline__ void trace(int) {}
+__device__ __forceinline__ void trace_cta(int) {}
+#endif
 
 __device__ __forceinline__ void tc_tma2d(uint32_t dst, const void* tmap, int c0, int c1, uint64_t* bar) {
     asm volatile(
@@ -73,14 +84,16 @@ __global__ void __launch_bounds__(THREADS, 1)
     gemm_tc_kernel(const fis_gemm_args a, const __grid_constant__ CUtensorMap tmb, int tma_b) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char* smem = (unsigned char*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-    uint64_t* full = (uint64_t*)(smem + STAGES * Smem<BN>::STAGE);
-    uint64_t* empty = full + STAGES;
-    uint64_t* done = empty + STAGES;
-    uint32_t* tmem_slot = (uint32_t*)(done + 1);
+    uint64_t* full = (uint64_t*)(smem + Smem<BN>::STAGES * Smem<BN>::STAGE);
+    uint64_t* empty = full + Smem<BN>::STAGES;
+    uint64_t* done = empty + Smem<BN>::STAGES;
+    uint64_t* rx_bar = done + 1;  // split-K: peers' partial row slices landed (complete_tx)
+    uint32_t* tmem_slot = (uint32_t*)(rx_bar + 1);
     int* last_flag = (int*)(tmem_slot + 1);  // followed by the epilogue tables
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    if (tid == 0) { trace(0); trace_cta(0); }
+    __shared__ int s_ltr;
+    if (tid == 0) { trace(0); trace_cta(0); s_ltr = ltr_begin(1); }
     const int n0 = blockIdx.x * BN, m0 = blockIdx.y * BM;
     const int kblocks = (a.k + BK - 1) / BK;
     const int kper = (kblocks + a.splits - 1) / a.splits;
@@ -88,11 +101,12 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int nk = max(0, kb1 - kb0);
 
     if (tid == 0) {
-        for (int s = 0; s < STAGES; s++) {
+        for (int s = 0; s < Smem<BN>::STAGES; s++) {
             mbar_init(full + s, PRODUCERS + (tma_b ? 1 : 0));
             mbar_init(empty + s, 1);
         }
         mbar_init(done, 1);
+        mbar_init(rx_bar, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == MMA_WARP) {
@@ -105,10 +119,13 @@ __global__ void __launch_bounds__(THREADS, 1)
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
     if (tid == 0) trace(1);
+    // split-K: announce this CTA's barriers initialised; the matching wait comes right before the
+    // first push into a peer (long satisfied by then)
+    if (a.splits > 1) asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
     // gather metadata of the producer's row: pixel + (CONV) the select-on-read decision of every
     // tap of both concat segments, in a shared table; read before the programmatic-launch wait
     // when the row/index lists are static (they are inside a captured edit step)
-    int* seltab = (int*)(((uintptr_t)(smem + STAGES * Smem<BN>::STAGE + 256 + Smem<BN>::EPI) + 15) & ~(uintptr_t)15);
+    int* seltab = (int*)(((uintptr_t)(smem + Smem<BN>::STAGES * Smem<BN>::STAGE + 256 + Smem<BN>::EPI) + 15) & ~(uintptr_t)15);
     const int ar = tid >> 1, half_id = tid & 1;
     int row_p = 0;
     bool row_valid = false;
@@ -120,11 +137,20 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (a.a_mode == FIS_A_CONV3X3 && half_id < a.nsrc) build_sel(a, row_p, half_id, seltab + (ar * 2 + half_id) * 9);
     };
     if (a.static_meta) build_meta();
+    // the step counter is written by the host before the step (outside the captured graph), so it
+    // is read before the wait: its load latency overlaps the previous kernel too
+    const int t = cur_step(a.step);
+    const int ls = s_ltr;
+    if (tid == 0) ltr(ls, 1);
+    if (tma_b && warp == MMA_WARP + 0 && lane == 0 && !a.b.step_stride) {
+        // weights: pull this CTA's B tiles into L2 while the previous kernel still runs
+        for (int i = 0; i < nk; i++) tma_prefetch2d(&tmb, (kb0 + i) * BK, n0);
+    }
     pdl_trigger();
     pdl_wait();  // everything above (barrier init, TMEM alloc, static metadata) overlaps the previous kernel
+    if (tid == 0) ltr(ls, 2);
     if (!a.static_meta) build_meta();
     if (tid == 0) trace(2);
-    const int t = cur_step(a.step);
 
     if (warp < MMA_WARP) {
         // ------------------------------------------------------------ producers
@@ -144,9 +170,9 @@ __global__ void __launch_bounds__(THREADS, 1)
         const int bn = n0 + ar;
         const char* brow = bbase + (long long)bn * a.b.ld * 2;
         for (int i = 0; i < nk; i++) {
-            const int s = i % STAGES;
+            const int s = i % Smem<BN>::STAGES;
             const int k0 = (kb0 + i) * BK;
-            if (i >= STAGES) mbar_wait(empty + s, ((i / STAGES) & 1) ^ 1);
+            if (i >= Smem<BN>::STAGES) mbar_wait(empty + s, ((i / Smem<BN>::STAGES) & 1) ^ 1);
             const uint32_t sa = sbase + s * Smem<BN>::STAGE;
             const uint32_t sb = sa + Smem<BN>::A_BYTES;
             const char* src = nullptr;
@@ -187,7 +213,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                 }
             }
             // the barrier counts this thread's arrival when all its prior cp.async have landed:
-            // no thread-side wait, STAGES stages of loads stay in flight
+            // no thread-side wait, Smem<BN>::STAGES stages of loads stay in flight
             cp_async_arrive_noinc(full + s);
             if (tid == 0 && i == 0) trace(3);
         }
@@ -197,10 +223,10 @@ __global__ void __launch_bounds__(THREADS, 1)
                                ((uint32_t)(BM >> 4) << 24);
         const uint32_t sbase = smem_u32(smem);
         for (int i = 0; i < nk; i++) {
-            const int s = i % STAGES;
-            mbar_wait(full + s, (i / STAGES) & 1);
-            if (lane == 0 && i == 0) trace(4);
-            if (lane == 0 && i == nk - 1) trace(5);
+            const int s = i % Smem<BN>::STAGES;
+            mbar_wait(full + s, (i / Smem<BN>::STAGES) & 1);
+            if (lane == 0 && i == 0) { trace(4); ltr(ls, 3); }
+            if (lane == 0 && i == nk - 1) { trace(5); ltr(ls, 4); }
             tc_fence_after();
             if (lane == 0) {
                 const uint32_t sa = sbase + s * Smem<BN>::STAGE;
@@ -271,7 +297,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         asm volatile("bar.sync 1, 256;" ::: "memory");
         if (tid == 0) trace(10);
         mbar_wait(done, 0);
-        if (tid == 0) { trace(6); trace_cta(1); }
+        if (tid == 0) { trace(6); trace_cta(1); ltr(ls, 5); }
         tc_fence_after();
         const int quarter = warp & 3, half = warp >> 2;
         const int lr = quarter * 32 + lane, r = m0 + lr;
@@ -290,90 +316,138 @@ __global__ void __launch_bounds__(THREADS, 1)
                 : "r"(taddr + 16 * q));
         }
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-        if (S > 1) {
+        {
+            // stage the fp32 tile (the split-K partial, or the whole tile when S == 1) in the idle
+            // pipeline buffers; the stores below run columns-fastest across threads (coalesced), not
+            // one row per thread (a warp's 32 row stores are 32 separate lines: ~4.5 us per tile)
             float* p = part + lr * PLD + half * HC;
 #pragma unroll
             for (int q = 0; q < HC / 4; q++)
                 *(float4*)(p + 4 * q) = nk > 0 ? make_float4(__uint_as_float(u[4 * q]), __uint_as_float(u[4 * q + 1]),
                                                              __uint_as_float(u[4 * q + 2]), __uint_as_float(u[4 * q + 3]))
                                                : make_float4(0.f, 0.f, 0.f, 0.f);
-        } else if (r < a.m) {
-#pragma unroll
-            for (int q = 0; q < HC / 16; q++) {
-                const int cb = half * HC + 16 * q;
-                if (n0 + cb >= a.n) break;
-                float v[16];
-#pragma unroll
-                for (int j = 0; j < 16; j++) v[j] = nk > 0 ? __uint_as_float(u[16 * q + j]) : 0.f;
-                row_epilogue_any(a, e, tb, r, cb, n0, v);
-            }
         }
     }
-    if (tid == 0) trace(8);
+    if (tid == 0) { trace(8); ltr(ls, 6); }
     tc_fence_before();
     __syncthreads();
-    if (tid == 0) trace(9);
+    if (tid == 0) { trace(9); ltr(ls, 8); }
     if (warp == MMA_WARP)
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(BN < 32 ? 32 : BN));
-    if (S > 1) {
-        // cluster-wide deterministic split-K reduction over DSMEM: CTA z reduces rows
-        // [z*rows_per, (z+1)*rows_per) of the tile, summing the S partials in split order.
-        asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-        if (tid == 0) trace_cta(2);
-        uint32_t rank;
-        asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
-        const int rows_per = (BM + S - 1) / S;
-        const int rbeg = (int)rank * rows_per, rend = min(BM, rbeg + rows_per);
-        const uint32_t part_s = smem_u32(part);
-        // phase 1: float4 items of the slice; the S remote partials are loaded as one batch and
-        // summed in split order into a local fp32 slice buffer (after this CTA's own partial)
-        float* red = part + BM * PLD;
-        const int q4 = BN / 4;
-        for (int item = tid; item < (rend - rbeg) * q4; item += THREADS) {
-            const int lr = rbeg + item / q4, c4 = (item % q4) * 4;
-            const uint32_t off = (uint32_t)((lr * PLD + c4) * 4);
-            float4 x[16];
-#pragma unroll
-            for (int z = 0; z < 16; z++) {
-                if (z < S) {
-                    uint32_t ra;
-                    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(part_s + off), "r"(z));
-                    asm volatile("ld.shared::cluster.v4.f32 {%0,%1,%2,%3}, [%4];"
-                                 : "=f"(x[z].x), "=f"(x[z].y), "=f"(x[z].z), "=f"(x[z].w) : "r"(ra));
-                }
-            }
-            float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-            for (int z = 0; z < 16; z++) {
-                if (z < S) { acc.x += x[z].x; acc.y += x[z].y; acc.z += x[z].z; acc.w += x[z].w; }
-            }
-            *(float4*)(red + (lr - rbeg) * PLD + c4) = acc;
-        }
-        __syncthreads();
-        // phase 2: fused epilogue of the reduced slice rows, 16-column chunks
+    if (tid == 0) ltr(ls, 9);
+    // fused epilogue of tile rows [rbeg, rend) from an fp32 staging buffer (row lr at src + (lr - rbeg) * PLD),
+    // 16-column chunks; transposed outputs (V^T of a fused QKV, or d_trans) go rows-fastest across threads so a
+    // warp stores 32 consecutive rows of each column, row-major outputs columns-fastest
+    const bool tile_trans = a.d_trans || (a.d2_trans && a.n_split > 0 && n0 >= a.n_split);
+    // plain bf16 row-major output with bias only (projections, most convs): a compact inline path
+    const bool plain = a.epi == FIS_EPI_NONE && a.alpha == 1.0f && !e.pre && !e.res && !e.bias2 && !a.d_rows &&
+                       !tile_trans && a.n_split == 0 && a.d.dtype == FIS_BF16 && (a.d.ld % 8) == 0 &&
+                       (((uintptr_t)e.d) & 15) == 0 && (a.n % 16) == 0;
+    auto epi_rows = [&](const float* src, int rbeg, int rend) {
         const int chunks = BN / 16;
-        // transposed outputs (V^T of a fused QKV, or d_trans): rows fastest across threads so a warp
-        // stores 32 consecutive rows of each column (coalesced); row-major outputs: columns fastest
-        const bool tile_trans = a.d_trans || (a.d2_trans && a.n_split > 0 && n0 >= a.n_split);
         const int nrows = rend - rbeg;
+        if (plain) {
+#pragma unroll 1
+            for (int item = tid; item < nrows * chunks; item += THREADS) {
+                const int lr = rbeg + item / chunks, cb = (item % chunks) * 16;
+                const int r = m0 + lr;
+                if (r >= a.m || n0 + cb >= a.n) continue;
+                const float* q = src + (lr - rbeg) * PLD + cb;
+                uint4 o[2];
+                __nv_bfloat162* h = (__nv_bfloat162*)o;
+#pragma unroll
+                for (int k4 = 0; k4 < 4; k4++) {
+                    const float4 f = *(const float4*)(q + 4 * k4);
+                    h[2 * k4] = __floats2bfloat162_rn(__fadd_rn(f.x, tb.bias[cb + 4 * k4]),
+                                                      __fadd_rn(f.y, tb.bias[cb + 4 * k4 + 1]));
+                    h[2 * k4 + 1] = __floats2bfloat162_rn(__fadd_rn(f.z, tb.bias[cb + 4 * k4 + 2]),
+                                                          __fadd_rn(f.w, tb.bias[cb + 4 * k4 + 3]));
+                }
+                uint4* dst = (uint4*)((__nv_bfloat16*)e.d + (long long)r * a.d.ld + n0 + cb);
+                dst[0] = o[0];
+                dst[1] = o[1];
+            }
+            return;
+        }
         for (int item = tid; item < nrows * chunks; item += THREADS) {
             const int lr = rbeg + (tile_trans ? item % nrows : item / chunks);
             const int cb = (tile_trans ? item / nrows : item % chunks) * 16;
             const int r = m0 + lr;
             if (r >= a.m || n0 + cb >= a.n) continue;
             float v[16];
-            const float* p = red + (lr - rbeg) * PLD + cb;
+            const float* q = src + (lr - rbeg) * PLD + cb;
 #pragma unroll
-            for (int q = 0; q < 4; q++) {
-                const float4 f = *(const float4*)(p + 4 * q);
-                v[4 * q] = f.x; v[4 * q + 1] = f.y; v[4 * q + 2] = f.z; v[4 * q + 3] = f.w;
+            for (int k4 = 0; k4 < 4; k4++) {
+                const float4 f = *(const float4*)(q + 4 * k4);
+                v[4 * k4] = f.x; v[4 * k4 + 1] = f.y; v[4 * k4 + 2] = f.z; v[4 * k4 + 3] = f.w;
             }
             row_epilogue_any(a, e, tb, r, cb, n0, v);
         }
-        // keep every CTA's shared memory alive until all peers finished reading it
-        asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    };
+    if (S == 1) {
+        epi_rows(part, 0, min(BM, a.m - m0));
+    } else {
+        // split-K over the S CTAs of a cluster, deterministic: CTA z owns rows [z*rows_per, ...) of
+        // the tile; every CTA pushes each peer's row slice of its fp32 partial into that peer's
+        // dedicated receive buffer with one DSMEM bulk copy (complete_tx on the peer's rx_bar), so
+        // no cluster-wide barrier sits between the partials and the reduction; the owner sums the S
+        // partials in split order (bitwise the same as a sequential reduction) and runs the epilogue
+        uint32_t rank;
+        asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+        const int rows_per = (BM + S - 1) / S;
+        const int rbeg = min(BM, (int)rank * rows_per), rend = min(BM, rbeg + rows_per);
+        float* rx = (float*)(((uintptr_t)(seltab + BM * 2 * 9) + 15) & ~(uintptr_t)15);
+        const uint32_t slice_floats = (uint32_t)rows_per * PLD;
+        asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");  // peers' rx_bar initialised
+        if (tid == 0) {
+            // incoming bytes: S - 1 slices of this CTA's rows
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(rx_bar)),
+                         "r"((uint32_t)((S - 1) * (rend - rbeg) * PLD * 4))
+                         : "memory");
+            fence_async_smem();  // generic-proxy partial writes -> bulk-copy reads
+            const uint32_t part_s = smem_u32(part), rx_s = smem_u32(rx), bar_s = smem_u32(rx_bar);
+            for (int p = 0; p < S; p++) {
+                if (p == (int)rank) continue;
+                const int pb = min(BM, p * rows_per), pe = min(BM, pb + rows_per);
+                if (pe <= pb) continue;
+                const int slot = (int)rank < p ? (int)rank : (int)rank - 1;  // my slot in peer p's buffer
+                uint32_t dst, bar;
+                asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(dst) : "r"(rx_s + slot * slice_floats * 4), "r"(p));
+                asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(bar) : "r"(bar_s), "r"(p));
+                asm volatile(
+                    "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+                    "r"(part_s + (uint32_t)(pb * PLD * 4)), "r"((uint32_t)((pe - pb) * PLD * 4)), "r"(bar)
+                    : "memory");
+            }
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
+        if (rend > rbeg) {
+            mbar_wait(rx_bar, 0);
+            const int chunks = BN / 16, nrows = rend - rbeg;
+            for (int item = tid; item < nrows * chunks; item += THREADS) {
+                const int lr = rbeg + (tile_trans ? item % nrows : item / chunks);
+                const int cb = (tile_trans ? item / nrows : item % chunks) * 16;
+                const int r = m0 + lr;
+                if (r >= a.m || n0 + cb >= a.n) continue;
+                float v[16];
+#pragma unroll
+                for (int j = 0; j < 16; j++) v[j] = 0.f;
+                for (int z = 0; z < S; z++) {  // split order
+                    const float* q = z == (int)rank ? part + lr * PLD + cb
+                                                    : rx + (z < (int)rank ? z : z - 1) * slice_floats + (lr - rbeg) * PLD + cb;
+#pragma unroll
+                    for (int k4 = 0; k4 < 4; k4++) {
+                        const float4 f = *(const float4*)(q + 4 * k4);
+                        v[4 * k4] += f.x; v[4 * k4 + 1] += f.y; v[4 * k4 + 2] += f.z; v[4 * k4 + 3] += f.w;
+                    }
+                }
+                row_epilogue_any(a, e, tb, r, cb, n0, v);
+            }
+        }
+        // this CTA's outgoing copies must have read its partial before the shared memory goes away
+        if (tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
     }
-    if (tid == 0) { trace(7); trace_cta(3); }
+    if (tid == 0) { trace(7); trace_cta(3); ltr(ls, 7); }
 }
 
 template <int BN>
@@ -492,6 +566,8 @@ int fis_gemm_tc_launch(const fis_gemm_args* a, cudaStream_t stream) {
     if (a->n <= 128 || (a->n % 128) != 0) return fis::tc::launch<128>(a, stream);
     return fis::tc::launch<128>(a, stream);
 }
+
+FIS_LTR_SETTER(fis_ltr_set_tc)
 
 extern "C" int fis_trace(int on) {
     return cudaMemcpyToSymbol(fis::tc::g_trace_on, &on, sizeof(int)) == cudaSuccess ? FIS_OK : FIS_ERR_LAUNCH;

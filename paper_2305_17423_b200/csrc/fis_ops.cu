@@ -8,9 +8,11 @@ namespace fis {
 
 // ---- group norm statistics (tensors.py:129-146): two-pass f64, rounded to f32
 __global__ void __launch_bounds__(256) gn_stats_kernel(const fis_gn_stats_args a) {
+    const int ls = ltr_begin(11);
+    const int t = cur_step(a.step);  // host-written before the step: read before the wait
     pdl_trigger();
     pdl_wait();
-    const int t = cur_step(a.step);
+    ltr(ls, 2);
     const int g = blockIdx.x, img = blockIdx.y;  // one CTA per (group, stacked image)
     const int cpg = a.c / a.groups;
     const long long cnt = (long long)a.hw * cpg;
@@ -101,9 +103,11 @@ __global__ void __launch_bounds__(256) gn_stats_kernel(const fis_gn_stats_args a
 
 // ---- normalise with given stats (+SiLU) (tensors.py:149-180, unet.py:291-293)
 __global__ void gn_apply_kernel(const fis_gn_apply_args a) {
+    const int ls = ltr_begin(7);
+    const int t = cur_step(a.step);  // host-written before the step: read before the wait
     pdl_trigger();
     pdl_wait();
-    const int t = cur_step(a.step);
+    ltr(ls, 2);
     const char* x = ref_base(a.x, t);
     const float* mean = (const float*)ref_base(a.mean, t);
     const float* var = (const float*)ref_base(a.var, t);
@@ -184,9 +188,11 @@ __global__ void gn_apply_kernel(const fis_gn_apply_args a) {
 
 // ---- scaled row softmax; one warp per row (tensors.py:183-192, unet.py:555-566)
 __global__ void softmax_kernel(const fis_softmax_args a) {
+    const int ls = ltr_begin(8);
+    const int t = cur_step(a.step);  // host-written before the step: read before the wait
     pdl_trigger();
     pdl_wait();
-    const int t = cur_step(a.step);
+    ltr(ls, 2);
     const int warps = blockDim.x / 32;
     const int row = blockIdx.x * warps + threadIdx.x / 32;
     const int lane = threadIdx.x & 31;
@@ -272,9 +278,11 @@ __global__ void softmax_kernel(const fis_softmax_args a) {
 
 // ---- 2x2 average pool with select-on-read (unet.py:296-298; numpy order (a+b)+(c+d))
 __global__ void pool2_kernel(const fis_pool_args a) {
+    const int ls = ltr_begin(6);
+    const int t = cur_step(a.step);  // host-written before the step: read before the wait
     pdl_trigger();
     pdl_wait();
-    const int t = cur_step(a.step);
+    ltr(ls, 2);
     const char* fr = a.src.fresh.ptr ? ref_base(a.src.fresh, t) : nullptr;
     const char* ca = a.src.cache.ptr ? ref_base(a.src.cache, t) : nullptr;
     char* out = ref_base(a.out, t);
@@ -325,9 +333,11 @@ __global__ void pool2_kernel(const fis_pool_args a) {
 
 // ---- full-map materialisation: out[q] = select(q)
 __global__ void materialize_kernel(const fis_materialize_args a) {
+    const int ls = ltr_begin(9);
+    const int t = cur_step(a.step);  // host-written before the step: read before the wait
     pdl_trigger();
     pdl_wait();
-    const int t = cur_step(a.step);
+    ltr(ls, 2);
     const char* fr = a.src.fresh.ptr ? ref_base(a.src.fresh, t) : nullptr;
     const char* ca = a.src.cache.ptr ? ref_base(a.src.cache, t) : nullptr;
     char* out = ref_base(a.out, t);
@@ -340,9 +350,11 @@ __global__ void materialize_kernel(const fis_materialize_args a) {
 
 // ---- nearest 2x upsample of a dense map (unet.py:301-302), 8 channels per thread
 __global__ void up2_kernel(const fis_pool_args a) {
+    const int ls = ltr_begin(10);
+    const int t = cur_step(a.step);  // host-written before the step: read before the wait
     pdl_trigger();
     pdl_wait();
-    const int t = cur_step(a.step);
+    ltr(ls, 2);
     const char* fr = ref_base(a.src.fresh, t);
     char* out = ref_base(a.out, t);
     const int ow = 2 * a.src.w, ohw = 4 * a.src.h * a.src.w, cv = a.c / 8;
@@ -361,10 +373,12 @@ __global__ void up2_kernel(const fis_pool_args a) {
 // (group, stacked image): the group's hw x cpg block is read three times from L2 instead of
 // a statistics launch followed by a separate apply launch (same arithmetic as the pair)
 __global__ void __launch_bounds__(256) gn_fused_kernel(const fis_gn_apply_args a) {
+    const int ls = ltr_begin(5);
+    const int t = cur_step(a.step);  // host-written before the step: read before the wait
     pdl_trigger();
     pdl_wait();
+    ltr(ls, 2);
     const int hw = a.img_rows;  // pixels per image (set by fis_gn)
-    const int t = cur_step(a.step);
     const int g = blockIdx.x, img = blockIdx.y, tid = threadIdx.x;
     const int cpg = a.c / a.groups, vpg = cpg / 8, items = hw * vpg;
     const long long cnt = (long long)hw * cpg;
@@ -535,9 +549,11 @@ namespace fis {
 
 template <int CPL>  // channels per lane = C / 32 rounded up (<= 40 for C = 1280)
 __global__ void __launch_bounds__(256) xattn_kernel(const fis_xattn_args a) {
+    const int ls = ltr_begin(12);
+    const int t = cur_step(a.step);  // host-written before the step: read before the wait
     pdl_trigger();
     pdl_wait();
-    const int t = cur_step(a.step);
+    ltr(ls, 2);
     const int warps = blockDim.x >> 5;
     const int row = blockIdx.x * warps + (threadIdx.x >> 5);
     const int lane = threadIdx.x & 31;
@@ -629,3 +645,5 @@ extern "C" int fis_xattn(const fis_xattn_args* a, void* stream) {
     else e = fis_launch(fis::xattn_kernel<40>, grid, block, 0, (cudaStream_t)stream, *a);
     return e == cudaSuccess ? FIS_OK : FIS_ERR_LAUNCH;
 }
+
+FIS_LTR_SETTER(fis_ltr_set_ops)

@@ -41,6 +41,14 @@ __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.a
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
+// L2 prefetch of one TMA box (no shared-memory destination, no completion): issued for operands
+// that no kernel of the step writes (weights, per-edit text K/V) BEFORE griddepcontrol.wait, so
+// their HBM latency overlaps the previous kernel and the main loop streams them from L2
+__device__ __forceinline__ void tma_prefetch2d(const void* tmap, int c0, int c1) {
+    asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(tmap), "r"(c0), "r"(c1)
+                 : "memory");
+}
+
 // K-major, 128B-swizzled UMMA shared-memory descriptor (LBO=16B, SBO=1024B, version 1)
 __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
     return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
