@@ -25,7 +25,7 @@ Sections of the JSON line beyond the base contract:
   roofline       gated-conv gather-GEMMs of the timed step (algorithmic FLOPs / CUPTI time)
   kernels        per-op-class share of the step (CUPTI, graph replay)
   sweep          C3: sparse step vs mask ratio 1..100% + random-dilated 10%, vs the dense step
-  fp32_parity    the same step in the fp32 parity precision
+  fp32_parity    the same step with fp32 operands on the tensor cores (3xTF32; *_simt: SIMT FFMA)
   c4             SD-2 shape (96x96, 1024-wide text): sparse step + multi-round edit() e2e
   batched        C5: 64 requests over the N GPUs, each GPU's share stepped as one stacked batch
   cpu_baseline   the reference package's own CPU path (baseline/_ref) on a bounded sample
@@ -463,7 +463,8 @@ def run_ours(args):
     del runner, ep
     # --- the same step in the fp32 parity precision (SIMT fp32; the numerics of tensors.py:76-94)
     if args.precision == "bf16" and not args.no_fp32:
-        line["fp32_parity"] = fp32_parity_step(U, P, cfg, args, mask)
+        line["fp32_parity"] = fp32_parity_step(U, P, cfg, args, mask, "tf32x3")
+        line["fp32_parity_simt"] = fp32_parity_step(U, P, cfg, args, mask, "fp32")
     # --- C4: SD-2 shape, multi-round edits against one HBM generation
     if not args.no_c4:
         line["c4"] = c4_section(U, P, args)
@@ -543,12 +544,13 @@ def mask_sweep(eng, U, P, cfg, arena, kv, lat0, args, dense_ms):
     return out
 
 
-def fp32_parity_step(U, P, cfg, args, mask):
-    """The C2 sparse step in fp32 parity precision (fp32 operands, fp32 accumulate)."""
+def fp32_parity_step(U, P, cfg, args, mask, precision="fp32"):
+    """The C2 sparse step with fp32 operands: "fp32" (SIMT FFMA, the reference numerics) or
+    "tf32x3" (tcgen05 kind::tf32, 3xTF32 split, fp32 accumulate)."""
     import torch
-    eng = U.get_engine(cfg, "fp32")
+    eng = U.get_engine(cfg, precision)
     store = P.CacheStore()
-    P.generate_dense(P.PromptTokens(OLD_IDS), cfg, store, record="engine", precision="fp32")
+    P.generate_dense(P.PromptTokens(OLD_IDS), cfg, store, record="engine", precision=precision)
     kv = eng.text_kv(P.embed_tokens(P.PromptTokens(NEW_IDS), cfg))
     lat0 = U._to_nhwc(P.initial_latent(cfg), eng.dev)
     ep = U.EditPlan(eng, store.arena, mask, kv, lat0)
@@ -556,9 +558,12 @@ def fp32_parity_step(U, P, cfg, args, mask):
     store.close()
     del ep, store
     torch.cuda.empty_cache()
-    return {"ms_per_step": ms, "edit_steps_per_s": 1e3 / ms, "dtype": "f32",
-            "note": "same C2 10% step, set_precision('fp32'): fp32 operands / accumulation (SIMT FFMA GEMMs), "
-                    "the parity mode pinned to the oracle at <= 1e-4 per step (tests/test_gpu_c2_parity.py)"}
+    note = {"fp32": "set_precision('fp32'): fp32 operands / accumulation on SIMT FFMA GEMMs",
+            "tf32x3": "set_precision('tf32x3'): fp32 operands on the tcgen05 tensor cores as 3xTF32 (big*big + "
+                      "big*small + small*big, kind::tf32, fp32 accumulate)"}[precision]
+    return {"ms_per_step": ms, "edit_steps_per_s": 1e3 / ms, "dtype": "f32", "precision": precision,
+            "note": f"same C2 10% step, {note}; pinned to the oracle at <= 1e-4 latent max-abs per sampled step "
+                    "(tests/test_gpu_c2_parity.py)"}
 
 
 def c4_section(U, P, args):
@@ -685,7 +690,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--mask", type=float, default=0.10)
-    ap.add_argument("--precision", default="bf16", choices=["fp32", "bf16"])
+    ap.add_argument("--precision", default="bf16", choices=["fp32", "tf32x3", "bf16"])
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-fp32", action="store_true")

@@ -101,14 +101,15 @@ typedef struct {
     long long ws_floats;    /* capacity of ws (bounds the automatic split choice) */
     int* counters;          /* per-tile arrival counters (zeroed, self-resetting) */
     const int* step;
-    int impl;               /* 0 auto, 1 SIMT fp32-accumulate, 2 tcgen05 bf16 */
+    int impl;               /* 0 auto, 1 SIMT fp32-accumulate, 2 tcgen05 bf16, 3 tcgen05 3xTF32 on fp32
+                               operands (SIMT when the shape is not supported) */
     int static_meta;        /* 1: rows/index lists are not written by the preceding kernel, so the
                                gather metadata may be read before the programmatic-launch wait */
 } fis_gemm_args;
 
 int fis_gemm(const fis_gemm_args* args, void* stream);
 /* which kernel fis_gemm picks for these arguments: 0 SIMT, 1 per-op tcgen05 (split-K clusters),
- * 2 persistent large-M tcgen05 (TMA / gather4 staging); host-only, no launch */
+ * 2 persistent large-M tcgen05 (TMA / gather4 staging), 3 per-op tcgen05 3xTF32; host-only */
 int fis_gemm_kernel_kind(const fis_gemm_args* a);
 /* number of persistent-kernel launches so far (diagnostics / tests) */
 long long fis_gemm_big_launch_count(void);

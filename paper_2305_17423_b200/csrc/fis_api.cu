@@ -5,6 +5,9 @@ int fis_gemm_simt_launch(const fis_gemm_args* a, cudaStream_t stream);
 int fis_gemm_tc_launch(const fis_gemm_args* a, cudaStream_t stream);
 int fis_gemm_tc_supported(const fis_gemm_args* a);
 int fis_gemm_tc_choose_splits(int m, int n, int k);
+int fis_gemm_tf32_supported(const fis_gemm_args* a);
+int fis_gemm_tf32_choose_splits(int m, int n, int k);
+int fis_gemm_tf32_launch(const fis_gemm_args* a, cudaStream_t stream);
 int fis_gemm_big_eligible(const fis_gemm_args* a);
 int fis_gemm_big_launch(const fis_gemm_args* a, cudaStream_t stream);
 
@@ -73,8 +76,9 @@ static int fis_choose_splits(const fis_gemm_args* a, bool tc) {
 }
 
 // Which kernel fis_gemm would run for these arguments: 0 SIMT, 1 per-op tcgen05, 2 persistent
-// large-M tcgen05 (csrc/fis_gemm_big.cu). Host-only query (no launch).
+// large-M tcgen05 (csrc/fis_gemm_big.cu), 3 per-op tcgen05 3xTF32 (fp32 operands). Host-only query (no launch).
 int fis_gemm_kernel_kind(const fis_gemm_args* a) {
+    if (a->impl == 3) return fis_gemm_tf32_supported(a) ? 3 : 0;
     const bool tc = a->impl == 2 || (a->impl == 0 && fis_gemm_tc_supported(a));
     if (!tc) return 0;
     return a->impl == 0 && fis_gemm_big_eligible(a) ? 2 : 1;
@@ -101,6 +105,10 @@ int fis_gemm(const fis_gemm_args* a, void* stream) {
         if (rc != FIS_ERR_UNSUPPORTED) return rc;
     }
     fis_gemm_args g = *a;
+    if (a->impl == 3 && fis_gemm_tf32_supported(a)) {  // fp32 operands on the tensor cores (3xTF32)
+        if (g.splits <= 0) g.splits = fis_gemm_tf32_choose_splits(a->m, a->n, a->k);
+        return fis_gemm_tf32_launch(&g, (cudaStream_t)stream);
+    }
     if (g.splits <= 0) g.splits = fis_choose_splits(&g, tc);
     if (!tc && g.splits > 1 && (!g.ws || !g.counters)) return FIS_ERR_SHAPE;
     return tc ? fis_gemm_tc_launch(&g, (cudaStream_t)stream) : fis_gemm_simt_launch(&g, (cudaStream_t)stream);

@@ -28,12 +28,17 @@ namespace tc {
 
 constexpr int PRODUCERS = 256, THREADS = 288, MMA_WARP = 8;
 
-template <int BN>
+// X3 (fp32 on the tensor cores, 3xTF32): a K block is 32 fp32 (one 128-byte SW128 row, like 64
+// bf16); every operand tile exists twice in the stage, as its tf32-rounded "big" part and the fp32
+// remainder "small" (the producers split their own rows in place after cp.async lands), and each
+// K block issues big*big + big*small + small*big tf32 MMAs into the fp32 accumulator.
+template <int BN, bool X3 = false>
 struct Smem {
-    static constexpr int A_BYTES = BM * BK * 2;
-    static constexpr int B_BYTES = BN * BK * 2;
+    static constexpr int A_BYTES = BM * 128 * (X3 ? 2 : 1);  // [big][small] when X3
+    static constexpr int B_BYTES = BN * 128 * (X3 ? 2 : 1);
+    static constexpr int A_PART = BM * 128, B_PART = BN * 128;
     static constexpr int STAGE = A_BYTES + B_BYTES;
-    static constexpr int STAGES = 4;
+    static constexpr int STAGES = X3 ? 3 : 4;
     static constexpr int EPI = BN * 32;  // per-column epilogue tables
     static constexpr int SEL = BM * 2 * 9 * 4;  // per-row, per-segment, per-tap select-on-read table
     // split-K receive buffer (dedicated: peers push into it while this CTA's main loop may still
@@ -41,7 +46,8 @@ struct Smem {
     static constexpr int rx_bytes(int S) { return (S - 1) * ((BM + S - 1) / S) * (BN + 4) * 4; }
     static constexpr int rx_max(int S) { return S > 16 ? 0 : (rx_bytes(S) > rx_max(S + 1) ? rx_bytes(S) : rx_max(S + 1)); }
     static constexpr int RX = rx_max(2);
-    static constexpr int TOTAL = STAGES * STAGE + 1024 /*align*/ + 256 /*barriers*/ + EPI + SEL + 16 + RX;
+    static constexpr int BASE = STAGES * STAGE + 1024 /*align*/ + 256 /*barriers*/ + EPI + SEL + 16;
+    static constexpr int TOTAL = BASE + RX;  // with the split-K receive buffer
 };
 
 // Phase timestamps (%globaltimer, ns) of CTA (0,0,0) for profiling the fixed per-launch cost;
@@ -79,14 +85,39 @@ __device__ __forceinline__ void tc_tma2d(uint32_t dst, const void* tmap, int c0,
 
 // tma_b: the B tile {64 x BN} of each stage is one TMA load (thread 0, expect_tx on the stage's
 // full barrier) instead of BN rows of cp.async (weights stream faster; fewer producer instructions)
-template <int BN>
+__device__ __forceinline__ float tf32_big(float x) {
+    uint32_t r;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+    return __uint_as_float(r);
+}
+// split this thread's 16-byte chunk at byte offset off of a raw fp32 tile (in the "small" half):
+// big -> off - part_bytes, small stays at off (x - big is exact in fp32)
+__device__ __forceinline__ void x3_split(unsigned char* small_tile, int part_bytes, uint32_t off) {
+    float4 x = *(float4*)(small_tile + off);
+    float4 b = make_float4(tf32_big(x.x), tf32_big(x.y), tf32_big(x.z), tf32_big(x.w));
+    *(float4*)(small_tile - part_bytes + off) = b;
+    // the remainder rounded to tf32 too (the tensor core would truncate it)
+    *(float4*)(small_tile + off) =
+        make_float4(tf32_big(x.x - b.x), tf32_big(x.y - b.y), tf32_big(x.z - b.z), tf32_big(x.w - b.w));
+}
+
+template <int BN, bool X3>
 __global__ void __launch_bounds__(THREADS, 1)
     gemm_tc_kernel(const fis_gemm_args a, const __grid_constant__ CUtensorMap tmb, int tma_b) {
+    using SM = Smem<BN, X3>;
+    constexpr int ES = X3 ? 4 : 2;             // operand element bytes
+    constexpr int BKE = 128 / ES;              // K elements per K block (one 128-byte row)
+    constexpr int EPC = 16 / ES;               // K elements per 16-byte chunk
+    // X3: the tensor core's fp32 accumulate truncates (~2^-24 per MMA, linear in the K steps), so
+    // the big*big products of K block i go to accumulator i % NBIG and both small-product terms to
+    // their own accumulator; the epilogue sums them in fp32 (round to nearest), fixed order
+    constexpr int NBIG = X3 ? 512 / BN - 1 : 1;
+    constexpr int TCOLS = X3 ? 512 : (BN < 32 ? 32 : BN);
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char* smem = (unsigned char*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-    uint64_t* full = (uint64_t*)(smem + Smem<BN>::STAGES * Smem<BN>::STAGE);
-    uint64_t* empty = full + Smem<BN>::STAGES;
-    uint64_t* done = empty + Smem<BN>::STAGES;
+    uint64_t* full = (uint64_t*)(smem + SM::STAGES * SM::STAGE);
+    uint64_t* empty = full + SM::STAGES;
+    uint64_t* done = empty + SM::STAGES;
     uint64_t* rx_bar = done + 1;  // split-K: peers' partial row slices landed (complete_tx)
     uint32_t* tmem_slot = (uint32_t*)(rx_bar + 1);
     int* last_flag = (int*)(tmem_slot + 1);  // followed by the epilogue tables
@@ -95,13 +126,13 @@ __global__ void __launch_bounds__(THREADS, 1)
     __shared__ int s_ltr;
     if (tid == 0) { trace(0); trace_cta(0); s_ltr = ltr_begin(1); }
     const int n0 = blockIdx.x * BN, m0 = blockIdx.y * BM;
-    const int kblocks = (a.k + BK - 1) / BK;
+    const int kblocks = (a.k + BKE - 1) / BKE;
     const int kper = (kblocks + a.splits - 1) / a.splits;
     const int kb0 = blockIdx.z * kper, kb1 = min(kblocks, kb0 + kper);
     const int nk = max(0, kb1 - kb0);
 
     if (tid == 0) {
-        for (int s = 0; s < Smem<BN>::STAGES; s++) {
+        for (int s = 0; s < SM::STAGES; s++) {
             mbar_init(full + s, PRODUCERS + (tma_b ? 1 : 0));
             mbar_init(empty + s, 1);
         }
@@ -111,7 +142,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
     if (warp == MMA_WARP) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                     "n"(BN < 32 ? 32 : BN));
+                     "n"(TCOLS));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     tc_fence_before();
@@ -125,7 +156,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     // gather metadata of the producer's row: pixel + (CONV) the select-on-read decision of every
     // tap of both concat segments, in a shared table; read before the programmatic-launch wait
     // when the row/index lists are static (they are inside a captured edit step)
-    int* seltab = (int*)(((uintptr_t)(smem + Smem<BN>::STAGES * Smem<BN>::STAGE + 256 + Smem<BN>::EPI) + 15) & ~(uintptr_t)15);
+    int* seltab = (int*)(((uintptr_t)(smem + SM::STAGES * SM::STAGE + 256 + SM::EPI) + 15) & ~(uintptr_t)15);
     const int ar = tid >> 1, half_id = tid & 1;
     int row_p = 0;
     bool row_valid = false;
@@ -144,7 +175,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     if (tid == 0) ltr(ls, 1);
     if (tma_b && warp == MMA_WARP + 0 && lane == 0 && !a.b.step_stride) {
         // weights: pull this CTA's B tiles into L2 while the previous kernel still runs
-        for (int i = 0; i < nk; i++) tma_prefetch2d(&tmb, (kb0 + i) * BK, n0);
+        for (int i = 0; i < nk; i++) tma_prefetch2d(&tmb, (kb0 + i) * BKE, n0);
     }
     pdl_trigger();
     pdl_wait();  // everything above (barrier init, TMEM alloc, static metadata) overlaps the previous kernel
@@ -168,17 +199,29 @@ __global__ void __launch_bounds__(THREADS, 1)
         const int* mysel = seltab + ar * 2 * 9;
         const int src0c = a.nsrc > 0 ? a.src[0].c : 0;
         const int bn = n0 + ar;
-        const char* brow = bbase + (long long)bn * a.b.ld * 2;
+        const char* brow = bbase + (long long)bn * a.b.ld * ES;
+        constexpr int LAG = 2;  // X3: stages of this thread's copies in flight before it splits one
+        auto x3_publish = [&](int q) {  // split this thread's chunks of stage q in place, publish it
+            unsigned char* st = smem + (q % SM::STAGES) * SM::STAGE;
+#pragma unroll
+            for (int j = j0; j < j0 + 4; j++) {
+                x3_split(st + SM::A_PART, SM::A_PART, sw128_off(ar, j));
+                if (ar < BN) x3_split(st + SM::A_BYTES + SM::B_PART, SM::B_PART, sw128_off(ar, j));
+            }
+            fence_async_smem();
+            mbar_arrive(full + q % SM::STAGES);
+        };
         for (int i = 0; i < nk; i++) {
-            const int s = i % Smem<BN>::STAGES;
-            const int k0 = (kb0 + i) * BK;
-            if (i >= Smem<BN>::STAGES) mbar_wait(empty + s, ((i / Smem<BN>::STAGES) & 1) ^ 1);
-            const uint32_t sa = sbase + s * Smem<BN>::STAGE;
-            const uint32_t sb = sa + Smem<BN>::A_BYTES;
+            const int s = i % SM::STAGES;
+            const int k0 = (kb0 + i) * BKE;
+            if (i >= SM::STAGES) mbar_wait(empty + s, ((i / SM::STAGES) & 1) ^ 1);
+            // X3: raw fp32 rows land in the "small" halves and are split in place
+            const uint32_t sa = sbase + s * SM::STAGE + (X3 ? SM::A_PART : 0);
+            const uint32_t sb = sbase + s * SM::STAGE + SM::A_BYTES + (X3 ? SM::B_PART : 0);
             const char* src = nullptr;
             if (row_valid) {
                 if (a.a_mode == FIS_A_ROWS) {
-                    if (k0 < a.k) src = abase + ((long long)row_p * a.a.ld + k0) * 2;
+                    if (k0 < a.k) src = abase + ((long long)row_p * a.a.ld + k0) * ES;
                 } else {
                     const int tap = k0 / cin;
                     int c = k0 - tap * cin;
@@ -187,58 +230,86 @@ __global__ void __launch_bounds__(THREADS, 1)
                     const int sel = mysel[seg * 9 + tap];
                     if (sel != SEL_ZERO) {
                         const fis_src& sr = a.src[seg];
-                        if (sel >= 0) src = (seg ? f1 : f0) + ((long long)sel * sr.fresh.ld + c) * 2;
-                        else src = (seg ? c1p : c0p) + ((long long)(-2 - sel) * sr.cache.ld + c) * 2;
+                        if (sel >= 0) src = (seg ? f1 : f0) + ((long long)sel * sr.fresh.ld + c) * ES;
+                        else src = (seg ? c1p : c0p) + ((long long)(-2 - sel) * sr.cache.ld + c) * ES;
                     }
                 }
             }
 #pragma unroll
             for (int j = j0; j < j0 + 4; j++) {
-                const bool ok = src != nullptr && (a.a_mode == FIS_A_CONV3X3 || k0 + j * 8 < a.k);
+                const bool ok = src != nullptr && (a.a_mode == FIS_A_CONV3X3 || k0 + j * EPC < a.k);
                 cp_async16(sa + sw128_off(ar, j), ok ? (const void*)(src + j * 16) : (const void*)bbase, ok);
             }
             if (tma_b) {
                 if (tid == 0) {
                     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(full + s)),
-                                 "r"((uint32_t)(BN * BK * 2))
+                                 "r"((uint32_t)(BN * 128))
                                  : "memory");
                     tc_tma2d(sb, &tmb, k0, n0, full + s);
                 }
             } else if (ar < BN) {  // B: weight row ar of this N tile
 #pragma unroll
                 for (int j = j0; j < j0 + 4; j++) {
-                    const bool ok = bn < a.n && k0 + j * 8 < a.k;
-                    cp_async16(sb + sw128_off(ar, j), ok ? (const void*)(brow + (k0 + j * 8) * 2) : (const void*)bbase,
+                    const bool ok = bn < a.n && k0 + j * EPC < a.k;
+                    cp_async16(sb + sw128_off(ar, j), ok ? (const void*)(brow + (long long)(k0 + j * EPC) * ES)
+                                                         : (const void*)bbase,
                                ok);
                 }
             }
-            // the barrier counts this thread's arrival when all its prior cp.async have landed:
-            // no thread-side wait, Smem<BN>::STAGES stages of loads stay in flight
-            cp_async_arrive_noinc(full + s);
+            if (X3) {
+                cp_commit();
+                if (i >= LAG) {
+                    cp_wait<LAG>();
+                    x3_publish(i - LAG);
+                }
+            } else {
+                // the barrier counts this thread's arrival when all its prior cp.async have landed:
+                // no thread-side wait, SM::STAGES stages of loads stay in flight
+                cp_async_arrive_noinc(full + s);
+            }
             if (tid == 0 && i == 0) trace(3);
+        }
+        if (X3) {  // drain: split and publish the last LAG stages
+            cp_wait<0>();
+            for (int q = nk - LAG < 0 ? 0 : nk - LAG; q < nk; q++) x3_publish(q);
         }
     } else {
         // ------------------------------------------------------------ MMA issuer
-        const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
+        // c = F32; a, b = BF16 (1) or TF32 (2); K-major; N >> 3; M >> 4
+        const uint32_t fmt = X3 ? 2u : 1u;
+        const uint32_t idesc = (1u << 4) | (fmt << 7) | (fmt << 10) | ((uint32_t)(BN >> 3) << 17) |
                                ((uint32_t)(BM >> 4) << 24);
         const uint32_t sbase = smem_u32(smem);
         for (int i = 0; i < nk; i++) {
-            const int s = i % Smem<BN>::STAGES;
-            mbar_wait(full + s, (i / Smem<BN>::STAGES) & 1);
+            const int s = i % SM::STAGES;
+            mbar_wait(full + s, (i / SM::STAGES) & 1);
             if (lane == 0 && i == 0) { trace(4); ltr(ls, 3); }
             if (lane == 0 && i == nk - 1) { trace(5); ltr(ls, 4); }
             tc_fence_after();
             if (lane == 0) {
-                const uint32_t sa = sbase + s * Smem<BN>::STAGE;
-                const uint32_t sb = sa + Smem<BN>::A_BYTES;
+                const uint32_t sa = sbase + s * SM::STAGE;
+                const uint32_t sb = sa + SM::A_BYTES;
 #pragma unroll
-                for (int kk = 0; kk < BK / 16; kk++) {
+                for (int kk = 0; kk < 4; kk++) {  // 4 MMAs of 32 bytes of K (16 bf16 / 8 tf32)
                     const uint64_t ad = sw128_desc(sa + kk * 32), bd = sw128_desc(sb + kk * 32);
                     const uint32_t acc = (i > 0 || kk > 0) ? 1u : 0u;
-                    asm volatile(
-                        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-                        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem),
-                        "l"(ad), "l"(bd), "r"(idesc), "r"(acc));
+                    if (X3) {
+                        const uint64_t as = sw128_desc(sa + SM::A_PART + kk * 32);
+                        const uint64_t bs = sw128_desc(sb + SM::B_PART + kk * 32);
+                        const uint32_t dbig = tmem + (uint32_t)((i % NBIG) * BN), dsmall = tmem + (uint32_t)(NBIG * BN);
+                        const uint32_t acc_big = (i >= NBIG || kk > 0) ? 1u : 0u;
+                        asm volatile(
+                            "{\n.reg .pred p, q, r;\nsetp.ne.b32 p, %7, 0;\nsetp.eq.b32 q, 0, 0;\nsetp.ne.b32 r, %8, 0;\n"
+                            "tcgen05.mma.cta_group::1.kind::tf32 [%1], %2, %4, %6, p;\n"
+                            "tcgen05.mma.cta_group::1.kind::tf32 [%1], %3, %5, %6, q;\n"
+                            "tcgen05.mma.cta_group::1.kind::tf32 [%0], %3, %4, %6, r;\n}\n" ::"r"(dbig),
+                            "r"(dsmall), "l"(as), "l"(ad), "l"(bd), "l"(bs), "r"(idesc), "r"(acc), "r"(acc_big));
+                    } else {
+                        asm volatile(
+                            "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+                            "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem),
+                            "l"(ad), "l"(bd), "r"(idesc), "r"(acc));
+                    }
                 }
                 asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                                  smem_u32(empty + s))
@@ -305,6 +376,28 @@ __global__ void __launch_bounds__(THREADS, 1)
         constexpr int HC = BN / 2;  // columns per warp half
         uint32_t u[HC];
         const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) + half * HC;
+        if (X3 && nk > 0) {  // small-product accumulator + the big*big accumulators in use, in order
+            float accv[HC];
+            const int nb = nk < NBIG ? nk : NBIG;
+            for (int b = -1; b < nb; b++) {
+                const uint32_t ta = taddr + (uint32_t)((b < 0 ? NBIG : b) * BN);
+#pragma unroll
+                for (int q = 0; q < HC / 16; q++) {
+                    asm volatile(
+                        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+                        : "=r"(u[16 * q + 0]), "=r"(u[16 * q + 1]), "=r"(u[16 * q + 2]), "=r"(u[16 * q + 3]),
+                          "=r"(u[16 * q + 4]), "=r"(u[16 * q + 5]), "=r"(u[16 * q + 6]), "=r"(u[16 * q + 7]),
+                          "=r"(u[16 * q + 8]), "=r"(u[16 * q + 9]), "=r"(u[16 * q + 10]), "=r"(u[16 * q + 11]),
+                          "=r"(u[16 * q + 12]), "=r"(u[16 * q + 13]), "=r"(u[16 * q + 14]), "=r"(u[16 * q + 15])
+                        : "r"(ta + 16 * q));
+                }
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+                for (int j = 0; j < HC; j++) accv[j] = b < 0 ? __uint_as_float(u[j]) : __fadd_rn(accv[j], __uint_as_float(u[j]));
+            }
+#pragma unroll
+            for (int j = 0; j < HC; j++) u[j] = __float_as_uint(accv[j]);
+        } else {
 #pragma unroll
         for (int q = 0; q < HC / 16; q++) {
             asm volatile(
@@ -316,6 +409,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                 : "r"(taddr + 16 * q));
         }
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        }
         {
             // stage the fp32 tile (the split-K partial, or the whole tile when S == 1) in the idle
             // pipeline buffers; the stores below run columns-fastest across threads (coalesced), not
@@ -333,7 +427,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     __syncthreads();
     if (tid == 0) { trace(9); ltr(ls, 8); }
     if (warp == MMA_WARP)
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(BN < 32 ? 32 : BN));
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(TCOLS));
     if (tid == 0) ltr(ls, 9);
     // fused epilogue of tile rows [rbeg, rend) from an fp32 staging buffer (row lr at src + (lr - rbeg) * PLD),
     // 16-column chunks; transposed outputs (V^T of a fused QKV, or d_trans) go rows-fastest across threads so a
@@ -450,14 +544,16 @@ __global__ void __launch_bounds__(THREADS, 1)
     if (tid == 0) { trace(7); trace_cta(3); ltr(ls, 7); }
 }
 
-template <int BN>
+template <int BN, bool X3>
 int launch(const fis_gemm_args* a, cudaStream_t stream) {
-    const int smem = Smem<BN>::TOTAL;
+    using SM = Smem<BN, X3>;
+    const int smem = a->splits > 1 ? SM::TOTAL : SM::BASE;
     static bool configured = false;
     if (!configured) {
-        if (cudaFuncSetAttribute(gemm_tc_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
+        if (cudaFuncSetAttribute(gemm_tc_kernel<BN, X3>, cudaFuncAttributeMaxDynamicSharedMemorySize, SM::TOTAL) !=
+            cudaSuccess)
             return FIS_ERR_UNSUPPORTED;
-        cudaFuncSetAttribute(gemm_tc_kernel<BN>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        cudaFuncSetAttribute(gemm_tc_kernel<BN, X3>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
         configured = true;
     }
     const int S = a->splits > 1 ? a->splits : 1;
@@ -488,23 +584,24 @@ int launch(const fis_gemm_args* a, cudaStream_t stream) {
         tm = fis_weight_map(a->b.ptr, a->n, a->k, a->b.ld, BN);
     CUtensorMap none;
     std::memset(&none, 0, sizeof(none));
-    return cudaLaunchKernelEx(&cfg, gemm_tc_kernel<BN>, *a, tm ? *tm : none, tm ? 1 : 0) == cudaSuccess ? FIS_OK
+    return cudaLaunchKernelEx(&cfg, gemm_tc_kernel<BN, X3>, *a, tm ? *tm : none, tm ? 1 : 0) == cudaSuccess ? FIS_OK
                                                                                                       : FIS_ERR_LAUNCH;
 }
 
 // How many clusters of S CTAs (split-K) the device co-schedules for this kernel, S = 1..16
 // (GPC packing: ~18 SMs per GPC, 1 CTA per SM). Cached per BN.
-template <int BN>
+template <int BN, bool X3>
 int active_clusters(int S) {
+    using SM = Smem<BN, X3>;
     static int table[17] = {0};
     if (S < 1 || S > 16) return 0;
     if (table[S]) return table[S];
-    cudaFuncSetAttribute(gemm_tc_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, Smem<BN>::TOTAL);
-    cudaFuncSetAttribute(gemm_tc_kernel<BN>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaFuncSetAttribute(gemm_tc_kernel<BN, X3>, cudaFuncAttributeMaxDynamicSharedMemorySize, SM::TOTAL);
+    cudaFuncSetAttribute(gemm_tc_kernel<BN, X3>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(1, 1, S);
     cfg.blockDim = dim3(THREADS);
-    cfg.dynamicSmemBytes = Smem<BN>::TOTAL;
+    cfg.dynamicSmemBytes = SM::TOTAL;
     cudaLaunchAttribute attr;
     attr.id = cudaLaunchAttributeClusterDimension;
     attr.val.clusterDim.x = 1;
@@ -513,19 +610,19 @@ int active_clusters(int S) {
     cfg.attrs = &attr;
     cfg.numAttrs = 1;
     int n = 0;
-    if (cudaOccupancyMaxActiveClusters(&n, gemm_tc_kernel<BN>, &cfg) != cudaSuccess) n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, gemm_tc_kernel<BN, X3>, &cfg) != cudaSuccess) n = 0;
     cudaGetLastError();
     table[S] = n > 0 ? n : -1;
     return table[S];
 }
 
 // Largest S such that all tiles' clusters run in one wave and each split keeps >= 3 K blocks.
-template <int BN>
+template <int BN, bool X3>
 int choose_splits(long long tiles, long long kb) {
     int best = 1;
     for (int S = 2; S <= 16; S++) {
         if (kb / S < 3) break;
-        const int ac = active_clusters<BN>(S);
+        const int ac = active_clusters<BN, X3>(S);
         if (ac >= tiles) best = S;
     }
     return best;
@@ -556,15 +653,40 @@ int fis_gemm_tc_supported(const fis_gemm_args* a) {
 
 int fis_gemm_tc_choose_splits(int m, int n, int k) {
     const long long kb = (k + fis::tc::BK - 1) / fis::tc::BK;
-    if (n <= 64) return fis::tc::choose_splits<64>((long long)((m + 127) / 128) * ((n + 63) / 64), kb);
-    return fis::tc::choose_splits<128>((long long)((m + 127) / 128) * ((n + 127) / 128), kb);
+    if (n <= 64) return fis::tc::choose_splits<64, false>((long long)((m + 127) / 128) * ((n + 63) / 64), kb);
+    return fis::tc::choose_splits<128, false>((long long)((m + 127) / 128) * ((n + 127) / 128), kb);
 }
 
 int fis_gemm_tc_launch(const fis_gemm_args* a, cudaStream_t stream) {
     if (!fis_gemm_tc_supported(a)) return FIS_ERR_UNSUPPORTED;
-    if (a->n <= 64) return fis::tc::launch<64>(a, stream);
-    if (a->n <= 128 || (a->n % 128) != 0) return fis::tc::launch<128>(a, stream);
-    return fis::tc::launch<128>(a, stream);
+    if (a->n <= 64) return fis::tc::launch<64, false>(a, stream);
+    return fis::tc::launch<128, false>(a, stream);
+}
+
+// 3xTF32 path (fp32 operands on the tensor cores): fp32 A sources and B with 16-byte aligned rows;
+// CONV segments whose channel counts are multiples of 32 (a 32-wide fp32 K block never straddles a
+// tap or a concat boundary); ROWS mode any K. 128 x 64 tiles.
+int fis_gemm_tf32_supported(const fis_gemm_args* a) {
+    if (a->b.dtype != FIS_F32 || (a->b.ld % 4)) return 0;
+    if (a->n_split > 0 && (a->n_split % 32)) return 0;
+    if (a->a_mode == FIS_A_ROWS) return a->a.dtype == FIS_F32 && (a->a.ld % 4) == 0;
+    for (int i = 0; i < a->nsrc; i++) {
+        const fis_src& s = a->src[i];
+        if (s.c % 32) return 0;
+        if (s.fresh.dtype != FIS_F32 || (s.fresh.ld % 4)) return 0;
+        if (s.index && (s.cache.dtype != FIS_F32 || (s.cache.ld % 4))) return 0;
+    }
+    return 1;
+}
+
+int fis_gemm_tf32_choose_splits(int m, int n, int k) {
+    const long long kb = (k + 31) / 32;
+    return fis::tc::choose_splits<64, true>((long long)((m + 127) / 128) * ((n + 63) / 64), kb);
+}
+
+int fis_gemm_tf32_launch(const fis_gemm_args* a, cudaStream_t stream) {
+    if (!fis_gemm_tf32_supported(a)) return FIS_ERR_UNSUPPORTED;
+    return fis::tc::launch<64, true>(a, stream);
 }
 
 FIS_LTR_SETTER(fis_ltr_set_tc)

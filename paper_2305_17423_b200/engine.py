@@ -29,6 +29,7 @@ from .model import (NORM_EPS, UNetConfig, build_registry, embed_ids, initial_lat
                     step_scale)
 
 _ESIZE = {torch.float32: 4, torch.bfloat16: 2}
+PRECISIONS = ("fp32", "tf32x3", "bf16")
 
 
 class DRef:
@@ -107,12 +108,14 @@ class Launcher:
 
     def __init__(self, precision: str = "fp32", device=None):
         L.require_cuda()
-        if precision not in ("fp32", "bf16"):
-            raise ContractViolation(f"precision must be 'fp32' or 'bf16', got {precision!r}")
+        if precision not in PRECISIONS:
+            raise ContractViolation(f"precision must be one of {PRECISIONS}, got {precision!r}")
         self.precision = precision
         self.dev = torch.device(device or "cuda")
-        self.act = torch.float32 if precision == "fp32" else torch.bfloat16
-        self.gemm_impl = 1 if precision == "fp32" else 0
+        # fp32: fp32 operands, SIMT FFMA (the reference numerics, parity mode); tf32x3: fp32 operands on
+        # the tensor cores as 3xTF32 (big*big + big*small + small*big, fp32 accumulate); bf16: perf mode
+        self.act = torch.bfloat16 if precision == "bf16" else torch.float32
+        self.gemm_impl = {"fp32": 1, "tf32x3": 3, "bf16": 0}[precision]
         self.sms = L.lib().fis_device_sm_count()
         # namespace of the request being driven: requests that run concurrently (one CUDA stream
         # each) own separate scratch activations, split-K workspaces and step counters

@@ -8,8 +8,9 @@ plus UNetConfig, PromptTokens, SharedTokenMap, EditSession, UNet, initial_latent
 embed_tokens. All compute runs in libfisedit kernels on the GPU; inputs and
 outputs at this boundary are float32 NCHW numpy arrays as in the reference.
 
-Precision: `set_precision("fp32")` (default; fp32 operands, fp32 accumulate —
-the parity mode) or `set_precision("bf16")` (bf16 operands/activations on the
+Precision: `set_precision("fp32")` (default; fp32 operands, fp32 accumulate on SIMT FFMA —
+the parity mode), `set_precision("tf32x3")` (fp32 operands on the tcgen05 tensor cores as a
+3xTF32 split, fp32 accumulate) or `set_precision("bf16")` (bf16 operands/activations on the
 tcgen05 tensor cores, fp32 accumulate, fp32 softmax/GN/latent — the perf mode).
 """
 
@@ -37,8 +38,9 @@ _ENGINES: dict = {}
 
 def set_precision(p: str) -> None:
     global _PRECISION
-    if p not in ("fp32", "bf16"):
-        raise ConfigError(f"precision must be 'fp32' or 'bf16', got {p!r}")
+    from .engine import PRECISIONS
+    if p not in PRECISIONS:
+        raise ConfigError(f"precision must be one of {PRECISIONS}, got {p!r}")
     _PRECISION = p
 
 
