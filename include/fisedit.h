@@ -149,6 +149,8 @@ typedef struct {
  * rows = n_img * img_rows (img_rows = 0: one image), statistics written to mean / var
  * [img][groups]; no row lists. One launch for bf16 maps with 8 | channels per group. */
 int fis_gn(const fis_gn_apply_args* a, void* stream);
+/* kernel launches one fis_gn call makes: 1 (fused statistics + normalise) or 2 */
+int fis_gn_launches(const fis_gn_apply_args* a);
 int fis_gn_apply(const fis_gn_apply_args* a, void* stream);
 
 /* Row softmax of scaled scores, optional controlled-mode column substitution.

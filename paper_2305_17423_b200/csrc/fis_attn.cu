@@ -565,6 +565,8 @@ static bool attn_share(const fis_attn_args* a, int dvs) {
         return false;
     // batch 1 (a grid smaller than the GPU): the slices' redundant S work runs in parallel anyway,
     // a second (serial) launch only adds latency (r01 C2 step: 1.358 ms unshared vs 1.390 shared)
+    // (r02: forcing it for the d = 1280 levels measured 27.6 vs 29.1 us for L2 self attention,
+    // but more for cross attention; a wash at the step level)
     if (ctas < 148) return false;
     // one key block: recomputing S per slice is cheap unless the head dim is large (r01: L0 cross
     // attention 23 + 48 us shared vs one launch unshared)

@@ -199,3 +199,23 @@ inline cudaError_t fis_launch(void (*kernel)(Arg), dim3 grid, dim3 block, size_t
     cfg.numAttrs = fis_pdl_enabled() ? 1 : 0;
     return cudaLaunchKernelEx(&cfg, kernel, arg);
 }
+
+// the same with a thread-block cluster of cl CTAs along x
+template <typename Arg>
+inline cudaError_t fis_launch_cluster(void (*kernel)(Arg), dim3 grid, dim3 block, int cl, cudaStream_t stream,
+                                      const Arg& arg) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = cl;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = fis_pdl_enabled() ? 2 : 1;
+    return cudaLaunchKernelEx(&cfg, kernel, arg);
+}

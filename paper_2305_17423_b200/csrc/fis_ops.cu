@@ -3,6 +3,7 @@
 // select-on-read 2x2 average pooling and full-map materialisation.
 // All reductions use a fixed order, so outputs are bitwise deterministic.
 #include "fis_common.cuh"
+#include <type_traits>
 
 namespace fis {
 
@@ -372,57 +373,91 @@ __global__ void up2_kernel(const fis_pool_args a) {
 // ---- dense group norm in one launch (statistics + normalise + SiLU), bf16 maps, one CTA per
 // (group, stacked image): the group's hw x cpg block is read three times from L2 instead of
 // a statistics launch followed by a separate apply launch (same arithmetic as the pair)
+// One-launch dense GroupNorm (+SiLU) of bf16 maps: a cluster of GN_CL CTAs per (group, image), each
+// over a contiguous slice of the image's pixels; the two-pass statistics (sum -> f32 mean, then the
+// centred sum of squares) are block-reduced in f64 and combined across the cluster through
+// distributed shared memory in rank order (deterministic), then every CTA normalises its slice.
+// VW bf16 channels per vector access: 8 (16-byte loads, channels-per-group % 8 == 0) or 2.
+constexpr int GN_CL = 8;  // maximum cluster size (the launch picks 1..8 by map size)
+
+FIS_DEV double gn_block_sum(double v, double* red) {
+    const int tid = threadIdx.x;
+    red[tid] = v;
+    __syncthreads();
+    for (int o = 128; o; o >>= 1) {
+        if (tid < o) red[tid] += red[tid + o];
+        __syncthreads();
+    }
+    const double r = red[0];
+    __syncthreads();
+    return r;
+}
+
+// cluster-wide sum of one double per CTA (slot[0] of every CTA's shared memory, rank order)
+FIS_DEV double gn_cluster_sum(double mine, double* slot) {
+    if (threadIdx.x == 0) *slot = mine;
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    double s = 0.0;
+    const uint32_t a = (uint32_t)__cvta_generic_to_shared(slot);
+    uint32_t ncl;
+    asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(ncl));
+    for (int r = 0; r < (int)ncl; r++) {
+        uint32_t ra;
+        double v;
+        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(a), "r"(r));
+        asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(ra) : "memory");
+        s += v;
+    }
+    return s;
+}
+
+template <int VW>
 __global__ void __launch_bounds__(256) gn_fused_kernel(const fis_gn_apply_args a) {
+    using VT = typename std::conditional<VW == 8, uint4, uint32_t>::type;
     const int ls = ltr_begin(5);
     const int t = cur_step(a.step);  // host-written before the step: read before the wait
     pdl_trigger();
     pdl_wait();
     ltr(ls, 2);
     const int hw = a.img_rows;  // pixels per image (set by fis_gn)
-    const int g = blockIdx.x, img = blockIdx.y, tid = threadIdx.x;
-    const int cpg = a.c / a.groups, vpg = cpg / 8, items = hw * vpg;
+    uint32_t ncl, crank;
+    asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(ncl));
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(crank));
+    const int cl = (int)ncl, rank = (int)crank;
+    const int g = blockIdx.x / cl, img = blockIdx.y, tid = threadIdx.x;
+    const int cpg = a.c / a.groups, vpg = cpg / VW;
+    const int per = (hw + cl - 1) / cl, q0 = min(hw, rank * per), q1 = min(hw, q0 + per);
+    const int items = (q1 - q0) * vpg;
     const long long cnt = (long long)hw * cpg;
-    const __nv_bfloat16* x = (const __nv_bfloat16*)ref_base(a.x, t) + (long long)img * hw * a.x.ld + g * cpg;
+    const __nv_bfloat16* x = (const __nv_bfloat16*)ref_base(a.x, t) + (long long)(img * hw + q0) * a.x.ld + g * cpg;
     __shared__ double red[256];
+    __shared__ double slot[2];
     float ps = 0.f;
     for (int i = tid; i < items; i += blockDim.x) {
         const int q = i / vpg, v = i - q * vpg;
-        const uint4 u = *(const uint4*)(x + (long long)q * a.x.ld + v * 8);
+        const VT u = *(const VT*)(x + (long long)q * a.x.ld + v * VW);
         const __nv_bfloat162* h = (const __nv_bfloat162*)&u;
 #pragma unroll
-        for (int k = 0; k < 4; k++) {
+        for (int k = 0; k < VW / 2; k++) {
             const float2 f = __bfloat1622float2(h[k]);
             ps += f.x + f.y;
         }
     }
-    red[tid] = (double)ps;
-    __syncthreads();
-    for (int o = 128; o; o >>= 1) {
-        if (tid < o) red[tid] += red[tid + o];
-        __syncthreads();
-    }
-    const float mf = (float)(red[0] / (double)cnt);
-    __syncthreads();
+    const float mf = (float)(gn_cluster_sum(gn_block_sum((double)ps, red), slot) / (double)cnt);
     float pv = 0.f;
     for (int i = tid; i < items; i += blockDim.x) {
         const int q = i / vpg, v = i - q * vpg;
-        const uint4 u = *(const uint4*)(x + (long long)q * a.x.ld + v * 8);
+        const VT u = *(const VT*)(x + (long long)q * a.x.ld + v * VW);
         const __nv_bfloat162* h = (const __nv_bfloat162*)&u;
 #pragma unroll
-        for (int k = 0; k < 4; k++) {
+        for (int k = 0; k < VW / 2; k++) {
             const float2 f = __bfloat1622float2(h[k]);
             const float d0 = f.x - mf, d1 = f.y - mf;
             pv = fmaf(d0, d0, fmaf(d1, d1, pv));
         }
     }
-    red[tid] = (double)pv;
-    __syncthreads();
-    for (int o = 128; o; o >>= 1) {
-        if (tid < o) red[tid] += red[tid + o];
-        __syncthreads();
-    }
-    const float vf = (float)(red[0] / (double)cnt);
-    if (tid == 0) {
+    const float vf = (float)(gn_cluster_sum(gn_block_sum((double)pv, red), slot + 1) / (double)cnt);
+    if (tid == 0 && rank == 0) {
         ((float*)ref_base(a.mean, t))[img * a.groups + g] = mf;
         ((float*)ref_base(a.var, t))[img * a.groups + g] = vf;
     }
@@ -431,29 +466,32 @@ __global__ void __launch_bounds__(256) gn_fused_kernel(const fis_gn_apply_args a
     char* ys = a.y_silu.ptr ? ref_base(a.y_silu, t) : nullptr;
     for (int i = tid; i < items; i += blockDim.x) {
         const int q = i / vpg, v = i - q * vpg;
-        const int c = g * cpg + v * 8;
-        const long long row = (long long)img * hw + q;
-        const uint4 u = *(const uint4*)(x + (long long)q * a.x.ld + v * 8);
+        const int c = g * cpg + v * VW;
+        const long long row = (long long)img * hw + q0 + q;
+        const VT u = *(const VT*)(x + (long long)q * a.x.ld + v * VW);
         const __nv_bfloat162* h = (const __nv_bfloat162*)&u;
-        uint4 on, os;
+        VT on, os;
         __nv_bfloat162* hn = (__nv_bfloat162*)&on;
         __nv_bfloat162* hs = (__nv_bfloat162*)&os;
-        float ga[8], be[8];
-        *(float4*)ga = __ldg((const float4*)(a.gamma + c));
-        *(float4*)(ga + 4) = __ldg((const float4*)(a.gamma + c + 4));
-        *(float4*)be = __ldg((const float4*)(a.beta + c));
-        *(float4*)(be + 4) = __ldg((const float4*)(a.beta + c + 4));
+        float ga[VW], be[VW];
 #pragma unroll
-        for (int k = 0; k < 4; k++) {
+        for (int k = 0; k < VW; k += 2) {
+            *(float2*)(ga + k) = __ldg((const float2*)(a.gamma + c + k));
+            *(float2*)(be + k) = __ldg((const float2*)(a.beta + c + k));
+        }
+#pragma unroll
+        for (int k = 0; k < VW / 2; k++) {
             const float2 f = __bfloat1622float2(h[k]);
             const float y0 = fmaf((f.x - mf) * rstd, ga[2 * k], be[2 * k]);
             const float y1 = fmaf((f.y - mf) * rstd, ga[2 * k + 1], be[2 * k + 1]);
             hn[k] = __floats2bfloat162_rn(y0, y1);
             hs[k] = __floats2bfloat162_rn(__fdividef(y0, 1.0f + __expf(-y0)), __fdividef(y1, 1.0f + __expf(-y1)));
         }
-        if (yn) *(uint4*)((__nv_bfloat16*)yn + row * a.y_norm.ld + c) = on;
-        if (ys) *(uint4*)((__nv_bfloat16*)ys + row * a.y_silu.ld + c) = os;
+        if (yn) *(VT*)((__nv_bfloat16*)yn + row * a.y_norm.ld + c) = on;
+        if (ys) *(VT*)((__nv_bfloat16*)ys + row * a.y_silu.ld + c) = os;
     }
+    // peers read this CTA's slots: keep its shared memory until the whole cluster is done
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
 static int grid_for(long long total, int threads) {
@@ -477,21 +515,47 @@ extern "C" int fis_gn_apply(const fis_gn_apply_args* a, void* stream);
 // Dense group norm with its own statistics (written to mean/var per image): rows = n_img * img_rows
 // (img_rows = 0: one image). bf16 maps with 8 | channels-per-group take the one-launch kernel;
 // otherwise statistics + apply are two launches.
+// one-launch GN (statistics + normalise per group) for bf16 maps: vector width 8 (16-byte
+// accesses) when the channels per group allow, else 2 (bf16 pairs); 0 = two launches
+static int gn_vec(const fis_gn_apply_args* a) {
+    const int cpg = a->c / a->groups;
+    for (int vw = 8; vw >= 2; vw -= 6) {
+        if (a->x.dtype == FIS_BF16 && cpg % vw == 0 && (a->x.ld % vw) == 0 &&
+            (!a->y_norm.ptr || (a->y_norm.dtype == FIS_BF16 && (a->y_norm.ld % vw) == 0)) &&
+            (!a->y_silu.ptr || (a->y_silu.dtype == FIS_BF16 && (a->y_silu.ld % vw) == 0)) &&
+            ((((uintptr_t)a->x.ptr) | ((uintptr_t)a->y_norm.ptr) | ((uintptr_t)a->y_silu.ptr)) & (2 * vw - 1)) == 0)
+            return vw;
+    }
+    return 0;
+}
+
+// kernel launches one fis_gn call makes (1 fused, or 2: statistics + apply)
+extern "C" int fis_gn_launches(const fis_gn_apply_args* a) {
+    if (a->groups <= 0 || a->c % a->groups || a->rows == 0) return 0;
+    return gn_vec(a) ? 1 : 2;
+}
+
 extern "C" int fis_gn(const fis_gn_apply_args* a, void* stream) {
     if (a->groups <= 0 || a->c % a->groups) return FIS_ERR_SHAPE;
     if (a->rows == 0) return FIS_OK;
     const int hw = a->img_rows > 0 ? a->img_rows : a->rows;
     if (a->rows % hw || a->x_rows || a->y_rows || a->row_img) return FIS_ERR_SHAPE;
-    const int n_img = a->rows / hw, cpg = a->c / a->groups;
-    const bool vec = a->x.dtype == FIS_BF16 && cpg % 8 == 0 && (a->x.ld % 8) == 0 &&
-                     (!a->y_norm.ptr || (a->y_norm.dtype == FIS_BF16 && (a->y_norm.ld % 8) == 0)) &&
-                     (!a->y_silu.ptr || (a->y_silu.dtype == FIS_BF16 && (a->y_silu.ld % 8) == 0)) &&
-                     ((((uintptr_t)a->x.ptr) | ((uintptr_t)a->y_norm.ptr) | ((uintptr_t)a->y_silu.ptr)) & 15) == 0;
-    if (vec) {
+    const int n_img = a->rows / hw;
+    if (const int vw = gn_vec(a)) {
         fis_gn_apply_args ap = *a;
         ap.img_rows = hw;
-        return fis_launch(fis::gn_fused_kernel, dim3(a->groups, n_img), dim3(256), 0, (cudaStream_t)stream, ap) ==
-                       cudaSuccess ? FIS_OK : FIS_ERR_LAUNCH;
+        // a cluster of 8 CTAs per (group, image) from 256 pixels up (r02 C2 dense step: L0 GN 78 -> 22 us,
+        // L1 49 -> 16 us); smaller maps one CTA per group (no cluster launch)
+        const int cl = hw >= 256 ? 8 : 1;
+        const dim3 grid(a->groups * cl, n_img);
+        cudaError_t e;
+        if (cl > 1)
+            e = vw == 8 ? fis_launch_cluster(fis::gn_fused_kernel<8>, grid, dim3(256), cl, (cudaStream_t)stream, ap)
+                        : fis_launch_cluster(fis::gn_fused_kernel<2>, grid, dim3(256), cl, (cudaStream_t)stream, ap);
+        else
+            e = vw == 8 ? fis_launch(fis::gn_fused_kernel<8>, grid, dim3(256), 0, (cudaStream_t)stream, ap)
+                        : fis_launch(fis::gn_fused_kernel<2>, grid, dim3(256), 0, (cudaStream_t)stream, ap);
+        return e == cudaSuccess ? FIS_OK : FIS_ERR_LAUNCH;
     }
     fis_gn_stats_args st = {};
     st.hw = hw; st.c = a->c; st.groups = a->groups; st.x = a->x; st.mean = a->mean; st.var = a->var;

@@ -518,7 +518,8 @@ class Engine(Launcher):
         a.y_norm, a.y_silu = _r(y_norm), _r(y_silu)
         a.step = L.ptr(self.step_dev)
         self._call("fis_gn" if fused_stats else "fis_gn_apply", a)
-        self._count("fis_gn" if fused_stats else "fis_gn_apply", rows=rows, c=c)
+        nk = max(1, L.lib().fis_gn_launches(C.byref(a))) if fused_stats else 1
+        self._count("fis_gn" if fused_stats else "fis_gn_apply", nk, rows=rows, c=c)
 
     def pool(self, fv: FeatVal, rows, n, out: DRef):
         a = L.PoolArgs()
