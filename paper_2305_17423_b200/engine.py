@@ -92,7 +92,9 @@ class Weights:
                 self.sa[i.layer_id] = (torch.from_numpy(np.ascontiguousarray(wqkv)).to(dev, act),
                                        1.0 / math.sqrt(i.channels))
             else:
-                self.ca[i.layer_id] = (torch.from_numpy(np.ascontiguousarray(p["wq"].T)).to(dev, act),
+                # wq [C_in, C_out] as the reference stores it (q = g . wq): the per-edit score matrix
+                # M^T = K . wq^T... see Engine.text_kv
+                self.ca[i.layer_id] = (torch.from_numpy(np.ascontiguousarray(p["wq"])).to(dev, act),
                                        torch.from_numpy(np.ascontiguousarray(p["wk_text"].T)).to(dev, f32),
                                        torch.from_numpy(np.ascontiguousarray(p["wv_text"].T)).to(dev, f32),
                                        1.0 / math.sqrt(i.channels))
@@ -371,7 +373,12 @@ class Engine(Launcher):
 
     # ------------------------------------------------------------ text K/V
     def text_kv(self, text_emb: np.ndarray):
-        """Per cross layer K [n_text, C] and V^T [C, pad16(n_text)] (unet.py:476-479), once per prompt."""
+        """Per cross layer, once per prompt: text K [n_text, C] and V^T [C, pad16(n_text)]
+        (unet.py:476-479) and the score matrix M^T = K . wq^T [n_text, C].
+
+        Cross attention reassociates its scores: (x wq) K^T = x (wq K^T) = x M, so the step feeds
+        the layer input x straight into the attention kernel with M^T as its key matrix and skips
+        the per-step query projection (one launch and a C x C GEMM per cross layer and step)."""
         nt = text_emb.shape[0]
         emb = torch.from_numpy(np.ascontiguousarray(text_emb, dtype=np.float32)).to(self.dev)
         out = {}
@@ -379,13 +386,15 @@ class Engine(Launcher):
             c = wq.shape[0]
             k = torch.empty((nt, c), dtype=self.act, device=self.dev)
             vt = torch.zeros((c, _pad(nt)), dtype=self.act, device=self.dev)
+            mt = torch.empty((nt, c), dtype=self.act, device=self.dev)
             self.gemm(nt, c, emb.shape[1], a=DRef(emb), b=DRef(wk), d=DRef(k), splits=1)
             self.gemm(nt, c, emb.shape[1], a=DRef(emb), b=DRef(wv), d=DRef(vt), d_trans=True, splits=1)
+            self.gemm(nt, c, c, a=DRef(k), b=DRef(wq), d=DRef(mt), splits=1)
             v = None
             if self.fused_xattn:  # row-major V only for the SIMT cross-attention kernel
                 v = torch.empty((nt, c), dtype=self.act, device=self.dev)
                 self.gemm(nt, c, emb.shape[1], a=DRef(emb), b=DRef(wv), d=DRef(v), splits=1)
-            out[lid] = (k, vt, v)
+            out[lid] = (k, vt, v, mt)
         return out
 
     def text_kv_stacked(self, text_embs):
@@ -404,9 +413,11 @@ class Engine(Launcher):
             c = wq.shape[0]
             k = torch.empty((R * ks, c), dtype=self.act, device=self.dev)
             vt = torch.empty((c, R * ks), dtype=self.act, device=self.dev)
+            mt = torch.empty((R * ks, c), dtype=self.act, device=self.dev)
             self.gemm(R * ks, c, emb.shape[1], a=DRef(emb_d), b=DRef(wk), d=DRef(k))
             self.gemm(R * ks, c, emb.shape[1], a=DRef(emb_d), b=DRef(wv), d=DRef(vt), d_trans=True)
-            out[lid] = (k, vt, None)
+            self.gemm(R * ks, c, c, a=DRef(k), b=DRef(wq), d=DRef(mt))
+            out[lid] = (k, vt, None, mt)
         kseg = torch.tensor([v for r in range(R) for v in (r * ks, r * ks + nts[r])], dtype=torch.int32,
                             device=self.dev)
         return out, kseg, max(nts)
@@ -447,28 +458,27 @@ class Engine(Launcher):
         segs (batched requests): (q_seg, k_seg, nseg, max_q) -- each request's rows attend to its
         own prompt's keys (stacked K / V^T of all requests)."""
         wq, _, _, scale = self.W.ca[lid]
-        k, vt, v = kv[lid]
+        k, vt, v, mt = kv[lid]
         c, nt = wq.shape[0], k.shape[0]
         ntp = vt.shape[1]
         cap = self.cap(level)
-        q = self.scratch(f"q{tag}", (cap, c))
-        self.gemm(m, c, c, a=x, b=DRef(wq), d=DRef(q), b_static=True)
+        # scores x (wq K^T) = x M: the layer input is the query, M^T (per edit) the key matrix
         if segs is not None:
-            self.attn(m, nt, c, DRef(q), DRef(k), DRef(vt), scale, x, out, pre, segs=segs)
+            self.attn(m, nt, c, x, DRef(mt), DRef(vt), scale, x, out, pre, segs=segs)
             return
         if ctrl is None and map_ is None and nt <= 128 and self.fused_xattn:
             # scores + softmax + P.V + residual in one launch (text context <= 128 tokens)
-            a = L.XattnArgs(m, c, nt, DRef(q).ref(), DRef(k).ref(), DRef(v).ref(), scale, x.ref(), _r(pre),
+            a = L.XattnArgs(m, c, nt, x.ref(), DRef(mt).ref(), DRef(v).ref(), scale, x.ref(), _r(pre),
                             out.ref(), L.ptr(self.step_dev))
             self._call("fis_xattn", a)
             self._count("fis_xattn", m=m, n_keys=nt)
             return
-        if ctrl is None and map_ is None and self.use_fused_attn(c, m, nt, pre):
-            self.attn(m, nt, c, DRef(q), DRef(k), DRef(vt), scale, x, out, pre)
+        if ctrl is None and map_ is None and self.use_fused_attn(c, m, nt, pre) and not x.ss:
+            self.attn(m, nt, c, x, DRef(mt), DRef(vt), scale, x, out, pre)
             return
         S = self.scratch(f"Sx{tag}", (cap, ntp), torch.float32)  # ld padded: 16-byte aligned rows
         P = self.scratch(f"Px{tag}", (cap, ntp), zero=True)
-        self.gemm(m, nt, c, a=DRef(q), b=DRef(k), d=DRef(S), b_static=True)  # text K: per edit
+        self.gemm(m, nt, c, a=x, b=DRef(mt), d=DRef(S), b_static=True)  # M^T: per edit
         if ctrl is not None:
             cached, verbatim, pairs = ctrl
             self.softmax(m, nt, ntp, DRef(S), scale, DRef(P), map_, cached=cached, verbatim=verbatim, pairs=pairs)

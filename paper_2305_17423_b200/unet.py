@@ -584,11 +584,13 @@ def stack_text_kv(eng: Engine, kvs):
         c = kvs[0][lid][0].shape[1]
         K = torch.zeros((R * ks, c), dtype=eng.act, device=eng.dev)
         VT = torch.zeros((c, R * ks), dtype=eng.act, device=eng.dev)
+        MT = torch.zeros((R * ks, c), dtype=eng.act, device=eng.dev)
         for r, kv in enumerate(kvs):
-            k, vt, _ = kv[lid]
+            k, vt, _, mt = kv[lid]
             K[r * ks: r * ks + nts[r]] = k
             VT[:, r * ks: r * ks + nts[r]] = vt[:, :nts[r]]
-        out[lid] = (K, VT, None)
+            MT[r * ks: r * ks + nts[r]] = mt
+        out[lid] = (K, VT, None, MT)
     kseg = torch.tensor([v for r in range(R) for v in (r * ks, r * ks + nts[r])], dtype=torch.int32, device=eng.dev)
     return out, kseg
 
