@@ -172,9 +172,10 @@ __global__ void __launch_bounds__(THREADS, 1)
         // cross attention: K and V^T are the per-edit text keys / values (no kernel of the step writes
         // them) -> pull this CTA's chunks into L2 while the previous kernel runs. Self attention reads
         // K / V from the QKV GEMM just before it (already in L2): K lives in the Q buffer's rows.
-        const char* qb = (const char*)a.q.ptr;
-        const char* kb = (const char*)a.k.ptr;
-        const bool self_kv = kb >= qb && kb < qb + (long long)a.m * a.q.ld * 2;
+        // self attention passes the keys as the layer input s (written by the kernel before the
+        // projection): only the cross-attention text matrices are prefetched (K with a different
+        // row count than the queries, or V^T narrower than the query count)
+        const bool self_kv = a.n_keys == a.m;
         if (!self_kv) {
             const int nkb2 = (n_keys + 127) / 128, dch2 = a.d / 64;
             for (int j = 0; j < nkb2; j++)

@@ -88,8 +88,12 @@ class Weights:
             elif i.kind == "norm":
                 self.norm[i.layer_id] = (torch.from_numpy(p["gamma"]).to(dev, f32), torch.from_numpy(p["beta"]).to(dev, f32))
             elif i.kind == "self_attn":
-                wqkv = np.concatenate([p["wq"].T, p["wk"].T, p["wv"].T], axis=0)  # [3C, C]
-                self.sa[i.layer_id] = (torch.from_numpy(np.ascontiguousarray(wqkv)).to(dev, act),
+                # scores reassociated: (s wq)(s wk)^T = (s (wq wk^T)) s^T, so the projection GEMM makes
+                # Q' = s (wq wk^T) and V only (B = [(wq wk^T)^T; wv^T], [2C, C]; the product in f64) and
+                # the keys are s itself: 2/3 of the QKV weights and FLOPs
+                mqk = (p["wq"].astype(np.float64) @ p["wk"].astype(np.float64).T).T
+                wqv = np.concatenate([mqk, p["wv"].T.astype(np.float64)], axis=0).astype(np.float32)  # [2C, C]
+                self.sa[i.layer_id] = (torch.from_numpy(np.ascontiguousarray(wqv)).to(dev, act),
                                        1.0 / math.sqrt(i.channels))
             else:
                 # wq [C_in, C_out] as the reference stores it (q = g . wq): the per-edit score matrix
@@ -424,31 +428,31 @@ class Engine(Launcher):
 
     # ------------------------------------------------------------ building blocks
     def attn_self(self, lid, m, s: DRef, y1: DRef, level, tag, pre=None, segs=None):
-        """y1 = s + softmax(s Wq (s Wk)^T * scale) (s Wv) over m tokens (sparse.py:265-300/341-349).
+        """y1 = s + softmax(s Wq (s Wk)^T * scale) (s Wv) over m tokens (sparse.py:265-300/341-349),
+        computed as softmax(Q' s^T * scale) (s Wv) with Q' = s (Wq Wk^T) (Weights.sa).
 
         segs (batched requests): (q_seg, nseg, max_q) -- each request's rows attend to its own rows."""
-        wqkv, scale = self.W.sa[lid]
-        c = wqkv.shape[1]
+        wqv, scale = self.W.sa[lid]
+        c = wqv.shape[1]
         cap = self.cap(level)
         mp = _pad(cap)
-        qk = self.scratch(f"qk{tag}", (cap, 2 * c))
+        qk = self.scratch(f"q2{tag}", (cap, c))
         vt = self.scratch(f"vt{tag}", (c, mp), zero=True)
-        # one GEMM for Q|K (row-major) and V (stored transposed as the PV B operand)
-        self.gemm(m, 3 * c, c, a=s, b=DRef(wqkv), d=DRef(qk), n_split=2 * c, d2=DRef(vt, ld=mp), d2_trans=True,
+        # one GEMM for Q' (row-major) and V (stored transposed as the PV B operand)
+        self.gemm(m, 2 * c, c, a=s, b=DRef(wqv), d=DRef(qk), n_split=c, d2=DRef(vt, ld=mp), d2_trans=True,
                   b_static=True)
-        qkr = DRef(qk)
+        qr = DRef(qk)
         if segs is not None:
             qseg, nseg, maxq = segs
-            self.attn(m, m, c, qkr, qkr.cols(c), DRef(vt, ld=mp), scale, s, y1, pre,
-                      segs=(qseg, qseg, nseg, maxq, maxq))
+            self.attn(m, m, c, qr, s, DRef(vt, ld=mp), scale, s, y1, pre, segs=(qseg, qseg, nseg, maxq, maxq))
             return
         if self.use_fused_attn(c, m, m, pre):
-            # S = QK^T, softmax and P.V (+ residual) in one tcgen05 kernel (fis_attn)
-            self.attn(m, m, c, qkr, qkr.cols(c), DRef(vt, ld=mp), scale, s, y1, pre)
+            # S = Q' s^T, softmax and P.V (+ residual) in one tcgen05 kernel (fis_attn)
+            self.attn(m, m, c, qr, s, DRef(vt, ld=mp), scale, s, y1, pre)
             return
         S = self.scratch(f"S{tag}", (cap, cap), torch.float32)  # unfused path only (cap^2)
         P = self.scratch(f"P{tag}", (cap, mp), zero=True)
-        self.gemm(m, m, c, a=qkr, b=qkr.cols(c), d=DRef(S, ld=_pad(m)))
+        self.gemm(m, m, c, a=qr, b=s, d=DRef(S, ld=_pad(m)))
         self.softmax(m, m, _pad(m), DRef(S, ld=_pad(m)), scale, DRef(P, ld=_pad(m)))
         self.gemm(m, c, m, a=DRef(P, ld=_pad(m)), b=DRef(vt, ld=mp), d=y1, res=s, pre=pre)
 
