@@ -718,6 +718,28 @@ class Arena:
         v.outputs = {}
         return v
 
+    def map_tensors(self, fn) -> "Arena":
+        """A copy of this arena with every slab replaced by fn(slab) (host <-> device tiering)."""
+        a = Arena.__new__(Arena)
+        a.__dict__.update({k: v for k, v in self.__dict__.items()
+                           if k not in ("latent", "feature", "stats", "maps", "outputs")})
+        a.latent = fn(self.latent)
+        a.feature = {k: fn(t) for k, t in self.feature.items()}
+        a.stats = {k: (fn(m), fn(v)) for k, (m, v) in self.stats.items()}
+        a.maps = {k: fn(t) for k, t in self.maps.items()}
+        a.outputs = {k: fn(t) for k, t in self.outputs.items()}
+        return a
+
+    def slabs(self):
+        """(name, tensor) of every slab in a fixed order (the spill sidecar's record order)."""
+        out = [(("latent",), self.latent)]
+        out += [(("feature", *k), t) for k, t in self.feature.items()]
+        for k, (m, v) in self.stats.items():
+            out += [(("mean", k), m), (("var", k), v)]
+        out += [(("map", k), t) for k, t in self.maps.items()]
+        out += [(("out", k), t) for k, t in self.outputs.items()]
+        return out
+
     def nbytes(self):
         ts = [self.latent, *self.feature.values(), *self.maps.values(), *self.outputs.values()]
         ts += [x for p in self.stats.values() for x in p]
