@@ -777,7 +777,8 @@ int fis_gemm_big_launch(const fis_gemm_args* a, cudaStream_t stream) {
     if (amode == fis::big::A_CPASYNC && gmode == 1 && gather_ok(a) && encode_gather(a, &gm))
         amode = fis::big::A_TMA_GATHER;
     int bn = fis_gemm_big_bn(a->n);
-    if (amode == fis::big::A_CPASYNC || amode == fis::big::A_TMA_GATHER) {
+    static int wide_off = getenv("FIS_BIG_WIDE") && getenv("FIS_BIG_WIDE")[0] == '0';
+    if ((amode == fis::big::A_CPASYNC || amode == fis::big::A_TMA_GATHER) && !wide_off) {
         const int w = wide_bn(a->n);
         if (w) bn = w;
     }
