@@ -674,11 +674,13 @@ def stacked_requests(eng, U, P, cfg, args, peak_tf, ids):
         per = []
         for o, us, name in table:
             if o["op"] == "fis_gemm" and o.get("gathered"):
-                lvl = next(l for l in padded if padded[l] == o["m"])
+                lvl = o.get("level")
+                if lvl is None:
+                    lvl = next(l for l in padded if padded[l] == o["m"])
                 conv_us += us
                 fl = gated_conv_flops(o, active[lvl])
                 conv_fl += fl
-                per.append({"m_rows": o["m"], "n": o["n"], "k": o["k"], "us": round(us, 2),
+                per.append({"m_rows": o["m"], "n": o["n"], "k": o["k"], "us": round(us, 2), "halo": o.get("halo"),
                             "tflops": round(fl / (us * 1e-6) / 1e12, 1) if us else None})
         tf = conv_fl / (conv_us * 1e-6) / 1e12 if conv_us else 0.0
         gc_ = {"bound": "tensor", "achieved": tf, "peak": peak_tf, "unit": "TFLOP/s",

@@ -94,7 +94,8 @@ typedef struct {
     int n_split;            /* >0: columns n >= n_split go to d2 at column n - n_split (fused QKV) */
     fis_ref d2;
     int d2_trans;
-    const int* d_rows;      /* optional row remap for the output (and res/lat/pre): row = d_rows[r] */
+    const int* d_rows;      /* optional row remap for the output (and res/lat/pre): row = d_rows[r];
+                               d_rows[r] < 0: row r is computed but not stored */
     /* scheduling */
     int splits;             /* split-K factor; 0 = choose from the tile shape and SM count */
     float* ws;              /* splits*m*n floats when splits > 1 */
@@ -105,11 +106,17 @@ typedef struct {
                                operands (SIMT when the shape is not supported) */
     int static_meta;        /* 1: rows/index lists are not written by the preceding kernel, so the
                                gather metadata may be read before the programmatic-launch wait */
+    int m_halo;             /* CONV with rows + d_rows: 1 = the GEMM rows are runs of horizontally
+                               adjacent pixels, each run framed by its left / right neighbour pixel
+                               (or -1 at the image border) as rows with d_rows = -1 (not stored); the
+                               persistent kernel then stages each channel block once per kernel row
+                               (dy) and reads the three dx taps as 1-row shifts (fis_gemm_halo.cu) */
 } fis_gemm_args;
 
 int fis_gemm(const fis_gemm_args* args, void* stream);
 /* which kernel fis_gemm picks for these arguments: 0 SIMT, 1 per-op tcgen05 (split-K clusters),
- * 2 persistent large-M tcgen05 (TMA / gather4 staging), 3 per-op tcgen05 3xTF32; host-only */
+ * 2 persistent large-M tcgen05 (TMA / gather4 staging), 3 per-op tcgen05 3xTF32, 4 halo-staged
+ * persistent gather conv (m_halo); host-only */
 int fis_gemm_kernel_kind(const fis_gemm_args* a);
 /* number of persistent-kernel launches so far (diagnostics / tests) */
 long long fis_gemm_big_launch_count(void);

@@ -43,7 +43,8 @@ class GemmArgs(C.Structure):
                 ("beta", C.c_void_p), ("groups", C.c_int), ("eps", C.c_float), ("pre2", Ref), ("lat", Ref),
                 ("step_scale", C.c_float), ("res", Ref), ("d", Ref), ("d_trans", C.c_int), ("n_split", C.c_int), ("d2", Ref), ("d2_trans", C.c_int),
                 ("d_rows", C.c_void_p), ("splits", C.c_int), ("ws", C.c_void_p), ("ws_floats", C.c_longlong), ("counters", C.c_void_p),
-                ("step", C.c_void_p), ("impl", C.c_int), ("static_meta", C.c_int)]
+                ("step", C.c_void_p), ("impl", C.c_int), ("static_meta", C.c_int),
+                ("m_halo", C.c_int)]
 
 
 class GnStatsArgs(C.Structure):

@@ -8,6 +8,8 @@ int fis_gemm_tc_choose_splits(int m, int n, int k);
 int fis_gemm_tf32_supported(const fis_gemm_args* a);
 int fis_gemm_tf32_choose_splits(int m, int n, int k);
 int fis_gemm_tf32_launch(const fis_gemm_args* a, cudaStream_t stream);
+int fis_gemm_halo_ok(const fis_gemm_args* a);
+int fis_gemm_halo_launch(const fis_gemm_args* a, cudaStream_t stream);
 int fis_gemm_big_eligible(const fis_gemm_args* a);
 int fis_gemm_big_launch(const fis_gemm_args* a, cudaStream_t stream);
 
@@ -76,9 +78,11 @@ static int fis_choose_splits(const fis_gemm_args* a, bool tc) {
 }
 
 // Which kernel fis_gemm would run for these arguments: 0 SIMT, 1 per-op tcgen05, 2 persistent
-// large-M tcgen05 (csrc/fis_gemm_big.cu), 3 per-op tcgen05 3xTF32 (fp32 operands). Host-only query (no launch).
+// large-M tcgen05 (csrc/fis_gemm_big.cu), 3 per-op tcgen05 3xTF32 (fp32 operands), 4 halo-staged
+// persistent gather conv (csrc/fis_gemm_halo.cu). Host-only query (no launch).
 int fis_gemm_kernel_kind(const fis_gemm_args* a) {
     if (a->impl == 3) return fis_gemm_tf32_supported(a) ? 3 : 0;
+    if (a->impl == 0 && fis_gemm_halo_ok(a)) return 4;
     const bool tc = a->impl == 2 || (a->impl == 0 && fis_gemm_tc_supported(a));
     if (!tc) return 0;
     return a->impl == 0 && fis_gemm_big_eligible(a) ? 2 : 1;
@@ -99,6 +103,11 @@ int fis_gemm(const fis_gemm_args* a, void* stream) {
     if (a->epi == FIS_EPI_GN_SILU && (a->groups <= 0 || a->n % a->groups || !a->gn_mean.ptr || !a->gn_var.ptr))
         return a->gn_mean.ptr ? FIS_ERR_SHAPE : FIS_ERR_CACHE_MISS;
     const bool tc = a->impl == 2 || (a->impl == 0 && fis_gemm_tc_supported(a));
+    // halo-mode gathered convs of the stacked step: staged once per kernel row (fis_gemm_halo.cu)
+    if (a->impl == 0 && fis_gemm_halo_ok(a)) {
+        const int rc = fis_gemm_halo_launch(a, (cudaStream_t)stream);
+        if (rc != FIS_ERR_UNSUPPORTED) return rc;
+    }
     // large M (stacked requests): persistent tcgen05 kernel with TMA weights (fis_gemm_big.cu)
     if (tc && a->impl == 0 && fis_gemm_big_eligible(a)) {
         const int rc = fis_gemm_big_launch(a, (cudaStream_t)stream);

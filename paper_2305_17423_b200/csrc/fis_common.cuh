@@ -145,6 +145,7 @@ FIS_DEV void epilogue_store(const fis_gemm_args& a, const EpiCtx& e, int r, int 
     float v = acc * a.alpha;
     if (a.bias) v = __fadd_rn(v, __ldg(a.bias + n));
     const int orow = a.d_rows ? __ldg(a.d_rows + r) : r;
+    if (orow < 0) return;  // framing row of a halo-mode conv
     if (e.pre) store_elem(e.pre, a.pre.dtype, (long long)orow * a.pre.ld + n, v);
     if (e.bias2) v = __fadd_rn(v, load_elem(e.bias2, a.bias2.dtype, n));
     if (a.epi == FIS_EPI_GN_SILU) {

@@ -87,7 +87,8 @@ __global__ void __launch_bounds__(STHREADS) gemm_simt_kernel(const fis_gemm_args
             const int row = lr + 16 * i;
             const int r = m0 + row;
             float v = 0.f;
-            if (r < a.m && k < a.k) v = gather_a(a, t, f0, c0p, f1, c1p, abase, r, k, rowp[row], rowy[row], rowx[row]);
+            if (r < a.m && k < a.k && rowp[row] >= 0)  // rowp < 0: framing row at an image border
+                v = gather_a(a, t, f0, c0p, f1, c1p, abase, r, k, rowp[row], rowy[row], rowx[row]);
             As[lk][row] = v;
             const int n = n0 + row;
             float bv = 0.f;

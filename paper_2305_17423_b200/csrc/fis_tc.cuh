@@ -137,6 +137,7 @@ __device__ __forceinline__ void row_epilogue(const fis_gemm_args& a, const EpiCt
     const int nvalid = min(16, a.n - n);
     if (nvalid <= 0) return;
     const int orow = a.d_rows ? __ldg(a.d_rows + r) : r;
+    if (orow < 0) return;  // a framing row of a halo-mode conv: computed, not stored
 #pragma unroll
     for (int j = 0; j < 16; j++) v[j] = __fadd_rn(v[j] * a.alpha, tb.bias[c0 + j]);
     if (e.pre) store_row16(e.pre, a.pre.dtype, (long long)orow * a.pre.ld + n, nvalid, v);
@@ -200,6 +201,11 @@ constexpr int SEL_ZERO = INT_MIN;
 // >= 0 fresh row (or full-map pixel), <= -2 cache pixel (-2 - q), SEL_ZERO = zero padding.
 __device__ __forceinline__ void build_sel(const fis_gemm_args& a, int p, int seg, int* out9) {
     const fis_src& s = a.src[seg];
+    if (p < 0) {  // framing row at the image border (halo-mode rows): zeros
+#pragma unroll
+        for (int tap = 0; tap < 9; tap++) out9[tap] = SEL_ZERO;
+        return;
+    }
     // pixels of several stacked images (batched requests): image = p / (out_h * out_w); taps never
     // cross an image border; the source pixel is offset by the image's h * w source pixels
     const int ipx = a.out_h * a.out_w;

@@ -210,7 +210,7 @@ class Launcher:
 
     def gemm(self, m, n, k, *, a=None, rows=None, srcs=None, out_hw=None, b: DRef, d: DRef, alpha=1.0, bias=None,
              bias2=None, pre=None, epi=L.EPI_NONE, gn=None, lat=None, res=None, d_trans=False, splits=None,
-             n_split=0, d2=None, d2_trans=False, b_static=False):
+             n_split=0, d2=None, d2_trans=False, b_static=False, d_rows=None, m_halo=False, log_level=None):
         """b_static: B is not produced inside the step (weights, per-edit text K/V), so the step VM
         may stage it before the previous op completes."""
         if m == 0:
@@ -227,6 +227,8 @@ class Launcher:
             g.a_mode = L.A_ROWS
             g.a = a.ref()
         g.rows = L.ptr(rows)
+        g.d_rows = L.ptr(d_rows)
+        g.m_halo = 1 if m_halo else 0
         g.b = b.ref()
         g.alpha = alpha
         g.bias = L.ptr(bias)
@@ -254,7 +256,8 @@ class Launcher:
         g.static_meta = 1 if self.static_meta else 0
         self.last_gemm = g  # inspected by tests (fis_gemm_kernel_kind)
         self._call("fis_gemm", g, b_static)
-        self._count("fis_gemm", m=m, n=n, k=k, gathered=rows is not None and srcs is not None, conv=srcs is not None)
+        self._count("fis_gemm", m=m, n=n, k=k, gathered=rows is not None and srcs is not None, conv=srcs is not None,
+                    level=log_level, halo=bool(m_halo))
 
     def softmax(self, rows, cols, pad_cols, s: DRef, scale, p: DRef, map_: DRef | None = None, cached=None,
                 verbatim=False, pairs=None):
@@ -618,8 +621,20 @@ class Engine(Launcher):
         b, bias, cin = self.W.conv[lid]
         rows, m = plan.rows(level)
         srcs = [self.src(fv, up) for fv, up in inputs]
+        # halo-mode epilogues: bias (+ time bias) or the out conv's step update (no GN, no recording)
+        plain = all(v is None or k_ in ("epi", "lat", "bias2") for k_, v in kw.items()) and \
+            kw.get("epi", L.EPI_NONE) in (L.EPI_NONE, L.EPI_STEP)
+        halo = plan.halo_rows(level) if plain and self.act == torch.bfloat16 else None
+        if halo is not None and all(fv.c % 64 == 0 for fv, _ in inputs):
+            # stacked sparse level: rows as framed runs of adjacent pixels, staged once per kernel row
+            # (csrc/fis_gemm_halo.cu); framing rows are computed but not stored (d_rows = -1)
+            pix, outi, mh = halo
+            self.gemm(mh, b.shape[0], b.shape[1], rows=pix, srcs=srcs, out_hw=self.grid(level), b=DRef(b), d=out,
+                      bias=bias, b_static=True, d_rows=outi, m_halo=True, log_level=level,
+                      **{k_: v for k_, v in kw.items() if v is not None})
+            return
         self.gemm(m, b.shape[0], b.shape[1], rows=rows, srcs=srcs, out_hw=self.grid(level), b=DRef(b), d=out,
-                  bias=bias, b_static=True, **kw)
+                  bias=bias, b_static=True, log_level=level, **kw)
 
     def _block(self, plan, blk, x: FeatVal, fo):
         """conv -> GN -> SiLU -> +self-attn -> +cross-attn (unet.py:452-458)."""
@@ -631,7 +646,7 @@ class Engine(Launcher):
         nl = blk["norm"]
         if plan.batch > 1:
             # stacked requests: GN statistics per image, so the norm runs after the conv
-            co = DRef(self.scratch(f"co{tag}", (cap, c)))
+            co = DRef(self.scratch(f"co{tag}", (cap, c), zero=True))  # padding rows stay finite (halo convs)
             self._conv(plan, blk["conv"], [(x, False)], co, level)
             mean, var = plan.stats(nl)
             if plan.sparse(level):  # cached statistics of each row's request
@@ -769,6 +784,10 @@ class StepPlan:
     def rows(self, level):
         return None, self.eng.cap(level)
 
+    def halo_rows(self, level):
+        """(pixel per GEMM row, output row or -1, rows) of a halo-mode conv at this level, or None."""
+        return None
+
     def latent_in(self) -> FeatVal:
         return FeatVal(slab(self.latents, prev=True), 0, self.eng.config.latent_channels)
 
@@ -843,7 +862,9 @@ class SparsePlan(StepPlan):
 
     def out_buf(self, f) -> DRef:
         if self.sparse(f.level):
-            return DRef(self.eng.scratch(f"sfeat{f.key}", (self.eng.cap(f.level), f.channels)))
+            # zeroed once: rows that pad each stacked request's run are never written by halo-mode
+            # convs and must stay finite (attention multiplies them by P = 0)
+            return DRef(self.eng.scratch(f"sfeat{f.key}", (self.eng.cap(f.level), f.channels), zero=True))
         return DRef(self.eng.scratch(f"feat{f.key}", (self.eng.cap(f.level), f.channels)))
 
     def value(self, f) -> FeatVal:
@@ -873,8 +894,9 @@ class BatchedSparsePlan(SparsePlan):
     """
 
     def __init__(self, eng: Engine, kv, arena: Arena, lists, lat_rows: torch.Tensor, qsegs, kseg, row_img,
-                 max_keys: int = 256):
+                 max_keys: int = 256, halo=None):
         super().__init__(eng, kv, arena, lists, lat_rows)
+        self._halo = halo or {}  # gated level -> (pixel per GEMM row, output row / -1, rows) (halo_lists)
         self._max_keys = max_keys  # longest prompt (text keys of one request)
         self.batch = arena.batch
         self._qsegs = qsegs      # level -> (int32 [2R] device, R, max rows per request)
@@ -884,6 +906,9 @@ class BatchedSparsePlan(SparsePlan):
     def segments(self, level):
         return self._qsegs[level]
 
+    def halo_rows(self, level):
+        return self._halo.get(level) if self.sparse(level) else None
+
     def key_segments(self):
         return self._kseg
 
@@ -892,3 +917,33 @@ class BatchedSparsePlan(SparsePlan):
 
     def row_img(self, level):
         return self._row_img[level]
+
+
+def halo_lists(pixels: np.ndarray, out_rows: np.ndarray, h: int, w: int):
+    """GEMM rows of a halo-mode conv (fis_gemm_args.m_halo): the active pixels (stacked ids
+    img * h * w + y * w + x, row-major per image) grouped into runs of horizontally adjacent
+    pixels, each run framed by its left / right neighbour (-1 at the image border) as a row that
+    is computed but not stored. Returns (pixel per row, output row per row or -1)."""
+    pixels = np.asarray(pixels, np.int64)
+    out_rows = np.asarray(out_rows, np.int64)
+    if pixels.size == 0:
+        return np.zeros(0, np.int32), np.zeros(0, np.int32)
+    x = pixels % w
+    brk = np.ones(pixels.size, bool)
+    brk[1:] = (pixels[1:] != pixels[:-1] + 1) | (x[1:] == 0)
+    starts = np.flatnonzero(brk)
+    ends = np.append(starts[1:], pixels.size) - 1
+    n_runs = starts.size
+    total = pixels.size + 2 * n_runs
+    pix = np.empty(total, np.int64)
+    out = np.full(total, -1, np.int64)
+    # position of each pixel in the framed sequence: its index + 2 * (run ordinal) + 1
+    run_id = np.cumsum(brk) - 1
+    pos = np.arange(pixels.size) + 2 * run_id + 1
+    pix[pos] = pixels
+    out[pos] = out_rows
+    lpos = starts + 2 * np.arange(n_runs)
+    rpos = ends + 2 * np.arange(n_runs) + 2
+    pix[lpos] = np.where(x[starts] > 0, pixels[starts] - 1, -1)
+    pix[rpos] = np.where(x[ends] < w - 1, pixels[ends] + 1, -1)
+    return pix.astype(np.int32), out.astype(np.int32)

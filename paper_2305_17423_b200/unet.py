@@ -24,7 +24,7 @@ import torch
 
 from . import _lib as L
 from .cache import CacheStore, Role
-from .engine import Arena, BatchedSparsePlan, DRef, Engine, FeatVal, SparsePlan, StepPlan, _pad, slab
+from .engine import Arena, BatchedSparsePlan, DRef, Engine, FeatVal, SparsePlan, StepPlan, _pad, halo_lists, slab
 from .errors import CacheMissError, ConfigError, ContractViolation
 from .masks import BinaryMask, DevicePlan, run_detect
 from .model import (LayerInfo, UNetConfig, build_registry, embed_ids, initial_latent_np, lcs_pairs,
@@ -649,7 +649,25 @@ class BatchedEditPlan:
             lid0 = next(iter(kvs[0]))
             max_keys = max(kv_[lid0][0].shape[0] for kv_ in kvs)
         self.kv = kv
-        self.plan = BatchedSparsePlan(eng, kv, stacked, lists, self.lat_rows, qsegs, kseg, row_img, max_keys)
+        # halo-mode GEMM rows of the gated levels' convs (framed runs of adjacent pixels; the rows'
+        # outputs land at each request's compact row positions, engine.halo_lists)
+        halo = {}
+        for l in lists:
+            hw = eng.hw(l)
+            hl, wl = eng.grid(l)
+            px_parts, out_parts, start = [], [], 0
+            for r, dp in enumerate(self.dps):
+                n = dp.n_active[l]
+                px_parts.append(dp.rows[l][:n].long() + r * hw)
+                out_parts.append(torch.arange(start, start + n, device=dev))
+                start += _pad(n)
+            if start == 0:
+                continue
+            pix, outi = halo_lists(torch.cat(px_parts).cpu().numpy(), torch.cat(out_parts).cpu().numpy(), hl, wl)
+            halo[l] = (torch.from_numpy(pix).to(dev), torch.from_numpy(outi).to(dev), int(pix.size))
+        self.halo = halo
+        self.plan = BatchedSparsePlan(eng, kv, stacked, lists, self.lat_rows, qsegs, kseg, row_img, max_keys,
+                                      halo=halo)
 
     def final_latents(self, eng: Engine, stacked: Arena) -> torch.Tensor:
         """[R * hw, Cl] f32: fresh rows where masked, the cached generation elsewhere."""
