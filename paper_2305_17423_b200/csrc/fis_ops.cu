@@ -544,9 +544,10 @@ extern "C" int fis_gn(const fis_gn_apply_args* a, void* stream) {
     if (const int vw = gn_vec(a)) {
         fis_gn_apply_args ap = *a;
         ap.img_rows = hw;
-        // a cluster of 8 CTAs per (group, image) from 256 pixels up (r02 C2 dense step: L0 GN 78 -> 22 us,
-        // L1 49 -> 16 us); smaller maps one CTA per group (no cluster launch)
-        const int cl = hw >= 256 ? 8 : 1;
+        // a cluster of 8 CTAs per (group, image) when the (group, image) CTAs alone would leave most SMs
+        // idle and the maps are large (r02 C2 dense step: L0 GN 78 -> 22 us, L1 49 -> 16 us); stacked
+        // requests already give thousands of CTAs: one per (group, image), no cluster
+        const int cl = hw >= 256 && (long long)a->groups * n_img < 148 ? 8 : 1;
         const dim3 grid(a->groups * cl, n_img);
         cudaError_t e;
         if (cl > 1)
