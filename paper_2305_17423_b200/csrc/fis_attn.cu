@@ -32,14 +32,22 @@ constexpr int STAGES = 4;
 constexpr int A_BYTES = 128 * 64 * 2;            // Q chunk (K chunk at +A_BYTES)
 constexpr int STAGE = 2 * A_BYTES;               // = V^T chunk bytes at dvs = 256
 constexpr int P_BYTES = 2 * 128 * 64 * 2;        // P tile: 128 rows x 128 keys, two 64-key SW128 chunks
-constexpr int SMEM = STAGES * STAGE + 2 * P_BYTES + 1024 + 256 + 1024;  // + key-split statistics exchange
+// d-split receive buffer (P_DSPLIT: peers' fp32 partial-S row slices), starting at P tile 1
+constexpr int RX_EXTRA = 24 * 1024;
+constexpr int SMEM = STAGES * STAGE + 2 * P_BYTES + RX_EXTRA + 1024 + 256 + 1024;  // + key-split statistics exchange
 constexpr uint32_t O_COL = 256;                  // TMEM: S buffers at 0 / 128, O at 256
+constexpr int EPI_LD = 256 + 4;                  // O staging row pitch (floats; spans the stages + P tiles)
 // P sharing across the value slices of a query tile (segments of <= 256 keys): a P_OUT launch
 // (slice 0 only) computes S, the softmax and writes P (bf16, [row][256]) to scratch; the P_IN
 // launch (every slice) TMA-loads those P tiles and runs only P.V + the epilogue
 // P_OUT_KS: P_OUT for two-block key runs split over a 2-CTA cluster (CTA = one key block); the
 // row max / sum of the two blocks are exchanged through distributed shared memory
-constexpr int P_NONE = 0, P_OUT = 1, P_IN = 2, P_OUT_KS = 3;
+// P_DSPLIT (batch 1, <= 128 keys): the value-slice CTAs of a query tile form a cluster and split the
+// S reduction (the head dim d) between them instead of each recomputing all of S: CTA z computes
+// the partial S over its d chunks, pushes the partial row slices to their owners (DSMEM bulk
+// copies), owners sum the partials in cluster-rank order, run the softmax of their rows and push
+// the bf16 P rows into every CTA's P tile; each CTA then runs P.V for its value slice.
+constexpr int P_NONE = 0, P_OUT = 1, P_IN = 2, P_OUT_KS = 3, P_DSPLIT = 4;
 
 FIS_DEV void cluster_sync_all() {
     asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
@@ -94,19 +102,22 @@ __global__ void __launch_bounds__(THREADS, 1)
     attn_kernel(const fis_attn_args a, const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
                 const __grid_constant__ CUtensorMap tv, const __grid_constant__ CUtensorMap tp, int dvs, int pmode_in) {
     const bool ks = pmode_in == P_OUT_KS;
-    const int pmode = ks ? P_OUT : pmode_in;
+    const bool dsp = pmode_in == P_DSPLIT;
+    const int pmode = ks ? P_OUT : (dsp ? P_NONE : pmode_in);
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     unsigned char* ptile = smem + STAGES * STAGE;
-    uint64_t* full = (uint64_t*)(ptile + 2 * P_BYTES);
+    float* rxbuf = (float*)(ptile + P_BYTES);  // P_DSPLIT receive slots (P tile 1 + RX_EXTRA)
+    uint64_t* full = (uint64_t*)(ptile + 2 * P_BYTES + RX_EXTRA);
     uint64_t* empty = full + STAGES;
     uint64_t* s_ready = empty + STAGES;  // [2]
     uint64_t* s_free = s_ready + 2;      // [2]
     uint64_t* p_ready = s_free + 2;      // [2]
     uint64_t* p_free = p_ready + 2;      // [2]
     uint64_t* o_done = p_free + 2;
-    uint32_t* tmem_slot = (uint32_t*)(o_done + 1);
-    float2* xst = (float2*)(ptile + 2 * P_BYTES + 256);  // [128] key-split (max, sum) exchange
+    uint64_t* rx_bar = o_done + 1;       // P_DSPLIT: peers' partial row slices landed
+    uint32_t* tmem_slot = (uint32_t*)(rx_bar + 1);
+    float2* xst = (float2*)(ptile + 2 * P_BYTES + RX_EXTRA + 256);  // [128] key-split (max, sum) exchange
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int ls = ltr_begin(2 + pmode_in * 16);  // thread 0 of CTA (0,0,0) only
@@ -139,6 +150,11 @@ __global__ void __launch_bounds__(THREADS, 1)
     const bool resident = nkb == 2;
     const int first_pass = single ? 2 : 1;
     const int pw = ((a.max_seg_k + 127) / 128) * 128;  // P scratch row width (P sharing)
+    // P_DSPLIT: cluster rank = value slice; this CTA's d chunks [kc0, kc1) and owned rows [rbeg, rend)
+    const int cs = dsp ? (int)gridDim.x : 1, rank = (int)blockIdx.x;
+    const int kc0 = dsp ? rank * dch / cs : 0, kc1 = dsp ? (rank + 1) * dch / cs : dch;
+    const int rp = (128 + cs - 1) / cs;
+    const int rbeg = min(128, rank * rp), rend = min(128, rbeg + rp);
     if (tid == 0) {
         for (int i = 0; i < STAGES; i++) {
             mbar_init(full + i, 1);
@@ -147,11 +163,16 @@ __global__ void __launch_bounds__(THREADS, 1)
         for (int b = 0; b < 2; b++) {
             mbar_init(s_ready + b, 1);
             mbar_init(s_free + b, 128);
-            mbar_init(p_ready + b, pmode == P_IN ? 1 : 128);
+            mbar_init(p_ready + b, (pmode == P_IN || dsp) ? 1 : 128);
             mbar_init(p_free + b, 1);
         }
         mbar_init(o_done, 1);
+        mbar_init(rx_bar, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        if (dsp && rend > rbeg)  // incoming: cs - 1 partial slices of this CTA's rows
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(rx_bar)),
+                         "r"((uint32_t)((cs - 1) * (rend - rbeg) * 512))
+                         : "memory");
     }
     if (warp == TMA_WARP && lane == 0) {
         asm volatile("prefetch.tensormap [%0];" ::"l"(&tq) : "memory");
@@ -166,6 +187,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    if (dsp) asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");  // barriers initialised
     const int t = cur_step(a.step);  // host-written before the step: safe to read before the wait
     ltr(ls, 1);
     if (warp == TMA_WARP && lane == 0 && a.nseg == 0 && !idle) {
@@ -177,9 +199,9 @@ __global__ void __launch_bounds__(THREADS, 1)
         // row count than the queries, or V^T narrower than the query count)
         const bool self_kv = a.n_keys == a.m;
         if (!self_kv) {
-            const int nkb2 = (n_keys + 127) / 128, dch2 = a.d / 64;
+            const int nkb2 = (n_keys + 127) / 128;
             for (int j = 0; j < nkb2; j++)
-                for (int kc = 0; kc < dch2; kc++) tma_prefetch2d(&tk, kc * 64, k_beg + j * 128);
+                for (int kc = kc0; kc < kc1; kc++) tma_prefetch2d(&tk, kc * 64, k_beg + j * 128);
             for (int j = 0; j < nkb2; j++)
                 for (int h = 0; h < 2; h++) tma_prefetch2d(&tv, k_beg + j * 128 + h * 64, c0);
         }
@@ -217,7 +239,16 @@ __global__ void __launch_bounds__(THREADS, 1)
                     tma2d(sbase + st * STAGE, &tv, k_beg + j * 128 + h * 64, c0, full + st);
                 }
             };
-            if (pmode == P_IN) {  // P tiles of this query tile from the scratch (written by the P_OUT launch)
+            if (dsp) {  // this CTA's d chunks of S, then its V^T slice into stages 0-1 (part lives in 2-3)
+                for (int kc = kc0; kc < kc1; kc++) {
+                    const int st = stage(2 * A_BYTES);
+                    const uint32_t sa = sbase + st * STAGE;
+                    tma2d(sa, &tq, kc * 64, m0, full + st);
+                    tma2d(sa + A_BYTES, &tk, kc * 64, k_beg, full + st);
+                }
+                it = STAGES;
+                load_v(0);
+            } else if (pmode == P_IN) {  // P tiles of this query tile from the scratch (written by the P_OUT launch)
                 for (int j = 0; j < nkb; j++) {
                     const int pb = j & 1;
                     if (j >= 2) mbar_wait(p_free + pb, ((j >> 1) & 1) ^ 1);  // P.V_{j-2} done with the buffer
@@ -295,7 +326,26 @@ __global__ void __launch_bounds__(THREADS, 1)
                 it++;
             }
         };
-        if (pmode == P_IN) {
+        if (dsp) {
+            for (int kc = kc0; kc < kc1; kc++) {
+                const int st = it % STAGES;
+                mbar_wait(full + st, (it / STAGES) & 1);
+                tc_fence_after();
+                if (lane == 0) {
+                    const uint32_t sa = sbase + st * STAGE, sbb = sa + A_BYTES;
+#pragma unroll
+                    for (int kk = 0; kk < 4; kk++)
+                        mma_bf16(tmem, sw128_desc(sa + kk * 32), sw128_desc(sbb + kk * 32), id_s,
+                                 (kc != kc0 || kk) ? 1u : 0u);
+                    mma_commit(empty + st);
+                    if (kc == kc1 - 1) mma_commit(s_ready);
+                }
+                __syncwarp();
+                it++;
+            }
+            it = STAGES;
+            mma_pv(0);
+        } else if (pmode == P_IN) {
             for (int j = 0; j < nkb; j++) mma_pv(j);
         } else if (pmode == P_OUT) {
             if (!(resident || single))
@@ -323,7 +373,127 @@ __global__ void __launch_bounds__(THREADS, 1)
         float mrow = -INFINITY, lrow = 0.f;
         int sb = 0;
         float v[32];
-        for (int pass = first_pass; pass <= 2 && pmode != P_IN; pass++) {
+        if (dsp) {
+            // 1. partial S (this CTA's d chunks) -> part: fp32 [128][128] in stages 2-3, 16-byte units
+            //    XOR-swizzled by row (conflict-free row-per-thread writes; rows stay contiguous)
+            unsigned char* part = smem + 2 * STAGE;
+            mbar_wait(s_ready, 0);
+            ltr(ls, 3);
+            tc_fence_after();
+#pragma unroll 1
+            for (int cb = 0; cb < 128; cb += 32) {
+                tmem_ld32(tmem + lane_off + cb, v);
+#pragma unroll
+                for (int q = 0; q < 8; q++) {
+                    const int u = (cb >> 2) + q;
+                    *(float4*)(part + lr * 512 + ((u ^ (lr & 7)) << 4)) = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+                }
+            }
+            fence_async_smem();
+            asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");  // peers' barriers initialised
+            asm volatile("bar.sync 3, 128;" ::: "memory");
+            const uint32_t part_s = smem_u32(part);
+            if (tid == 0) {  // 2. each peer's row slice of the partial -> its receive slot for this rank
+                for (int p = 0; p < cs; p++) {
+                    if (p == rank) continue;
+                    const int pb = min(128, p * rp), pe = min(128, pb + rp);
+                    if (pe <= pb) continue;
+                    const int slot = rank < p ? rank : rank - 1;
+                    uint32_t dst, bar;
+                    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(dst) : "r"(smem_u32(rxbuf) + (uint32_t)(slot * rp * 512)), "r"(p));
+                    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(bar) : "r"(smem_u32(rx_bar)), "r"(p));
+                    asm volatile(
+                        "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+                        "r"(part_s + (uint32_t)(pb * 512)), "r"((uint32_t)((pe - pb) * 512)), "r"(bar)
+                        : "memory");
+                }
+                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            }
+            // 3. owned rows: sum the partials in rank order, softmax, bf16 P rows -> the local P tile.
+            //    4 threads per row (32 keys each), rows i and i + 32 when a CTA owns 64 rows
+            const int own = rend - rbeg;
+            if (own > 0) mbar_wait(rx_bar, 0);
+            ltr(ls, 5);
+            const int seg = tid & 3, kbase = seg * 32, lim = n_keys - kbase;
+#pragma unroll 1
+            for (int i = tid >> 2; i < ((own + 31) & ~31); i += 32) {
+                const bool act = i < own;
+                const int r = rbeg + i;
+                float x[32];
+#pragma unroll
+                for (int q = 0; q < 32; q++) x[q] = 0.f;
+                if (act) {
+                    for (int z = 0; z < cs; z++) {
+                        const unsigned char* src = z == rank ? part + r * 512
+                                                             : (const unsigned char*)rxbuf + (z < rank ? z : z - 1) * rp * 512 + i * 512;
+#pragma unroll
+                        for (int q = 0; q < 8; q++) {
+                            const int u = seg * 8 + q;
+                            const float4 f = *(const float4*)(src + ((u ^ (r & 7)) << 4));
+                            x[4 * q] += f.x; x[4 * q + 1] += f.y; x[4 * q + 2] += f.z; x[4 * q + 3] += f.w;
+                        }
+                    }
+                }
+                float cm = -INFINITY;
+#pragma unroll
+                for (int q = 0; q < 32; q++)
+                    if (q < lim) cm = fmaxf(cm, x[q]);
+                cm = fmaxf(cm, __shfl_xor_sync(0xffffffffu, cm, 1));
+                cm = fmaxf(cm, __shfl_xor_sync(0xffffffffu, cm, 2));
+                const float mn = cm * sl;
+                float add = 0.f;
+#pragma unroll
+                for (int q = 0; q < 32; q++)
+                    if (q < lim) add += ex2(fmaf(x[q], sl, -mn));
+                add += __shfl_xor_sync(0xffffffffu, add, 1);
+                add += __shfl_xor_sync(0xffffffffu, add, 2);
+                const float off = mn + __log2f(add);
+                if (act) {
+                    unsigned char* pt = ptile + (kbase >> 6) * (128 * 128);
+#pragma unroll
+                    for (int u = 0; u < 4; u++) {
+                        uint4 pk;
+                        __nv_bfloat162* h = (__nv_bfloat162*)&pk;
+#pragma unroll
+                        for (int e2 = 0; e2 < 4; e2++) {
+                            const int q0 = 8 * u + 2 * e2;
+                            const float p0 = q0 < lim ? ex2(fmaf(x[q0], sl, -off)) : 0.f;
+                            const float p1 = q0 + 1 < lim ? ex2(fmaf(x[q0 + 1], sl, -off)) : 0.f;
+                            h[e2] = __floats2bfloat162_rn(p0, p1);
+                        }
+                        *(uint4*)(pt + sw128_off(r, ((kbase & 63) >> 3) + u)) = pk;
+                    }
+                }
+            }
+            fence_async_smem();
+            asm volatile("bar.sync 3, 128;" ::: "memory");
+            if (tid == 0) {  // 4. the owned P rows -> every peer's P tile; then expect the peers' rows
+                const uint32_t pt_s = smem_u32(ptile);
+                if (own > 0)
+                    for (int p = 0; p < cs; p++) {
+                        if (p == rank) continue;
+                        uint32_t bar;
+                        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(bar) : "r"(smem_u32(p_ready)), "r"(p));
+                        for (int h = 0; h < 2; h++) {
+                            const uint32_t off = pt_s + (uint32_t)(h * 128 * 128 + rbeg * 128);
+                            uint32_t dst;
+                            asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(dst) : "r"(off), "r"(p));
+                            asm volatile(
+                                "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+                                "r"(off), "r"((uint32_t)(own * 128)), "r"(bar)
+                                : "memory");
+                        }
+                    }
+                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(p_ready)),
+                             "r"((uint32_t)((128 - own) * 256))
+                             : "memory");
+                ltr(ls, 6);
+                // the outgoing copies have read part / P before the epilogue reuses the stages
+                asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+            }
+        }
+        for (int pass = first_pass; pass <= 2 && pmode != P_IN && !dsp; pass++) {
             if (resident) sb = 0;  // pass 2 re-reads the resident S blocks (their phases already completed)
             for (int j = 0; j < nkb; j++) {
                 const int b = sb & 1;
@@ -419,51 +589,96 @@ __global__ void __launch_bounds__(THREADS, 1)
                 sb++;
             }
         }
-        // epilogue: O row slice + residual -> out
+        // epilogue: stage the O row slice (fp32) in the idle pipeline stages; the stores run below
         if (pmode == P_OUT) goto done;
         mbar_wait(o_done, 0);
         ltr(ls, 4);
         tc_fence_after();
-        {
-            // stage the O row slice (fp32) in the idle pipeline stages, then the 128 softmax threads
-            // add the residual and store 16-column chunks columns-fastest (coalesced 16-byte runs)
-            // instead of one row per thread (whose residual loads serialised one L2 round trip per
-            // 32 columns)
-            constexpr int OLD = 256 + 4;  // staging row pitch (floats)
-            float* ost = (float*)smem;
+        if (dsp) asm volatile("bar.sync 3, 128;" ::: "memory");  // thread 0's outgoing copies done reading
+        float* ost = (float*)smem;
 #pragma unroll 1
-            for (int cb = 0; cb < dvs; cb += 32) {
-                tmem_ld32(tmem + lane_off + O_COL + cb, v);
+        for (int cb = 0; cb < dvs; cb += 32) {
+            tmem_ld32(tmem + lane_off + O_COL + cb, v);
 #pragma unroll
-                for (int q = 0; q < 8; q++)
-                    *(float4*)(ost + lr * OLD + cb + 4 * q) = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
-            }
-            asm volatile("bar.sync 2, 128;" ::: "memory");
-            char* ob = ref_base(a.out, t);
-            char* pbp = a.pre.ptr ? ref_base(a.pre, t) : nullptr;
-            const char* rb = a.res.ptr ? ref_base(a.res, t) : nullptr;
-            const int chunks = dvs / 16;
-            const int nrows = min(128, q_end - m0);
+            for (int q = 0; q < 8; q++)
+                *(float4*)(ost + lr * EPI_LD + cb + 4 * q) = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+        }
+    }
+    if (dsp && warp >= 4) asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+    if (pmode != P_OUT) {
+        // all six warps: residual + O -> out, 16-column chunks columns-fastest (coalesced 16-byte runs);
+        // each thread first issues the residual loads of EB chunks, then adds and stores them, so the
+        // L2 round trips overlap (one per chunk serialised ~0.5 us each: 16 chunks per thread at
+        // dvs = 256 made the epilogue ~9 us)
+        asm volatile("bar.sync 2, 192;" ::: "memory");
+        const float* ost = (const float*)smem;
+        char* ob = ref_base(a.out, t);
+        char* pbp = a.pre.ptr ? ref_base(a.pre, t) : nullptr;
+        const char* rb = a.res.ptr ? ref_base(a.res, t) : nullptr;
+        const bool fast = (!rb || (a.res.dtype == FIS_BF16 && (a.res.ld % 8) == 0 && (((uintptr_t)rb) & 15) == 0)) &&
+                          a.out.dtype == FIS_BF16 && (a.out.ld % 8) == 0 && (((uintptr_t)ob) & 15) == 0 && !pbp &&
+                          (a.dv % 16) == 0;
+        const int chunks = dvs / 16;
+        const int nrows = min(128, q_end - m0), total = nrows * chunks;
+        constexpr int EB = 6;
 #pragma unroll 1
-            for (int item = tid; item < nrows * chunks; item += 128) {
-                const int rr = item / chunks, cc = (item % chunks) * 16;
-                const int n = c0 + cc, row = m0 + rr;
-                const int nvalid = min(16, a.dv - n);
-                if (nvalid <= 0) continue;
-                float w[16];
+        for (int i0 = tid; i0 < total; i0 += THREADS * EB) {
+            if (fast) {
+                uint4 rr[EB][2];
 #pragma unroll
-                for (int q = 0; q < 4; q++) {
-                    const float4 f = *(const float4*)(ost + rr * OLD + cc + 4 * q);
-                    w[4 * q] = f.x; w[4 * q + 1] = f.y; w[4 * q + 2] = f.z; w[4 * q + 3] = f.w;
+                for (int e = 0; e < EB; e++) {
+                    const int item = i0 + e * THREADS;
+                    rr[e][0] = rr[e][1] = make_uint4(0u, 0u, 0u, 0u);
+                    if (rb && item < total) {
+                        const __nv_bfloat16* p = (const __nv_bfloat16*)rb +
+                                                 (long long)(m0 + item / chunks) * a.res.ld + c0 + (item % chunks) * 16;
+                        rr[e][0] = FIS_LD_U4(p);
+                        rr[e][1] = FIS_LD_U4(p + 8);
+                    }
                 }
-                if (pbp) store_row16(pbp, a.pre.dtype, (long long)row * a.pre.ld + n, nvalid, w);
-                if (rb) {
-                    float q[16];
-                    load_row16(rb, a.res.dtype, (long long)row * a.res.ld + n, nvalid, q);
 #pragma unroll
-                    for (int e2 = 0; e2 < 16; e2++) w[e2] = __fadd_rn(w[e2], q[e2]);
+                for (int e = 0; e < EB; e++) {
+                    const int item = i0 + e * THREADS;
+                    if (item >= total) break;
+                    const int rr_ = item / chunks, cc = (item % chunks) * 16;
+                    const float* src = ost + rr_ * EPI_LD + cc;
+                    const __nv_bfloat162* hr = (const __nv_bfloat162*)rr[e];
+                    uint4 o[2];
+                    __nv_bfloat162* ho = (__nv_bfloat162*)o;
+#pragma unroll
+                    for (int k4 = 0; k4 < 4; k4++) {
+                        const float4 f = *(const float4*)(src + 4 * k4);
+                        const float2 r0 = __bfloat1622float2(hr[2 * k4]), r1 = __bfloat1622float2(hr[2 * k4 + 1]);
+                        ho[2 * k4] = __floats2bfloat162_rn(__fadd_rn(f.x, r0.x), __fadd_rn(f.y, r0.y));
+                        ho[2 * k4 + 1] = __floats2bfloat162_rn(__fadd_rn(f.z, r1.x), __fadd_rn(f.w, r1.y));
+                    }
+                    uint4* dst = (uint4*)((__nv_bfloat16*)ob + (long long)(m0 + rr_) * a.out.ld + c0 + cc);
+                    dst[0] = o[0];
+                    dst[1] = o[1];
                 }
-                store_row16(ob, a.out.dtype, (long long)row * a.out.ld + n, nvalid, w);
+            } else {
+                for (int e = 0; e < EB; e++) {
+                    const int item = i0 + e * THREADS;
+                    if (item >= total) break;
+                    const int rr_ = item / chunks, cc = (item % chunks) * 16;
+                    const int n = c0 + cc, row = m0 + rr_;
+                    const int nvalid = min(16, a.dv - n);
+                    if (nvalid <= 0) continue;
+                    float w[16];
+#pragma unroll
+                    for (int q = 0; q < 4; q++) {
+                        const float4 f = *(const float4*)(ost + rr_ * EPI_LD + cc + 4 * q);
+                        w[4 * q] = f.x; w[4 * q + 1] = f.y; w[4 * q + 2] = f.z; w[4 * q + 3] = f.w;
+                    }
+                    if (pbp) store_row16(pbp, a.pre.dtype, (long long)row * a.pre.ld + n, nvalid, w);
+                    if (rb) {
+                        float q[16];
+                        load_row16(rb, a.res.dtype, (long long)row * a.res.ld + n, nvalid, q);
+#pragma unroll
+                        for (int e2 = 0; e2 < 16; e2++) w[e2] = __fadd_rn(w[e2], q[e2]);
+                    }
+                    store_row16(ob, a.out.dtype, (long long)row * a.out.ld + n, nvalid, w);
+                }
             }
         }
     }
@@ -575,6 +790,18 @@ static bool attn_share(const fis_attn_args* a, int dvs) {
     return a->max_seg_k <= 256 || ctas >= 2 * 148;
 }
 
+// d-split (P_DSPLIT) for this call? Batch-1 runs of <= 128 keys whose grid leaves the GPU mostly
+// idle: the cs = dv / dvs value-slice CTAs of a query tile share the S reduction (<= 4 d chunks
+// each) instead of each computing all of it.
+static bool attn_dsplit(const fis_attn_args* a, int dvs) {
+    static int off = getenv("FIS_ATTN_DSPLIT") && getenv("FIS_ATTN_DSPLIT")[0] == '0';
+    const int cs = a->dv / dvs, dch = a->d / 64;
+    if (off || a->nseg > 0 || a->n_keys > 128 || cs < 2 || cs > 8 || dch < cs || (dch + cs - 1) / cs > 4) return false;
+    const int rp = (128 + cs - 1) / cs;
+    if ((cs - 1) * rp * 512 > fis::attn::P_BYTES + fis::attn::RX_EXTRA) return false;
+    return (long long)cs * ((a->m + 127) / 128) < 148;
+}
+
 // Kernel launches one fis_attn call makes (1, or 2 when the value slices share P); 0 = unsupported.
 extern "C" int fis_attn_launches(const fis_attn_args* a) {
     const int dvs = attn_slice(a->dv);
@@ -643,6 +870,19 @@ extern "C" int fis_attn(const fis_attn_args* a, void* stream) {
         cfg.numAttrs = fis_pdl_enabled() ? 1 : 0;
     }
     cfg.gridDim = grid;
+    if (!share && attn_dsplit(a, dvs)) {  // the value slices of a query tile = one cluster
+        cudaLaunchAttribute at2[2];
+        at2[0] = attr[0];
+        at2[1].id = cudaLaunchAttributeClusterDimension;
+        at2[1].val.clusterDim.x = grid.x;
+        at2[1].val.clusterDim.y = 1;
+        at2[1].val.clusterDim.z = 1;
+        cfg.attrs = fis_pdl_enabled() ? at2 : at2 + 1;
+        cfg.numAttrs = fis_pdl_enabled() ? 2 : 1;
+        return cudaLaunchKernelEx(&cfg, fis::attn::attn_kernel, *a, tq, tk, tv, tp, dvs, (int)fis::attn::P_DSPLIT) ==
+                       cudaSuccess
+                   ? FIS_OK : FIS_ERR_LAUNCH;
+    }
     return cudaLaunchKernelEx(&cfg, fis::attn::attn_kernel, *a, tq, tk, tv, tp, dvs,
                               share ? (int)fis::attn::P_IN : (int)fis::attn::P_NONE) == cudaSuccess
                ? FIS_OK : FIS_ERR_LAUNCH;

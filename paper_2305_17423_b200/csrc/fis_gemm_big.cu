@@ -762,6 +762,11 @@ static int wide_bn(int n) {
     return 0;
 }
 
+// TMA staging of A for the per-op kernel (fis_gemm_tc.cu): 0 none, 1 contiguous rows, 2 dense conv
+int fis_tma_a_encode(const fis_gemm_args* a, CUtensorMap* ta, CUtensorMap* ta2) {
+    return choose_amode(a, ta, ta2);
+}
+
 static long long g_big_launched = 0;
 // persistent-kernel launches so far (tests check that fis_gemm did not fall back to the per-op kernel)
 extern "C" long long fis_gemm_big_launch_count(void) { return g_big_launched; }

@@ -22,6 +22,7 @@
 
 // weight tensor maps (cached per buffer), defined with the persistent GEMM
 const CUtensorMap* fis_weight_map(const void* base, long long n, long long k, long long ld, int box);
+int fis_tma_a_encode(const fis_gemm_args* a, CUtensorMap* ta, CUtensorMap* ta2);
 
 namespace fis {
 namespace tc {
@@ -83,6 +84,19 @@ __device__ __forceinline__ void tc_tma2d(uint32_t dst, const void* tmap, int c0,
         : "memory");
 }
 
+__device__ __forceinline__ void tc_tma4d(uint32_t dst, const void* tmap, int c0, int c1, int c2, int c3, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], "
+        "[%6];" ::"r"(dst),
+        "l"(tmap), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar))
+        : "memory");
+}
+
+// amode (A staging): 0 cp.async by the producer threads (gathered / select-on-read rows);
+// 1 TMA box {64 x 128} of contiguous rows; 2 dense 3x3 conv, one 4-D box per tap (TMA zero fill =
+// the conv padding). With TMA A, thread 0 alone feeds the pipeline (full barrier count 1).
+constexpr int AM_CPASYNC = 0, AM_ROWS = 1, AM_CONV = 2;
+
 // tma_b: the B tile {64 x BN} of each stage is one TMA load (thread 0, expect_tx on the stage's
 // full barrier) instead of BN rows of cp.async (weights stream faster; fewer producer instructions)
 __device__ __forceinline__ float tf32_big(float x) {
@@ -103,7 +117,8 @@ __device__ __forceinline__ void x3_split(unsigned char* small_tile, int part_byt
 
 template <int BN, bool X3>
 __global__ void __launch_bounds__(THREADS, 1)
-    gemm_tc_kernel(const fis_gemm_args a, const __grid_constant__ CUtensorMap tmb, int tma_b) {
+    gemm_tc_kernel(const fis_gemm_args a, const __grid_constant__ CUtensorMap tmb, int tma_b,
+                   const __grid_constant__ CUtensorMap tma0, const __grid_constant__ CUtensorMap tma1, int amode) {
     using SM = Smem<BN, X3>;
     constexpr int ES = X3 ? 4 : 2;             // operand element bytes
     constexpr int BKE = 128 / ES;              // K elements per K block (one 128-byte row)
@@ -133,7 +148,7 @@ __global__ void __launch_bounds__(THREADS, 1)
 
     if (tid == 0) {
         for (int s = 0; s < SM::STAGES; s++) {
-            mbar_init(full + s, PRODUCERS + (tma_b ? 1 : 0));
+            mbar_init(full + s, amode ? 1 : PRODUCERS + (tma_b ? 1 : 0));
             mbar_init(empty + s, 1);
         }
         mbar_init(done, 1);
@@ -173,9 +188,19 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int t = cur_step(a.step);
     const int ls = s_ltr;
     if (tid == 0) ltr(ls, 1);
+    // weights (no kernel writes them): the first stages' B tiles go straight into shared memory and
+    // the rest into L2 while the previous kernel still runs; with TMA A the stage's A bytes are
+    // expected here too (issued after the wait)
+    const int pre = tma_b ? min(nk, SM::STAGES) : 0;
+    if (tid == 0)
+        for (int i = 0; i < pre; i++) {
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(full + i)),
+                         "r"((uint32_t)(BN * 128 + (amode ? SM::A_BYTES : 0)))
+                         : "memory");
+            tc_tma2d(smem_u32(smem) + i * SM::STAGE + SM::A_BYTES, &tmb, (kb0 + i) * BKE, n0, full + i);
+        }
     if (tma_b && warp == MMA_WARP + 0 && lane == 0 && !a.b.step_stride) {
-        // weights: pull this CTA's B tiles into L2 while the previous kernel still runs
-        for (int i = 0; i < nk; i++) tma_prefetch2d(&tmb, (kb0 + i) * BKE, n0);
+        for (int i = pre; i < nk; i++) tma_prefetch2d(&tmb, (kb0 + i) * BKE, n0);
     }
     pdl_trigger();
     pdl_wait();  // everything above (barrier init, TMEM alloc, static metadata) overlaps the previous kernel
@@ -183,7 +208,38 @@ __global__ void __launch_bounds__(THREADS, 1)
     if (!a.static_meta) build_meta();
     if (tid == 0) trace(2);
 
-    if (warp < MMA_WARP) {
+    if (warp < MMA_WARP && amode) {
+        // ------------------------------------------------------------ TMA A (+ B) producer: thread 0
+        if (tid == 0) {
+            const uint32_t sbase = smem_u32(smem);
+            const int cin0 = a.nsrc > 0 ? a.src[0].c : 0, cin = cin0 + (a.nsrc > 1 ? a.src[1].c : 0);
+            const int ow = a.out_w, ohw = a.out_h * a.out_w;
+            const int img = amode == AM_CONV ? m0 / ohw : 0;
+            const int y0 = amode == AM_CONV && ohw >= BM ? (m0 - img * ohw) / ow : 0;
+            for (int i = 0; i < nk; i++) {
+                const int s = i % SM::STAGES;
+                const int k0 = (kb0 + i) * BKE;
+                const uint32_t sa = sbase + s * SM::STAGE;
+                if (i >= SM::STAGES) {
+                    mbar_wait(empty + s, ((i / SM::STAGES) & 1) ^ 1);
+                    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(full + s)),
+                                 "r"((uint32_t)(BN * 128 + SM::A_BYTES))
+                                 : "memory");
+                    tc_tma2d(sa + SM::A_BYTES, &tmb, k0, n0, full + s);
+                }
+                if (amode == AM_ROWS) {
+                    tc_tma2d(sa, &tma0, k0, m0, full + s);
+                } else {
+                    const int tap = k0 / cin;
+                    int c = k0 - tap * cin;
+                    const bool seg1 = c >= cin0;
+                    c -= seg1 ? cin0 : 0;
+                    tc_tma4d(sa, seg1 ? &tma1 : &tma0, c, tap % 3 - 1, y0 + tap / 3 - 1, img, full + s);
+                }
+                if (i == 0) trace(3);
+            }
+        }
+    } else if (warp < MMA_WARP) {
         // ------------------------------------------------------------ producers
         const char* abase = a.a.ptr ? ref_base(a.a, t) : nullptr;
         const char* f0 = a.nsrc > 0 && a.src[0].fresh.ptr ? ref_base(a.src[0].fresh, t) : nullptr;
@@ -241,7 +297,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                 cp_async16(sa + sw128_off(ar, j), ok ? (const void*)(src + j * 16) : (const void*)bbase, ok);
             }
             if (tma_b) {
-                if (tid == 0) {
+                if (tid == 0 && i >= SM::STAGES) {  // the first stages' B tiles were issued before the wait
                     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(full + s)),
                                  "r"((uint32_t)(BN * 128))
                                  : "memory");
@@ -582,10 +638,15 @@ int launch(const fis_gemm_args* a, cudaStream_t stream) {
     const CUtensorMap* tm = nullptr;
     if (!tma_off && a->b.dtype == FIS_BF16 && !a->b.step_stride && (a->b.ld % 8) == 0)
         tm = fis_weight_map(a->b.ptr, a->n, a->k, a->b.ld, BN);
-    CUtensorMap none;
+    CUtensorMap none, ta, ta2;
     std::memset(&none, 0, sizeof(none));
-    return cudaLaunchKernelEx(&cfg, gemm_tc_kernel<BN, X3>, *a, tm ? *tm : none, tm ? 1 : 0) == cudaSuccess ? FIS_OK
-                                                                                                      : FIS_ERR_LAUNCH;
+    std::memset(&ta, 0, sizeof(ta));
+    std::memset(&ta2, 0, sizeof(ta2));
+    static int tma_a_off = getenv("FIS_TC_TMA_A") && getenv("FIS_TC_TMA_A")[0] == '0';
+    const int amode = (!X3 && tm && !tma_a_off) ? fis_tma_a_encode(a, &ta, &ta2) : AM_CPASYNC;
+    return cudaLaunchKernelEx(&cfg, gemm_tc_kernel<BN, X3>, *a, tm ? *tm : none, tm ? 1 : 0, ta, ta2, amode) ==
+                   cudaSuccess
+               ? FIS_OK : FIS_ERR_LAUNCH;
 }
 
 // How many clusters of S CTAs (split-K) the device co-schedules for this kernel, S = 1..16
