@@ -268,11 +268,12 @@ def _op_log(eng, plan):
         eng.op_log = None
 
 
-def replay_kernels(runner, ops, T, reps=3):
+def replay_kernels(runner, ops, T, reps=9):
     """CUPTI kernel records of `reps` graph replays of the runner's captured step, mapped to ops.
 
-    Returns [(op dict, critical-path us, kernel name)] of the LAST replay (L2/TLB warm) or None
-    when the profiler sees a different kernel count than the op log."""
+    Returns [(op dict, critical-path us, kernel name)]: per op the MEDIAN over the replays after
+    the first (L2/TLB warm) of its critical-path time, or None when the profiler's kernel records
+    do not match the op log."""
     import torch
     from torch.profiler import ProfilerActivity, profile
     n_k = sum(o["kernels"] for o in ops)
@@ -291,33 +292,44 @@ def replay_kernels(runner, ops, T, reps=3):
             continue
         ks.append((e.time_range.start, e.time_range.end, nm))
     ks.sort()
-    # the last replay's kernels, checked against the op log (CUPTI may miss a kernel at the very
-    # start of the profiled window, never inside the last replay)
-    last = ks[-n_k:] if len(ks) >= n_k else []
     want = {"fis_gemm": "gemm", "fis_attn": "attn", "fis_gn": "gn_", "fis_gn_apply": "gn_apply",
             "fis_gn_stats": "gn_stats", "fis_pool2": "pool2", "fis_up2": "up2", "fis_softmax": "softmax",
             "fis_materialize": "materialize", "fis_xattn": "xattn"}
-    names = [k[2] for k in last]
-    pos, ok = 0, len(last) == n_k and len(ks) > (reps - 1) * n_k
-    for o in ops:
-        for _ in range(o["kernels"]):
-            ok = ok and want.get(o["op"], "fis") in names[pos]
-            pos += 1
-    if not ok:
+
+    def one(rep):  # per-op critical-path us of one replay's kernel records, or None on a mismatch
+        if len(rep) != n_k:
+            return None
+        pos = 0
+        for o in ops:
+            for _ in range(o["kernels"]):
+                if want.get(o["op"], "fis") not in rep[pos][2]:
+                    return None
+                pos += 1
+        out, i, prev_end = [], 0, None
+        for o in ops:
+            seg = rep[i:i + o["kernels"]]
+            i += o["kernels"]
+            end = max(x[1] for x in seg)
+            start = min(x[0] for x in seg)
+            out.append(max(0.0, end - (max(prev_end, start) if prev_end is not None else start)))
+            prev_end = end if prev_end is None else max(prev_end, end)
+        return out
+
+    # replays from the end (CUPTI may miss a kernel at the very start of the profiled window)
+    nrep = min(reps - 1, len(ks) // n_k) if n_k else 0
+    per = [one(ks[len(ks) - (q + 1) * n_k:len(ks) - q * n_k]) for q in range(nrep)]
+    per = [p for p in per if p is not None]
+    if not per or per[0] is None or one(ks[-n_k:]) is None:
         from collections import Counter
-        print(f"replay_kernels: {len(ks)} CUPTI kernels for {reps} x {n_k} expected, last replay "
-              f"{'matches' if ok else 'does not match'} the op log; {Counter(k[2][:40] for k in ks).most_common(8)}",
-              file=sys.stderr)
+        print(f"replay_kernels: {len(ks)} CUPTI kernels for {reps} x {n_k} expected, the last replay does not "
+              f"match the op log; {Counter(k[2][:40] for k in ks).most_common(8)}", file=sys.stderr)
         return None
-    out, i, prev_end = [], 0, None
-    for o in ops:
-        seg = last[i:i + o["kernels"]]
+    import statistics
+    last = ks[-n_k:]
+    out, i = [], 0
+    for j, o in enumerate(ops):
+        out.append((o, statistics.median(p[j] for p in per), last[i][2]))
         i += o["kernels"]
-        end = max(s[1] for s in seg)
-        start = min(s[0] for s in seg)
-        crit = end - (max(prev_end, start) if prev_end is not None else start)
-        out.append((o, max(0.0, crit), seg[0][2]))
-        prev_end = end if prev_end is None else max(prev_end, end)
     return out
 
 

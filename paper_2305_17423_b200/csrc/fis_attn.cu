@@ -48,6 +48,11 @@ constexpr int EPI_LD = 256 + 4;                  // O staging row pitch (floats;
 // copies), owners sum the partials in cluster-rank order, run the softmax of their rows and push
 // the bf16 P rows into every CTA's P tile; each CTA then runs P.V for its value slice.
 constexpr int P_NONE = 0, P_OUT = 1, P_IN = 2, P_OUT_KS = 3, P_DSPLIT = 4;
+// flag on P_NONE: runs of >= 3 key blocks take ONE pass (online softmax: P_j = 2^(s - m_run) with a
+// lazily raised running max, O rescaled in TMEM only when a block's max exceeds m_run by > 8, O / l
+// in the epilogue) instead of a statistics pass that recomputes every S block
+constexpr int P_ONEPASS_OK = 8;
+constexpr float RESCALE_SLACK = 8.f;  // log2 units: unnormalised P <= 2^8
 
 FIS_DEV void cluster_sync_all() {
     asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
@@ -71,6 +76,16 @@ FIS_DEV float ex2(float x) {
     float y;
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
+}
+FIS_DEV void tmem_st32(uint32_t taddr, const float* v) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+        "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+        "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7]), "f"(v[8]), "f"(v[9]),
+        "f"(v[10]), "f"(v[11]), "f"(v[12]), "f"(v[13]), "f"(v[14]), "f"(v[15]), "f"(v[16]), "f"(v[17]), "f"(v[18]),
+        "f"(v[19]), "f"(v[20]), "f"(v[21]), "f"(v[22]), "f"(v[23]), "f"(v[24]), "f"(v[25]), "f"(v[26]), "f"(v[27]),
+        "f"(v[28]), "f"(v[29]), "f"(v[30]), "f"(v[31])
+        : "memory");
 }
 FIS_DEV uint32_t idesc_bf16(int M, int N) {
     return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
@@ -101,6 +116,8 @@ FIS_DEV void tmem_ld32(uint32_t taddr, float* v) {
 __global__ void __launch_bounds__(THREADS, 1)
     attn_kernel(const fis_attn_args a, const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
                 const __grid_constant__ CUtensorMap tv, const __grid_constant__ CUtensorMap tp, int dvs, int pmode_in) {
+    const bool onepass_ok = (pmode_in & P_ONEPASS_OK) != 0;
+    pmode_in &= ~P_ONEPASS_OK;
     const bool ks = pmode_in == P_OUT_KS;
     const bool dsp = pmode_in == P_DSPLIT;
     const int pmode = ks ? P_OUT : (dsp ? P_NONE : pmode_in);
@@ -148,7 +165,8 @@ __global__ void __launch_bounds__(THREADS, 1)
     // two key blocks: both S blocks stay resident in the two TMEM buffers, so the statistics pass
     // and the P pass read the same S (no recompute, half the Q/K traffic)
     const bool resident = nkb == 2;
-    const int first_pass = single ? 2 : 1;
+    const bool onepass = onepass_ok && pmode == P_NONE && !dsp && nkb >= 3;
+    const int first_pass = (single || onepass) ? 2 : 1;
     const int pw = ((a.max_seg_k + 127) / 128) * 128;  // P scratch row width (P sharing)
     // P_DSPLIT: cluster rank = value slice; this CTA's d chunks [kc0, kc1) and owned rows [rbeg, rend)
     const int cs = dsp ? (int)gridDim.x : 1, rank = (int)blockIdx.x;
@@ -268,7 +286,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                 load_v(0);
                 load_v(1);
             } else {
-                if (!single)
+                if (!single && !onepass)
                     for (int j = 0; j < nkb; j++) load_s(j);
                 for (int u = 0; u <= nkb; u++) {
                     if (u < nkb) load_s(u);
@@ -357,7 +375,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             mma_pv(0);
             mma_pv(1);
         } else {
-            if (!single)
+            if (!single && !onepass)
                 for (int j = 0; j < nkb; j++) mma_s();
             for (int u = 0; u <= nkb; u++) {
                 if (u < nkb) mma_s();
@@ -555,9 +573,44 @@ __global__ void __launch_bounds__(THREADS, 1)
                     mbar_arrive(s_free + b);
                 } else if (pass == 2) {  // P_j -> bf16 P tile j & 1 (SW128, K-major)
                     const int pb = j & 1;
+                    float off;
+                    if (onepass) {
+                        float cm = -INFINITY;
+#pragma unroll 1
+                        for (int cb = 0; cb < 128; cb += 32) {
+                            tmem_ld32(trow + cb, v);
+                            const int lim = n_keys - kbase - cb;
+#pragma unroll
+                            for (int q = 0; q < 32; q++)
+                                if (q < lim) cm = fmaxf(cm, v[q]);
+                        }
+                        const float mb = cm * sl;
+                        if (j == 0) mrow = mb;
+                        const bool need = j > 0 && mb > mrow + RESCALE_SLACK;
+                        if (__any_sync(0xffffffffu, need)) {  // warp-collective TMEM access
+                            mbar_wait(p_free + ((j - 1) & 1), ((j - 1) >> 1) & 1);  // P.V_{j-1} done: O stable
+                            tc_fence_after();
+                            const float f = need ? ex2(mrow - mb) : 1.f;
+#pragma unroll 1
+                            for (int cb = 0; cb < dvs; cb += 32) {
+                                tmem_ld32(tmem + lane_off + O_COL + cb, v);
+#pragma unroll
+                                for (int q = 0; q < 32; q++) v[q] *= f;
+                                tmem_st32(tmem + lane_off + O_COL + cb, v);
+                            }
+                            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+                            if (need) {
+                                lrow *= f;
+                                mrow = mb;
+                            }
+                        }
+                        off = mrow;
+                    } else {
+                        off = mrow + __log2f(lrow);
+                    }
                     if (j >= 2) mbar_wait(p_free + pb, ((j >> 1) & 1) ^ 1);  // P.V_{j-2} done
-                    const float off = mrow + __log2f(lrow);
                     unsigned char* pt0 = ptile + pb * P_BYTES;
+                    float psum = 0.f;
 #pragma unroll 1
                     for (int cb = 0; cb < 128; cb += 32) {
                         tmem_ld32(trow + cb, v);
@@ -572,12 +625,14 @@ __global__ void __launch_bounds__(THREADS, 1)
                                 const int q0 = 8 * u + 2 * e2;
                                 const float p0 = q0 < lim ? ex2(fmaf(v[q0], sl, -off)) : 0.f;
                                 const float p1 = q0 + 1 < lim ? ex2(fmaf(v[q0 + 1], sl, -off)) : 0.f;
+                                psum += p0 + p1;
                                 h[e2] = __floats2bfloat162_rn(p0, p1);
                             }
                             const int unit = ((cb & 63) >> 3) + u;
                             *(uint4*)(pt + sw128_off(lr, unit)) = pk;
                         }
                     }
+                    if (onepass) lrow += psum;
                     tc_fence_before();
                     mbar_arrive(s_free + b);  // S_j fully read
                     fence_async_smem();       // generic-proxy P writes -> tensor-core reads
@@ -596,9 +651,14 @@ __global__ void __launch_bounds__(THREADS, 1)
         tc_fence_after();
         if (dsp) asm volatile("bar.sync 3, 128;" ::: "memory");  // thread 0's outgoing copies done reading
         float* ost = (float*)smem;
+        const float inv_l = onepass ? 1.f / lrow : 1.f;  // one pass: O holds the unnormalised sum
 #pragma unroll 1
         for (int cb = 0; cb < dvs; cb += 32) {
             tmem_ld32(tmem + lane_off + O_COL + cb, v);
+            if (onepass) {
+#pragma unroll
+                for (int q = 0; q < 32; q++) v[q] *= inv_l;
+            }
 #pragma unroll
             for (int q = 0; q < 8; q++)
                 *(float4*)(ost + lr * EPI_LD + cb + 4 * q) = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
@@ -796,7 +856,8 @@ static bool attn_share(const fis_attn_args* a, int dvs) {
 static bool attn_dsplit(const fis_attn_args* a, int dvs) {
     static int off = getenv("FIS_ATTN_DSPLIT") && getenv("FIS_ATTN_DSPLIT")[0] == '0';
     const int cs = a->dv / dvs, dch = a->d / 64;
-    if (off || a->nseg > 0 || a->n_keys > 128 || cs < 2 || cs > 8 || dch < cs || (dch + cs - 1) / cs > 4) return false;
+    // (d >= 1024: at d = 320 / 640 the exchange costs what the split saves, r02 step tables)
+    if (off || a->nseg > 0 || a->n_keys > 128 || cs < 2 || cs > 8 || dch < 16 || (dch + cs - 1) / cs > 4) return false;
     const int rp = (128 + cs - 1) / cs;
     if ((cs - 1) * rp * 512 > fis::attn::P_BYTES + fis::attn::RX_EXTRA) return false;
     return (long long)cs * ((a->m + 127) / 128) < 148;
@@ -883,7 +944,9 @@ extern "C" int fis_attn(const fis_attn_args* a, void* stream) {
                        cudaSuccess
                    ? FIS_OK : FIS_ERR_LAUNCH;
     }
+    static int onepass_off = getenv("FIS_ATTN_ONEPASS") && getenv("FIS_ATTN_ONEPASS")[0] == '0';
     return cudaLaunchKernelEx(&cfg, fis::attn::attn_kernel, *a, tq, tk, tv, tp, dvs,
-                              share ? (int)fis::attn::P_IN : (int)fis::attn::P_NONE) == cudaSuccess
+                              share ? (int)fis::attn::P_IN
+                                    : (int)fis::attn::P_NONE | (onepass_off ? 0 : fis::attn::P_ONEPASS_OK)) == cudaSuccess
                ? FIS_OK : FIS_ERR_LAUNCH;
 }
