@@ -12,6 +12,8 @@ int fis_gemm_halo_ok(const fis_gemm_args* a);
 int fis_gemm_halo_launch(const fis_gemm_args* a, cudaStream_t stream);
 int fis_gemm_big_eligible(const fis_gemm_args* a);
 int fis_gemm_big_launch(const fis_gemm_args* a, cudaStream_t stream);
+int fis_conv_small_ok(const fis_gemm_args* a);
+int fis_conv_small_launch(const fis_gemm_args* a, cudaStream_t stream);
 
 extern "C" {
 int fis_ltr_set_tc(unsigned long long* p);
@@ -19,10 +21,11 @@ int fis_ltr_set_attn(unsigned long long* p);
 int fis_ltr_set_simt(unsigned long long* p);
 int fis_ltr_set_ops(unsigned long long* p);
 int fis_ltr_set_big(unsigned long long* p);
+int fis_ltr_set_small(unsigned long long* p);
 
 int fis_trace_launches(unsigned long long* buf) {
     return fis_ltr_set_tc(buf) | fis_ltr_set_attn(buf) | fis_ltr_set_simt(buf) | fis_ltr_set_ops(buf) |
-           fis_ltr_set_big(buf);
+           fis_ltr_set_big(buf) | fis_ltr_set_small(buf);
 }
 
 int fis_abi_version(void) { return FIS_ABI_VERSION; }
@@ -79,9 +82,11 @@ static int fis_choose_splits(const fis_gemm_args* a, bool tc) {
 
 // Which kernel fis_gemm would run for these arguments: 0 SIMT, 1 per-op tcgen05, 2 persistent
 // large-M tcgen05 (csrc/fis_gemm_big.cu), 3 per-op tcgen05 3xTF32 (fp32 operands), 4 halo-staged
-// persistent gather conv (csrc/fis_gemm_halo.cu). Host-only query (no launch).
+// persistent gather conv (csrc/fis_gemm_halo.cu), 5 few-input-channel 3x3 conv on the FMA pipes
+// (csrc/fis_conv_small.cu). Host-only query (no launch).
 int fis_gemm_kernel_kind(const fis_gemm_args* a) {
     if (a->impl == 3) return fis_gemm_tf32_supported(a) ? 3 : 0;
+    if (a->impl == 0 && fis_conv_small_ok(a)) return 5;
     if (a->impl == 0 && fis_gemm_halo_ok(a)) return 4;
     const bool tc = a->impl == 2 || (a->impl == 0 && fis_gemm_tc_supported(a));
     if (!tc) return 0;
@@ -103,6 +108,11 @@ int fis_gemm(const fis_gemm_args* a, void* stream) {
     if (a->epi == FIS_EPI_GN_SILU && (a->groups <= 0 || a->n % a->groups || !a->gn_mean.ptr || !a->gn_var.ptr))
         return a->gn_mean.ptr ? FIS_ERR_SHAPE : FIS_ERR_CACHE_MISS;
     const bool tc = a->impl == 2 || (a->impl == 0 && fis_gemm_tc_supported(a));
+    // the latent stem conv (C_in = 4): FMA pipes, weights and taps staged once per 64 rows
+    if (a->impl == 0 && fis_conv_small_ok(a)) {
+        const int rc = fis_conv_small_launch(a, (cudaStream_t)stream);
+        if (rc != FIS_ERR_UNSUPPORTED) return rc;
+    }
     // halo-mode gathered convs of the stacked step: staged once per kernel row (fis_gemm_halo.cu)
     if (a->impl == 0 && fis_gemm_halo_ok(a)) {
         const int rc = fis_gemm_halo_launch(a, (cudaStream_t)stream);

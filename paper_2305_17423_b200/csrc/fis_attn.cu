@@ -87,6 +87,15 @@ FIS_DEV void tmem_st32(uint32_t taddr, const float* v) {
         "f"(v[28]), "f"(v[29]), "f"(v[30]), "f"(v[31])
         : "memory");
 }
+// mbarrier wait ordering memory at cluster scope (barriers arrived on by peer CTAs)
+FIS_DEV void mbar_wait_cluster(uint64_t* b, uint32_t parity) {
+    asm volatile(
+        "{\n.reg .pred p;\nWAITC_%=:\n"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAITC_%=;\n}\n" ::"r"(smem_u32(b)),
+        "r"(parity)
+        : "memory");
+}
 FIS_DEV uint32_t idesc_bf16(int M, int N) {
     return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
@@ -132,8 +141,10 @@ __global__ void __launch_bounds__(THREADS, 1)
     uint64_t* p_ready = s_free + 2;      // [2]
     uint64_t* p_free = p_ready + 2;      // [2]
     uint64_t* o_done = p_free + 2;
-    uint64_t* rx_bar = o_done + 1;       // P_DSPLIT: peers' partial row slices landed
-    uint32_t* tmem_slot = (uint32_t*)(rx_bar + 1);
+    uint64_t* rx_bar = o_done + 1;       // P_DSPLIT: peers' partial row slices landed (one phase per round)
+    uint64_t* tx_ok = rx_bar + 1;        // P_DSPLIT: every peer consumed its receive buffer (per round)
+    uint64_t* part_free = tx_ok + 1;     // P_DSPLIT, 2 key blocks: stages 2-3 free for V^T of block 1
+    uint32_t* tmem_slot = (uint32_t*)(part_free + 1);
     float2* xst = (float2*)(ptile + 2 * P_BYTES + RX_EXTRA + 256);  // [128] key-split (max, sum) exchange
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -186,6 +197,8 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
         mbar_init(o_done, 1);
         mbar_init(rx_bar, 1);
+        mbar_init(tx_ok, cs > 1 ? cs - 1 : 1);
+        mbar_init(part_free, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         if (dsp && rend > rbeg)  // incoming: cs - 1 partial slices of this CTA's rows
             asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(rx_bar)),
@@ -257,15 +270,23 @@ __global__ void __launch_bounds__(THREADS, 1)
                     tma2d(sbase + st * STAGE, &tv, k_beg + j * 128 + h * 64, c0, full + st);
                 }
             };
-            if (dsp) {  // this CTA's d chunks of S, then its V^T slice into stages 0-1 (part lives in 2-3)
-                for (int kc = kc0; kc < kc1; kc++) {
-                    const int st = stage(2 * A_BYTES);
-                    const uint32_t sa = sbase + st * STAGE;
-                    tma2d(sa, &tq, kc * 64, m0, full + st);
-                    tma2d(sa + A_BYTES, &tk, kc * 64, k_beg, full + st);
-                }
-                it = STAGES;
+            if (dsp) {
+                // this CTA's d chunks of every S block, the ring padded to a whole cycle (empty
+                // stages complete at once), then V^T of block 0 into stages 0-1 (the partial-S
+                // exchange buffer lives in stages 2-3) and, once the exchange is over, block 1's
+                for (int kc = kc0; kc < kc1; kc++)
+                    for (int j = 0; j < nkb; j++) {
+                        const int st = stage(2 * A_BYTES);
+                        const uint32_t sa = sbase + st * STAGE;
+                        tma2d(sa, &tq, kc * 64, m0, full + st);
+                        tma2d(sa + A_BYTES, &tk, kc * 64, k_beg + j * 128, full + st);
+                    }
+                while (it % STAGES) stage(0);
                 load_v(0);
+                if (nkb > 1) {
+                    mbar_wait(part_free, 0);
+                    load_v(1);
+                }
             } else if (pmode == P_IN) {  // P tiles of this query tile from the scratch (written by the P_OUT launch)
                 for (int j = 0; j < nkb; j++) {
                     const int pb = j & 1;
@@ -345,24 +366,31 @@ __global__ void __launch_bounds__(THREADS, 1)
             }
         };
         if (dsp) {
-            for (int kc = kc0; kc < kc1; kc++) {
+            for (int kc = kc0; kc < kc1; kc++)
+                for (int j = 0; j < nkb; j++) {
+                    const int st = it % STAGES;
+                    mbar_wait(full + st, (it / STAGES) & 1);
+                    tc_fence_after();
+                    if (lane == 0) {
+                        const uint32_t sa = sbase + st * STAGE, sbb = sa + A_BYTES;
+#pragma unroll
+                        for (int kk = 0; kk < 4; kk++)
+                            mma_bf16(tmem + j * 128, sw128_desc(sa + kk * 32), sw128_desc(sbb + kk * 32), id_s,
+                                     (kc != kc0 || kk) ? 1u : 0u);
+                        mma_commit(empty + st);
+                        if (kc == kc1 - 1) mma_commit(s_ready + j);
+                    }
+                    __syncwarp();
+                    it++;
+                }
+            while (it % STAGES) {  // the producer's padding stages
                 const int st = it % STAGES;
                 mbar_wait(full + st, (it / STAGES) & 1);
-                tc_fence_after();
-                if (lane == 0) {
-                    const uint32_t sa = sbase + st * STAGE, sbb = sa + A_BYTES;
-#pragma unroll
-                    for (int kk = 0; kk < 4; kk++)
-                        mma_bf16(tmem, sw128_desc(sa + kk * 32), sw128_desc(sbb + kk * 32), id_s,
-                                 (kc != kc0 || kk) ? 1u : 0u);
-                    mma_commit(empty + st);
-                    if (kc == kc1 - 1) mma_commit(s_ready);
-                }
+                if (lane == 0) mma_commit(empty + st);
                 __syncwarp();
                 it++;
             }
-            it = STAGES;
-            mma_pv(0);
+            for (int j = 0; j < nkb; j++) mma_pv(j);
         } else if (pmode == P_IN) {
             for (int j = 0; j < nkb; j++) mma_pv(j);
         } else if (pmode == P_OUT) {
@@ -392,82 +420,130 @@ __global__ void __launch_bounds__(THREADS, 1)
         int sb = 0;
         float v[32];
         if (dsp) {
-            // 1. partial S (this CTA's d chunks) -> part: fp32 [128][128] in stages 2-3, 16-byte units
-            //    XOR-swizzled by row (conflict-free row-per-thread writes; rows stay contiguous)
+            // per key block j (round j): 1. the partial S_j (this CTA's d chunks) -> part: fp32
+            // [128][128] in stages 2-3, 16-byte units XOR-swizzled by row (conflict-free row-per-
+            // thread writes; rows stay contiguous); 2. each peer's row slice -> its receive slot for
+            // this rank (DSMEM bulk copy); 3. the owned rows' partials summed in rank order. Then the
+            // softmax of the owned rows over all blocks and the bf16 P rows -> every CTA's P tiles.
+            // 4 threads per owned row (32 keys of each block); two row iterations when a CTA owns 64
+            // rows (one key block only)
             unsigned char* part = smem + 2 * STAGE;
-            mbar_wait(s_ready, 0);
-            ltr(ls, 3);
-            tc_fence_after();
-#pragma unroll 1
-            for (int cb = 0; cb < 128; cb += 32) {
-                tmem_ld32(tmem + lane_off + cb, v);
-#pragma unroll
-                for (int q = 0; q < 8; q++) {
-                    const int u = (cb >> 2) + q;
-                    *(float4*)(part + lr * 512 + ((u ^ (lr & 7)) << 4)) = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
-                }
-            }
-            fence_async_smem();
-            asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");  // peers' barriers initialised
-            asm volatile("bar.sync 3, 128;" ::: "memory");
             const uint32_t part_s = smem_u32(part);
-            if (tid == 0) {  // 2. each peer's row slice of the partial -> its receive slot for this rank
-                for (int p = 0; p < cs; p++) {
-                    if (p == rank) continue;
-                    const int pb = min(128, p * rp), pe = min(128, pb + rp);
-                    if (pe <= pb) continue;
-                    const int slot = rank < p ? rank : rank - 1;
-                    uint32_t dst, bar;
-                    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(dst) : "r"(smem_u32(rxbuf) + (uint32_t)(slot * rp * 512)), "r"(p));
-                    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(bar) : "r"(smem_u32(rx_bar)), "r"(p));
-                    asm volatile(
-                        "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
-                        "r"(part_s + (uint32_t)(pb * 512)), "r"((uint32_t)((pe - pb) * 512)), "r"(bar)
-                        : "memory");
-                }
-                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-            }
-            // 3. owned rows: sum the partials in rank order, softmax, bf16 P rows -> the local P tile.
-            //    4 threads per row (32 keys each), rows i and i + 32 when a CTA owns 64 rows
             const int own = rend - rbeg;
-            if (own > 0) mbar_wait(rx_bar, 0);
-            ltr(ls, 5);
-            const int seg = tid & 3, kbase = seg * 32, lim = n_keys - kbase;
-#pragma unroll 1
-            for (int i = tid >> 2; i < ((own + 31) & ~31); i += 32) {
-                const bool act = i < own;
+            const int seg = tid & 3, kbase = seg * 32;
+            const int niter = (own + 31) >> 5;
+            float xs[2][32];
+            auto sum_rows = [&](float (&x)[32], int i) {
                 const int r = rbeg + i;
-                float x[32];
 #pragma unroll
                 for (int q = 0; q < 32; q++) x[q] = 0.f;
-                if (act) {
-                    for (int z = 0; z < cs; z++) {
-                        const unsigned char* src = z == rank ? part + r * 512
-                                                             : (const unsigned char*)rxbuf + (z < rank ? z : z - 1) * rp * 512 + i * 512;
+                if (i >= own) return;
+                for (int z = 0; z < cs; z++) {
+                    const unsigned char* src = z == rank ? part + r * 512
+                                                         : (const unsigned char*)rxbuf + (z < rank ? z : z - 1) * rp * 512 + i * 512;
 #pragma unroll
-                        for (int q = 0; q < 8; q++) {
-                            const int u = seg * 8 + q;
-                            const float4 f = *(const float4*)(src + ((u ^ (r & 7)) << 4));
-                            x[4 * q] += f.x; x[4 * q + 1] += f.y; x[4 * q + 2] += f.z; x[4 * q + 3] += f.w;
-                        }
+                    for (int q = 0; q < 8; q++) {
+                        const int u = seg * 8 + q;
+                        const float4 f = *(const float4*)(src + ((u ^ (r & 7)) << 4));
+                        x[4 * q] += f.x; x[4 * q + 1] += f.y; x[4 * q + 2] += f.z; x[4 * q + 3] += f.w;
                     }
                 }
+            };
+            for (int j = 0; j < nkb; j++) {
+                // part lives in stages 2-3: round 0 waits for EVERY S block (the last blocks' MMAs read
+                // those stages after block 0 completes)
+                if (j == 0)
+                    for (int b = 0; b < nkb; b++) mbar_wait(s_ready + b, 0);
+                if (j == 0) ltr(ls, 3);
+                tc_fence_after();
+                if (j > 0) asm volatile("bar.sync 3, 128;" ::: "memory");  // round j-1's copies have read part
+#pragma unroll 1
+                for (int cb = 0; cb < 128; cb += 32) {
+                    tmem_ld32(tmem + lane_off + j * 128 + cb, v);
+#pragma unroll
+                    for (int q = 0; q < 8; q++) {
+                        const int u = (cb >> 2) + q;
+                        *(float4*)(part + lr * 512 + ((u ^ (lr & 7)) << 4)) = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+                    }
+                }
+                fence_async_smem();
+                if (j == 0) asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");  // peers' barriers initialised
+                asm volatile("bar.sync 3, 128;" ::: "memory");
+                if (tid == 0) {
+                    if (j > 0) mbar_wait_cluster(tx_ok, (j - 1) & 1);  // every peer consumed round j-1
+                    for (int p = 0; p < cs; p++) {
+                        if (p == rank) continue;
+                        const int pb = min(128, p * rp), pe = min(128, pb + rp);
+                        if (pe <= pb) continue;
+                        const int slot = rank < p ? rank : rank - 1;
+                        uint32_t dst, bar;
+                        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(dst) : "r"(smem_u32(rxbuf) + (uint32_t)(slot * rp * 512)), "r"(p));
+                        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(bar) : "r"(smem_u32(rx_bar)), "r"(p));
+                        asm volatile(
+                            "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+                            "r"(part_s + (uint32_t)(pb * 512)), "r"((uint32_t)((pe - pb) * 512)), "r"(bar)
+                            : "memory");
+                    }
+                    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                }
+                if (own > 0) mbar_wait(rx_bar, j & 1);
+                if (j == 0) ltr(ls, 5);
+                if (nkb > 1) {
+                    if (j == 0) sum_rows(xs[0], tid >> 2);
+                    else sum_rows(xs[1], tid >> 2);
+                } else {
+                    sum_rows(xs[0], tid >> 2);
+                    if (niter > 1) sum_rows(xs[1], (tid >> 2) + 32);
+                }
+                asm volatile("bar.sync 3, 128;" ::: "memory");  // receive buffer and part fully read
+                if (tid == 0) {
+                    if (j + 1 < nkb && own > 0)  // re-arm for round j+1 before releasing the peers
+                        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(rx_bar)),
+                                     "r"((uint32_t)((cs - 1) * own * 512))
+                                     : "memory");
+                    for (int p = 0; p < cs; p++) {
+                        if (p == rank) continue;
+                        uint32_t rb;
+                        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rb) : "r"(smem_u32(tx_ok)), "r"(p));
+                        asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(rb) : "memory");
+                    }
+                    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // round j's copies have read part
+                    if (j == nkb - 1 && nkb > 1) mbar_arrive(part_free);  // V^T of block 1 may overwrite stages 2-3
+                }
+            }
+            // softmax of one owned row (this thread's 32 keys of each block) -> the local P tiles
+            auto emit = [&](const float (&x0)[32], const float (&x1)[32], int nb, int i) {
+                const bool act = i < own;
+                const int r = rbeg + i;
+                const int lim0 = n_keys - kbase, lim1 = n_keys - 128 - kbase;
                 float cm = -INFINITY;
 #pragma unroll
                 for (int q = 0; q < 32; q++)
-                    if (q < lim) cm = fmaxf(cm, x[q]);
+                    if (q < lim0) cm = fmaxf(cm, x0[q]);
+                if (nb > 1) {
+#pragma unroll
+                    for (int q = 0; q < 32; q++)
+                        if (q < lim1) cm = fmaxf(cm, x1[q]);
+                }
                 cm = fmaxf(cm, __shfl_xor_sync(0xffffffffu, cm, 1));
                 cm = fmaxf(cm, __shfl_xor_sync(0xffffffffu, cm, 2));
                 const float mn = cm * sl;
                 float add = 0.f;
 #pragma unroll
                 for (int q = 0; q < 32; q++)
-                    if (q < lim) add += ex2(fmaf(x[q], sl, -mn));
+                    if (q < lim0) add += ex2(fmaf(x0[q], sl, -mn));
+                if (nb > 1) {
+#pragma unroll
+                    for (int q = 0; q < 32; q++)
+                        if (q < lim1) add += ex2(fmaf(x1[q], sl, -mn));
+                }
                 add += __shfl_xor_sync(0xffffffffu, add, 1);
                 add += __shfl_xor_sync(0xffffffffu, add, 2);
                 const float off = mn + __log2f(add);
-                if (act) {
-                    unsigned char* pt = ptile + (kbase >> 6) * (128 * 128);
+                if (!act) return;
+                for (int b = 0; b < nb; b++) {
+                    const int lim = b ? lim1 : lim0;
+                    unsigned char* pt = ptile + b * P_BYTES + (kbase >> 6) * (128 * 128);
 #pragma unroll
                     for (int u = 0; u < 4; u++) {
                         uint4 pk;
@@ -475,37 +551,49 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
                         for (int e2 = 0; e2 < 4; e2++) {
                             const int q0 = 8 * u + 2 * e2;
-                            const float p0 = q0 < lim ? ex2(fmaf(x[q0], sl, -off)) : 0.f;
-                            const float p1 = q0 + 1 < lim ? ex2(fmaf(x[q0 + 1], sl, -off)) : 0.f;
+                            const float y0 = b ? x1[q0] : x0[q0], y1 = b ? x1[q0 + 1] : x0[q0 + 1];
+                            const float p0 = q0 < lim ? ex2(fmaf(y0, sl, -off)) : 0.f;
+                            const float p1 = q0 + 1 < lim ? ex2(fmaf(y1, sl, -off)) : 0.f;
                             h[e2] = __floats2bfloat162_rn(p0, p1);
                         }
                         *(uint4*)(pt + sw128_off(r, ((kbase & 63) >> 3) + u)) = pk;
                     }
                 }
+            };
+            if (nkb > 1) {
+                emit(xs[0], xs[1], 2, tid >> 2);
+            } else {
+                emit(xs[0], xs[0], 1, tid >> 2);
+                if (niter > 1) emit(xs[1], xs[1], 1, (tid >> 2) + 32);
             }
             fence_async_smem();
             asm volatile("bar.sync 3, 128;" ::: "memory");
-            if (tid == 0) {  // 4. the owned P rows -> every peer's P tile; then expect the peers' rows
+            if (tid == 0) {  // 4. the owned P rows -> every peer's P tiles; then expect the peers' rows
+                // P tile 1 aliases the receive buffers: every peer has consumed its last round
+                if (nkb > 1) mbar_wait_cluster(tx_ok, (nkb - 1) & 1);
                 const uint32_t pt_s = smem_u32(ptile);
                 if (own > 0)
                     for (int p = 0; p < cs; p++) {
                         if (p == rank) continue;
-                        uint32_t bar;
-                        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(bar) : "r"(smem_u32(p_ready)), "r"(p));
-                        for (int h = 0; h < 2; h++) {
-                            const uint32_t off = pt_s + (uint32_t)(h * 128 * 128 + rbeg * 128);
-                            uint32_t dst;
-                            asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(dst) : "r"(off), "r"(p));
-                            asm volatile(
-                                "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
-                                "r"(off), "r"((uint32_t)(own * 128)), "r"(bar)
-                                : "memory");
+                        for (int b = 0; b < nkb; b++) {
+                            uint32_t bar;
+                            asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(bar) : "r"(smem_u32(p_ready + b)), "r"(p));
+                            for (int h = 0; h < 2; h++) {
+                                const uint32_t off = pt_s + (uint32_t)(b * P_BYTES + h * 128 * 128 + rbeg * 128);
+                                uint32_t dst;
+                                asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(dst) : "r"(off), "r"(p));
+                                asm volatile(
+                                    "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+                                    "r"(off), "r"((uint32_t)(own * 128)), "r"(bar)
+                                    : "memory");
+                            }
                         }
                     }
                 asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(p_ready)),
-                             "r"((uint32_t)((128 - own) * 256))
-                             : "memory");
+                for (int b = 0; b < nkb; b++)
+                    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(p_ready + b)),
+                                 "r"((uint32_t)((128 - own) * 256))
+                                 : "memory");
                 ltr(ls, 6);
                 // the outgoing copies have read part / P before the epilogue reuses the stages
                 asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
@@ -857,8 +945,9 @@ static bool attn_dsplit(const fis_attn_args* a, int dvs) {
     static int off = getenv("FIS_ATTN_DSPLIT") && getenv("FIS_ATTN_DSPLIT")[0] == '0';
     const int cs = a->dv / dvs, dch = a->d / 64;
     // (d >= 1024: at d = 320 / 640 the exchange costs what the split saves, r02 step tables)
-    if (off || a->nseg > 0 || a->n_keys > 128 || cs < 2 || cs > 8 || dch < 16 || (dch + cs - 1) / cs > 4) return false;
+    if (off || a->nseg > 0 || a->n_keys > 256 || cs < 2 || cs > 8 || dch < 16 || (dch + cs - 1) / cs > 4) return false;
     const int rp = (128 + cs - 1) / cs;
+    if (a->n_keys > 128 && rp > 32) return false;  // two key blocks: one owned-row iteration
     if ((cs - 1) * rp * 512 > fis::attn::P_BYTES + fis::attn::RX_EXTRA) return false;
     return (long long)cs * ((a->m + 127) / 128) < 148;
 }

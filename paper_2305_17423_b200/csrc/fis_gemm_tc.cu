@@ -544,8 +544,11 @@ __global__ void __launch_bounds__(THREADS, 1)
         // partials in split order (bitwise the same as a sequential reduction) and runs the epilogue
         uint32_t rank;
         asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
-        const int rows_per = (BM + S - 1) / S;
-        const int rbeg = min(BM, (int)rank * rows_per), rend = min(BM, rbeg + rows_per);
+        // only the tile's valid rows are exchanged (M = 64 / 100-row GEMMs at batch 1 would push
+        // 50% / 22% padding rows through the ~20 B/cycle DSMEM port)
+        const int vrows = min(BM, a.m - m0);
+        const int rows_per = (vrows + S - 1) / S;
+        const int rbeg = min(vrows, (int)rank * rows_per), rend = min(vrows, rbeg + rows_per);
         float* rx = (float*)(((uintptr_t)(seltab + BM * 2 * 9) + 15) & ~(uintptr_t)15);
         const uint32_t slice_floats = (uint32_t)rows_per * PLD;
         asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");  // peers' rx_bar initialised
@@ -558,7 +561,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             const uint32_t part_s = smem_u32(part), rx_s = smem_u32(rx), bar_s = smem_u32(rx_bar);
             for (int p = 0; p < S; p++) {
                 if (p == (int)rank) continue;
-                const int pb = min(BM, p * rows_per), pe = min(BM, pb + rows_per);
+                const int pb = min(vrows, p * rows_per), pe = min(vrows, pb + rows_per);
                 if (pe <= pb) continue;
                 const int slot = (int)rank < p ? (int)rank : (int)rank - 1;  // my slot in peer p's buffer
                 uint32_t dst, bar;

@@ -141,3 +141,48 @@ def test_gathered_conv_with_gn_silu(env):
     yn = (y - mu) * rs * gamma + beta
     ref = yn * torch.sigmoid(yn)
     assert (r[0].float() - ref).abs().max().item() <= 8e-2
+
+
+@pytest.mark.parametrize("R,h,w,cout,sparse", [(1, 64, 64, 320, True), (64, 64, 64, 320, True), (2, 16, 16, 64, False)])
+def test_small_cin_stem_conv(env, R, h, w, cout, sparse):
+    """The latent stem conv (C_in = 4, K = 36, csrc/fis_conv_small.cu): fp32 latent rows with
+    select-on-read (fresh active rows / cached latent), bias + per-step time bias, bf16 output,
+    against torch fp32 conv2d on the same values."""
+    L, DRef, NULL, lz = env
+    g = torch.Generator(device="cuda").manual_seed(R + cout)
+    cin, hw = 4, h * w
+    if sparse:
+        act = torch.zeros((R, h, w), dtype=torch.bool, device="cuda")
+        for r in range(R):
+            y0, x0 = (7 * r) % (h // 2), (5 * r) % (w // 2)
+            act[r, y0:y0 + h // 3, x0:x0 + w // 4] = True
+        act = act.flatten()
+        rows = act.nonzero().flatten().to(torch.int32)
+    else:
+        rows = None
+    n = rows.numel() if sparse else R * hw
+    cache = torch.randn((R * hw, cin), device="cuda", generator=g)
+    fresh = torch.randn((n, cin), device="cuda", generator=g) if sparse else cache
+    W = _rnd(g, cout, 9 * cin, scale=1 / math.sqrt(9 * cin))
+    bias = torch.randn(cout, device="cuda", generator=g)
+    tbias = torch.randn(cout, device="cuda", generator=g)
+    out = torch.empty((n, cout), device="cuda", dtype=torch.bfloat16)
+    if sparse:
+        index = torch.full((R * hw,), -1, dtype=torch.int32, device="cuda")
+        index[rows.long()] = torch.arange(n, dtype=torch.int32, device="cuda")
+        src = L.Src(DRef(fresh).ref(), DRef(cache).ref(), L.ptr(index), h, w, cin, 0)
+    else:
+        src = L.Src(DRef(fresh).ref(), NULL, None, h, w, cin, 0)
+    lz.gemm(n, cout, 9 * cin, rows=rows, srcs=[src], out_hw=(h, w), b=DRef(W), d=DRef(out), bias=bias,
+            bias2=DRef(tbias))
+    torch.cuda.synchronize()
+    assert _kind(lz) == 5  # the FMA-pipe stem kernel ran (no SIMT fallback)
+    full = cache.clone()
+    if sparse:
+        full[rows.long()] = fresh
+    xi = full.reshape(R, h, w, cin).permute(0, 3, 1, 2)
+    Wk = W.float().reshape(cout, 3, 3, cin).permute(0, 3, 1, 2)
+    y = torch.nn.functional.conv2d(xi, Wk, bias + tbias, padding=1).permute(0, 2, 3, 1).reshape(R * hw, cout)
+    if sparse:
+        y = y[rows.long()]
+    assert (out.float() - y).abs().max().item() <= 3e-2 * max(1.0, y.abs().max().item())

@@ -128,7 +128,9 @@ def test_transposed_store_and_residual(env):
 @pytest.mark.parametrize("m,nk,d", [(400, 400, 320), (100, 100, 640), (256, 256, 1280), (64, 64, 1280),
                                     (400, 77, 320), (1024, 1024, 320), (37, 5, 64), (300, 129, 128),
                                     # d-split clusters (<= 128 keys, small grids): cs = 5, 4, 3, 2 value slices
-                                    (256, 77, 1280), (64, 77, 1280), (100, 77, 640), (200, 50, 768), (130, 128, 512)])
+                                    (256, 77, 1280), (64, 77, 1280), (100, 77, 640), (200, 50, 768), (130, 128, 512),
+                                    # two-round d-split (129-256 keys): cs = 5, 4
+                                    (200, 190, 1280), (256, 129, 1024), (64, 256, 1280)])
 def test_fused_attention_vs_torch(env, m, nk, d):
     """fis_attn (tcgen05 S=QK^T, softmax, P.V, + residual) against torch fp32 on the same bf16 inputs."""
     L, DRef, NULL, lz = env
