@@ -786,6 +786,17 @@ int fis_gemm_big_launch(const fis_gemm_args* a, cudaStream_t stream) {
     if ((amode == fis::big::A_CPASYNC || amode == fis::big::A_TMA_GATHER) && !wide_off) {
         const int w = wide_bn(a->n);
         if (w) bn = w;
+    } else if (!wide_off && !getenv("FIS_BIG_BN")) {
+        // TMA-staged A: a 320-wide tile (two N = 160 MMAs per K block) when it needs fewer waves
+        // of tiles x tile width (e.g. 4096 x 1280: 160 tiles of 256 = 2 waves on 148 SMs, 128
+        // tiles of 320 = 1 wave)
+        const int w = wide_bn(a->n);
+        if (w) {
+            const long long mt = (a->m + 127) / 128;
+            const long long t0 = mt * ((a->n + bn - 1) / bn), t1 = mt * ((a->n + w - 1) / w);
+            const long long c0 = (t0 + sms() - 1) / sms() * bn, c1 = (t1 + sms() - 1) / sms() * w;
+            if (c1 < c0) bn = w;
+        }
     }
     const CUtensorMap* tm = weight_map(a->b.ptr, a->n, a->k, a->b.ld, bn > 256 ? bn / 2 : bn);
     if (!tm) return FIS_ERR_UNSUPPORTED;

@@ -82,7 +82,8 @@ def test_rows_and_qkv_split(env):
     assert torch.equal(outs[0][0], outs[1][0]) and torch.equal(outs[0][1], outs[1][1])
 
 
-@pytest.mark.parametrize("R,h,w,cin,cout", [(32, 16, 16, 128, 256), (160, 8, 8, 128, 256), (4, 64, 64, 64, 320)])
+@pytest.mark.parametrize("R,h,w,cin,cout", [(32, 16, 16, 128, 256), (160, 8, 8, 128, 256), (4, 64, 64, 64, 320),
+                                             (16, 16, 16, 128, 1280)])  # last: 320-wide tiles (1 wave)
 def test_dense_stacked_conv(env, R, h, w, cin, cout):
     L, DRef, NULL, lz = env
     g = torch.Generator(device="cuda").manual_seed(R + h)
