@@ -117,10 +117,12 @@ int fis_gemm(const fis_gemm_args* args, void* stream);
 /* which kernel fis_gemm picks for these arguments: 0 SIMT, 1 per-op tcgen05 (split-K clusters),
  * 2 persistent large-M tcgen05 (TMA / gather4 staging), 3 per-op tcgen05 3xTF32, 4 halo-staged
  * persistent gather conv (m_halo), 5 few-input-channel 3x3 conv on the FMA pipes (the latent stem
- * conv, C_in <= 8); host-only */
+ * conv, C_in <= 8), 6 persistent 2-SM CTA-pair GEMM (tcgen05 cta_group::2, TMA-staged A); host-only */
 int fis_gemm_kernel_kind(const fis_gemm_args* a);
 /* number of persistent-kernel launches so far (diagnostics / tests) */
 long long fis_gemm_big_launch_count(void);
+/* number of 2-SM (CTA pair) GEMM launches so far (diagnostics / tests) */
+long long fis_gemm_pair_launch_count(void);
 /* workspace floats / counters needed for a given problem */
 long long fis_gemm_ws_floats(int m, int n, int splits);
 int fis_gemm_counters(int m, int n);

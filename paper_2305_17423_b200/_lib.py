@@ -127,7 +127,7 @@ _SIGS = {
     "fis_mask_plan": MaskPlanArgs, "fis_vm_run": VmArgs,
 }
 
-EXPORTS = tuple(_SIGS) + ("fis_vm_plan", "fis_vm_plan_tma", "fis_vm_op_size", "fis_vm_attn_slice", "fis_attn_launches", "fis_gn_launches", "fis_gemm_kernel_kind", "fis_gemm_big_launch_count", "fis_gemm_ws_floats", "fis_gemm_counters", "fis_mask_detect_smem", "fis_abi_version",
+EXPORTS = tuple(_SIGS) + ("fis_vm_plan", "fis_vm_plan_tma", "fis_vm_op_size", "fis_vm_attn_slice", "fis_attn_launches", "fis_gn_launches", "fis_gemm_kernel_kind", "fis_gemm_big_launch_count", "fis_gemm_pair_launch_count", "fis_gemm_ws_floats", "fis_gemm_counters", "fis_mask_detect_smem", "fis_abi_version",
                           "fis_last_error", "fis_device_sm_count")
 
 
@@ -160,6 +160,7 @@ def lib():
         L.fis_gemm_kernel_kind.argtypes = [C.POINTER(GemmArgs)]
         L.fis_gemm_kernel_kind.restype = C.c_int
         L.fis_gemm_big_launch_count.restype = C.c_longlong
+        L.fis_gemm_pair_launch_count.restype = C.c_longlong
         L.fis_gn_launches.argtypes = [C.POINTER(GnApplyArgs)]
         L.fis_gn_launches.restype = C.c_int
         L.fis_trace_launches.argtypes = [C.c_void_p]

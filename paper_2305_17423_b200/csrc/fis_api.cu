@@ -13,6 +13,9 @@ int fis_gemm_halo_launch(const fis_gemm_args* a, cudaStream_t stream);
 int fis_gemm_big_eligible(const fis_gemm_args* a);
 int fis_gemm_big_launch(const fis_gemm_args* a, cudaStream_t stream);
 int fis_conv_small_ok(const fis_gemm_args* a);
+int fis_gemm_pair_ok(const fis_gemm_args* a, int single_bn);
+int fis_gemm_pair_launch(const fis_gemm_args* a, cudaStream_t stream);
+int fis_gemm_big_bn(int n);
 int fis_conv_small_launch(const fis_gemm_args* a, cudaStream_t stream);
 
 extern "C" {
@@ -22,10 +25,11 @@ int fis_ltr_set_simt(unsigned long long* p);
 int fis_ltr_set_ops(unsigned long long* p);
 int fis_ltr_set_big(unsigned long long* p);
 int fis_ltr_set_small(unsigned long long* p);
+int fis_ltr_set_pair(unsigned long long* p);
 
 int fis_trace_launches(unsigned long long* buf) {
     return fis_ltr_set_tc(buf) | fis_ltr_set_attn(buf) | fis_ltr_set_simt(buf) | fis_ltr_set_ops(buf) |
-           fis_ltr_set_big(buf) | fis_ltr_set_small(buf);
+           fis_ltr_set_big(buf) | fis_ltr_set_small(buf) | fis_ltr_set_pair(buf);
 }
 
 int fis_abi_version(void) { return FIS_ABI_VERSION; }
@@ -83,14 +87,16 @@ static int fis_choose_splits(const fis_gemm_args* a, bool tc) {
 // Which kernel fis_gemm would run for these arguments: 0 SIMT, 1 per-op tcgen05, 2 persistent
 // large-M tcgen05 (csrc/fis_gemm_big.cu), 3 per-op tcgen05 3xTF32 (fp32 operands), 4 halo-staged
 // persistent gather conv (csrc/fis_gemm_halo.cu), 5 few-input-channel 3x3 conv on the FMA pipes
-// (csrc/fis_conv_small.cu). Host-only query (no launch).
+// (csrc/fis_conv_small.cu), 6 persistent 2-SM (CTA pair, cta_group::2) GEMM with TMA-staged A
+// (csrc/fis_gemm_pair.cu). Host-only query (no launch).
 int fis_gemm_kernel_kind(const fis_gemm_args* a) {
     if (a->impl == 3) return fis_gemm_tf32_supported(a) ? 3 : 0;
     if (a->impl == 0 && fis_conv_small_ok(a)) return 5;
     if (a->impl == 0 && fis_gemm_halo_ok(a)) return 4;
     const bool tc = a->impl == 2 || (a->impl == 0 && fis_gemm_tc_supported(a));
     if (!tc) return 0;
-    return a->impl == 0 && fis_gemm_big_eligible(a) ? 2 : 1;
+    if (a->impl == 0 && fis_gemm_big_eligible(a)) return fis_gemm_pair_ok(a, fis_gemm_big_bn(a->n)) ? 6 : 2;
+    return 1;
 }
 
 int fis_gemm(const fis_gemm_args* a, void* stream) {
@@ -120,6 +126,10 @@ int fis_gemm(const fis_gemm_args* a, void* stream) {
     }
     // large M (stacked requests): persistent tcgen05 kernel with TMA weights (fis_gemm_big.cu)
     if (tc && a->impl == 0 && fis_gemm_big_eligible(a)) {
+        if (fis_gemm_pair_ok(a, fis_gemm_big_bn(a->n))) {  // 2-SM tiles: half the B traffic per SM
+            const int rc = fis_gemm_pair_launch(a, (cudaStream_t)stream);
+            if (rc != FIS_ERR_UNSUPPORTED) return rc;
+        }
         const int rc = fis_gemm_big_launch(a, (cudaStream_t)stream);
         if (rc != FIS_ERR_UNSUPPORTED) return rc;
     }

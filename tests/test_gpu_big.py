@@ -187,3 +187,62 @@ def test_small_cin_stem_conv(env, R, h, w, cout, sparse):
     if sparse:
         y = y[rows.long()]
     assert (out.float() - y).abs().max().item() <= 3e-2 * max(1.0, y.abs().max().item())
+
+
+@pytest.mark.parametrize("R,h,w,cin,cout,two", [(32, 16, 16, 128, 512, False), (8, 32, 32, 128, 256, True),
+                                                 (48, 8, 8, 64, 768, False)])
+def test_pair_kernel_dense_conv(env, R, h, w, cin, cout, two):
+    """The 2-SM CTA-pair GEMM (csrc/fis_gemm_pair.cu, tcgen05 cta_group::2, M = 256): dense stacked
+    3x3 conv (one or two concatenated sources, 4-D TMA taps) against the single-SM persistent kernel
+    and torch; the pair kernel must really run (launch counter)."""
+    import ctypes
+    L, DRef, NULL, lz = env
+    g = torch.Generator(device="cuda").manual_seed(R + cout)
+    hw = h * w
+    x = _rnd(g, R * hw, cin)
+    x2 = _rnd(g, R * hw, cin) if two else None
+    ct = cin * (2 if two else 1)
+    W = _rnd(g, cout, 9 * ct, scale=1 / math.sqrt(9 * ct))
+    bias = torch.randn(cout, device="cuda", generator=g)
+    out = torch.empty((R * hw, cout), device="cuda", dtype=torch.bfloat16)
+    srcs = [L.Src(DRef(x).ref(), NULL, None, h, w, cin, 0)]
+    if two:
+        srcs.append(L.Src(DRef(x2).ref(), NULL, None, h, w, cin, 0))
+    res = []
+    for mode in ("2", "0"):
+        os.environ["FIS_PAIR"] = mode
+        out.zero_()
+        n0 = L.lib().fis_gemm_pair_launch_count()
+        lz.gemm(R * hw, cout, 9 * ct, srcs=srcs, out_hw=(h, w), b=DRef(W), d=DRef(out), bias=bias)
+        torch.cuda.synchronize()
+        ran = L.lib().fis_gemm_pair_launch_count() > n0
+        assert ran == (mode == "2"), "pair kernel launch state"
+        if mode == "2":
+            assert L.lib().fis_gemm_kernel_kind(ctypes.byref(lz.last_gemm)) == 6
+        res.append(out.clone())
+    os.environ.pop("FIS_PAIR", None)
+    xi = x.float().reshape(R, h, w, cin)
+    if two:
+        xi = torch.cat([xi, x2.float().reshape(R, h, w, cin)], dim=3)
+    Wk = W.float().reshape(cout, 3, 3, ct).permute(0, 3, 1, 2)
+    ref = torch.nn.functional.conv2d(xi.permute(0, 3, 1, 2), Wk, bias, padding=1).permute(0, 2, 3, 1).reshape(R * hw, cout)
+    assert (res[0].float() - ref).abs().max().item() <= 5e-2
+    assert (res[0].float() - res[1].float()).abs().max().item() <= 2e-2  # vs the single-SM kernel
+
+
+def test_pair_kernel_rows(env):
+    L, DRef, NULL, lz = env
+    g = torch.Generator(device="cuda").manual_seed(11)
+    m, k, n = 5000, 640, 1280  # ragged last pair tile
+    A = _rnd(g, m, k)
+    B = _rnd(g, n, k, scale=1 / math.sqrt(k))
+    res = _rnd(g, m, n)
+    D = torch.empty((m, n), device="cuda", dtype=torch.bfloat16)
+    os.environ["FIS_PAIR"] = "2"
+    n0 = L.lib().fis_gemm_pair_launch_count()
+    lz.gemm(m, n, k, a=DRef(A), b=DRef(B), d=DRef(D), res=DRef(res))
+    torch.cuda.synchronize()
+    os.environ.pop("FIS_PAIR", None)
+    assert L.lib().fis_gemm_pair_launch_count() > n0
+    ref = A.float() @ B.float().t() + res.float()
+    assert (D.float() - ref).abs().max().item() <= 5e-2
