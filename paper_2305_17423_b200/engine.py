@@ -601,7 +601,7 @@ class Engine(Launcher):
             elif op == "fuse":
                 lid, fu, fs, fo = ins[1], ins[2], ins[3], ins[4]
                 up = vals[fu.key]
-                if not plan.sparse(fo.level) and up.index is None and self.act == torch.bfloat16:
+                if not plan.sparse(fo.level) and up.index is None and self.act == torch.bfloat16 and self.capture is None:
                     # dense level: materialise the 2x upsample once so the fuse conv's A operand is a
                     # dense map the GEMM stages with TMA (one 4-D box per tap)
                     buf = DRef(self.scratch(f"up{fo.level}", (self.cap(fo.level), fu.channels)))

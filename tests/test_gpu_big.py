@@ -37,6 +37,7 @@ def _both(run, out):
     the first run really launched the persistent kernel (no silent fallback)."""
     from paper_2305_17423_b200 import _lib as L
     res = []
+    os.environ["FIS_PAIR"] = "0"  # the single-SM persistent kernel (the CTA-pair kernel has its own tests)
     for big in ("1", "0"):
         os.environ["FIS_BIG"] = big
         out.zero_()
@@ -47,6 +48,7 @@ def _both(run, out):
             assert L.lib().fis_gemm_big_launch_count() > n0, "persistent GEMM fell back to the per-op kernel"
         res.append(out.clone())
     os.environ.pop("FIS_BIG", None)
+    os.environ.pop("FIS_PAIR", None)
     return res
 
 
@@ -64,7 +66,7 @@ def test_rows_and_qkv_split(env):
     bias = torch.randn(c, device="cuda", generator=g)
     D = torch.empty((m, c), device="cuda", dtype=torch.bfloat16)
     r = _both(lambda: lz.gemm(m, c, k, a=DRef(A), b=DRef(B), d=DRef(D), bias=bias, res=DRef(res)), D)
-    assert _kind(lz) == 2
+    assert _kind(lz) in (2, 6)  # persistent single-SM or CTA-pair kernel for this shape
     assert torch.equal(r[0], r[1])
     ref = (A.float() @ B[:c].float().t() + bias + res.float())
     assert (r[0].float() - ref).abs().max().item() <= 5e-2
@@ -93,7 +95,7 @@ def test_dense_stacked_conv(env, R, h, w, cin, cout):
     out = torch.empty((R * hw, cout), device="cuda", dtype=torch.bfloat16)
     src = L.Src(DRef(x).ref(), NULL, None, h, w, cin, 0)
     r = _both(lambda: lz.gemm(R * hw, cout, 9 * cin, srcs=[src], out_hw=(h, w), b=DRef(W), d=DRef(out)), out)
-    assert _kind(lz) == 2
+    assert _kind(lz) in (2, 6)  # persistent single-SM or CTA-pair kernel for this shape
     assert torch.equal(r[0], r[1])
     xi = x.float().reshape(R, h, w, cin).permute(0, 3, 1, 2)
     Wk = W.float().reshape(cout, 3, 3, cin).permute(0, 3, 1, 2)
@@ -128,7 +130,7 @@ def test_gathered_conv_with_gn_silu(env):
     run = lambda: lz.gemm(n, cout, 9 * cin, rows=rows, srcs=[src], out_hw=(h, w), b=DRef(W), d=DRef(out), bias=bias,
                           epi=L.EPI_GN_SILU, gn=(DRef(mean), DRef(var), gamma, beta, groups))
     r = _both(run, out)
-    assert _kind(lz) == 2
+    assert _kind(lz) in (2, 6)  # persistent single-SM or CTA-pair kernel for this shape
     assert torch.equal(r[0], r[1])
     # reference: select-on-read map, conv, cached-stat GN, SiLU (fp32 on the same bf16 values)
     full = cache.float().clone()
