@@ -932,6 +932,10 @@ static bool attn_share(const fis_attn_args* a, int dvs) {
     // (r02: forcing it for the d = 1280 levels measured 27.6 vs 29.1 us for L2 self attention,
     // but more for cross attention; a wash at the step level)
     if (ctas < 148) return false;
+    // runs of >= 3 key blocks over <= 2 value slices: the one-pass kernel (no statistics pass)
+    // recomputes S once per slice, cheaper than P_OUT's two S passes + the P_IN launch (r02, R = 64:
+    // L0 self attention 131 -> 113 us; at 5 slices sharing still wins)
+    if (slices <= 2 && a->max_seg_k > 256) return false;
     // one key block: recomputing S per slice is cheap unless the head dim is large (r01: L0 cross
     // attention 23 + 48 us shared vs one launch unshared)
     if (a->max_seg_k <= 128) return (long long)a->d * (slices - 1) >= 1280;

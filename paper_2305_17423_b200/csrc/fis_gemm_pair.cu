@@ -38,7 +38,8 @@ constexpr int B_BYTES = (BN / 2) * BK * 2;    // 16 KB: this CTA's half of the B
 constexpr int STAGE = A_BYTES + B_BYTES;
 constexpr int STAGES = 6;
 constexpr int AM_ROWS = 1, AM_CONV = 2;
-constexpr int SMEM = STAGES * STAGE + 1024 + 256 + 6 * BN * 4 + 64;
+constexpr int STG_BYTES = 8 * 16 * 32 * 2;  // per epilogue warp: a 16-column x 32-row bf16 transpose tile
+constexpr int SMEM = STAGES * STAGE + 1024 + 256 + 6 * BN * 4 + STG_BYTES + 64;
 
 FIS_DEV uint32_t cluster_rank() {
     uint32_t r;
@@ -97,6 +98,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     uint64_t* acc_empty = acc_full + 2;   // [2]
     uint32_t* tmem_slot = (uint32_t*)(acc_empty + 2);
     float* tabs = (float*)(smem + STAGES * STAGE + 256);
+    __nv_bfloat16* stg_all = (__nv_bfloat16*)(tabs + 6 * BN);  // [8 warps][16][32]
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const uint32_t rank = cluster_rank();
@@ -210,8 +212,12 @@ __global__ void __launch_bounds__(THREADS, 1)
         const int lr = quarter * 32 + lane;
         const EpiCtx e = make_epi(a, t);
         const bool fast = a.epi == FIS_EPI_NONE && a.alpha == 1.0f && !e.pre && !e.pre2 && !e.bias2 && !e.lat &&
-                          !a.d_rows && !a.d_trans && a.n_split == 0 && a.d.dtype == FIS_BF16 && (a.d.ld % 8) == 0 &&
+                          !a.d_rows && !a.d_trans && a.d.dtype == FIS_BF16 && (a.d.ld % 8) == 0 &&
                           (((uintptr_t)e.d) & 15) == 0 && (!e.res || (a.res.ld % 8) == 0);
+        // fused QKV: the V^T part (n >= n_split) goes transposed to d2 through a per-warp staging tile
+        const bool tfast = fast && !e.res && a.n_split > 0 && a.d2_trans && a.d2.dtype == FIS_BF16 &&
+                           (a.d2.ld % 8) == 0 && (((uintptr_t)e.d2) & 15) == 0;
+        const int nrow_end = a.n_split > 0 ? a.n_split : a.n;  // row-major columns
         EpiTab tb;
         tb.mean = tabs;
         tb.rstd = tb.mean + BN;
@@ -253,11 +259,33 @@ __global__ void __launch_bounds__(THREADS, 1)
                 uint32_t u[16];
                 tmem_ld16(taddr + cb, u);
                 const int n = n0 + cb;
+                if (tfast && n >= a.n_split && n + 16 <= a.n) {  // warp-uniform: V^T chunk
+                    __nv_bfloat16* stg = stg_all + (warp < TMA_WARP ? warp + 4 : warp - 6) * (16 * 32);
+#pragma unroll
+                    for (int j = 0; j < 16; j++)
+                        stg[j * 32 + lane] = __float2bfloat16_rn(__fadd_rn(__uint_as_float(u[j]), tb.bias[cb + j]));
+                    __syncwarp();
+                    const int r0 = m0 + quarter * 32, dn = n - a.n_split;
+#pragma unroll
+                    for (int q = 0; q < 2; q++) {
+                        const int idx = lane + 32 * q, j = idx >> 2, p8 = (idx & 3) * 8;
+                        const uint4 val = *(const uint4*)(stg + j * 32 + p8);
+                        __nv_bfloat16* dst = (__nv_bfloat16*)e.d2 + (long long)(dn + j) * a.d2.ld + r0 + p8;
+                        if (r0 + p8 + 8 <= a.m) {
+                            *(uint4*)dst = val;
+                        } else {
+                            const __nv_bfloat16* sv = (const __nv_bfloat16*)&val;
+                            for (int i = 0; i < 8 && r0 + p8 + i < a.m; i++) dst[i] = sv[i];
+                        }
+                    }
+                    __syncwarp();
+                    continue;
+                }
                 if (r >= a.m || n >= a.n) continue;
                 float v[16];
 #pragma unroll
                 for (int j = 0; j < 16; j++) v[j] = __uint_as_float(u[j]);
-                if (fast && n + 16 <= a.n) {
+                if (fast && n + 16 <= nrow_end) {
 #pragma unroll
                     for (int j = 0; j < 16; j++) v[j] = __fadd_rn(v[j], tb.bias[cb + j]);
                     if (e.res) {
@@ -311,9 +339,11 @@ int fis_gemm_pair_ok(const fis_gemm_args* a, int single_bn) {
     // FIS_PAIR=0 disables, =2 forces (read per call: tests switch it; fis_gemm runs at capture time)
     const char* env = getenv("FIS_PAIR");
     const int off = env && env[0] == '0', force = env && env[0] == '2';
-    if (off || a->splits > 1 || a->b.step_stride || a->b.dtype != FIS_BF16 || (a->b.ld % 8) || a->d_trans ||
-        a->n_split > 0 || a->rows || a->n < 256)
+    if (off || a->splits > 1 || a->b.step_stride || a->b.dtype != FIS_BF16 || (a->b.ld % 8) || a->d_trans || a->rows ||
+        a->n < 256)
         return 0;
+    // fused QKV (V^T to d2): 16-column chunks never straddle the split
+    if (a->n_split > 0 && (a->n_split % 16 || !a->d2_trans)) return 0;
     CUtensorMap ta, ta2;
     if (!fis_tma_a_encode(a, &ta, &ta2)) return 0;
     const long long sms = pair_sms();

@@ -248,3 +248,30 @@ def test_pair_kernel_rows(env):
     assert L.lib().fis_gemm_pair_launch_count() > n0
     ref = A.float() @ B.float().t() + res.float()
     assert (D.float() - ref).abs().max().item() <= 5e-2
+
+
+def test_pair_kernel_qkv_split(env):
+    """Fused QKV on the CTA-pair kernel: Q' row-major, V^T transposed into d2 (per-warp staging)."""
+    L, DRef, NULL, lz = env
+    g = torch.Generator(device="cuda").manual_seed(12)
+    m, k, c = 4000, 640, 640
+    A = _rnd(g, m, k)
+    B = _rnd(g, 2 * c, k, scale=1 / math.sqrt(k))
+    bias = torch.randn(2 * c, device="cuda", generator=g)
+    outs = []
+    for mode in ("2", "0"):
+        os.environ["FIS_PAIR"] = mode
+        qk = torch.zeros((m, c), device="cuda", dtype=torch.bfloat16)
+        vt = torch.zeros((c, 4096), device="cuda", dtype=torch.bfloat16)
+        n0 = L.lib().fis_gemm_pair_launch_count()
+        lz.gemm(m, 2 * c, k, a=DRef(A), b=DRef(B), d=DRef(qk), bias=bias, n_split=c, d2=DRef(vt, ld=4096),
+                d2_trans=True)
+        torch.cuda.synchronize()
+        assert (L.lib().fis_gemm_pair_launch_count() > n0) == (mode == "2")
+        outs.append((qk.clone(), vt.clone()))
+    os.environ.pop("FIS_PAIR", None)
+    ref = A.float() @ B.float().t() + bias
+    assert (outs[0][0].float() - ref[:, :c]).abs().max().item() <= 5e-2
+    assert (outs[0][1][:, :m].float().t() - ref[:, c:]).abs().max().item() <= 5e-2
+    assert (outs[0][0].float() - outs[1][0].float()).abs().max().item() <= 2e-2
+    assert (outs[0][1].float() - outs[1][1].float()).abs().max().item() <= 2e-2
