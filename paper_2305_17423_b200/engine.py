@@ -98,9 +98,12 @@ class Weights:
             else:
                 # wq [C_in, C_out] as the reference stores it (q = g . wq): the per-edit score matrix
                 # M^T = K . wq^T... see Engine.text_kv
+                # text K / V weights: fp32 in the fp32 / tf32x3 modes; bf16 (like every other weight)
+                # in bf16 mode so the per-edit text K / V GEMMs run on the tensor cores
+                wt = f32 if act == f32 else act
                 self.ca[i.layer_id] = (torch.from_numpy(np.ascontiguousarray(p["wq"])).to(dev, act),
-                                       torch.from_numpy(np.ascontiguousarray(p["wk_text"].T)).to(dev, f32),
-                                       torch.from_numpy(np.ascontiguousarray(p["wv_text"].T)).to(dev, f32),
+                                       torch.from_numpy(np.ascontiguousarray(p["wk_text"].T)).to(dev, wt),
+                                       torch.from_numpy(np.ascontiguousarray(p["wv_text"].T)).to(dev, wt),
                                        1.0 / math.sqrt(i.channels))
         self.time_bias = torch.from_numpy(topo["time_bias"]).to(dev, f32)
 
@@ -148,6 +151,7 @@ class Launcher:
         # capture mode: launches are recorded as (entry point, args) for the step VM instead of run
         self.capture: list | None = None
         self.use_vm = precision == "bf16" and os.environ.get("FIS_VM", "0") == "1"
+        self._kv_graphs = {}  # (n_text, text_dim) -> (graph, embedding buffer, outputs) of text_kv
 
     def _call(self, name, args, b_static=False):
         if self.capture is not None:
@@ -385,18 +389,57 @@ class Engine(Launcher):
 
         Cross attention reassociates its scores: (x wq) K^T = x (wq K^T) = x M, so the step feeds
         the layer input x straight into the attention kernel with M^T as its key matrix and skips
-        the per-step query projection (one launch and a C x C GEMM per cross layer and step)."""
-        nt = text_emb.shape[0]
-        emb = torch.from_numpy(np.ascontiguousarray(text_emb, dtype=np.float32)).to(self.dev)
+        the per-step query projection (one launch and a C x C GEMM per cross layer and step).
+
+        The 3 GEMMs x cross layers run as one captured CUDA graph per prompt length (the Python
+        launch overhead of ~42 GEMM calls was ~4.5 ms of every edit); every call copies the new
+        embeddings in, replays, and returns fresh copies of the outputs."""
+        emb_h = torch.from_numpy(np.ascontiguousarray(text_emb, dtype=np.float32))
+        if self.capture is not None or os.environ.get("FIS_KV_GRAPH", "1") == "0":
+            return self._text_kv(emb_h.to(self.dev))
+        key = tuple(emb_h.shape)
+        ent = self._kv_graphs.get(key)
+        if ent is None:
+            emb_buf = emb_h.to(self.dev)
+            self._text_kv(emb_buf)  # warm-up outside the capture
+            torch.cuda.synchronize()
+            g = torch.cuda.CUDAGraph()
+            s = torch.cuda.Stream()
+            s.wait_stream(torch.cuda.current_stream())
+            import gc
+            gc_on = gc.isenabled()
+            gc.disable()
+            try:
+                with torch.cuda.stream(s):
+                    with torch.cuda.graph(g, stream=s):
+                        outs = self._text_kv(emb_buf)
+            finally:
+                if gc_on:
+                    gc.enable()
+            torch.cuda.current_stream().wait_stream(s)
+            ent = self._kv_graphs[key] = (g, emb_buf, outs)
+        g, emb_buf, outs = ent
+        emb_buf.copy_(emb_h)
+        g.replay()
+        return {lid: tuple(x.clone() if x is not None else None for x in kv) for lid, kv in outs.items()}
+
+    def _text_kv(self, emb: torch.Tensor):
+        nt = emb.shape[0]
         out = {}
+        # bf16 mode: the embeddings as bf16 operands -> tcgen05 split-K GEMMs (fp32 embeddings would
+        # take the SIMT kernel: ~100 us per layer GEMM); fp32 / tf32x3 keep the unsplit fp32 path
+        bf = self.act == torch.bfloat16
+        if bf:
+            emb = emb.to(torch.bfloat16)
+        sp = None if bf else 1
         for lid, (wq, wk, wv, scale) in self.W.ca.items():
             c = wq.shape[0]
             k = torch.empty((nt, c), dtype=self.act, device=self.dev)
             vt = torch.zeros((c, _pad(nt)), dtype=self.act, device=self.dev)
             mt = torch.empty((nt, c), dtype=self.act, device=self.dev)
-            self.gemm(nt, c, emb.shape[1], a=DRef(emb), b=DRef(wk), d=DRef(k), splits=1)
-            self.gemm(nt, c, emb.shape[1], a=DRef(emb), b=DRef(wv), d=DRef(vt), d_trans=True, splits=1)
-            self.gemm(nt, c, c, a=DRef(k), b=DRef(wq), d=DRef(mt), splits=1)
+            self.gemm(nt, c, emb.shape[1], a=DRef(emb), b=DRef(wk), d=DRef(k), splits=sp)
+            self.gemm(nt, c, emb.shape[1], a=DRef(emb), b=DRef(wv), d=DRef(vt), d_trans=True, splits=sp)
+            self.gemm(nt, c, c, a=DRef(k), b=DRef(wq), d=DRef(mt), splits=sp)
             v = None
             if self.fused_xattn:  # row-major V only for the SIMT cross-attention kernel
                 v = torch.empty((nt, c), dtype=self.act, device=self.dev)
@@ -415,6 +458,8 @@ class Engine(Launcher):
         for r, e in enumerate(text_embs):
             emb[r * ks: r * ks + nts[r]] = e
         emb_d = torch.from_numpy(emb).to(self.dev)
+        if self.act == torch.bfloat16:  # tensor-core GEMMs with the bf16 text K / V weights
+            emb_d = emb_d.to(torch.bfloat16)
         out = {}
         for lid, (wq, wk, wv, scale) in self.W.ca.items():
             c = wq.shape[0]

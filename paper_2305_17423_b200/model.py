@@ -244,16 +244,18 @@ def step_program(config: UNetConfig, topo):
 def lcs_pairs(old_ids, new_ids):
     """(old index, new index) pairs of the longest common subsequence (unet.py:174-195)."""
     la, lb = len(old_ids), len(new_ids)
-    dp = np.zeros((la + 1, lb + 1), dtype=np.int32)
+    # plain Python rows (numpy scalar indexing made this ~2 ms for 77 x 77 tokens)
+    dp = [[0] * (lb + 1) for _ in range(la + 1)]
     for i in range(1, la + 1):
+        a, prev, row = old_ids[i - 1], dp[i - 1], dp[i]
         for j in range(1, lb + 1):
-            dp[i, j] = dp[i - 1, j - 1] + 1 if old_ids[i - 1] == new_ids[j - 1] else max(dp[i - 1, j], dp[i, j - 1])
+            row[j] = prev[j - 1] + 1 if a == new_ids[j - 1] else (prev[j] if prev[j] >= row[j - 1] else row[j - 1])
     pairs, i, j = [], la, lb
     while i > 0 and j > 0:
         if old_ids[i - 1] == new_ids[j - 1]:
             pairs.append((i - 1, j - 1))
             i, j = i - 1, j - 1
-        elif dp[i - 1, j] >= dp[i, j - 1]:
+        elif dp[i - 1][j] >= dp[i][j - 1]:
             i -= 1
         else:
             j -= 1
