@@ -661,12 +661,12 @@ def stacked_requests(eng, U, P, cfg, args, peak_tf, ids):
     run = U._Runner(eng, bp.plan, True, ns=0)
     ms = _time_runner(run, cfg.steps, max(5, args.steps // 2), 3)
     # end to end through the public API: R sessions (host masks, prompts) in, R host latents out;
-    # one untimed call first (its graph capture and allocations), then the median of two calls
+    # one untimed call first (its graph capture and allocations), then the median of three calls
     mk = lambda: [P.EditSession.create(o, n, cfg, st_, user_mask=P.BinaryMask(b)) for (o, n, b), st_ in zip(reqs, stores)]
     P.edit_batch(mk(), cfg)
     import gc
     e2e_calls = []
-    for _ in range(2):
+    for _ in range(3):
         sessions = mk()
         gc.collect()
         torch.cuda.synchronize()
@@ -711,7 +711,7 @@ def stacked_requests(eng, U, P, cfg, args, peak_tf, ids):
             "gated_conv": gc_, "kernels": kern,
             "e2e": {"edit_steps_per_s": R * cfg.steps / e2e_s, "seconds": e2e_s,
                     "call_seconds": [round(x, 4) for x in e2e_calls],
-                    "note": "median of 2 edit_batch() calls after an untimed one: R sessions (host masks, prompts) -> "
+                    "note": "median of 3 edit_batch() calls after an untimed one: R sessions (host masks, prompts) -> "
                             "R host latents, all T steps incl. planning and graph capture"},
             "result_gather": {"requests_on_rank0": len(gathered), "seconds": gather_s},
             "setup_generation_s": setup_s,
