@@ -680,21 +680,25 @@ class BatchedEditPlan:
 
 
 def edit_batch(sessions, config: UNetConfig) -> list:
-    """R edits whose stores come from one `generate_dense_batch`, stepped as ONE stacked batch.
+    """Edits whose stores come from one `generate_dense_batch` (any subset of its generations, one
+    session each), stepped as ONE stacked batch.
 
     Per request this matches `edit(session, config, session.store)` (unet.py:823-899) up to the
     bf16 bound: masks (user or detected) and prompts are per request; all requests must share
-    the sparse phase's first step (same t2 with detection, or all user masks). Returns one
-    EditResult per session (MAC reports omitted: `macs` is None)."""
+    the sparse phase's first step (same t2 with detection, or all user masks). Generations of the
+    batch without a session ride along with an empty mask (no active rows) and are not returned.
+    Returns one EditResult per session, in the given order."""
     if not sessions:
         return []
     views = [s.store.arena for s in sessions]
     stacked = getattr(views[0], "stacked", None)
+    idx = [getattr(v, "index", -1) for v in views]
     if stacked is None or any(getattr(v, "stacked", None) is not stacked for v in views) or \
-            sorted(v.index for v in views) != list(range(stacked.batch)):
-        raise ContractViolation("edit_batch needs the stores of one generate_dense_batch, one session each")
+            len(set(idx)) != len(idx) or min(idx) < 0 or max(idx) >= stacked.batch:
+        raise ContractViolation("edit_batch needs stores of one generate_dense_batch, one session each")
     order = sorted(range(len(sessions)), key=lambda i: views[i].index)
     sessions = [sessions[i] for i in order]
+    views = [views[i] for i in order]
     outcomes = [detect_mask(s, config, s.store) for s in sessions]
     starts = {1 if o.from_user_mask else s.t2 + 1 for s, o in zip(sessions, outcomes)}
     if len(starts) != 1:
@@ -721,15 +725,25 @@ def edit_batch(sessions, config: UNetConfig) -> list:
     full = [o.mask is not None and o.mask.all_active() for o in outcomes]
     batch_masks = [BinaryMask(np.zeros((H, W), dtype=bool)) if f else m for f, m in zip(full, masks)]
     texts = [embed_tokens(s.new_tokens, config) for s in sessions]
-    skv = eng.text_kv_stacked(texts)
-    bp = BatchedEditPlan(eng, stacked, batch_masks, None, lat0s, stacked_kv=skv)
+    # generations of the stacked batch without a session: empty mask, any prompt / start latent
+    nb = stacked.batch
+    slot = {v.index: r for r, v in enumerate(views)}
+    empty = BinaryMask(np.zeros((H, W), dtype=bool))
+    if len(slot) < nb and lat_init is None:
+        lat_init = _to_nhwc(initial_latent_np(config), eng.dev)
+    b_masks = [batch_masks[slot[i]] if i in slot else empty for i in range(nb)]
+    b_lat0 = [lat0s[slot[i]] if i in slot else lat_init for i in range(nb)]
+    b_texts = [texts[slot[i]] if i in slot else texts[0] for i in range(nb)]
+    skv = eng.text_kv_stacked(b_texts)
+    bp = BatchedEditPlan(eng, stacked, b_masks, None, b_lat0, stacked_kv=skv)
     _Runner(eng, bp.plan, _use_graphs()).run(start, T)
     final = bp.final_latents(eng, stacked)
     hw = eng.hw(0)
+    img = [v.index for v in views]  # stacked image of each (sorted) session
     for r, f in enumerate(full):
         if f:
-            final[r * hw:(r + 1) * hw] = _dense_edit(eng, eng.text_kv(texts[r]), lat0s[r], start)
-    fin = final.view(len(sessions), H, W, cl).permute(0, 3, 1, 2).contiguous().cpu().numpy()  # one D2H
+            final[img[r] * hw:(img[r] + 1) * hw] = _dense_edit(eng, eng.text_kv(texts[r]), lat0s[r], start)
+    fin = final.view(nb, H, W, cl).permute(0, 3, 1, 2).contiguous().cpu().numpy()  # one D2H
     unet = UNet(config)
     results = [None] * len(sessions)
     for r, (s, o) in enumerate(zip(sessions, outcomes)):
@@ -740,9 +754,9 @@ def edit_batch(sessions, config: UNetConfig) -> list:
             if full[r]:
                 _add_dense_macs(phase2, unet, n_new, T - start + 1)
             else:
-                _add_sparse_macs(phase2, unet, n_new, bp.dps[r], T - start + 1)
-                plans = _gather_plans(unet, bp.dps[r])
+                _add_sparse_macs(phase2, unet, n_new, bp.dps[img[r]], T - start + 1)
+                plans = _gather_plans(unet, bp.dps[img[r]])
         rep = _build_report(unet, n_new, config, [o.phase1_macs, phase2])
-        results[order[r]] = EditResult(fin[r:r + 1], rep, s.store.stats(), o.mask, o.no_edit,
+        results[order[r]] = EditResult(fin[img[r]:img[r] + 1], rep, s.store.stats(), o.mask, o.no_edit,
                                        o.phase1_macs.total, phase2.total, plans)
     return results

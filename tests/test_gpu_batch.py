@@ -131,3 +131,36 @@ def test_edit_batch_rejects_foreign_stores(P):
     with pytest.raises(P.ContractViolation):
         P.edit_batch([P.EditSession.create((3, 5, 7, 11), (3, 5, 9, 11), cfg, store,
                                            user_mask=P.centered_square_mask(32, 32, 0.1))], cfg)
+
+
+def test_edit_batch_subset_in_any_order(P):
+    """Any subset of one generate_dense_batch, sessions in any order: the missing generations ride
+    along with empty masks, each returned result equals its own edit() (bf16 bound) and keeps its
+    own generation outside the mask bit-exactly; detected masks read their own generation."""
+    cfg = _cfg(P)
+    stores = [P.CacheStore() for _ in REQS]
+    finals = P.generate_dense_batch([P.PromptTokens(o) for o, _, _ in REQS], cfg, stores)
+    pick = [3, 1]  # a subset, out of order
+    sessions = []
+    for i in pick:
+        old, new, (y0, x0, side) = REQS[i]
+        sessions.append(P.EditSession.create(old, new, cfg, stores[i], user_mask=P.BinaryMask(_square(32, 32, y0, x0, side))))
+    res = P.edit_batch(sessions, cfg)
+    assert len(res) == len(pick)
+    for r, i in zip(res, pick):
+        old, new, (y0, x0, side) = REQS[i]
+        m = P.BinaryMask(_square(32, 32, y0, x0, side))
+        assert np.array_equal(r.latent[:, :, ~m.bits], finals[i][:, :, ~m.bits])
+        store = P.CacheStore()
+        P.generate_dense(P.PromptTokens(old), cfg, store, record="engine")
+        one = P.edit(P.EditSession.create(old, new, cfg, store, user_mask=m), cfg, store)
+        assert np.abs(r.latent - one.latent).max() <= BF16_FINAL_TOL
+    # detected masks (no user mask), order reversed
+    det = [P.EditSession.create(REQS[i][0], REQS[i][1], cfg, stores[i]) for i in (2, 0)]
+    res = P.edit_batch(det, cfg)
+    for r, i in zip(res, (2, 0)):
+        store = P.CacheStore()
+        P.generate_dense(P.PromptTokens(REQS[i][0]), cfg, store, record="engine")
+        one = P.edit(P.EditSession.create(REQS[i][0], REQS[i][1], cfg, store), cfg, store)
+        assert np.array_equal(r.mask.bits, one.mask.bits)
+        assert np.abs(r.latent - one.latent).max() <= BF16_FINAL_TOL
