@@ -294,7 +294,7 @@ def replay_kernels(runner, ops, T, reps=9):
     ks.sort()
     want = {"fis_gemm": "gemm", "fis_attn": "attn", "fis_gn": "gn_", "fis_gn_apply": "gn_apply",
             "fis_gn_stats": "gn_stats", "fis_pool2": "pool2", "fis_up2": "up2", "fis_softmax": "softmax",
-            "fis_materialize": "materialize", "fis_xattn": "xattn"}
+            "fis_materialize": "materialize"}
 
     def one(rep):  # per-op critical-path us of one replay's kernel records, or None on a mismatch
         if len(rep) != n_k:

@@ -181,23 +181,6 @@ typedef struct {
 } fis_softmax_args;
 int fis_softmax(const fis_softmax_args* a, void* stream);
 
-/* Fused cross-attention for text contexts of <= 128 tokens: one warp per query row computes
- * softmax(q K^T * scale) V and adds the residual: out = res + attn.  Replaces
- * attention_scores + apply_attention on the text K/V (sparse.py:303-338, 352-361) and the
- * residual add (unet.py:457). */
-typedef struct {
-    int rows, c, n_text;
-    fis_ref q;              /* [rows, ld] query projections */
-    fis_ref k;              /* [n_text, ld] text keys */
-    fis_ref v;              /* [n_text, ld] text values */
-    float scale;
-    fis_ref res;            /* [rows, ld] residual (may be NULL) */
-    fis_ref pre;            /* optional store of the attention output before the residual */
-    fis_ref out;            /* [rows, ld] */
-    const int* step;
-} fis_xattn_args;
-int fis_xattn(const fis_xattn_args* a, void* stream);
-
 /* Fused tensor-core attention (tcgen05): out = res + softmax(Q K^T * scale) V for one query
  * tile of 128 rows x one output-channel slice per CTA; S and the O slice accumulate in TMEM,
  * P goes through a swizzled shared-memory tile into the P.V MMA. Replaces attention_scores +

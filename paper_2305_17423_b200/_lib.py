@@ -65,11 +65,6 @@ class SoftmaxArgs(C.Structure):
                 ("pair_old", C.c_void_p), ("pair_new", C.c_void_p), ("step", C.c_void_p)]
 
 
-class XattnArgs(C.Structure):
-    _fields_ = [("rows", C.c_int), ("c", C.c_int), ("n_text", C.c_int), ("q", Ref), ("k", Ref), ("v", Ref),
-                ("scale", C.c_float), ("res", Ref), ("pre", Ref), ("out", Ref), ("step", C.c_void_p)]
-
-
 class AttnArgs(C.Structure):
     _fields_ = [("m", C.c_int), ("n_keys", C.c_int), ("d", C.c_int), ("dv", C.c_int), ("q", Ref), ("k", Ref),
                 ("vt", Ref), ("scale", C.c_float), ("res", Ref), ("pre", Ref), ("out", Ref), ("step", C.c_void_p),
@@ -122,7 +117,7 @@ VM_KINDS = {"fis_gemm": (1, "gemm"), "fis_softmax": (2, "softmax"), "fis_gn_stat
             "fis_attn": (7, "attn"), "fis_gn": (8, "gn_apply")}
 
 _SIGS = {
-    "fis_gemm": GemmArgs, "fis_attn": AttnArgs, "fis_xattn": XattnArgs, "fis_gn_stats": GnStatsArgs, "fis_gn_apply": GnApplyArgs, "fis_gn": GnApplyArgs, "fis_softmax": SoftmaxArgs,
+    "fis_gemm": GemmArgs, "fis_attn": AttnArgs, "fis_gn_stats": GnStatsArgs, "fis_gn_apply": GnApplyArgs, "fis_gn": GnApplyArgs, "fis_softmax": SoftmaxArgs,
     "fis_pool2": PoolArgs, "fis_up2": PoolArgs, "fis_materialize": MaterializeArgs, "fis_mask_detect": MaskDetectArgs,
     "fis_mask_plan": MaskPlanArgs, "fis_vm_run": VmArgs,
 }

@@ -609,106 +609,4 @@ extern "C" int fis_materialize(const fis_materialize_args* a, void* stream) {
                    cudaSuccess ? FIS_OK : FIS_ERR_LAUNCH;
 }
 
-// ---- fused cross-attention over a short text context (<= 128 tokens), warp per query row
-namespace fis {
-
-template <int CPL>  // channels per lane = C / 32 rounded up (<= 40 for C = 1280)
-__global__ void __launch_bounds__(256) xattn_kernel(const fis_xattn_args a) {
-    const int ls = ltr_begin(12);
-    const int t = cur_step(a.step);  // host-written before the step: read before the wait
-    pdl_trigger();
-    pdl_wait();
-    ltr(ls, 2);
-    const int warps = blockDim.x >> 5;
-    const int row = blockIdx.x * warps + (threadIdx.x >> 5);
-    const int lane = threadIdx.x & 31;
-    if (row >= a.rows) return;
-    const char* qb = ref_base(a.q, t);
-    const char* kb = ref_base(a.k, t);
-    const char* vb = ref_base(a.v, t);
-    // lane owns channels c = lane + 32*i
-    float q[CPL];
-#pragma unroll
-    for (int i = 0; i < CPL; i++) {
-        const int c = lane + 32 * i;
-        q[i] = c < a.c ? load_elem(qb, a.q.dtype, (long long)row * a.q.ld + c) : 0.f;
-    }
-    float sc[4];
-#pragma unroll
-    for (int jb = 0; jb < 4; jb++) {
-        sc[jb] = -INFINITY;
-        if (jb * 32 >= a.n_text) continue;
-#pragma unroll 4
-        for (int jj = 0; jj < 32; jj++) {
-            const int j = jb * 32 + jj;
-            if (j >= a.n_text) break;
-            float d = 0.f;
-#pragma unroll
-            for (int i = 0; i < CPL; i++) {
-                const int c = lane + 32 * i;
-                if (c < a.c) d = fmaf(q[i], load_elem(kb, a.k.dtype, (long long)j * a.k.ld + c), d);
-            }
-            d = warp_sum(d);
-            if (lane == jj) sc[jb] = d * a.scale;
-        }
-    }
-    float m = fmaxf(fmaxf(sc[0], sc[1]), fmaxf(sc[2], sc[3]));
-    m = warp_max(m);
-    float sum = 0.f;
-#pragma unroll
-    for (int jb = 0; jb < 4; jb++) {
-        sc[jb] = (jb * 32 + lane < a.n_text) ? expf(sc[jb] - m) : 0.f;
-        sum += sc[jb];
-    }
-    sum = warp_sum(sum);
-    const float inv = 1.0f / sum;
-    float o[CPL];
-#pragma unroll
-    for (int i = 0; i < CPL; i++) o[i] = 0.f;
-#pragma unroll
-    for (int jb = 0; jb < 4; jb++) {
-        if (jb * 32 >= a.n_text) continue;
-        const float pj_all = sc[jb] * inv;  // softmax weight of token jb*32+lane (f32, tensors.py:192)
-#pragma unroll 4
-        for (int jj = 0; jj < 32; jj++) {
-            const int j = jb * 32 + jj;
-            if (j >= a.n_text) break;
-            const float pj = __shfl_sync(0xffffffffu, pj_all, jj);
-#pragma unroll
-            for (int i = 0; i < CPL; i++) {
-                const int c = lane + 32 * i;
-                if (c < a.c) o[i] = fmaf(pj, load_elem(vb, a.v.dtype, (long long)j * a.v.ld + c), o[i]);
-            }
-        }
-    }
-    char* ob = ref_base(a.out, t);
-    char* pb = a.pre.ptr ? ref_base(a.pre, t) : nullptr;
-    const char* rb = a.res.ptr ? ref_base(a.res, t) : nullptr;
-#pragma unroll
-    for (int i = 0; i < CPL; i++) {
-        const int c = lane + 32 * i;
-        if (c >= a.c) continue;
-        float v = o[i];
-        if (pb) store_elem(pb, a.pre.dtype, (long long)row * a.pre.ld + c, v);
-        if (rb) v = __fadd_rn(v, load_elem(rb, a.res.dtype, (long long)row * a.res.ld + c));
-        store_elem(ob, a.out.dtype, (long long)row * a.out.ld + c, v);
-    }
-}
-
-}  // namespace fis
-
-extern "C" int fis_xattn(const fis_xattn_args* a, void* stream) {
-    if (a->rows == 0) return FIS_OK;
-    if (a->n_text < 1 || a->n_text > 128 || a->c < 1 || a->c > 32 * 40) return FIS_ERR_UNSUPPORTED;
-    const int warps = 8;
-    const dim3 grid((a->rows + warps - 1) / warps), block(32 * warps);
-    cudaError_t e;
-    const int cpl = (a->c + 31) / 32;
-    if (cpl <= 4) e = fis_launch(fis::xattn_kernel<4>, grid, block, 0, (cudaStream_t)stream, *a);
-    else if (cpl <= 10) e = fis_launch(fis::xattn_kernel<10>, grid, block, 0, (cudaStream_t)stream, *a);
-    else if (cpl <= 20) e = fis_launch(fis::xattn_kernel<20>, grid, block, 0, (cudaStream_t)stream, *a);
-    else e = fis_launch(fis::xattn_kernel<40>, grid, block, 0, (cudaStream_t)stream, *a);
-    return e == cudaSuccess ? FIS_OK : FIS_ERR_LAUNCH;
-}
-
 FIS_LTR_SETTER(fis_ltr_set_ops)

@@ -137,7 +137,6 @@ class Launcher:
         # kernels of a step back to ops with it)
         self.op_log: list | None = None
         self._scratch = {}
-        self.fused_xattn = False  # SIMT xattn is latency-bound; superseded by fis_attn
         # tcgen05 fused attention (csrc/fis_attn.cu: TMA-fed, log2 softmax, resident S for <= 256
         # keys, P shared across value slices) instead of S GEMM -> softmax -> P.V GEMM: C2 sparse
         # step 1.416 vs 1.506 ms, dense step 2.83 vs 3.30 ms (r01). Stacked requests always use it
@@ -440,11 +439,7 @@ class Engine(Launcher):
             self.gemm(nt, c, emb.shape[1], a=DRef(emb), b=DRef(wk), d=DRef(k), splits=sp)
             self.gemm(nt, c, emb.shape[1], a=DRef(emb), b=DRef(wv), d=DRef(vt), d_trans=True, splits=sp)
             self.gemm(nt, c, c, a=DRef(k), b=DRef(wq), d=DRef(mt), splits=sp)
-            v = None
-            if self.fused_xattn:  # row-major V only for the SIMT cross-attention kernel
-                v = torch.empty((nt, c), dtype=self.act, device=self.dev)
-                self.gemm(nt, c, emb.shape[1], a=DRef(emb), b=DRef(wv), d=DRef(v), splits=1)
-            out[lid] = (k, vt, v, mt)
+            out[lid] = (k, vt, None, mt)
         return out
 
     def text_kv_stacked(self, text_embs):
@@ -517,13 +512,6 @@ class Engine(Launcher):
         # scores x (wq K^T) = x M: the layer input is the query, M^T (per edit) the key matrix
         if segs is not None:
             self.attn(m, nt, c, x, DRef(mt), DRef(vt), scale, x, out, pre, segs=segs)
-            return
-        if ctrl is None and map_ is None and nt <= 128 and self.fused_xattn:
-            # scores + softmax + P.V + residual in one launch (text context <= 128 tokens)
-            a = L.XattnArgs(m, c, nt, x.ref(), DRef(mt).ref(), DRef(v).ref(), scale, x.ref(), _r(pre),
-                            out.ref(), L.ptr(self.step_dev))
-            self._call("fis_xattn", a)
-            self._count("fis_xattn", m=m, n_keys=nt)
             return
         if ctrl is None and map_ is None and self.use_fused_attn(c, m, nt, pre) and not x.ss:
             self.attn(m, nt, c, x, DRef(mt), DRef(vt), scale, x, out, pre)

@@ -41,7 +41,7 @@ def test_struct_layout_matches_header():
                "fis_softmax_args": Lb.SoftmaxArgs, "fis_pool_args": Lb.PoolArgs,
                "fis_materialize_args": Lb.MaterializeArgs, "fis_mask_detect_args": Lb.MaskDetectArgs,
                "fis_mask_plan_args": Lb.MaskPlanArgs,
-               "fis_attn_args": Lb.AttnArgs, "fis_xattn_args": Lb.XattnArgs, "fis_vm_op": Lb.VmOp,
+               "fis_attn_args": Lb.AttnArgs, "fis_vm_op": Lb.VmOp,
                "fis_vm_args": Lb.VmArgs}
     body = "\n".join(f'printf("{n} %zu\\n", sizeof({n}));' for n in structs)
     code = f'#include <stdio.h>\n#include "fisedit.h"\nint main(void){{ {body} return 0; }}\n'
