@@ -333,8 +333,10 @@ static int pair_sms() {
 }
 
 // The pair kernel takes large-M GEMMs whose A the TMA can stage (dense conv taps / contiguous rows),
-// static bf16 weights, no split-K / transposed / split outputs, when its 256 x 256 tiles need no more
-// time than the single-SM kernel's tiles (rounds of tiles x width at ~0.85 vs ~0.63 of the peak).
+// static bf16 weights, no split-K / transposed outputs (a fused QKV's V^T half is fine), when its
+// 256 x 256 tiles need no more time than the single-SM kernel's tiles (rounds of tiles x width at the
+// measured ~0.92 vs ~0.55 of the tensor peak: ncu tensor-pipe utilisation of the 64-request step,
+// profiles/r02/ncu_gemms_R64_*.csv).
 int fis_gemm_pair_ok(const fis_gemm_args* a, int single_bn) {
     // FIS_PAIR=0 disables, =2 forces (read per call: tests switch it; fis_gemm runs at capture time)
     const char* env = getenv("FIS_PAIR");
@@ -348,12 +350,12 @@ int fis_gemm_pair_ok(const fis_gemm_args* a, int single_bn) {
     if (!fis_tma_a_encode(a, &ta, &ta2)) return 0;
     const long long sms = pair_sms();
     const long long t2 = (long long)((a->m + 255) / 256) * ((a->n + 255) / 256);
-    const double c2 = (double)((t2 + sms / 2 - 1) / (sms / 2)) * 256 / 0.85;
+    const double c2 = (double)((t2 + sms / 2 - 1) / (sms / 2)) * 256 / 0.92;
     double c1 = 0;
     for (int bn : {single_bn, 320}) {  // the single-SM kernel's 256-wide tiles or 320-wide (two MMAs)
         if (bn == 320 && a->n % 320) continue;
         const long long t1 = (long long)((a->m + 127) / 128) * ((a->n + bn - 1) / bn);
-        const double c = (double)((t1 + sms - 1) / sms) * bn / 0.63;
+        const double c = (double)((t1 + sms - 1) / sms) * bn / 0.55;
         if (c1 == 0 || c < c1) c1 = c;
     }
     return force || c2 < c1;
