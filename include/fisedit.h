@@ -273,81 +273,6 @@ typedef struct {
 } fis_mask_plan_args;
 int fis_mask_plan(const fis_mask_plan_args* a, void* stream);
 
-/* ---------------------------------------------------------------------------------------
- * Persistent step VM.  One CTA per SM executes a whole recorded op list (a UNet step: gather-
- * GEMMs, softmax, group norm, pooling) in a single launch.  Op j's work items are spread over
- * the CTAs starting at CTA cta0 (rotating from op to op); an item waits until every item of
- * op `dep` has completed (a device-scope counter per op), so ops run back to back without
- * launch gaps and the weight (B) tiles of the next GEMM are staged into shared memory while
- * the previous op drains.  Replaces the per-layer dispatch of UNet.forward under SparseMode /
- * DenseMode (unet.py:430-458, 578-663) for a captured step.
- * ------------------------------------------------------------------------------------- */
-#define FIS_VM_GEMM 1
-#define FIS_VM_SOFTMAX 2
-#define FIS_VM_GN_STATS 3
-#define FIS_VM_GN_APPLY 4
-#define FIS_VM_POOL 5
-#define FIS_VM_MATERIALIZE 6
-#define FIS_VM_ATTN 7        /* fused attention (fis_attn_args), keys + value slice <= 512 TMEM columns */
-#define FIS_VM_GN 8          /* group norm: statistics of each group over the full map + normalisation (+SiLU),
-                                one item per group (fis_gn_apply_args: mean / var are written) */
-
-typedef struct {
-    int kind;               /* FIS_VM_* (set by the caller, with the matching args) */
-    int b_static;           /* GEMM, set by the caller: B is not written by any op of the program
-                               (weights, per-edit text K/V), so it may be loaded before `dep` resolves */
-    /* filled by fis_vm_plan */
-    int n_items;            /* work items (GEMM: tiles x splits) */
-    int n_done;             /* completion count (GEMM: output tiles) */
-    int cta0;               /* CTA of item 0 */
-    int dep;                /* op waited for (-1: none) */
-    int dep_target;         /* its n_done */
-    int impl;               /* GEMM: 2 tcgen05, 1 SIMT */
-    int bn, tiles_n, tiles_m, splits;  /* ATTN: bn = value slice, tiles_n = slices, tiles_m = query tiles */
-    int sync_base;          /* GEMM split-K: first per-tile arrival counter */
-    int tmap_a, tmap_b;     /* TMA tensor maps in the plan's map table (-1: cp.async).  GEMM: A (ROWS, or
-                               CONV segment 0 as a 3-D [H][W][C] map) / B.  ATTN: Q / K */
-    int tmap_a2;            /* GEMM: CONV segment 1.  ATTN: V^T */
-    int pad_;
-    union {
-        fis_gemm_args gemm;
-        fis_softmax_args softmax;
-        fis_gn_stats_args gn_stats;
-        fis_gn_apply_args gn_apply;
-        fis_pool_args pool;
-        fis_materialize_args materialize;
-        fis_attn_args attn;
-    } u;
-} fis_vm_op;
-
-/* Plans ops[0..n) for a VM of n_ctas CTAs (0 = one per SM): tiling, split-K, item placement and
- * dependencies.  Returns the workspace floats and sync ints fis_vm_run needs. */
-int fis_vm_plan(fis_vm_op* ops, int n, int n_ctas, long long* ws_floats, int* sync_ints);
-/* Same, also encoding TMA tensor maps (128-byte CUtensorMap records) for the operands TMA can
- * load (plain bf16 matrices, 16-byte aligned) into tmaps[0..cap); *n_tmaps = maps written. */
-int fis_vm_plan_tma(fis_vm_op* ops, int n, int n_ctas, long long* ws_floats, int* sync_ints, void* tmaps, int cap,
-                    int* n_tmaps);
-
-typedef struct {
-    const fis_vm_op* ops;   /* device copy of the planned ops */
-    int n_ops;
-    int n_ctas;             /* as planned */
-    int* sync;              /* sync_ints zeroed ints (reset by the kernel on exit) */
-    int n_sync;             /* sync_ints */
-    float* ws;              /* ws_floats floats (split-K partials) */
-    const int* step;        /* device step index t used by every op of the launch (NULL => 0) */
-    const void* tmaps;      /* device copy of the plan's tensor maps (64-byte aligned) */
-    unsigned long long* trace; /* optional [n_ops][2]: first item start / last item end (globaltimer ns);
-                                  initialise to {~0ull, 0} */
-    int poll_ns;            /* back-off between dependency polls (0 = default) */
-    int trace_op;           /* optional: op whose items record phase stamps ... */
-    unsigned long long* trace_items; /* ... into [n_items][8] (globaltimer ns) */
-} fis_vm_args;
-int fis_vm_run(const fis_vm_args* a, void* stream);
-int fis_vm_op_size(void);
-/* value-slice width the VM uses for an attention op, 0 if the shape is not supported */
-int fis_vm_attn_slice(int m, int n_keys, int d, int dv);
-
 /* profiling: phase timestamps (%globaltimer ns) of CTA (0,0,0) of tcgen05 GEMM launches */
 int fis_trace(int on);
 int fis_trace_read(unsigned long long* out16);

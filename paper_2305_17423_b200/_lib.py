@@ -94,35 +94,14 @@ class MaskPlanArgs(C.Structure):
                 ("index", C.c_void_p * MAX_LEVELS), ("tiles", C.c_void_p * MAX_LEVELS), ("counts", C.c_void_p)]
 
 
-class VmArgsU(C.Union):
-    _fields_ = [("gemm", GemmArgs), ("softmax", SoftmaxArgs), ("gn_stats", GnStatsArgs), ("gn_apply", GnApplyArgs),
-                ("pool", PoolArgs), ("materialize", MaterializeArgs), ("attn", AttnArgs)]
-
-
-class VmOp(C.Structure):
-    _fields_ = [("kind", C.c_int), ("b_static", C.c_int), ("n_items", C.c_int), ("n_done", C.c_int), ("cta0", C.c_int), ("dep", C.c_int),
-                ("dep_target", C.c_int), ("impl", C.c_int), ("bn", C.c_int), ("tiles_n", C.c_int),
-                ("tiles_m", C.c_int), ("splits", C.c_int), ("sync_base", C.c_int), ("tmap_a", C.c_int),
-                ("tmap_b", C.c_int), ("tmap_a2", C.c_int), ("pad_", C.c_int), ("u", VmArgsU)]
-
-
-class VmArgs(C.Structure):
-    _fields_ = [("ops", C.c_void_p), ("n_ops", C.c_int), ("n_ctas", C.c_int), ("sync", C.c_void_p),
-                ("n_sync", C.c_int), ("ws", C.c_void_p), ("step", C.c_void_p), ("tmaps", C.c_void_p), ("trace", C.c_void_p), ("poll_ns", C.c_int), ("trace_op", C.c_int), ("trace_items", C.c_void_p)]
-
-
-# ops the step VM executes: C entry point -> (FIS_VM_* kind, union member)
-VM_KINDS = {"fis_gemm": (1, "gemm"), "fis_softmax": (2, "softmax"), "fis_gn_stats": (3, "gn_stats"),
-            "fis_gn_apply": (4, "gn_apply"), "fis_pool2": (5, "pool"), "fis_materialize": (6, "materialize"),
-            "fis_attn": (7, "attn"), "fis_gn": (8, "gn_apply")}
 
 _SIGS = {
     "fis_gemm": GemmArgs, "fis_attn": AttnArgs, "fis_gn_stats": GnStatsArgs, "fis_gn_apply": GnApplyArgs, "fis_gn": GnApplyArgs, "fis_softmax": SoftmaxArgs,
     "fis_pool2": PoolArgs, "fis_up2": PoolArgs, "fis_materialize": MaterializeArgs, "fis_mask_detect": MaskDetectArgs,
-    "fis_mask_plan": MaskPlanArgs, "fis_vm_run": VmArgs,
+    "fis_mask_plan": MaskPlanArgs,
 }
 
-EXPORTS = tuple(_SIGS) + ("fis_vm_plan", "fis_vm_plan_tma", "fis_vm_op_size", "fis_vm_attn_slice", "fis_attn_launches", "fis_gn_launches", "fis_gemm_kernel_kind", "fis_gemm_big_launch_count", "fis_gemm_pair_launch_count", "fis_gemm_ws_floats", "fis_gemm_counters", "fis_mask_detect_smem", "fis_abi_version",
+EXPORTS = tuple(_SIGS) + ("fis_attn_launches", "fis_gn_launches", "fis_gemm_kernel_kind", "fis_gemm_big_launch_count", "fis_gemm_pair_launch_count", "fis_gemm_ws_floats", "fis_gemm_counters", "fis_mask_detect_smem", "fis_abi_version",
                           "fis_last_error", "fis_device_sm_count")
 
 
@@ -144,14 +123,6 @@ def lib():
         L.fis_gemm_counters.restype = C.c_int
         L.fis_mask_detect_smem.argtypes = [C.c_int, C.c_int]
         L.fis_mask_detect_smem.restype = C.c_longlong
-        L.fis_vm_plan.argtypes = [C.c_void_p, C.c_int, C.c_int, C.POINTER(C.c_longlong), C.POINTER(C.c_int)]
-        L.fis_vm_plan.restype = C.c_int
-        L.fis_vm_plan_tma.argtypes = [C.c_void_p, C.c_int, C.c_int, C.POINTER(C.c_longlong), C.POINTER(C.c_int),
-                                      C.c_void_p, C.c_int, C.POINTER(C.c_int)]
-        L.fis_vm_plan_tma.restype = C.c_int
-        L.fis_vm_op_size.restype = C.c_int
-        L.fis_vm_attn_slice.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int]
-        L.fis_vm_attn_slice.restype = C.c_int
         L.fis_gemm_kernel_kind.argtypes = [C.POINTER(GemmArgs)]
         L.fis_gemm_kernel_kind.restype = C.c_int
         L.fis_gemm_big_launch_count.restype = C.c_longlong
@@ -162,8 +133,6 @@ def lib():
         L.fis_trace_launches.restype = C.c_int
         L.fis_attn_launches.argtypes = [C.POINTER(AttnArgs)]
         L.fis_attn_launches.restype = C.c_int
-        if L.fis_vm_op_size() != C.sizeof(VmOp):
-            raise RuntimeError(f"libfisedit fis_vm_op layout mismatch ({L.fis_vm_op_size()} vs {C.sizeof(VmOp)})")
         L.fis_abi_version.restype = C.c_int
         L.fis_last_error.restype = C.c_char_p
         L.fis_device_sm_count.restype = C.c_int

@@ -60,20 +60,10 @@ FIS_DEV char* ref_base(const fis_ref& r, int t) {
     return (char*)r.ptr + (long long)t * r.step_stride;
 }
 
-// FIS_LOADS_CG (the step VM's translation unit): element loads go through L2 only (ld.global.cg).
-// The VM reads data produced by other CTAs of the same launch after a relaxed poll, without an L1
-// invalidation, so no such read may hit a stale L1 line.
-#ifdef FIS_LOADS_CG
-#define FIS_LD_U16(p) __ldcg((const unsigned short*)(p))
-#define FIS_LD_F32(p) __ldcg((const float*)(p))
-#define FIS_LD_U4(p) __ldcg((const uint4*)(p))
-#define FIS_LD_F4(p) __ldcg((const float4*)(p))
-#else
 #define FIS_LD_U16(p) (*(const unsigned short*)(p))
 #define FIS_LD_F32(p) (*(const float*)(p))
 #define FIS_LD_U4(p) (*(const uint4*)(p))
 #define FIS_LD_F4(p) (*(const float4*)(p))
-#endif
 
 FIS_DEV float load_elem(const char* base, int dtype, long long idx) {
     if (dtype == FIS_BF16) return __uint_as_float((uint32_t)FIS_LD_U16((const __nv_bfloat16*)base + idx) << 16);

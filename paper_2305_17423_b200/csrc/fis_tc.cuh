@@ -1,5 +1,5 @@
 // tcgen05 / cp.async / UMMA-descriptor helpers and the fused GEMM row epilogue shared by
-// the per-op tcgen05 kernels (fis_gemm_tc.cu) and the persistent step VM (fis_vm.cu).
+// tcgen05 GEMM / conv kernels (fis_gemm_tc.cu, fis_gemm_big.cu, fis_gemm_pair.cu, fis_gemm_halo.cu).
 #pragma once
 #include "fis_common.cuh"
 #include <climits>

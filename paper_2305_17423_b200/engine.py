@@ -147,22 +147,14 @@ class Launcher:
         self.static_meta = False
         self.groups = 1
         self.step_scale_value = 1.0
-        # capture mode: launches are recorded as (entry point, args) for the step VM instead of run
-        self.capture: list | None = None
-        self.use_vm = precision == "bf16" and os.environ.get("FIS_VM", "0") == "1"
         self._kv_graphs = {}  # (n_text, text_dim) -> (graph, embedding buffer, outputs) of text_kv
 
     def _call(self, name, args, b_static=False):
-        if self.capture is not None:
-            if name not in L.VM_KINDS:
-                raise ContractViolation(f"{name} cannot run inside the step VM")
-            self.capture.append((name, args, b_static))
-            return
         L.call(name, args)
 
     def _count(self, name, kernels=1, **info):
         self.launches += kernels
-        if self.op_log is not None and self.capture is None:
+        if self.op_log is not None:
             self.op_log.append(dict(op=name, kernels=kernels, **info))
 
     def _state(self):
@@ -214,8 +206,7 @@ class Launcher:
     def gemm(self, m, n, k, *, a=None, rows=None, srcs=None, out_hw=None, b: DRef, d: DRef, alpha=1.0, bias=None,
              bias2=None, pre=None, epi=L.EPI_NONE, gn=None, lat=None, res=None, d_trans=False, splits=None,
              n_split=0, d2=None, d2_trans=False, b_static=False, d_rows=None, m_halo=False, log_level=None):
-        """b_static: B is not produced inside the step (weights, per-edit text K/V), so the step VM
-        may stage it before the previous op completes."""
+        """b_static: B is not produced inside the step (weights, per-edit text K/V)."""
         if m == 0:
             return
         g = L.GemmArgs()
@@ -276,77 +267,6 @@ class Launcher:
         self._call("fis_softmax", a)
         self._count("fis_softmax", rows=rows, cols=cols)
 
-class VmProgram:
-    """A recorded step (list of launches) planned for the persistent step VM (csrc/fis_vm.cu).
-
-    One `run()` = one cooperative launch executing every op of the step back to back."""
-
-    def __init__(self, lz: Launcher, calls):
-        n = len(calls)
-        if n == 0:
-            raise ContractViolation("empty step program")
-        ops = (L.VmOp * n)()
-        for i, (name, args, b_static) in enumerate(calls):
-            kind, field = L.VM_KINDS[name]
-            ops[i].kind = kind
-            ops[i].b_static = 1 if b_static else 0
-            setattr(ops[i].u, field, args)
-        ws, si, nt = L.C.c_longlong(0), L.C.c_int(0), L.C.c_int(0)
-        cap = 3 * n
-        maps = (L.C.c_ubyte * (128 * cap))()
-        use_tma = os.environ.get("FIS_VM_TMA", "1") != "0"
-        st = L.lib().fis_vm_plan_tma(L.C.byref(ops), n, 0, L.C.byref(ws), L.C.byref(si), maps if use_tma else None,
-                                     cap if use_tma else 0, L.C.byref(nt))
-        if st != 0:
-            raise ContractViolation(f"fis_vm_plan failed (status {st})")
-        self.n_tmaps = nt.value
-        self.tmaps = torch.frombuffer(bytearray(bytes(maps)[:128 * max(1, nt.value)]), dtype=torch.uint8).to(lz.dev)
-        self.calls = calls  # keeps the argument structs (and what they point to) alive
-        self.n_ops = n
-        self.ops_host = ops
-        raw = torch.frombuffer(bytearray(bytes(ops)), dtype=torch.uint8)
-        self.ops_dev = raw.to(lz.dev)
-        self.sync = torch.zeros(si.value, dtype=torch.int32, device=lz.dev)
-        self.ws = torch.empty(max(4, ws.value), dtype=torch.float32, device=lz.dev)
-        self.args = L.VmArgs(self.ops_dev.data_ptr(), n, 0, self.sync.data_ptr(), si.value, self.ws.data_ptr(),
-                             lz.step_dev.data_ptr(), self.tmaps.data_ptr(), None,
-                             int(os.environ.get("FIS_VM_POLL_NS", "0")), -1, None)
-        self.lz = lz
-        self.trace = None
-
-    def enable_trace(self, on: bool = True):
-        """Per-op [first item start, last item end] globaltimer stamps (profiling)."""
-        if on:
-            self.trace = torch.zeros((self.n_ops, 2), dtype=torch.int64, device=self.lz.dev)
-            self.args.trace = self.trace.data_ptr()
-        else:
-            self.trace, self.args.trace = None, None
-
-    def trace_op(self, j):
-        """Record per-item phase stamps of op j ([n_items][8] globaltimer ns)."""
-        n = self.ops_host[j].n_items
-        self.items_trace = torch.zeros((max(1, n), 16), dtype=torch.int64, device=self.lz.dev)
-        self.args.trace_op, self.args.trace_items = j, self.items_trace.data_ptr()
-
-    def reset_trace(self):
-        if self.trace is not None:
-            self.trace[:, 0].fill_(-1)  # ~0ull: atomicMin start
-            self.trace[:, 1].zero_()
-
-    def read_trace(self):
-        """[(kind, n_items, splits, start_ns, end_ns)] relative to the first op's start."""
-        tr = self.trace.cpu().numpy().view(np.uint64).astype(np.float64)
-        t0 = tr[:, 0].min()
-        return [(k, n, s, tr[i, 0] - t0, tr[i, 1] - t0) for i, (k, n, s) in enumerate(self.items())]
-
-    def items(self):
-        return [(self.ops_host[i].kind, self.ops_host[i].n_items, self.ops_host[i].splits) for i in range(self.n_ops)]
-
-    def run(self):
-        L.call("fis_vm_run", self.args)
-        self.lz.launches += 1
-
-
 class Engine(Launcher):
     """One model (config + precision) resident on one GPU."""
 
@@ -394,7 +314,7 @@ class Engine(Launcher):
         launch overhead of ~42 GEMM calls was ~4.5 ms of every edit); every call copies the new
         embeddings in, replays, and returns fresh copies of the outputs."""
         emb_h = torch.from_numpy(np.ascontiguousarray(text_emb, dtype=np.float32))
-        if self.capture is not None or os.environ.get("FIS_KV_GRAPH", "1") == "0":
+        if os.environ.get("FIS_KV_GRAPH", "1") == "0":
             return self._text_kv(emb_h.to(self.dev))
         key = tuple(emb_h.shape)
         ent = self._kv_graphs.get(key)
@@ -529,10 +449,6 @@ class Engine(Launcher):
     def use_fused_attn(self, d, m=None, n_keys=None, pre=None):
         if self.act != torch.bfloat16 or d % 64:
             return False
-        if self.capture is not None and m is not None and pre is None:
-            # the step VM runs attention over one key block as one fused op (S in TMEM, P via shared
-            # memory); longer key ranges parallelise better as S GEMM -> softmax -> P.V (r01 timings)
-            return n_keys <= 128 and L.lib().fis_vm_attn_slice(m, n_keys, d, d) > 0
         return self.fused_attn
 
     def attn(self, m, n_keys, d, q: DRef, k: DRef, vt: DRef, scale, res: DRef, out: DRef, pre=None, segs=None):
@@ -593,25 +509,11 @@ class Engine(Launcher):
         self._count("fis_materialize", c=fv.c)
 
     # ------------------------------------------------------------ one UNet step
-    def record_step(self, plan: "StepPlan") -> VmProgram:
-        """Record one step's launches (nothing runs) and plan them for the step VM."""
-        self.capture = []
-        n0 = self.launches
-        try:
-            self.run_step(plan)
-            calls = self.capture
-        finally:
-            self.capture = None
-            self.launches = n0
-        return VmProgram(self, calls)
-
     def run_step(self, plan: "StepPlan"):
         """Launch one UNet forward + step update (unet.py:430-458,693) for the current device step."""
         vals = {}
         cfg = self.config
         self.batch = plan.batch
-        if plan.batch > 1 and self.capture is not None:
-            raise ContractViolation("batched steps run as per-op graphs, not in the step VM")
         for ins in self.prog:
             op = ins[0]
             if op == "stem":
@@ -634,7 +536,7 @@ class Engine(Launcher):
             elif op == "fuse":
                 lid, fu, fs, fo = ins[1], ins[2], ins[3], ins[4]
                 up = vals[fu.key]
-                if not plan.sparse(fo.level) and up.index is None and self.act == torch.bfloat16 and self.capture is None:
+                if not plan.sparse(fo.level) and up.index is None and self.act == torch.bfloat16:
                     # dense level: materialise the 2x upsample once so the fuse conv's A operand is a
                     # dense map the GEMM stages with TMA (one 4-D box per tap)
                     buf = DRef(self.scratch(f"up{fo.level}", (self.cap(fo.level), fu.channels)))
@@ -696,8 +598,7 @@ class Engine(Launcher):
             co = plan.record(blk["conv"], 0) or DRef(self.scratch(f"co{tag}", (cap, c)))
             self._conv(plan, blk["conv"], [(x, False)], co, level)
             mean, var = plan.stats(nl)
-            # statistics + normalisation (+ SiLU) of each group in one op (fis_gn; the step VM
-            # runs the same op kind)
+            # statistics + normalisation (+ SiLU) of each group in one launch (fis_gn)
             self.gn_apply(nl, co, cap, c, mean, var, plan.record(nl, 0), s, fused_stats=True)
         y1 = DRef(self.scratch(f"y1{tag}", (cap, c)))
         qs = plan.segments(level)

@@ -231,13 +231,11 @@ def _to_nchw(t: torch.Tensor, c, h, w) -> np.ndarray:
 # ---------------------------------------------------------------------------
 
 class _Runner:
-    """Drives Engine steps for t in a range: eagerly, through one captured CUDA graph, or (bf16)
-    as one persistent step-VM launch per step (csrc/fis_vm.cu)."""
+    """Drives Engine steps for t in a range: eagerly or through one captured CUDA graph."""
 
     def __init__(self, eng: Engine, plan, use_graph: bool, ns: int = 0):
         self.eng, self.plan, self.use_graph, self.ns = eng, plan, use_graph, ns
         self.graph = None
-        self.vm = None
         self.launches_per_step = None
 
     def step(self, t: int):
@@ -248,12 +246,6 @@ class _Runner:
         eng.step_dev.fill_(t)
         if not self.use_graph:
             eng.run_step(self.plan)
-            return
-        if eng.use_vm and self.plan.batch == 1:
-            if self.vm is None:
-                self.vm = eng.record_step(self.plan)
-                self.launches_per_step = 1
-            self.vm.run()
             return
         if self.graph is None:
             # warm (allocates scratch), then capture one step; replays read t from step_dev
@@ -446,7 +438,7 @@ def _cached_runner(eng: Engine, store: CacheStore, start: int, ep: "EditPlan", k
     edit's row lists, pixel->row maps, start latent rows and text K/V are copied (device to
     device) into the buffers that graph reads, instead of capturing a new one. The graphs are
     owned by the store (CacheStore.graph_cache: freed with it, or by close())."""
-    if not _use_graphs() or eng.use_vm:
+    if not _use_graphs():
         return _Runner(eng, ep.plan, _use_graphs())
     graphs = store.graph_cache()
     n_text = next(iter(kv.values()))[0].shape[0]

@@ -9,7 +9,6 @@ P.set_precision("bf16")
 cfg = P.UNetConfig(latent_h=64, latent_w=64, latent_channels=4, channels=(320, 640, 1280, 1280), blocks_per_level=2,
                    groups=32, steps=2, t1=1, t2=1, text_dim=768, vocab_size=49408, seed=0)
 eng = U.get_engine(cfg)
-eng.use_vm = False
 old = tuple(range(1, 78))
 new = tuple(99 if i == 3 else v for i, v in enumerate(old))
 store = P.CacheStore()
