@@ -96,3 +96,18 @@ def test_cli_usage_errors_and_report_checks(tmp_path):
     with pytest.raises(ContractViolation):
         cli.BenchReport.from_json({"runs": [dict(rec, speedup=4.0)]})
     json.dumps(cli.BenchReport.from_json({"runs": [rec]}).to_json())
+
+
+def test_lcs_pairs_matches_oracle():
+    """The package's LCS (SharedTokenMap, reference unet.py:174-195; plain-Python DP rows) returns the
+    same pairs as the oracle restatement, ties included, on random and edge-case prompts."""
+    import random
+    from oracle import sparsedit_oracle as O
+    from paper_2305_17423_b200.model import lcs_pairs
+    rng = random.Random(7)
+    cases = [((), ()), ((1,), ()), ((), (2,)), ((1, 2, 3), (1, 2, 3)), ((1, 2, 3), (3, 2, 1)), ((5, 5, 5), (5, 5))]
+    for _ in range(200):
+        la, lb = rng.randrange(0, 30), rng.randrange(0, 30)
+        cases.append((tuple(rng.randrange(6) for _ in range(la)), tuple(rng.randrange(6) for _ in range(lb))))
+    for a, b in cases:
+        assert lcs_pairs(a, b) == tuple(O.lcs_pairs(a, b)), (a, b)
