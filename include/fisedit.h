@@ -210,6 +210,10 @@ typedef struct {
 int fis_attn(const fis_attn_args* a, void* stream);
 /* kernel launches one fis_attn call makes: 1, or 2 when the value slices share P (0: unsupported) */
 int fis_attn_launches(const fis_attn_args* a);
+/* workspace bytes fis_attn can use for m queries, runs of <= max_keys keys and dv value columns
+ * (P sharing scratch, or the split-KV partials of long runs + completion counters); pass it
+ * zero-initialised as ws / ws_bytes */
+long long fis_attn_ws_bytes(int m, int max_keys, int dv);
 
 /* 2x2 average pool with select-on-read of the finer map (unet.py:296-298).
  * Output rows are coarse pixels rows[i] (NULL => all (h/2)*(w/2)). */

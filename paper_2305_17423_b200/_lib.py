@@ -101,7 +101,7 @@ _SIGS = {
     "fis_mask_plan": MaskPlanArgs,
 }
 
-EXPORTS = tuple(_SIGS) + ("fis_attn_launches", "fis_gn_launches", "fis_gemm_kernel_kind", "fis_gemm_big_launch_count", "fis_gemm_pair_launch_count", "fis_gemm_ws_floats", "fis_gemm_counters", "fis_mask_detect_smem", "fis_abi_version",
+EXPORTS = tuple(_SIGS) + ("fis_attn_launches", "fis_attn_ws_bytes", "fis_gn_launches", "fis_gemm_kernel_kind", "fis_gemm_big_launch_count", "fis_gemm_pair_launch_count", "fis_gemm_ws_floats", "fis_gemm_counters", "fis_mask_detect_smem", "fis_abi_version",
                           "fis_last_error", "fis_device_sm_count")
 
 
@@ -131,6 +131,8 @@ def lib():
         L.fis_gn_launches.restype = C.c_int
         L.fis_trace_launches.argtypes = [C.c_void_p]
         L.fis_trace_launches.restype = C.c_int
+        L.fis_attn_ws_bytes.argtypes = [C.c_int, C.c_int, C.c_int]
+        L.fis_attn_ws_bytes.restype = C.c_longlong
         L.fis_attn_launches.argtypes = [C.POINTER(AttnArgs)]
         L.fis_attn_launches.restype = C.c_int
         L.fis_abi_version.restype = C.c_int

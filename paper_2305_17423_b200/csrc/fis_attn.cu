@@ -52,6 +52,11 @@ constexpr int P_NONE = 0, P_OUT = 1, P_IN = 2, P_OUT_KS = 3, P_DSPLIT = 4;
 // lazily raised running max, O rescaled in TMEM only when a block's max exceeds m_run by > 8, O / l
 // in the epilogue) instead of a statistics pass that recomputes every S block
 constexpr int P_ONEPASS_OK = 8;
+// flag on P_NONE (batch 1, no segments): the key run is split over gridDim.z CTAs per (query tile,
+// value slice) -- flash-decoding style: each runs the one-pass loop over its key blocks and writes
+// its unnormalised O rows + (running max, sum) to the workspace; the last CTA of the group
+// (atomic counter) merges the partials in split order (deterministic), adds the residual, stores
+constexpr int P_SPLITKV = 16;
 constexpr float RESCALE_SLACK = 8.f;  // log2 units: unnormalised P <= 2^8
 
 FIS_DEV void cluster_sync_all() {
@@ -126,7 +131,8 @@ __global__ void __launch_bounds__(THREADS, 1)
     attn_kernel(const fis_attn_args a, const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
                 const __grid_constant__ CUtensorMap tv, const __grid_constant__ CUtensorMap tp, int dvs, int pmode_in) {
     const bool onepass_ok = (pmode_in & P_ONEPASS_OK) != 0;
-    pmode_in &= ~P_ONEPASS_OK;
+    const bool splitkv = (pmode_in & P_SPLITKV) != 0;
+    pmode_in &= ~(P_ONEPASS_OK | P_SPLITKV);
     const bool ks = pmode_in == P_OUT_KS;
     const bool dsp = pmode_in == P_DSPLIT;
     const int pmode = ks ? P_OUT : (dsp ? P_NONE : pmode_in);
@@ -171,12 +177,19 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
         if (n_keys > 128) n_keys = 128;
     }
+    // split-KV: this CTA's key blocks [kv0, kv0 + kvper) of the run
+    const int kvs = splitkv ? (int)gridDim.z : 1, kvz = splitkv ? (int)blockIdx.z : 0;
+    const int kvper = splitkv ? ((n_keys + 127) / 128 + kvs - 1) / kvs : 0;
+    if (splitkv) {
+        k_beg += kvz * kvper * 128;
+        n_keys = min(n_keys - kvz * kvper * 128, kvper * 128);  // >= 1 (host: every split owns a block)
+    }
     const int nkb = (n_keys + 127) / 128, dch = a.d / 64;
-    const bool single = nkb == 1;
+    const bool single = nkb == 1 && !splitkv;
     // two key blocks: both S blocks stay resident in the two TMEM buffers, so the statistics pass
     // and the P pass read the same S (no recompute, half the Q/K traffic)
-    const bool resident = nkb == 2;
-    const bool onepass = onepass_ok && pmode == P_NONE && !dsp && nkb >= 3;
+    const bool resident = nkb == 2 && !splitkv;
+    const bool onepass = (onepass_ok && pmode == P_NONE && !dsp && nkb >= 3) || splitkv;
     const int first_pass = (single || onepass) ? 2 : 1;
     const int pw = ((a.max_seg_k + 127) / 128) * 128;  // P scratch row width (P sharing)
     // P_DSPLIT: cluster rank = value slice; this CTA's d chunks [kc0, kc1) and owned rows [rbeg, rend)
@@ -735,6 +748,77 @@ __global__ void __launch_bounds__(THREADS, 1)
         // epilogue: stage the O row slice (fp32) in the idle pipeline stages; the stores run below
         if (pmode == P_OUT) goto done;
         mbar_wait(o_done, 0);
+        if (splitkv) {
+            // partial rows [tile][slice][split][128][dvs + 4] (O unnormalised, then max, sum; 16-B rows)
+            tc_fence_after();
+            const int nsl = a.dv / dvs, grp = blockIdx.y * nsl + blockIdx.x;
+            const int pitch = dvs + 4;
+            float* pbase = (float*)a.ws + (long long)grp * kvs * 128 * pitch;
+            float* mine = pbase + ((long long)kvz * 128 + lr) * pitch;
+#pragma unroll 1
+            for (int cb = 0; cb < dvs; cb += 32) {
+                tmem_ld32(tmem + lane_off + O_COL + cb, v);
+#pragma unroll
+                for (int q = 0; q < 8; q++)
+                    __stcg((float4*)(mine + cb + 4 * q), make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]));
+            }
+            __stcg(mine + dvs, mrow);
+            __stcg(mine + dvs + 1, lrow);
+            __threadfence();
+            asm volatile("bar.sync 3, 128;" ::: "memory");
+            int* cnt = (int*)((char*)a.ws + a.ws_bytes) - 1024 + grp;
+            __shared__ int s_last;
+            if (tid == 0) s_last = atomicAdd(cnt, 1) == kvs - 1;
+            asm volatile("bar.sync 3, 128;" ::: "memory");
+            if (!s_last) goto done;
+            __threadfence();
+            // merge: M = max m_z, L = sum l_z 2^(m_z - M), O = sum O_z 2^(m_z - M) / L (+ residual)
+            float mz[8], wz[8];
+            float M = -INFINITY;
+            for (int z = 0; z < kvs; z++) {
+                mz[z] = __ldcg(pbase + ((long long)z * 128 + lr) * pitch + dvs);
+                M = fmaxf(M, mz[z]);
+            }
+            float Ls = 0.f;
+            for (int z = 0; z < kvs; z++) {
+                wz[z] = ex2(mz[z] - M);
+                Ls = fmaf(__ldcg(pbase + ((long long)z * 128 + lr) * pitch + dvs + 1), wz[z], Ls);
+            }
+            const float inv = 1.f / Ls;
+            char* ob = ref_base(a.out, t);
+            char* pbp = a.pre.ptr ? ref_base(a.pre, t) : nullptr;
+            const char* rb = a.res.ptr ? ref_base(a.res, t) : nullptr;
+            if (r < q_end) {
+#pragma unroll 1
+                for (int cb = 0; cb < dvs; cb += 16) {
+                    float w[16], q[16];
+                    if (rb) load_row16(rb, a.res.dtype, (long long)r * a.res.ld + c0 + cb, 16, q);
+#pragma unroll
+                    for (int e2 = 0; e2 < 16; e2++) w[e2] = 0.f;
+                    for (int z = 0; z < kvs; z++) {
+                        const float* src = pbase + ((long long)z * 128 + lr) * pitch + cb;
+#pragma unroll
+                        for (int e4 = 0; e4 < 4; e4++) {
+                            const float4 f = __ldcg((const float4*)(src + 4 * e4));
+                            w[4 * e4] = fmaf(f.x, wz[z], w[4 * e4]);
+                            w[4 * e4 + 1] = fmaf(f.y, wz[z], w[4 * e4 + 1]);
+                            w[4 * e4 + 2] = fmaf(f.z, wz[z], w[4 * e4 + 2]);
+                            w[4 * e4 + 3] = fmaf(f.w, wz[z], w[4 * e4 + 3]);
+                        }
+                    }
+#pragma unroll
+                    for (int e2 = 0; e2 < 16; e2++) w[e2] *= inv;
+                    if (pbp) store_row16(pbp, a.pre.dtype, (long long)r * a.pre.ld + c0 + cb, 16, w);
+                    if (rb) {
+#pragma unroll
+                        for (int e2 = 0; e2 < 16; e2++) w[e2] = __fadd_rn(w[e2], q[e2]);
+                    }
+                    store_row16(ob, a.out.dtype, (long long)r * a.out.ld + c0 + cb, 16, w);
+                }
+            }
+            if (tid == 0) *cnt = 0;  // ready for the next launch
+            goto done;
+        }
         ltr(ls, 4);
         tc_fence_after();
         if (dsp) asm volatile("bar.sync 3, 128;" ::: "memory");  // thread 0's outgoing copies done reading
@@ -753,7 +837,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
     }
     if (dsp && warp >= 4) asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
-    if (pmode != P_OUT) {
+    if (pmode != P_OUT && !splitkv) {
         // all six warps: residual + O -> out, 16-column chunks columns-fastest (coalesced 16-byte runs);
         // each thread first issues the residual loads of EB chunks, then adds and stores them, so the
         // L2 round trips overlap (one per chunk serialised ~0.5 us each: 16 chunks per thread at
@@ -956,6 +1040,36 @@ static bool attn_dsplit(const fis_attn_args* a, int dvs) {
     return (long long)cs * ((a->m + 127) / 128) < 148;
 }
 
+// Split-KV factor for batch-1 runs of >= 16 key blocks whose grid leaves most SMs idle: the
+// largest split with >= 2 key blocks per CTA that keeps the grid within one wave (<= 8), if the
+// workspace holds the partials (the caller sizes it: fis_attn_ws_bytes).
+static int attn_kv_splits(const fis_attn_args* a, int dvs) {
+    static int off = getenv("FIS_ATTN_SPLITKV") && getenv("FIS_ATTN_SPLITKV")[0] == '0';
+    const int nkb = (a->n_keys + 127) / 128;
+    // runs of >= 16 key blocks only: the merge (the last CTA re-reads every partial row) costs more
+    // than the split saves on shorter runs (r02 batch 1: 400 keys 18 -> 42 us, 1024 keys 40 -> 68 us;
+    // dense 4096 keys 88 -> 79 us)
+    if (off || a->nseg > 0 || nkb < 16 || !a->ws) return 1;
+    const int slices = a->dv / dvs, tiles = (a->m + 127) / 128;
+    const long long ctas = (long long)slices * tiles;
+    if (ctas > 1024) return 1;  // counter slots
+    int kvs = (int)(148 / ctas);
+    if (kvs > nkb / 2) kvs = nkb / 2;
+    if (kvs > 8) kvs = 8;
+    if (kvs < 2) return 1;
+    const int kvper = (nkb + kvs - 1) / kvs;
+    kvs = (nkb + kvper - 1) / kvper;  // every split owns >= 1 block
+    const long long need = ctas * kvs * 128 * (dvs + 4) * 4 + 4096;
+    return need <= a->ws_bytes ? kvs : 1;
+}
+
+// Workspace bytes a fis_attn call can use (P sharing scratch or split-KV partials + counters).
+extern "C" long long fis_attn_ws_bytes(int m, int max_keys, int dv) {
+    const long long mp = (m + 127) / 128 * 128, pw = (max_keys + 127) / 128 * 128;
+    const long long p = mp * pw * 2, kv = mp * (long long)(dv + 32) * 8 * 4;
+    return (p > kv ? p : kv) + 4096;
+}
+
 // Kernel launches one fis_attn call makes (1, or 2 when the value slices share P); 0 = unsupported.
 extern "C" int fis_attn_launches(const fis_attn_args* a) {
     const int dvs = attn_slice(a->dv);
@@ -1038,6 +1152,16 @@ extern "C" int fis_attn(const fis_attn_args* a, void* stream) {
                    ? FIS_OK : FIS_ERR_LAUNCH;
     }
     static int onepass_off = getenv("FIS_ATTN_ONEPASS") && getenv("FIS_ATTN_ONEPASS")[0] == '0';
+    if (!share && !onepass_off) {
+        const int kvs = attn_kv_splits(a, dvs);
+        if (kvs > 1) {
+            cfg.gridDim = dim3(grid.x, grid.y, kvs);
+            return cudaLaunchKernelEx(&cfg, fis::attn::attn_kernel, *a, tq, tk, tv, tp, dvs,
+                                      (int)fis::attn::P_NONE | fis::attn::P_ONEPASS_OK | fis::attn::P_SPLITKV) ==
+                           cudaSuccess
+                       ? FIS_OK : FIS_ERR_LAUNCH;
+        }
+    }
     return cudaLaunchKernelEx(&cfg, fis::attn::attn_kernel, *a, tq, tk, tv, tp, dvs,
                               share ? (int)fis::attn::P_IN
                                     : (int)fis::attn::P_NONE | (onepass_off ? 0 : fis::attn::P_ONEPASS_OK)) == cudaSuccess

@@ -460,9 +460,11 @@ class Engine(Launcher):
         if segs is not None:
             qseg, kseg, nseg, maxq, maxk = segs
             a.nseg, a.max_seg_q, a.q_seg, a.k_seg = nseg, maxq, L.ptr(qseg), L.ptr(kseg)
-        if maxk <= 4096:  # value slices share one P per query tile (P scratch [m, 128 * ceil(maxk / 128)])
-            ws = self.scratch("attn_p", (m * _pad(maxk, 128),), torch.bfloat16)
-            a.max_seg_k, a.ws, a.ws_bytes = maxk, L.ptr(ws), ws.numel() * 2
+        # workspace: the P scratch of value slices sharing one P per query tile, or the split-KV
+        # partials (+ completion counters, zeroed once and reset by the kernel)
+        nbytes = int(L.lib().fis_attn_ws_bytes(m, maxk, d))
+        ws = self.scratch("attn_ws", (nbytes,), torch.uint8, zero=True)
+        a.max_seg_k, a.ws, a.ws_bytes = maxk, L.ptr(ws), nbytes
         self._call("fis_attn", a)
         # kernels (2 when P is shared)
         self._count("fis_attn", max(1, L.lib().fis_attn_launches(C.byref(a))), m=m, n_keys=n_keys, d=d,

@@ -130,7 +130,9 @@ def test_transposed_store_and_residual(env):
                                     # d-split clusters (<= 128 keys, small grids): cs = 5, 4, 3, 2 value slices
                                     (256, 77, 1280), (64, 77, 1280), (100, 77, 640), (200, 50, 768), (130, 128, 512),
                                     # two-round d-split (129-256 keys): cs = 5, 4
-                                    (200, 190, 1280), (256, 129, 1024), (64, 256, 1280)])
+                                    (200, 190, 1280), (256, 129, 1024), (64, 256, 1280),
+                                    # split-KV (runs of >= 3 key blocks on small grids): 2, 4, 3 splits
+                                    (130, 700, 320), (128, 1024, 640), (50, 777, 256)])
 def test_fused_attention_vs_torch(env, m, nk, d):
     """fis_attn (tcgen05 S=QK^T, softmax, P.V, + residual) against torch fp32 on the same bf16 inputs."""
     L, DRef, NULL, lz = env
@@ -149,6 +151,10 @@ def test_fused_attention_vs_torch(env, m, nk, d):
     out = torch.full((m, d), float("nan"), device="cuda", dtype=bf)
     a = L.AttnArgs(m, nk, d, d, DRef(Q).ref(), DRef(K).ref(), DRef(Vt, ld=ldv).ref(), scale, DRef(res).ref(), NULL,
                    DRef(out).ref(), None)
+    # the engine's workspace (zeroed): lets long runs on small grids take the split-KV path
+    nb = int(L.lib().fis_attn_ws_bytes(m, nk, d))
+    ws = torch.zeros(nb, device="cuda", dtype=torch.uint8)
+    a.max_seg_k, a.ws, a.ws_bytes = nk, L.ptr(ws), nb
     L.call("fis_attn", a)
     torch.cuda.synchronize()
     err = (out.float() - ref).abs().max().item()
