@@ -54,8 +54,9 @@ constexpr int P_NONE = 0, P_OUT = 1, P_IN = 2, P_OUT_KS = 3, P_DSPLIT = 4;
 constexpr int P_ONEPASS_OK = 8;
 // flag on P_NONE (batch 1, no segments): the key run is split over gridDim.z CTAs per (query tile,
 // value slice) -- flash-decoding style: each runs the one-pass loop over its key blocks and writes
-// its unnormalised O rows + (running max, sum) to the workspace; the last CTA of the group
-// (atomic counter) merges the partials in split order (deterministic), adds the residual, stores
+// its unnormalised O rows + (running max, sum) to the workspace; after a group barrier (arrive /
+// depart counters; the grid is below one wave) every split CTA merges 128 / splits rows of the
+// tile in split order (deterministic), adds the residual and stores
 constexpr int P_SPLITKV = 16;
 constexpr float RESCALE_SLACK = 8.f;  // log2 units: unnormalised P <= 2^8
 
@@ -766,57 +767,84 @@ __global__ void __launch_bounds__(THREADS, 1)
             __stcg(mine + dvs + 1, lrow);
             __threadfence();
             asm volatile("bar.sync 3, 128;" ::: "memory");
-            int* cnt = (int*)((char*)a.ws + a.ws_bytes) - 1024 + grp;
-            __shared__ int s_last;
-            if (tid == 0) s_last = atomicAdd(cnt, 1) == kvs - 1;
+            // every split CTA of the group waits for all partials (the groups' CTAs are co-resident:
+            // the grid is below one wave), then merges its own 128 / kvs rows
+            int* arrive = (int*)((char*)a.ws + a.ws_bytes) - 1024 + 2 * grp;
+            int* depart = arrive + 1;
+            if (tid == 0) {
+                atomicAdd(arrive, 1);
+                int seen;
+                do {
+                    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(seen) : "l"(arrive) : "memory");
+                } while (seen < kvs);
+            }
             asm volatile("bar.sync 3, 128;" ::: "memory");
-            if (!s_last) goto done;
             __threadfence();
-            // merge: M = max m_z, L = sum l_z 2^(m_z - M), O = sum O_z 2^(m_z - M) / L (+ residual)
-            float mz[8], wz[8];
-            float M = -INFINITY;
-            for (int z = 0; z < kvs; z++) {
-                mz[z] = __ldcg(pbase + ((long long)z * 128 + lr) * pitch + dvs);
-                M = fmaxf(M, mz[z]);
+            // per-row merge weights: w_z = 2^(m_z - M) / sum_z l_z 2^(m_z - M)
+            __shared__ float sw[128][8];
+            const int rpc = (128 + kvs - 1) / kvs, rb0 = min(128, kvz * rpc), rb1 = min(128, rb0 + rpc);
+            if (lr >= rb0 && lr < rb1) {
+                float mz[8];
+                float M = -INFINITY;
+                for (int z = 0; z < kvs; z++) {
+                    mz[z] = __ldcg(pbase + ((long long)z * 128 + lr) * pitch + dvs);
+                    M = fmaxf(M, mz[z]);
+                }
+                float Ls = 0.f;
+                for (int z = 0; z < kvs; z++)
+                    Ls = fmaf(__ldcg(pbase + ((long long)z * 128 + lr) * pitch + dvs + 1), ex2(mz[z] - M), Ls);
+                const float inv = 1.f / Ls;
+                for (int z = 0; z < kvs; z++) sw[lr][z] = ex2(mz[z] - M) * inv;
             }
-            float Ls = 0.f;
-            for (int z = 0; z < kvs; z++) {
-                wz[z] = ex2(mz[z] - M);
-                Ls = fmaf(__ldcg(pbase + ((long long)z * 128 + lr) * pitch + dvs + 1), wz[z], Ls);
-            }
-            const float inv = 1.f / Ls;
+            asm volatile("bar.sync 3, 128;" ::: "memory");
             char* ob = ref_base(a.out, t);
             char* pbp = a.pre.ptr ? ref_base(a.pre, t) : nullptr;
             const char* rb = a.res.ptr ? ref_base(a.res, t) : nullptr;
-            if (r < q_end) {
+            const int chunks = dvs / 16, nrows = max(0, min(rb1, q_end - m0) - rb0), total = nrows * chunks;
+            // items (row, 16-column chunk), consecutive threads on consecutive chunks of a row;
+            // 2 items per thread in flight (their partial-chunk loads issued before use)
 #pragma unroll 1
-                for (int cb = 0; cb < dvs; cb += 16) {
-                    float w[16], q[16];
-                    if (rb) load_row16(rb, a.res.dtype, (long long)r * a.res.ld + c0 + cb, 16, q);
+            for (int i0 = tid; i0 < total; i0 += 256) {
+                float w[2][16], q[2][16];
 #pragma unroll
-                    for (int e2 = 0; e2 < 16; e2++) w[e2] = 0.f;
+                for (int h = 0; h < 2; h++) {
+                    const int item = i0 + 128 * h;
+#pragma unroll
+                    for (int e2 = 0; e2 < 16; e2++) w[h][e2] = 0.f;
+                    if (item >= total) continue;
+                    const int rr = rb0 + item / chunks, cb = (item % chunks) * 16;
+                    if (rb) load_row16(rb, a.res.dtype, (long long)(m0 + rr) * a.res.ld + c0 + cb, 16, q[h]);
                     for (int z = 0; z < kvs; z++) {
-                        const float* src = pbase + ((long long)z * 128 + lr) * pitch + cb;
+                        const float* src = pbase + ((long long)z * 128 + rr) * pitch + cb;
+                        const float wt = sw[rr][z];
 #pragma unroll
                         for (int e4 = 0; e4 < 4; e4++) {
                             const float4 f = __ldcg((const float4*)(src + 4 * e4));
-                            w[4 * e4] = fmaf(f.x, wz[z], w[4 * e4]);
-                            w[4 * e4 + 1] = fmaf(f.y, wz[z], w[4 * e4 + 1]);
-                            w[4 * e4 + 2] = fmaf(f.z, wz[z], w[4 * e4 + 2]);
-                            w[4 * e4 + 3] = fmaf(f.w, wz[z], w[4 * e4 + 3]);
+                            w[h][4 * e4] = fmaf(f.x, wt, w[h][4 * e4]);
+                            w[h][4 * e4 + 1] = fmaf(f.y, wt, w[h][4 * e4 + 1]);
+                            w[h][4 * e4 + 2] = fmaf(f.z, wt, w[h][4 * e4 + 2]);
+                            w[h][4 * e4 + 3] = fmaf(f.w, wt, w[h][4 * e4 + 3]);
                         }
                     }
+                }
 #pragma unroll
-                    for (int e2 = 0; e2 < 16; e2++) w[e2] *= inv;
-                    if (pbp) store_row16(pbp, a.pre.dtype, (long long)r * a.pre.ld + c0 + cb, 16, w);
+                for (int h = 0; h < 2; h++) {
+                    const int item = i0 + 128 * h;
+                    if (item >= total) continue;
+                    const int rr = rb0 + item / chunks, cb = (item % chunks) * 16;
+                    const long long row = m0 + rr;
+                    if (pbp) store_row16(pbp, a.pre.dtype, row * a.pre.ld + c0 + cb, 16, w[h]);
                     if (rb) {
 #pragma unroll
-                        for (int e2 = 0; e2 < 16; e2++) w[e2] = __fadd_rn(w[e2], q[e2]);
+                        for (int e2 = 0; e2 < 16; e2++) w[h][e2] = __fadd_rn(w[h][e2], q[h][e2]);
                     }
-                    store_row16(ob, a.out.dtype, (long long)r * a.out.ld + c0 + cb, 16, w);
+                    store_row16(ob, a.out.dtype, row * a.out.ld + c0 + cb, 16, w[h]);
                 }
             }
-            if (tid == 0) *cnt = 0;  // ready for the next launch
+            if (tid == 0 && atomicAdd(depart, 1) == kvs - 1) {  // everyone is past the wait: reset
+                *arrive = 0;
+                *depart = 0;
+            }
             goto done;
         }
         ltr(ls, 4);
@@ -1040,19 +1068,19 @@ static bool attn_dsplit(const fis_attn_args* a, int dvs) {
     return (long long)cs * ((a->m + 127) / 128) < 148;
 }
 
-// Split-KV factor for batch-1 runs of >= 16 key blocks whose grid leaves most SMs idle: the
+// Split-KV factor for batch-1 runs of >= 8 key blocks whose grid leaves most SMs idle: the
 // largest split with >= 2 key blocks per CTA that keeps the grid within one wave (<= 8), if the
 // workspace holds the partials (the caller sizes it: fis_attn_ws_bytes).
 static int attn_kv_splits(const fis_attn_args* a, int dvs) {
     static int off = getenv("FIS_ATTN_SPLITKV") && getenv("FIS_ATTN_SPLITKV")[0] == '0';
     const int nkb = (a->n_keys + 127) / 128;
-    // runs of >= 16 key blocks only: the merge (the last CTA re-reads every partial row) costs more
-    // than the split saves on shorter runs (r02 batch 1: 400 keys 18 -> 42 us, 1024 keys 40 -> 68 us;
-    // dense 4096 keys 88 -> 79 us)
-    if (off || a->nseg > 0 || nkb < 16 || !a->ws) return 1;
+    // runs of >= 8 key blocks: the split CTAs merge their own rows after a group barrier; on
+    // shorter runs the partial round trip costs more than the split saves (r02, C2 batch 1 / dense
+    // step: 400 keys 18 -> 23.5 us, 1024 keys 40 -> 26-32 us, 4096 keys 88 -> 60 us)
+    if (off || a->nseg > 0 || nkb < 8 || !a->ws) return 1;
     const int slices = a->dv / dvs, tiles = (a->m + 127) / 128;
     const long long ctas = (long long)slices * tiles;
-    if (ctas > 1024) return 1;  // counter slots
+    if (ctas > 512) return 1;  // counter slots (2 per group)
     int kvs = (int)(148 / ctas);
     if (kvs > nkb / 2) kvs = nkb / 2;
     if (kvs > 8) kvs = 8;
