@@ -131,8 +131,8 @@ def test_transposed_store_and_residual(env):
                                     (256, 77, 1280), (64, 77, 1280), (100, 77, 640), (200, 50, 768), (130, 128, 512),
                                     # two-round d-split (129-256 keys): cs = 5, 4
                                     (200, 190, 1280), (256, 129, 1024), (64, 256, 1280),
-                                    # split-KV (runs of >= 3 key blocks on small grids): 2, 4, 3 splits
-                                    (130, 700, 320), (128, 1024, 640), (50, 777, 256)])
+                                    # split-KV (runs of >= 8 key blocks on small grids)
+                                    (130, 1100, 320), (128, 1024, 640), (50, 1500, 256)])
 def test_fused_attention_vs_torch(env, m, nk, d):
     """fis_attn (tcgen05 S=QK^T, softmax, P.V, + residual) against torch fp32 on the same bf16 inputs."""
     L, DRef, NULL, lz = env
