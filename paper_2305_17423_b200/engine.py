@@ -148,6 +148,7 @@ class Launcher:
         self.groups = 1
         self.step_scale_value = 1.0
         self._kv_graphs = {}  # (n_text, text_dim) -> (graph, embedding buffer, outputs) of text_kv
+        self._kv_seen = {}    # prompt shapes seen once (captured on the second use)
 
     def _call(self, name, args, b_static=False):
         L.call(name, args)
@@ -310,14 +311,18 @@ class Engine(Launcher):
         the layer input x straight into the attention kernel with M^T as its key matrix and skips
         the per-step query projection (one launch and a C x C GEMM per cross layer and step).
 
-        The 3 GEMMs x cross layers run as one captured CUDA graph per prompt length (the Python
-        launch overhead of ~42 GEMM calls was ~4.5 ms of every edit); every call copies the new
-        embeddings in, replays, and returns fresh copies of the outputs."""
+        From the second prompt of a given length on, the 3 GEMMs x cross layers run as one captured
+        CUDA graph per prompt length (the Python launch overhead of ~42 GEMM calls was ~4.5 ms of
+        every edit); every call copies the new embeddings in, replays, and returns fresh copies."""
         emb_h = torch.from_numpy(np.ascontiguousarray(text_emb, dtype=np.float32))
         if os.environ.get("FIS_KV_GRAPH", "1") == "0":
             return self._text_kv(emb_h.to(self.dev))
         key = tuple(emb_h.shape)
         ent = self._kv_graphs.get(key)
+        if ent is None and self._kv_seen.get(key, 0) == 0:
+            # first prompt of this length: eager (a one-off length does not pay a capture)
+            self._kv_seen[key] = 1
+            return self._text_kv(emb_h.to(self.dev))
         if ent is None:
             emb_buf = emb_h.to(self.dev)
             self._text_kv(emb_buf)  # warm-up outside the capture
