@@ -1092,9 +1092,10 @@ static int attn_kv_splits(const fis_attn_args* a, int dvs) {
 }
 
 // Workspace bytes a fis_attn call can use (P sharing scratch or split-KV partials + counters).
+// Split-KV grids stay within one wave (<= 148 CTAs of 128 rows x <= 256 + 4 floats).
 extern "C" long long fis_attn_ws_bytes(int m, int max_keys, int dv) {
     const long long mp = (m + 127) / 128 * 128, pw = (max_keys + 127) / 128 * 128;
-    const long long p = mp * pw * 2, kv = mp * (long long)(dv + 32) * 8 * 4;
+    const long long p = mp * pw * 2, kv = 148ll * 128 * ((dv < 256 ? dv : 256) + 4) * 4;
     return (p > kv ? p : kv) + 4096;
 }
 
