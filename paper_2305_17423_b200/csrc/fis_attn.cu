@@ -1184,11 +1184,22 @@ extern "C" int fis_attn(const fis_attn_args* a, void* stream) {
     if (!share && !onepass_off) {
         const int kvs = attn_kv_splits(a, dvs);
         if (kvs > 1) {
-            cfg.gridDim = dim3(grid.x, grid.y, kvs);
-            return cudaLaunchKernelEx(&cfg, fis::attn::attn_kernel, *a, tq, tk, tv, tp, dvs,
-                                      (int)fis::attn::P_NONE | fis::attn::P_ONEPASS_OK | fis::attn::P_SPLITKV) ==
-                           cudaSuccess
-                       ? FIS_OK : FIS_ERR_LAUNCH;
+            // the split CTAs of a group meet at a barrier before merging: a cooperative launch makes
+            // the whole grid co-resident (a spinning grid could otherwise hold SMs that the rest of
+            // its CTAs -- or another spinning grid on a concurrent stream -- wait for)
+            cudaLaunchConfig_t c2 = cfg;
+            cudaLaunchAttribute at[2];
+            at[0].id = cudaLaunchAttributeCooperative;
+            at[0].val.cooperative = 1;
+            at[1] = attr[0];
+            c2.attrs = at;
+            c2.numAttrs = fis_pdl_enabled() ? 2 : 1;
+            c2.gridDim = dim3(grid.x, grid.y, kvs);
+            if (cudaLaunchKernelEx(&c2, fis::attn::attn_kernel, *a, tq, tk, tv, tp, dvs,
+                                   (int)fis::attn::P_NONE | fis::attn::P_ONEPASS_OK | fis::attn::P_SPLITKV) ==
+                cudaSuccess)
+                return FIS_OK;
+            cudaGetLastError();  // not co-schedulable here: the unsplit kernel below
         }
     }
     return cudaLaunchKernelEx(&cfg, fis::attn::attn_kernel, *a, tq, tk, tv, tp, dvs,
