@@ -427,7 +427,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (tid == 0) { trace(6); trace_cta(1); ltr(ls, 5); }
         tc_fence_after();
         const int quarter = warp & 3, half = warp >> 2;
-        const int lr = quarter * 32 + lane, r = m0 + lr;
+        const int lr = quarter * 32 + lane;
         // all TMEM loads of this thread's row segment first, one wait (latency paid once)
         constexpr int HC = BN / 2;  // columns per warp half
         uint32_t u[HC];

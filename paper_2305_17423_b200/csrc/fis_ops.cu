@@ -373,12 +373,11 @@ __global__ void up2_kernel(const fis_pool_args a) {
 // ---- dense group norm in one launch (statistics + normalise + SiLU), bf16 maps, one CTA per
 // (group, stacked image): the group's hw x cpg block is read three times from L2 instead of
 // a statistics launch followed by a separate apply launch (same arithmetic as the pair)
-// One-launch dense GroupNorm (+SiLU) of bf16 maps: a cluster of GN_CL CTAs per (group, image), each
+// One-launch dense GroupNorm (+SiLU) of bf16 maps: a cluster of up to 8 CTAs per (group, image), each
 // over a contiguous slice of the image's pixels; the two-pass statistics (sum -> f32 mean, then the
 // centred sum of squares) are block-reduced in f64 and combined across the cluster through
 // distributed shared memory in rank order (deterministic), then every CTA normalises its slice.
 // VW bf16 channels per vector access: 8 (16-byte loads, channels-per-group % 8 == 0) or 2.
-constexpr int GN_CL = 8;  // maximum cluster size (the launch picks 1..8 by map size)
 
 FIS_DEV double gn_block_sum(double v, double* red) {
     const int tid = threadIdx.x;
@@ -503,7 +502,6 @@ static int grid_for(long long total, int threads) {
 
 }  // namespace fis
 
-static int fis_check(void) { return cudaGetLastError() == cudaSuccess ? FIS_OK : FIS_ERR_LAUNCH; }
 
 extern "C" int fis_gn_stats(const fis_gn_stats_args* a, void* stream) {
     if (a->groups <= 0 || a->c % a->groups) return FIS_ERR_SHAPE;
