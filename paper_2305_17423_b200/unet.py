@@ -280,9 +280,15 @@ class _Runner:
             gc_on = gc.isenabled()
             gc.disable()  # a collection inside the capture could destroy other graphs (invalidating it)
             try:
+                # capture_begin / capture_end directly: torch.cuda.graph() empties the caching
+                # allocator before every capture (cudaFree of every cached block: up to ~0.5 s
+                # with a large arena resident, measured in edit_batch)
                 with torch.cuda.stream(s):
-                    with torch.cuda.graph(g, stream=s):
+                    g.capture_begin()
+                    try:
                         eng.run_step(self.plan)
+                    finally:
+                        g.capture_end()
             finally:
                 if gc_on:
                     gc.enable()

@@ -27,8 +27,10 @@ for i in range(6):
     pr.disable()
     times.append(time.perf_counter() - t)
     profs.append(pr)
+    print(f"call {i}: {times[-1]:.3f} s  allocated {torch.cuda.memory_allocated() / 1e9:.1f} GB  reserved "
+          f"{torch.cuda.memory_reserved() / 1e9:.1f} GB  free {torch.cuda.mem_get_info()[0] / 1e9:.1f} GB", flush=True)
 print("calls (s):", [round(x, 3) for x in times])
 k = int(np.argmax(times))
 out = io.StringIO()
-pstats.Stats(profs[k], stream=out).sort_stats("cumulative").print_stats(25)
+pstats.Stats(profs[k], stream=out).sort_stats(os.environ.get("SORT", "cumulative")).print_stats(40)
 print(out.getvalue()[:6000])
