@@ -26,10 +26,12 @@ int fis_ltr_set_ops(unsigned long long* p);
 int fis_ltr_set_big(unsigned long long* p);
 int fis_ltr_set_small(unsigned long long* p);
 int fis_ltr_set_pair(unsigned long long* p);
+int fis_ltr_set_short(unsigned long long* p);
 
 int fis_trace_launches(unsigned long long* buf) {
     return fis_ltr_set_tc(buf) | fis_ltr_set_attn(buf) | fis_ltr_set_simt(buf) | fis_ltr_set_ops(buf) |
-           fis_ltr_set_big(buf) | fis_ltr_set_small(buf) | fis_ltr_set_pair(buf);
+           fis_ltr_set_big(buf) | fis_ltr_set_small(buf) | fis_ltr_set_pair(buf) |
+           fis_ltr_set_short(buf);
 }
 
 int fis_abi_version(void) { return FIS_ABI_VERSION; }

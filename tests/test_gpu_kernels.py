@@ -132,7 +132,9 @@ def test_transposed_store_and_residual(env):
                                     # two-round d-split (129-256 keys): cs = 5, 4
                                     (200, 190, 1280), (256, 129, 1024), (64, 256, 1280),
                                     # split-KV (runs of >= 8 key blocks on small grids)
-                                    (130, 1100, 320), (128, 1024, 640), (50, 1500, 256)])
+                                    (130, 1100, 320), (128, 1024, 640), (50, 1500, 256),
+                                    # short-run kernel (>= 16 query tiles, <= 128 keys)
+                                    (4096, 77, 320), (2100, 128, 640), (3000, 20, 1280)])
 def test_fused_attention_vs_torch(env, m, nk, d):
     """fis_attn (tcgen05 S=QK^T, softmax, P.V, + residual) against torch fp32 on the same bf16 inputs."""
     L, DRef, NULL, lz = env
@@ -165,7 +167,11 @@ def test_fused_attention_vs_torch(env, m, nk, d):
     (320, [205, 410, 1024, 0, 37], None, 0),          # self-attention: keys = own rows
     (640, [64, 300, 129], [77, 77, 77], 80),           # cross-attention: stacked prompts padded to 80
     (1280, [256, 256, 256], None, 0),
-    (640, [100, 256, 17], None, 0)])
+    (640, [100, 256, 17], None, 0),
+    # >= 16 query tiles with every key run <= 128: the persistent short-run kernel (fis_attn_short.cu)
+    (320, [205, 410, 1024, 77, 300, 0, 515] * 3, [77, 60, 77, 1, 77, 77, 33] * 3, 80),
+    (1280, [64] * 40, None, 0),
+    (640, [128, 200, 17, 256] * 6, [77] * 24, 80)])
 @pytest.mark.parametrize("share", [False, True])
 def test_segment_attention_vs_torch(env, d, qlens, klens, kpad, share):
     """fis_attn with ragged segments (batched requests): each query run attends to its own key run only."""
