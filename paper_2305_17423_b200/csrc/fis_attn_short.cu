@@ -471,24 +471,26 @@ __global__ void __launch_bounds__(THREADS, 1)
             if (job == 2 && leader) ltr(ls_sh, 13);
             if (half * 64 < w) {
                 unsigned char* boxp = eb + half * CH;
-                float v[32];
-#pragma unroll 1
-                for (int c32 = 0; c32 < 2; c32++) {
-                    tmem_ld32(tlane + 128 + b * 128 + half * 64 + c32 * 32, v);
+                // both 32-column TMEM loads and the residual reads in flight before one wait
+                uint32_t o[64];
+                tmem_ld32_nw(tlane + 128 + b * 128 + half * 64, o);
+                tmem_ld32_nw(tlane + 128 + b * 128 + half * 64 + 32, o + 32);
+                uint4 rr[8];
 #pragma unroll
-                    for (int u4 = 0; u4 < 4; u4++) {
-                        uint4* p = (uint4*)(boxp + sw128_off(er, c32 * 4 + u4));
-                        uint4 rr = *p;
-                        uint32_t* h = (uint32_t*)&rr;
+                for (int k = 0; k < 8; k++) rr[k] = *(const uint4*)(boxp + sw128_off(er, k));
+                tmem_wait_ld();
 #pragma unroll
-                        for (int e2 = 0; e2 < 4; e2++) {
-                            const float lo = __uint_as_float(h[e2] << 16), hi = __uint_as_float(h[e2] & 0xffff0000u);
-                            const __nv_bfloat162 o = __floats2bfloat162_rn(__fadd_rn(v[8 * u4 + 2 * e2], lo),
-                                                                           __fadd_rn(v[8 * u4 + 2 * e2 + 1], hi));
-                            h[e2] = *(const uint32_t*)&o;
-                        }
-                        *p = rr;
+                for (int k = 0; k < 8; k++) {
+                    uint32_t* h = (uint32_t*)&rr[k];
+#pragma unroll
+                    for (int e2 = 0; e2 < 4; e2++) {
+                        const float lo = __uint_as_float(h[e2] << 16), hi = __uint_as_float(h[e2] & 0xffff0000u);
+                        const __nv_bfloat162 ov =
+                            __floats2bfloat162_rn(__fadd_rn(__uint_as_float(o[8 * k + 2 * e2]), lo),
+                                                  __fadd_rn(__uint_as_float(o[8 * k + 2 * e2 + 1]), hi));
+                        h[e2] = *(const uint32_t*)&ov;
                     }
+                    *(uint4*)(boxp + sw128_off(er, k)) = rr[k];
                 }
             }
             tc_fence_before();
