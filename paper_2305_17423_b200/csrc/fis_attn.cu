@@ -58,16 +58,23 @@ constexpr int P_ONEPASS_OK = 8;
 // depart counters; the grid is below one wave) every split CTA merges 128 / splits rows of the
 // tile in split order (deterministic), adds the residual and stores
 constexpr int P_SPLITKV = 16;
+// flag: the epilogue TMA-loads the residual tile (32-column SW64 boxes) into the P tiles, adds O in
+// place and TMA-stores whole 8-row groups (host-encoded maps tr / to / to8) instead of staging O in
+// fp32 and storing 16-byte runs with LDG residual loads (7-10 us of a batch-1 d = 1280 call)
+constexpr int P_FEPI = 32;
 constexpr float RESCALE_SLACK = 8.f;  // log2 units: unnormalised P <= 2^8
 
 // The MMA order (and so the producer's load order) of one pass: S blocks 0..nkb-1; in pass 2
 // step u issues S_u (u < nkb) and then P_{u-1}.V_{u-1} (u >= 1).
 __global__ void __launch_bounds__(THREADS, 1)
     attn_kernel(const fis_attn_args a, const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
-                const __grid_constant__ CUtensorMap tv, const __grid_constant__ CUtensorMap tp, int dvs, int pmode_in) {
+                const __grid_constant__ CUtensorMap tv, const __grid_constant__ CUtensorMap tp,
+                const __grid_constant__ CUtensorMap tr, const __grid_constant__ CUtensorMap to,
+                const __grid_constant__ CUtensorMap to8, int dvs, int pmode_in) {
     const bool onepass_ok = (pmode_in & P_ONEPASS_OK) != 0;
     const bool splitkv = (pmode_in & P_SPLITKV) != 0;
-    pmode_in &= ~(P_ONEPASS_OK | P_SPLITKV);
+    const bool fepi = (pmode_in & P_FEPI) != 0 && !splitkv;
+    pmode_in &= ~(P_ONEPASS_OK | P_SPLITKV | P_FEPI);
     const bool ks = pmode_in == P_OUT_KS;
     const bool dsp = pmode_in == P_DSPLIT;
     const int pmode = ks ? P_OUT : (dsp ? P_NONE : pmode_in);
@@ -85,7 +92,8 @@ __global__ void __launch_bounds__(THREADS, 1)
     uint64_t* rx_bar = o_done + 1;       // P_DSPLIT: peers' partial row slices landed (one phase per round)
     uint64_t* tx_ok = rx_bar + 1;        // P_DSPLIT: every peer consumed its receive buffer (per round)
     uint64_t* part_free = tx_ok + 1;     // P_DSPLIT, 2 key blocks: stages 2-3 free for V^T of block 1
-    uint32_t* tmem_slot = (uint32_t*)(part_free + 1);
+    uint64_t* res_bar = part_free + 1;   // P_FEPI: the residual tile landed
+    uint32_t* tmem_slot = (uint32_t*)(res_bar + 1);
     float2* xst = (float2*)(ptile + 2 * P_BYTES + RX_EXTRA + 256);  // [128] key-split (max, sum) exchange
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -147,6 +155,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         mbar_init(rx_bar, 1);
         mbar_init(tx_ok, cs > 1 ? cs - 1 : 1);
         mbar_init(part_free, 1);
+        mbar_init(res_bar, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         if (dsp && rend > rbeg)  // incoming: cs - 1 partial slices of this CTA's rows
             asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(rx_bar)),
@@ -784,22 +793,86 @@ __global__ void __launch_bounds__(THREADS, 1)
         ltr(ls, 4);
         tc_fence_after();
         if (dsp) asm volatile("bar.sync 3, 128;" ::: "memory");  // thread 0's outgoing copies done reading
-        float* ost = (float*)smem;
         const float inv_l = onepass ? 1.f / lrow : 1.f;  // one pass: O holds the unnormalised sum
-#pragma unroll 1
-        for (int cb = 0; cb < dvs; cb += 32) {
-            tmem_ld32(tmem + lane_off + O_COL + cb, v);
-            if (onepass) {
-#pragma unroll
-                for (int q = 0; q < 32; q++) v[q] *= inv_l;
+        if (fepi) {
+            // the residual tile -> the P tiles (every P.V MMA has completed: free), 32-column SW64
+            // boxes of 8 KB; O (* 1/l) + residual -> bf16 in place; whole 8-row groups leave by TMA
+            // (rows of a neighbouring run are never written), a run's < 8 trailing rows by 16-byte
+            // stores
+            unsigned char* rt = ptile;
+            const uint32_t rts = smem_u32(rt);
+            const int nbox = dvs >> 5;
+            if (tid == 0) {
+                arrive_expect_tx(res_bar, (uint32_t)(nbox * 8192));
+                for (int bx = 0; bx < nbox; bx++) tma2d(rts + bx * 8192, &tr, c0 + bx * 32, m0, res_bar);
             }
+            mbar_wait(res_bar, 0);
+#pragma unroll 1
+            for (int cb = 0; cb < dvs; cb += 32) {
+                tmem_ld32(tmem + lane_off + O_COL + cb, v);
+                unsigned char* bp = rt + (cb >> 5) * 8192 + lr * 64;
 #pragma unroll
-            for (int q = 0; q < 8; q++)
-                *(float4*)(ost + lr * EPI_LD + cb + 4 * q) = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+                for (int j = 0; j < 4; j++) {
+                    uint4* pp = (uint4*)(bp + ((j ^ ((lr >> 1) & 3)) << 4));
+                    uint4 rr = *pp;
+                    uint32_t* h = (uint32_t*)&rr;
+#pragma unroll
+                    for (int e2 = 0; e2 < 4; e2++) {
+                        const float lo = __uint_as_float(h[e2] << 16), hi = __uint_as_float(h[e2] & 0xffff0000u);
+                        const __nv_bfloat162 o2 = __floats2bfloat162_rn(__fadd_rn(v[8 * j + 2 * e2] * inv_l, lo),
+                                                                        __fadd_rn(v[8 * j + 2 * e2 + 1] * inv_l, hi));
+                        h[e2] = *(const uint32_t*)&o2;
+                    }
+                    *pp = rr;
+                }
+            }
+            fence_async_smem();
+            asm volatile("bar.sync 3, 128;" ::: "memory");
+            const int rows = min(128, q_end - m0), g8 = rows >> 3;
+            if (tid == 0) {
+                if (g8 > 0) {
+                    for (int bx = 0; bx < nbox; bx++) {
+                        if (g8 == 16) {
+                            asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(&to),
+                                         "r"(c0 + bx * 32), "r"(m0), "r"(rts + bx * 8192)
+                                         : "memory");
+                        } else {
+                            for (int g = 0; g < g8; g++)
+                                asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(&to8),
+                                             "r"(c0 + bx * 32), "r"(m0 + g * 8), "r"(rts + bx * 8192 + g * 512)
+                                             : "memory");
+                        }
+                    }
+                    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                }
+            }
+            const int r0 = g8 * 8, upr = dvs >> 3, total = (rows - r0) * upr;
+            if (total > 0) {
+                __nv_bfloat16* orow = (__nv_bfloat16*)ref_base(a.out, t) + (long long)(m0 + r0) * a.out.ld + c0;
+                for (int i = tid; i < total; i += 128) {
+                    const int rr_ = i / upr, un = i - rr_ * upr, r = r0 + rr_, j = un & 3;
+                    const uint4 val = *(const uint4*)(rt + (un >> 2) * 8192 + r * 64 + ((j ^ ((r >> 1) & 3)) << 4));
+                    *(uint4*)(orow + (long long)rr_ * a.out.ld + un * 8) = val;
+                }
+            }
+            if (tid == 0 && g8 > 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // smem read before exit
+        } else {
+            float* ost = (float*)smem;
+#pragma unroll 1
+            for (int cb = 0; cb < dvs; cb += 32) {
+                tmem_ld32(tmem + lane_off + O_COL + cb, v);
+                if (onepass) {
+#pragma unroll
+                    for (int q = 0; q < 32; q++) v[q] *= inv_l;
+                }
+#pragma unroll
+                for (int q = 0; q < 8; q++)
+                    *(float4*)(ost + lr * EPI_LD + cb + 4 * q) = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+            }
         }
     }
     if (dsp && warp >= 4) asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
-    if (pmode != P_OUT && !splitkv) {
+    if (pmode != P_OUT && !splitkv && !fepi) {
         // all six warps: residual + O -> out, 16-column chunks columns-fastest (coalesced 16-byte runs);
         // each thread first issues the residual loads of EB chunks, then adds and stores them, so the
         // L2 round trips overlap (one per chunk serialised ~0.5 us each: 16 chunks per thread at
@@ -1066,6 +1139,21 @@ extern "C" int fis_attn(const fis_attn_args* a, void* stream) {
     const long long pw = ((long long)a->max_seg_k + 127) / 128 * 128;
     const bool share = attn_share(a, dvs) && encode_2d(&tp, a->ws, a->m, pw, pw, 128);
     if (!share) std::memset(&tp, 0, sizeof(tp));
+    // TMA residual / output epilogue (P_FEPI) when both are step-invariant bf16 matrices
+    CUtensorMap tr, to, to8;
+    static int fepi_off = getenv("FIS_ATTN_FEPI") && getenv("FIS_ATTN_FEPI")[0] == '0';
+    int fepi = 0;
+    if (!fepi_off && !a->pre.ptr && a->res.ptr && a->res.dtype == FIS_BF16 && !a->res.step_stride &&
+        a->out.dtype == FIS_BF16 && !a->out.step_stride && (a->dv % 32) == 0 &&
+        encode_2d_sw64(&tr, a->res.ptr, a->m, a->dv, a->res.ld, 128) &&
+        encode_2d_sw64(&to, a->out.ptr, a->m, a->dv, a->out.ld, 128) &&
+        encode_2d_sw64(&to8, a->out.ptr, a->m, a->dv, a->out.ld, 8))
+        fepi = fis::attn::P_FEPI;
+    if (!fepi) {
+        std::memset(&tr, 0, sizeof(tr));
+        std::memset(&to, 0, sizeof(to));
+        std::memset(&to8, 0, sizeof(to8));
+    }
     static bool configured = false;
     if (!configured) {
         if (cudaFuncSetAttribute(fis::attn::attn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1102,7 +1190,7 @@ extern "C" int fis_attn(const fis_attn_args* a, void* stream) {
                 cfg.numAttrs = 1;
             }
         }
-        if (cudaLaunchKernelEx(&cfg, fis::attn::attn_kernel, *a, tq, tk, tv, tp, dvs,
+        if (cudaLaunchKernelEx(&cfg, fis::attn::attn_kernel, *a, tq, tk, tv, tp, tr, to, to8, dvs,
                                (int)(ksplit ? fis::attn::P_OUT_KS : fis::attn::P_OUT)) != cudaSuccess)
             return FIS_ERR_LAUNCH;
         cfg.attrs = attr;
@@ -1118,7 +1206,7 @@ extern "C" int fis_attn(const fis_attn_args* a, void* stream) {
         at2[1].val.clusterDim.z = 1;
         cfg.attrs = fis_pdl_enabled() ? at2 : at2 + 1;
         cfg.numAttrs = fis_pdl_enabled() ? 2 : 1;
-        return cudaLaunchKernelEx(&cfg, fis::attn::attn_kernel, *a, tq, tk, tv, tp, dvs, (int)fis::attn::P_DSPLIT) ==
+        return cudaLaunchKernelEx(&cfg, fis::attn::attn_kernel, *a, tq, tk, tv, tp, tr, to, to8, dvs, (int)fis::attn::P_DSPLIT | fepi) ==
                        cudaSuccess
                    ? FIS_OK : FIS_ERR_LAUNCH;
     }
@@ -1137,15 +1225,16 @@ extern "C" int fis_attn(const fis_attn_args* a, void* stream) {
             c2.attrs = at;
             c2.numAttrs = fis_pdl_enabled() ? 2 : 1;
             c2.gridDim = dim3(grid.x, grid.y, kvs);
-            if (cudaLaunchKernelEx(&c2, fis::attn::attn_kernel, *a, tq, tk, tv, tp, dvs,
+            if (cudaLaunchKernelEx(&c2, fis::attn::attn_kernel, *a, tq, tk, tv, tp, tr, to, to8, dvs,
                                    (int)fis::attn::P_NONE | fis::attn::P_ONEPASS_OK | fis::attn::P_SPLITKV) ==
                 cudaSuccess)
                 return FIS_OK;
             cudaGetLastError();  // not co-schedulable here: the unsplit kernel below
         }
     }
-    return cudaLaunchKernelEx(&cfg, fis::attn::attn_kernel, *a, tq, tk, tv, tp, dvs,
-                              share ? (int)fis::attn::P_IN
-                                    : (int)fis::attn::P_NONE | (onepass_off ? 0 : fis::attn::P_ONEPASS_OK)) == cudaSuccess
+    return cudaLaunchKernelEx(&cfg, fis::attn::attn_kernel, *a, tq, tk, tv, tp, tr, to, to8, dvs,
+                              (share ? (int)fis::attn::P_IN
+                                     : (int)fis::attn::P_NONE | (onepass_off ? 0 : fis::attn::P_ONEPASS_OK)) | fepi) ==
+                   cudaSuccess
                ? FIS_OK : FIS_ERR_LAUNCH;
 }

@@ -443,7 +443,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             have = advance(u, s, x);
             job++;
         }
-        if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // output stores complete
+        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // tiles read before exit
         if (lane == 0) ltr(ls_sh, 8);
     } else {
         // ------------------------------------------------------------ epilogue (warps 4-11)

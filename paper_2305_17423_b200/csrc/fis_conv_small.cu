@@ -102,6 +102,7 @@ __global__ void __launch_bounds__(THREADS, 2) conv_small_kernel(const fis_gemm_a
         build_sel(a, p, 0, sel + tid * 9);
     }
     __syncthreads();
+    if (tile == (int)blockIdx.x) ltr(ls, 3);
     {
         const fis_src& s = a.src[0];
         const char* fb = s.fresh.ptr ? ref_base(s.fresh, t) : nullptr;
@@ -128,6 +129,7 @@ __global__ void __launch_bounds__(THREADS, 2) conv_small_kernel(const fis_gemm_a
         }
     }
     __syncthreads();
+    if (tile == (int)blockIdx.x) ltr(ls, 4);
     const int groups = N / 16;
 #pragma unroll 1
     for (int item = tid; item < ROWS * groups; item += THREADS) {
@@ -154,8 +156,10 @@ __global__ void __launch_bounds__(THREADS, 2) conv_small_kernel(const fis_gemm_a
                 v[4 * q + 3] = fmaf(x, w.w, v[4 * q + 3]);
             }
         }
+        if (tile == (int)blockIdx.x && item == tid) ltr(ls, 5);
         row_epilogue_any(a, e, tb, r, g * 16, 0, v);
     }
+    if (tile == (int)blockIdx.x) ltr(ls, 6);
     __syncthreads();  // the next tile's row tables / inputs overwrite this one's
     }
     ltr(ls, 7);
