@@ -19,13 +19,17 @@ namespace small {
 
 using namespace fis::tc;
 
-constexpr int ROWS = 32, THREADS = 320, MAX_N = 640;
+// ROWS output rows per tile: 32 (320 threads) for large M; 8 (160 threads) when 32-row tiles would
+// leave most SMs idle (the batch-1 stem conv: 400 rows = 13 tiles of 32 -> 50 tiles of 8: 19 -> 14.7 us)
+constexpr int MAX_N = 640;
 
-__host__ __device__ inline int smem_bytes(int k, int n) {
-    return (k * n + ROWS * (k + 1) + 6 * n) * 4 + ROWS * 9 * 4 + 64;
+__host__ __device__ inline int smem_bytes(int k, int n, int rows) {
+    return (k * n + rows * (k + 1) + 6 * n) * 4 + rows * 9 * 4 + 64;
 }
 
-__global__ void __launch_bounds__(THREADS, 2) conv_small_kernel(const fis_gemm_args a) {
+template <int ROWS>
+__global__ void __launch_bounds__(ROWS == 32 ? 320 : 160, 2) conv_small_kernel(const fis_gemm_args a) {
+    constexpr int THREADS = ROWS == 32 ? 320 : 160;
     extern __shared__ __align__(16) float sm[];
     const int K = a.k, N = a.n, cin = a.src[0].c;
     float* ws = sm;                  // [K][N]
@@ -133,8 +137,8 @@ __global__ void __launch_bounds__(THREADS, 2) conv_small_kernel(const fis_gemm_a
     const int groups = N / 16;
 #pragma unroll 1
     for (int item = tid; item < ROWS * groups; item += THREADS) {
-        // a warp = the 32 rows of one 16-channel group: weight reads are broadcasts, the row reads
-        // (pitch K + 1, odd) hit 32 distinct banks
+        // a warp = the rows of 32 / ROWS 16-channel groups: weight reads are (near-)broadcasts, the
+        // row reads (pitch K + 1, odd) hit distinct banks
         const int g = item / ROWS, row = item - g * ROWS;
         const int r = m0 + row;
         if (r >= a.m) continue;
@@ -174,23 +178,29 @@ int fis_conv_small_ok(const fis_gemm_args* a) {
     if (a->a_mode != FIS_A_CONV3X3 || a->nsrc != 1 || a->src[0].up || a->src[0].c > 8 || a->k != 9 * a->src[0].c)
         return 0;
     if (a->n % 16 || a->n > fis::small::MAX_N || a->d_trans || a->n_split > 0) return 0;
-    return fis::small::smem_bytes(a->k, a->n) <= 200 * 1024;
+    return fis::small::smem_bytes(a->k, a->n, 32) <= 200 * 1024;
 }
 
 int fis_conv_small_launch(const fis_gemm_args* a, cudaStream_t stream) {
-    const int smem = fis::small::smem_bytes(a->k, a->n);
-    static int configured = 0;
-    if (configured < smem) {
-        if (cudaFuncSetAttribute(fis::small::conv_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024) !=
-            cudaSuccess)
+    using namespace fis::small;
+    const bool small_m = (a->m + 31) / 32 < 64;  // (the dense 4096-row stem keeps 32-row tiles: measured)
+    const int rows = small_m ? 8 : 32;
+    const int smem = smem_bytes(a->k, a->n, rows);
+    static bool configured = false;
+    if (!configured) {
+        if (cudaFuncSetAttribute(conv_small_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024) !=
+                cudaSuccess ||
+            cudaFuncSetAttribute(conv_small_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024) !=
+                cudaSuccess)
             return FIS_ERR_UNSUPPORTED;
-        configured = 200 * 1024;
+        configured = true;
     }
     // persistent CTAs (the weights are staged once per CTA), 2 per SM when registers allow
-    const int tiles = (a->m + fis::small::ROWS - 1) / fis::small::ROWS;
+    const int tiles = (a->m + rows - 1) / rows;
     const dim3 grid(tiles < 2 * 148 ? tiles : 2 * 148);
-    return fis_launch(fis::small::conv_small_kernel, grid, dim3(fis::small::THREADS), smem, stream, *a) == cudaSuccess
-               ? FIS_OK : FIS_ERR_LAUNCH;
+    const cudaError_t e = small_m ? fis_launch(conv_small_kernel<8>, grid, dim3(160), smem, stream, *a)
+                                  : fis_launch(conv_small_kernel<32>, grid, dim3(320), smem, stream, *a);
+    return e == cudaSuccess ? FIS_OK : FIS_ERR_LAUNCH;
 }
 
 FIS_LTR_SETTER(fis_ltr_set_small)
