@@ -443,8 +443,10 @@ __global__ void __launch_bounds__(THREADS, 1)
                     }
                     asm volatile("cp.async.bulk.commit_group;" ::: "memory");
                 }
+                if (j == 1) ltr(ls, 9);
                 if (own > 0) mbar_wait(rx_bar, j & 1);
                 if (j == 0) ltr(ls, 5);
+                if (j == 1) ltr(ls, 10);
                 if (nkb > 1) {
                     if (j == 0) sum_rows(xs[0], tid >> 2);
                     else sum_rows(xs[1], tid >> 2);
@@ -466,6 +468,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                     }
                     asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // round j's copies have read part
                     if (j == nkb - 1 && nkb > 1) mbar_arrive(part_free);  // V^T of block 1 may overwrite stages 2-3
+                    if (j == 0) ltr(ls, 8);
                 }
             }
             // softmax of one owned row (this thread's 32 keys of each block) -> the local P tiles
@@ -519,6 +522,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             };
             if (nkb > 1) {
                 emit(xs[0], xs[1], 2, tid >> 2);
+                ltr(ls, 11);
             } else {
                 emit(xs[0], xs[0], 1, tid >> 2);
                 if (niter > 1) emit(xs[1], xs[1], 1, (tid >> 2) + 32);

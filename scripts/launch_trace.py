@@ -68,7 +68,7 @@ def main():
         st, en = st - c0, en - c0
         row = tr[i]
         kind = KIND.get(int(row[15]) % 16, "?")
-        ph = [(row[p] - t0) / 1e3 if row[p] > 0 else float("nan") for p in range(8)]
+        ph = [(row[p] - t0) / 1e3 if row[p] > 0 else float("nan") for p in range(12)]
         ref = prev_end if prev_end is not None else 0.0
         o = ops[i] if i < len(ops) else {}
         desc = {k: v for k, v in o.items() if k not in ("kernels",)}
