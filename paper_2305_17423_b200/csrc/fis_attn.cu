@@ -1131,7 +1131,7 @@ extern "C" int fis_attn(const fis_attn_args* a, void* stream) {
         return FIS_ERR_UNSUPPORTED;
     const int dvs = attn_slice(a->dv);
     if (!dvs) return FIS_ERR_UNSUPPORTED;
-    {  // every key run <= 128 keys on a large grid: the persistent short-run kernel
+    {  // every key run <= 256 keys on a large grid: the persistent short-run kernel
         const int r = fis_attn_short_launch(a, (cudaStream_t)stream);
         if (r >= 0) return r;
     }

@@ -1,6 +1,6 @@
-// Short-run attention on tcgen05 (sm_100a): every key run <= 128 keys -- the stacked step's cross
+// Short-run attention on tcgen05 (sm_100a): every key run <= 256 keys -- the stacked step's cross
 // attention (77-token prompts, sparse.py:303-338/352-361) and short self-attention runs (the
-// 8x8 level, sparse.py:265-300) -- as ONE persistent kernel per call:
+// 8x8 and 16x16 levels, sparse.py:265-300) -- as ONE persistent kernel per call:
 //
 //   out[r, :] = res[r, :] + softmax(Q K^T * scale)[r, :] V        (unet.py:279-293, 555-566)
 //
@@ -32,23 +32,32 @@
 #include <cstdlib>
 #include <cstring>
 
-#ifndef FIS_SHORT_STAGES
-#define FIS_SHORT_STAGES 3
-#endif
-
 namespace fis {
 namespace attn_short {
 
 using namespace fis::attn;
 
 constexpr int THREADS = 480, EPI_WARP0 = 4, TMA_WARP = 12, MMA_WARP = 13, STORE_WARP = 14;
-constexpr int STAGES = FIS_SHORT_STAGES, STAGE = 32768;  // Q chunk (16 KB) + K chunk (<= 16 KB), or 2 V^T chunks
-constexpr int CH = 16384;                 // one SW128 chunk: 128 rows x 128 B
-constexpr int PT = 2 * CH;                // P tile: 128 rows x 128 keys (bf16), two 64-key chunks
-constexpr int NEB = 6 - FIS_SHORT_STAGES, EBUF = 2 * CH;  // residual / output tiles: 128 rows x 128 columns (bf16)
-constexpr int NOB = 3;                    // O buffers in TMEM (128 columns each, after S at 0)
-constexpr int MAX_RUNS = 127;                        // runs per call (tile-count prefix in shared memory)
-constexpr int SMEM = STAGES * STAGE + PT + NEB * EBUF + 1024 + 256 + 4 * (MAX_RUNS + 1);
+constexpr int CH = 16384;       // one SW128 chunk: 128 rows x 128 B
+constexpr int MAX_RUNS = 127;   // runs per call (tile-count prefix in shared memory)
+// Per key-run bound KMAX:
+//   128: value slices of SW = 128 columns; stages of 32 KB (Q chunk 16 KB + K chunk <= 16 KB, or two
+//        V^T chunks {64 keys x 128}); P tile 32 KB; S in TMEM columns 0-127, three 128-column O buffers
+//   256: (129-256-key runs: the stacked step's 16x16-level self attention) SW = 64; two 48 KB
+//        stages (Q 16 KB + K <= 32 KB, or four V^T chunks {64 keys x 64}); P tile 64 KB; S in
+//        columns 0-255, four 64-column O buffers
+// Residual / output staging: three tiles of 128 rows x SW columns.
+template <int KMAX> struct KC;
+template <> struct KC<128> {
+    static constexpr int SW = 128, STAGES = 3, STAGE = 32768, PT = 32768, NOB = 3, NEB = 3;
+};
+template <> struct KC<256> {
+    static constexpr int SW = 64, STAGES = 2, STAGE = 49152, PT = 65536, NOB = 4, NEB = 3;
+};
+template <int KMAX> constexpr int smem_bytes() {
+    return KC<KMAX>::STAGES * KC<KMAX>::STAGE + KC<KMAX>::PT + KC<KMAX>::NEB * KC<KMAX>::SW * 256 + 1024 + 256 +
+           4 * (MAX_RUNS + 1);
+}
 
 struct Unit {
     int m0, rows, k0, nk, s0, s1;
@@ -99,11 +108,15 @@ FIS_DEV bool seek_unit(const fis_attn_args& a, const Sched& sc, int& u, Unit& x)
     return false;
 }
 
+template <int KMAX>
 __global__ void __launch_bounds__(THREADS, 1)
     attn_short_kernel(const fis_attn_args a, const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tq16,
                       const __grid_constant__ CUtensorMap tk, const __grid_constant__ CUtensorMap tv,
                       const __grid_constant__ CUtensorMap tr, const __grid_constant__ CUtensorMap to,
                       const __grid_constant__ CUtensorMap to8, int KP, int G_req) {
+    constexpr int SW = KC<KMAX>::SW, STAGES = KC<KMAX>::STAGES, STAGE = KC<KMAX>::STAGE, PT = KC<KMAX>::PT;
+    constexpr int NOB = KC<KMAX>::NOB, NEB = KC<KMAX>::NEB, EBUF = SW * 256;
+    constexpr uint32_t OCOL = KMAX;  // TMEM: S in columns [0, KMAX), O buffer b at OCOL + b * SW
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     unsigned char* ptile = smem + STAGES * STAGE;
@@ -122,7 +135,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     int* cum = (int*)(ebuf + NEB * EBUF + 256);  // [MAX_RUNS + 1]
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int dch = a.d / 64, ns = (a.dv + 127) / 128;
+    const int dch = a.d / 64, ns = (a.dv + SW - 1) / SW;
     __shared__ int ls_sh;  // launch-trace slot (profiling builds; -1 otherwise)
     if (tid == 0) {
         ls_sh = ltr_begin(13);
@@ -238,8 +251,8 @@ __global__ void __launch_bounds__(THREADS, 1)
                 for (int s = x.s0; s < x.s1; s++) {
                     const int st = it % STAGES;
                     if (it >= STAGES) mbar_wait(empty + st, ((it / STAGES) & 1) ^ 1);
-                    arrive_expect_tx(full + st, (uint32_t)(nvc * CH));
-                    for (int h = 0; h < nvc; h++) tma2d(sbase + st * STAGE + h * CH, &tv, x.k0 + h * 64, s * 128, full + st);
+                    arrive_expect_tx(full + st, (uint32_t)(nvc * SW * 128));
+                    for (int h = 0; h < nvc; h++) tma2d(sbase + st * STAGE + h * (SW * 128), &tv, x.k0 + h * 64, s * SW, full + st);
                     it++;
                 }
             }
@@ -280,10 +293,11 @@ __global__ void __launch_bounds__(THREADS, 1)
                 tc_fence_after();
                 if (lane == 0) {
                     const uint32_t sv = sbase + st * STAGE;
-                    const uint32_t id_o = idesc_bf16(128, min(128, a.dv - s * 128));
+                    const uint32_t id_o = idesc_bf16(128, min(SW, a.dv - s * SW));
                     for (int kk = 0; kk < ksteps; kk++) {
-                        const uint32_t off = (uint32_t)((kk >> 2) * CH + (kk & 3) * 32);
-                        mma_bf16(tmem + 128 + b * 128, sw128_desc(pbase + off), sw128_desc(sv + off), id_o,
+                        const uint32_t offp = (uint32_t)((kk >> 2) * CH + (kk & 3) * 32);
+                        const uint32_t offv = (uint32_t)((kk >> 2) * (SW * 128) + (kk & 3) * 32);
+                        mma_bf16(tmem + OCOL + b * SW, sw128_desc(pbase + offp), sw128_desc(sv + offv), id_o,
                                  kk ? 1u : 0u);
                     }
                     mma_commit(empty + st);
@@ -382,10 +396,10 @@ __global__ void __launch_bounds__(THREADS, 1)
             return true;
         };
         auto load_res = [&](const Unit& xx, int ss, int b) {
-            const int nbox = min(128, a.dv - ss * 128) / 64;
+            const int nbox = min(SW, a.dv - ss * SW) / 64;
             arrive_expect_tx(r_full + b, (uint32_t)(nbox * CH));
             for (int bx = 0; bx < nbox; bx++)
-                tma2d(ebase + b * EBUF + bx * CH, &tr, ss * 128 + bx * 64, xx.m0, r_full + b);
+                tma2d(ebase + b * EBUF + bx * CH, &tr, ss * SW + bx * 64, xx.m0, r_full + b);
         };
         int u = u0, s = have0 ? x0.s0 : 0;
         Unit x = x0;
@@ -404,19 +418,19 @@ __global__ void __launch_bounds__(THREADS, 1)
             const int eb_i = job % NEB;
             const unsigned char* eb = ebuf + eb_i * EBUF;
             const uint32_t ebs = ebase + eb_i * EBUF;
-            const int w = min(128, a.dv - s * 128), nbox = w / 64;
+            const int w = min(SW, a.dv - s * SW), nbox = w / 64;
             mbar_wait(staged + eb_i, (job / NEB) & 1);
             const int g8 = tma_out ? (x.rows >> 3) : 0;
             if (lane == 0) {
                 for (int bx = 0; bx < nbox; bx++) {
                     if (g8 == 16) {
                         asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(&to),
-                                     "r"(s * 128 + bx * 64), "r"(x.m0), "r"(ebs + bx * CH)
+                                     "r"(s * SW + bx * 64), "r"(x.m0), "r"(ebs + bx * CH)
                                      : "memory");
                     } else {
                         for (int g = 0; g < g8; g++)
                             asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(&to8),
-                                         "r"(s * 128 + bx * 64), "r"(x.m0 + g * 8), "r"(ebs + bx * CH + g * 1024)
+                                         "r"(s * SW + bx * 64), "r"(x.m0 + g * 8), "r"(ebs + bx * CH + g * 1024)
                                          : "memory");
                     }
                 }
@@ -425,7 +439,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             const int r0 = g8 * 8, upr = w >> 3, total = (x.rows - r0) * upr;
             if (total > 0) {
                 const int sh = w == 128 ? 4 : 3;
-                __nv_bfloat16* orow = (__nv_bfloat16*)ob + (long long)(x.m0 + r0) * a.out.ld + s * 128;
+                __nv_bfloat16* orow = (__nv_bfloat16*)ob + (long long)(x.m0 + r0) * a.out.ld + s * SW;
                 for (int i = lane; i < total; i += 32) {
                     const int r = i >> sh, un = i & (upr - 1);
                     const uint4 val = *(const uint4*)(eb + (un >> 3) * CH + sw128_off(r0 + r, un & 7));
@@ -462,25 +476,28 @@ __global__ void __launch_bounds__(THREADS, 1)
             const int eb_i = job % NEB;
             unsigned char* eb = ebuf + eb_i * EBUF;
             const int b = job % NOB;
-            const int w = min(128, a.dv - s * 128);
+            const int w = min(SW, a.dv - s * SW);
             mbar_wait(r_full + eb_i, (job / NEB) & 1);
             if (job == 2 && leader) ltr(ls_sh, 12);
             mbar_wait(o_full + b, (job / NOB) & 1);
             tc_fence_after();
             if (job == 0 && leader) ltr(ls_sh, 4);
             if (job == 2 && leader) ltr(ls_sh, 13);
-            if (half * 64 < w) {
-                unsigned char* boxp = eb + half * CH;
-                // both 32-column TMEM loads and the residual reads in flight before one wait
-                uint32_t o[64];
-                tmem_ld32_nw(tlane + 128 + b * 128 + half * 64, o);
-                tmem_ld32_nw(tlane + 128 + b * 128 + half * 64 + 32, o + 32);
-                uint4 rr[8];
+            constexpr int HC = SW / 2;  // columns per thread: its half of the slice
+            if (half * HC < w) {
+                const int c0 = half * HC;
+                unsigned char* boxp = eb + (c0 >> 6) * CH;
+                const int u0 = (c0 & 63) >> 3;
+                // the TMEM loads and the residual reads in flight before one wait
+                uint32_t o[HC];
 #pragma unroll
-                for (int k = 0; k < 8; k++) rr[k] = *(const uint4*)(boxp + sw128_off(er, k));
+                for (int c32 = 0; c32 < HC / 32; c32++) tmem_ld32_nw(tlane + OCOL + b * SW + c0 + c32 * 32, o + 32 * c32);
+                uint4 rr[HC / 8];
+#pragma unroll
+                for (int k = 0; k < HC / 8; k++) rr[k] = *(const uint4*)(boxp + sw128_off(er, u0 + k));
                 tmem_wait_ld();
 #pragma unroll
-                for (int k = 0; k < 8; k++) {
+                for (int k = 0; k < HC / 8; k++) {
                     uint32_t* h = (uint32_t*)&rr[k];
 #pragma unroll
                     for (int e2 = 0; e2 < 4; e2++) {
@@ -490,7 +507,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                                                   __fadd_rn(__uint_as_float(o[8 * k + 2 * e2 + 1]), hi));
                         h[e2] = *(const uint32_t*)&ov;
                     }
-                    *(uint4*)(boxp + sw128_off(er, k)) = rr[k];
+                    *(uint4*)(boxp + sw128_off(er, u0 + k)) = rr[k];
                 }
             }
             tc_fence_before();
@@ -518,7 +535,7 @@ __global__ void __launch_bounds__(THREADS, 1)
 
 FIS_LTR_SETTER(fis_ltr_set_short)
 
-// Would fis_attn_short_launch take this call? Every key run <= 128 keys, no pre-residual output,
+// Would fis_attn_short_launch take this call? Every key run <= 256 keys, no pre-residual output,
 // bf16 residual / output with 16-byte rows, and a grid
 // of >= 16 query tiles (stacked requests; batch-1 grids keep the general kernel's d-split /
 // latency paths). FIS_ATTN_SHORT=0 disables it, =2 forces it for every eligible shape.
@@ -526,7 +543,7 @@ int fis_attn_short_ok(const fis_attn_args* a) {
     static int mode = getenv("FIS_ATTN_SHORT") ? atoi(getenv("FIS_ATTN_SHORT")) : 1;
     if (mode == 0) return 0;
     const int maxk = a->nseg > 0 ? a->max_seg_k : a->n_keys;
-    if (maxk < 1 || maxk > 128 || a->pre.ptr || !a->res.ptr || a->res.dtype != FIS_BF16 || (a->res.ld % 8) ||
+    if (maxk < 1 || maxk > 256 || a->pre.ptr || !a->res.ptr || a->res.dtype != FIS_BF16 || (a->res.ld % 8) ||
         (((uintptr_t)a->res.ptr) & 15) || a->res.step_stride || a->out.dtype != FIS_BF16 || (a->out.ld % 8) ||
         (((uintptr_t)a->out.ptr) & 15) || (a->out.step_stride % 16) || (a->dv % 64) || (a->d % 64) ||
         a->nseg > fis::attn_short::MAX_RUNS)
@@ -550,7 +567,7 @@ int fis_attn_short_launch(const fis_attn_args* a, cudaStream_t stream) {
     const int KP = (maxk + 15) / 16 * 16;
     CUtensorMap tq, tq16, tk, tv, tr, to, to8;
     if (!encode_2d(&tq, a->q.ptr, a->m, a->d, a->q.ld, 128) || !encode_2d(&tq16, a->q.ptr, a->m, a->d, a->q.ld, 16) || !encode_2d(&tk, a->k.ptr, a->n_keys, a->d, a->k.ld, KP) ||
-        !encode_2d(&tv, a->vt.ptr, a->dv, a->n_keys, a->vt.ld, 128) ||
+        !encode_2d(&tv, a->vt.ptr, a->dv, a->n_keys, a->vt.ld, KP <= 128 ? 128 : 64) ||
         !encode_2d(&tr, a->res.ptr, a->m, a->dv, a->res.ld, 128))
         return -1;
     // output maps (whole tiles / 8-row groups); a per-step output stride takes the row-store path
@@ -566,20 +583,24 @@ int fis_attn_short_launch(const fis_attn_args* a, cudaStream_t stream) {
     static int g_env = getenv("FIS_ATTN_SHORT_G") ? atoi(getenv("FIS_ATTN_SHORT_G")) : 0;
     static bool configured = false;
     if (!configured) {
-        if (cudaFuncSetAttribute(attn_short_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM) != cudaSuccess)
+        if (cudaFuncSetAttribute(attn_short_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes<128>()) !=
+                cudaSuccess ||
+            cudaFuncSetAttribute(attn_short_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes<256>()) !=
+                cudaSuccess)
             return -1;
         configured = true;
     }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)nsm);  // persistent: one CTA per SM loops over the units
     cfg.blockDim = dim3(THREADS);
-    cfg.dynamicSmemBytes = SMEM;
+    cfg.dynamicSmemBytes = KP <= 128 ? smem_bytes<128>() : smem_bytes<256>();
     cfg.stream = stream;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = fis_pdl_enabled() ? 1 : 0;
-    return cudaLaunchKernelEx(&cfg, attn_short_kernel, *a, tq, tq16, tk, tv, tr, to, to8, KP, g_env) == cudaSuccess
-               ? FIS_OK : FIS_ERR_LAUNCH;
+    const cudaError_t e = KP <= 128 ? cudaLaunchKernelEx(&cfg, attn_short_kernel<128>, *a, tq, tq16, tk, tv, tr, to, to8, KP, g_env)
+                                    : cudaLaunchKernelEx(&cfg, attn_short_kernel<256>, *a, tq, tq16, tk, tv, tr, to, to8, KP, g_env);
+    return e == cudaSuccess ? FIS_OK : FIS_ERR_LAUNCH;
 }

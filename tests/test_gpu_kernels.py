@@ -171,7 +171,10 @@ def test_fused_attention_vs_torch(env, m, nk, d):
     # >= 16 query tiles with every key run <= 128: the persistent short-run kernel (fis_attn_short.cu)
     (320, [205, 410, 1024, 77, 300, 0, 515] * 3, [77, 60, 77, 1, 77, 77, 33] * 3, 80),
     (1280, [64] * 40, None, 0),
-    (640, [128, 200, 17, 256] * 6, [77] * 24, 80)])
+    (640, [128, 200, 17, 256] * 6, [77] * 24, 80),
+    # 129-256-key runs on >= 16 query tiles: the short-run kernel's 256-key configuration
+    (1280, [256] * 10, None, 0),
+    (640, [200, 150, 256, 129, 0] * 5, None, 0)])
 @pytest.mark.parametrize("share", [False, True])
 def test_segment_attention_vs_torch(env, d, qlens, klens, kpad, share):
     """fis_attn with ragged segments (batched requests): each query run attends to its own key run only."""
