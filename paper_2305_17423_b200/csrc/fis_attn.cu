@@ -619,7 +619,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                         }
                     }
                     tc_fence_before();
-                    mbar_arrive(s_free + b);
+                    if (!resident) mbar_arrive(s_free + b);
                 } else if (pass == 2) {  // P_j -> bf16 P tile j & 1 (SW128, K-major)
                     const int pb = j & 1;
                     float off;
@@ -683,12 +683,14 @@ __global__ void __launch_bounds__(THREADS, 1)
                     }
                     if (onepass) lrow += psum;
                     tc_fence_before();
-                    mbar_arrive(s_free + b);  // S_j fully read
+                    // S_j fully read (resident S blocks are never re-issued: nobody waits on s_free, and
+                    // a second arrival per thread without a wait in between is a barrier misuse)
+                    if (!resident) mbar_arrive(s_free + b);
                     fence_async_smem();       // generic-proxy P writes -> tensor-core reads
                     mbar_arrive(p_ready + pb);
                 } else {
                     tc_fence_before();
-                    mbar_arrive(s_free + b);
+                    if (!resident) mbar_arrive(s_free + b);
                 }
                 sb++;
             }
