@@ -340,38 +340,59 @@ class Engine(Launcher):
                 with torch.cuda.stream(s):
                     g.capture_begin()
                     try:
-                        outs = self._text_kv(emb_buf)
+                        _, flat = self._text_kv(emb_buf, want_flat=True)
                     finally:
                         g.capture_end()
             finally:
                 if gc_on:
                     gc.enable()
             torch.cuda.current_stream().wait_stream(s)
-            ent = self._kv_graphs[key] = (g, emb_buf, outs)
-        g, emb_buf, outs = ent
+            ent = self._kv_graphs[key] = (g, emb_buf, flat)
+        g, emb_buf, flat = ent
         emb_buf.copy_(emb_h)
         g.replay()
-        return {lid: tuple(x.clone() if x is not None else None for x in kv) for lid, kv in outs.items()}
+        # the outputs live in one flat buffer: one copy gives the caller its own K / V^T / M^T (the
+        # next replay overwrites the graph's buffer; 48 per-tensor clones cost ~1 ms per edit)
+        return self._kv_views(flat.clone(), emb_h.shape[0])
 
-    def _text_kv(self, emb: torch.Tensor):
-        nt = emb.shape[0]
+    def _kv_layout(self, nt):
+        """Element offsets of every cross layer's K [nt, C], V^T [C, pad16(nt)] and M^T [nt, C] in
+        one flat buffer (each view 128-byte aligned), and the buffer's length."""
+        lay, off = [], 0
+        for lid, (wq, _, _, _) in self.W.ca.items():
+            c = wq.shape[0]
+            views = []
+            for shape in ((nt, c), (c, _pad(nt)), (nt, c)):
+                views.append((off, shape))
+                off += (shape[0] * shape[1] + 63) // 64 * 64
+            lay.append((lid, views))
+        return lay, off
+
+    def _kv_views(self, flat, nt):
         out = {}
+        for lid, views in self._kv_layout(nt)[0]:
+            k, vt, mt = (flat[o:o + sh[0] * sh[1]].view(sh) for o, sh in views)
+            out[lid] = (k, vt, None, mt)
+        return out
+
+    def _text_kv(self, emb: torch.Tensor, want_flat: bool = False):
+        nt = emb.shape[0]
         # bf16 mode: the embeddings as bf16 operands -> tcgen05 split-K GEMMs (fp32 embeddings would
         # take the SIMT kernel: ~100 us per layer GEMM); fp32 / tf32x3 keep the unsplit fp32 path
         bf = self.act == torch.bfloat16
         if bf:
             emb = emb.to(torch.bfloat16)
         sp = None if bf else 1
+        # every output in one zeroed flat buffer (V^T's pad columns stay zero)
+        flat = torch.zeros(self._kv_layout(nt)[1], dtype=self.act, device=self.dev)
+        out = self._kv_views(flat, nt)
         for lid, (wq, wk, wv, scale) in self.W.ca.items():
             c = wq.shape[0]
-            k = torch.empty((nt, c), dtype=self.act, device=self.dev)
-            vt = torch.zeros((c, _pad(nt)), dtype=self.act, device=self.dev)
-            mt = torch.empty((nt, c), dtype=self.act, device=self.dev)
+            k, vt, _, mt = out[lid]
             self.gemm(nt, c, emb.shape[1], a=DRef(emb), b=DRef(wk), d=DRef(k), splits=sp)
             self.gemm(nt, c, emb.shape[1], a=DRef(emb), b=DRef(wv), d=DRef(vt), d_trans=True, splits=sp)
             self.gemm(nt, c, c, a=DRef(k), b=DRef(wq), d=DRef(mt), splits=sp)
-            out[lid] = (k, vt, None, mt)
-        return out
+        return (out, flat) if want_flat else out
 
     def text_kv_stacked(self, text_embs):
         """Text K / V^T of R prompts computed as ONE GEMM pair per cross layer over the stacked
