@@ -131,7 +131,9 @@ def run_detect(h, w, c, t1, t2, radius, x_ref=None, y_ref=None, values_in=None):
 class DevicePlan:
     """Output of fis_mask_plan: per-level bits, active pixel lists, pixel->row maps, tile lists."""
 
-    def __init__(self, mask_dev: torch.Tensor, h, w, levels, radius=0, tiles=True):
+    def __init__(self, mask_dev: torch.Tensor, h, w, levels, radius=0, tiles=True, sync=True):
+        """sync=False: the plan kernel is launched but its counts are not read back yet (call
+        DevicePlan.finish_all over a batch of plans: one device->host copy for all of them)."""
         dev = mask_dev.device
         self.h, self.w, self.levels = h, w, levels
         self.bits, self.rows, self.index, self.tiles = [], [], [], []
@@ -152,9 +154,19 @@ class DevicePlan:
         self.counts_dev = torch.zeros(2 * levels, dtype=torch.int32, device=dev)
         a.counts = L.ptr(self.counts_dev)
         L.call("fis_mask_plan", a)
-        c = self.counts_dev.cpu().tolist()  # one sync per plan: sizes the GEMM launches
-        self.n_active = c[:levels]
-        self.n_tiles = c[levels:]
+        if sync:
+            self._set_counts(self.counts_dev.cpu().tolist())  # one sync per plan: sizes the GEMM launches
+
+    def _set_counts(self, c):
+        self.n_active = c[:self.levels]
+        self.n_tiles = c[self.levels:]
+
+    @staticmethod
+    def finish_all(plans):
+        """Read the counts of plans built with sync=False in one device->host copy."""
+        if plans:
+            for dp, c in zip(plans, torch.stack([dp.counts_dev for dp in plans]).cpu().tolist()):
+                dp._set_counts(c)
 
     def level_bits(self, l) -> np.ndarray:
         return self.bits[l].cpu().numpy().astype(bool).reshape(self.h >> l, self.w >> l)

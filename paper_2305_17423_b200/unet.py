@@ -19,6 +19,7 @@ from __future__ import annotations
 from collections import defaultdict
 from dataclasses import dataclass, field
 
+import os
 import numpy as np
 import torch
 
@@ -629,8 +630,10 @@ class BatchedEditPlan:
             raise ContractViolation("batched edits run in bf16 (fused segment attention)")
         dev, i32 = eng.dev, torch.int32
         self.R = R
-        self.dps = [DevicePlan(torch.from_numpy(m.bits.astype(np.uint8).ravel()).to(dev), cfg.latent_h,
-                               cfg.latent_w, cfg.levels) for m in masks]
+        # all R masks in one host->device copy, all R plan kernels before one read-back of their counts
+        bits_d = torch.from_numpy(np.stack([m.bits.astype(np.uint8).ravel() for m in masks])).to(dev)
+        self.dps = [DevicePlan(bits_d[r], cfg.latent_h, cfg.latent_w, cfg.levels, sync=False) for r in range(R)]
+        DevicePlan.finish_all(self.dps)
         lists, qsegs, row_img = {}, {}, {}
         for l in range(cfg.levels):
             hw = eng.hw(l)
@@ -754,7 +757,7 @@ def edit_batch(sessions, config: UNetConfig) -> list:
     b_texts = [texts[slot[i]] if i in slot else texts[0] for i in range(nb)]
     skv = eng.text_kv_stacked(b_texts)
     bp = BatchedEditPlan(eng, stacked, b_masks, None, b_lat0, stacked_kv=skv)
-    _Runner(eng, bp.plan, _use_graphs()).run(start, T)
+    _Runner(eng, bp.plan, _use_graphs() and os.environ.get("FIS_BATCH_GRAPH", "1") != "0").run(start, T)
     final = bp.final_latents(eng, stacked)
     hw = eng.hw(0)
     img = [v.index for v in views]  # stacked image of each (sorted) session
