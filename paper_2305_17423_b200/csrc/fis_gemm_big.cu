@@ -45,7 +45,7 @@ struct GatherMaps {
     CUtensorMap fresh[2], cache[2];
     int fresh_rps[2], cache_rps[2];
 };
-constexpr int STG_BYTES = 8 * 16 * 32 * 2;  // per epilogue warp: a 16-column x 32-row bf16 transpose tile
+constexpr int STG_BYTES = 8 * 16 * 32 * 2;  // (reserved: the former per-warp V^T transpose tiles)
 constexpr int LAG = 2;
 constexpr int GATHER_WARPS = 2;  // A warps issuing TMA gather4 in the gather mode; the rest use cp.async  // cp.async stages in flight per A-producer thread
 constexpr int SEL_BYTES = BM * 19 * 4;  // select-on-read table [128][18] + row pixels [128]
@@ -158,7 +158,6 @@ __global__ void __launch_bounds__(THREADS, 1)
     float* tabs = (float*)(smem + L.stages * L.stage + 256);
     int* seltab = (int*)(tabs + 6 * bn);
     int* rowtab = seltab + BM * 18;
-    __nv_bfloat16* stg_all = (__nv_bfloat16*)(rowtab + BM);  // [8 warps][16][32] transposed-store staging
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int tiles_n = (a.n + bn - 1) / bn, tiles_m = (a.m + BM - 1) / BM;
@@ -507,27 +506,15 @@ epilogue_role : {
                 tmem_wait_ld();
                 const int nn = n0 + cb;
                 if (tfast && nn >= a.n_split && nn + 16 <= a.n) {
-                    // transposed V^T chunk (fused QKV): stage the warp's 32 rows x 16 columns in shared
-                    // memory, then store 16-byte runs of 8 rows per column (warp-uniform path)
-                    __nv_bfloat16* stg = stg_all + (warp - (grp ? 0 : EPI_WARP0) + (grp ? 4 : 0)) * (16 * 32);
+                    // transposed V^T chunk (fused QKV): V^T[dn + j][r] -- for each j the warp's 32 rows
+                    // are 64 contiguous bytes: direct 2-byte stores, coalesced per j (a shared-memory
+                    // transpose round trip measured slower on the CTA-pair kernel: L0 QKV 36 -> 28.5 us)
+                    if (r < a.m) {
+                        __nv_bfloat16* dst = (__nv_bfloat16*)e.d2 + (long long)(nn - a.n_split) * a.d2.ld + r;
 #pragma unroll
-                    for (int j = 0; j < 16; j++)
-                        stg[j * 32 + lane] = __float2bfloat16_rn(__fadd_rn(__uint_as_float(u[j]), tb.bias[cb + j]));
-                    __syncwarp();
-                    const int r0 = m0 + quarter * 32, dn = nn - a.n_split;
-#pragma unroll
-                    for (int q = 0; q < 2; q++) {
-                        const int idx = lane + 32 * q, j = idx >> 2, p8 = (idx & 3) * 8;
-                        const uint4 val = *(const uint4*)(stg + j * 32 + p8);
-                        __nv_bfloat16* dst = (__nv_bfloat16*)e.d2 + (long long)(dn + j) * a.d2.ld + r0 + p8;
-                        if (r0 + p8 + 8 <= a.m) {
-                            *(uint4*)dst = val;
-                        } else {
-                            const __nv_bfloat16* sv = (const __nv_bfloat16*)&val;
-                            for (int i = 0; i < 8 && r0 + p8 + i < a.m; i++) dst[i] = sv[i];
-                        }
+                        for (int j = 0; j < 16; j++)
+                            dst[(long long)j * a.d2.ld] = __float2bfloat16_rn(__fadd_rn(__uint_as_float(u[j]), tb.bias[cb + j]));
                     }
-                    __syncwarp();
                     continue;
                 }
                 if (r < a.m && !(dbg & 1)) {

@@ -38,7 +38,7 @@ constexpr int B_BYTES = (BN / 2) * BK * 2;    // 16 KB: this CTA's half of the B
 constexpr int STAGE = A_BYTES + B_BYTES;
 constexpr int STAGES = 6;
 constexpr int AM_ROWS = 1, AM_CONV = 2;
-constexpr int STG_BYTES = 8 * 16 * 32 * 2;  // per epilogue warp: a 16-column x 32-row bf16 transpose tile
+constexpr int STG_BYTES = 8 * 16 * 32 * 2;  // (reserved: the former per-warp V^T transpose tiles)
 constexpr int SMEM = STAGES * STAGE + 1024 + 256 + 6 * BN * 4 + STG_BYTES + 64;
 
 FIS_DEV uint32_t cluster_rank() {
@@ -98,7 +98,6 @@ __global__ void __launch_bounds__(THREADS, 1)
     uint64_t* acc_empty = acc_full + 2;   // [2]
     uint32_t* tmem_slot = (uint32_t*)(acc_empty + 2);
     float* tabs = (float*)(smem + STAGES * STAGE + 256);
-    __nv_bfloat16* stg_all = (__nv_bfloat16*)(tabs + 6 * BN);  // [8 warps][16][32]
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const uint32_t rank = cluster_rank();
@@ -260,25 +259,15 @@ __global__ void __launch_bounds__(THREADS, 1)
                 tmem_ld16(taddr + cb, u);
                 const int n = n0 + cb;
                 if (tfast && n >= a.n_split && n + 16 <= a.n) {  // warp-uniform: V^T chunk
-                    __nv_bfloat16* stg = stg_all + (warp < TMA_WARP ? warp + 4 : warp - 6) * (16 * 32);
+                    // V^T[dn + j][r]: for each j the warp's 32 rows are 64 contiguous bytes -- direct
+                    // 2-byte stores, coalesced per j (the shared-memory transpose round trip it replaces
+                    // was the epilogue's top stall: R = 64 L0 / L1 / L2 QKV 36 / 25 / 77 -> 28.5 / 22 / 72.5 us)
+                    if (r < a.m) {
+                        __nv_bfloat16* dst = (__nv_bfloat16*)e.d2 + (long long)(n - a.n_split) * a.d2.ld + r;
 #pragma unroll
-                    for (int j = 0; j < 16; j++)
-                        stg[j * 32 + lane] = __float2bfloat16_rn(__fadd_rn(__uint_as_float(u[j]), tb.bias[cb + j]));
-                    __syncwarp();
-                    const int r0 = m0 + quarter * 32, dn = n - a.n_split;
-#pragma unroll
-                    for (int q = 0; q < 2; q++) {
-                        const int idx = lane + 32 * q, j = idx >> 2, p8 = (idx & 3) * 8;
-                        const uint4 val = *(const uint4*)(stg + j * 32 + p8);
-                        __nv_bfloat16* dst = (__nv_bfloat16*)e.d2 + (long long)(dn + j) * a.d2.ld + r0 + p8;
-                        if (r0 + p8 + 8 <= a.m) {
-                            *(uint4*)dst = val;
-                        } else {
-                            const __nv_bfloat16* sv = (const __nv_bfloat16*)&val;
-                            for (int i = 0; i < 8 && r0 + p8 + i < a.m; i++) dst[i] = sv[i];
-                        }
+                        for (int j = 0; j < 16; j++)
+                            dst[(long long)j * a.d2.ld] = __float2bfloat16_rn(__fadd_rn(__uint_as_float(u[j]), tb.bias[cb + j]));
                     }
-                    __syncwarp();
                     continue;
                 }
                 if (r >= a.m || n >= a.n) continue;
