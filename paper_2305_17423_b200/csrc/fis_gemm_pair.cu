@@ -22,6 +22,7 @@
 //                     then one arrival on the leader's accumulator-empty barrier.
 #include "fis_tc.cuh"
 #include "fis_tma.cuh"
+#include <cstdlib>
 
 int fis_tma_a_encode(const fis_gemm_args* a, CUtensorMap* ta, CUtensorMap* ta2);
 const CUtensorMap* fis_weight_map(const void* base, long long n, long long k, long long ld, int box);
@@ -36,10 +37,15 @@ constexpr int BN = 256;                       // pair tile: 256 rows x 256 colum
 constexpr int A_BYTES = BM * BK * 2;          // 16 KB: this CTA's 128 rows of the K block
 constexpr int B_BYTES = (BN / 2) * BK * 2;    // 16 KB: this CTA's half of the B tile
 constexpr int STAGE = A_BYTES + B_BYTES;
-constexpr int STAGES = 6;
+// OST (small K, plain row-major epilogue): 5 stages + two 16 KB output staging boxes for TMA stores
+template <bool OST> struct Cfg {
+    static constexpr int STAGES = OST ? 5 : 6;
+};
 constexpr int AM_ROWS = 1, AM_CONV = 2;
 constexpr int STG_BYTES = 8 * 16 * 32 * 2;  // (reserved: the former per-warp V^T transpose tiles)
-constexpr int SMEM = STAGES * STAGE + 1024 + 256 + 6 * BN * 4 + STG_BYTES + 64;
+constexpr int TAIL = 15360;  // barriers (256) + epilogue tables (6 x BN floats) + reserved, 1 KB aligned
+static_assert(256 + 6 * BN * 4 + STG_BYTES <= TAIL, "pair kernel tail");
+template <bool OST> constexpr int smem_bytes() { return Cfg<OST>::STAGES * STAGE + TAIL + (OST ? 2 * 16384 : 0); }
 
 FIS_DEV uint32_t cluster_rank() {
     uint32_t r;
@@ -86,9 +92,12 @@ FIS_DEV void tmem_ld16(uint32_t taddr, uint32_t* u) {
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
+template <bool OST>
 __global__ void __launch_bounds__(THREADS, 1)
     gemm_pair_kernel(const fis_gemm_args a, const __grid_constant__ CUtensorMap tmap_b,
-                     const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_a2, int amode) {
+                     const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_a2,
+                     const __grid_constant__ CUtensorMap tmap_d, int amode) {
+    constexpr int STAGES = Cfg<OST>::STAGES;
     const int ls = ltr_begin(14);
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -98,6 +107,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     uint64_t* acc_empty = acc_full + 2;   // [2]
     uint32_t* tmem_slot = (uint32_t*)(acc_empty + 2);
     float* tabs = (float*)(smem + STAGES * STAGE + 256);
+    unsigned char* ostg = smem + STAGES * STAGE + TAIL;  // OST: two [128 x 64] bf16 SW128 boxes
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const uint32_t rank = cluster_rank();
@@ -217,6 +227,8 @@ __global__ void __launch_bounds__(THREADS, 1)
         const bool tfast = fast && !e.res && a.n_split > 0 && a.d2_trans && a.d2.dtype == FIS_BF16 &&
                            (a.d2.ld % 8) == 0 && (((uintptr_t)e.d2) & 15) == 0;
         const int nrow_end = a.n_split > 0 ? a.n_split : a.n;  // row-major columns
+        const bool ost = OST && fast && (a.n_split % 64) == 0;
+        int nbox = 0;
         EpiTab tb;
         tb.mean = tabs;
         tb.rstd = tb.mean + BN;
@@ -254,10 +266,39 @@ __global__ void __launch_bounds__(THREADS, 1)
             tc_fence_after();
             const uint32_t taddr = tmem + buf * BN + ((uint32_t)(quarter * 32) << 16);
             const int r = m0 + lr;
-            for (int cb = 16 * grp; cb < BN; cb += 32) {  // the two warp groups take alternate chunks
+            for (int bx = 0; bx < BN / 64; bx++) {
+            // OST: a 64-column box of plain row-major outputs goes through a SW128 staging box and
+            // one TMA store instead of 32-byte row stores per thread
+            const bool sbox = ost && n0 + bx * 64 + 64 <= nrow_end;
+            unsigned char* sb = ostg + (nbox & 1) * 16384;
+            if (sbox) {
+                if (et == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");  // box nbox - 2 read
+                asm volatile("bar.sync 1, 256;" ::: "memory");
+            }
+            for (int h = 0; h < 2; h++) {  // the two warp groups take alternate 16-column chunks
+                const int cb = bx * 64 + 16 * grp + 32 * h;
                 uint32_t u[16];
                 tmem_ld16(taddr + cb, u);
                 const int n = n0 + cb;
+                if (sbox) {
+                    float v[16];
+#pragma unroll
+                    for (int j = 0; j < 16; j++) v[j] = __fadd_rn(__uint_as_float(u[j]), tb.bias[cb + j]);
+                    if (e.res && r < a.m) {
+                        float q[16];
+                        load_row16(e.res, a.res.dtype, (long long)r * a.res.ld + n, 16, q);
+#pragma unroll
+                        for (int j = 0; j < 16; j++) v[j] = __fadd_rn(v[j], q[j]);
+                    }
+                    uint4 o[2];
+                    __nv_bfloat162* hh = (__nv_bfloat162*)o;
+#pragma unroll
+                    for (int j = 0; j < 8; j++) hh[j] = __floats2bfloat162_rn(v[2 * j], v[2 * j + 1]);
+                    const int un = (cb & 63) >> 3;
+                    *(uint4*)(sb + sw128_off(lr, un)) = o[0];
+                    *(uint4*)(sb + sw128_off(lr, un + 1)) = o[1];
+                    continue;
+                }
                 if (tfast && n >= a.n_split && n + 16 <= a.n) {  // warp-uniform: V^T chunk
                     // V^T[dn + j][r]: for each j the warp's 32 rows are 64 contiguous bytes -- direct
                     // 2-byte stores, coalesced per j (the shared-memory transpose round trip it replaces
@@ -294,6 +335,18 @@ __global__ void __launch_bounds__(THREADS, 1)
                     row_epilogue_any(a, e, tb, r, cb, n0, v);
                 }
             }
+            if (sbox) {
+                fence_async_smem();  // generic-proxy box writes -> the TMA store
+                asm volatile("bar.sync 1, 256;" ::: "memory");
+                if (et == 0) {
+                    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(&tmap_d),
+                                 "r"(n0 + bx * 64), "r"(m0), "r"(smem_u32(sb))
+                                 : "memory");
+                    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                }
+                nbox++;
+            }
+            }
             tc_fence_before();
             asm volatile("bar.sync 1, 256;" ::: "memory");  // every epilogue thread of this CTA read the buffer
             if (et == 0)
@@ -301,6 +354,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                                  leader_empty0 + (uint32_t)(buf * 8))
                              : "memory");
         }
+        if (OST && et == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // staging read before exit
     }
     ltr(ls, 7);
     tc_fence_before();
@@ -350,18 +404,34 @@ int fis_gemm_pair_ok(const fis_gemm_args* a, int single_bn) {
     return force || c2 < c1;
 }
 
+// OST variant for small-K GEMMs with a plain bf16 row-major epilogue (FIS_PAIR_OST: 0 off, 2 any K)
+static bool pair_ost(const fis_gemm_args* a, CUtensorMap* td) {
+    static int mode = getenv("FIS_PAIR_OST") ? atoi(getenv("FIS_PAIR_OST")) : 1;
+    if (mode == 0 || (mode == 1 && a->k > 640)) return false;
+    if (a->epi != FIS_EPI_NONE || a->alpha != 1.0f || a->pre.ptr || a->pre2.ptr || a->bias2.ptr || a->lat.ptr ||
+        a->d_rows || a->d_trans || a->d.dtype != FIS_BF16 || a->d.step_stride || (a->d.ld % 8) ||
+        (a->res.ptr && ((a->res.ld % 8) || a->res.step_stride)) || (a->n_split % 64))
+        return false;
+    const int ncols = a->n_split > 0 ? a->n_split : a->n;
+    return encode_2d(td, a->d.ptr, a->m, ncols, a->d.ld, 128);
+}
+
 int fis_gemm_pair_launch(const fis_gemm_args* a, cudaStream_t stream) {
-    CUtensorMap ta, ta2;
+    CUtensorMap ta, ta2, td;
     std::memset(&ta, 0, sizeof(ta));
     std::memset(&ta2, 0, sizeof(ta2));
+    std::memset(&td, 0, sizeof(td));
     const int amode = fis_tma_a_encode(a, &ta, &ta2);
     if (!amode) return FIS_ERR_UNSUPPORTED;
     const CUtensorMap* tm = fis_weight_map(a->b.ptr, a->n, a->k, a->b.ld, fis::pair::BN / 2);
     if (!tm) return FIS_ERR_UNSUPPORTED;
+    const bool ost = pair_ost(a, &td);
     static bool configured = false;
     if (!configured) {
-        if (cudaFuncSetAttribute(fis::pair::gemm_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 fis::pair::SMEM + 1024) != cudaSuccess)
+        if (cudaFuncSetAttribute(fis::pair::gemm_pair_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 fis::pair::smem_bytes<false>() + 1024) != cudaSuccess ||
+            cudaFuncSetAttribute(fis::pair::gemm_pair_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 fis::pair::smem_bytes<true>() + 1024) != cudaSuccess)
             return FIS_ERR_UNSUPPORTED;
         configured = true;
     }
@@ -370,7 +440,7 @@ int fis_gemm_pair_launch(const fis_gemm_args* a, cudaStream_t stream) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(2 * npairs);
     cfg.blockDim = dim3(fis::pair::THREADS);
-    cfg.dynamicSmemBytes = fis::pair::SMEM + 1024;
+    cfg.dynamicSmemBytes = (ost ? fis::pair::smem_bytes<true>() : fis::pair::smem_bytes<false>()) + 1024;
     cfg.stream = stream;
     cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -381,8 +451,9 @@ int fis_gemm_pair_launch(const fis_gemm_args* a, cudaStream_t stream) {
     attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = fis_pdl_enabled() ? 2 : 1;
-    if (cudaLaunchKernelEx(&cfg, fis::pair::gemm_pair_kernel, *a, *tm, ta, ta2, amode) != cudaSuccess)
-        return FIS_ERR_LAUNCH;
+    const cudaError_t e = ost ? cudaLaunchKernelEx(&cfg, fis::pair::gemm_pair_kernel<true>, *a, *tm, ta, ta2, td, amode)
+                              : cudaLaunchKernelEx(&cfg, fis::pair::gemm_pair_kernel<false>, *a, *tm, ta, ta2, td, amode);
+    if (e != cudaSuccess) return FIS_ERR_LAUNCH;
     g_pair_launched++;
     return FIS_OK;
 }
