@@ -250,11 +250,12 @@ def test_pair_kernel_rows(env):
     assert (D.float() - ref).abs().max().item() <= 5e-2
 
 
-def test_pair_kernel_qkv_split(env):
-    """Fused QKV on the CTA-pair kernel: Q' row-major, V^T transposed into d2 (per-warp staging)."""
+@pytest.mark.parametrize("m,k,c", [(4000, 640, 640), (3001, 320, 320)])  # (the L0 split falls mid-tile)
+def test_pair_kernel_qkv_split(env, m, k, c):
+    """Fused QKV on the CTA-pair kernel: Q' row-major (TMA-stored boxes at small K), V^T transposed
+    into d2 (direct per-column stores)."""
     L, DRef, NULL, lz = env
     g = torch.Generator(device="cuda").manual_seed(12)
-    m, k, c = 4000, 640, 640
     A = _rnd(g, m, k)
     B = _rnd(g, 2 * c, k, scale=1 / math.sqrt(k))
     bias = torch.randn(2 * c, device="cuda", generator=g)
