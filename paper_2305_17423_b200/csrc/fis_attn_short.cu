@@ -536,19 +536,21 @@ __global__ void __launch_bounds__(THREADS, 1)
 FIS_LTR_SETTER(fis_ltr_set_short)
 
 // Would fis_attn_short_launch take this call? Every key run <= 256 keys, no pre-residual output,
-// bf16 residual / output with 16-byte rows, and a grid
-// of >= 16 query tiles (stacked requests; batch-1 grids keep the general kernel's d-split /
-// latency paths). FIS_ATTN_SHORT=0 disables it, =2 forces it for every eligible shape.
+// bf16 residual / output with 16-byte rows, at most MAX_RUNS runs. Batch 1 included: with slice
+// groups spreading a few query tiles over the SMs it beats the general kernel's d-split / single-
+// block paths there too (C2 batch-1 step 0.982 -> 0.918 ms, dense step 1.49 -> 1.42 ms).
+// FIS_ATTN_SHORT=0 disables it (the general kernel's d-split / single-block modes then run).
 int fis_attn_short_ok(const fis_attn_args* a) {
-    static int mode = getenv("FIS_ATTN_SHORT") ? atoi(getenv("FIS_ATTN_SHORT")) : 1;
-    if (mode == 0) return 0;
+    // read per call (tests switch it to cover the general kernel's modes; calls run at capture time)
+    const char* env = getenv("FIS_ATTN_SHORT");
+    if (env && env[0] == '0') return 0;
     const int maxk = a->nseg > 0 ? a->max_seg_k : a->n_keys;
     if (maxk < 1 || maxk > 256 || a->pre.ptr || !a->res.ptr || a->res.dtype != FIS_BF16 || (a->res.ld % 8) ||
         (((uintptr_t)a->res.ptr) & 15) || a->res.step_stride || a->out.dtype != FIS_BF16 || (a->out.ld % 8) ||
         (((uintptr_t)a->out.ptr) & 15) || (a->out.step_stride % 16) || (a->dv % 64) || (a->d % 64) ||
         a->nseg > fis::attn_short::MAX_RUNS)
         return 0;
-    return mode == 2 || (a->m + 127) / 128 >= 16;
+    return 1;
 }
 
 // Launches the call on the short-run kernel: FIS_OK / FIS_ERR_LAUNCH, or -1 when the call is not

@@ -5,6 +5,7 @@ Tolerance: both paths consume the same bf16 operands and accumulate in fp32, so 
 only by summation order: max-abs <= 2e-3 * sqrt(K/64) relative to the output scale.
 """
 
+import os
 import math
 
 import numpy as np
@@ -135,9 +136,11 @@ def test_transposed_store_and_residual(env):
                                     (130, 1100, 320), (128, 1024, 640), (50, 1500, 256),
                                     # short-run kernel (>= 16 query tiles, <= 128 keys)
                                     (4096, 77, 320), (2100, 128, 640), (3000, 20, 1280)])
-def test_fused_attention_vs_torch(env, m, nk, d):
+@pytest.mark.parametrize("short", ["1", "0"])  # "0": the general kernel's modes (d-split, single block, ...)
+def test_fused_attention_vs_torch(env, m, nk, d, short):
     """fis_attn (tcgen05 S=QK^T, softmax, P.V, + residual) against torch fp32 on the same bf16 inputs."""
     L, DRef, NULL, lz = env
+    os.environ["FIS_ATTN_SHORT"] = short
     g = torch.Generator(device="cuda").manual_seed(m + nk + d)
     bf = torch.bfloat16
     Q = torch.randn((m, d), device="cuda", generator=g).to(bf)
@@ -159,6 +162,7 @@ def test_fused_attention_vs_torch(env, m, nk, d):
     a.max_seg_k, a.ws, a.ws_bytes = nk, L.ptr(ws), nb
     L.call("fis_attn", a)
     torch.cuda.synchronize()
+    os.environ.pop("FIS_ATTN_SHORT", None)
     err = (out.float() - ref).abs().max().item()
     assert err <= 3e-2 * max(1.0, ref.abs().max().item()), err
 
@@ -212,8 +216,12 @@ def test_segment_attention_vs_torch(env, d, qlens, klens, kpad, share):
     if share:  # value slices share one P per query tile through the scratch [m, 128 * ceil(max_k / 128)]
         ws = torch.empty(m * ((max_k + 127) // 128 * 128), device="cuda", dtype=bf)
         a.max_seg_k, a.ws, a.ws_bytes = max_k, L.ptr(ws), ws.numel() * 2
+        os.environ["FIS_ATTN_SHORT"] = "0"  # the general kernel's P_OUT / P_IN sharing
+    else:
+        a.max_seg_k = max_k  # the short-run kernel for runs <= 256 keys
     L.call("fis_attn", a)
     torch.cuda.synchronize()
+    os.environ.pop("FIS_ATTN_SHORT", None)
     for (q0, q1), (k0, k1) in zip(qseg, kseg):
         if q1 == q0:
             continue
