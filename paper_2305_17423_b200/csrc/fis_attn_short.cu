@@ -567,9 +567,15 @@ int fis_attn_short_launch(const fis_attn_args* a, cudaStream_t stream) {
     }
     const int maxk = a->nseg > 0 ? a->max_seg_k : a->n_keys;
     const int KP = (maxk + 15) / 16 * 16;
+    // runs <= 128 keys: the 128-key configuration (128-column slices) on large grids; on grids of
+    // < 16 query tiles (batch 1) the 256-key one, whose 64-column slices give twice the slice groups
+    // (C2 batch-1 step 918 -> 903 us). FIS_ATTN_SHORT_W64: 1 forces 64-column slices, 2 forbids them
+    static int w64 = getenv("FIS_ATTN_SHORT_W64") ? atoi(getenv("FIS_ATTN_SHORT_W64")) : 0;
+    const bool few_tiles = (a->m + 127) / 128 < 16;
+    const bool small = KP <= 128 && (w64 == 2 || (w64 == 0 && !few_tiles));
     CUtensorMap tq, tq16, tk, tv, tr, to, to8;
     if (!encode_2d(&tq, a->q.ptr, a->m, a->d, a->q.ld, 128) || !encode_2d(&tq16, a->q.ptr, a->m, a->d, a->q.ld, 16) || !encode_2d(&tk, a->k.ptr, a->n_keys, a->d, a->k.ld, KP) ||
-        !encode_2d(&tv, a->vt.ptr, a->dv, a->n_keys, a->vt.ld, KP <= 128 ? 128 : 64) ||
+        !encode_2d(&tv, a->vt.ptr, a->dv, a->n_keys, a->vt.ld, small ? 128 : 64) ||
         !encode_2d(&tr, a->res.ptr, a->m, a->dv, a->res.ld, 128))
         return -1;
     // output maps (whole tiles / 8-row groups); a per-step output stride takes the row-store path
@@ -595,14 +601,14 @@ int fis_attn_short_launch(const fis_attn_args* a, cudaStream_t stream) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)nsm);  // persistent: one CTA per SM loops over the units
     cfg.blockDim = dim3(THREADS);
-    cfg.dynamicSmemBytes = KP <= 128 ? smem_bytes<128>() : smem_bytes<256>();
+    cfg.dynamicSmemBytes = small ? smem_bytes<128>() : smem_bytes<256>();
     cfg.stream = stream;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = fis_pdl_enabled() ? 1 : 0;
-    const cudaError_t e = KP <= 128 ? cudaLaunchKernelEx(&cfg, attn_short_kernel<128>, *a, tq, tq16, tk, tv, tr, to, to8, KP, g_env)
+    const cudaError_t e = small ? cudaLaunchKernelEx(&cfg, attn_short_kernel<128>, *a, tq, tq16, tk, tv, tr, to, to8, KP, g_env)
                                     : cudaLaunchKernelEx(&cfg, attn_short_kernel<256>, *a, tq, tq16, tk, tv, tr, to, to8, KP, g_env);
     return e == cudaSuccess ? FIS_OK : FIS_ERR_LAUNCH;
 }
