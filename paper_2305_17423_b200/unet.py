@@ -518,17 +518,20 @@ def edit(session: EditSession, config: UNetConfig, store: CacheStore) -> EditRes
         m = torch.from_numpy(mask.bits.ravel().copy()).to(eng.dev)[:, None]
         lat0 = torch.where(m, outcome._control_dev, arena.latent[session.t2])
     plans = {}
+    # the host-side accounting (MACs, gather plans -- its tile read-back is a device sync) runs
+    # before the steps are queued or while they execute, so only the final latent copy waits on them
     if mask.all_active():
-        final = _dense_edit(eng, kv, lat0, start)
         _add_dense_macs(phase2, unet, n_new, T - start + 1)
+        rep = _build_report(unet, n_new, config, [outcome.phase1_macs, phase2])
+        final = _dense_edit(eng, kv, lat0, start)
     else:
         ep = EditPlan(eng, arena, mask, kv, lat0)
-        _cached_runner(eng, store, start, ep, kv).run(start, T)
-        final = ep.final_latent(eng, arena)
         _add_sparse_macs(phase2, unet, n_new, ep.dp, T - start + 1)
         plans = _gather_plans(unet, ep.dp)
+        rep = _build_report(unet, n_new, config, [outcome.phase1_macs, phase2])
+        _cached_runner(eng, store, start, ep, kv).run(start, T)
+        final = ep.final_latent(eng, arena)
     latent = _to_nchw(final, cl, H, W)
-    rep = _build_report(unet, n_new, config, [outcome.phase1_macs, phase2])
     return EditResult(latent, rep, store.stats(), mask, False, outcome.phase1_macs.total, phase2.total, plans)
 
 
