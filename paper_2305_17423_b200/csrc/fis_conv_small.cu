@@ -76,6 +76,14 @@ __global__ void __launch_bounds__(ROWS == 32 ? 320 : 160, 2) conv_small_kernel(c
             }
         }
     }
+    // the first tile's select-on-read table before the dependency wait: row lists and pixel maps are
+    // plan data (no kernel of the step writes them)
+    const int ntiles = (a.m + ROWS - 1) / ROWS;
+    if ((int)blockIdx.x < ntiles && tid < ROWS) {
+        const int r = (int)blockIdx.x * ROWS + tid;
+        const int p = r < a.m ? (a.rows ? __ldg(a.rows + r) : r) : -1;
+        build_sel(a, p, 0, sel + tid * 9);
+    }
     pdl_trigger();
     pdl_wait();
     ltr(ls, 2);
@@ -96,11 +104,10 @@ __global__ void __launch_bounds__(ROWS == 32 ? 320 : 160, 2) conv_small_kernel(c
             tb.rstd[c] = 0.f;
         }
     }
-    const int ntiles = (a.m + ROWS - 1) / ROWS;
 #pragma unroll 1
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {  // persistent: weights staged once
     const int m0 = tile * ROWS;
-    if (tid < ROWS) {
+    if (tile != (int)blockIdx.x && tid < ROWS) {
         const int r = m0 + tid;
         const int p = r < a.m ? (a.rows ? __ldg(a.rows + r) : r) : -1;
         build_sel(a, p, 0, sel + tid * 9);
