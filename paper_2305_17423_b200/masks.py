@@ -174,8 +174,26 @@ class DevicePlan:
     def origins(self, l):
         hl, wl = self.h >> l, self.w >> l
         tw = (wl + 1) // 2
-        t = self.tiles[l][: self.n_tiles[l]].cpu().numpy()
+        ht = getattr(self, "_host_tiles", None)
+        t = ht[l] if ht is not None else self.tiles[l][: self.n_tiles[l]].cpu().numpy()
         return tuple((int(2 * (i // tw)), int(2 * (i % tw))) for i in t)
+
+    @staticmethod
+    def fetch_tiles_all(plans):
+        """Host copies of every plan's tile lists in one device->host transfer (origins() then reads
+        them without a device sync: the stacked edit computes its reports while its steps run)."""
+        parts = [dp.tiles[l][: dp.n_tiles[l]] for dp in plans for l in range(dp.levels) if dp.tiles[l] is not None]
+        if not parts:
+            return
+        flat = torch.cat(parts).cpu().numpy()
+        i = 0
+        for dp in plans:
+            ht = []
+            for l in range(dp.levels):
+                n = dp.n_tiles[l] if dp.tiles[l] is not None else 0
+                ht.append(flat[i:i + n])
+                i += n
+            dp._host_tiles = ht
 
 
 def _mask_dev(mask: BinaryMask) -> torch.Tensor:

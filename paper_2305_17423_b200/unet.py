@@ -760,6 +760,7 @@ def edit_batch(sessions, config: UNetConfig) -> list:
     b_texts = [texts[slot[i]] if i in slot else texts[0] for i in range(nb)]
     skv = eng.text_kv_stacked(b_texts)
     bp = BatchedEditPlan(eng, stacked, b_masks, None, b_lat0, stacked_kv=skv)
+    DevicePlan.fetch_tiles_all(bp.dps)  # (one transfer, before the steps are queued)
     _Runner(eng, bp.plan, _use_graphs() and os.environ.get("FIS_BATCH_GRAPH", "1") != "0").run(start, T)
     final = bp.final_latents(eng, stacked)
     hw = eng.hw(0)
@@ -767,9 +768,9 @@ def edit_batch(sessions, config: UNetConfig) -> list:
     for r, f in enumerate(full):
         if f:
             final[img[r] * hw:(img[r] + 1) * hw] = _dense_edit(eng, eng.text_kv(texts[r]), lat0s[r], start)
-    fin = final.view(nb, H, W, cl).permute(0, 3, 1, 2).contiguous().cpu().numpy()  # one D2H
+    # per-request accounting on the host while the queued steps run (no device sync in it)
     unet = _unet_of(config)
-    results = [None] * len(sessions)
+    acct = []
     for r, (s, o) in enumerate(zip(sessions, outcomes)):
         n_new = len(s.new_tokens.ids)
         phase2 = _MacsCounter()
@@ -780,7 +781,10 @@ def edit_batch(sessions, config: UNetConfig) -> list:
             else:
                 _add_sparse_macs(phase2, unet, n_new, bp.dps[img[r]], T - start + 1)
                 plans = _gather_plans(unet, bp.dps[img[r]])
-        rep = _build_report(unet, n_new, config, [o.phase1_macs, phase2])
+        acct.append((_build_report(unet, n_new, config, [o.phase1_macs, phase2]), phase2, plans))
+    fin = final.view(nb, H, W, cl).permute(0, 3, 1, 2).contiguous().cpu().numpy()  # one D2H
+    results = [None] * len(sessions)
+    for r, ((s, o), (rep, phase2, plans)) in enumerate(zip(zip(sessions, outcomes), acct)):
         results[order[r]] = EditResult(fin[img[r]:img[r] + 1], rep, s.store.stats(), o.mask, o.no_edit,
                                        o.phase1_macs.total, phase2.total, plans)
     return results
